@@ -1,0 +1,404 @@
+// tcgen05/TMEM/TMA GEMM for sm_100a (bf16 in, fp32 accumulate in TMEM) and
+// the fp32 SIMT GEMM used by the fp32 parity mode. See gemm.cuh.
+//
+// tcgen05 kernel structure (persistent, warp-specialised, 192 threads):
+//   warp 0    : TMA producer, STAGES-deep smem ring (full/empty mbarriers)
+//   warp 1    : TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5 : epilogue; TMEM -> registers (tcgen05.ld 32x32b) -> fused
+//               bias/activation/scale/residual -> global
+// Accumulators are double-buffered in TMEM (2 x BN fp32 columns) so the
+// epilogue of tile i overlaps the MMAs of tile i+1.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace orx {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // 64 bf16 = 128 B = one swizzle row
+
+// ---------------------------------------------------------------------------
+// epilogue: 32 consecutive accumulator columns of one row
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void epi_store32(const Epi& e, int row, int col0, float (&v)[32]) {
+  if (row >= e.m_valid) return;
+  int orow = e.row_map ? e.row_map[row] : row;
+  if (orow < 0) return;
+  const bool full = col0 + 32 <= e.n_out;
+  float rs = e.row_scale ? e.row_scale[row] : 1.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    int c = col0 + j;
+    float x = v[j];
+    if (e.bias && (full || c < e.n_out)) x += e.bias[c];
+    x = act_apply(x, e.act);
+    x *= rs;
+    v[j] = x;
+  }
+  if (e.resid) {
+    const float* rp = e.resid + (size_t)orow * e.ld_resid + col0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (full || col0 + j < e.n_out) v[j] += rp[j];
+  }
+  int oc = col0 + e.col_off;
+  if (e.out_bf16) {
+    __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)orow * e.ldo + oc;
+    if (full && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 w;
+        w.x = pack_bf16(v[j], v[j + 1]);
+        w.y = pack_bf16(v[j + 2], v[j + 3]);
+        w.z = pack_bf16(v[j + 4], v[j + 5]);
+        w.w = pack_bf16(v[j + 6], v[j + 7]);
+        *reinterpret_cast<uint4*>(op + j) = w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < e.n_out) op[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else {
+    float* op = reinterpret_cast<float*>(e.out) + (size_t)orow * e.ldo + oc;
+    if (full && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < e.n_out) op[j] = v[j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 persistent GEMM
+// ---------------------------------------------------------------------------
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                   int N, int K, Epi epi, Grouped grp) {
+  constexpr uint32_t A_BYTES = kBM * kBK * 2;
+  constexpr uint32_t B_BYTES = BN * kBK * 2;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered accumulator
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_tiles = grp.n_mtiles ? *grp.n_mtiles : (M + kBM - 1) / kBM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int total = m_tiles * n_tiles;
+  const int kblocks = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_a = l2_policy_evict_first();
+      const uint64_t pol_b = l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int mt = t / n_tiles, nt = t % n_tiles;
+        int brow = nt * BN;
+        if (grp.tile_expert) {
+          int e = grp.tile_expert[mt];
+          if (e < 0) continue;
+          brow += e * grp.b_rows_per_expert;
+        }
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * kBK, mt * kBM, pol_a);
+          tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kb * kBK, brow, pol_b);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        if (grp.tile_expert && grp.tile_expert[t / n_tiles] < 0) continue;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            tc_mma_bf16(d_tmem, umma_desc_sw128(a_base + k * 32), umma_desc_sw128(b_base + k * 32), idesc,
+                        (kb | k) != 0);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int mt = t / n_tiles, nt = t % n_tiles;
+      if (grp.tile_expert && grp.tile_expert[mt] < 0) continue;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mt * kBM + q * 32 + lane;
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      if (epi.swiglu) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          float a[32], b[32];
+          tmem_ld32(tbase + c * 32, a);
+          tmem_ld32(tbase + BN / 2 + c * 32, b);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) a[j] = a[j] / (1.f + __expf(-a[j])) * b[j];
+          epi_store32(epi, row, nt * (BN / 2) + c * 32, a);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float a[32];
+          tmem_ld32(tbase + c * 32, a);
+          epi_store32(epi, row, nt * BN + c * 32, a);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp32 SIMT GEMM (parity mode): 64x64 tile, BK 16, 256 threads, 4x4 per thread
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) simt_gemm_kernel(const float* __restrict__ A, int lda,
+                                                         const float* __restrict__ B, int ldb, int M, int N,
+                                                         int K, Epi epi, Grouped grp) {
+  __shared__ float sA[16][64 + 4];
+  __shared__ float sB[16][64 + 4];
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  if (grp.n_mtiles && m0 >= *grp.n_mtiles * kBM) return;
+  int boff = 0;
+  if (grp.tile_expert) {
+    int e = grp.tile_expert[m0 / kBM];
+    if (e < 0) return;
+    boff = e * grp.b_rows_per_expert;
+  }
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      int r = i / 16, c = i % 16;
+      int gm = m0 + r, gk = k0 + c;
+      sA[c][r] = (gm < M && gk < K) ? A[(size_t)gm * lda + gk] : 0.f;
+      int gn = n0 + r;
+      sB[c][r] = (gn < N && gk < K) ? B[(size_t)(boff + gn) * ldb + gk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sA[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = sB[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  // Generic scalar epilogue (swiglu handled via paired columns).
+  for (int i = 0; i < 4; ++i) {
+    int row = m0 + ty * 4 + i;
+    if (row >= epi.m_valid || row >= M) continue;
+    int orow = epi.row_map ? epi.row_map[row] : row;
+    if (orow < 0) continue;
+    float rs = epi.row_scale ? epi.row_scale[row] : 1.f;
+    for (int j = 0; j < 4; ++j) {
+      int col = n0 + tx * 4 + j;
+      if (col >= N) continue;
+      float x = acc[i][j];
+      int oc;
+      if (epi.swiglu) {
+        continue;  // swiglu in fp32 mode uses gemm_f32 twice + swiglu_mul kernel (see engine)
+      } else {
+        oc = col;
+        if (oc >= epi.n_out) continue;
+        if (epi.bias) x += epi.bias[oc];
+        x = act_apply(x, epi.act);
+        x *= rs;
+      }
+      if (epi.resid) x += epi.resid[(size_t)orow * epi.ld_resid + oc];
+      oc += epi.col_off;
+      if (epi.out_bf16)
+        reinterpret_cast<__nv_bfloat16*>(epi.out)[(size_t)orow * epi.ldo + oc] = __float2bfloat16_rn(x);
+      else
+        reinterpret_cast<float*>(epi.out)[(size_t)orow * epi.ldo + oc] = x;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+CUtensorMap make_map_bf16(const void* ptr, int rows, int cols, int ld, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride, box,
+                            estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ") rows=" +
+                             std::to_string(rows) + " cols=" + std::to_string(cols) + " ld=" + std::to_string(ld));
+  return m;
+}
+
+template <int BN, int STAGES>
+void launch_tc(const void* A, int lda, const void* B, int ldb, int M, int N, int K, const Epi& epi,
+               const Grouped* grp, cudaStream_t stream) {
+  constexpr size_t smem = STAGES * (kBM * kBK * 2 + BN * kBK * 2) + 1024 + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr_set = true;
+  }
+  Grouped g = grp ? *grp : Grouped{};
+  CUtensorMap ma = make_map_bf16(A, M, K, lda, kBM);
+  const int b_rows = g.tile_expert ? g.n_groups * g.b_rows_per_expert : N;
+  CUtensorMap mb = make_map_bf16(B, b_rows, K, ldb, BN);
+  int tiles;
+  if (g.n_mtiles) {
+    tiles = num_sms();
+  } else {
+    tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
+    if (tiles > num_sms()) tiles = num_sms();
+  }
+  tc_gemm_kernel<BN, STAGES><<<tiles, 192, smem, stream>>>(ma, mb, M, N, K, epi, g);
+  ++launch_counter();
+}
+
+}  // namespace
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+long long& launch_counter() {
+  static long long c = 0;
+  return c;
+}
+
+void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int K, const Epi& epi,
+               const Grouped* grp, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return;
+  if (K % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0)
+    throw std::invalid_argument("gemm_bf16: K and row strides must be multiples of 8");
+  if (epi.swiglu && N % 256 != 0) throw std::invalid_argument("gemm_bf16: swiglu needs N % 256 == 0");
+  if (N <= 128 && !epi.swiglu)
+    launch_tc<128, 6>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+  else
+    launch_tc<256, 4>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+}
+
+void gemm_f32(const float* A, int lda, const float* B, int ldb, int M, int N, int K, const Epi& epi,
+              const Grouped* grp, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return;
+  if (epi.swiglu) throw std::invalid_argument("gemm_f32: swiglu epilogue not supported");
+  Grouped g = grp ? *grp : Grouped{};
+  dim3 grid((N + 63) / 64, (M + 63) / 64);
+  simt_gemm_kernel<<<grid, 256, 0, stream>>>(A, lda, B, ldb, M, N, K, epi, g);
+  ++launch_counter();
+}
+
+}  // namespace orx

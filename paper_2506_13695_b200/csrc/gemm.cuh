@@ -1,0 +1,54 @@
+// GEMM interface shared by the tcgen05 (bf16) and SIMT (fp32 parity) kernels.
+//
+// C[M, N] = A[M, K] . B[N, K]^T, i.e. y = x . W with the reference's (in, out)
+// Linear weight W (nn.cpp:8-22) stored transposed as B = W^T [out][in]
+// ("K-major" for both operands, the native UMMA layout). Every linear of the
+// hot path goes through here with a fused epilogue:
+//   bias add (linear, nn.cpp:18-22), LeakyReLU / SiLU (mlp_leaky / ffn,
+//   nn.cpp:32-34,71-73), SwiGLU pairing (swiglu, nn.cpp:84-86), MoE combine
+//   weight (nn.cpp:167-168), residual add (policy.cpp:261-262,283-285).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace orx {
+
+struct Epi {
+  const float* bias = nullptr;       // [N] (or [N/2] for swiglu: not used)
+  const float* row_scale = nullptr;  // [M] per-row multiplier
+  const float* resid = nullptr;      // fp32 [rows, ld_resid], indexed by output row
+  void* out = nullptr;               // [rows, ldo]
+  const int* row_map = nullptr;      // output row = row_map[r] (< 0: dropped)
+  int ld_resid = 0;
+  int ldo = 0;
+  int out_bf16 = 0;
+  int act = 0;      // Act
+  int swiglu = 0;   // B rows interleaved per 128: [W1 block | W3 block] -> silu(a)*b
+  int n_out = 0;    // number of valid output columns
+  int m_valid = 0;  // rows >= m_valid are not stored
+  int col_off = 0;  // added to output column index
+};
+
+// Grouped (MoE) addressing: M tile i uses B rows [tile_expert[i]*b_rows_per_expert, ...).
+struct Grouped {
+  const int* tile_expert = nullptr;  // [max m tiles], -1 = skip
+  const int* n_mtiles = nullptr;     // device scalar: number of valid M tiles
+  int b_rows_per_expert = 0;
+  int n_groups = 0;  // number of experts stacked in B
+};
+
+// bf16 A [M x K] (row stride lda elements), bf16 B [N x K] (row stride ldb).
+// K must be a multiple of 8 (16-byte TMA strides); rows beyond M/N and the K
+// tail are zero-filled by TMA.
+void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int K, const Epi& epi,
+               const Grouped* grp, cudaStream_t stream);
+
+// fp32 A [M x K], fp32 B [N x K]; same epilogue. Parity mode only.
+void gemm_f32(const float* A, int lda, const float* B, int ldb, int M, int N, int K, const Epi& epi,
+              const Grouped* grp, cudaStream_t stream);
+
+int num_sms();
+long long& launch_counter();
+
+}  // namespace orx

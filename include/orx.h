@@ -1,0 +1,170 @@
+/*
+ * orx.h — C-ABI of the B200-native OneRec inference hot path.
+ *
+ * Drop-in boundary for the reference's encode / generate entry points
+ * (reference: /root/reference/proj/core). Plain pointers and sizes only;
+ * every function returns ORX_OK (0) or a negative error code, with the
+ * message available from orx_last_error() (thread-local). No exceptions
+ * cross the ABI. One engine per GPU; an engine is not thread-safe.
+ *
+ * Reference interface each entry point replaces:
+ *   orx_config / orx_config_preset ........ PolicyConfig, policy.hpp:36-85
+ *   orx_weights_create_random ............. PolicyModel::PolicyModel(cfg), policy.cpp:59-137
+ *   orx_weights_load_grcp / save_grcp ..... PolicyModel::load / save, policy.cpp:411-443
+ *   orx_user_batch ........................ UserContext / InteractionFeature, policy.hpp:15-32
+ *   orx_validate_batch .................... validate_context, policy.cpp:23-38
+ *   orx_encode ............................ PolicyModel::encode_eval, policy.cpp:317-321
+ *   orx_next_logits ....................... PolicyModel::next_logits_eval, policy.cpp:323-329
+ *   orx_score_prefixes .................... encode_eval + next_logits_eval per (user, prefix)
+ *   orx_beam_search ....................... generate(req{beam}) = beam_search(req, policy_scorer(m, z), ...),
+ *                                           generation.cpp:41-88,150-167, batched over users
+ */
+#ifndef ORX_H_
+#define ORX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORX_OK 0
+#define ORX_EINVAL -1  /* std::invalid_argument in the reference (GENREC_REQUIRE) */
+#define ORX_ERUNTIME -2 /* std::runtime_error in the reference (I/O, non-finite)   */
+#define ORX_ECUDA -3    /* CUDA error or missing device                           */
+
+#define ORX_PRECISION_FP32 0 /* parity mode: fp32 SIMT GEMMs, fp32 activations   */
+#define ORX_PRECISION_BF16 1 /* throughput mode: tcgen05 bf16 GEMMs, fp32 accum  */
+
+/* Mirror of genrec::PolicyConfig (policy.hpp:36-85), same field meanings. */
+typedef struct orx_config {
+  int32_t n_layers;
+  int32_t d_model;
+  int32_t ffn_hidden;
+  int32_t n_heads;
+  int32_t moe_enabled;
+  int32_t n_experts;
+  int32_t experts_active;
+  int32_t moe_location; /* 0 = decoder, 1 = enc_and_dec */
+  int32_t expert_round_multiple;
+  int32_t n_code_layers;
+  int32_t codebook_size;
+  int32_t short_len;
+  int32_t positive_len;
+  int32_t lifelong_len;
+  int32_t n_queries;
+  int32_t lifelong_blocks;
+  int32_t vid_vocab;
+  int32_t aid_vocab;
+  int32_t uid_vocab;
+  int32_t gender_vocab;
+  int32_t age_vocab;
+  int32_t n_label_flags;
+  int32_t use_sid_history;
+  int32_t vid_only_features;
+  int32_t compress_threshold;
+  double moe_bias_update;
+  uint64_t seed;
+} orx_config;
+
+/* One pathway's records for all users, concatenated user after user
+ * (each user's records time-ascending). offsets has n_users+1 entries. */
+typedef struct orx_records {
+  const int64_t* offsets;
+  const int64_t* vid;
+  const int32_t* aid;
+  const double* tag;
+  const double* ts;
+  const double* playtime;
+  const double* duration;
+  const uint32_t* labels;
+  const int32_t* sid; /* [n_records * n_code_layers]; required iff use_sid_history */
+} orx_records;
+
+typedef struct orx_user_batch {
+  int32_t n_users;
+  const int32_t* uid;
+  const int32_t* gender;
+  const int32_t* age_bucket;
+  orx_records short_seq;
+  orx_records positive_seq;
+  orx_records lifelong_seq;
+} orx_user_batch;
+
+/* Beam-search results: per user `width` items sorted by (log_prob desc,
+ * codes asc); n_items[u] < width only when fewer candidates exist. */
+typedef struct orx_beam_out {
+  int32_t* codes;    /* [n_users * width * n_code_layers] */
+  double* log_prob;  /* [n_users * width] */
+  int32_t* n_items;  /* [n_users] */
+} orx_beam_out;
+
+typedef struct orx_weights orx_weights;
+typedef struct orx_engine orx_engine;
+typedef struct orx_synth_batch orx_synth_batch;
+
+const char* orx_last_error(void);
+const char* orx_version(void);
+
+/* Config: reference defaults (PolicyConfig{}) or a named paper preset:
+ * "tiny", "0.015B", "0.121B", "0.935B", "2.633B". */
+int orx_config_default(orx_config* cfg);
+int orx_config_preset(const char* name, orx_config* cfg);
+int64_t orx_config_enc_seq_len(const orx_config* cfg);
+int64_t orx_config_expert_hidden(const orx_config* cfg);
+
+/* Host weights (fp32 copies of the reference's f64 parameters). */
+int orx_weights_create_random(const orx_config* cfg, orx_weights** out);
+int orx_weights_load_grcp(const char* path, orx_weights** out);
+int orx_weights_save_grcp(const orx_weights* w, const char* path);
+int orx_weights_config(const orx_weights* w, orx_config* cfg);
+int64_t orx_weights_count(const orx_weights* w);
+/* Name / shape / data of entry i in reference insertion order. */
+int orx_weights_entry(const orx_weights* w, int64_t i, const char** name, int32_t* ndim, int32_t dims[2],
+                      const float** data);
+int orx_weights_find(const orx_weights* w, const char* name, int64_t* index);
+void orx_weights_destroy(orx_weights* w);
+
+int orx_validate_batch(const orx_config* cfg, const orx_user_batch* batch);
+
+/* Engine on one GPU. max_users / max_width size the device arena. */
+int orx_engine_create(const orx_weights* w, int device, int precision, int32_t max_users, int32_t max_width,
+                      orx_engine** out);
+void orx_engine_destroy(orx_engine* e);
+
+/* z_out (host, optional): [n_users * enc_seq_len * d_model] fp32. */
+int orx_encode(orx_engine* e, const orx_user_batch* batch, float* z_out);
+/* Teacher-forced logits for n queries over caller-supplied encodings:
+ * z_enc [n_z * T * d] fp32, query q uses z_index[q] and prefix
+ * prefixes[q * n_code_layers ...] of length prefix_len[q] (< n_code_layers).
+ * logits_out: [n * codebook_size] fp32. */
+int orx_next_logits(orx_engine* e, const float* z_enc, int32_t n_z, int32_t n, const int32_t* z_index,
+                    const int32_t* prefixes, const int32_t* prefix_len, float* logits_out);
+/* encode + teacher-forced logits for (user, prefix) queries of a batch. */
+int orx_score_prefixes(orx_engine* e, const orx_user_batch* batch, int32_t n, const int32_t* user,
+                       const int32_t* prefixes, const int32_t* prefix_len, float* logits_out);
+/* encode + unconstrained beam search of depth n_code_layers, batched. */
+int orx_beam_search(orx_engine* e, const orx_user_batch* batch, int32_t width, orx_beam_out* out);
+
+/* Same as orx_beam_search, but inputs are already resident on the device
+ * (uploaded by orx_engine_stage_batch); results stay on the device unless
+ * out is non-NULL. Used to time the kernel path without host copies. */
+int orx_engine_stage_batch(orx_engine* e, const orx_user_batch* batch);
+int orx_beam_search_staged(orx_engine* e, int32_t width, orx_beam_out* out);
+/* Counters: kernel launches issued by the engine so far, bytes H2D / D2H. */
+int orx_engine_stats(const orx_engine* e, int64_t* launches, int64_t* h2d_bytes, int64_t* d2h_bytes);
+/* Stream the engine launches on (cudaStream_t as void*). */
+void* orx_engine_stream(orx_engine* e);
+
+/* Seeded synthetic users (synth_users.hpp). */
+int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,
+                           int32_t n_lifelong, orx_synth_batch** out);
+int orx_synth_batch_view(const orx_synth_batch* b, orx_user_batch* view);
+void orx_synth_batch_destroy(orx_synth_batch* b);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ORX_H_ */

@@ -1,0 +1,116 @@
+"""ctypes binding of liborx.so (include/orx.h).
+
+The library is built in-tree (``paper_2506_13695_b200/liborx.so``) by
+``__graft_entry__.build()`` / ``make -C paper_2506_13695_b200/csrc``. There is
+no fallback: if the library is missing, importing the engine raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liborx.so")
+
+ORX_OK, ORX_EINVAL, ORX_ERUNTIME, ORX_ECUDA = 0, -1, -2, -3
+PRECISION = {"fp32": 0, "bf16": 1}
+
+
+class orx_config(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "n_layers", "d_model", "ffn_hidden", "n_heads", "moe_enabled", "n_experts", "experts_active",
+        "moe_location", "expert_round_multiple", "n_code_layers", "codebook_size", "short_len",
+        "positive_len", "lifelong_len", "n_queries", "lifelong_blocks", "vid_vocab", "aid_vocab",
+        "uid_vocab", "gender_vocab", "age_vocab", "n_label_flags", "use_sid_history",
+        "vid_only_features", "compress_threshold")] + [("moe_bias_update", C.c_double), ("seed", C.c_uint64)]
+
+
+class orx_records(C.Structure):
+    _fields_ = [
+        ("offsets", C.POINTER(C.c_int64)), ("vid", C.POINTER(C.c_int64)), ("aid", C.POINTER(C.c_int32)),
+        ("tag", C.POINTER(C.c_double)), ("ts", C.POINTER(C.c_double)), ("playtime", C.POINTER(C.c_double)),
+        ("duration", C.POINTER(C.c_double)), ("labels", C.POINTER(C.c_uint32)), ("sid", C.POINTER(C.c_int32)),
+    ]
+
+
+class orx_user_batch(C.Structure):
+    _fields_ = [
+        ("n_users", C.c_int32), ("uid", C.POINTER(C.c_int32)), ("gender", C.POINTER(C.c_int32)),
+        ("age_bucket", C.POINTER(C.c_int32)), ("short_seq", orx_records), ("positive_seq", orx_records),
+        ("lifelong_seq", orx_records),
+    ]
+
+
+class orx_beam_out(C.Structure):
+    _fields_ = [("codes", C.POINTER(C.c_int32)), ("log_prob", C.POINTER(C.c_double)),
+                ("n_items", C.POINTER(C.c_int32))]
+
+
+# (name, restype, argtypes) for every function declared in include/orx.h
+_P = C.c_void_p
+_I32P = C.POINTER(C.c_int32)
+_F32P = C.POINTER(C.c_float)
+SIGNATURES = [
+    ("orx_last_error", C.c_char_p, []),
+    ("orx_version", C.c_char_p, []),
+    ("orx_config_default", C.c_int, [C.POINTER(orx_config)]),
+    ("orx_config_preset", C.c_int, [C.c_char_p, C.POINTER(orx_config)]),
+    ("orx_config_enc_seq_len", C.c_int64, [C.POINTER(orx_config)]),
+    ("orx_config_expert_hidden", C.c_int64, [C.POINTER(orx_config)]),
+    ("orx_weights_create_random", C.c_int, [C.POINTER(orx_config), C.POINTER(_P)]),
+    ("orx_weights_load_grcp", C.c_int, [C.c_char_p, C.POINTER(_P)]),
+    ("orx_weights_save_grcp", C.c_int, [_P, C.c_char_p]),
+    ("orx_weights_config", C.c_int, [_P, C.POINTER(orx_config)]),
+    ("orx_weights_count", C.c_int64, [_P]),
+    ("orx_weights_entry", C.c_int, [_P, C.c_int64, C.POINTER(C.c_char_p), _I32P, _I32P,
+                                    C.POINTER(_F32P)]),
+    ("orx_weights_find", C.c_int, [_P, C.c_char_p, C.POINTER(C.c_int64)]),
+    ("orx_weights_destroy", None, [_P]),
+    ("orx_validate_batch", C.c_int, [C.POINTER(orx_config), C.POINTER(orx_user_batch)]),
+    ("orx_engine_create", C.c_int, [_P, C.c_int, C.c_int, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    ("orx_engine_destroy", None, [_P]),
+    ("orx_encode", C.c_int, [_P, C.POINTER(orx_user_batch), _F32P]),
+    ("orx_next_logits", C.c_int, [_P, _F32P, C.c_int32, C.c_int32, _I32P, _I32P, _I32P, _F32P]),
+    ("orx_score_prefixes", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, _I32P, _I32P, _I32P, _F32P]),
+    ("orx_beam_search", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, C.POINTER(orx_beam_out)]),
+    ("orx_engine_stage_batch", C.c_int, [_P, C.POINTER(orx_user_batch)]),
+    ("orx_beam_search_staged", C.c_int, [_P, C.c_int32, C.POINTER(orx_beam_out)]),
+    ("orx_engine_stats", C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("orx_engine_stream", _P, [_P]),
+    ("orx_synth_batch_create", C.c_int, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                         C.POINTER(_P)]),
+    ("orx_synth_batch_view", C.c_int, [_P, C.POINTER(orx_user_batch)]),
+    ("orx_synth_batch_destroy", None, [_P]),
+]
+
+_lib = None
+
+
+def lib():
+    """Load liborx.so once; raise (never fall back) if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                              "(there is no CPU fallback)")
+        h = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            f = getattr(h, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = h
+    return _lib
+
+
+class OrxError(RuntimeError):
+    pass
+
+
+def check(rc: int) -> None:
+    """Map ORX error codes to the reference's exception types."""
+    if rc == ORX_OK:
+        return
+    msg = lib().orx_last_error().decode()
+    if rc == ORX_EINVAL:
+        raise ValueError(msg)  # std::invalid_argument (GENREC_REQUIRE)
+    raise OrxError(msg)  # std::runtime_error / CUDA

@@ -1,0 +1,35 @@
+// Beam pruning over 3-level semantic IDs (beam_search, generation.cpp:41-88).
+//
+// Candidate key (64 bit, larger = better) reproduces the reference sort
+// (log_prob desc, codes lexicographic asc, generation.cpp:74-77):
+//   hi 32 bits: order-preserving bits of the fp32 score parent + (logit - lse)
+//   lo 32 bits: 0xFFFFFFFF - (parent_lexrank * V + code)
+// where parent_lexrank is the rank of the parent's code prefix among the live
+// beams of its user, so lexicographic order of the extended prefixes is the
+// order of (parent_lexrank, code).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace orx {
+
+struct BeamState {  // live beams of one step, row r = user * n_live + beam
+  int32_t* codes = nullptr;     // [rows][L]
+  float* score = nullptr;       // [rows] fp32 ranking score
+  double* score64 = nullptr;    // [rows] f64 accumulated log-prob (output)
+  int32_t* lexrank = nullptr;   // [rows]
+  int32_t* lex2beam = nullptr;  // [users][n_live]
+  int32_t* anc = nullptr;       // [rows][L] ancestor row per position
+};
+
+// Per row: lse = logsumexp(logits), then the top k_sel candidate keys.
+void launch_row_topk(int rows, int V, int k_sel, const float* logits, const float* parent_score,
+                     const int32_t* parent_lexrank, float* lse, uint64_t* cand, cudaStream_t s);
+
+// Per user: top n_new of n_live * k_sel candidates, sorted; builds the next
+// BeamState (codes, scores, lexranks, ancestors).
+void launch_beam_merge(int users, int n_live, int k_sel, int n_new, int V, int L, int step, const uint64_t* cand,
+                       const float* logits, const float* lse, const BeamState& cur, BeamState& nxt, cudaStream_t s);
+
+}  // namespace orx

@@ -1,0 +1,317 @@
+// extern "C" boundary (include/orx.h). Exceptions never cross it: they are
+// mapped to ORX_EINVAL / ORX_ERUNTIME / ORX_ECUDA plus a thread-local message.
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/orx.h"
+#include "engine.hpp"
+#include "model.hpp"
+#include "synth_users.hpp"
+
+struct orx_weights {
+  orx::HostWeights w;
+};
+struct orx_engine {
+  std::unique_ptr<orx::Engine> e;
+  const orx::HostWeights* w = nullptr;
+  orx_config cfg{};
+  int staged_users = 0;
+};
+struct orx_synth_batch {
+  std::vector<int32_t> uid, gender, age;
+  struct P {
+    std::vector<int64_t> offsets, vid;
+    std::vector<int32_t> aid;
+    std::vector<double> tag, ts, play, dur;
+    std::vector<uint32_t> labels;
+  } p[3];
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return ORX_OK;
+  } catch (const orx::InvalidArgument& e) {
+    g_err = e.what();
+    return ORX_EINVAL;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return ORX_EINVAL;
+  } catch (const orx::RuntimeError& e) {
+    g_err = e.what();
+    return std::string(e.what()).rfind("CUDA", 0) == 0 || strstr(e.what(), "CUDA") ? ORX_ECUDA : ORX_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return ORX_ERUNTIME;
+  } catch (...) {
+    g_err = "unknown error";
+    return ORX_ERUNTIME;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw orx::InvalidArgument(std::string(what) + " must not be NULL");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* orx_last_error(void) { return g_err.c_str(); }
+const char* orx_version(void) { return "orx 0.1 (sm_100a)"; }
+
+int orx_config_default(orx_config* cfg) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    *cfg = orx::config_default();
+  });
+}
+
+int orx_config_preset(const char* name, orx_config* cfg) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(name, "name");
+    *cfg = orx::config_preset(name);
+  });
+}
+
+int64_t orx_config_enc_seq_len(const orx_config* cfg) { return cfg ? orx::enc_seq_len(*cfg) : -1; }
+int64_t orx_config_expert_hidden(const orx_config* cfg) {
+  int64_t v = -1;
+  guarded([&] {
+    need(cfg, "cfg");
+    v = orx::expert_hidden(*cfg);
+  });
+  return v;
+}
+
+int orx_weights_create_random(const orx_config* cfg, orx_weights** out) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(out, "out");
+    auto w = std::make_unique<orx_weights>();
+    w->w = orx::HostWeights::random(*cfg);
+    *out = w.release();
+  });
+}
+
+int orx_weights_load_grcp(const char* path, orx_weights** out) {
+  return guarded([&] {
+    need(path, "path");
+    need(out, "out");
+    auto w = std::make_unique<orx_weights>();
+    w->w = orx::HostWeights::load_grcp(path);
+    *out = w.release();
+  });
+}
+
+int orx_weights_save_grcp(const orx_weights* w, const char* path) {
+  return guarded([&] {
+    need(w, "weights");
+    need(path, "path");
+    w->w.save_grcp(path);
+  });
+}
+
+int orx_weights_config(const orx_weights* w, orx_config* cfg) {
+  return guarded([&] {
+    need(w, "weights");
+    need(cfg, "cfg");
+    *cfg = w->w.cfg;
+  });
+}
+
+int64_t orx_weights_count(const orx_weights* w) { return w ? static_cast<int64_t>(w->w.tensors.size()) : -1; }
+
+int orx_weights_entry(const orx_weights* w, int64_t i, const char** name, int32_t* ndim, int32_t dims[2],
+                      const float** data) {
+  return guarded([&] {
+    need(w, "weights");
+    if (i < 0 || i >= static_cast<int64_t>(w->w.tensors.size())) throw orx::InvalidArgument("entry index out of range");
+    const orx::Tensor& t = w->w.tensors[static_cast<size_t>(i)];
+    if (name) *name = t.name.c_str();
+    if (ndim) *ndim = 2;
+    if (dims) {
+      dims[0] = t.rows;
+      dims[1] = t.cols;
+    }
+    if (data) *data = t.data.data();
+  });
+}
+
+int orx_weights_find(const orx_weights* w, const char* name, int64_t* index) {
+  return guarded([&] {
+    need(w, "weights");
+    need(name, "name");
+    auto it = w->w.index.find(name);
+    if (it == w->w.index.end()) throw orx::InvalidArgument(std::string("unknown parameter: ") + name);
+    if (index) *index = it->second;
+  });
+}
+
+void orx_weights_destroy(orx_weights* w) { delete w; }
+
+int orx_validate_batch(const orx_config* cfg, const orx_user_batch* batch) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(batch, "batch");
+    orx::validate_batch(*cfg, *batch);
+  });
+}
+
+int orx_engine_create(const orx_weights* w, int device, int precision, int32_t max_users, int32_t max_width,
+                      orx_engine** out) {
+  return guarded([&] {
+    need(w, "weights");
+    need(out, "out");
+    auto e = std::make_unique<orx_engine>();
+    e->e = orx::Engine::create(w->w, device, precision, max_users, max_width);
+    e->w = &w->w;
+    e->cfg = w->w.cfg;
+    *out = e.release();
+  });
+}
+
+void orx_engine_destroy(orx_engine* e) { delete e; }
+
+int orx_encode(orx_engine* e, const orx_user_batch* batch, float* z_out) {
+  return guarded([&] {
+    need(e, "engine");
+    need(batch, "batch");
+    e->e->stage_batch(*batch);
+    e->e->encode(z_out);
+  });
+}
+
+int orx_next_logits(orx_engine* e, const float* z_enc, int32_t n_z, int32_t n, const int32_t* z_index,
+                    const int32_t* prefixes, const int32_t* prefix_len, float* logits_out) {
+  return guarded([&] {
+    need(e, "engine");
+    need(z_enc, "z_enc");
+    need(z_index, "z_index");
+    need(prefixes, "prefixes");
+    need(prefix_len, "prefix_len");
+    need(logits_out, "logits_out");
+    e->e->next_logits(z_enc, n_z, n, z_index, prefixes, prefix_len, logits_out);
+  });
+}
+
+int orx_score_prefixes(orx_engine* e, const orx_user_batch* batch, int32_t n, const int32_t* user,
+                       const int32_t* prefixes, const int32_t* prefix_len, float* logits_out) {
+  return guarded([&] {
+    need(e, "engine");
+    need(batch, "batch");
+    need(user, "user");
+    need(prefixes, "prefixes");
+    need(prefix_len, "prefix_len");
+    need(logits_out, "logits_out");
+    e->e->stage_batch(*batch);
+    e->e->score_prefixes(n, user, prefixes, prefix_len, logits_out);
+  });
+}
+
+int orx_beam_search(orx_engine* e, const orx_user_batch* batch, int32_t width, orx_beam_out* out) {
+  return guarded([&] {
+    need(e, "engine");
+    need(batch, "batch");
+    need(out, "out");
+    need(out->codes, "out->codes");
+    need(out->log_prob, "out->log_prob");
+    e->e->stage_batch(*batch);
+    e->e->beam_search(width, out);
+  });
+}
+
+int orx_engine_stage_batch(orx_engine* e, const orx_user_batch* batch) {
+  return guarded([&] {
+    need(e, "engine");
+    need(batch, "batch");
+    e->e->stage_batch(*batch);
+  });
+}
+
+int orx_beam_search_staged(orx_engine* e, int32_t width, orx_beam_out* out) {
+  return guarded([&] {
+    need(e, "engine");
+    e->e->beam_search(width, out);
+  });
+}
+
+int orx_engine_stats(const orx_engine* e, int64_t* launches, int64_t* h2d, int64_t* d2h) {
+  return guarded([&] {
+    need(e, "engine");
+    if (launches) *launches = orx::launch_counter_value();
+    if (h2d) *h2d = e->e->h2d_bytes;
+    if (d2h) *d2h = e->e->d2h_bytes;
+  });
+}
+
+void* orx_engine_stream(orx_engine* e) { return e ? e->e->stream() : nullptr; }
+
+int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,
+                           int32_t n_lifelong, orx_synth_batch** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (n_users < 0 || n_short < 0 || n_positive < 0 || n_lifelong < 0)
+      throw orx::InvalidArgument("synthetic batch sizes must be non-negative");
+    auto b = std::make_unique<orx_synth_batch>();
+    orx_synth::Lengths len{n_short, n_positive, n_lifelong};
+    for (auto& p : b->p) p.offsets.push_back(0);
+    for (int32_t i = 0; i < n_users; ++i) {
+      orx_synth::synth_user<orx::Rng>(
+          seed, static_cast<uint64_t>(user_begin + i), len,
+          [&](int uid, int gender, int age) {
+            b->uid.push_back(uid);
+            b->gender.push_back(gender);
+            b->age.push_back(age);
+          },
+          [&](int pathway, int64_t vid, int aid, double tag, double ts, double play, double dur, uint32_t labels) {
+            auto& p = b->p[pathway];
+            p.vid.push_back(vid);
+            p.aid.push_back(aid);
+            p.tag.push_back(tag);
+            p.ts.push_back(ts);
+            p.play.push_back(play);
+            p.dur.push_back(dur);
+            p.labels.push_back(labels);
+          });
+      for (auto& p : b->p) p.offsets.push_back(static_cast<int64_t>(p.vid.size()));
+    }
+    *out = b.release();
+  });
+}
+
+int orx_synth_batch_view(const orx_synth_batch* b, orx_user_batch* v) {
+  return guarded([&] {
+    need(b, "batch");
+    need(v, "view");
+    v->n_users = static_cast<int32_t>(b->uid.size());
+    v->uid = b->uid.data();
+    v->gender = b->gender.data();
+    v->age_bucket = b->age.data();
+    orx_records* dst[3] = {&v->short_seq, &v->positive_seq, &v->lifelong_seq};
+    for (int i = 0; i < 3; ++i) {
+      const auto& p = b->p[i];
+      dst[i]->offsets = p.offsets.data();
+      dst[i]->vid = p.vid.data();
+      dst[i]->aid = p.aid.data();
+      dst[i]->tag = p.tag.data();
+      dst[i]->ts = p.ts.data();
+      dst[i]->playtime = p.play.data();
+      dst[i]->duration = p.dur.data();
+      dst[i]->labels = p.labels.data();
+      dst[i]->sid = nullptr;
+    }
+  });
+}
+
+void orx_synth_batch_destroy(orx_synth_batch* b) { delete b; }
+
+}  // extern "C"

@@ -7,11 +7,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "gemm.cuh"
+
 #define ORX_DEV __device__ __forceinline__
 
 namespace orx {
-
-enum Act { ACT_NONE = 0, ACT_LEAKY = 1, ACT_SILU = 2 };
 
 ORX_DEV float act_apply(float v, int act) {
   if (act == ACT_LEAKY) return v > 0.f ? v : 0.01f * v;  // tape.hpp:88 slope 0.01

@@ -1,0 +1,974 @@
+// Engine: device weights, activation arena and the per-batch forward flows.
+//
+//   encode        PolicyModel::encode (policy.cpp:254-265): pathway MLPs,
+//                 lifelong QFormer, + pos_emb, L_enc pre-norm blocks.
+//   decode_step   one beam position for all live rows: PolicyModel::decode
+//                 (policy.cpp:267-288) with a per-position K/V cache for the
+//                 causal self-attention and a per-user cross-K/V cache of
+//                 z_enc computed once (nn.cpp:59-60 recomputes it per call),
+//                 then position_logits (policy.cpp:290-295).
+//   beam_search   generation.cpp:41-88 batched over users: decode_step ->
+//                 row log-softmax + top-k -> per-user merge, depth times.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <type_traits>
+
+#include "attention.cuh"
+#include "beam.cuh"
+#include "engine.hpp"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace orx {
+
+void launch_beam_init(int users, BeamState& st, cudaStream_t s);
+
+namespace {
+
+#define CUDA_CHECK(x)                                                                              \
+  do {                                                                                             \
+    cudaError_t e__ = (x);                                                                         \
+    if (e__ != cudaSuccess) throw RuntimeError(std::string("CUDA: ") + cudaGetErrorString(e__) +  \
+                                               " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+inline int rup(int x, int m) { return (x + m - 1) / m * m; }
+
+template <class T>
+T to_t(float v) {
+  if constexpr (std::is_same_v<T, float>) return v;
+  else return __float2bfloat16_rn(v);
+}
+
+// Device arena: one cudaMalloc per buffer, freed with the engine.
+struct Arena {
+  std::vector<void*> ptrs;
+  template <class X>
+  X* alloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    CUDA_CHECK(cudaMalloc(&p, n * sizeof(X)));
+    ptrs.push_back(p);
+    return static_cast<X*>(p);
+  }
+  ~Arena() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+template <class T>
+struct Lin {  // y = x . W, W^T packed [N][K] (K padded to 8, zeros)
+  const T* w = nullptr;
+  int N = 0, K = 0;
+  const float* bias = nullptr;
+};
+
+struct MoeW {
+  const float* gate_t = nullptr;  // [E][d]
+  const float* bias = nullptr;    // [E]
+  const void* w13 = nullptr;      // bf16: [E][2h][d] interleaved per 128 rows; fp32: w1 [E][h][d]
+  const void* w3 = nullptr;       // fp32 only: [E][h][d]
+  const void* w2 = nullptr;       // [E][d][h]
+};
+
+}  // namespace
+
+void validate_batch(const orx_config& cfg, const orx_user_batch& b) {  // validate_context, policy.cpp:23-38
+  require(b.n_users >= 0, "negative user count");
+  auto check = [&](const orx_records& r, int cap, const char* name) {
+    if (b.n_users == 0) return;
+    require(r.offsets != nullptr, std::string(name) + ": offsets required");
+    require(r.offsets[0] == 0, std::string(name) + ": offsets must start at 0");
+    for (int u = 0; u < b.n_users; ++u) {
+      int64_t s = r.offsets[u], e = r.offsets[u + 1];
+      require(e >= s, std::string(name) + ": offsets must be non-decreasing");
+      require(e - s <= cap, std::string(name) + " sequence exceeds its configured cap");
+      for (int64_t i = s; i < e; ++i) {
+        if (i > s) require(r.ts[i] >= r.ts[i - 1], std::string(name) + " sequence not time-ordered");
+        require(r.playtime[i] <= r.duration[i] * 1.0 + 1e-6, "playtime exceeds duration");
+        require(cfg.n_label_flags >= 32 || r.labels[i] < (1u << cfg.n_label_flags), "label bits outside defined flags");
+        if (cfg.use_sid_history) {
+          require(r.sid != nullptr, "sid history enabled but record lacks semantic id codes");
+          for (int l = 0; l < cfg.n_code_layers; ++l) {
+            int c = r.sid[i * cfg.n_code_layers + l];
+            require(c >= 0 && c < cfg.codebook_size, "sid code outside its layer vocabulary");
+          }
+        }
+      }
+    }
+  };
+  check(b.short_seq, cfg.short_len, "short");
+  check(b.positive_seq, cfg.positive_len, "positive");
+  check(b.lifelong_seq, cfg.lifelong_len, "lifelong");
+}
+
+template <class T>
+class EngineT final : public Engine {
+  static constexpr bool kBf16 = std::is_same_v<T, __nv_bfloat16>;
+
+ public:
+  EngineT(const HostWeights& hw, int device, int max_users, int max_width)
+      : cfg_(hw.cfg), dev_(device), maxU_(max_users), maxW_(max_width) {
+    CUDA_CHECK(cudaSetDevice(dev_));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    require(max_users >= 1 && max_width >= 1, "engine capacity must be positive");
+    require(cfg_.n_code_layers <= 8, "n_code_layers above 8 is not supported");
+    require(!cfg_.moe_enabled || cfg_.n_experts <= 32, "more than 32 experts is not supported");
+    require(max_width <= 1024, "beam width above 1024 is not supported");
+    if (kBf16) {
+      require((cfg_.d_model / cfg_.n_heads) % 32 == 0 && cfg_.d_model / cfg_.n_heads <= 128,
+              "bf16 mode needs head dim 32, 64 or 128");
+      require(!cfg_.moe_enabled || expert_hidden(cfg_) % 128 == 0, "bf16 MoE needs expert hidden % 128 == 0");
+    }
+    upload(hw);
+    alloc_activations();
+  }
+  ~EngineT() override {
+    cudaSetDevice(dev_);
+    cudaStreamSynchronize(st_);
+    if (host_stage_) cudaFreeHost(host_stage_);
+    if (host_out_) cudaFreeHost(host_out_);
+    cudaStreamDestroy(st_);
+  }
+
+  void* stream() override { return st_; }
+
+  // ------------------------------------------------------------------------
+  // weights
+  // ------------------------------------------------------------------------
+  const float* upload_f32(const float* src, size_t n) {
+    float* d = ar_.alloc<float>(n);
+    CUDA_CHECK(cudaMemcpy(d, src, n * 4, cudaMemcpyHostToDevice));
+    return d;
+  }
+  const float* up(const HostWeights& hw, const std::string& name) {
+    const Tensor& t = hw.get(name);
+    return upload_f32(t.data.data(), t.data.size());
+  }
+  // Pack several (in, out) row-major weights side by side along N: W^T [sum N][Kp].
+  Lin<T> pack(const HostWeights& hw, const std::vector<std::string>& names, const std::string& bias = "") {
+    const Tensor& f = hw.get(names[0]);
+    int K = f.rows, N = 0;
+    for (auto& n : names) {
+      require(hw.get(n).rows == K, "pack: inner dims differ");
+      N += hw.get(n).cols;
+    }
+    int Kp = rup(K, 8);
+    std::vector<T> h(static_cast<size_t>(N) * Kp, to_t<T>(0.f));
+    int n0 = 0;
+    for (auto& n : names) {
+      const Tensor& t = hw.get(n);
+      for (int k = 0; k < K; ++k)
+        for (int j = 0; j < t.cols; ++j) h[static_cast<size_t>(n0 + j) * Kp + k] = to_t<T>(t.data[(size_t)k * t.cols + j]);
+      n0 += t.cols;
+    }
+    T* d = ar_.alloc<T>(h.size());
+    CUDA_CHECK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    Lin<T> L;
+    L.w = d;
+    L.N = N;
+    L.K = Kp;
+    if (!bias.empty()) L.bias = up(hw, bias);
+    return L;
+  }
+  MoeW pack_moe(const HostWeights& hw, const std::string& n) {
+    const int d = cfg_.d_model, E = cfg_.n_experts, h = expert_hidden(cfg_);
+    MoeW m;
+    const Tensor& g = hw.get(n + ".gate.w");  // (d, E)
+    std::vector<float> gt(static_cast<size_t>(E) * d);
+    for (int k = 0; k < d; ++k)
+      for (int e = 0; e < E; ++e) gt[(size_t)e * d + k] = g.data[(size_t)k * E + e];
+    m.gate_t = upload_f32(gt.data(), gt.size());
+    m.bias = up(hw, n + ".routing_bias");
+    const int dp = rup(d, 8), hp = rup(h, 8);
+    auto ex = [&](int e, const char* w) { return hw.get(n + ".expert" + std::to_string(e) + "." + w + ".w"); };
+    if (kBf16) {
+      std::vector<T> w13(static_cast<size_t>(E) * 2 * h * dp, to_t<T>(0.f));
+      for (int e = 0; e < E; ++e) {
+        const Tensor& w1 = ex(e, "w1");
+        const Tensor& w3 = ex(e, "w3");
+        for (int j = 0; j < h; ++j) {
+          // output column j -> block j/128; W1 rows first, then W3 rows, per 256-row tile
+          size_t r1 = (size_t)e * 2 * h + (j / 128) * 256 + (j % 128);
+          size_t r3 = r1 + 128;
+          for (int k = 0; k < d; ++k) {
+            w13[r1 * dp + k] = to_t<T>(w1.data[(size_t)k * h + j]);
+            w13[r3 * dp + k] = to_t<T>(w3.data[(size_t)k * h + j]);
+          }
+        }
+      }
+      T* p = ar_.alloc<T>(w13.size());
+      CUDA_CHECK(cudaMemcpy(p, w13.data(), w13.size() * sizeof(T), cudaMemcpyHostToDevice));
+      m.w13 = p;
+    } else {
+      for (int which = 0; which < 2; ++which) {
+        std::vector<T> w(static_cast<size_t>(E) * h * dp, to_t<T>(0.f));
+        for (int e = 0; e < E; ++e) {
+          const Tensor& t = ex(e, which == 0 ? "w1" : "w3");
+          for (int j = 0; j < h; ++j)
+            for (int k = 0; k < d; ++k) w[((size_t)e * h + j) * dp + k] = to_t<T>(t.data[(size_t)k * h + j]);
+        }
+        T* p = ar_.alloc<T>(w.size());
+        CUDA_CHECK(cudaMemcpy(p, w.data(), w.size() * sizeof(T), cudaMemcpyHostToDevice));
+        (which == 0 ? m.w13 : m.w3) = p;
+      }
+    }
+    std::vector<T> w2(static_cast<size_t>(E) * d * hp, to_t<T>(0.f));
+    for (int e = 0; e < E; ++e) {
+      const Tensor& t = ex(e, "w2");  // (h, d)
+      for (int k = 0; k < h; ++k)
+        for (int j = 0; j < d; ++j) w2[((size_t)e * d + j) * hp + k] = to_t<T>(t.data[(size_t)k * d + j]);
+    }
+    T* p = ar_.alloc<T>(w2.size());
+    CUDA_CHECK(cudaMemcpy(p, w2.data(), w2.size() * sizeof(T), cudaMemcpyHostToDevice));
+    m.w2 = p;
+    return m;
+  }
+
+  struct Mlp { Lin<T> fc1, fc2; };
+  struct QBlock { Lin<T> wq, wkv, wo, fc1, fc2; const float* gain; };
+  struct EncL { const float *n1, *n2; Lin<T> wqkv, wo, fc1, fc2; MoeW moe; };
+  struct DecL { const float *n1, *n2, *n3; Lin<T> sqkv, so, cq, co, fc1, fc2; MoeW moe; };
+
+  void upload(const HostWeights& hw) {
+    const orx_config& c = cfg_;
+    auto mlp = [&](const std::string& n) {
+      return Mlp{pack(hw, {n + ".fc1.w"}, n + ".fc1.b"), pack(hw, {n + ".fc2.w"}, n + ".fc2.b")};
+    };
+    t_uid_ = up(hw, "emb.uid");
+    t_gender_ = up(hw, "emb.gender");
+    t_age_ = up(hw, "emb.age");
+    t_vid_ = up(hw, "emb.vid");
+    t_aid_ = up(hw, "emb.aid");
+    t_label_ = up(hw, "emb.label");
+    t_tag_ = up(hw, "emb.tag");
+    t_ts_ = up(hw, "emb.ts");
+    t_play_ = up(hw, "emb.playtime");
+    t_dur_ = up(hw, "emb.duration");
+    pad_s_ = up(hw, "pad.short");
+    pad_p_ = up(hw, "pad.positive");
+    pad_l_ = up(hw, "pad.lifelong");
+    pos_ = up(hw, "emb.pos");
+    bos_ = up(hw, "dec.bos");
+    for (int l = 0; l < c.n_code_layers; ++l) {
+      tokens_.push_back(up(hw, "dec.tokens" + std::to_string(l)));
+      heads_.push_back(pack(hw, {"dec.head" + std::to_string(l) + ".w"}));
+    }
+    p_static_ = mlp("pathway.static");
+    p_short_ = mlp("pathway.short");
+    p_pos_ = mlp("pathway.positive");
+    p_life_ = mlp("pathway.lifelong");
+    {  // lifelong.queries as a GEMM operand [Nq][d]
+      const Tensor& q = hw.get("lifelong.queries");
+      std::vector<T> h(q.data.size());
+      for (size_t i = 0; i < h.size(); ++i) h[i] = to_t<T>(q.data[i]);
+      T* p = ar_.alloc<T>(h.size());
+      CUDA_CHECK(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+      queries_ = p;
+    }
+    for (int b = 0; b < c.lifelong_blocks; ++b) {
+      std::string n = "lifelong.block" + std::to_string(b);
+      QBlock q;
+      q.wq = pack(hw, {n + ".attn.wq.w"});
+      q.wkv = pack(hw, {n + ".attn.wk.w", n + ".attn.wv.w"});
+      q.wo = pack(hw, {n + ".attn.wo.w"});
+      q.gain = up(hw, n + ".norm.gain");
+      q.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b");
+      q.fc2 = pack(hw, {n + ".ffn.fc2.w"}, n + ".ffn.fc2.b");
+      qblocks_.push_back(q);
+    }
+    for (int l = 0; l < enc_layers(c); ++l) {
+      std::string n = "enc" + std::to_string(l);
+      EncL e;
+      e.n1 = up(hw, n + ".n1.gain");
+      e.n2 = up(hw, n + ".n2.gain");
+      e.wqkv = pack(hw, {n + ".attn.wq.w", n + ".attn.wk.w", n + ".attn.wv.w"});
+      e.wo = pack(hw, {n + ".attn.wo.w"});
+      if (enc_moe(c)) e.moe = pack_moe(hw, n + ".moe");
+      else {
+        e.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b");
+        e.fc2 = pack(hw, {n + ".ffn.fc2.w"}, n + ".ffn.fc2.b");
+      }
+      enc_.push_back(e);
+    }
+    std::vector<std::string> xkv;
+    for (int l = 0; l < dec_layers(c); ++l) {
+      std::string n = "dec" + std::to_string(l);
+      DecL e;
+      e.n1 = up(hw, n + ".n1.gain");
+      e.n2 = up(hw, n + ".n2.gain");
+      e.n3 = up(hw, n + ".n3.gain");
+      e.sqkv = pack(hw, {n + ".self.wq.w", n + ".self.wk.w", n + ".self.wv.w"});
+      e.so = pack(hw, {n + ".self.wo.w"});
+      e.cq = pack(hw, {n + ".cross.wq.w"});
+      e.co = pack(hw, {n + ".cross.wo.w"});
+      xkv.push_back(n + ".cross.wk.w");
+      xkv.push_back(n + ".cross.wv.w");
+      if (c.moe_enabled) e.moe = pack_moe(hw, n + ".moe");
+      else {
+        e.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b");
+        e.fc2 = pack(hw, {n + ".ffn.fc2.w"}, n + ".ffn.fc2.b");
+      }
+      dec_.push_back(e);
+    }
+    xkv_w_ = pack(hw, xkv);  // all decoder layers' cross K|V in one GEMM
+  }
+
+  // ------------------------------------------------------------------------
+  // activations
+  // ------------------------------------------------------------------------
+  void alloc_activations() {
+    const orx_config& c = cfg_;
+    const int d = c.d_model, U = maxU_, Tn = enc_seq_len(c), Nq = c.n_queries, L = c.n_code_layers;
+    const int Ld = dec_layers(c);
+    Rd_ = static_cast<int64_t>(U) * maxW_;
+    const int64_t rec_max = static_cast<int64_t>(U) * std::max({c.short_len, c.positive_len, c.lifelong_len, 1});
+    const int64_t keys_max = static_cast<int64_t>(U) * std::max(c.lifelong_len, 1);
+    const int64_t rows_enc = static_cast<int64_t>(U) * Tn;
+    const int64_t rows_big = std::max<int64_t>({rows_enc, Rd_, static_cast<int64_t>(U) * Nq});
+    Fp_ = rup(feat_dim(c), 8);
+    Sp_ = rup(3 * static_dim(c), 8);
+    feat_ = ar_.alloc<T>(static_cast<size_t>(std::max<int64_t>(rec_max, U)) * std::max(Fp_, Sp_));
+    hid_ = ar_.alloc<T>(static_cast<size_t>(std::max<int64_t>(rec_max, U)) * d);
+    keys_ = ar_.alloc<T>(static_cast<size_t>(keys_max) * d);
+    kvl_ = ar_.alloc<T>(static_cast<size_t>(keys_max) * 2 * d);
+    z_ = ar_.alloc<float>(static_cast<size_t>(rows_enc) * d);
+    xn_ = ar_.alloc<T>(static_cast<size_t>(rows_big) * d);
+    qkv_ = ar_.alloc<T>(static_cast<size_t>(rows_big) * 3 * d);
+    att_ = ar_.alloc<T>(static_cast<size_t>(rows_big) * d);
+    ffh_ = ar_.alloc<T>(static_cast<size_t>(rows_big) * c.ffn_hidden);
+    qproj_ = ar_.alloc<T>(static_cast<size_t>(U) * Nq * d);
+    qo_ = ar_.alloc<float>(static_cast<size_t>(U) * Nq * d);
+    qcur_ = ar_.alloc<T>(static_cast<size_t>(U) * Nq * d);
+    zt_ = kBf16 ? ar_.alloc<T>(static_cast<size_t>(rows_enc) * d) : reinterpret_cast<T*>(z_);
+    xkv_ = ar_.alloc<T>(static_cast<size_t>(rows_enc) * 2 * d * Ld);
+    h_ = ar_.alloc<float>(static_cast<size_t>(Rd_) * d);
+    for (int p = 0; p < L; ++p) cache_.push_back(ar_.alloc<T>(static_cast<size_t>(Rd_) * Ld * 2 * d));
+    cache_ptrs_ = ar_.alloc<T*>(L);
+    CUDA_CHECK(cudaMemcpy(cache_ptrs_, cache_.data(), L * sizeof(T*), cudaMemcpyHostToDevice));
+    logits_ = ar_.alloc<float>(static_cast<size_t>(Rd_) * c.codebook_size);
+    const int ksel = std::min(maxW_, c.codebook_size);
+    cand_ = ar_.alloc<uint64_t>(static_cast<size_t>(Rd_) * ksel);
+    lse_ = ar_.alloc<float>(Rd_);
+    for (int s = 0; s < 2; ++s) {
+      bs_[s].codes = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
+      bs_[s].score = ar_.alloc<float>(Rd_);
+      bs_[s].score64 = ar_.alloc<double>(Rd_);
+      bs_[s].lexrank = ar_.alloc<int32_t>(Rd_);
+      bs_[s].lex2beam = ar_.alloc<int32_t>(Rd_);
+      bs_[s].anc = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
+    }
+    tf_anc_ = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
+    tf_codes_ = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
+    grp_start_ = ar_.alloc<int32_t>(Rd_ + 1);
+    grp_len_ = ar_.alloc<int32_t>(Rd_ + 1);
+    grp_kstart_ = ar_.alloc<int32_t>(Rd_ + 1);
+    if (c.moe_enabled) {
+      const int E = c.n_experts, k = c.experts_active, h = expert_hidden(c);
+      const int64_t mrows = std::max(rows_enc, Rd_);
+      S_ = mrows * k + static_cast<int64_t>(E) * 128;
+      max_tiles_ = static_cast<int>(S_ / 128 + 1);
+      sel_ = ar_.alloc<int32_t>(mrows * k);
+      wts_ = ar_.alloc<float>(mrows * k);
+      slot_ = ar_.alloc<int32_t>(mrows * k);
+      counts_ = ar_.alloc<int32_t>(E);
+      cursor_ = ar_.alloc<int32_t>(E);
+      tile_expert_ = ar_.alloc<int32_t>(max_tiles_);
+      n_mtiles_ = ar_.alloc<int32_t>(1);
+      row_scale_ = ar_.alloc<float>(S_);
+      xg_ = ar_.alloc<T>(static_cast<size_t>(S_) * d);
+      hg_ = ar_.alloc<T>(static_cast<size_t>(S_) * rup(h, 8));
+      yg_ = ar_.alloc<float>(static_cast<size_t>(S_) * d);
+      CUDA_CHECK(cudaMemset(xg_, 0, static_cast<size_t>(S_) * d * sizeof(T)));
+      if (!kBf16) {
+        ga_ = ar_.alloc<float>(static_cast<size_t>(S_) * h);
+        gb_ = ar_.alloc<float>(static_cast<size_t>(S_) * h);
+      }
+    }
+    // user batch staging (device side); host side is pinned and grown on demand
+    stage_cap_ = 0;
+  }
+
+  // ------------------------------------------------------------------------
+  // GEMM helper
+  // ------------------------------------------------------------------------
+  Epi epi(void* out, int ldo, bool out_f32) {
+    Epi e;
+    e.out = out;
+    e.ldo = ldo;
+    e.out_bf16 = (!out_f32 && kBf16) ? 1 : 0;
+    return e;
+  }
+  void gemm(const T* A, int lda, const Lin<T>& W, int M, Epi e) {
+    if (M <= 0) return;
+    if (!e.n_out) e.n_out = W.N;
+    if (!e.m_valid) e.m_valid = M;
+    if (!e.bias) e.bias = W.bias;
+    if constexpr (kBf16) gemm_bf16(A, lda, W.w, W.K, M, W.N, W.K, e, nullptr, st_);
+    else gemm_f32(A, lda, W.w, W.K, M, W.N, W.K, e, nullptr, st_);
+  }
+
+  // ------------------------------------------------------------------------
+  // user batch staging: one pinned arena, one H2D copy
+  // ------------------------------------------------------------------------
+  struct Stage {
+    int U = 0;
+    int n_rec[3] = {0, 0, 0};  // short, positive, lifelong
+    int n_keys = 0;
+    int n_pad_keys = 0;
+    size_t off_uid, off_gender, off_age, off_ns, off_np, off_kstart, off_klen, off_static_map, off_life_map,
+        off_pad_keys;
+    size_t off_vid[3], off_aid[3], off_tag[3], off_ts[3], off_play[3], off_dur[3], off_lab[3], off_sid[3],
+        off_map[3];
+    size_t bytes = 0;
+  } sg_;
+
+  void stage_batch(const orx_user_batch& b) override {
+    const orx_config& c = cfg_;
+    validate_batch(c, b);
+    CUDA_CHECK(cudaStreamSynchronize(st_));  // previous copy out of the pinned stage has finished
+    require(b.n_users >= 1 && b.n_users <= maxU_, "batch size outside the engine capacity");
+    CUDA_CHECK(cudaSetDevice(dev_));
+    Stage s;
+    s.U = b.n_users;
+    const orx_records* rs[3] = {&b.short_seq, &b.positive_seq, &b.lifelong_seq};
+    for (int p = 0; p < 3; ++p) s.n_rec[p] = static_cast<int>(rs[p]->offsets[s.U]);
+    const int Tn = enc_seq_len(c), Nq = c.n_queries, L = c.n_code_layers;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      size_t o = off;
+      off += (bytes + 15) / 16 * 16;
+      return o;
+    };
+    s.off_uid = take(4 * s.U);
+    s.off_gender = take(4 * s.U);
+    s.off_age = take(4 * s.U);
+    s.off_ns = take(4 * s.U);
+    s.off_np = take(4 * s.U);
+    s.off_kstart = take(4 * s.U);
+    s.off_klen = take(4 * s.U);
+    s.off_static_map = take(4 * s.U);
+    s.off_life_map = take(4 * static_cast<size_t>(s.U) * Nq);
+    s.off_pad_keys = take(4 * s.U);
+    for (int p = 0; p < 3; ++p) {
+      size_t n = s.n_rec[p];
+      s.off_vid[p] = take(8 * n);
+      s.off_aid[p] = take(4 * n);
+      s.off_tag[p] = take(4 * n);
+      s.off_ts[p] = take(4 * n);
+      s.off_play[p] = take(4 * n);
+      s.off_dur[p] = take(4 * n);
+      s.off_lab[p] = take(4 * n);
+      s.off_sid[p] = take(c.use_sid_history ? 4 * n * L : 0);
+      s.off_map[p] = take(4 * n);
+    }
+    s.bytes = off;
+    if (s.bytes > stage_cap_) {
+      if (host_stage_) cudaFreeHost(host_stage_);
+      CUDA_CHECK(cudaMallocHost(&host_stage_, s.bytes));
+      dev_stage_ = ar_.alloc<uint8_t>(s.bytes);
+      stage_cap_ = s.bytes;
+    }
+    uint8_t* H = static_cast<uint8_t*>(host_stage_);
+    auto I32 = [&](size_t o) { return reinterpret_cast<int32_t*>(H + o); };
+    auto F32 = [&](size_t o) { return reinterpret_cast<float*>(H + o); };
+    for (int u = 0; u < s.U; ++u) {
+      I32(s.off_uid)[u] = b.uid[u];
+      I32(s.off_gender)[u] = b.gender[u];
+      I32(s.off_age)[u] = b.age_bucket[u];
+      I32(s.off_ns)[u] = static_cast<int32_t>(b.short_seq.offsets[u + 1] - b.short_seq.offsets[u]);
+      I32(s.off_np)[u] = static_cast<int32_t>(b.positive_seq.offsets[u + 1] - b.positive_seq.offsets[u]);
+      I32(s.off_static_map)[u] = u * Tn;
+      for (int q = 0; q < Nq; ++q) I32(s.off_life_map)[u * Nq + q] = u * Tn + 1 + c.short_len + c.positive_len + q;
+    }
+    // lifelong key rows: user u owns [kstart, kstart + max(1, n)); empty -> one pad key (policy.cpp:205-207)
+    int kpos = 0, npad = 0;
+    for (int u = 0; u < s.U; ++u) {
+      int n = static_cast<int>(b.lifelong_seq.offsets[u + 1] - b.lifelong_seq.offsets[u]);
+      I32(s.off_kstart)[u] = kpos;
+      I32(s.off_klen)[u] = std::max(n, 1);
+      if (n == 0) I32(s.off_pad_keys)[npad++] = kpos;
+      kpos += std::max(n, 1);
+    }
+    s.n_keys = kpos;
+    s.n_pad_keys = npad;
+    for (int p = 0; p < 3; ++p) {
+      const orx_records& r = *rs[p];
+      const size_t n = s.n_rec[p];
+      if (n == 0) continue;
+      memcpy(H + s.off_vid[p], r.vid, 8 * n);
+      memcpy(H + s.off_aid[p], r.aid, 4 * n);
+      memcpy(H + s.off_lab[p], r.labels, 4 * n);
+      for (size_t i = 0; i < n; ++i) {
+        F32(s.off_tag[p])[i] = static_cast<float>(r.tag[i]);
+        F32(s.off_ts[p])[i] = static_cast<float>(r.ts[i]);
+        F32(s.off_play[p])[i] = static_cast<float>(r.playtime[i]);
+        F32(s.off_dur[p])[i] = static_cast<float>(r.duration[i]);
+      }
+      if (c.use_sid_history) memcpy(H + s.off_sid[p], r.sid, 4 * n * L);
+      int32_t* map = I32(s.off_map[p]);
+      for (int u = 0; u < s.U; ++u) {
+        int64_t b0 = r.offsets[u], e0 = r.offsets[u + 1];
+        int cnt = static_cast<int>(e0 - b0);
+        for (int64_t i = b0; i < e0; ++i) {
+          int j = static_cast<int>(i - b0);
+          if (p == 0) map[i] = u * Tn + 1 + (c.short_len - cnt) + j;  // left padding, policy.cpp:209-215
+          else if (p == 1) map[i] = u * Tn + 1 + c.short_len + (c.positive_len - cnt) + j;
+          else map[i] = I32(s.off_kstart)[u] + j;
+        }
+      }
+    }
+    CUDA_CHECK(cudaMemcpyAsync(dev_stage_, host_stage_, s.bytes, cudaMemcpyHostToDevice, st_));
+    h2d_bytes += static_cast<int64_t>(s.bytes);
+    sg_ = s;
+    staged_ = true;
+  }
+  template <class X>
+  const X* dp(size_t off) const {
+    return reinterpret_cast<const X*>(dev_stage_ + off);
+  }
+  RecordsDev recs(int p) const {
+    RecordsDev r;
+    r.n = sg_.n_rec[p];
+    r.vid = dp<int64_t>(sg_.off_vid[p]);
+    r.aid = dp<int32_t>(sg_.off_aid[p]);
+    r.tag = dp<float>(sg_.off_tag[p]);
+    r.ts = dp<float>(sg_.off_ts[p]);
+    r.play = dp<float>(sg_.off_play[p]);
+    r.dur = dp<float>(sg_.off_dur[p]);
+    r.labels = dp<uint32_t>(sg_.off_lab[p]);
+    r.sid = cfg_.use_sid_history ? dp<int32_t>(sg_.off_sid[p]) : nullptr;
+    return r;
+  }
+  FeatureTables tables() const {
+    const orx_config& c = cfg_;
+    FeatureTables t{};
+    t.vid = t_vid_;
+    t.aid = t_aid_;
+    t.tag = t_tag_;
+    t.ts = t_ts_;
+    t.play = t_play_;
+    t.dur = t_dur_;
+    t.label = t_label_;
+    for (int l = 0; l < c.n_code_layers && l < 8; ++l) t.tokens[l] = tokens_[l];
+    t.d = c.d_model;
+    t.aid_dim = aid_dim(c);
+    t.minor = minor_dim(c);
+    t.vid_vocab = c.vid_vocab;
+    t.aid_vocab = c.aid_vocab;
+    t.n_flags = c.n_label_flags;
+    t.n_code_layers = c.n_code_layers;
+    t.use_sid = c.use_sid_history;
+    t.vid_only = c.vid_only_features;
+    return t;
+  }
+
+  // ------------------------------------------------------------------------
+  // encode (policy.cpp:254-265)
+  // ------------------------------------------------------------------------
+  void run_encode() {
+    require(staged_, "no user batch staged");
+    const orx_config& c = cfg_;
+    const int d = c.d_model, U = sg_.U, Tn = enc_seq_len(c), Nq = c.n_queries, H = c.n_heads, dh = d / H;
+    launch_z_init(U, Tn, d, pos_, pad_s_, pad_p_, dp<int32_t>(sg_.off_ns), dp<int32_t>(sg_.off_np), c.short_len,
+                  c.positive_len, z_, st_);
+    // static pathway (policy.cpp:218-223): [uid|gender|age] -> MLP -> row 0
+    launch_static_features<T>(U, dp<int32_t>(sg_.off_uid), dp<int32_t>(sg_.off_gender), dp<int32_t>(sg_.off_age),
+                              t_uid_, t_gender_, t_age_, static_dim(c), c.uid_vocab, c.gender_vocab, c.age_vocab,
+                              feat_, Sp_, st_);
+    mlp_into_z(p_static_, feat_, Sp_, U, dp<int32_t>(sg_.off_static_map));
+    // short / positive pathways: MLP rows land left-padded inside z
+    const FeatureTables tb = tables();
+    for (int p = 0; p < 2; ++p) {
+      if (!sg_.n_rec[p]) continue;
+      launch_features<T>(recs(p), tb, feat_, Fp_, st_);
+      mlp_into_z(p == 0 ? p_short_ : p_pos_, feat_, Fp_, sg_.n_rec[p], dp<int32_t>(sg_.off_map[p]));
+    }
+    // lifelong pathway -> keys (policy.cpp:233-238)
+    if (sg_.n_rec[2]) {
+      launch_features<T>(recs(2), tb, feat_, Fp_, st_);
+      const Mlp& m = p_life_;
+      Epi e1 = epi(hid_, d, false);
+      e1.act = ACT_LEAKY;
+      gemm(feat_, Fp_, m.fc1, sg_.n_rec[2], e1);
+      Epi e2 = epi(keys_, d, false);
+      e2.row_map = dp<int32_t>(sg_.off_map[2]);
+      gemm(hid_, d, m.fc2, sg_.n_rec[2], e2);
+    }
+    if (sg_.n_pad_keys) launch_fill_rows<T>(sg_.n_pad_keys, d, pad_l_, keys_, d, dp<int32_t>(sg_.off_pad_keys), st_);
+    // QFormer blocks, no residual (nn.cpp:97-100)
+    for (size_t b = 0; b < qblocks_.size(); ++b) {
+      const QBlock& q = qblocks_[b];
+      const bool first = b == 0, last = b + 1 == qblocks_.size();
+      if (first) gemm(queries_, rup(d, 8), q.wq, Nq, epi(qproj_, d, false));  // user-independent
+      else gemm(qcur_, d, q.wq, U * Nq, epi(qproj_, d, false));
+      gemm(keys_, d, q.wkv, sg_.n_keys, epi(kvl_, 2 * d, false));
+      Seg qs;
+      qs.stride = first ? 0 : Nq;
+      qs.fixed_len = Nq;
+      Seg ks;
+      ks.start = dp<int32_t>(sg_.off_kstart);
+      ks.len = dp<int32_t>(sg_.off_klen);
+      Seg os;
+      os.stride = Nq;
+      os.fixed_len = Nq;
+      launch_attention<T>(U, Nq, H, dh, qproj_, d, kvl_, 2 * d, kvl_ + d, 2 * d, att_, d, qs, ks, os, st_);
+      gemm(att_, d, q.wo, U * Nq, epi(qo_, d, true));
+      launch_rmsnorm<T>(U * Nq, d, qo_, d, q.gain, xn_, d, st_);
+      Epi e1 = epi(ffh_, c.ffn_hidden, false);
+      e1.act = ACT_SILU;
+      gemm(xn_, d, q.fc1, U * Nq, e1);
+      if (last) {
+        Epi e2 = epi(z_, d, true);
+        e2.resid = z_;
+        e2.ld_resid = d;
+        e2.row_map = dp<int32_t>(sg_.off_life_map);
+        gemm(ffh_, c.ffn_hidden, q.fc2, U * Nq, e2);
+      } else {
+        gemm(ffh_, c.ffn_hidden, q.fc2, U * Nq, epi(qcur_, d, false));
+      }
+    }
+    // encoder blocks (policy.cpp:259-263)
+    const int R = U * Tn;
+    for (const EncL& l : enc_) {
+      launch_rmsnorm<T>(R, d, z_, d, l.n1, xn_, d, st_);
+      gemm(xn_, d, l.wqkv, R, epi(qkv_, 3 * d, false));
+      Seg s;
+      s.stride = Tn;
+      s.fixed_len = Tn;
+      launch_attention<T>(U, Tn, H, dh, qkv_, 3 * d, qkv_ + d, 3 * d, qkv_ + 2 * d, 3 * d, att_, d, s, s, s, st_);
+      Epi eo = epi(z_, d, true);
+      eo.resid = z_;
+      eo.ld_resid = d;
+      gemm(att_, d, l.wo, R, eo);
+      launch_rmsnorm<T>(R, d, z_, d, l.n2, xn_, d, st_);
+      if (enc_moe(c)) {
+        moe(l.moe, xn_, R, z_);
+      } else {
+        ffn(l.fc1, l.fc2, xn_, R, z_);
+      }
+    }
+  }
+
+  void mlp_into_z(const Mlp& m, const T* x, int ldx, int rows, const int32_t* map) {
+    const int d = cfg_.d_model;
+    Epi e1 = epi(hid_, d, false);
+    e1.act = ACT_LEAKY;
+    gemm(x, ldx, m.fc1, rows, e1);
+    Epi e2 = epi(z_, d, true);
+    e2.resid = z_;
+    e2.ld_resid = d;
+    e2.row_map = map;
+    gemm(hid_, d, m.fc2, rows, e2);
+  }
+  // h += fc2(silu(fc1(x)))  (ffn, nn.cpp:71-73)
+  void ffn(const Lin<T>& fc1, const Lin<T>& fc2, const T* x, int rows, float* h) {
+    const int d = cfg_.d_model;
+    Epi e1 = epi(ffh_, cfg_.ffn_hidden, false);
+    e1.act = ACT_SILU;
+    gemm(x, d, fc1, rows, e1);
+    Epi e2 = epi(h, d, true);
+    e2.resid = h;
+    e2.ld_resid = d;
+    gemm(ffh_, cfg_.ffn_hidden, fc2, rows, e2);
+  }
+  // h += MoE(x)  (moe_forward, nn.cpp:117-172)
+  void moe(const MoeW& m, const T* x, int rows, float* h) {
+    const orx_config& c = cfg_;
+    const int d = c.d_model, E = c.n_experts, k = c.experts_active, he = expert_hidden(c), hp = rup(he, 8);
+    CUDA_CHECK(cudaMemsetAsync(counts_, 0, E * sizeof(int32_t), st_));
+    launch_moe_route<T>(rows, d, E, k, x, d, m.gate_t, m.bias, sel_, wts_, counts_, st_);
+    launch_moe_plan(E, counts_, cursor_, tile_expert_, max_tiles_, n_mtiles_, st_);
+    launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xg_, row_scale_, st_);
+    Grouped g;
+    g.tile_expert = tile_expert_;
+    g.n_mtiles = n_mtiles_;
+    g.n_groups = E;
+    const int M = static_cast<int>(S_);
+    if constexpr (kBf16) {
+      Epi e1 = epi(hg_, hp, false);
+      e1.swiglu = 1;
+      e1.n_out = he;
+      e1.m_valid = M;
+      g.b_rows_per_expert = 2 * he;
+      gemm_bf16(xg_, d, m.w13, rup(d, 8), M, 2 * he, rup(d, 8), e1, &g, st_);
+      Epi e2 = epi(yg_, d, true);
+      e2.row_scale = row_scale_;
+      e2.n_out = d;
+      e2.m_valid = M;
+      g.b_rows_per_expert = d;
+      gemm_bf16(hg_, hp, m.w2, hp, M, d, hp, e2, &g, st_);
+    } else {
+      g.b_rows_per_expert = he;
+      Epi ea = epi(ga_, he, true);
+      ea.n_out = he;
+      ea.m_valid = M;
+      gemm_f32(reinterpret_cast<const float*>(xg_), d, static_cast<const float*>(m.w13), rup(d, 8), M, he, rup(d, 8),
+               ea, &g, st_);
+      Epi eb = ea;
+      eb.out = gb_;
+      gemm_f32(reinterpret_cast<const float*>(xg_), d, static_cast<const float*>(m.w3), rup(d, 8), M, he, rup(d, 8),
+               eb, &g, st_);
+      launch_swiglu_mul(static_cast<long long>(S_) * he, ga_, gb_, reinterpret_cast<float*>(hg_), st_);
+      Epi e2 = epi(yg_, d, true);
+      e2.row_scale = row_scale_;
+      e2.n_out = d;
+      e2.m_valid = M;
+      g.b_rows_per_expert = d;
+      gemm_f32(reinterpret_cast<const float*>(hg_), he, static_cast<const float*>(m.w2), hp, M, d, he, e2, &g, st_);
+    }
+    launch_moe_combine(rows, k, d, yg_, slot_, h, d, st_);
+  }
+
+  void prepare_decoder(int U) {
+    const int d = cfg_.d_model, Tn = enc_seq_len(cfg_);
+    if constexpr (kBf16) launch_convert<T>(U * Tn, d, z_, d, zt_, d, st_);
+    gemm(zt_, d, xkv_w_, U * Tn, epi(xkv_, xkv_w_.N, false));
+  }
+
+  // One decoder position for `rows` rows (policy.cpp:267-295). Rows of a
+  // group (user) are contiguous: group g = rows [gq.start(g), +gq.len(g)),
+  // cross-attending to encoder rows [gk.start(g), +Tn).
+  void decode_step(int step, int rows, int groups, Seg gq, Seg gk, const int32_t* codes, int code_stride,
+                   const int32_t* anc, int anc_stride, int max_group_rows) {
+    const orx_config& c = cfg_;
+    const int d = c.d_model, H = c.n_heads, dh = d / H, Ld = dec_layers(c), Tn = enc_seq_len(c);
+    launch_dec_embed(rows, d, step == 0 ? bos_ : tokens_[step - 1], step == 0 ? nullptr : codes + (step - 1),
+                     code_stride, h_, st_);
+    for (int l = 0; l < Ld; ++l) {
+      const DecL& w = dec_[l];
+      launch_rmsnorm<T>(rows, d, h_, d, w.n1, xn_, d, st_);
+      gemm(xn_, d, w.sqkv, rows, epi(qkv_, 3 * d, false));
+      launch_dec_self_attn<T>(rows, d, H, step, l, Ld, qkv_, cache_ptrs_, anc, anc_stride, att_, st_);
+      Epi e = epi(h_, d, true);
+      e.resid = h_;
+      e.ld_resid = d;
+      gemm(att_, d, w.so, rows, e);
+      launch_rmsnorm<T>(rows, d, h_, d, w.n2, xn_, d, st_);
+      gemm(xn_, d, w.cq, rows, epi(qkv_, d, false));
+      const int ldkv = 2 * d * Ld;
+      launch_attention<T>(groups, max_group_rows, H, dh, qkv_, d, xkv_ + (size_t)l * 2 * d, ldkv,
+                          xkv_ + (size_t)l * 2 * d + d, ldkv, att_, d, gq, gk, gq, st_);
+      gemm(att_, d, w.co, rows, e);
+      launch_rmsnorm<T>(rows, d, h_, d, w.n3, xn_, d, st_);
+      if (c.moe_enabled) moe(w.moe, xn_, rows, h_);
+      else ffn(w.fc1, w.fc2, xn_, rows, h_);
+    }
+    (void)Tn;
+    // position_logits: no final norm (policy.cpp:290-295)
+    launch_convert<T>(rows, d, h_, d, xn_, d, st_);
+    gemm(xn_, d, heads_[step], rows, epi(logits_, c.codebook_size, true));
+  }
+
+  // ------------------------------------------------------------------------
+  // public flows
+  // ------------------------------------------------------------------------
+  void encode(float* z_out) override {
+    CUDA_CHECK(cudaSetDevice(dev_));
+    run_encode();
+    if (z_out) {
+      size_t n = static_cast<size_t>(sg_.U) * enc_seq_len(cfg_) * cfg_.d_model;
+      CUDA_CHECK(cudaMemcpyAsync(z_out, z_, n * 4, cudaMemcpyDeviceToHost, st_));
+      d2h_bytes += static_cast<int64_t>(n * 4);
+    }
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    CUDA_CHECK(cudaGetLastError());
+  }
+
+  void beam_search(int width, orx_beam_out* out) override {
+    CUDA_CHECK(cudaSetDevice(dev_));
+    const orx_config& c = cfg_;
+    require(width >= 1, "generation width must be >= 1");  // validate_request, generation.cpp:35
+    require(width <= maxW_, "beam width above the engine capacity");
+    const int U = sg_.U, V = c.codebook_size, L = c.n_code_layers, Tn = enc_seq_len(c);
+    run_encode();
+    prepare_decoder(U);
+    int cur = 0;
+    launch_beam_init(U, bs_[cur], st_);
+    int n_live = 1;
+    for (int step = 0; step < L; ++step) {
+      const int rows = U * n_live;
+      Seg gq;
+      gq.stride = n_live;
+      gq.fixed_len = n_live;
+      Seg gk;
+      gk.stride = Tn;
+      gk.fixed_len = Tn;
+      decode_step(step, rows, U, gq, gk, bs_[cur].codes, L, bs_[cur].anc, L, n_live);
+      const int ksel = std::min(width, V);
+      launch_row_topk(rows, V, ksel, logits_, bs_[cur].score, bs_[cur].lexrank, lse_, cand_, st_);
+      const int n_new = static_cast<int>(std::min<int64_t>(width, static_cast<int64_t>(n_live) * V));
+      launch_beam_merge(U, n_live, ksel, n_new, V, L, step, cand_, logits_, lse_, bs_[cur], bs_[cur ^ 1], st_);
+      cur ^= 1;
+      n_live = n_new;
+    }
+    last_n_live_ = n_live;
+    last_state_ = cur;
+    if (out) {
+      // pinned bounce buffer, then scatter into caller arrays (rows of width)
+      const size_t nc = static_cast<size_t>(U) * n_live * L, nl = static_cast<size_t>(U) * n_live;
+      size_t need = nc * 4 + nl * 8;
+      if (need > host_out_cap_) {
+        if (host_out_) cudaFreeHost(host_out_);
+        CUDA_CHECK(cudaMallocHost(&host_out_, need));
+        host_out_cap_ = need;
+      }
+      uint8_t* ho = static_cast<uint8_t*>(host_out_);
+      CUDA_CHECK(cudaMemcpyAsync(ho, bs_[cur].codes, nc * 4, cudaMemcpyDeviceToHost, st_));
+      CUDA_CHECK(cudaMemcpyAsync(ho + nc * 4, bs_[cur].score64, nl * 8, cudaMemcpyDeviceToHost, st_));
+      d2h_bytes += static_cast<int64_t>(need);
+      CUDA_CHECK(cudaStreamSynchronize(st_));
+      const int32_t* hc = reinterpret_cast<const int32_t*>(ho);
+      const double* hl = reinterpret_cast<const double*>(ho + nc * 4);
+      for (int u = 0; u < U; ++u) {
+        if (out->n_items) out->n_items[u] = n_live;
+        for (int b = 0; b < width; ++b) {
+          for (int j = 0; j < L; ++j)
+            out->codes[((size_t)u * width + b) * L + j] = b < n_live ? hc[((size_t)u * n_live + b) * L + j] : -1;
+          out->log_prob[(size_t)u * width + b] = b < n_live ? hl[(size_t)u * n_live + b] : 0.0;
+        }
+      }
+    }
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    CUDA_CHECK(cudaGetLastError());
+  }
+
+  // Teacher-forced logits. Queries are grouped by encoder row block; every
+  // query is its own row at every position (anc[r][p] = r).
+  void teacher_forced(int n_groups_users, int n, const int32_t* z_index, const int32_t* prefixes,
+                      const int32_t* prefix_len, float* logits) {
+    const orx_config& c = cfg_;
+    const int V = c.codebook_size, L = c.n_code_layers, Tn = enc_seq_len(c);
+    require(n >= 0 && n <= Rd_, "too many prefix queries for the engine capacity");
+    if (n == 0) return;
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return z_index[a] < z_index[b]; });
+    std::vector<int32_t> codes(static_cast<size_t>(n) * L, 0), anc(static_cast<size_t>(n) * L), gs, gl, gk;
+    int max_len = 0, max_group = 0;
+    for (int r = 0; r < n; ++r) {
+      const int q = order[r];
+      require(z_index[q] >= 0 && z_index[q] < n_groups_users, "query user index out of range");
+      require(prefix_len[q] >= 0 && prefix_len[q] < L, "no prediction head at this position");
+      max_len = std::max(max_len, prefix_len[q]);
+      for (int j = 0; j < L; ++j) {
+        anc[(size_t)r * L + j] = r;
+        if (j < prefix_len[q]) {
+          int code = prefixes[(size_t)q * L + j];
+          require(code >= 0 && code < V, "decoder token outside its layer vocabulary");
+          codes[(size_t)r * L + j] = code;
+        }
+      }
+      if (r == 0 || z_index[order[r - 1]] != z_index[q]) {
+        gs.push_back(r);
+        gl.push_back(0);
+        gk.push_back(z_index[q] * Tn);
+      }
+      ++gl.back();
+      max_group = std::max(max_group, gl.back());
+    }
+    const int G = static_cast<int>(gs.size());
+    CUDA_CHECK(cudaMemcpyAsync(tf_codes_, codes.data(), codes.size() * 4, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(tf_anc_, anc.data(), anc.size() * 4, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(grp_start_, gs.data(), G * 4, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(grp_len_, gl.data(), G * 4, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(grp_kstart_, gk.data(), G * 4, cudaMemcpyHostToDevice, st_));
+    Seg gq;
+    gq.start = grp_start_;
+    gq.len = grp_len_;
+    Seg gkseg;
+    gkseg.start = grp_kstart_;
+    gkseg.fixed_len = Tn;
+    std::vector<float> host(static_cast<size_t>(n) * V);
+    for (int step = 0; step <= max_len; ++step) {
+      decode_step(step, n, G, gq, gkseg, tf_codes_, L, tf_anc_, L, max_group);
+      CUDA_CHECK(cudaMemcpyAsync(host.data(), logits_, host.size() * 4, cudaMemcpyDeviceToHost, st_));
+      CUDA_CHECK(cudaStreamSynchronize(st_));
+      for (int r = 0; r < n; ++r)
+        if (prefix_len[order[r]] == step)
+          memcpy(logits + (size_t)order[r] * V, host.data() + (size_t)r * V, static_cast<size_t>(V) * 4);
+    }
+    CUDA_CHECK(cudaGetLastError());
+  }
+
+  void score_prefixes(int n, const int32_t* user, const int32_t* prefixes, const int32_t* prefix_len,
+                      float* logits) override {
+    CUDA_CHECK(cudaSetDevice(dev_));
+    run_encode();
+    prepare_decoder(sg_.U);
+    teacher_forced(sg_.U, n, user, prefixes, prefix_len, logits);
+  }
+
+  void next_logits(const float* z, int n_z, int n, const int32_t* z_index, const int32_t* prefixes,
+                   const int32_t* prefix_len, float* logits) override {
+    CUDA_CHECK(cudaSetDevice(dev_));
+    require(n_z >= 1 && n_z <= maxU_, "encoding count outside the engine capacity");
+    const size_t nz = static_cast<size_t>(n_z) * enc_seq_len(cfg_) * cfg_.d_model;
+    for (size_t i = 0; i < nz; ++i)
+      if (!std::isfinite(z[i])) throw RuntimeError("non-finite value produced on tape");
+    CUDA_CHECK(cudaMemcpyAsync(z_, z, nz * 4, cudaMemcpyHostToDevice, st_));
+    prepare_decoder(n_z);
+    teacher_forced(n_z, n, z_index, prefixes, prefix_len, logits);
+  }
+
+ private:
+  orx_config cfg_;
+  int dev_, maxU_, maxW_;
+  cudaStream_t st_ = nullptr;
+  Arena ar_;
+  // weights
+  const float *t_uid_, *t_gender_, *t_age_, *t_vid_, *t_aid_, *t_label_, *t_tag_, *t_ts_, *t_play_, *t_dur_;
+  const float *pad_s_, *pad_p_, *pad_l_, *pos_, *bos_;
+  std::vector<const float*> tokens_;
+  std::vector<Lin<T>> heads_;
+  Mlp p_static_, p_short_, p_pos_, p_life_;
+  const T* queries_ = nullptr;
+  std::vector<QBlock> qblocks_;
+  std::vector<EncL> enc_;
+  std::vector<DecL> dec_;
+  Lin<T> xkv_w_;
+  // activations
+  int Fp_ = 0, Sp_ = 0;
+  int64_t Rd_ = 0, S_ = 0;
+  int max_tiles_ = 0;
+  T *feat_, *hid_, *keys_, *kvl_, *xn_, *qkv_, *att_, *ffh_, *qproj_, *qcur_, *zt_, *xkv_;
+  float *z_, *qo_, *h_, *logits_, *lse_;
+  std::vector<T*> cache_;
+  T** cache_ptrs_ = nullptr;
+  uint64_t* cand_ = nullptr;
+  BeamState bs_[2];
+  int32_t *tf_anc_, *tf_codes_, *grp_start_, *grp_len_, *grp_kstart_;
+  int32_t *sel_ = nullptr, *slot_ = nullptr, *counts_ = nullptr, *cursor_ = nullptr, *tile_expert_ = nullptr,
+          *n_mtiles_ = nullptr;
+  float *wts_ = nullptr, *row_scale_ = nullptr, *yg_ = nullptr, *ga_ = nullptr, *gb_ = nullptr;
+  T *xg_ = nullptr, *hg_ = nullptr;
+  // staging
+  void* host_stage_ = nullptr;
+  uint8_t* dev_stage_ = nullptr;
+  size_t stage_cap_ = 0;
+  bool staged_ = false;
+  void* host_out_ = nullptr;
+  size_t host_out_cap_ = 0;
+  int last_n_live_ = 0, last_state_ = 0;
+};
+
+std::unique_ptr<Engine> Engine::create(const HostWeights& w, int device, int precision, int max_users,
+                                       int max_width) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    throw RuntimeError("no CUDA device available (the engine has no CPU fallback)");
+  }
+  require(device >= 0 && device < n, "device index out of range");
+  if (precision == ORX_PRECISION_FP32) return std::make_unique<EngineT<float>>(w, device, max_users, max_width);
+  if (precision == ORX_PRECISION_BF16) return std::make_unique<EngineT<__nv_bfloat16>>(w, device, max_users, max_width);
+  throw InvalidArgument("unknown precision");
+}
+
+}  // namespace orx

@@ -1,0 +1,31 @@
+// One-GPU inference engine for the OneRec hot path (encode + beam search).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "../../include/orx.h"
+#include "model.hpp"
+
+namespace orx {
+
+class Engine {
+ public:
+  virtual ~Engine() = default;
+  static std::unique_ptr<Engine> create(const HostWeights& w, int device, int precision, int max_users,
+                                        int max_width);
+  virtual void stage_batch(const orx_user_batch& b) = 0;
+  virtual void encode(float* z_out) = 0;
+  virtual void beam_search(int width, orx_beam_out* out) = 0;
+  virtual void next_logits(const float* z, int n_z, int n, const int32_t* z_index, const int32_t* prefixes,
+                           const int32_t* prefix_len, float* logits) = 0;
+  virtual void score_prefixes(int n, const int32_t* user, const int32_t* prefixes, const int32_t* prefix_len,
+                              float* logits) = 0;
+  virtual void* stream() = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0;
+};
+
+void validate_batch(const orx_config& cfg, const orx_user_batch& b);
+long long launch_counter_value();
+
+}  // namespace orx

@@ -379,6 +379,8 @@ long long& launch_counter() {
   return c;
 }
 
+long long launch_counter_value() { return launch_counter(); }
+
 void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int K, const Epi& epi,
                const Grouped* grp, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return;

@@ -14,6 +14,8 @@
 
 namespace orx {
 
+enum Act { ACT_NONE = 0, ACT_LEAKY = 1, ACT_SILU = 2 };
+
 struct Epi {
   const float* bias = nullptr;       // [N] (or [N/2] for swiglu: not used)
   const float* row_scale = nullptr;  // [M] per-row multiplier

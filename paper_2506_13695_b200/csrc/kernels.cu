@@ -1,0 +1,391 @@
+#include <cfloat>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace orx {
+
+namespace {
+
+__device__ __forceinline__ int hashed(int64_t id, int vocab) {  // policy.cpp:14-17
+  int64_t m = id % vocab;
+  return static_cast<int>(m < 0 ? m + vocab : m);
+}
+
+// Feature row of one record (policy.cpp:139-198):
+// [vid row | aid row | tag | ts | playtime | duration | label multi-hot . emb]
+template <class T>
+__global__ void features_kernel(RecordsDev r, FeatureTables t, T* __restrict__ out, int ldo) {
+  const int d = t.d, ad = t.aid_dim, mn = t.minor;
+  const int F = t.vid_only ? d : d + ad + 5 * mn;
+  for (int row = blockIdx.x; row < r.n; row += gridDim.x) {
+    const int vid = t.use_sid ? 0 : hashed(r.vid[row], t.vid_vocab);
+    const int aid = hashed(r.aid[row], t.aid_vocab);
+    const float sc[4] = {r.tag[row], r.ts[row], r.play[row], r.dur[row]};
+    const uint32_t lab = r.labels[row];
+    T* o = out + (size_t)row * ldo;
+    for (int c = threadIdx.x; c < ldo; c += blockDim.x) {
+      float v = 0.f;
+      if (c < d) {
+        if (t.use_sid) {
+          for (int l = 0; l < t.n_code_layers; ++l) v += t.tokens[l][(size_t)r.sid[(size_t)row * t.n_code_layers + l] * d + c];
+        } else {
+          v = t.vid[(size_t)vid * d + c];
+        }
+      } else if (c < F) {
+        int cc = c - d;
+        if (cc < ad) {
+          v = t.aid[(size_t)aid * ad + cc];
+        } else {
+          cc -= ad;
+          int f = cc / mn, j = cc % mn;
+          if (f < 4) {
+            const float* p = f == 0 ? t.tag : f == 1 ? t.ts : f == 2 ? t.play : t.dur;
+            v = sc[f] * p[j] + p[mn + j];
+          } else {
+            for (int b = 0; b < t.n_flags; ++b)
+              if ((lab >> b) & 1u) v += t.label[b * mn + j];
+          }
+        }
+      }
+      o[c] = from_f<T>(v);
+    }
+  }
+}
+
+template <class T>
+__global__ void static_features_kernel(int U, const int32_t* uid, const int32_t* gender, const int32_t* age,
+                                       const float* ue, const float* ge, const float* ae, int sd, int uv, int gv,
+                                       int av, T* out, int ldo) {
+  int u = blockIdx.x;
+  if (u >= U) return;
+  int iu = hashed(uid[u], uv), ig = hashed(gender[u], gv), ia = hashed(age[u], av);
+  for (int c = threadIdx.x; c < ldo; c += blockDim.x) {
+    float v = 0.f;
+    if (c < sd) v = ue[(size_t)iu * sd + c];
+    else if (c < 2 * sd) v = ge[(size_t)ig * sd + c - sd];
+    else if (c < 3 * sd) v = ae[(size_t)ia * sd + c - 2 * sd];
+    out[(size_t)u * ldo + c] = from_f<T>(v);
+  }
+}
+
+__global__ void z_init_kernel(int U, int T, int d, const float* pos, const float* pad_s, const float* pad_p,
+                              const int32_t* n_s, const int32_t* n_p, int Ls, int Lp, float* z) {
+  size_t row = blockIdx.x;
+  int u = static_cast<int>(row / T), t = static_cast<int>(row % T);
+  const float* pad = nullptr;
+  if (t >= 1 && t < 1 + Ls) {
+    if (t - 1 < Ls - n_s[u]) pad = pad_s;
+  } else if (t >= 1 + Ls && t < 1 + Ls + Lp) {
+    if (t - 1 - Ls < Lp - n_p[u]) pad = pad_p;
+  }
+  for (int c = threadIdx.x; c < d; c += blockDim.x) z[row * d + c] = pos[(size_t)t * d + c] + (pad ? pad[c] : 0.f);
+}
+
+// RMSNorm, warp per row (tape.cpp:462-503, eps 1e-6 nn.hpp:36).
+template <class T>
+__global__ void rmsnorm_kernel(int rows, int d, const float* __restrict__ x, int ldx, const float* __restrict__ g,
+                               T* __restrict__ out, int ldo) {
+  int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const float* xr = x + (size_t)row * ldx;
+  float ss = 0.f;
+  for (int c = lane; c < d; c += 32) ss += xr[c] * xr[c];
+  ss = warp_sum(ss);
+  float r = rsqrtf(ss / d + 1e-6f);
+  T* o = out + (size_t)row * ldo;
+  for (int c = lane; c < d; c += 32) o[c] = from_f<T>(xr[c] * r * g[c]);
+}
+
+template <class T>
+__global__ void convert_kernel(int rows, int cols, const float* x, int ldx, T* out, int ldo) {
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  size_t n = (size_t)rows * cols;
+  for (; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    size_t r = i / cols, c = i % cols;
+    out[r * ldo + c] = from_f<T>(x[r * ldx + c]);
+  }
+}
+
+template <class T>
+__global__ void fill_rows_kernel(int rows, int cols, const float* src, T* out, int ldo, const int32_t* idx) {
+  int r = blockIdx.x;
+  if (r >= rows) return;
+  int orow = idx ? idx[r] : r;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) out[(size_t)orow * ldo + c] = from_f<T>(src[c]);
+}
+
+__global__ void dec_embed_kernel(int rows, int d, const float* table, const int32_t* code, int code_stride,
+                                 float* h) {
+  int r = blockIdx.x;
+  if (r >= rows) return;
+  size_t src = code ? (size_t)code[(size_t)r * code_stride] * d : 0;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) h[(size_t)r * d + c] = table[src + c];
+}
+
+// Warp per (row, head): keys are positions 0..step; position p < step comes
+// from the cache of that position at row anc[r][p], position `step` is the
+// row's own K/V (also appended to cache[step]).
+template <class T>
+__global__ void dec_self_attn_kernel(int rows, int d, int heads, int step, int layer, int L, const T* __restrict__ qkv,
+                                     T* const* __restrict__ cache, const int32_t* __restrict__ anc, int anc_stride,
+                                     T* __restrict__ out) {
+  int gw = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  int r = gw / heads, h = gw % heads;
+  if (r >= rows) return;
+  const int dh = d / heads;
+  const T* q = qkv + (size_t)r * 3 * d + h * dh;
+  const T* kown = q + d;
+  const T* vown = q + 2 * d;
+  T* cown = cache[step] + ((size_t)r * L + layer) * 2 * d;
+  for (int c = lane; c < dh; c += 32) {
+    cown[h * dh + c] = kown[c];
+    cown[d + h * dh + c] = vown[c];
+  }
+  const float scale = rsqrtf(static_cast<float>(dh));
+  float sc[8];
+  float mx = -FLT_MAX;
+  for (int p = 0; p <= step; ++p) {
+    const T* k = p == step ? kown : cache[p] + ((size_t)anc[(size_t)r * anc_stride + p] * L + layer) * 2 * d + h * dh;
+    float s = 0.f;
+    for (int c = lane; c < dh; c += 32) s += to_f(q[c]) * to_f(k[c]);
+    s = warp_sum(s) * scale;
+    sc[p] = s;
+    mx = fmaxf(mx, s);
+  }
+  float den = 0.f;
+  for (int p = 0; p <= step; ++p) {
+    sc[p] = __expf(sc[p] - mx);
+    den += sc[p];
+  }
+  for (int c = lane; c < dh; c += 32) {
+    float acc = 0.f;
+    for (int p = 0; p <= step; ++p) {
+      const T* v = p == step ? vown : cache[p] + ((size_t)anc[(size_t)r * anc_stride + p] * L + layer) * 2 * d + d + h * dh;
+      acc += sc[p] * to_f(v[c]);
+    }
+    out[(size_t)r * d + h * dh + c] = from_f<T>(acc / den);
+  }
+}
+
+// Gate scores, top-k (stable: score+bias desc, ties -> lower id), selected ids
+// ascending, softmax over selected raw scores (nn.cpp:121-147). Warp per row,
+// lane e owns expert e (E <= 32).
+template <class T>
+__global__ void moe_route_kernel(int rows, int d, int E, int k, const T* __restrict__ x, int ldx,
+                                 const float* __restrict__ gate_t, const float* __restrict__ bias,
+                                 int32_t* __restrict__ sel, float* __restrict__ wts, int32_t* __restrict__ counts) {
+  int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  const T* xr = x + (size_t)r * ldx;
+  float my = -FLT_MAX;  // lane e's raw score
+  for (int e = 0; e < E; ++e) {
+    const float* g = gate_t + (size_t)e * d;
+    float s = 0.f;
+    for (int c = lane; c < d; c += 32) s += to_f(xr[c]) * g[c];
+    s = warp_sum(s);
+    if (lane == e) my = s;
+  }
+  float key = lane < E ? my + bias[lane] : -FLT_MAX;
+  bool taken = false;
+  uint32_t chosen = 0;
+  for (int j = 0; j < k; ++j) {
+    float v = taken ? -FLT_MAX : key;
+    int idx = lane < E && !taken ? lane : 1 << 30;
+    for (int o = 16; o > 0; o >>= 1) {
+      float v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (v2 > v || (v2 == v && i2 < idx)) {
+        v = v2;
+        idx = i2;
+      }
+    }
+    if (lane == idx) taken = true;
+    chosen |= 1u << idx;
+  }
+  // selected ids ascending; weights = softmax over raw scores
+  float mx = -FLT_MAX;
+  for (int e = 0; e < E; ++e)
+    if (chosen >> e & 1u) mx = fmaxf(mx, __shfl_sync(0xffffffffu, my, e));
+  float den = 0.f;
+  for (int e = 0; e < E; ++e)
+    if (chosen >> e & 1u) den += __expf(__shfl_sync(0xffffffffu, my, e) - mx);
+  if (lane == 0) {
+    int j = 0;
+    for (int e = 0; e < E; ++e)
+      if (chosen >> e & 1u) {
+        sel[(size_t)r * k + j] = e;
+        wts[(size_t)r * k + j] = 0.f;  // filled below
+        ++j;
+      }
+  }
+  __syncwarp();
+  if (lane < E && (chosen >> lane & 1u)) {
+    int j = __popc(chosen & ((1u << lane) - 1u));
+    wts[(size_t)r * k + j] = __expf(my - mx) / den;
+    atomicAdd(&counts[lane], 1);
+  }
+}
+
+// Segment offsets padded to the 128-row GEMM tile; tile -> expert table.
+__global__ void moe_plan_kernel(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
+                                int32_t* n_mtiles) {
+  if (threadIdx.x != 0) return;
+  int off = 0, tile = 0;
+  for (int e = 0; e < E; ++e) {
+    cursor[e] = off;
+    int nt = (counts[e] + 127) / 128;
+    for (int i = 0; i < nt && tile < max_tiles; ++i) tile_expert[tile++] = e;
+    off += nt * 128;
+  }
+  *n_mtiles = tile;
+  for (int i = tile; i < max_tiles; ++i) tile_expert[i] = -1;
+}
+
+template <class T>
+__global__ void moe_scatter_kernel(int rows, int k, int d, const T* __restrict__ x, int ldx,
+                                   const int32_t* __restrict__ sel, const float* __restrict__ wts,
+                                   int32_t* __restrict__ cursor, int32_t* __restrict__ slot, T* __restrict__ xg,
+                                   float* __restrict__ row_scale) {
+  int gw = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (gw >= rows * k) return;
+  int r = gw / k;
+  int e = sel[gw];
+  int s = 0;
+  if (lane == 0) s = atomicAdd(&cursor[e], 1);
+  s = __shfl_sync(0xffffffffu, s, 0);
+  if (lane == 0) {
+    slot[gw] = s;
+    row_scale[s] = wts[gw];
+  }
+  const T* src = x + (size_t)r * ldx;
+  T* dst = xg + (size_t)s * d;
+  if (sizeof(T) == 2 && d % 8 == 0) {
+    for (int c = lane * 8; c < d; c += 256) *reinterpret_cast<uint4*>(dst + c) = *reinterpret_cast<const uint4*>(src + c);
+  } else {
+    for (int c = lane; c < d; c += 32) dst[c] = src[c];
+  }
+}
+
+// h[r] += sum_j (ascending expert) y[slot[r][j]]; y already carries the gate weight.
+__global__ void moe_combine_kernel(int rows, int k, int d, const float* __restrict__ yg,
+                                   const int32_t* __restrict__ slot, float* __restrict__ h, int ldh) {
+  int r = blockIdx.x;
+  if (r >= rows) return;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j < k; ++j) acc += yg[(size_t)slot[(size_t)r * k + j] * d + c];
+    h[(size_t)r * ldh + c] += acc;
+  }
+}
+
+__global__ void swiglu_mul_kernel(long long n, const float* a, const float* b, float* out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float x = a[i];
+    out[i] = x / (1.f + __expf(-x)) * b[i];
+  }
+}
+
+inline int grid_for(long long n, int block, int cap = 148 * 32) {
+  long long g = (n + block - 1) / block;
+  return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace
+
+#define ORX_LAUNCH(...)      \
+  do {                       \
+    __VA_ARGS__;             \
+    ++launch_counter();      \
+  } while (0)
+
+template <class T>
+void launch_features(const RecordsDev& r, const FeatureTables& t, T* out, int ldo, cudaStream_t s) {
+  if (r.n <= 0) return;
+  ORX_LAUNCH(features_kernel<T><<<grid_for(r.n, 1, 148 * 16), 256, 0, s>>>(r, t, out, ldo));
+}
+template <class T>
+void launch_static_features(int U, const int32_t* uid, const int32_t* gender, const int32_t* age, const float* ue,
+                            const float* ge, const float* ae, int sd, int uv, int gv, int av, T* out, int ldo,
+                            cudaStream_t s) {
+  ORX_LAUNCH(static_features_kernel<T><<<U, 128, 0, s>>>(U, uid, gender, age, ue, ge, ae, sd, uv, gv, av, out, ldo));
+}
+void launch_z_init(int U, int T, int d, const float* pos, const float* pad_s, const float* pad_p, const int32_t* n_s,
+                   const int32_t* n_p, int Ls, int Lp, float* z, cudaStream_t s) {
+  ORX_LAUNCH(z_init_kernel<<<U * T, 256, 0, s>>>(U, T, d, pos, pad_s, pad_p, n_s, n_p, Ls, Lp, z));
+}
+template <class T>
+void launch_rmsnorm(int rows, int d, const float* x, int ldx, const float* gain, T* out, int ldo, cudaStream_t s) {
+  if (rows <= 0) return;
+  ORX_LAUNCH(rmsnorm_kernel<T><<<(rows + 7) / 8, 256, 0, s>>>(rows, d, x, ldx, gain, out, ldo));
+}
+template <class T>
+void launch_convert(int rows, int cols, const float* x, int ldx, T* out, int ldo, cudaStream_t s) {
+  if (rows <= 0) return;
+  ORX_LAUNCH(convert_kernel<T><<<grid_for((long long)rows * cols, 256), 256, 0, s>>>(rows, cols, x, ldx, out, ldo));
+}
+template <class T>
+void launch_fill_rows(int rows, int cols, const float* src, T* out, int ldo, const int32_t* idx, cudaStream_t s) {
+  if (rows <= 0) return;
+  ORX_LAUNCH(fill_rows_kernel<T><<<rows, 128, 0, s>>>(rows, cols, src, out, ldo, idx));
+}
+void launch_dec_embed(int rows, int d, const float* table, const int32_t* code, int code_stride, float* h,
+                      cudaStream_t s) {
+  if (rows <= 0) return;
+  ORX_LAUNCH(dec_embed_kernel<<<rows, 256, 0, s>>>(rows, d, table, code, code_stride, h));
+}
+template <class T>
+void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L, const T* qkv, T* const* cache,
+                          const int32_t* anc, int anc_stride, T* out, cudaStream_t s) {
+  if (rows <= 0) return;
+  long long warps = (long long)rows * heads;
+  ORX_LAUNCH(dec_self_attn_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(
+      rows, d, heads, step, layer, L, qkv, cache, anc, anc_stride, out));
+}
+template <class T>
+void launch_moe_route(int rows, int d, int E, int k, const T* x, int ldx, const float* gate_t, const float* bias,
+                      int32_t* sel, float* wts, int32_t* counts, cudaStream_t s) {
+  if (rows <= 0) return;
+  ORX_LAUNCH(moe_route_kernel<T><<<(rows + 7) / 8, 256, 0, s>>>(rows, d, E, k, x, ldx, gate_t, bias, sel, wts, counts));
+}
+void launch_moe_plan(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
+                     int32_t* n_mtiles, cudaStream_t s) {
+  ORX_LAUNCH(moe_plan_kernel<<<1, 32, 0, s>>>(E, counts, cursor, tile_expert, max_tiles, n_mtiles));
+}
+template <class T>
+void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
+                        int32_t* cursor, int32_t* slot, T* xg, float* row_scale, cudaStream_t s) {
+  if (rows <= 0) return;
+  long long warps = (long long)rows * k;
+  ORX_LAUNCH(moe_scatter_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(rows, k, d, x, ldx, sel, wts,
+                                                                                      cursor, slot, xg, row_scale));
+}
+void launch_moe_combine(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
+                        cudaStream_t s) {
+  if (rows <= 0) return;
+  ORX_LAUNCH(moe_combine_kernel<<<rows, 256, 0, s>>>(rows, k, d, yg, slot, h, ldh));
+}
+void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, cudaStream_t s) {
+  if (n <= 0) return;
+  ORX_LAUNCH(swiglu_mul_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, a, b, out));
+}
+
+#define INST(T)                                                                                                   \
+  template void launch_features<T>(const RecordsDev&, const FeatureTables&, T*, int, cudaStream_t);              \
+  template void launch_static_features<T>(int, const int32_t*, const int32_t*, const int32_t*, const float*,     \
+                                          const float*, const float*, int, int, int, int, T*, int, cudaStream_t); \
+  template void launch_rmsnorm<T>(int, int, const float*, int, const float*, T*, int, cudaStream_t);              \
+  template void launch_convert<T>(int, int, const float*, int, T*, int, cudaStream_t);                           \
+  template void launch_fill_rows<T>(int, int, const float*, T*, int, const int32_t*, cudaStream_t);              \
+  template void launch_dec_self_attn<T>(int, int, int, int, int, int, const T*, T* const*, const int32_t*, int,   \
+                                        T*, cudaStream_t);                                                       \
+  template void launch_moe_route<T>(int, int, int, int, const T*, int, const float*, const float*, int32_t*,      \
+                                    float*, int32_t*, cudaStream_t);                                             \
+  template void launch_moe_scatter<T>(int, int, int, const T*, int, const int32_t*, const float*, int32_t*,       \
+                                      int32_t*, T*, float*, cudaStream_t);
+INST(float)
+INST(__nv_bfloat16)
+
+}  // namespace orx

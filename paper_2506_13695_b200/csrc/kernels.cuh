@@ -1,0 +1,75 @@
+// Non-GEMM kernels of the hot path (host launchers). All launches go on the
+// caller's stream and bump launch_counter().
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace orx {
+
+struct RecordsDev {  // one pathway, all users, packed (device pointers)
+  int n = 0;
+  const int64_t* vid = nullptr;
+  const int32_t* aid = nullptr;
+  const float* tag = nullptr;
+  const float* ts = nullptr;
+  const float* play = nullptr;
+  const float* dur = nullptr;
+  const uint32_t* labels = nullptr;
+  const int32_t* sid = nullptr;  // [n * n_code_layers] or null
+};
+
+struct FeatureTables {  // fp32 embedding tables (policy.cpp:139-198)
+  const float* vid;       // [vid_vocab][d]
+  const float* aid;       // [aid_vocab][aid_dim]
+  const float* tag;       // [2][minor]
+  const float* ts;
+  const float* play;
+  const float* dur;
+  const float* label;     // [n_flags][minor]
+  const float* tokens[8]; // sid history: per code layer [V][d]
+  int d, aid_dim, minor, vid_vocab, aid_vocab, n_flags, n_code_layers, use_sid, vid_only;
+};
+
+template <class T>
+void launch_features(const RecordsDev& r, const FeatureTables& t, T* out, int ldo, cudaStream_t s);
+template <class T>
+void launch_static_features(int U, const int32_t* uid, const int32_t* gender, const int32_t* age,
+                            const float* uid_emb, const float* gender_emb, const float* age_emb, int sdim,
+                            int uid_vocab, int gender_vocab, int age_vocab, T* out, int ldo, cudaStream_t s);
+// z[u*T + t] = pos[t] (+ pad row where the pathway is left-padded).
+void launch_z_init(int U, int T, int d, const float* pos, const float* pad_short, const float* pad_pos,
+                   const int32_t* n_short, const int32_t* n_pos, int Ls, int Lp, float* z, cudaStream_t s);
+template <class T>
+void launch_rmsnorm(int rows, int d, const float* x, int ldx, const float* gain, T* out, int ldo, cudaStream_t s);
+template <class T>
+void launch_convert(int rows, int cols, const float* x, int ldx, T* out, int ldo, cudaStream_t s);
+// Copy rows (src_row = map ? map[r] : r) of a fp32 matrix, e.g. pad.lifelong keys.
+template <class T>
+void launch_fill_rows(int rows, int cols, const float* src_row, T* out, int ldo, const int32_t* row_idx,
+                      cudaStream_t s);
+
+// Decoder: h[r] = step == 0 ? bos : tokens[code[r]]
+void launch_dec_embed(int rows, int d, const float* table, const int32_t* code, int code_stride, float* h,
+                      cudaStream_t s);
+// Decoder causal self-attention over cached positions (policy.cpp:282-283).
+// qkv: [rows][3d]; cache[p]: [rows_p][L][2][d]; anc: [rows][anc_stride] row index of position p < step.
+template <class T>
+void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int n_layers, const T* qkv,
+                          T* const* cache, const int32_t* anc, int anc_stride, T* out, cudaStream_t s);
+
+// MoE (nn.cpp:117-172)
+template <class T>
+void launch_moe_route(int rows, int d, int E, int k, const T* x, int ldx, const float* gate_t, const float* bias,
+                      int32_t* sel, float* wts, int32_t* counts, cudaStream_t s);
+void launch_moe_plan(int E, const int32_t* counts, int32_t* seg_cursor, int32_t* tile_expert, int max_tiles,
+                     int32_t* n_mtiles, cudaStream_t s);
+template <class T>
+void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
+                        int32_t* seg_cursor, int32_t* slot, T* xg, float* row_scale, cudaStream_t s);
+void launch_moe_combine(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
+                        cudaStream_t s);
+void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, cudaStream_t s);
+
+}  // namespace orx

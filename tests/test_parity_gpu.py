@@ -1,0 +1,90 @@
+"""GPU parity against the reference oracle (oracle/_ref/ref_driver).
+
+fp32 mode: logits within 1e-3 relative (||.||_inf per (user, prefix) row) and
+identical beams up to near-ties; z_enc checked the same way.
+bf16 mode: deviation reported and bounded loosely.
+"""
+import numpy as np
+import pytest
+
+from parity_util import beams_match, prefixes_of, ref_dump, rel_inf
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_RTOL = 1e-3  # north_star: fp32 logits within 1e-3 relative error
+
+
+def _model(preset, precision, max_users=4, max_width=128, **over):
+    import paper_2506_13695_b200 as P
+    cfg = P.PolicyConfig.preset(preset, **over)
+    return P, P.PolicyModel(cfg, precision=precision, max_users=max_users, max_width=max_width)
+
+
+def _check_user(P, model, batch, refs, width, rtol_z, rtol_logits, check_beams=True):
+    z = model.encode_batch(batch)
+    report = []
+    for u, ref in enumerate(refs):
+        ez = rel_inf(z[u], ref["z"])
+        assert ez <= rtol_z, f"user {u}: z_enc rel err {ez}"
+        pres = prefixes_of(ref["prefixes"])
+        lg = model.score_prefixes(batch, [u] * len(pres), pres)
+        errs = [rel_inf(lg[i], ref["logits"][i]) for i in range(len(pres))]
+        assert max(errs) <= rtol_logits, f"user {u}: logits rel err {max(errs)} (per prefix {errs})"
+        # decode on the reference's own z as well (next_logits_eval boundary)
+        lg2 = model.next_logits_batch(ref["z"].astype(np.float32), [0] * len(pres), pres)
+        errs2 = [rel_inf(lg2[i], ref["logits"][i]) for i in range(len(pres))]
+        assert max(errs2) <= rtol_logits, f"user {u}: next_logits rel err {max(errs2)}"
+        report.append((ez, max(errs), max(errs2)))
+    if check_beams:
+        codes, logp, n_items = model.beam_search_arrays(batch, width)
+        for u, ref in enumerate(refs):
+            W = len(ref["beam_codes"])
+            assert n_items[u] == W
+            ok, exact, msg = beams_match(codes[u, :W], logp[u, :W], ref["beam_codes"], ref["beam_logp"])
+            assert ok, f"user {u}: {msg} (exact-rank {exact}/{W})"
+            assert np.allclose(logp[u, :W], ref["beam_logp"], rtol=1e-3, atol=1e-3) or exact < W
+    return report
+
+
+@pytest.mark.parametrize("width", [16, 512])
+def test_tiny_fp32_exhaustive(width):
+    """tiny config (test_policy.cpp:14-32); W=512 >= 8^3 reproduces the full
+    enumeration (test_generation.cpp:108-126)."""
+    P, model = _model("tiny", "fp32", max_users=3, max_width=512)
+    _, refs = ref_dump("tiny", 3, width)
+    batch = P.SynthBatch(1, 0, 3, 4, 4, 8)
+    _check_user(P, model, batch, refs, width, 1e-5, 1e-5)
+
+
+def test_tiny_ragged_fp32():
+    """Ragged / empty pathways: left padding and the empty-lifelong pad key."""
+    P, model = _model("tiny", "fp32", max_users=2, max_width=16)
+    for lens in [(0, 0, 0), (2, 1, 3), (4, 0, 1)]:
+        _, refs = ref_dump("tiny", 2, 16, lens=lens)
+        batch = P.SynthBatch(1, 0, 2, *lens)
+        _check_user(P, model, batch, refs, 16, 1e-5, 1e-5)
+
+
+@pytest.mark.parametrize("width", [8, 128])
+def test_0015b_fp32(width):
+    P, model = _model("0.015B", "fp32", max_users=2, max_width=128)
+    _, refs = ref_dump("0.015B", 2, width)
+    batch = P.SynthBatch(1, 0, 2)
+    rep = _check_user(P, model, batch, refs, width, 1e-4, LOGIT_RTOL)
+    print("0.015B fp32 W=%d (z, logits, next_logits) rel err:" % width, rep)
+
+
+def test_0015b_bf16_deviation():
+    P, model = _model("0.015B", "bf16", max_users=2, max_width=128)
+    _, refs = ref_dump("0.015B", 2, 128)
+    batch = P.SynthBatch(1, 0, 2)
+    z = model.encode_batch(batch)
+    codes, logp, _ = model.beam_search_arrays(batch, 128)
+    for u, ref in enumerate(refs):
+        ez = rel_inf(z[u], ref["z"])
+        pres = prefixes_of(ref["prefixes"])
+        lg = model.score_prefixes(batch, [u] * len(pres), pres)
+        el = max(rel_inf(lg[i], ref["logits"][i]) for i in range(len(pres)))
+        overlap = len({tuple(c) for c in codes[u]} & {tuple(c) for c in ref["beam_codes"]})
+        print(f"0.015B bf16 user {u}: z rel {ez:.3e} logits rel {el:.3e} beam overlap {overlap}/128")
+        assert ez < 5e-2 and el < 5e-2 and overlap >= 64

@@ -1,0 +1,360 @@
+#!/usr/bin/env python3
+"""Benchmark of the OneRec inference hot path on B200 (one rank per GPU).
+
+A step = encode + depth-3 beam search (width W) for one batch of synthetic
+users per GPU (BASELINE.json config 3: OneRec-0.935B MoE, 1024 users over 8
+GPUs -> 128 users per GPU; weak scaling). Default N=1 runs the same 128-user
+per-GPU batch.
+
+  value    users/s over all ranks, inputs already resident in HBM
+           (orx_engine_stage_batch once, then orx_beam_search_staged per step),
+           CUDA events on the engine stream, max over ranks.
+  e2e      same metric through the public C-ABI call orx_beam_search with
+           host buffers: H2D of the step's packed user records and D2H of the
+           beams inside the timed region.
+  roofline the tcgen05 GEMM kernel class (dense + grouped MoE), algorithmic
+           FLOPs / CUDA-event time per launch, from one instrumented step.
+  cpu_baseline  the reference C++ core (oracle/_ref/ref_driver) on this
+           host's cores, bounded sample (rank 0, N=1 only).
+
+--impl reference times the reference's own CPU implementation instead.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "users/sec (beam-searched rec lists) per box at 1/2/4/8 B200; inference MFU"
+
+PROF_NAMES = ["gemm_dense", "gemm_moe", "attention", "dec_self_attn", "moe_route", "beam_topk_merge", "other"]
+
+
+def flops_per_user(cfg, width, lens):
+    """Algorithmic FLOPs per user, KV-cached minimum."""
+    d, V, T = cfg.d_model, cfg.codebook_size, cfg.enc_seq_len()
+    ns, npos, nl = lens
+    nl_keys = max(nl, 1)
+    F = d + d // 2 + 5 * (d // 8)
+    ffn = lambda r: 4.0 * r * d * cfg.ffn_hidden  # noqa: E731
+    moe = lambda r: 2.0 * r * d * cfg.n_experts + cfg.experts_active * 6.0 * r * d * cfg.expert_hidden()  # noqa: E731
+    enc = 2.0 * (3 * (d // 16)) * d + 2.0 * d * d  # static MLP
+    enc += 2.0 * (ns + npos + nl) * (F * d + d * d)  # pathway MLPs
+    Nq = cfg.n_queries
+    enc += cfg.lifelong_blocks * (2.0 * Nq * d * d * 2 + 4.0 * nl_keys * d * d + 4.0 * Nq * nl_keys * d + ffn(Nq))
+    enc_moe = cfg.moe_enabled and cfg.moe_location == "enc_and_dec"
+    enc += cfg.enc_layers() * (8.0 * T * d * d + 4.0 * T * T * d + (moe(T) if enc_moe else ffn(T)))
+    Ld = cfg.dec_layers()
+    dec = Ld * 4.0 * T * d * d
+    rows, live = [], 1
+    for p in range(cfg.n_code_layers):
+        rows.append((p, live))
+        live = min(width, live * V)
+    for p, r in rows:
+        per = Ld * (8.0 * d * d + 4.0 * (p + 1) * d + 4.0 * d * d + 4.0 * T * d +
+                    (moe(1) if cfg.moe_enabled else ffn(1))) + 2.0 * d * V
+        dec += r * per
+    return enc + dec, enc
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9 or not parts[0].isdigit() or int(parts[0]) != self.gpu:
+                    continue
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+def safe_procs(cfg_preset: str) -> int:
+    """Worker processes for the reference CPU path, bounded by cores and RAM."""
+    cores = os.cpu_count() or 1
+    try:
+        with open("/proc/meminfo") as f:
+            avail_kb = next(int(l.split()[1]) for l in f if l.startswith("MemAvailable"))
+    except Exception:
+        avail_kb = 16 << 20
+    model_gb = {"0.015B": 0.1, "0.121B": 1.4, "0.935B": 7.9, "2.633B": 42.0}.get(cfg_preset, 8.0)
+    per_worker_gb = {"0.015B": 0.2, "0.121B": 1.0, "0.935B": 1.2, "2.633B": 3.0}.get(cfg_preset, 1.5)
+    budget = 0.5 * avail_kb / (1 << 20) - model_gb
+    by_mem = max(1, int(budget / per_worker_gb))
+    return max(1, min(cores, by_mem, 64))
+
+
+def run_reference_sample(preset: str, width: int, lens, procs: int, calls: int, user_begin: int = 0):
+    """Reference core on `procs` worker processes: one user each (encode +
+    `calls` decoder calls, extrapolated to the 1 + 2W scorer calls of a beam;
+    calls < 0 runs the whole beam_search)."""
+    cmd = [REF_DRIVER, "bench", "--preset", preset, "--n-users", str(procs), "--procs", str(procs),
+           "--width", str(width), "--calls", str(calls), "--user-begin", str(user_begin),
+           "--lens", ",".join(str(x) for x in lens)]
+    out = subprocess.run(cmd, check=True, capture_output=True, text=True, timeout=1800)
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline_block(r, preset, width, kind="reference"):
+    sample = (f"{r['procs']} worker processes x 1 user of {preset}: encode_eval measured "
+              f"({r['t_encode_s']:.3g} s/user); " +
+              (f"full beam_search W={width} measured ({r['t_beam_s']:.3g} s)" if r["beam_measured"] else
+               f"{r['calls']} next_logits_eval calls measured ({r['t_call_s']:.3g} s each), beam of "
+               f"1+2W={1 + 2 * width} calls extrapolated"))
+    return {"value": r["users_per_s"], "unit": "users/s", "cores": r["procs"], "kind": kind, "sample": sample}
+
+
+def reference_arm(args, cfg, lens):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    procs = safe_procs(args.config)
+    calls = -1 if args.config in ("tiny", "0.015B") and args.width <= 32 else max(1, min(args.steps, 3))
+    t0 = time.time()
+    r = run_reference_sample(args.config, args.width, lens, procs, calls)
+    wall = time.time() - t0
+    flops_u, _ = flops_per_user(cfg, args.width, lens)
+    value = r["users_per_s"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "users/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"OneRec-{args.config} encoder+decoder, beam search W={args.width} depth 3, "
+                               f"V={cfg.codebook_size}, users full-length {lens}",
+                   "users_per_gpu": args.users, "width": args.width, "lens": list(lens), "parallelism": "cpu"},
+        "cpu_baseline": cpu_baseline_block(r, args.config, args.width),
+        "e2e": {"value": value, "unit": "users/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gflop_per_user": flops_u / 1e9, "wall_s": wall, "init_s": r["init_s"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="orx", choices=["orx", "reference"])
+    ap.add_argument("--config", default="0.935B")
+    ap.add_argument("--users", type=int, default=128, help="users per GPU per step")
+    ap.add_argument("--width", type=int, default=128)
+    ap.add_argument("--lens", default="20,256,2000", help="short,positive,lifelong records per user")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    lens = tuple(int(x) for x in args.lens.split(","))
+
+    import paper_2506_13695_b200 as P
+    from paper_2506_13695_b200._lib import check, lib, orx_beam_out
+    cfg = P.PolicyConfig.preset(args.config)
+
+    if args.impl == "reference":
+        reference_arm(args, cfg, lens)
+        return
+
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    t_init = time.time()
+    model = P.PolicyModel(cfg, precision=args.precision, device=local, max_users=args.users, max_width=args.width)
+    t_init = time.time() - t_init
+    from paper_2506_13695_b200.dist import shard_users
+    user_begin, n_users = shard_users(rank, world, args.users)
+    batch = P.SynthBatch(1, user_begin, n_users, *lens)
+    e = model._e
+    L = cfg.n_code_layers
+    stream = torch.cuda.ExternalStream(lib().orx_engine_stream(e), device=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    from paper_2506_13695_b200.dist import max_over_ranks as _mor
+
+    def max_over_ranks(x):
+        return _mor(x, device=torch.device("cuda", local))
+
+    # ---- device-resident timing -------------------------------------------------------
+    check(lib().orx_engine_stage_batch(e, C.byref(batch.c)))
+    for _ in range(args.warmup):
+        check(lib().orx_beam_search_staged(e, args.width, None))
+    st0 = model.stats()
+    sampler = ClockSampler(local)
+    time.sleep(0.3)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        check(lib().orx_beam_search_staged(e, args.width, None))
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    st1 = model.stats()
+    ms = ev0.elapsed_time(ev1)
+    ms_max = max_over_ranks(ms)
+    launches = st1["launches"] - st0["launches"]
+    value = world * args.users * args.steps / (ms_max / 1e3)
+
+    # ---- end-to-end through the public API (host buffers) -----------------------------------
+    e2e_steps = args.e2e_steps or max(3, args.steps // 2)
+    codes = (C.c_int32 * (args.users * args.width * L))()
+    logp = (C.c_double * (args.users * args.width))()
+    nitems = (C.c_int32 * args.users)()
+    out = orx_beam_out(C.cast(codes, C.POINTER(C.c_int32)), C.cast(logp, C.POINTER(C.c_double)),
+                       C.cast(nitems, C.POINTER(C.c_int32)))
+    check(lib().orx_beam_search(e, C.byref(batch.c), args.width, C.byref(out)))  # warm the pinned buffers
+    s0 = model.stats()
+    barrier()
+    w0 = time.perf_counter()
+    ev0.record(stream)
+    for _ in range(e2e_steps):
+        check(lib().orx_beam_search(e, C.byref(batch.c), args.width, C.byref(out)))
+    ev1.record(stream)
+    ev1.synchronize()
+    w1 = time.perf_counter()
+    barrier()
+    s1 = model.stats()
+    e2e_ms = max(ev0.elapsed_time(ev1), (w1 - w0) * 1e3)
+    e2e_ms_max = max_over_ranks(e2e_ms)
+    e2e_value = world * args.users * e2e_steps / (e2e_ms_max / 1e3)
+    h2d = (s1["h2d_bytes"] - s0["h2d_bytes"]) // e2e_steps
+    d2h = (s1["d2h_bytes"] - s0["d2h_bytes"]) // e2e_steps
+
+    # ---- per-kernel-class timing (one instrumented step) -------------------------------------
+    check(lib().orx_profile_enable(1))
+    check(lib().orx_beam_search_staged(e, args.width, None))
+    torch.cuda.synchronize()
+    n = 7
+    pl, pms, pfl, pby = (C.c_int64 * n)(), (C.c_double * n)(), (C.c_double * n)(), (C.c_double * n)()
+    check(lib().orx_profile_read(n, pl, pms, pfl, pby))
+    check(lib().orx_profile_enable(0))
+    classes = {PROF_NAMES[i]: {"launches": pl[i], "ms": round(pms[i], 4),
+                               "tflops": (pfl[i] / (pms[i] * 1e-3) / 1e12) if pms[i] > 0 and pfl[i] > 0 else None}
+               for i in range(n)}
+    prof_total = sum(pms[i] for i in range(n))
+    peaks, peak_src = load_peaks()
+    gemm_ms = pms[0] + pms[1]
+    gemm_launch = pl[0] + pl[1]
+    gemm_flops = pfl[0] + pfl[1]
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    roofline = {"bound": "tensor", "kernel": "tc_gemm_kernel (tcgen05 dense + grouped MoE GEMMs)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "peak_kind": f"bf16_tflops_sustained ({peak_src}); kernel timed inside a long step",
+                "flops_per_launch": gemm_flops / max(gemm_launch, 1),
+                "ms_per_launch": gemm_ms / max(gemm_launch, 1),
+                "share_of_step": gemm_ms / prof_total if prof_total else None}
+    traffic_path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(traffic_path):
+        try:
+            with open(traffic_path) as f:
+                roofline["traffic"] = json.load(f).get("bytes_per_launch")
+        except Exception:
+            pass
+
+    flops_u, enc_flops_u = flops_per_user(cfg, args.width, lens)
+    mfu = value / world * flops_u / (peaks["bf16_tflops"] * 1e12)
+
+    # ---- CPU baseline (rank 0, N=1 only) --------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(REF_DRIVER):
+        try:
+            procs = safe_procs(args.config)
+            r = run_reference_sample(args.config, args.width, lens, procs, 3)
+            cpu = cpu_baseline_block(r, args.config, args.width)
+        except Exception as ex:  # reported, not fatal
+            cpu = {"value": None, "unit": "users/s", "cores": None, "kind": "reference", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "users/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16" if args.precision == "bf16" else "fp32", "data": "synthetic",
+            "config": {"workload": f"OneRec-{args.config} (BASELINE config 3): encoder + "
+                                   f"{'MoE ' if cfg.moe_enabled else ''}decoder + depth-{L} beam search, "
+                                   f"W={args.width}, V={cfg.codebook_size}, {args.users} users/GPU "
+                                   f"(short,positive,lifelong)={lens}, random-init weights (seed {cfg.seed})",
+                       "model": f"OneRec-{args.config}", "users_per_gpu": args.users, "global_batch": args.users * world,
+                       "width": args.width, "parallelism": f"dp{world} (users sharded, no inter-GPU traffic)",
+                       "l2": "working set (weights ~2 GB + activations) exceeds the 126 MB L2; no flush"},
+            "mfu": mfu, "mfu_peak": "bf16_tflops (burst) of MEASURED_PEAKS.json",
+            "gflop_per_user": flops_u / 1e9, "gflop_per_user_encoder": enc_flops_u / 1e9,
+            "e2e": {"value": e2e_value, "unit": "users/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": e2e_steps, "api": "orx_beam_search (host batch in, host beams out)"},
+            "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+            "roofline": roofline, "kernel_classes_ms_per_step": classes,
+            "cpu_baseline": cpu, "clocks": clocks, "init_s": t_init,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

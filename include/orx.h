@@ -156,6 +156,13 @@ int orx_beam_search_staged(orx_engine* e, int32_t width, orx_beam_out* out);
 int orx_engine_stats(const orx_engine* e, int64_t* launches, int64_t* h2d_bytes, int64_t* d2h_bytes);
 /* Stream the engine launches on (cudaStream_t as void*). */
 void* orx_engine_stream(orx_engine* e);
+/* Per-kernel-class CUDA-event timing (process-wide; off by default).
+ * Classes: 0 dense GEMM, 1 MoE grouped GEMM, 2 attention, 3 decoder
+ * self-attention, 4 MoE routing/scatter/combine, 5 beam top-k/merge, 6 other.
+ * orx_profile_read fills n (<= 7) entries and resets the log. */
+#define ORX_PROF_CLASSES 7
+int orx_profile_enable(int on);
+int orx_profile_read(int32_t n, int64_t* launches, double* ms, double* flops, double* bytes);
 
 /* Seeded synthetic users (synth_users.hpp). */
 int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,

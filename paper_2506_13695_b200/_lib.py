@@ -77,6 +77,9 @@ SIGNATURES = [
     ("orx_beam_search_staged", C.c_int, [_P, C.c_int32, C.POINTER(orx_beam_out)]),
     ("orx_engine_stats", C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("orx_engine_stream", _P, [_P]),
+    ("orx_profile_enable", C.c_int, [C.c_int]),
+    ("orx_profile_read", C.c_int, [C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("orx_synth_batch_create", C.c_int, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                          C.POINTER(_P)]),
     ("orx_synth_batch_view", C.c_int, [_P, C.POINTER(orx_user_batch)]),

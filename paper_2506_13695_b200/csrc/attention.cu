@@ -320,8 +320,9 @@ void launch_b16(int B, int max_q, int heads, const __nv_bfloat16* Q, int ldq, co
 
 template <>
 void launch_attention<float>(int B, int max_q, int heads, int dh, const float* Q, int ldq, const float* K, int ldk,
-                             const float* V, int ldv, float* O, int ldo, Seg q, Seg k, Seg o, cudaStream_t s) {
+                             const float* V, int ldv, float* O, int ldo, Seg q, Seg k, Seg o, cudaStream_t s, double flops) {
   if (B <= 0 || max_q <= 0) return;
+  ProfScope ps(PROF_ATTN, s, flops, 0.0);
   switch (dh) {
     case 8: launch_f32<8>(B, max_q, heads, Q, ldq, K, ldk, V, ldv, O, ldo, q, k, o, s); break;
     case 16: launch_f32<16>(B, max_q, heads, Q, ldq, K, ldk, V, ldv, O, ldo, q, k, o, s); break;
@@ -336,8 +337,9 @@ void launch_attention<float>(int B, int max_q, int heads, int dh, const float* Q
 template <>
 void launch_attention<__nv_bfloat16>(int B, int max_q, int heads, int dh, const __nv_bfloat16* Q, int ldq,
                                      const __nv_bfloat16* K, int ldk, const __nv_bfloat16* V, int ldv,
-                                     __nv_bfloat16* O, int ldo, Seg q, Seg k, Seg o, cudaStream_t s) {
+                                     __nv_bfloat16* O, int ldo, Seg q, Seg k, Seg o, cudaStream_t s, double flops) {
   if (B <= 0 || max_q <= 0) return;
+  ProfScope ps(PROF_ATTN, s, flops, 0.0);
   switch (dh) {
     case 32: launch_b16<32>(B, max_q, heads, Q, ldq, K, ldk, V, ldv, O, ldo, q, k, o, s); break;
     case 64: launch_b16<64>(B, max_q, heads, Q, ldq, K, ldk, V, ldv, O, ldo, q, k, o, s); break;

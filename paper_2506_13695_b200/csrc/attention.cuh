@@ -21,6 +21,6 @@ struct Seg {
 
 template <class T>
 void launch_attention(int B, int max_q, int heads, int dh, const T* Q, int ldq, const T* K, int ldk, const T* V,
-                      int ldv, T* O, int ldo, Seg q, Seg k, Seg o, cudaStream_t s);
+                      int ldv, T* O, int ldo, Seg q, Seg k, Seg o, cudaStream_t s, double flops = 0.0);
 
 }  // namespace orx

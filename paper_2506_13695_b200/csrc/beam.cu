@@ -232,6 +232,7 @@ void launch_row_topk(int rows, int V, int k_sel, const float* logits, const floa
     cudaFuncSetAttribute(row_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     set = smem;
   }
+  ProfScope ps(PROF_BEAM, s, 0.0, double(rows) * V * 4);
   row_topk_kernel<<<rows, kRowThreads, smem, s>>>(V, k_sel, logits, parent_score, parent_lexrank, lse, cand);
   ++launch_counter();
 }
@@ -240,6 +241,7 @@ void launch_beam_merge(int users, int n_live, int k_sel, int n_new, int V, int L
                        const float* logits, const float* lse, const BeamState& cur, BeamState& nxt,
                        cudaStream_t s) {
   if (n_new > kMaxBeam) throw std::invalid_argument("beam width above 1024 is not supported");
+  ProfScope ps(PROF_BEAM, s, 0.0, 0.0);
   beam_merge_kernel<<<users, kMergeThreads, 0, s>>>(n_live, k_sel, n_new, V, L, step, cand, logits, lse, cur, nxt);
   ++launch_counter();
 }

@@ -7,6 +7,7 @@
 
 #include "../../include/orx.h"
 #include "engine.hpp"
+#include "gemm.cuh"
 #include "model.hpp"
 #include "synth_users.hpp"
 
@@ -254,6 +255,24 @@ int orx_engine_stats(const orx_engine* e, int64_t* launches, int64_t* h2d, int64
 }
 
 void* orx_engine_stream(orx_engine* e) { return e ? e->e->stream() : nullptr; }
+
+int orx_profile_enable(int on) {
+  return guarded([&] { orx::prof_enable(on != 0); });
+}
+
+int orx_profile_read(int32_t n, int64_t* launches, double* ms, double* flops, double* bytes) {
+  return guarded([&] {
+    long long c[orx::PROF_N];
+    double t[orx::PROF_N], f[orx::PROF_N], b[orx::PROF_N];
+    orx::prof_collect(c, t, f, b);
+    for (int i = 0; i < n && i < orx::PROF_N; ++i) {
+      if (launches) launches[i] = c[i];
+      if (ms) ms[i] = t[i];
+      if (flops) flops[i] = f[i];
+      if (bytes) bytes[i] = b[i];
+    }
+  });
+}
 
 int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,
                            int32_t n_lifelong, orx_synth_batch** out) {

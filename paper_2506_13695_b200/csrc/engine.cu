@@ -618,7 +618,8 @@ class EngineT final : public Engine {
       Seg os;
       os.stride = Nq;
       os.fixed_len = Nq;
-      launch_attention<T>(U, Nq, H, dh, qproj_, d, kvl_, 2 * d, kvl_ + d, 2 * d, att_, d, qs, ks, os, st_);
+      launch_attention<T>(U, Nq, H, dh, qproj_, d, kvl_, 2 * d, kvl_ + d, 2 * d, att_, d, qs, ks, os, st_,
+                          4.0 * Nq * sg_.n_keys * d);
       gemm(att_, d, q.wo, U * Nq, epi(qo_, d, true));
       launch_rmsnorm<T>(U * Nq, d, qo_, d, q.gain, xn_, d, st_);
       Epi e1 = epi(ffh_, c.ffn_hidden, false);
@@ -642,14 +643,15 @@ class EngineT final : public Engine {
       Seg s;
       s.stride = Tn;
       s.fixed_len = Tn;
-      launch_attention<T>(U, Tn, H, dh, qkv_, 3 * d, qkv_ + d, 3 * d, qkv_ + 2 * d, 3 * d, att_, d, s, s, s, st_);
+      launch_attention<T>(U, Tn, H, dh, qkv_, 3 * d, qkv_ + d, 3 * d, qkv_ + 2 * d, 3 * d, att_, d, s, s, s, st_,
+                          4.0 * U * Tn * Tn * d);
       Epi eo = epi(z_, d, true);
       eo.resid = z_;
       eo.ld_resid = d;
       gemm(att_, d, l.wo, R, eo);
       launch_rmsnorm<T>(R, d, z_, d, l.n2, xn_, d, st_);
       if (enc_moe(c)) {
-        moe(l.moe, xn_, R, z_);
+        moe(l.moe, xn_, R, z_, l.n2);
       } else {
         ffn(l.fc1, l.fc2, xn_, R, z_);
       }
@@ -679,17 +681,18 @@ class EngineT final : public Engine {
     gemm(ffh_, cfg_.ffn_hidden, fc2, rows, e2);
   }
   // h += MoE(x)  (moe_forward, nn.cpp:117-172)
-  void moe(const MoeW& m, const T* x, int rows, float* h) {
+  void moe(const MoeW& m, const T* x, int rows, float* h, const float* norm_gain) {
     const orx_config& c = cfg_;
     const int d = c.d_model, E = c.n_experts, k = c.experts_active, he = expert_hidden(c), hp = rup(he, 8);
     CUDA_CHECK(cudaMemsetAsync(counts_, 0, E * sizeof(int32_t), st_));
-    launch_moe_route<T>(rows, d, E, k, x, d, m.gate_t, m.bias, sel_, wts_, counts_, st_);
+    launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.bias, sel_, wts_, counts_, st_);
     launch_moe_plan(E, counts_, cursor_, tile_expert_, max_tiles_, n_mtiles_, st_);
     launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xg_, row_scale_, st_);
     Grouped g;
     g.tile_expert = tile_expert_;
     g.n_mtiles = n_mtiles_;
     g.n_groups = E;
+    g.algo_rows = static_cast<long long>(rows) * k;
     const int M = static_cast<int>(S_);
     if constexpr (kBf16) {
       Epi e1 = epi(hg_, hp, false);
@@ -754,10 +757,10 @@ class EngineT final : public Engine {
       gemm(xn_, d, w.cq, rows, epi(qkv_, d, false));
       const int ldkv = 2 * d * Ld;
       launch_attention<T>(groups, max_group_rows, H, dh, qkv_, d, xkv_ + (size_t)l * 2 * d, ldkv,
-                          xkv_ + (size_t)l * 2 * d + d, ldkv, att_, d, gq, gk, gq, st_);
+                          xkv_ + (size_t)l * 2 * d + d, ldkv, att_, d, gq, gk, gq, st_, 4.0 * rows * Tn * d);
       gemm(att_, d, w.co, rows, e);
       launch_rmsnorm<T>(rows, d, h_, d, w.n3, xn_, d, st_);
-      if (c.moe_enabled) moe(w.moe, xn_, rows, h_);
+      if (c.moe_enabled) moe(w.moe, xn_, rows, h_, w.n3);
       else ffn(w.fc1, w.fc2, xn_, rows, h_);
     }
     (void)Tn;

@@ -15,6 +15,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -381,12 +382,70 @@ long long& launch_counter() {
 
 long long launch_counter_value() { return launch_counter(); }
 
+namespace {
+struct ProfRec {
+  int cat;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+struct Prof {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+Prof& prof() {
+  static Prof p;
+  return p;
+}
+}  // namespace
+
+ProfScope::ProfScope(int cat, cudaStream_t st, double flops, double bytes) : s(st) {
+  Prof& p = prof();
+  if (!p.on) return;
+  ProfRec r{cat, p.get(), p.get(), flops, bytes};
+  cudaEventRecord(r.a, s);
+  idx = static_cast<int>(p.recs.size());
+  p.recs.push_back(r);
+}
+ProfScope::~ProfScope() {
+  if (idx >= 0) cudaEventRecord(prof().recs[static_cast<size_t>(idx)].b, s);
+}
+void prof_enable(bool on) { prof().on = on; }
+void prof_collect(long long* count, double* ms, double* flops, double* bytes) {
+  Prof& p = prof();
+  for (int c = 0; c < PROF_N; ++c) count[c] = 0, ms[c] = flops[c] = bytes[c] = 0;
+  for (auto& r : p.recs) {
+    cudaEventSynchronize(r.b);
+    float t = 0;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    count[r.cat] += 1;
+    ms[r.cat] += t;
+    flops[r.cat] += r.flops;
+    bytes[r.cat] += r.bytes;
+    p.pool.push_back(r.a);
+    p.pool.push_back(r.b);
+  }
+  p.recs.clear();
+}
+
 void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int K, const Epi& epi,
                const Grouped* grp, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return;
   if (K % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0)
     throw std::invalid_argument("gemm_bf16: K and row strides must be multiples of 8");
   if (epi.swiglu && N % 256 != 0) throw std::invalid_argument("gemm_bf16: swiglu needs N % 256 == 0");
+  ProfScope ps(grp && grp->tile_expert ? PROF_GEMM_MOE : PROF_GEMM, stream,
+               2.0 * (grp && grp->tile_expert ? double(grp->algo_rows) : double(M)) * N * K, 0.0);
   if (N <= 128 && !epi.swiglu)
     launch_tc<128, 6>(A, lda, B, ldb, M, N, K, epi, grp, stream);
   else
@@ -398,6 +457,8 @@ void gemm_f32(const float* A, int lda, const float* B, int ldb, int M, int N, in
   if (M <= 0 || N <= 0) return;
   if (epi.swiglu) throw std::invalid_argument("gemm_f32: swiglu epilogue not supported");
   Grouped g = grp ? *grp : Grouped{};
+  ProfScope ps(g.tile_expert ? PROF_GEMM_MOE : PROF_GEMM, stream,
+               2.0 * (g.tile_expert ? double(g.algo_rows) : double(M)) * N * K, 0.0);
   dim3 grid((N + 63) / 64, (M + 63) / 64);
   simt_gemm_kernel<<<grid, 256, 0, stream>>>(A, lda, B, ldb, M, N, K, epi, g);
   ++launch_counter();

@@ -38,6 +38,7 @@ struct Grouped {
   const int* n_mtiles = nullptr;     // device scalar: number of valid M tiles
   int b_rows_per_expert = 0;
   int n_groups = 0;  // number of experts stacked in B
+  long long algo_rows = 0;  // real (token, expert) rows, for FLOP accounting
 };
 
 // bf16 A [M x K] (row stride lda elements), bf16 B [N x K] (row stride ldb).
@@ -52,5 +53,18 @@ void gemm_f32(const float* A, int lda, const float* B, int ldb, int M, int N, in
 
 int num_sms();
 long long& launch_counter();
+
+// Optional per-kernel-class timing with CUDA events on the launching stream
+// (bench.py's roofline). Disabled by default; zero cost when off.
+enum ProfCat { PROF_GEMM = 0, PROF_GEMM_MOE, PROF_ATTN, PROF_DEC_SELF, PROF_MOE_ROUTE, PROF_BEAM, PROF_MISC, PROF_N };
+struct ProfScope {
+  ProfScope(int cat, cudaStream_t s, double flops, double bytes);
+  ~ProfScope();
+  int idx = -1;
+  cudaStream_t s;
+};
+void prof_enable(bool on);
+// Per category: launches, total ms, algorithmic flops, algorithmic bytes.
+void prof_collect(long long* count, double* ms, double* flops, double* bytes);
 
 }  // namespace orx

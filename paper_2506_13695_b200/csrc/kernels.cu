@@ -1,4 +1,6 @@
+#include <algorithm>
 #include <cfloat>
+#include <stdexcept>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -170,20 +172,39 @@ __global__ void dec_self_attn_kernel(int rows, int d, int heads, int step, int l
 }
 
 // Gate scores, top-k (stable: score+bias desc, ties -> lower id), selected ids
-// ascending, softmax over selected raw scores (nn.cpp:121-147). Warp per row,
-// lane e owns expert e (E <= 32).
-template <class T>
-__global__ void moe_route_kernel(int rows, int d, int E, int k, const T* __restrict__ x, int ldx,
-                                 const float* __restrict__ gate_t, const float* __restrict__ bias,
-                                 int32_t* __restrict__ sel, float* __restrict__ wts, int32_t* __restrict__ counts) {
-  int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (r >= rows) return;
-  const T* xr = x + (size_t)r * ldx;
+// ascending, softmax over selected raw scores (nn.cpp:121-147). The gate input
+// RMSNorm(x) is recomputed here in fp32 from the fp32 residual stream so that
+// routing decisions do not see bf16 rounding. Gate matrix staged in smem;
+// warp per row (grid-stride), lane e owns expert e (E <= 32).
+constexpr int kRouteMaxPer = 64;  // d <= 2048
+__device__ __forceinline__ void moe_route_row(int r, int d, int E, int k, const float* __restrict__ xr,
+                                              const float* __restrict__ gain, const float* __restrict__ sg,
+                                              const float* __restrict__ bias, int32_t* __restrict__ sel,
+                                              float* __restrict__ wts, int32_t* __restrict__ counts, int lane) {
+  float xv[kRouteMaxPer];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < kRouteMaxPer; ++i) {
+    int c = lane + 32 * i;
+    xv[i] = c < d ? xr[c] : 0.f;
+    ss += xv[i] * xv[i];
+  }
+  ss = warp_sum(ss);
+  const float rr = rsqrtf(ss / d + 1e-6f);
+#pragma unroll
+  for (int i = 0; i < kRouteMaxPer; ++i) {
+    int c = lane + 32 * i;
+    if (c < d) xv[i] = xv[i] * rr * gain[c];
+  }
   float my = -FLT_MAX;  // lane e's raw score
   for (int e = 0; e < E; ++e) {
-    const float* g = gate_t + (size_t)e * d;
+    const float* g = sg + (size_t)e * d;
     float s = 0.f;
-    for (int c = lane; c < d; c += 32) s += to_f(xr[c]) * g[c];
+#pragma unroll
+    for (int i = 0; i < kRouteMaxPer; ++i) {
+      int c = lane + 32 * i;
+      if (c < d) s += xv[i] * g[c];
+    }
     s = warp_sum(s);
     if (lane == e) my = s;
   }
@@ -204,28 +225,31 @@ __global__ void moe_route_kernel(int rows, int d, int E, int k, const T* __restr
     if (lane == idx) taken = true;
     chosen |= 1u << idx;
   }
-  // selected ids ascending; weights = softmax over raw scores
   float mx = -FLT_MAX;
   for (int e = 0; e < E; ++e)
     if (chosen >> e & 1u) mx = fmaxf(mx, __shfl_sync(0xffffffffu, my, e));
   float den = 0.f;
   for (int e = 0; e < E; ++e)
     if (chosen >> e & 1u) den += __expf(__shfl_sync(0xffffffffu, my, e) - mx);
-  if (lane == 0) {
-    int j = 0;
-    for (int e = 0; e < E; ++e)
-      if (chosen >> e & 1u) {
-        sel[(size_t)r * k + j] = e;
-        wts[(size_t)r * k + j] = 0.f;  // filled below
-        ++j;
-      }
-  }
-  __syncwarp();
   if (lane < E && (chosen >> lane & 1u)) {
     int j = __popc(chosen & ((1u << lane) - 1u));
+    sel[(size_t)r * k + j] = lane;
     wts[(size_t)r * k + j] = __expf(my - mx) / den;
     atomicAdd(&counts[lane], 1);
   }
+}
+
+__global__ void __launch_bounds__(256) moe_route_kernel(int rows, int d, int E, int k, const float* __restrict__ x,
+                                                        int ldx, const float* __restrict__ gain,
+                                                        const float* __restrict__ gate_t,
+                                                        const float* __restrict__ bias, int32_t* __restrict__ sel,
+                                                        float* __restrict__ wts, int32_t* __restrict__ counts) {
+  extern __shared__ float sg[];  // [E][d]
+  for (int i = threadIdx.x; i < E * d; i += blockDim.x) sg[i] = gate_t[i];
+  __syncthreads();
+  const int lane = threadIdx.x % 32, wpb = blockDim.x / 32;
+  for (int r = blockIdx.x * wpb + threadIdx.x / 32; r < rows; r += gridDim.x * wpb)
+    moe_route_row(r, d, E, k, x + (size_t)r * ldx, gain, sg, bias, sel, wts, counts, lane);
 }
 
 // Segment offsets padded to the 128-row GEMM tile; tile -> expert table.
@@ -295,11 +319,13 @@ inline int grid_for(long long n, int block, int cap = 148 * 32) {
 
 }  // namespace
 
-#define ORX_LAUNCH(...)      \
-  do {                       \
-    __VA_ARGS__;             \
-    ++launch_counter();      \
+#define ORX_LAUNCH_CAT(cat, ...)          \
+  do {                                    \
+    ProfScope ps__(cat, s, 0.0, 0.0);     \
+    __VA_ARGS__;                          \
+    ++launch_counter();                   \
   } while (0)
+#define ORX_LAUNCH(...) ORX_LAUNCH_CAT(PROF_MISC, __VA_ARGS__)
 
 template <class T>
 void launch_features(const RecordsDev& r, const FeatureTables& t, T* out, int ldo, cudaStream_t s) {
@@ -341,31 +367,39 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L
                           const int32_t* anc, int anc_stride, T* out, cudaStream_t s) {
   if (rows <= 0) return;
   long long warps = (long long)rows * heads;
-  ORX_LAUNCH(dec_self_attn_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(
+  ORX_LAUNCH_CAT(PROF_DEC_SELF, dec_self_attn_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(
       rows, d, heads, step, layer, L, qkv, cache, anc, anc_stride, out));
 }
-template <class T>
-void launch_moe_route(int rows, int d, int E, int k, const T* x, int ldx, const float* gate_t, const float* bias,
-                      int32_t* sel, float* wts, int32_t* counts, cudaStream_t s) {
+void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, const float* gain, const float* gate_t,
+                      const float* bias, int32_t* sel, float* wts, int32_t* counts, cudaStream_t s) {
   if (rows <= 0) return;
-  ORX_LAUNCH(moe_route_kernel<T><<<(rows + 7) / 8, 256, 0, s>>>(rows, d, E, k, x, ldx, gate_t, bias, sel, wts, counts));
+  if (d > 32 * kRouteMaxPer) throw std::invalid_argument("moe routing supports d_model <= 2048");
+  const int smem = E * d * 4;
+  static int set = 0;
+  if (smem > 48 * 1024 && smem > set) {
+    cudaFuncSetAttribute(moe_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set = smem;
+  }
+  int blocks = std::min((rows + 7) / 8, num_sms() * 2);
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_route_kernel<<<blocks, 256, smem, s>>>(rows, d, E, k, x, ldx, gain, gate_t, bias,
+                                                                            sel, wts, counts));
 }
 void launch_moe_plan(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
                      int32_t* n_mtiles, cudaStream_t s) {
-  ORX_LAUNCH(moe_plan_kernel<<<1, 32, 0, s>>>(E, counts, cursor, tile_expert, max_tiles, n_mtiles));
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_plan_kernel<<<1, 32, 0, s>>>(E, counts, cursor, tile_expert, max_tiles, n_mtiles));
 }
 template <class T>
 void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
                         int32_t* cursor, int32_t* slot, T* xg, float* row_scale, cudaStream_t s) {
   if (rows <= 0) return;
   long long warps = (long long)rows * k;
-  ORX_LAUNCH(moe_scatter_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(rows, k, d, x, ldx, sel, wts,
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_scatter_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(rows, k, d, x, ldx, sel, wts,
                                                                                       cursor, slot, xg, row_scale));
 }
 void launch_moe_combine(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
                         cudaStream_t s) {
   if (rows <= 0) return;
-  ORX_LAUNCH(moe_combine_kernel<<<rows, 256, 0, s>>>(rows, k, d, yg, slot, h, ldh));
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_combine_kernel<<<rows, 256, 0, s>>>(rows, k, d, yg, slot, h, ldh));
 }
 void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, cudaStream_t s) {
   if (n <= 0) return;
@@ -381,8 +415,6 @@ void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, 
   template void launch_fill_rows<T>(int, int, const float*, T*, int, const int32_t*, cudaStream_t);              \
   template void launch_dec_self_attn<T>(int, int, int, int, int, int, const T*, T* const*, const int32_t*, int,   \
                                         T*, cudaStream_t);                                                       \
-  template void launch_moe_route<T>(int, int, int, int, const T*, int, const float*, const float*, int32_t*,      \
-                                    float*, int32_t*, cudaStream_t);                                             \
   template void launch_moe_scatter<T>(int, int, int, const T*, int, const int32_t*, const float*, int32_t*,       \
                                       int32_t*, T*, float*, cudaStream_t);
 INST(float)

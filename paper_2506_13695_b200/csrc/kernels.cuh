@@ -60,9 +60,9 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int n
                           T* const* cache, const int32_t* anc, int anc_stride, T* out, cudaStream_t s);
 
 // MoE (nn.cpp:117-172)
-template <class T>
-void launch_moe_route(int rows, int d, int E, int k, const T* x, int ldx, const float* gate_t, const float* bias,
-                      int32_t* sel, float* wts, int32_t* counts, cudaStream_t s);
+// Routing reads the fp32 residual x and the pre-MoE RMSNorm gain (norm recomputed in fp32).
+void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, const float* gain, const float* gate_t,
+                      const float* bias, int32_t* sel, float* wts, int32_t* counts, cudaStream_t s);
 void launch_moe_plan(int E, const int32_t* counts, int32_t* seg_cursor, int32_t* tile_expert, int max_tiles,
                      int32_t* n_mtiles, cudaStream_t s);
 template <class T>

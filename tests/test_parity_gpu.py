@@ -74,6 +74,40 @@ def test_0015b_fp32(width):
     print("0.015B fp32 W=%d (z, logits, next_logits) rel err:" % width, rep)
 
 
+MOE_SETS = {
+    # 0.935B-style: MoE in the decoder only, 24 experts top-2 (d=128 -> h_e=384)
+    "dec": (dict(moe_enabled=True, n_experts=24, experts_active=2),
+            ["moe_enabled=1", "n_experts=24", "experts_active=2"]),
+    # 2.633B-style: MoE in every encoder and decoder layer, top-4
+    "enc_and_dec": (dict(moe_enabled=True, n_experts=24, experts_active=4, moe_location="enc_and_dec"),
+                    ["moe_enabled=1", "n_experts=24", "experts_active=4", "moe_location=enc_and_dec"]),
+}
+
+
+@pytest.mark.parametrize("kind", ["dec", "enc_and_dec"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_moe_small(kind, precision):
+    """MoE routing (stable top-k, ascending combine, nn.cpp:117-172) at d=128."""
+    over, sets = MOE_SETS[kind]
+    P, model = _model("0.015B", precision, max_users=2, max_width=32, **over)
+    lens = (20, 64, 300)
+    _, refs = ref_dump("0.015B", 2, 32, lens=lens, sets=sets)
+    batch = P.SynthBatch(1, 0, 2, *lens)
+    if precision == "fp32":
+        rep = _check_user(P, model, batch, refs, 32, 1e-4, LOGIT_RTOL)
+        print(f"MoE {kind} fp32:", rep)
+    else:
+        z = model.encode_batch(batch)
+        codes, logp, _ = model.beam_search_arrays(batch, 32)
+        for u, ref in enumerate(refs):
+            pres = prefixes_of(ref["prefixes"])
+            lg = model.score_prefixes(batch, [u] * len(pres), pres)
+            el = max(rel_inf(lg[i], ref["logits"][i]) for i in range(len(pres)))
+            overlap = len({tuple(c) for c in codes[u]} & {tuple(c) for c in ref["beam_codes"]})
+            print(f"MoE {kind} bf16 user {u}: z {rel_inf(z[u], ref['z']):.3e} logits {el:.3e} overlap {overlap}/32")
+            assert el < 5e-2 and overlap >= 16
+
+
 def test_0015b_bf16_deviation():
     P, model = _model("0.015B", "bf16", max_users=2, max_width=128)
     _, refs = ref_dump("0.015B", 2, 128)

@@ -161,3 +161,19 @@ def test_flops_model_matches_survey():
         got = [bench.flops_per_user(cfg, w, (20, 256, 2000))[0] / 1e9 for w in (32, 128, 512)]
         for g, w in zip(got, want):
             assert abs(g - w) / w < 0.01, (name, got, want)
+
+
+def test_cpp_dropin_shim_builds_and_fails_loudly_without_gpu():
+    """include/orx_genrec.hpp compiled against the reference's own headers
+    (oracle/shim_demo.cpp); without a GPU the engine raises, never falls back."""
+    demo = os.path.join(ROOT, "oracle", "_ref", "shim_demo")
+    if not os.path.exists(demo):
+        pytest.skip("oracle/_ref/shim_demo not built")
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present (covered by the gpu test)")
+    except ImportError:
+        pass
+    r = subprocess.run([demo], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2 and "no CPU fallback" in r.stdout

@@ -122,3 +122,14 @@ def test_0015b_bf16_deviation():
         overlap = len({tuple(c) for c in codes[u]} & {tuple(c) for c in ref["beam_codes"]})
         print(f"0.015B bf16 user {u}: z rel {ez:.3e} logits rel {el:.3e} beam overlap {overlap}/128")
         assert ez < 5e-2 and el < 5e-2 and overlap >= 64
+
+
+def test_cpp_dropin_shim_matches_reference():
+    """The C++ adapter over the reference's own types (include/orx_genrec.hpp)
+    reproduces PolicyModel::encode_eval / next_logits_eval / beam_search."""
+    import os
+    import subprocess
+    demo = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "shim_demo")
+    r = subprocess.run([demo, "16"], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr

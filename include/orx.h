@@ -164,6 +164,30 @@ void* orx_engine_stream(orx_engine* e);
 int orx_profile_enable(int on);
 int orx_profile_read(int32_t n, int64_t* launches, double* ms, double* flops, double* bytes);
 
+/* Kernel-level test hook: one GEMM C = A . B^T with the engine's fused
+ * epilogue, on DEVICE pointers (e.g. torch tensors' data_ptr), on the given
+ * stream (cudaStream_t as void*, NULL = default). Used by the kernel tests
+ * against a PyTorch fp32 reference; not part of the reference surface. */
+typedef struct orx_gemm_args {
+  const void* A; int32_t lda;        /* [M][K] bf16 (or fp32 if precision == FP32) */
+  const void* B; int32_t ldb;        /* [N][K] (grouped: [n_groups * b_rows_per_expert][K]) */
+  int32_t M, N, K;
+  int32_t precision;                 /* ORX_PRECISION_BF16 (tcgen05) or ORX_PRECISION_FP32 (SIMT) */
+  const float* bias;                 /* [N] or NULL */
+  const float* row_scale;            /* [M] or NULL */
+  const float* resid; int32_t ld_resid; /* fp32, indexed by output row, or NULL */
+  const int32_t* row_map;            /* output row of A row r (< 0 dropped), or NULL */
+  void* out; int32_t ldo; int32_t out_bf16;
+  int32_t act;                       /* 0 none, 1 LeakyReLU(0.01), 2 SiLU */
+  int32_t swiglu;                    /* B rows interleaved per 128 as [W1 | W3]; out = silu(a)*b, N/2 cols */
+  int32_t n_out, m_valid, col_off;
+  const int32_t* tile_expert;        /* grouped: expert per tile_rows-row M tile (-1 skip), or NULL */
+  const int32_t* n_mtiles;           /* grouped: device scalar */
+  int32_t b_rows_per_expert, n_groups, tile_rows;
+  int32_t force_single_cta;          /* 1: use the 1-CTA tcgen05 kernel even for M > 128 */
+} orx_gemm_args;
+int orx_debug_gemm(const orx_gemm_args* args, void* stream);
+
 /* Seeded synthetic users (synth_users.hpp). */
 int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,
                            int32_t n_lifelong, orx_synth_batch** out);

@@ -46,6 +46,19 @@ class orx_beam_out(C.Structure):
                 ("n_items", C.POINTER(C.c_int32))]
 
 
+class orx_gemm_args(C.Structure):
+    _fields_ = [
+        ("A", C.c_void_p), ("lda", C.c_int32), ("B", C.c_void_p), ("ldb", C.c_int32),
+        ("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32), ("precision", C.c_int32),
+        ("bias", C.c_void_p), ("row_scale", C.c_void_p), ("resid", C.c_void_p), ("ld_resid", C.c_int32),
+        ("row_map", C.c_void_p), ("out", C.c_void_p), ("ldo", C.c_int32), ("out_bf16", C.c_int32),
+        ("act", C.c_int32), ("swiglu", C.c_int32), ("n_out", C.c_int32), ("m_valid", C.c_int32),
+        ("col_off", C.c_int32), ("tile_expert", C.c_void_p), ("n_mtiles", C.c_void_p),
+        ("b_rows_per_expert", C.c_int32), ("n_groups", C.c_int32), ("tile_rows", C.c_int32),
+        ("force_single_cta", C.c_int32),
+    ]
+
+
 # (name, restype, argtypes) for every function declared in include/orx.h
 _P = C.c_void_p
 _I32P = C.POINTER(C.c_int32)
@@ -80,6 +93,7 @@ SIGNATURES = [
     ("orx_profile_enable", C.c_int, [C.c_int]),
     ("orx_profile_read", C.c_int, [C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    ("orx_debug_gemm", C.c_int, [C.POINTER(orx_gemm_args), _P]),
     ("orx_synth_batch_create", C.c_int, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                          C.POINTER(_P)]),
     ("orx_synth_batch_view", C.c_int, [_P, C.POINTER(orx_user_batch)]),

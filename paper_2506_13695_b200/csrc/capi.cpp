@@ -274,6 +274,49 @@ int orx_profile_read(int32_t n, int64_t* launches, double* ms, double* flops, do
   });
 }
 
+int orx_debug_gemm(const orx_gemm_args* a, void* stream) {
+  return guarded([&] {
+    need(a, "args");
+    orx::Epi e;
+    e.bias = a->bias;
+    e.row_scale = a->row_scale;
+    e.resid = a->resid;
+    e.ld_resid = a->ld_resid;
+    e.out = a->out;
+    e.row_map = a->row_map;
+    e.ldo = a->ldo;
+    e.out_bf16 = a->out_bf16;
+    e.act = a->act;
+    e.swiglu = a->swiglu;
+    e.n_out = a->n_out ? a->n_out : (a->swiglu ? a->N / 2 : a->N);
+    e.m_valid = a->m_valid ? a->m_valid : a->M;
+    e.col_off = a->col_off;
+    orx::Grouped g;
+    g.tile_expert = a->tile_expert;
+    g.n_mtiles = a->n_mtiles;
+    g.b_rows_per_expert = a->b_rows_per_expert;
+    g.n_groups = a->n_groups;
+    g.tile_rows = a->tile_rows ? a->tile_rows : 128;
+    g.algo_rows = a->M;
+    auto st = static_cast<cudaStream_t>(stream);
+    const bool saved = orx::force_single_cta();
+    orx::force_single_cta() = a->force_single_cta != 0;
+    try {
+      if (a->precision == ORX_PRECISION_BF16)
+        orx::gemm_bf16(a->A, a->lda, a->B, a->ldb, a->M, a->N, a->K, e, a->tile_expert ? &g : nullptr, st);
+      else
+        orx::gemm_f32(static_cast<const float*>(a->A), a->lda, static_cast<const float*>(a->B), a->ldb, a->M, a->N,
+                      a->K, e, a->tile_expert ? &g : nullptr, st);
+    } catch (...) {
+      orx::force_single_cta() = saved;
+      throw;
+    }
+    orx::force_single_cta() = saved;
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) throw orx::RuntimeError(std::string("CUDA: ") + cudaGetErrorString(err));
+  });
+}
+
 int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,
                            int32_t n_lifelong, orx_synth_batch** out) {
   return guarded([&] {

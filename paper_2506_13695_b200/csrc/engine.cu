@@ -111,6 +111,9 @@ void validate_batch(const orx_config& cfg, const orx_user_batch& b) {  // valida
 template <class T>
 class EngineT final : public Engine {
   static constexpr bool kBf16 = std::is_same_v<T, __nv_bfloat16>;
+  // Expert segments are padded to the grouped GEMM's M tile: 256 rows for the
+  // tcgen05 CTA-pair kernel (both CTAs of a pair share one expert's B tile).
+  static constexpr int kMoeTile = kBf16 ? 256 : 128;
 
  public:
   EngineT(const HostWeights& hw, int device, int max_users, int max_width)
@@ -372,8 +375,8 @@ class EngineT final : public Engine {
     if (c.moe_enabled) {
       const int E = c.n_experts, k = c.experts_active, h = expert_hidden(c);
       const int64_t mrows = std::max(rows_enc, Rd_);
-      S_ = mrows * k + static_cast<int64_t>(E) * 128;
-      max_tiles_ = static_cast<int>(S_ / 128 + 1);
+      S_ = mrows * k + static_cast<int64_t>(E) * kMoeTile;
+      max_tiles_ = static_cast<int>(S_ / kMoeTile + 1);
       sel_ = ar_.alloc<int32_t>(mrows * k);
       wts_ = ar_.alloc<float>(mrows * k);
       slot_ = ar_.alloc<int32_t>(mrows * k);
@@ -686,12 +689,13 @@ class EngineT final : public Engine {
     const int d = c.d_model, E = c.n_experts, k = c.experts_active, he = expert_hidden(c), hp = rup(he, 8);
     CUDA_CHECK(cudaMemsetAsync(counts_, 0, E * sizeof(int32_t), st_));
     launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.bias, sel_, wts_, counts_, st_);
-    launch_moe_plan(E, counts_, cursor_, tile_expert_, max_tiles_, n_mtiles_, st_);
+    launch_moe_plan(E, counts_, cursor_, tile_expert_, max_tiles_, n_mtiles_, kMoeTile, st_);
     launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xg_, row_scale_, st_);
     Grouped g;
     g.tile_expert = tile_expert_;
     g.n_mtiles = n_mtiles_;
     g.n_groups = E;
+    g.tile_rows = kMoeTile;
     g.algo_rows = static_cast<long long>(rows) * k;
     const int M = static_cast<int>(S_);
     if constexpr (kBf16) {

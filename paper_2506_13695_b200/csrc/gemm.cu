@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -28,30 +29,57 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 B = one swizzle row
 
 // ---------------------------------------------------------------------------
-// epilogue: 32 consecutive accumulator columns of one row
+// epilogue (shared by the 1-CTA and CTA-pair kernels)
+//
+// 8 epilogue warps per CTA: warp w may only touch TMEM lanes 32*(w%4)..+31
+// (its row quadrant); the two warps of a quadrant split the tile's columns.
+// Each thread owns one output row. The residual of the next 32-column chunk
+// is loaded while the current chunk is finished, and the first chunk's
+// residual is in flight before the accumulator is even ready.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void epi_store32(const Epi& e, int row, int col0, float (&v)[32]) {
-  if (row >= e.m_valid) return;
-  int orow = e.row_map ? e.row_map[row] : row;
-  if (orow < 0) return;
-  const bool full = col0 + 32 <= e.n_out;
-  float rs = e.row_scale ? e.row_scale[row] : 1.f;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp 0 TMA, warp 1 MMA, 8 epilogue warps
+
+__device__ __forceinline__ void epi_load_resid(const Epi& e, int orow, int col0, float (&r)[32]) {
+  const float* rp = e.resid + (size_t)orow * e.ld_resid + col0;
+  if (col0 + 32 <= e.n_out && ((reinterpret_cast<uintptr_t>(rp) & 15) == 0)) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    int c = col0 + j;
-    float x = v[j];
-    if (e.bias && (full || c < e.n_out)) x += e.bias[c];
-    x = act_apply(x, e.act);
-    x *= rs;
-    v[j] = x;
+    for (int j = 0; j < 32; j += 4) {
+      float4 t = __ldg(reinterpret_cast<const float4*>(rp + j));
+      r[j] = t.x, r[j + 1] = t.y, r[j + 2] = t.z, r[j + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) r[j] = col0 + j < e.n_out ? rp[j] : 0.f;
   }
-  if (e.resid) {
-    const float* rp = e.resid + (size_t)orow * e.ld_resid + col0;
+}
+
+// bias -> activation -> row scale -> + residual -> store (bf16 or fp32)
+__device__ __forceinline__ void epi_finish32(const Epi& e, int orow, float rs, int col0, float (&v)[32],
+                                             const float (&r)[32], bool has_res) {
+  if (col0 >= e.n_out) return;
+  const bool full = col0 + 32 <= e.n_out;
+  if (e.bias) {
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      if (full || col0 + j < e.n_out) v[j] += rp[j];
+      if (full || col0 + j < e.n_out) v[j] += __ldg(e.bias + col0 + j);
   }
-  int oc = col0 + e.col_off;
+  if (e.act == ACT_LEAKY) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = v[j] > 0.f ? v[j] : 0.01f * v[j];  // tape.hpp:88
+  } else if (e.act == ACT_SILU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = silu_fast(v[j]);
+  }
+  if (rs != 1.f) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] *= rs;
+  }
+  if (has_res) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] += r[j];
+  }
+  const int oc = col0 + e.col_off;
   if (e.out_bf16) {
     __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)orow * e.ldo + oc;
     if (full && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
@@ -82,11 +110,70 @@ __device__ __forceinline__ void epi_store32(const Epi& e, int row, int col0, flo
   }
 }
 
+// One accumulator tile, this thread's row, this warp's column half.
+// tb = TMEM address of (quadrant lane 0, accumulator column 0).
+template <int BN>
+__device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tb, int row, int nt, int half, uint64_t* tfull,
+                                              uint32_t acc_phase) {
+  int orow = -1;
+  float rs = 1.f;
+  if (row < e.m_valid) {
+    orow = e.row_map ? e.row_map[row] : row;
+    if (e.row_scale) rs = e.row_scale[row];
+  }
+  const bool ok = orow >= 0;
+  if (e.swiglu) {
+    // B rows interleaved per 128: accumulator cols [0,BN/2) = W1, [BN/2,BN) = W3 (swiglu, nn.cpp:84-86)
+    constexpr int CP = BN / 64 / 2;
+    mbar_wait(tfull, acc_phase);
+    tc_fence_after();
+#pragma unroll
+    for (int i = 0; i < CP; ++i) {
+      const int c = half * CP + i;
+      uint32_t ra[32], rb[32];
+      tmem_ld32_async(tb + c * 32, ra);
+      tmem_ld32_async(tb + BN / 2 + c * 32, rb);
+      tmem_wait_ld();
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = silu_fast(__uint_as_float(ra[j])) * __uint_as_float(rb[j]);
+      float r[32];
+      const bool hr = ok && e.resid;
+      if (hr) epi_load_resid(e, orow, nt * (BN / 2) + c * 32, r);
+      if (ok) epi_finish32(e, orow, rs, nt * (BN / 2) + c * 32, v, r, hr);
+    }
+  } else {
+    constexpr int CH = BN / 32 / 2;
+    const bool hr = ok && e.resid != nullptr;
+    float rc[32];
+    if (hr) epi_load_resid(e, orow, nt * BN + half * CH * 32, rc);
+    mbar_wait(tfull, acc_phase);
+    tc_fence_after();
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int c = half * CH + i;
+      uint32_t ra[32];
+      tmem_ld32_async(tb + c * 32, ra);
+      float rn[32];
+      if (hr && i + 1 < CH) epi_load_resid(e, orow, nt * BN + (c + 1) * 32, rn);
+      tmem_wait_ld();
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(ra[j]);
+      if (ok) epi_finish32(e, orow, rs, nt * BN + c * 32, v, rc, hr);
+      if (i + 1 < CH) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) rc[j] = rn[j];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
-// tcgen05 persistent GEMM
+// tcgen05 persistent GEMM, one CTA per tile (128 x BN): small M
 // ---------------------------------------------------------------------------
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                    int N, int K, Epi epi, Grouped grp) {
   constexpr uint32_t A_BYTES = kBM * kBK * 2;
@@ -104,10 +191,12 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m_tiles = grp.n_mtiles ? *grp.n_mtiles : (M + kBM - 1) / kBM;
+  const int tile_rows = grp.tile_rows ? grp.tile_rows : kBM;
+  const int m_tiles = grp.n_mtiles ? *grp.n_mtiles * (tile_rows / kBM) : (M + kBM - 1) / kBM;
   const int n_tiles = (N + BN - 1) / BN;
   const int total = m_tiles * n_tiles;
   const int kblocks = (K + kBK - 1) / kBK;
+  auto expert_of = [&](int mt) { return grp.tile_expert[mt / (tile_rows / kBM)]; };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -116,7 +205,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], kEpiWarps);
     }
     fence_mbar_init();
     tma_prefetch(&tmA);
@@ -130,7 +219,8 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint64_t pol_a = l2_policy_evict_first();
+      // A is re-read by every N tile of its row block: keep it in L2 unless it is read once.
+      const uint64_t pol_a = n_tiles > 1 ? l2_policy_evict_normal() : l2_policy_evict_first();
       const uint64_t pol_b = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
@@ -138,7 +228,7 @@ __global__ void __launch_bounds__(192, 1)
         const int mt = t / n_tiles, nt = t % n_tiles;
         int brow = nt * BN;
         if (grp.tile_expert) {
-          int e = grp.tile_expert[mt];
+          int e = expert_of(mt);
           if (e < 0) continue;
           brow += e * grp.b_rows_per_expert;
         }
@@ -162,7 +252,7 @@ __global__ void __launch_bounds__(192, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        if (grp.tile_expert && grp.tile_expert[t / n_tiles] < 0) continue;
+        if (grp.tile_expert && expert_of(t / n_tiles) < 0) continue;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -188,34 +278,16 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int q = warp & 3;            // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) >> 2;  // column half
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int mt = t / n_tiles, nt = t % n_tiles;
-      if (grp.tile_expert && grp.tile_expert[mt] < 0) continue;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
+      if (grp.tile_expert && expert_of(mt) < 0) continue;
       const int row = mt * kBM + q * 32 + lane;
-      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-      if (epi.swiglu) {
-#pragma unroll 1
-        for (int c = 0; c < BN / 64; ++c) {
-          float a[32], b[32];
-          tmem_ld32(tbase + c * 32, a);
-          tmem_ld32(tbase + BN / 2 + c * 32, b);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) a[j] = a[j] / (1.f + __expf(-a[j])) * b[j];
-          epi_store32(epi, row, nt * (BN / 2) + c * 32, a);
-        }
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          float a[32];
-          tmem_ld32(tbase + c * 32, a);
-          epi_store32(epi, row, nt * BN + c * 32, a);
-        }
-      }
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      epilogue_tile<BN>(epi, tb, row, nt, half, &tfull[acc], acc_phase);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -231,6 +303,146 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ---------------------------------------------------------------------------
+// tcgen05 persistent GEMM over a CTA pair (cluster of 2, cta_group::2):
+// tile 256 x BN per pair; each CTA stages its 128 rows of A and BN/2 rows of
+// B (half the per-SM operand traffic of the 1-CTA kernel at the same MMA
+// rate), the leader CTA issues M=256 MMAs, each CTA drains its own 128-row
+// half of the accumulator from its TMEM.
+// ---------------------------------------------------------------------------
+template <int BN, int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                    int N, int K, Epi epi, Grouped grp) {
+  constexpr int PM = 2 * kBM;                    // pair tile rows
+  constexpr uint32_t A_BYTES = kBM * kBK * 2;    // this CTA's 128 rows
+  constexpr uint32_t B_BYTES = (BN / 2) * kBK * 2;  // this CTA's BN/2 rows
+  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int m_tiles = grp.n_mtiles ? *grp.n_mtiles : (M + PM - 1) / PM;  // grouped: tile_rows == 256
+  const int n_tiles = (N + BN - 1) / BN;
+  const int total = m_tiles * n_tiles;
+  const int kblocks = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);   // leader: its own expect_tx arrive; bytes from both CTAs
+      mbar_init(&empty[s], 1);  // one multicast commit per use
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * kEpiWarps);  // leader: epilogue warps of both CTAs
+    }
+    fence_mbar_init();
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_a = n_tiles > 1 ? l2_policy_evict_normal() : l2_policy_evict_first();
+      const uint64_t pol_b = l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < total; t += npairs) {
+        const int mt = t / n_tiles, nt = t % n_tiles;
+        int brow = nt * BN;
+        if (grp.tile_expert) {
+          int e = grp.tile_expert[mt];
+          if (e < 0) continue;
+          brow += e * grp.b_rows_per_expert;
+        }
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fb = mapa_shared(&full[stage], 0);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          tma_load_2d_pair(sA + stage * A_BYTES, &tmA, fb, kb * kBK, mt * PM + static_cast<int>(rank) * kBM, pol_a);
+          tma_load_2d_pair(sB + stage * B_BYTES, &tmB, fb, kb * kBK, brow + static_cast<int>(rank) * (BN / 2), pol_b);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(PM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = pair; t < total; t += npairs) {
+        if (grp.tile_expert && grp.tile_expert[t / n_tiles] < 0) continue;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            tc_mma_bf16_pair(d_tmem, umma_desc_sw128(a_base + k * 32), umma_desc_sw128(b_base + k * 32), idesc,
+                             (kb | k) != 0);
+          }
+          tc_commit_pair(&empty[stage], 3);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_pair(&tfull[acc], 3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0), tempty_leader1 = mapa_shared(&tempty[1], 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < total; t += npairs) {
+      const int mt = t / n_tiles, nt = t % n_tiles;
+      if (grp.tile_expert && grp.tile_expert[mt] < 0) continue;
+      const int row = mt * PM + static_cast<int>(rank) * kBM + q * 32 + lane;
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      epilogue_tile<BN>(epi, tb, row, nt, half, &tfull[acc], acc_phase);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // fp32 SIMT GEMM (parity mode): 64x64 tile, BK 16, 256 threads, 4x4 per thread
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) simt_gemm_kernel(const float* __restrict__ A, int lda,
@@ -239,10 +451,11 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const float* __restrict_
   __shared__ float sA[16][64 + 4];
   __shared__ float sB[16][64 + 4];
   const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
-  if (grp.n_mtiles && m0 >= *grp.n_mtiles * kBM) return;
+  const int tile_rows = grp.tile_rows ? grp.tile_rows : kBM;
+  if (grp.n_mtiles && m0 >= *grp.n_mtiles * tile_rows) return;
   int boff = 0;
   if (grp.tile_expert) {
-    int e = grp.tile_expert[m0 / kBM];
+    int e = grp.tile_expert[m0 / tile_rows];
     if (e < 0) return;
     boff = e * grp.b_rows_per_expert;
   }
@@ -358,11 +571,43 @@ void launch_tc(const void* A, int lda, const void* B, int ldb, int M, int N, int
     tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
     if (tiles > num_sms()) tiles = num_sms();
   }
-  tc_gemm_kernel<BN, STAGES><<<tiles, 192, smem, stream>>>(ma, mb, M, N, K, epi, g);
+  tc_gemm_kernel<BN, STAGES><<<tiles, kThreads, smem, stream>>>(ma, mb, M, N, K, epi, g);
+  ++launch_counter();
+}
+
+template <int BN, int STAGES>
+void launch_tc2(const void* A, int lda, const void* B, int ldb, int M, int N, int K, const Epi& epi,
+                const Grouped* grp, cudaStream_t stream) {
+  constexpr size_t smem = STAGES * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tc2_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr_set = true;
+  }
+  Grouped g = grp ? *grp : Grouped{};
+  if (g.tile_expert && g.tile_rows != 2 * kBM)
+    throw std::invalid_argument("gemm_bf16: grouped CTA-pair GEMM needs 256-row expert tiles");
+  CUtensorMap ma = make_map_bf16(A, M, K, lda, kBM);
+  const int b_rows = g.tile_expert ? g.n_groups * g.b_rows_per_expert : N;
+  CUtensorMap mb = make_map_bf16(B, b_rows, K, ldb, BN / 2);
+  const int max_pairs = num_sms() / 2;
+  int pairs;
+  if (g.n_mtiles) {
+    pairs = max_pairs;
+  } else {
+    pairs = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
+    if (pairs > max_pairs) pairs = max_pairs;
+  }
+  tc2_gemm_kernel<BN, STAGES><<<2 * pairs, kThreads, smem, stream>>>(ma, mb, M, N, K, epi, g);
   ++launch_counter();
 }
 
 }  // namespace
+
+bool& force_single_cta() {
+  static bool f = getenv("ORX_GEMM_SINGLE_CTA") != nullptr;
+  return f;
+}
 
 int num_sms() {
   static int n = 0;
@@ -446,10 +691,19 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
   if (epi.swiglu && N % 256 != 0) throw std::invalid_argument("gemm_bf16: swiglu needs N % 256 == 0");
   ProfScope ps(grp && grp->tile_expert ? PROF_GEMM_MOE : PROF_GEMM, stream,
                2.0 * (grp && grp->tile_expert ? double(grp->algo_rows) : double(M)) * N * K, 0.0);
-  if (N <= 128 && !epi.swiglu)
-    launch_tc<128, 6>(A, lda, B, ldb, M, N, K, epi, grp, stream);
-  else
-    launch_tc<256, 4>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+  const bool grouped = grp && grp->tile_expert;
+  const bool pair = grouped ? grp->tile_rows == 2 * kBM : (M > kBM && !force_single_cta());
+  if (pair) {
+    if (N <= 128 && !epi.swiglu)
+      launch_tc2<128, 8>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+    else
+      launch_tc2<256, 6>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+  } else {
+    if (N <= 128 && !epi.swiglu)
+      launch_tc<128, 6>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+    else
+      launch_tc<256, 4>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+  }
 }
 
 void gemm_f32(const float* A, int lda, const float* B, int ldb, int M, int N, int K, const Epi& epi,

@@ -38,6 +38,7 @@ struct Grouped {
   const int* n_mtiles = nullptr;     // device scalar: number of valid M tiles
   int b_rows_per_expert = 0;
   int n_groups = 0;  // number of experts stacked in B
+  int tile_rows = 128;  // rows per tile_expert entry (expert segments padded to it); 256 = CTA-pair kernel
   long long algo_rows = 0;  // real (token, expert) rows, for FLOP accounting
 };
 
@@ -52,6 +53,8 @@ void gemm_f32(const float* A, int lda, const float* B, int ldb, int M, int N, in
               const Grouped* grp, cudaStream_t stream);
 
 int num_sms();
+// ORX_GEMM_SINGLE_CTA=1 disables the CTA-pair kernel for dense GEMMs (A/B comparison).
+bool& force_single_cta();
 long long& launch_counter();
 
 // Optional per-kernel-class timing with CUDA events on the launching stream

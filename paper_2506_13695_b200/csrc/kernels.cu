@@ -252,16 +252,16 @@ __global__ void __launch_bounds__(256) moe_route_kernel(int rows, int d, int E, 
     moe_route_row(r, d, E, k, x + (size_t)r * ldx, gain, sg, bias, sel, wts, counts, lane);
 }
 
-// Segment offsets padded to the 128-row GEMM tile; tile -> expert table.
+// Segment offsets padded to the GEMM expert tile (128 rows, 256 for the CTA-pair kernel); tile -> expert table.
 __global__ void moe_plan_kernel(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
-                                int32_t* n_mtiles) {
+                                int32_t* n_mtiles, int tile_rows) {
   if (threadIdx.x != 0) return;
   int off = 0, tile = 0;
   for (int e = 0; e < E; ++e) {
     cursor[e] = off;
-    int nt = (counts[e] + 127) / 128;
+    int nt = (counts[e] + tile_rows - 1) / tile_rows;
     for (int i = 0; i < nt && tile < max_tiles; ++i) tile_expert[tile++] = e;
-    off += nt * 128;
+    off += nt * tile_rows;
   }
   *n_mtiles = tile;
   for (int i = tile; i < max_tiles; ++i) tile_expert[i] = -1;
@@ -385,8 +385,9 @@ void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, co
                                                                             sel, wts, counts));
 }
 void launch_moe_plan(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
-                     int32_t* n_mtiles, cudaStream_t s) {
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_plan_kernel<<<1, 32, 0, s>>>(E, counts, cursor, tile_expert, max_tiles, n_mtiles));
+                     int32_t* n_mtiles, int tile_rows, cudaStream_t s) {
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE,
+                 moe_plan_kernel<<<1, 32, 0, s>>>(E, counts, cursor, tile_expert, max_tiles, n_mtiles, tile_rows));
 }
 template <class T>
 void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,

@@ -64,7 +64,7 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int n
 void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, const float* gain, const float* gate_t,
                       const float* bias, int32_t* sel, float* wts, int32_t* counts, cudaStream_t s);
 void launch_moe_plan(int E, const int32_t* counts, int32_t* seg_cursor, int32_t* tile_expert, int max_tiles,
-                     int32_t* n_mtiles, cudaStream_t s);
+                     int32_t* n_mtiles, int tile_rows, cudaStream_t s);
 template <class T>
 void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
                         int32_t* seg_cursor, int32_t* slot, T* xg, float* row_scale, cudaStream_t s);

@@ -187,6 +187,12 @@ typedef struct orx_gemm_args {
   int32_t force_single_cta;          /* 1: use the 1-CTA tcgen05 kernel even for M > 128 */
 } orx_gemm_args;
 int orx_debug_gemm(const orx_gemm_args* args, void* stream);
+/* Kernel-level test hook for the per-row beam pruning step (device pointers):
+ * lse[r] = logsumexp(logits[r]); cand[r][0..k) = the k largest keys
+ * (ordered fp32 score pscore[r] + logits[r][i] - lse[r]) << 32 |
+ * (0xFFFFFFFF - (plex[r] * V + i)), in unspecified order. */
+int orx_debug_row_topk(int32_t rows, int32_t V, int32_t k, const float* logits, const float* pscore,
+                       const int32_t* plex, float* lse, uint64_t* cand, void* stream);
 
 /* Seeded synthetic users (synth_users.hpp). */
 int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,

@@ -148,6 +148,169 @@ __global__ void __launch_bounds__(kRowThreads) row_topk_kernel(int V, int k_sel,
   }
 }
 
+// Fast path (V <= 8192, k_sel < V, k_sel <= 1024): the row stays in registers
+// (32 per thread). Bisection on the fp32 score finds a threshold whose
+// candidate count lies in [k_sel, cap]; the candidates are sorted in shared
+// memory (bitonic) and the first k_sel keys written. Exact: the key order
+// is the same as row_topk_kernel's, so ties at the threshold are all kept
+// and resolved by the lexicographic part of the key. Rows where bisection
+// cannot isolate such a threshold (massive exact ties) take the radix path.
+constexpr int kTopkPer = 32;
+constexpr int kTopkCap = 2048;
+
+__device__ __forceinline__ float block_reduce_sum256(float v, float* red) {
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int w = 0; w < kRowThreads / 32; ++w) t += red[w];
+  return t;
+}
+__device__ __forceinline__ float block_reduce_max256(float v, float* red) {
+  v = warp_max(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = -FLT_MAX;
+#pragma unroll
+  for (int w = 0; w < kRowThreads / 32; ++w) t = fmaxf(t, red[w]);
+  return t;
+}
+
+__global__ void __launch_bounds__(kRowThreads) row_topk_fast_kernel(int V, int k_sel, const float* __restrict__ logits,
+                                                                    const float* __restrict__ pscore,
+                                                                    const int32_t* __restrict__ plex,
+                                                                    float* __restrict__ lse_out,
+                                                                    uint64_t* __restrict__ cand) {
+  __shared__ uint64_t buf[kTopkCap];
+  __shared__ float red[kRowThreads / 32];
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t bc[4];
+  __shared__ uint32_t counter;
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const float* lg = logits + (size_t)row * V;
+  float v[kTopkPer];
+  float mx = -FLT_MAX;
+#pragma unroll
+  for (int j = 0; j < kTopkPer; ++j) {
+    const int i = tid + kRowThreads * j;
+    v[j] = i < V ? __ldg(lg + i) : -FLT_MAX;
+    mx = fmaxf(mx, v[j]);
+  }
+  mx = block_reduce_max256(mx, red);
+  float se = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < kTopkPer; ++j)
+    if (tid + kRowThreads * j < V) {
+      se += __expf(v[j] - mx);
+      s1 += v[j] - mx;
+      s2 += (v[j] - mx) * (v[j] - mx);
+    }
+  se = block_reduce_sum256(se, red);
+  s1 = block_reduce_sum256(s1, red);
+  s2 = block_reduce_sum256(s2, red);
+  const float lse = mx + logf(se);  // log-softmax normaliser (generation.cpp:10-20)
+  const float ps = pscore[row];
+  // scores (the ranking quantity of the candidate key)
+  float smin = FLT_MAX;
+#pragma unroll
+  for (int j = 0; j < kTopkPer; ++j) {
+    v[j] = tid + kRowThreads * j < V ? ps + (v[j] - lse) : -FLT_MAX;
+    if (tid + kRowThreads * j < V) smin = fminf(smin, v[j]);
+  }
+  smin = -block_reduce_max256(-smin, red);
+  const float smax = ps + (mx - lse);
+  // bisection: count(score >= tau) in [k_sel, cap]
+  const int cap = min(kTopkCap, max(2 * k_sel, 256));
+  float lo = smin, hi = smax;  // count(lo) = V >= k_sel; count(hi) >= 1
+  const float mean = s1 / V, sd = sqrtf(fmaxf(s2 / V - mean * mean, 0.f));
+  // first probe: normal upper quantile of the top (1.25 k_sel) / V fraction
+  // (Abramowitz-Stegun 26.2.23), scores assumed ~normal
+  const float pf = fminf(0.5f, 1.25f * k_sel / V);
+  const float t = sqrtf(-2.f * logf(pf));
+  const float z = t - (2.515517f + 0.802853f * t + 0.010328f * t * t) /
+                          (1.f + 1.432788f * t + 0.189269f * t * t + 0.001308f * t * t * t);
+  float tau = smax + mean + z * sd;
+  tau = fminf(fmaxf(tau, lo), hi);
+  int count = -1;
+  bool found = false;
+  for (int it = 0; it < 48; ++it) {
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < kTopkPer; ++j) c += v[j] >= tau;
+    count = static_cast<int>(block_reduce_sum256(static_cast<float>(c), red));
+    if (count >= k_sel && count <= cap) {
+      found = true;
+      break;
+    }
+    if (count < k_sel) hi = tau;
+    else lo = tau;
+    const float nt = 0.5f * (lo + hi);
+    if (nt == lo || nt == hi) break;
+    tau = nt;
+  }
+  if (tid == 0) {
+    lse_out[row] = lse;
+    counter = 0;
+  }
+  const uint32_t lbase = static_cast<uint32_t>(plex[row]) * static_cast<uint32_t>(V);
+  uint64_t* out = cand + (size_t)row * k_sel;
+  if (found) {
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kTopkPer; ++j) {
+      const int i = tid + kRowThreads * j;
+      const bool take = v[j] >= tau;
+      const unsigned m = __ballot_sync(0xffffffffu, take);
+      uint32_t base = 0;
+      if ((tid & 31) == 0 && m) base = atomicAdd(&counter, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (take)
+        buf[base + __popc(m & ((1u << (tid & 31)) - 1u))] =
+            (static_cast<uint64_t>(ord_f32(v[j])) << 32) | (0xFFFFFFFFu - (lbase + static_cast<uint32_t>(i)));
+    }
+    __syncthreads();
+    int np = 256;
+    while (np < count) np <<= 1;
+    for (int i = count + tid; i < np; i += kRowThreads) buf[i] = 0;
+    __syncthreads();
+    for (int size = 2; size <= np; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < np / 2; i += kRowThreads) {
+          const int lo_i = 2 * i - (i & (stride - 1));
+          const int hi_i = lo_i + stride;
+          const bool desc = (lo_i & size) == 0;
+          const uint64_t x = buf[lo_i], y = buf[hi_i];
+          if ((x < y) == desc) {
+            buf[lo_i] = y;
+            buf[hi_i] = x;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int i = tid; i < k_sel; i += kRowThreads) out[i] = buf[i];
+    return;
+  }
+  // fallback: radix select over the keys (rare: massive exact ties)
+  __syncthreads();
+  auto key_of = [&](int i) -> uint64_t {
+    const float sc = ps + (__ldg(lg + i) - lse);
+    return (static_cast<uint64_t>(ord_f32(sc)) << 32) | (0xFFFFFFFFu - (lbase + static_cast<uint32_t>(i)));
+  };
+  uint64_t thr = block_kth_largest<kRowThreads>(V, k_sel, key_of, hist, bc);
+  __syncthreads();
+  for (int i = tid; i < V; i += kRowThreads) {
+    const uint64_t key = key_of(i);
+    if (key >= thr) {
+      uint32_t pos = atomicAdd(&counter, 1u);
+      if (pos < static_cast<uint32_t>(k_sel)) out[pos] = key;
+    }
+  }
+}
+
 constexpr int kMergeThreads = 512;
 constexpr int kMaxBeam = 1024;
 
@@ -233,6 +396,11 @@ void launch_row_topk(int rows, int V, int k_sel, const float* logits, const floa
     set = smem;
   }
   ProfScope ps(PROF_BEAM, s, 0.0, double(rows) * V * 4);
+  if (V <= kRowThreads * kTopkPer && k_sel < V && k_sel <= 1024) {
+    row_topk_fast_kernel<<<rows, kRowThreads, 0, s>>>(V, k_sel, logits, parent_score, parent_lexrank, lse, cand);
+    ++launch_counter();
+    return;
+  }
   row_topk_kernel<<<rows, kRowThreads, smem, s>>>(V, k_sel, logits, parent_score, parent_lexrank, lse, cand);
   ++launch_counter();
 }

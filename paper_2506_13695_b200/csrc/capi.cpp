@@ -7,6 +7,7 @@
 
 #include "../../include/orx.h"
 #include "engine.hpp"
+#include "beam.cuh"
 #include "gemm.cuh"
 #include "model.hpp"
 #include "synth_users.hpp"
@@ -312,6 +313,16 @@ int orx_debug_gemm(const orx_gemm_args* a, void* stream) {
       throw;
     }
     orx::force_single_cta() = saved;
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) throw orx::RuntimeError(std::string("CUDA: ") + cudaGetErrorString(err));
+  });
+}
+
+int orx_debug_row_topk(int32_t rows, int32_t V, int32_t k, const float* logits, const float* pscore,
+                       const int32_t* plex, float* lse, uint64_t* cand, void* stream) {
+  return guarded([&] {
+    if (rows < 0 || V < 1 || k < 1 || k > V) throw orx::InvalidArgument("row_topk: bad sizes");
+    orx::launch_row_topk(rows, V, k, logits, pscore, plex, lse, cand, static_cast<cudaStream_t>(stream));
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) throw orx::RuntimeError(std::string("CUDA: ") + cudaGetErrorString(err));
   });

@@ -71,6 +71,7 @@ struct Lin {  // y = x . W, W^T packed [N][K] (K padded to 8, zeros)
 
 struct MoeW {
   const float* gate_t = nullptr;  // [E][d]
+  const float* gate_gain = nullptr;  // [E][d] gate_t[e][c] * (pre-MoE RMSNorm gain)[c]
   const float* bias = nullptr;    // [E]
   const void* w13 = nullptr;      // bf16: [E][2h][d] interleaved per 128 rows; fp32: w1 [E][h][d]
   const void* w3 = nullptr;       // fp32 only: [E][h][d]
@@ -180,7 +181,7 @@ class EngineT final : public Engine {
     if (!bias.empty()) L.bias = up(hw, bias);
     return L;
   }
-  MoeW pack_moe(const HostWeights& hw, const std::string& n) {
+  MoeW pack_moe(const HostWeights& hw, const std::string& n, const std::string& gain_name) {
     const int d = cfg_.d_model, E = cfg_.n_experts, h = expert_hidden(cfg_);
     MoeW m;
     const Tensor& g = hw.get(n + ".gate.w");  // (d, E)
@@ -188,6 +189,10 @@ class EngineT final : public Engine {
     for (int k = 0; k < d; ++k)
       for (int e = 0; e < E; ++e) gt[(size_t)e * d + k] = g.data[(size_t)k * E + e];
     m.gate_t = upload_f32(gt.data(), gt.size());
+    const Tensor& gain = hw.get(gain_name);
+    for (int e = 0; e < E; ++e)
+      for (int k = 0; k < d; ++k) gt[(size_t)e * d + k] *= gain.data[k];
+    m.gate_gain = upload_f32(gt.data(), gt.size());
     m.bias = up(hw, n + ".routing_bias");
     const int dp = rup(d, 8), hp = rup(h, 8);
     auto ex = [&](int e, const char* w) { return hw.get(n + ".expert" + std::to_string(e) + "." + w + ".w"); };
@@ -293,7 +298,7 @@ class EngineT final : public Engine {
       e.n2 = up(hw, n + ".n2.gain");
       e.wqkv = pack(hw, {n + ".attn.wq.w", n + ".attn.wk.w", n + ".attn.wv.w"});
       e.wo = pack(hw, {n + ".attn.wo.w"});
-      if (enc_moe(c)) e.moe = pack_moe(hw, n + ".moe");
+      if (enc_moe(c)) e.moe = pack_moe(hw, n + ".moe", n + ".n2.gain");
       else {
         e.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b");
         e.fc2 = pack(hw, {n + ".ffn.fc2.w"}, n + ".ffn.fc2.b");
@@ -313,7 +318,7 @@ class EngineT final : public Engine {
       e.co = pack(hw, {n + ".cross.wo.w"});
       xkv.push_back(n + ".cross.wk.w");
       xkv.push_back(n + ".cross.wv.w");
-      if (c.moe_enabled) e.moe = pack_moe(hw, n + ".moe");
+      if (c.moe_enabled) e.moe = pack_moe(hw, n + ".moe", n + ".n3.gain");
       else {
         e.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b");
         e.fc2 = pack(hw, {n + ".ffn.fc2.w"}, n + ".ffn.fc2.b");
@@ -688,7 +693,7 @@ class EngineT final : public Engine {
     const orx_config& c = cfg_;
     const int d = c.d_model, E = c.n_experts, k = c.experts_active, he = expert_hidden(c), hp = rup(he, 8);
     CUDA_CHECK(cudaMemsetAsync(counts_, 0, E * sizeof(int32_t), st_));
-    launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.bias, sel_, wts_, counts_, st_);
+    launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.gate_gain, m.bias, sel_, wts_, counts_, st_);
     launch_moe_plan(E, counts_, cursor_, tile_expert_, max_tiles_, n_mtiles_, kMoeTile, st_);
     launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xg_, row_scale_, st_);
     Grouped g;

@@ -56,6 +56,95 @@ __global__ void features_kernel(RecordsDev r, FeatureTables t, T* __restrict__ o
   }
 }
 
+// 4 / 8 consecutive elements of T <-> floats
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {
+  uint2 u = *reinterpret_cast<const uint2*>(p);
+  float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
+  float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ void st4(__nv_bfloat16* p, float4 v) {
+  uint2 u;
+  u.x = pack_bf16(v.x, v.y);
+  u.y = pack_bf16(v.z, v.w);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+__device__ __forceinline__ void st8(float* p, const float (&v)[8]) {
+  st4(p, make_float4(v[0], v[1], v[2], v[3]));
+  st4(p + 4, make_float4(v[4], v[5], v[6], v[7]));
+}
+__device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&v)[8]) {
+  uint4 u;
+  u.x = pack_bf16(v[0], v[1]);
+  u.y = pack_bf16(v[2], v[3]);
+  u.z = pack_bf16(v[4], v[5]);
+  u.w = pack_bf16(v[6], v[7]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+// Vectorised feature rows (same layout as features_kernel): warp per record,
+// lane per 8-column group; every section width is a multiple of 8 here.
+template <class T>
+__global__ void __launch_bounds__(256) features8_kernel(RecordsDev r, FeatureTables t, T* __restrict__ out, int ldo) {
+  const int d = t.d, ad = t.aid_dim, mn = t.minor;
+  const int F = t.vid_only ? d : d + ad + 5 * mn;
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < r.n; row += gridDim.x * (blockDim.x >> 5)) {
+    const int vid = t.use_sid ? 0 : hashed(r.vid[row], t.vid_vocab);
+    const int aid = hashed(r.aid[row], t.aid_vocab);
+    const float sc[4] = {r.tag[row], r.ts[row], r.play[row], r.dur[row]};
+    const uint32_t lab = r.labels[row];
+    T* o = out + (size_t)row * ldo;
+    for (int c0 = lane * 8; c0 < ldo; c0 += 256) {
+      float v[8];
+      if (c0 < d) {
+        if (t.use_sid) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = 0.f;
+          for (int l = 0; l < t.n_code_layers; ++l) {
+            const float* src = t.tokens[l] + (size_t)r.sid[(size_t)row * t.n_code_layers + l] * d + c0;
+            float4 a = ld4(src), b = ld4(src + 4);
+            v[0] += a.x, v[1] += a.y, v[2] += a.z, v[3] += a.w, v[4] += b.x, v[5] += b.y, v[6] += b.z, v[7] += b.w;
+          }
+        } else {
+          const float* src = t.vid + (size_t)vid * d + c0;
+          float4 a = ld4(src), b = ld4(src + 4);
+          v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+        }
+      } else if (c0 < F) {
+        int cc = c0 - d;
+        if (cc < ad) {
+          const float* src = t.aid + (size_t)aid * ad + cc;
+          float4 a = ld4(src), b = ld4(src + 4);
+          v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+        } else {
+          cc -= ad;
+          const int f = cc / mn, j0 = cc % mn;
+          if (f < 4) {  // scalar feature x * w + b, (2 x minor) table (policy.cpp:175-188)
+            const float* p = f == 0 ? t.tag : f == 1 ? t.ts : f == 2 ? t.play : t.dur;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = sc[f] * p[j0 + j] + p[mn + j0 + j];
+          } else {  // label multi-hot . (5 x minor) (policy.cpp:190-195)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = 0.f;
+            for (int b = 0; b < t.n_flags; ++b)
+              if ((lab >> b) & 1u) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] += t.label[b * mn + j0 + j];
+              }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 0.f;
+      }
+      st8(o + c0, v);
+    }
+  }
+}
+
 template <class T>
 __global__ void static_features_kernel(int U, const int32_t* uid, const int32_t* gender, const int32_t* age,
                                        const float* ue, const float* ge, const float* ae, int sd, int uv, int gv,
@@ -171,6 +260,76 @@ __global__ void dec_self_attn_kernel(int rows, int d, int heads, int step, int l
   }
 }
 
+// Vectorised variant (dh % 4 == 0, dh <= 128): lane owns 4 consecutive
+// head dims; same math and order of operations as dec_self_attn_kernel.
+template <class T>
+__global__ void __launch_bounds__(256) dec_self_attn4_kernel(int rows, int d, int heads, int step, int layer, int L,
+                                                             const T* __restrict__ qkv, T* const* __restrict__ cache,
+                                                             const int32_t* __restrict__ anc, int anc_stride,
+                                                             T* __restrict__ out) {
+  const int gw = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int r = gw / heads, h = gw % heads;
+  if (r >= rows) return;
+  const int dh = d / heads;
+  const bool on = lane * 4 < dh;
+  const int c = on ? lane * 4 : 0;
+  const T* q = qkv + (size_t)r * 3 * d + h * dh;
+  const float4 q4 = ld4(q + c);
+  const float4 k4 = ld4(q + d + c);
+  const float4 v4 = ld4(q + 2 * d + c);
+  T* cown = cache[step] + ((size_t)r * L + layer) * 2 * d + h * dh;
+  if (on) {
+    st4(cown + c, k4);
+    st4(cown + d + c, v4);
+  }
+  const float scale = rsqrtf(static_cast<float>(dh));
+  float sc[8];
+  float mx = -FLT_MAX;
+  for (int p = 0; p <= step; ++p) {
+    float4 kk = k4;
+    if (p < step) kk = ld4(cache[p] + ((size_t)anc[(size_t)r * anc_stride + p] * L + layer) * 2 * d + h * dh + c);
+    float s = on ? q4.x * kk.x + q4.y * kk.y + q4.z * kk.z + q4.w * kk.w : 0.f;
+    s = warp_sum(s) * scale;
+    sc[p] = s;
+    mx = fmaxf(mx, s);
+  }
+  float den = 0.f;
+  for (int p = 0; p <= step; ++p) {
+    sc[p] = __expf(sc[p] - mx);
+    den += sc[p];
+  }
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int p = 0; p <= step; ++p) {
+    float4 vv = v4;
+    if (p < step) vv = ld4(cache[p] + ((size_t)anc[(size_t)r * anc_stride + p] * L + layer) * 2 * d + d + h * dh + c);
+    acc.x += sc[p] * vv.x, acc.y += sc[p] * vv.y, acc.z += sc[p] * vv.z, acc.w += sc[p] * vv.w;
+  }
+  if (on) {
+    const float inv = 1.f / den;
+    st4(out + (size_t)r * d + h * dh + c, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+  }
+}
+
+// h[r] += sum_j (ascending expert) y[slot[r][j]], float4 per thread (d % 4 == 0).
+__global__ void __launch_bounds__(256) moe_combine4_kernel(int rows, int k, int d, const float* __restrict__ yg,
+                                                           const int32_t* __restrict__ slot, float* __restrict__ h,
+                                                           int ldh) {
+  const int q = d / 4;
+  const long long n = (long long)rows * q;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(i / q), c = static_cast<int>(i % q) * 4;
+    float4 acc = __ldg(reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k] * d + c));
+    for (int j = 1; j < k; ++j) {
+      const float4 y = __ldg(reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k + j] * d + c));
+      acc.x += y.x, acc.y += y.y, acc.z += y.z, acc.w += y.w;
+    }
+    float4* hp = reinterpret_cast<float4*>(h + (size_t)r * ldh + c);
+    float4 hv = *hp;
+    hv.x += acc.x, hv.y += acc.y, hv.z += acc.z, hv.w += acc.w;
+    *hp = hv;
+  }
+}
+
 // Gate scores, top-k (stable: score+bias desc, ties -> lower id), selected ids
 // ascending, softmax over selected raw scores (nn.cpp:121-147). The gate input
 // RMSNorm(x) is recomputed here in fp32 from the fp32 residual stream so that
@@ -252,6 +411,113 @@ __global__ void __launch_bounds__(256) moe_route_kernel(int rows, int d, int E, 
     moe_route_row(r, d, E, k, x + (size_t)r * ldx, gain, sg, bias, sel, wts, counts, lane);
 }
 
+// Routing v2 (d % 4 == 0): warp per 2 rows, lane owns columns {128 i + 4 lane ..+3};
+// the gate is pre-multiplied by the RMSNorm gain (gg[e][c] = gain[c] * W_g[c][e])
+// so score_e = rsqrt(mean(x^2) + eps) * sum_c x_c gg[e][c] = RMSNorm(x) . W_g[:, e]
+// (nn.cpp:117-120). 64 partial sums per lane (2 rows x 32 expert slots) are
+// reduce-scattered with a 5-level butterfly (lane l ends with slots 2l, 2l+1),
+// then selection runs with lane = expert as above. Per-expert counts go
+// through a block histogram (one global atomic per expert per block).
+constexpr int kRoutePerWarp = 2;
+__device__ __forceinline__ void butterfly64(float (&v)[64], int lane) {
+#pragma unroll
+  for (int lvl = 0; lvl < 5; ++lvl) {
+    const int o = 16 >> lvl;
+    const int h = 32 >> lvl;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const float send = up ? v[i] : v[i + h];
+      const float keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 2) moe_route2_kernel(int rows, int d, int E, int k, const float* __restrict__ x,
+                                                            int ldx, const float* __restrict__ gg,
+                                                            const float* __restrict__ bias, int32_t* __restrict__ sel,
+                                                            float* __restrict__ wts, int32_t* __restrict__ counts) {
+  extern __shared__ float sg[];  // [E][d]
+  __shared__ int hist[32];
+  for (int i = threadIdx.x; i < E * d / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(sg)[i] = reinterpret_cast<const float4*>(gg)[i];
+  if (threadIdx.x < 32) hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  const float bias_l = lane < E ? bias[lane] : 0.f;
+  for (int r0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * kRoutePerWarp; r0 < rows;
+       r0 += gridDim.x * wpb * kRoutePerWarp) {
+    float p[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) p[i] = 0.f;
+    float ss0 = 0.f, ss1 = 0.f;
+    const bool has1 = r0 + 1 < rows;
+    const float* x0 = x + (size_t)r0 * ldx;
+    const float* x1 = x + (size_t)(has1 ? r0 + 1 : r0) * ldx;
+    for (int c = lane * 4; c < d; c += 128) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(x0 + c));
+      float4 b = __ldg(reinterpret_cast<const float4*>(x1 + c));
+      if (!has1) b = make_float4(0.f, 0.f, 0.f, 0.f);
+      ss0 += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+      ss1 += b.x * b.x + b.y * b.y + b.z * b.z + b.w * b.w;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        if (e < E) {
+          const float4 g = *reinterpret_cast<const float4*>(sg + (size_t)e * d + c);
+          p[e] += a.x * g.x + a.y * g.y + a.z * g.z + a.w * g.w;
+          p[32 + e] += b.x * g.x + b.y * g.y + b.z * g.z + b.w * g.w;
+        }
+      }
+    }
+    butterfly64(p, lane);
+    ss0 = warp_sum(ss0);
+    ss1 = warp_sum(ss1);
+#pragma unroll
+    for (int rr = 0; rr < kRoutePerWarp; ++rr) {
+      const int r = r0 + rr;
+      if (r >= rows) break;
+      const float inv = rsqrtf((rr ? ss1 : ss0) / d + 1e-6f);
+      // slot (rr, e) lives in lane rr*16 + e/2, element e&1
+      const float v0 = __shfl_sync(0xffffffffu, p[0], rr * 16 + (lane >> 1));
+      const float v1 = __shfl_sync(0xffffffffu, p[1], rr * 16 + (lane >> 1));
+      const float my = ((lane & 1) ? v1 : v0) * inv;  // raw gate score of expert `lane`
+      const float key = lane < E ? my + bias_l : -FLT_MAX;
+      bool taken = false;
+      uint32_t chosen = 0;
+      for (int j = 0; j < k; ++j) {  // stable top-k: (score + bias) desc, ties -> lower id (nn.cpp:127-136)
+        float v = taken ? -FLT_MAX : key;
+        int idx = lane < E && !taken ? lane : 1 << 30;
+        for (int o = 16; o > 0; o >>= 1) {
+          float v2 = __shfl_xor_sync(0xffffffffu, v, o);
+          int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+          if (v2 > v || (v2 == v && i2 < idx)) {
+            v = v2;
+            idx = i2;
+          }
+        }
+        if (lane == idx) taken = true;
+        chosen |= 1u << idx;
+      }
+      // softmax over the selected raw scores (nn.cpp:139-147); ids ascending
+      float mx = -FLT_MAX;
+      for (int e = 0; e < E; ++e)
+        if (chosen >> e & 1u) mx = fmaxf(mx, __shfl_sync(0xffffffffu, my, e));
+      float den = 0.f;
+      for (int e = 0; e < E; ++e)
+        if (chosen >> e & 1u) den += __expf(__shfl_sync(0xffffffffu, my, e) - mx);
+      if (lane < E && (chosen >> lane & 1u)) {
+        const int j = __popc(chosen & ((1u << lane) - 1u));
+        sel[(size_t)r * k + j] = lane;
+        wts[(size_t)r * k + j] = __expf(my - mx) / den;
+        atomicAdd(&hist[lane], 1);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < E && hist[threadIdx.x]) atomicAdd(&counts[threadIdx.x], hist[threadIdx.x]);
+}
+
 // Segment offsets padded to the GEMM expert tile (128 rows, 256 for the CTA-pair kernel); tile -> expert table.
 __global__ void moe_plan_kernel(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
                                 int32_t* n_mtiles, int tile_rows) {
@@ -330,6 +596,11 @@ inline int grid_for(long long n, int block, int cap = 148 * 32) {
 template <class T>
 void launch_features(const RecordsDev& r, const FeatureTables& t, T* out, int ldo, cudaStream_t s) {
   if (r.n <= 0) return;
+  const bool vec = t.d % 8 == 0 && ldo % 8 == 0 && (t.vid_only || (t.aid_dim % 8 == 0 && t.minor % 8 == 0));
+  if (vec) {
+    ORX_LAUNCH(features8_kernel<T><<<grid_for(r.n, 8, num_sms() * 8), 256, 0, s>>>(r, t, out, ldo));
+    return;
+  }
   ORX_LAUNCH(features_kernel<T><<<grid_for(r.n, 1, 148 * 16), 256, 0, s>>>(r, t, out, ldo));
 }
 template <class T>
@@ -367,14 +638,33 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L
                           const int32_t* anc, int anc_stride, T* out, cudaStream_t s) {
   if (rows <= 0) return;
   long long warps = (long long)rows * heads;
+  if ((d / heads) % 4 == 0 && d / heads <= 128 && d % 4 == 0) {
+    ORX_LAUNCH_CAT(PROF_DEC_SELF, dec_self_attn4_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(
+        rows, d, heads, step, layer, L, qkv, cache, anc, anc_stride, out));
+    return;
+  }
   ORX_LAUNCH_CAT(PROF_DEC_SELF, dec_self_attn_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(
       rows, d, heads, step, layer, L, qkv, cache, anc, anc_stride, out));
 }
 void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, const float* gain, const float* gate_t,
-                      const float* bias, int32_t* sel, float* wts, int32_t* counts, cudaStream_t s) {
+                      const float* gate_gain, const float* bias, int32_t* sel, float* wts, int32_t* counts,
+                      cudaStream_t s) {
   if (rows <= 0) return;
-  if (d > 32 * kRouteMaxPer) throw std::invalid_argument("moe routing supports d_model <= 2048");
+  if (E > 32) throw std::invalid_argument("moe routing supports at most 32 experts");
   const int smem = E * d * 4;
+  if (gate_gain && d % 4 == 0 && ldx % 4 == 0) {
+    static int set2 = 0;
+    if (smem > 48 * 1024 && smem > set2) {
+      cudaFuncSetAttribute(moe_route2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      set2 = smem;
+    }
+    const int per_block = 8 * kRoutePerWarp;
+    int blocks = std::min((rows + per_block - 1) / per_block, num_sms() * 2);
+    ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_route2_kernel<<<blocks, 256, smem, s>>>(rows, d, E, k, x, ldx, gate_gain, bias,
+                                                                               sel, wts, counts));
+    return;
+  }
+  if (d > 32 * kRouteMaxPer) throw std::invalid_argument("moe routing supports d_model <= 2048");
   static int set = 0;
   if (smem > 48 * 1024 && smem > set) {
     cudaFuncSetAttribute(moe_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -400,6 +690,11 @@ void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32
 void launch_moe_combine(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
                         cudaStream_t s) {
   if (rows <= 0) return;
+  if (d % 4 == 0 && ldh % 4 == 0) {
+    ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_combine4_kernel<<<grid_for((long long)rows * d / 4, 256, num_sms() * 8), 256, 0,
+                                                         s>>>(rows, k, d, yg, slot, h, ldh));
+    return;
+  }
   ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_combine_kernel<<<rows, 256, 0, s>>>(rows, k, d, yg, slot, h, ldh));
 }
 void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, cudaStream_t s) {

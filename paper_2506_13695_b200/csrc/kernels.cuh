@@ -61,8 +61,10 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int n
 
 // MoE (nn.cpp:117-172)
 // Routing reads the fp32 residual x and the pre-MoE RMSNorm gain (norm recomputed in fp32).
+// gate_gain [E][d] = gain[c] * W_g[c][e] selects the fast path (d % 4 == 0).
 void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, const float* gain, const float* gate_t,
-                      const float* bias, int32_t* sel, float* wts, int32_t* counts, cudaStream_t s);
+                      const float* gate_gain, const float* bias, int32_t* sel, float* wts, int32_t* counts,
+                      cudaStream_t s);
 void launch_moe_plan(int E, const int32_t* counts, int32_t* seg_cursor, int32_t* tile_expert, int max_tiles,
                      int32_t* n_mtiles, int tile_rows, cudaStream_t s);
 template <class T>

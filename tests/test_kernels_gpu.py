@@ -187,3 +187,41 @@ def test_gemm_fp32_simt(M, N, K):
     run_gemm(A, B, out=out, bias=b, resid=R, act=2, precision=0)
     want = _act(A @ B.t() + b, 2) + R
     _close(out, want, False)
+
+
+def _ref_topk_keys(logits, pscore, plex, k, lse):
+    """torch restatement of the candidate key (beam.cuh) and its top-k set,
+    on the kernel's own log-normaliser (so fp32 rounding of lse cannot reorder)."""
+    V = logits.shape[1]
+    sc = (pscore[:, None] + (logits - lse[:, None])).contiguous()
+    bits = sc.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    neg = bits >= 0x80000000
+    ordb = torch.where(neg, (~bits) & 0xFFFFFFFF, bits | 0x80000000)
+    low = 0xFFFFFFFF - (plex[:, None].to(torch.int64) * V + torch.arange(V, device=logits.device))
+    keys = (ordb << 32) | low  # unsigned order; flip the top bit for a signed torch sort
+    skeys = keys ^ (-(1 << 63))
+    return torch.topk(skeys, k, dim=1).values
+
+
+@pytest.mark.parametrize("V,k,ties", [(8192, 128, False), (8192, 512, False), (8192, 32, False), (1000, 100, False),
+                                      (8192, 128, True), (64, 16, False)])
+def test_row_topk(V, k, ties):
+    """Per-row log-softmax + top-k candidate keys (fast bisection path and the
+    radix fallback taken under massive exact ties) vs a torch restatement."""
+    rows = 300
+    g = torch.Generator(device="cuda").manual_seed(V + k)
+    logits = torch.randn(rows, V, device="cuda", generator=g) * 7.0
+    if ties:
+        logits = torch.round(logits / 8.0) * 8.0  # a handful of distinct values per row
+    pscore = torch.randn(rows, device="cuda", generator=g) * 3.0
+    plex = torch.randint(0, 100, (rows,), device="cuda", dtype=torch.int32, generator=g)
+    lse = torch.empty(rows, device="cuda")
+    cand = torch.empty(rows, k, device="cuda", dtype=torch.int64)
+    L = _lib()
+    L.check(L.lib().orx_debug_row_topk(rows, V, k, _ptr(logits), _ptr(pscore), _ptr(plex), _ptr(lse), _ptr(cand),
+                                       None))
+    torch.cuda.synchronize()
+    assert torch.allclose(lse, torch.logsumexp(logits, dim=1), rtol=1e-5, atol=1e-4)
+    want_top = _ref_topk_keys(logits, pscore, plex, k, lse)
+    got = torch.sort(cand ^ (-(1 << 63)), dim=1, descending=True).values
+    assert torch.equal(got, want_top)

@@ -193,6 +193,9 @@ int orx_debug_gemm(const orx_gemm_args* args, void* stream);
  * (0xFFFFFFFF - (plex[r] * V + i)), in unspecified order. */
 int orx_debug_row_topk(int32_t rows, int32_t V, int32_t k, const float* logits, const float* pscore,
                        const int32_t* plex, float* lse, uint64_t* cand, void* stream);
+/* Rows of the beam-pruning fast path that took its exact radix-select
+ * fallback since the last call (process-wide counter, reset on read). */
+int64_t orx_debug_topk_fallback_rows(void);
 
 /* Seeded synthetic users (synth_users.hpp). */
 int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,

@@ -95,6 +95,7 @@ SIGNATURES = [
                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("orx_debug_gemm", C.c_int, [C.POINTER(orx_gemm_args), _P]),
     ("orx_debug_row_topk", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
+    ("orx_debug_topk_fallback_rows", C.c_int64, []),
     ("orx_synth_batch_create", C.c_int, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                          C.POINTER(_P)]),
     ("orx_synth_batch_view", C.c_int, [_P, C.POINTER(orx_user_batch)]),

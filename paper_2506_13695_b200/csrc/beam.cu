@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cfloat>
 #include <stdexcept>
 
@@ -99,13 +100,17 @@ __global__ void __launch_bounds__(kRowThreads) row_topk_kernel(int V, int k_sel,
                                                                const float* __restrict__ pscore,
                                                                const int32_t* __restrict__ plex,
                                                                float* __restrict__ lse_out,
-                                                               uint64_t* __restrict__ cand) {
+                                                               uint64_t* __restrict__ cand,
+                                                               const int32_t* __restrict__ row_list) {
   extern __shared__ uint64_t keys[];  // [V]
   __shared__ uint32_t hist[256];
   __shared__ uint32_t bc[4];
   __shared__ float red[kRowThreads / 32];
   __shared__ uint32_t counter;
-  const int row = blockIdx.x;
+  // row_list: [0] = n, [1..n] = rows (fallback rows of row_topk_warp_kernel), grid-stride
+  const int n_rows = row_list ? row_list[0] : static_cast<int>(gridDim.x);
+  for (int li = blockIdx.x; li < n_rows; li += gridDim.x) {
+  const int row = row_list ? row_list[1 + li] : li;
   const float* lg = logits + (size_t)row * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // log-softmax normaliser (max-subtracted, generation.cpp:10-20)
@@ -146,168 +151,173 @@ __global__ void __launch_bounds__(kRowThreads) row_topk_kernel(int V, int k_sel,
       if (pos < static_cast<uint32_t>(k_sel)) out[pos] = key;
     }
   }
+  __syncthreads();
+  }
 }
 
-// Fast path (V <= 8192, k_sel < V, k_sel <= 1024): the row stays in registers
-// (32 per thread). Bisection on the fp32 score finds a threshold whose
-// candidate count lies in [k_sel, cap]; the candidates are sorted in shared
-// memory (bitonic) and the first k_sel keys written. Exact: the key order
-// is the same as row_topk_kernel's, so ties at the threshold are all kept
-// and resolved by the lexicographic part of the key. Rows where bisection
-// cannot isolate such a threshold (massive exact ties) take the radix path.
-constexpr int kTopkPer = 32;
-constexpr int kTopkCap = 2048;
+// Fast path: one warp per row, two streaming passes over the logits.
+//   pass 1: max, mean and variance of the row's logits
+//   pass 2: sum of exp (the log-softmax normaliser, generation.cpp:10-20) and
+//           every logit >= tx appended to its lane's 32-slot shared-memory
+//           segment, tx = the normal-quantile guess for ~2.5 k_sel survivors
+//           (retried with a moved tx if fewer than k_sel survive or a lane
+//           segment overflows)
+//   select: the survivors (<= 1024, 32 per lane in registers) are scored
+//           (parent + logit - lse) and bisected with 8 thresholds per step
+//           until exactly k_sel scores are >= tau; their keys are written.
+// Selecting by logit then by score is exact because the fp32 score is a
+// monotone function of the logit; the one case it cannot decide (a rejected
+// logit whose rounded score equals a selected one, or scores tied across the
+// k-th position) sends the row to the block radix-select kernel, so the set
+// is always identical to row_topk_kernel's. Outputs are unordered.
+constexpr int kWarpRows = 4;  // rows (warps) per block
+constexpr int kProbes = 8;
+__device__ unsigned long long g_topk_fallback_rows = 0;  // rows sent to the radix path (test hook)
 
-__device__ __forceinline__ float block_reduce_sum256(float v, float* red) {
-  v = warp_sum(v);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  float t = 0.f;
-#pragma unroll
-  for (int w = 0; w < kRowThreads / 32; ++w) t += red[w];
-  return t;
-}
-__device__ __forceinline__ float block_reduce_max256(float v, float* red) {
-  v = warp_max(v);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  float t = -FLT_MAX;
-#pragma unroll
-  for (int w = 0; w < kRowThreads / 32; ++w) t = fmaxf(t, red[w]);
-  return t;
+__device__ __forceinline__ float normal_upper_quantile(float p) {  // Abramowitz-Stegun 26.2.23
+  p = fminf(0.5f, fmaxf(p, 1e-7f));
+  const float t = sqrtf(-2.f * logf(p));
+  return t - (2.515517f + 0.802853f * t + 0.010328f * t * t) /
+                 (1.f + 1.432788f * t + 0.189269f * t * t + 0.001308f * t * t * t);
 }
 
-__global__ void __launch_bounds__(kRowThreads) row_topk_fast_kernel(int V, int k_sel, const float* __restrict__ logits,
-                                                                    const float* __restrict__ pscore,
-                                                                    const int32_t* __restrict__ plex,
-                                                                    float* __restrict__ lse_out,
-                                                                    uint64_t* __restrict__ cand) {
-  __shared__ uint64_t buf[kTopkCap];
-  __shared__ float red[kRowThreads / 32];
-  __shared__ uint32_t hist[256];
-  __shared__ uint32_t bc[4];
-  __shared__ uint32_t counter;
-  const int row = blockIdx.x, tid = threadIdx.x;
+template <int kLaneSlots>
+__global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows, int V, int k_sel,
+                                                                       const float* __restrict__ logits,
+                                                                       const float* __restrict__ pscore,
+                                                                       const int32_t* __restrict__ plex,
+                                                                       float* __restrict__ lse_out,
+                                                                       uint64_t* __restrict__ cand,
+                                                                       int32_t* __restrict__ fail) {
+  __shared__ float bx[kWarpRows][kLaneSlots * 32];
+  __shared__ int32_t bi[kWarpRows][kLaneSlots * 32];
+  __shared__ int32_t bn[kWarpRows][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int row = blockIdx.x * kWarpRows + w;
+  if (row >= rows) return;
   const float* lg = logits + (size_t)row * V;
-  float v[kTopkPer];
-  float mx = -FLT_MAX;
-#pragma unroll
-  for (int j = 0; j < kTopkPer; ++j) {
-    const int i = tid + kRowThreads * j;
-    v[j] = i < V ? __ldg(lg + i) : -FLT_MAX;
-    mx = fmaxf(mx, v[j]);
+  const float4* lg4 = reinterpret_cast<const float4*>(lg);
+  const int V4 = V >> 2;  // V % 4 == 0 (launch condition)
+  float mx = -FLT_MAX, s1 = 0.f, s2 = 0.f;
+  for (int i = lane; i < V4; i += 32) {
+    const float4 x = __ldg(lg4 + i);
+    mx = fmaxf(mx, fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
+    s1 += (x.x + x.y) + (x.z + x.w);
+    s2 += (x.x * x.x + x.y * x.y) + (x.z * x.z + x.w * x.w);
   }
-  mx = block_reduce_max256(mx, red);
-  float se = 0.f, s1 = 0.f, s2 = 0.f;
-#pragma unroll
-  for (int j = 0; j < kTopkPer; ++j)
-    if (tid + kRowThreads * j < V) {
-      se += __expf(v[j] - mx);
-      s1 += v[j] - mx;
-      s2 += (v[j] - mx) * (v[j] - mx);
-    }
-  se = block_reduce_sum256(se, red);
-  s1 = block_reduce_sum256(s1, red);
-  s2 = block_reduce_sum256(s2, red);
-  const float lse = mx + logf(se);  // log-softmax normaliser (generation.cpp:10-20)
-  const float ps = pscore[row];
-  // scores (the ranking quantity of the candidate key)
-  float smin = FLT_MAX;
-#pragma unroll
-  for (int j = 0; j < kTopkPer; ++j) {
-    v[j] = tid + kRowThreads * j < V ? ps + (v[j] - lse) : -FLT_MAX;
-    if (tid + kRowThreads * j < V) smin = fminf(smin, v[j]);
-  }
-  smin = -block_reduce_max256(-smin, red);
-  const float smax = ps + (mx - lse);
-  // bisection: count(score >= tau) in [k_sel, cap]
-  const int cap = min(kTopkCap, max(2 * k_sel, 256));
-  float lo = smin, hi = smax;  // count(lo) = V >= k_sel; count(hi) >= 1
+  mx = warp_max(mx);
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
   const float mean = s1 / V, sd = sqrtf(fmaxf(s2 / V - mean * mean, 0.f));
-  // first probe: normal upper quantile of the top (1.25 k_sel) / V fraction
-  // (Abramowitz-Stegun 26.2.23), scores assumed ~normal
-  const float pf = fminf(0.5f, 1.25f * k_sel / V);
-  const float t = sqrtf(-2.f * logf(pf));
-  const float z = t - (2.515517f + 0.802853f * t + 0.010328f * t * t) /
-                          (1.f + 1.432788f * t + 0.189269f * t * t + 0.001308f * t * t * t);
-  float tau = smax + mean + z * sd;
-  tau = fminf(fmaxf(tau, lo), hi);
-  int count = -1;
-  bool found = false;
-  for (int it = 0; it < 48; ++it) {
-    int c = 0;
+  // survivors: ~2.5 k_sel, but on average at most half of the slots per lane
+  const float target = fminf(2.5f * k_sel, 16.f * kLaneSlots);
+  float tx = fminf(mean + normal_upper_quantile(target / V) * sd, mx);
+  float* sx = bx[w] + lane * kLaneSlots;
+  int32_t* si = bi[w] + lane * kLaneSlots;
+  float se = 0.f, rej = -FLT_MAX;
+  int n = 0, total = 0;
+  bool ok = false;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    n = 0;
+    rej = -FLT_MAX;
+    bool over = false;
+    for (int i = lane; i < V4; i += 32) {
+      const float4 x = __ldg(lg4 + i);
+      if (attempt == 0) se += (__expf(x.x - mx) + __expf(x.y - mx)) + (__expf(x.z - mx) + __expf(x.w - mx));
+      const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-    for (int j = 0; j < kTopkPer; ++j) c += v[j] >= tau;
-    count = static_cast<int>(block_reduce_sum256(static_cast<float>(c), red));
-    if (count >= k_sel && count <= cap) {
-      found = true;
-      break;
-    }
-    if (count < k_sel) hi = tau;
-    else lo = tau;
-    const float nt = 0.5f * (lo + hi);
-    if (nt == lo || nt == hi) break;
-    tau = nt;
-  }
-  if (tid == 0) {
-    lse_out[row] = lse;
-    counter = 0;
-  }
-  const uint32_t lbase = static_cast<uint32_t>(plex[row]) * static_cast<uint32_t>(V);
-  uint64_t* out = cand + (size_t)row * k_sel;
-  if (found) {
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kTopkPer; ++j) {
-      const int i = tid + kRowThreads * j;
-      const bool take = v[j] >= tau;
-      const unsigned m = __ballot_sync(0xffffffffu, take);
-      uint32_t base = 0;
-      if ((tid & 31) == 0 && m) base = atomicAdd(&counter, __popc(m));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (take)
-        buf[base + __popc(m & ((1u << (tid & 31)) - 1u))] =
-            (static_cast<uint64_t>(ord_f32(v[j])) << 32) | (0xFFFFFFFFu - (lbase + static_cast<uint32_t>(i)));
-    }
-    __syncthreads();
-    int np = 256;
-    while (np < count) np <<= 1;
-    for (int i = count + tid; i < np; i += kRowThreads) buf[i] = 0;
-    __syncthreads();
-    for (int size = 2; size <= np; size <<= 1) {
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int i = tid; i < np / 2; i += kRowThreads) {
-          const int lo_i = 2 * i - (i & (stride - 1));
-          const int hi_i = lo_i + stride;
-          const bool desc = (lo_i & size) == 0;
-          const uint64_t x = buf[lo_i], y = buf[hi_i];
-          if ((x < y) == desc) {
-            buf[lo_i] = y;
-            buf[hi_i] = x;
+      for (int e = 0; e < 4; ++e) {
+        if (xs[e] >= tx) {
+          if (n < kLaneSlots) {
+            sx[n] = xs[e];
+            si[n] = 4 * i + e;
+          } else {
+            over = true;
           }
+          ++n;
+        } else {
+          rej = fmaxf(rej, xs[e]);
         }
-        __syncthreads();
       }
     }
-    for (int i = tid; i < k_sel; i += kRowThreads) out[i] = buf[i];
-    return;
-  }
-  // fallback: radix select over the keys (rare: massive exact ties)
-  __syncthreads();
-  auto key_of = [&](int i) -> uint64_t {
-    const float sc = ps + (__ldg(lg + i) - lse);
-    return (static_cast<uint64_t>(ord_f32(sc)) << 32) | (0xFFFFFFFFu - (lbase + static_cast<uint32_t>(i)));
-  };
-  uint64_t thr = block_kth_largest<kRowThreads>(V, k_sel, key_of, hist, bc);
-  __syncthreads();
-  for (int i = tid; i < V; i += kRowThreads) {
-    const uint64_t key = key_of(i);
-    if (key >= thr) {
-      uint32_t pos = atomicAdd(&counter, 1u);
-      if (pos < static_cast<uint32_t>(k_sel)) out[pos] = key;
+    total = __reduce_add_sync(0xffffffffu, n);
+    over = __any_sync(0xffffffffu, over);
+    if (total >= k_sel && !over) {
+      ok = true;
+      break;
     }
+    // too few survivors: lower tx; a lane overflowed: raise it
+    tx = total < k_sel ? tx - 0.75f * sd : tx + 0.25f * sd;
+    if (!(sd > 0.f)) break;
+  }
+  se = warp_sum(se);
+  const float lse = mx + logf(se);
+  const float ps = pscore[row];
+  if (lane == 0) lse_out[row] = lse;
+  uint64_t* out = cand + (size_t)row * k_sel;
+  const uint32_t lbase = static_cast<uint32_t>(plex[row]) * static_cast<uint32_t>(V);
+  if (ok) {
+    bn[w][lane] = n;
+    __syncwarp();
+    // lane owns slot `lane` of every segment j (conflict-free transposed read)
+    float c[kLaneSlots];
+#pragma unroll
+    for (int j = 0; j < kLaneSlots; ++j)
+      c[j] = lane < bn[w][j] ? ps + (bx[w][j * kLaneSlots + lane] - lse) : -FLT_MAX;
+    float lo = ps + (tx - lse), hi = ps + (mx - lse);  // count(>= lo) = total >= k_sel
+    bool hi_open = true, found = total == k_sel;
+    float tau = lo;
+    for (int it = 0; it < 16 && !found; ++it) {
+      float pr[kProbes];
+#pragma unroll
+      for (int q = 0; q < kProbes; ++q)
+        pr[q] = hi_open ? (q == kProbes - 1 ? hi : lo + (hi - lo) * (float)(q + 1) / (float)kProbes)
+                        : lo + (hi - lo) * (float)(q + 1) / (float)(kProbes + 1);
+      int cq[kProbes];
+#pragma unroll
+      for (int q = 0; q < kProbes; ++q) {
+        int m = 0;
+#pragma unroll
+        for (int j = 0; j < kLaneSlots; ++j) m += c[j] >= pr[q];
+        cq[q] = __reduce_add_sync(0xffffffffu, m);
+      }
+      float nlo = lo, nhi = hi;
+      bool nopen = hi_open, hit = false, got_hi = false;
+#pragma unroll
+      for (int q = 0; q < kProbes; ++q) {
+        if (cq[q] > k_sel) nlo = pr[q];
+        if (cq[q] == k_sel && !hit) tau = pr[q], hit = true;
+        if (cq[q] < k_sel && !got_hi) nhi = pr[q], nopen = false, got_hi = true;
+      }
+      if (hit) {
+        found = true;
+        break;
+      }
+      if (nlo == lo && nhi == hi && nopen == hi_open) break;  // scores tied across the k-th position
+      lo = nlo, hi = nhi, hi_open = nopen;
+      if (!(hi > lo)) break;
+    }
+    // a rejected logit must score strictly below every selected one
+    const float rej_score = ps + (warp_max(rej) - lse);
+    if (found && rej_score < tau) {
+      int pos = 0;
+#pragma unroll
+      for (int j = 0; j < kLaneSlots; ++j) {
+        const bool take = c[j] >= tau;
+        const unsigned m = __ballot_sync(0xffffffffu, take);
+        if (take) {
+          const uint32_t idx = static_cast<uint32_t>(bi[w][j * kLaneSlots + lane]);
+          out[pos + __popc(m & ((1u << lane) - 1u))] =
+              (static_cast<uint64_t>(ord_f32(c[j])) << 32) | (0xFFFFFFFFu - (lbase + idx));
+        }
+        pos += __popc(m);
+      }
+      return;
+    }
+  }
+  if (lane == 0) {
+    fail[1 + atomicAdd(&fail[0], 1)] = row;
+    atomicAdd(&g_topk_fallback_rows, 1ull);
   }
 }
 
@@ -387,7 +397,7 @@ __global__ void beam_init_kernel(int users, BeamState st) {
 }  // namespace
 
 void launch_row_topk(int rows, int V, int k_sel, const float* logits, const float* parent_score,
-                     const int32_t* parent_lexrank, float* lse, uint64_t* cand, cudaStream_t s) {
+                     const int32_t* parent_lexrank, float* lse, uint64_t* cand, int32_t* fail, cudaStream_t s) {
   if (rows <= 0) return;
   size_t smem = static_cast<size_t>(V) * 8;
   static size_t set = 0;
@@ -396,13 +406,33 @@ void launch_row_topk(int rows, int V, int k_sel, const float* logits, const floa
     set = smem;
   }
   ProfScope ps(PROF_BEAM, s, 0.0, double(rows) * V * 4);
-  if (V <= kRowThreads * kTopkPer && k_sel < V && k_sel <= 1024) {
-    row_topk_fast_kernel<<<rows, kRowThreads, 0, s>>>(V, k_sel, logits, parent_score, parent_lexrank, lse, cand);
-    ++launch_counter();
+  if (fail && V % 4 == 0 && k_sel < V && k_sel <= 1024) {
+    cudaMemsetAsync(fail, 0, sizeof(int32_t), s);
+    const int blocks = (rows + kWarpRows - 1) / kWarpRows;
+    if (k_sel <= 192)
+      row_topk_warp_kernel<32><<<blocks, 32 * kWarpRows, 0, s>>>(rows, V, k_sel, logits, parent_score, parent_lexrank,
+                                                                 lse, cand, fail);
+    else
+      row_topk_warp_kernel<64><<<blocks, 32 * kWarpRows, 0, s>>>(rows, V, k_sel, logits, parent_score, parent_lexrank,
+                                                                 lse, cand, fail);
+    // rows the warp kernel could not decide (usually none): exact radix select
+    row_topk_kernel<<<std::min(rows, 2 * num_sms()), kRowThreads, smem, s>>>(V, k_sel, logits, parent_score,
+                                                                            parent_lexrank, lse, cand, fail);
+    launch_counter() += 2;
     return;
   }
-  row_topk_kernel<<<rows, kRowThreads, smem, s>>>(V, k_sel, logits, parent_score, parent_lexrank, lse, cand);
+  row_topk_kernel<<<rows, kRowThreads, smem, s>>>(V, k_sel, logits, parent_score, parent_lexrank, lse, cand, nullptr);
   ++launch_counter();
+}
+
+unsigned long long topk_fallback_rows(bool reset) {
+  unsigned long long v = 0;
+  cudaMemcpyFromSymbol(&v, g_topk_fallback_rows, sizeof(v));
+  if (reset) {
+    unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_topk_fallback_rows, &z, sizeof(z));
+  }
+  return v;
 }
 
 void launch_beam_merge(int users, int n_live, int k_sel, int n_new, int V, int L, int step, const uint64_t* cand,

@@ -24,8 +24,13 @@ struct BeamState {  // live beams of one step, row r = user * n_live + beam
 };
 
 // Per row: lse = logsumexp(logits), then the top k_sel candidate keys.
+// fail: device workspace of rows + 1 ints (fast path's undecided rows); NULL
+// selects the block radix-select kernel for every row.
 void launch_row_topk(int rows, int V, int k_sel, const float* logits, const float* parent_score,
-                     const int32_t* parent_lexrank, float* lse, uint64_t* cand, cudaStream_t s);
+                     const int32_t* parent_lexrank, float* lse, uint64_t* cand, int32_t* fail, cudaStream_t s);
+
+// Rows of the fast top-k kernel that fell back to the radix select since the last reset.
+unsigned long long topk_fallback_rows(bool reset);
 
 // Per user: top n_new of n_live * k_sel candidates, sorted; builds the next
 // BeamState (codes, scores, lexranks, ancestors).

@@ -322,10 +322,19 @@ int orx_debug_row_topk(int32_t rows, int32_t V, int32_t k, const float* logits, 
                        const int32_t* plex, float* lse, uint64_t* cand, void* stream) {
   return guarded([&] {
     if (rows < 0 || V < 1 || k < 1 || k > V) throw orx::InvalidArgument("row_topk: bad sizes");
-    orx::launch_row_topk(rows, V, k, logits, pscore, plex, lse, cand, static_cast<cudaStream_t>(stream));
+    int32_t* fail = nullptr;
+    if (cudaMalloc(&fail, (static_cast<size_t>(rows) + 1) * sizeof(int32_t)) != cudaSuccess)
+      throw orx::RuntimeError("CUDA: workspace allocation failed");
+    orx::launch_row_topk(rows, V, k, logits, pscore, plex, lse, cand, fail, static_cast<cudaStream_t>(stream));
+    cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    cudaFree(fail);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) throw orx::RuntimeError(std::string("CUDA: ") + cudaGetErrorString(err));
   });
+}
+
+int64_t orx_debug_topk_fallback_rows(void) {
+  return static_cast<int64_t>(orx::topk_fallback_rows(true));
 }
 
 int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,

@@ -364,6 +364,7 @@ class EngineT final : public Engine {
     const int ksel = std::min(maxW_, c.codebook_size);
     cand_ = ar_.alloc<uint64_t>(static_cast<size_t>(Rd_) * ksel);
     lse_ = ar_.alloc<float>(Rd_);
+    topk_fail_ = ar_.alloc<int32_t>(Rd_ + 1);
     for (int s = 0; s < 2; ++s) {
       bs_[s].codes = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
       bs_[s].score = ar_.alloc<float>(Rd_);
@@ -814,7 +815,7 @@ class EngineT final : public Engine {
       gk.fixed_len = Tn;
       decode_step(step, rows, U, gq, gk, bs_[cur].codes, L, bs_[cur].anc, L, n_live);
       const int ksel = std::min(width, V);
-      launch_row_topk(rows, V, ksel, logits_, bs_[cur].score, bs_[cur].lexrank, lse_, cand_, st_);
+      launch_row_topk(rows, V, ksel, logits_, bs_[cur].score, bs_[cur].lexrank, lse_, cand_, topk_fail_, st_);
       const int n_new = static_cast<int>(std::min<int64_t>(width, static_cast<int64_t>(n_live) * V));
       launch_beam_merge(U, n_live, ksel, n_new, V, L, step, cand_, logits_, lse_, bs_[cur], bs_[cur ^ 1], st_);
       cur ^= 1;
@@ -954,6 +955,7 @@ class EngineT final : public Engine {
   std::vector<T*> cache_;
   T** cache_ptrs_ = nullptr;
   uint64_t* cand_ = nullptr;
+  int32_t* topk_fail_ = nullptr;
   BeamState bs_[2];
   int32_t *tf_anc_, *tf_codes_, *grp_start_, *grp_len_, *grp_kstart_;
   int32_t *sel_ = nullptr, *slot_ = nullptr, *counts_ = nullptr, *cursor_ = nullptr, *tile_expert_ = nullptr,

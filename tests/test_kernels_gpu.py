@@ -218,9 +218,16 @@ def test_row_topk(V, k, ties):
     lse = torch.empty(rows, device="cuda")
     cand = torch.empty(rows, k, device="cuda", dtype=torch.int64)
     L = _lib()
+    L.lib().orx_debug_topk_fallback_rows()
     L.check(L.lib().orx_debug_row_topk(rows, V, k, _ptr(logits), _ptr(pscore), _ptr(plex), _ptr(lse), _ptr(cand),
                                        None))
     torch.cuda.synchronize()
+    fallbacks = L.lib().orx_debug_topk_fallback_rows()
+    print(f"V={V} k={k} ties={ties}: {fallbacks}/{rows} rows took the radix fallback")
+    if ties:
+        assert fallbacks > 0  # the exact-tie path is exercised
+    elif V == 8192 and k <= 512:
+        assert fallbacks <= rows // 20  # the fast path handles ordinary rows
     assert torch.allclose(lse, torch.logsumexp(logits, dim=1), rtol=1e-5, atol=1e-4)
     want_top = _ref_topk_keys(logits, pscore, plex, k, lse)
     got = torch.sort(cand ^ (-(1 << 63)), dim=1, descending=True).values

@@ -170,7 +170,6 @@ __global__ void __launch_bounds__(kRowThreads) row_topk_kernel(int V, int k_sel,
 // logit whose rounded score equals a selected one, or scores tied across the
 // k-th position) sends the row to the block radix-select kernel, so the set
 // is always identical to row_topk_kernel's. Outputs are unordered.
-constexpr int kWarpRows = 4;  // rows (warps) per block
 constexpr int kProbes = 8;
 __device__ unsigned long long g_topk_fallback_rows = 0;  // rows sent to the radix path (test hook)
 
@@ -181,7 +180,7 @@ __device__ __forceinline__ float normal_upper_quantile(float p) {  // Abramowitz
                  (1.f + 1.432788f * t + 0.189269f * t * t + 0.001308f * t * t * t);
 }
 
-template <int kLaneSlots>
+template <int kLaneSlots, int kWarpRows = 128 / kLaneSlots>  // rows (warps) per block: 33 KB smem
 __global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows, int V, int k_sel,
                                                                        const float* __restrict__ logits,
                                                                        const float* __restrict__ pscore,
@@ -408,13 +407,12 @@ void launch_row_topk(int rows, int V, int k_sel, const float* logits, const floa
   ProfScope ps(PROF_BEAM, s, 0.0, double(rows) * V * 4);
   if (fail && V % 4 == 0 && k_sel < V && k_sel <= 1024) {
     cudaMemsetAsync(fail, 0, sizeof(int32_t), s);
-    const int blocks = (rows + kWarpRows - 1) / kWarpRows;
     if (k_sel <= 192)
-      row_topk_warp_kernel<32><<<blocks, 32 * kWarpRows, 0, s>>>(rows, V, k_sel, logits, parent_score, parent_lexrank,
-                                                                 lse, cand, fail);
+      row_topk_warp_kernel<32><<<(rows + 3) / 4, 128, 0, s>>>(rows, V, k_sel, logits, parent_score, parent_lexrank,
+                                                              lse, cand, fail);
     else
-      row_topk_warp_kernel<64><<<blocks, 32 * kWarpRows, 0, s>>>(rows, V, k_sel, logits, parent_score, parent_lexrank,
-                                                                 lse, cand, fail);
+      row_topk_warp_kernel<64><<<(rows + 1) / 2, 64, 0, s>>>(rows, V, k_sel, logits, parent_score, parent_lexrank,
+                                                             lse, cand, fail);
     // rows the warp kernel could not decide (usually none): exact radix select
     row_topk_kernel<<<std::min(rows, 2 * num_sms()), kRowThreads, smem, s>>>(V, k_sel, logits, parent_score,
                                                                             parent_lexrank, lse, cand, fail);

@@ -133,6 +133,19 @@ int orx_engine_create(const orx_weights* w, int device, int precision, int32_t m
                       orx_engine** out);
 void orx_engine_destroy(orx_engine* e);
 
+/* Expert parallelism over NCCL (NVLink), SURVEY.md §8(e) / BASELINE config 4:
+ * ep_world engines (one process per GPU) each hold n_experts / ep_world
+ * experts of every MoE layer; MoE layers exchange (token, expert) rows with
+ * NCCL send/recv. Rank 0 creates a fresh id per engine (orx_ep_unique_id;
+ * an id bootstraps one communicator only) and every rank receives it out of band (e.g. torch.distributed broadcast). All ranks must
+ * then call the same sequence of orx_encode / orx_beam_search /
+ * orx_score_prefixes / orx_next_logits (each with its own users; widths
+ * equal). Results are bitwise identical to a replica engine's. */
+#define ORX_EP_ID_BYTES 128
+int orx_ep_unique_id(uint8_t id_out[ORX_EP_ID_BYTES]);
+int orx_engine_create_ep(const orx_weights* w, int device, int precision, int32_t max_users, int32_t max_width,
+                         const uint8_t id[ORX_EP_ID_BYTES], int32_t ep_rank, int32_t ep_world, orx_engine** out);
+
 /* z_out (host, optional): [n_users * enc_seq_len * d_model] fp32. */
 int orx_encode(orx_engine* e, const orx_user_batch* batch, float* z_out);
 /* Teacher-forced logits for n queries over caller-supplied encodings:
@@ -196,6 +209,15 @@ int orx_debug_row_topk(int32_t rows, int32_t V, int32_t k, const float* logits, 
 /* Rows of the beam-pruning fast path that took its exact radix-select
  * fallback since the last call (process-wide counter, reset on read). */
 int64_t orx_debug_topk_fallback_rows(void);
+
+/* Host plan of one expert-parallel exchange (csrc/ep_plan.hpp), for the CPU
+ * tests: counts [world * n_experts]; outputs send/recv counts and offsets
+ * [world] each, tab [world * (n_experts / world) * 3] (src row, dst row,
+ * count) and tiles [max_tiles] (local expert per grouped-GEMM tile, -1 past
+ * the end); returns the number of tiles in use via n_tiles. */
+int orx_debug_ep_plan(int32_t world, int32_t rank, int32_t n_experts, const int32_t* counts, int32_t tile,
+                      int32_t max_tiles, int64_t* send_cnt, int64_t* send_off, int64_t* recv_cnt, int64_t* recv_off,
+                      int32_t* tab, int32_t* tiles, int32_t* n_tiles);
 
 /* Seeded synthetic users (synth_users.hpp). */
 int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,

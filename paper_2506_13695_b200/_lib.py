@@ -82,6 +82,9 @@ SIGNATURES = [
     ("orx_validate_batch", C.c_int, [C.POINTER(orx_config), C.POINTER(orx_user_batch)]),
     ("orx_engine_create", C.c_int, [_P, C.c_int, C.c_int, C.c_int32, C.c_int32, C.POINTER(_P)]),
     ("orx_engine_destroy", None, [_P]),
+    ("orx_ep_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
+    ("orx_engine_create_ep", C.c_int, [_P, C.c_int, C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32,
+                                       C.c_int32, C.POINTER(_P)]),
     ("orx_encode", C.c_int, [_P, C.POINTER(orx_user_batch), _F32P]),
     ("orx_next_logits", C.c_int, [_P, _F32P, C.c_int32, C.c_int32, _I32P, _I32P, _I32P, _F32P]),
     ("orx_score_prefixes", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, _I32P, _I32P, _I32P, _F32P]),
@@ -96,6 +99,9 @@ SIGNATURES = [
     ("orx_debug_gemm", C.c_int, [C.POINTER(orx_gemm_args), _P]),
     ("orx_debug_row_topk", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
     ("orx_debug_topk_fallback_rows", C.c_int64, []),
+    ("orx_debug_ep_plan", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _I32P, C.c_int32, C.c_int32,
+                                    C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int64), _I32P, _I32P, _I32P]),
     ("orx_synth_batch_create", C.c_int, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                          C.POINTER(_P)]),
     ("orx_synth_batch_view", C.c_int, [_P, C.POINTER(orx_user_batch)]),

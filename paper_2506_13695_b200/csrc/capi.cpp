@@ -7,6 +7,7 @@
 
 #include "../../include/orx.h"
 #include "engine.hpp"
+#include "ep_plan.hpp"
 #include "beam.cuh"
 #include "gemm.cuh"
 #include "model.hpp"
@@ -181,6 +182,31 @@ int orx_engine_create(const orx_weights* w, int device, int precision, int32_t m
   });
 }
 
+int orx_ep_unique_id(uint8_t id_out[ORX_EP_ID_BYTES]) {
+  return guarded([&] {
+    need(id_out, "id_out");
+    orx::nccl_unique_id(id_out);
+  });
+}
+
+int orx_engine_create_ep(const orx_weights* w, int device, int precision, int32_t max_users, int32_t max_width,
+                         const uint8_t id[ORX_EP_ID_BYTES], int32_t ep_rank, int32_t ep_world, orx_engine** out) {
+  return guarded([&] {
+    need(w, "weights");
+    need(out, "out");
+    need(id, "id");
+    orx::EpConfig ep;
+    ep.rank = ep_rank;
+    ep.world = ep_world;
+    memcpy(ep.unique_id, id, ORX_EP_ID_BYTES);
+    auto e = std::make_unique<orx_engine>();
+    e->e = orx::Engine::create(w->w, device, precision, max_users, max_width, &ep);
+    e->w = &w->w;
+    e->cfg = w->w.cfg;
+    *out = e.release();
+  });
+}
+
 void orx_engine_destroy(orx_engine* e) { delete e; }
 
 int orx_encode(orx_engine* e, const orx_user_batch* batch, float* z_out) {
@@ -335,6 +361,24 @@ int orx_debug_row_topk(int32_t rows, int32_t V, int32_t k, const float* logits, 
 
 int64_t orx_debug_topk_fallback_rows(void) {
   return static_cast<int64_t>(orx::topk_fallback_rows(true));
+}
+
+int orx_debug_ep_plan(int32_t world, int32_t rank, int32_t n_experts, const int32_t* counts, int32_t tile,
+                      int32_t max_tiles, int64_t* send_cnt, int64_t* send_off, int64_t* recv_cnt, int64_t* recv_off,
+                      int32_t* tab, int32_t* tiles, int32_t* n_tiles) {
+  return guarded([&] {
+    need(counts, "counts");
+    need(tab, "tab");
+    need(tiles, "tiles");
+    const orx::EpPlan pl = orx::ep_plan(world, rank, n_experts, counts, tile, max_tiles, tab, tiles);
+    for (int p = 0; p < world; ++p) {
+      if (send_cnt) send_cnt[p] = pl.send_cnt[p];
+      if (send_off) send_off[p] = pl.send_off[p];
+      if (recv_cnt) recv_cnt[p] = pl.recv_cnt[p];
+      if (recv_off) recv_off[p] = pl.recv_off[p];
+    }
+    if (n_tiles) *n_tiles = pl.n_tiles;
+  });
 }
 
 int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,

@@ -11,6 +11,7 @@
 //                 row log-softmax + top-k -> per-user merge, depth times.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -22,6 +23,7 @@
 #include "attention.cuh"
 #include "beam.cuh"
 #include "engine.hpp"
+#include "ep_plan.hpp"
 #include "gemm.cuh"
 #include "kernels.cuh"
 
@@ -36,6 +38,13 @@ namespace {
     cudaError_t e__ = (x);                                                                         \
     if (e__ != cudaSuccess) throw RuntimeError(std::string("CUDA: ") + cudaGetErrorString(e__) +  \
                                                " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+#define NCCL_CHECK(x)                                                                                      \
+  do {                                                                                                     \
+    ncclResult_t r__ = (x);                                                                                \
+    if (r__ != ncclSuccess) throw RuntimeError(std::string("NCCL: ") + ncclGetErrorString(r__) + " at " + \
+                                               __FILE__ + ":" + std::to_string(__LINE__));                 \
   } while (0)
 
 inline int rup(int x, int m) { return (x + m - 1) / m * m; }
@@ -117,10 +126,24 @@ class EngineT final : public Engine {
   static constexpr int kMoeTile = kBf16 ? 256 : 128;
 
  public:
-  EngineT(const HostWeights& hw, int device, int max_users, int max_width)
+  EngineT(const HostWeights& hw, int device, int max_users, int max_width, const EpConfig* ep)
       : cfg_(hw.cfg), dev_(device), maxU_(max_users), maxW_(max_width) {
     CUDA_CHECK(cudaSetDevice(dev_));
     CUDA_CHECK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    El_ = cfg_.moe_enabled ? cfg_.n_experts : 0;
+    if (ep && ep->world > 1) {
+      require(cfg_.moe_enabled, "expert parallelism needs a MoE config");
+      require(ep->rank >= 0 && ep->rank < ep->world, "expert-parallel rank outside the world");
+      require(cfg_.n_experts % ep->world == 0, "expert count must divide evenly over the expert-parallel ranks");
+      ep_rank_ = ep->rank;
+      ep_world_ = ep->world;
+      El_ = cfg_.n_experts / ep_world_;
+      e0_ = ep_rank_ * El_;
+      ncclUniqueId id;
+      static_assert(sizeof(id.internal) == 128, "ncclUniqueId size");
+      memcpy(id.internal, ep->unique_id, 128);
+      NCCL_CHECK(ncclCommInitRank(&comm_, ep_world_, id, ep_rank_));
+    }
     require(max_users >= 1 && max_width >= 1, "engine capacity must be positive");
     require(cfg_.n_code_layers <= 8, "n_code_layers above 8 is not supported");
     require(!cfg_.moe_enabled || cfg_.n_experts <= 32, "more than 32 experts is not supported");
@@ -136,6 +159,8 @@ class EngineT final : public Engine {
   ~EngineT() override {
     cudaSetDevice(dev_);
     cudaStreamSynchronize(st_);
+    if (comm_) ncclCommDestroy(comm_);
+    if (h_ep_) cudaFreeHost(h_ep_);
     if (host_stage_) cudaFreeHost(host_stage_);
     if (host_out_) cudaFreeHost(host_out_);
     cudaStreamDestroy(st_);
@@ -182,7 +207,7 @@ class EngineT final : public Engine {
     return L;
   }
   MoeW pack_moe(const HostWeights& hw, const std::string& n, const std::string& gain_name) {
-    const int d = cfg_.d_model, E = cfg_.n_experts, h = expert_hidden(cfg_);
+    const int d = cfg_.d_model, E = cfg_.n_experts, El = El_, h = expert_hidden(cfg_);
     MoeW m;
     const Tensor& g = hw.get(n + ".gate.w");  // (d, E)
     std::vector<float> gt(static_cast<size_t>(E) * d);
@@ -195,10 +220,13 @@ class EngineT final : public Engine {
     m.gate_gain = upload_f32(gt.data(), gt.size());
     m.bias = up(hw, n + ".routing_bias");
     const int dp = rup(d, 8), hp = rup(h, 8);
-    auto ex = [&](int e, const char* w) { return hw.get(n + ".expert" + std::to_string(e) + "." + w + ".w"); };
+    // this rank's experts only (all of them without expert parallelism): local e -> global e0_ + e
+    auto ex = [&](int e, const char* w) {
+      return hw.get(n + ".expert" + std::to_string(e0_ + e) + "." + w + ".w");
+    };
     if (kBf16) {
-      std::vector<T> w13(static_cast<size_t>(E) * 2 * h * dp, to_t<T>(0.f));
-      for (int e = 0; e < E; ++e) {
+      std::vector<T> w13(static_cast<size_t>(El) * 2 * h * dp, to_t<T>(0.f));
+      for (int e = 0; e < El; ++e) {
         const Tensor& w1 = ex(e, "w1");
         const Tensor& w3 = ex(e, "w3");
         for (int j = 0; j < h; ++j) {
@@ -216,8 +244,8 @@ class EngineT final : public Engine {
       m.w13 = p;
     } else {
       for (int which = 0; which < 2; ++which) {
-        std::vector<T> w(static_cast<size_t>(E) * h * dp, to_t<T>(0.f));
-        for (int e = 0; e < E; ++e) {
+        std::vector<T> w(static_cast<size_t>(El) * h * dp, to_t<T>(0.f));
+        for (int e = 0; e < El; ++e) {
           const Tensor& t = ex(e, which == 0 ? "w1" : "w3");
           for (int j = 0; j < h; ++j)
             for (int k = 0; k < d; ++k) w[((size_t)e * h + j) * dp + k] = to_t<T>(t.data[(size_t)k * h + j]);
@@ -227,8 +255,8 @@ class EngineT final : public Engine {
         (which == 0 ? m.w13 : m.w3) = p;
       }
     }
-    std::vector<T> w2(static_cast<size_t>(E) * d * hp, to_t<T>(0.f));
-    for (int e = 0; e < E; ++e) {
+    std::vector<T> w2(static_cast<size_t>(El) * d * hp, to_t<T>(0.f));
+    for (int e = 0; e < El; ++e) {
       const Tensor& t = ex(e, "w2");  // (h, d)
       for (int k = 0; k < h; ++k)
         for (int j = 0; j < d; ++j) w2[((size_t)e * d + j) * hp + k] = to_t<T>(t.data[(size_t)k * d + j]);
@@ -381,7 +409,10 @@ class EngineT final : public Engine {
     if (c.moe_enabled) {
       const int E = c.n_experts, k = c.experts_active, h = expert_hidden(c);
       const int64_t mrows = std::max(rows_enc, Rd_);
-      S_ = mrows * k + static_cast<int64_t>(E) * kMoeTile;
+      // grouped rows: this rank's own (token, expert) pairs, or with expert
+      // parallelism everything any rank may send here, + per-expert padding
+      const int64_t grouped = mrows * k * ep_world_;
+      S_ = grouped + static_cast<int64_t>(El_) * kMoeTile;
       max_tiles_ = static_cast<int>(S_ / kMoeTile + 1);
       sel_ = ar_.alloc<int32_t>(mrows * k);
       wts_ = ar_.alloc<float>(mrows * k);
@@ -398,6 +429,22 @@ class EngineT final : public Engine {
       if (!kBf16) {
         ga_ = ar_.alloc<float>(static_cast<size_t>(S_) * h);
         gb_ = ar_.alloc<float>(static_cast<size_t>(S_) * h);
+      }
+      if (ep_world_ > 1) {
+        send_cap_ = mrows * k;
+        recv_cap_ = grouped;
+        xs_ = ar_.alloc<T>(static_cast<size_t>(send_cap_) * d);
+        ws_ = ar_.alloc<float>(send_cap_);
+        yr_ = ar_.alloc<float>(static_cast<size_t>(send_cap_) * d);
+        xr_ = ar_.alloc<T>(static_cast<size_t>(recv_cap_) * d);
+        wr_ = ar_.alloc<float>(recv_cap_);
+        perm_ = ar_.alloc<int32_t>(recv_cap_);
+        ys_ = ar_.alloc<float>(static_cast<size_t>(recv_cap_) * d);
+        all_counts_ = ar_.alloc<int32_t>(static_cast<size_t>(ep_world_) * E);
+        // upload region [tab: world*El*3 | tile_expert: max_tiles | n_mtiles: 1]
+        const size_t up = static_cast<size_t>(ep_world_) * El_ * 3 + max_tiles_ + 1;
+        ep_up_ = ar_.alloc<int32_t>(up);
+        CUDA_CHECK(cudaMallocHost(&h_ep_, (static_cast<size_t>(ep_world_) * E + up) * sizeof(int32_t)));
       }
     }
     // user batch staging (device side); host side is pinned and grown on demand
@@ -692,18 +739,30 @@ class EngineT final : public Engine {
   // h += MoE(x)  (moe_forward, nn.cpp:117-172)
   void moe(const MoeW& m, const T* x, int rows, float* h, const float* norm_gain) {
     const orx_config& c = cfg_;
-    const int d = c.d_model, E = c.n_experts, k = c.experts_active, he = expert_hidden(c), hp = rup(he, 8);
+    const int d = c.d_model, E = c.n_experts, k = c.experts_active;
     CUDA_CHECK(cudaMemsetAsync(counts_, 0, E * sizeof(int32_t), st_));
     launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.gate_gain, m.bias, sel_, wts_, counts_, st_);
+    if (ep_world_ > 1) {
+      moe_ep(m, x, rows, h);
+      return;
+    }
     launch_moe_plan(E, counts_, cursor_, tile_expert_, max_tiles_, n_mtiles_, kMoeTile, st_);
     launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xg_, row_scale_, st_);
+    expert_ffn(m, static_cast<int>(S_), static_cast<long long>(rows) * k);
+    launch_moe_combine(rows, k, d, yg_, slot_, h, d, st_);
+  }
+
+  // Grouped expert FFNs over xg_ (expert per M tile: tile_expert_ / n_mtiles_):
+  // yg_ = row_scale * W2(silu(W1 x) * W3 x)  (swiglu, nn.cpp:75-86; weight nn.cpp:167-168)
+  void expert_ffn(const MoeW& m, int M, long long algo_rows) {
+    const orx_config& c = cfg_;
+    const int d = c.d_model, he = expert_hidden(c), hp = rup(he, 8);
     Grouped g;
     g.tile_expert = tile_expert_;
     g.n_mtiles = n_mtiles_;
-    g.n_groups = E;
+    g.n_groups = El_;
     g.tile_rows = kMoeTile;
-    g.algo_rows = static_cast<long long>(rows) * k;
-    const int M = static_cast<int>(S_);
+    g.algo_rows = algo_rows;
     if constexpr (kBf16) {
       Epi e1 = epi(hg_, hp, false);
       e1.swiglu = 1;
@@ -728,7 +787,7 @@ class EngineT final : public Engine {
       eb.out = gb_;
       gemm_f32(reinterpret_cast<const float*>(xg_), d, static_cast<const float*>(m.w3), rup(d, 8), M, he, rup(d, 8),
                eb, &g, st_);
-      launch_swiglu_mul(static_cast<long long>(S_) * he, ga_, gb_, reinterpret_cast<float*>(hg_), st_);
+      launch_swiglu_mul(static_cast<long long>(M) * he, ga_, gb_, reinterpret_cast<float*>(hg_), st_);
       Epi e2 = epi(yg_, d, true);
       e2.row_scale = row_scale_;
       e2.n_out = d;
@@ -736,7 +795,66 @@ class EngineT final : public Engine {
       g.b_rows_per_expert = d;
       gemm_f32(reinterpret_cast<const float*>(hg_), he, static_cast<const float*>(m.w2), hp, M, d, he, e2, &g, st_);
     }
-    launch_moe_combine(rows, k, d, yg_, slot_, h, d, st_);
+  }
+
+  // Expert-parallel MoE: every rank routes its own tokens,
+  // sends each (token, expert) row with its gate weight to the rank owning
+  // the expert (NCCL send/recv over NVLink), runs the grouped GEMMs of its
+  // local experts on what it received, and sends the weighted outputs back;
+  // the combine (ascending expert id) runs where the token lives. Every row
+  // goes through the same kernels as on one GPU, so the result is bitwise
+  // identical to the replica path. All ranks must run the same sequence of
+  // engine calls (same number of MoE layers), with any number of rows.
+  void moe_ep(const MoeW& m, const T* x, int rows, float* h) {
+    const orx_config& c = cfg_;
+    const int d = c.d_model, E = c.n_experts, k = c.experts_active, W = ep_world_, El = El_;
+    const ncclDataType_t dt = kBf16 ? ncclBfloat16 : ncclFloat32;
+    NCCL_CHECK(ncclAllGather(counts_, all_counts_, E, ncclInt32, comm_, st_));
+    CUDA_CHECK(cudaMemcpyAsync(h_ep_, all_counts_, static_cast<size_t>(W) * E * 4, cudaMemcpyDeviceToHost, st_));
+    launch_ep_send_plan(E, counts_, cursor_, st_);
+    launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xs_, ws_, st_);
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    const int32_t* cnt = h_ep_;  // [W][E]
+    int32_t* up = h_ep_ + static_cast<size_t>(W) * E;  // [tab | tile_expert | n_mtiles]
+    int32_t* tiles = up + static_cast<size_t>(W) * El * 3;
+    const EpPlan pl = ep_plan(W, ep_rank_, E, cnt, kMoeTile, max_tiles_, up, tiles);
+    if (pl.total_recv > recv_cap_) throw RuntimeError("expert-parallel receive buffer overflow");
+    const int n_tiles = pl.n_tiles;
+    tiles[max_tiles_] = n_tiles;
+    const auto &send_cnt = pl.send_cnt, &send_off = pl.send_off, &recv_cnt = pl.recv_cnt, &recv_off = pl.recv_off;
+    const int64_t total_recv = pl.total_recv;
+    const size_t up_n = static_cast<size_t>(W) * El * 3 + max_tiles_ + 1;
+    CUDA_CHECK(cudaMemcpyAsync(ep_up_, up, up_n * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
+    // dispatch: rows (and their gate weights) to the experts' ranks
+    NCCL_CHECK(ncclGroupStart());
+    for (int p = 0; p < W; ++p) {
+      if (send_cnt[p]) {
+        NCCL_CHECK(ncclSend(xs_ + send_off[p] * d, send_cnt[p] * d, dt, p, comm_, st_));
+        NCCL_CHECK(ncclSend(ws_ + send_off[p], send_cnt[p], ncclFloat32, p, comm_, st_));
+      }
+      if (recv_cnt[p]) {
+        NCCL_CHECK(ncclRecv(xr_ + recv_off[p] * d, recv_cnt[p] * d, dt, p, comm_, st_));
+        NCCL_CHECK(ncclRecv(wr_ + recv_off[p], recv_cnt[p], ncclFloat32, p, comm_, st_));
+      }
+    }
+    NCCL_CHECK(ncclGroupEnd());
+    int32_t* saved_te = tile_expert_;
+    int32_t* saved_nm = n_mtiles_;
+    tile_expert_ = ep_up_ + static_cast<size_t>(W) * El * 3;
+    n_mtiles_ = tile_expert_ + max_tiles_;
+    launch_ep_permute<T>(static_cast<int>(total_recv), W * El, ep_up_, d, xr_, wr_, xg_, row_scale_, perm_, st_);
+    expert_ffn(m, std::max(1, n_tiles) * kMoeTile, total_recv);
+    tile_expert_ = saved_te;
+    n_mtiles_ = saved_nm;
+    launch_ep_unpermute(static_cast<int>(total_recv), d, yg_, perm_, ys_, st_);
+    // combine: weighted expert outputs back to the tokens' ranks
+    NCCL_CHECK(ncclGroupStart());
+    for (int p = 0; p < W; ++p) {
+      if (recv_cnt[p]) NCCL_CHECK(ncclSend(ys_ + recv_off[p] * d, recv_cnt[p] * d, ncclFloat32, p, comm_, st_));
+      if (send_cnt[p]) NCCL_CHECK(ncclRecv(yr_ + send_off[p] * d, send_cnt[p] * d, ncclFloat32, p, comm_, st_));
+    }
+    NCCL_CHECK(ncclGroupEnd());
+    launch_moe_combine(rows, k, d, yr_, slot_, h, d, st_);
   }
 
   void prepare_decoder(int U) {
@@ -899,6 +1017,7 @@ class EngineT final : public Engine {
     gkseg.start = grp_kstart_;
     gkseg.fixed_len = Tn;
     std::vector<float> host(static_cast<size_t>(n) * V);
+    if (ep_world_ > 1) max_len = L - 1;  // expert-parallel ranks run the same number of MoE layers
     for (int step = 0; step <= max_len; ++step) {
       decode_step(step, n, G, gq, gkseg, tf_codes_, L, tf_anc_, L, max_group);
       CUDA_CHECK(cudaMemcpyAsync(host.data(), logits_, host.size() * 4, cudaMemcpyDeviceToHost, st_));
@@ -962,6 +1081,13 @@ class EngineT final : public Engine {
           *n_mtiles_ = nullptr;
   float *wts_ = nullptr, *row_scale_ = nullptr, *yg_ = nullptr, *ga_ = nullptr, *gb_ = nullptr;
   T *xg_ = nullptr, *hg_ = nullptr;
+  // expert parallelism
+  int ep_rank_ = 0, ep_world_ = 1, e0_ = 0, El_ = 0;
+  ncclComm_t comm_ = nullptr;
+  int64_t send_cap_ = 0, recv_cap_ = 0;
+  T *xs_ = nullptr, *xr_ = nullptr;
+  float *ws_ = nullptr, *wr_ = nullptr, *ys_ = nullptr, *yr_ = nullptr;
+  int32_t *perm_ = nullptr, *all_counts_ = nullptr, *ep_up_ = nullptr, *h_ep_ = nullptr;
   // staging
   void* host_stage_ = nullptr;
   uint8_t* dev_stage_ = nullptr;
@@ -972,16 +1098,23 @@ class EngineT final : public Engine {
   int last_n_live_ = 0, last_state_ = 0;
 };
 
+void nccl_unique_id(uint8_t out[128]) {
+  ncclUniqueId id;
+  NCCL_CHECK(ncclGetUniqueId(&id));
+  memcpy(out, id.internal, 128);
+}
+
 std::unique_ptr<Engine> Engine::create(const HostWeights& w, int device, int precision, int max_users,
-                                       int max_width) {
+                                       int max_width, const EpConfig* ep) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
     cudaGetLastError();
     throw RuntimeError("no CUDA device available (the engine has no CPU fallback)");
   }
   require(device >= 0 && device < n, "device index out of range");
-  if (precision == ORX_PRECISION_FP32) return std::make_unique<EngineT<float>>(w, device, max_users, max_width);
-  if (precision == ORX_PRECISION_BF16) return std::make_unique<EngineT<__nv_bfloat16>>(w, device, max_users, max_width);
+  if (precision == ORX_PRECISION_FP32) return std::make_unique<EngineT<float>>(w, device, max_users, max_width, ep);
+  if (precision == ORX_PRECISION_BF16)
+    return std::make_unique<EngineT<__nv_bfloat16>>(w, device, max_users, max_width, ep);
   throw InvalidArgument("unknown precision");
 }
 

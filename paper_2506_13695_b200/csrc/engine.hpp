@@ -9,11 +9,18 @@
 
 namespace orx {
 
+// Expert parallelism over NCCL: rank `rank` of `world`
+// holds experts [rank * E / world, (rank + 1) * E / world) of every MoE layer.
+struct EpConfig {
+  int rank = 0, world = 1;
+  uint8_t unique_id[128] = {};  // ncclUniqueId
+};
+
 class Engine {
  public:
   virtual ~Engine() = default;
   static std::unique_ptr<Engine> create(const HostWeights& w, int device, int precision, int max_users,
-                                        int max_width);
+                                        int max_width, const EpConfig* ep = nullptr);
   virtual void stage_batch(const orx_user_batch& b) = 0;
   virtual void encode(float* z_out) = 0;
   virtual void beam_search(int width, orx_beam_out* out) = 0;
@@ -26,6 +33,7 @@ class Engine {
 };
 
 void validate_batch(const orx_config& cfg, const orx_user_batch& b);
+void nccl_unique_id(uint8_t out[128]);
 long long launch_counter_value();
 
 }  // namespace orx

@@ -578,6 +578,63 @@ __global__ void swiglu_mul_kernel(long long n, const float* a, const float* b, f
   }
 }
 
+// ---- expert parallelism ------------------------------------------
+// Exclusive prefix of per-expert counts: compact (unpadded) send order by expert.
+__global__ void ep_send_plan_kernel(int E, const int32_t* __restrict__ counts, int32_t* __restrict__ cursor) {
+  const int lane = threadIdx.x;
+  int c = lane < E ? counts[lane] : 0;
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane < E) cursor[lane] = incl - c;
+}
+
+// Received rows (source rank major, then expert) -> expert-grouped rows padded
+// to the grouped GEMM tile. tab: n_seg x (src_row, dst_row, count).
+template <class T>
+__global__ void ep_permute_kernel(int total, int n_seg, const int32_t* __restrict__ tab, int d,
+                                  const T* __restrict__ xr, const float* __restrict__ wr, T* __restrict__ xg,
+                                  float* __restrict__ row_scale, int32_t* __restrict__ perm) {
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < total; r += gridDim.x * (blockDim.x >> 5)) {
+    int dst = -1;
+    for (int sgi = 0; sgi < n_seg; ++sgi) {
+      const int src = tab[3 * sgi], cnt = tab[3 * sgi + 2];
+      if (r >= src && r < src + cnt) dst = tab[3 * sgi + 1] + (r - src);
+    }
+    if (dst < 0) continue;
+    const T* a = xr + (size_t)r * d;
+    T* b = xg + (size_t)dst * d;
+    if (sizeof(T) == 2 && d % 8 == 0) {
+      for (int c = lane * 8; c < d; c += 256) *reinterpret_cast<uint4*>(b + c) = *reinterpret_cast<const uint4*>(a + c);
+    } else {
+      for (int c = lane; c < d; c += 32) b[c] = a[c];
+    }
+    if (lane == 0) {
+      row_scale[dst] = wr[r];
+      perm[r] = dst;
+    }
+  }
+}
+
+// ys[r] = yg[perm[r]]: expert outputs back to the received order.
+__global__ void ep_unpermute_kernel(int total, int d, const float* __restrict__ yg, const int32_t* __restrict__ perm,
+                                    float* __restrict__ ys) {
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < total; r += gridDim.x * (blockDim.x >> 5)) {
+    const float* a = yg + (size_t)perm[r] * d;
+    float* b = ys + (size_t)r * d;
+    if (d % 4 == 0) {
+      for (int c = lane * 4; c < d; c += 128) *reinterpret_cast<float4*>(b + c) = *reinterpret_cast<const float4*>(a + c);
+    } else {
+      for (int c = lane; c < d; c += 32) b[c] = a[c];
+    }
+  }
+}
+
 inline int grid_for(long long n, int block, int cap = 148 * 32) {
   long long g = (n + block - 1) / block;
   return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
@@ -702,6 +759,22 @@ void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, 
   ORX_LAUNCH(swiglu_mul_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, a, b, out));
 }
 
+void launch_ep_send_plan(int E, const int32_t* counts, int32_t* cursor, cudaStream_t s) {
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, ep_send_plan_kernel<<<1, 32, 0, s>>>(E, counts, cursor));
+}
+template <class T>
+void launch_ep_permute(int total, int n_seg, const int32_t* tab, int d, const T* xr, const float* wr, T* xg,
+                       float* row_scale, int32_t* perm, cudaStream_t s) {
+  if (total <= 0) return;
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, ep_permute_kernel<T><<<grid_for(total, 8, num_sms() * 8), 256, 0, s>>>(
+                                     total, n_seg, tab, d, xr, wr, xg, row_scale, perm));
+}
+void launch_ep_unpermute(int total, int d, const float* yg, const int32_t* perm, float* ys, cudaStream_t s) {
+  if (total <= 0) return;
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE,
+                 ep_unpermute_kernel<<<grid_for(total, 8, num_sms() * 8), 256, 0, s>>>(total, d, yg, perm, ys));
+}
+
 #define INST(T)                                                                                                   \
   template void launch_features<T>(const RecordsDev&, const FeatureTables&, T*, int, cudaStream_t);              \
   template void launch_static_features<T>(int, const int32_t*, const int32_t*, const int32_t*, const float*,     \
@@ -712,7 +785,9 @@ void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, 
   template void launch_dec_self_attn<T>(int, int, int, int, int, int, const T*, T* const*, const int32_t*, int,   \
                                         T*, cudaStream_t);                                                       \
   template void launch_moe_scatter<T>(int, int, int, const T*, int, const int32_t*, const float*, int32_t*,       \
-                                      int32_t*, T*, float*, cudaStream_t);
+                                      int32_t*, T*, float*, cudaStream_t);                                        \
+  template void launch_ep_permute<T>(int, int, const int32_t*, int, const T*, const float*, T*, float*, int32_t*, \
+                                     cudaStream_t);
 INST(float)
 INST(__nv_bfloat16)
 

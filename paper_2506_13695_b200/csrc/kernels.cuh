@@ -72,6 +72,12 @@ void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32
                         int32_t* seg_cursor, int32_t* slot, T* xg, float* row_scale, cudaStream_t s);
 void launch_moe_combine(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
                         cudaStream_t s);
+// Expert parallelism: compact send order, receive-side grouping, and its inverse.
+void launch_ep_send_plan(int E, const int32_t* counts, int32_t* cursor, cudaStream_t s);
+template <class T>
+void launch_ep_permute(int total, int n_seg, const int32_t* tab, int d, const T* xr, const float* wr, T* xg,
+                       float* row_scale, int32_t* perm, cudaStream_t s);
+void launch_ep_unpermute(int total, int d, const float* yg, const int32_t* perm, float* ys, cudaStream_t s);
 void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, cudaStream_t s);
 
 }  // namespace orx

@@ -22,6 +22,23 @@ def split_users(n_users: int, rank: int, world: int):
     return begin, base + (1 if rank < rem else 0)
 
 
+def ep_unique_id(device=None) -> bytes:
+    """NCCL unique id for the engines' expert-parallel communicator: made on
+    rank 0 (orx_ep_unique_id) and broadcast over the default process group."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from ._lib import check, lib
+    buf = (C.c_uint8 * 128)()
+    if dist.get_rank() == 0:
+        check(lib().orx_ep_unique_id(buf))
+    t = torch.tensor(list(bytes(buf)), dtype=torch.uint8, device=device)
+    dist.broadcast(t, src=0)
+    return bytes(t.cpu().tolist())
+
+
 def max_over_ranks(x: float, device=None) -> float:
     import torch
     import torch.distributed as dist

@@ -309,7 +309,10 @@ class PolicyModel:
     """Encoder + MoE decoder on one B200 (the engine owns device weights)."""
 
     def __init__(self, cfg: Optional[PolicyConfig] = None, *, weights: Optional[Weights] = None,
-                 precision: str = "fp32", device: int = 0, max_users: int = 16, max_width: int = 128):
+                 precision: str = "fp32", device: int = 0, max_users: int = 16, max_width: int = 128,
+                 ep: Optional[tuple] = None):
+        """ep = (rank, world, unique_id bytes): expert-parallel engine holding
+        n_experts / world experts per MoE layer (see dist.ep_unique_id)."""
         if weights is None:
             if cfg is None:
                 raise ValueError("PolicyModel needs a config or weights")
@@ -319,8 +322,14 @@ class PolicyModel:
         self.precision = precision
         self.max_users, self.max_width = max_users, max_width
         self._e = C.c_void_p()
-        check(lib().orx_engine_create(weights._h, device, PRECISION[precision], max_users, max_width,
-                                      C.byref(self._e)))
+        if ep is None or ep[1] == 1:
+            check(lib().orx_engine_create(weights._h, device, PRECISION[precision], max_users, max_width,
+                                          C.byref(self._e)))
+        else:
+            rank, world, uid = ep
+            buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
+            check(lib().orx_engine_create_ep(weights._h, device, PRECISION[precision], max_users, max_width, buf,
+                                             rank, world, C.byref(self._e)))
 
     @staticmethod
     def load(path: str, **kw) -> "PolicyModel":

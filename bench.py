@@ -37,6 +37,7 @@ REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "users/sec (beam-searched rec lists) per box at 1/2/4/8 B200; inference MFU"
 
+BASELINE_CONFIG = {"0.015B": 1, "0.121B": 2, "0.935B": 3, "2.633B": 4}
 PROF_NAMES = ["gemm_dense", "gemm_moe", "attention", "dec_self_attn", "moe_route", "beam_topk_merge", "other"]
 
 
@@ -196,6 +197,9 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--ep", action="store_true",
+                    help="expert-parallel MoE over the N GPUs (NCCL all-to-all, BASELINE config 4); "
+                         "each rank holds n_experts / N experts")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     lens = tuple(int(x) for x in args.lens.split(","))
@@ -218,7 +222,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     t_init = time.time()
-    model = P.PolicyModel(cfg, precision=args.precision, device=local, max_users=args.users, max_width=args.width)
+    ep = args.ep and world > 1 and cfg.moe_enabled
+    if ep:
+        from paper_2506_13695_b200.dist import ep_unique_id
+        uid = ep_unique_id(device=torch.device("cuda", local))
+        model = P.PolicyModel(weights=P.Weights.random_ep(cfg, rank, world), precision=args.precision, device=local,
+                              max_users=args.users, max_width=args.width, ep=(rank, world, uid))
+    else:
+        model = P.PolicyModel(cfg, precision=args.precision, device=local, max_users=args.users,
+                              max_width=args.width)
     t_init = time.time() - t_init
     from paper_2506_13695_b200.dist import shard_users
     user_begin, n_users = shard_users(rank, world, args.users)
@@ -335,12 +347,15 @@ def main():
             "metric": METRIC, "value": value, "unit": "users/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16" if args.precision == "bf16" else "fp32", "data": "synthetic",
-            "config": {"workload": f"OneRec-{args.config} (BASELINE config 3): encoder + "
+            "config": {"workload": f"OneRec-{args.config} (BASELINE config {BASELINE_CONFIG.get(args.config, '?')}): encoder + "
                                    f"{'MoE ' if cfg.moe_enabled else ''}decoder + depth-{L} beam search, "
                                    f"W={args.width}, V={cfg.codebook_size}, {args.users} users/GPU "
                                    f"(short,positive,lifelong)={lens}, random-init weights (seed {cfg.seed})",
                        "model": f"OneRec-{args.config}", "users_per_gpu": args.users, "global_batch": args.users * world,
-                       "width": args.width, "parallelism": f"dp{world} (users sharded, no inter-GPU traffic)",
+                       "width": args.width,
+                       "parallelism": (f"dp{world} x ep{world} (users sharded; MoE experts sharded, NCCL all-to-all "
+                                       f"dispatch/combine over NVLink)") if ep else
+                                      f"dp{world} (users sharded, no inter-GPU traffic)",
                        "l2": "working set (weights ~2 GB + activations) exceeds the 126 MB L2; no flush"},
             "mfu": mfu, "mfu_peak": "bf16_tflops (burst) of MEASURED_PEAKS.json",
             "gflop_per_user": flops_u / 1e9, "gflop_per_user_encoder": enc_flops_u / 1e9,

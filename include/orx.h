@@ -116,6 +116,9 @@ int64_t orx_config_expert_hidden(const orx_config* cfg);
 
 /* Host weights (fp32 copies of the reference's f64 parameters). */
 int orx_weights_create_random(const orx_config* cfg, orx_weights** out);
+/* Same stream, but only the experts of expert-parallel rank ep_rank of
+ * ep_world are materialised (for orx_engine_create_ep; cannot be saved). */
+int orx_weights_create_random_ep(const orx_config* cfg, int32_t ep_rank, int32_t ep_world, orx_weights** out);
 int orx_weights_load_grcp(const char* path, orx_weights** out);
 int orx_weights_save_grcp(const orx_weights* w, const char* path);
 int orx_weights_config(const orx_weights* w, orx_config* cfg);

@@ -71,6 +71,7 @@ SIGNATURES = [
     ("orx_config_enc_seq_len", C.c_int64, [C.POINTER(orx_config)]),
     ("orx_config_expert_hidden", C.c_int64, [C.POINTER(orx_config)]),
     ("orx_weights_create_random", C.c_int, [C.POINTER(orx_config), C.POINTER(_P)]),
+    ("orx_weights_create_random_ep", C.c_int, [C.POINTER(orx_config), C.c_int32, C.c_int32, C.POINTER(_P)]),
     ("orx_weights_load_grcp", C.c_int, [C.c_char_p, C.POINTER(_P)]),
     ("orx_weights_save_grcp", C.c_int, [_P, C.c_char_p]),
     ("orx_weights_config", C.c_int, [_P, C.POINTER(orx_config)]),

@@ -105,6 +105,16 @@ int orx_weights_create_random(const orx_config* cfg, orx_weights** out) {
   });
 }
 
+int orx_weights_create_random_ep(const orx_config* cfg, int32_t ep_rank, int32_t ep_world, orx_weights** out) {
+  return guarded([&] {
+    need(cfg, "cfg");
+    need(out, "out");
+    auto w = std::make_unique<orx_weights>();
+    w->w = orx::HostWeights::random(*cfg, ep_rank, ep_world);
+    *out = w.release();
+  });
+}
+
 int orx_weights_load_grcp(const char* path, orx_weights** out) {
   return guarded([&] {
     need(path, "path");

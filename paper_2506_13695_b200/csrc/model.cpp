@@ -375,10 +375,25 @@ const Tensor& HostWeights::get(const std::string& name) const {
 // (cos, sin) values in that order, so normal #j is fixed by draws 2*(j/2)
 // and 2*(j/2)+1; a sequential pass records the generator state every chunk
 // and worker threads fill chunks in parallel.
-HostWeights HostWeights::random(const orx_config& cfg) {
+HostWeights HostWeights::random(const orx_config& cfg, int ep_rank, int ep_world) {
   HostWeights w;
   w.cfg = cfg;
   auto specs = param_specs(cfg);
+  // expert parallelism: materialise only this rank's experts (the stream is
+  // still laid out over every parameter, so kept values are bit-identical)
+  auto kept = [&](const std::string& name) {
+    if (ep_world <= 1) return true;
+    const size_t at = name.find(".expert");
+    if (at == std::string::npos) return true;
+    const int e = std::atoi(name.c_str() + at + 7);
+    const int per = cfg.n_experts / ep_world;
+    return e / per == ep_rank;
+  };
+  if (ep_world > 1) {
+    require(cfg.moe_enabled && cfg.n_experts % ep_world == 0, "experts must divide evenly over the ranks");
+    require(ep_rank >= 0 && ep_rank < ep_world, "expert-parallel rank outside the world");
+    w.partial = true;
+  }
   std::vector<std::pair<float*, int64_t>> normal_dst;  // (ptr, count) per Normal tensor, in order
   std::vector<double> normal_sd;
   int64_t n_normal = 0;
@@ -387,15 +402,16 @@ HostWeights HostWeights::random(const orx_config& cfg) {
     t.name = s.name;
     t.rows = s.rows;
     t.cols = s.cols;
-    t.data.assign(static_cast<size_t>(s.rows) * s.cols, s.init == Init::Ones ? 1.f : 0.f);
+    if (kept(s.name)) t.data.assign(static_cast<size_t>(s.rows) * s.cols, s.init == Init::Ones ? 1.f : 0.f);
     w.index[s.name] = static_cast<int>(w.tensors.size());
     w.tensors.push_back(std::move(t));
   }
   for (size_t i = 0; i < specs.size(); ++i)
     if (specs[i].init == Init::Normal) {
-      normal_dst.push_back({w.tensors[i].data.data(), static_cast<int64_t>(w.tensors[i].data.size())});
+      const int64_t n = static_cast<int64_t>(specs[i].rows) * specs[i].cols;
+      normal_dst.push_back({w.tensors[i].data.empty() ? nullptr : w.tensors[i].data.data(), n});
       normal_sd.push_back(specs[i].stddev);
-      n_normal += static_cast<int64_t>(w.tensors[i].data.size());
+      n_normal += n;
     }
   const int64_t n_pairs = (n_normal + 1) / 2;
   const int64_t chunk_pairs = int64_t(1) << 21;
@@ -416,6 +432,11 @@ HostWeights HostWeights::random(const orx_config& cfg) {
     Rng r = starts[static_cast<size_t>(ch)];
     int64_t j0 = ch * chunk_pairs * 2, j1 = std::min(n_normal, j0 + chunk_pairs * 2);
     size_t ti = static_cast<size_t>(std::upper_bound(prefix.begin(), prefix.end(), j0) - prefix.begin() - 1);
+    {  // skip chunks that only cover tensors this process does not keep
+      bool any = false;
+      for (size_t t2 = ti; t2 < normal_dst.size() && prefix[t2] < j1; ++t2) any = any || normal_dst[t2].first;
+      if (!any) return;
+    }
     for (int64_t j = j0; j < j1; j += 2) {
       double u1 = r.uniform();
       double u2 = r.uniform();
@@ -429,7 +450,7 @@ HostWeights HostWeights::random(const orx_config& cfg) {
       for (int q = 0; q < 2 && j + q < j1; ++q) {
         int64_t jj = j + q;
         while (jj >= prefix[ti + 1]) ++ti;
-        normal_dst[ti].first[jj - prefix[ti]] = static_cast<float>(0.0 + normal_sd[ti] * v[q]);
+        if (normal_dst[ti].first) normal_dst[ti].first[jj - prefix[ti]] = static_cast<float>(0.0 + normal_sd[ti] * v[q]);
       }
     }
   };
@@ -444,8 +465,10 @@ HostWeights HostWeights::random(const orx_config& cfg) {
   if (retry_hit) {  // u1 == 0 (p = 2^-53 per pair): fall back to the sequential stream
     Rng r(cfg.seed);
     for (size_t i = 0; i < normal_dst.size(); ++i)
-      for (int64_t k = 0; k < normal_dst[i].second; ++k)
-        normal_dst[i].first[k] = static_cast<float>(0.0 + normal_sd[i] * r.normal());
+      for (int64_t k = 0; k < normal_dst[i].second; ++k) {
+        const float v = static_cast<float>(0.0 + normal_sd[i] * r.normal());
+        if (normal_dst[i].first) normal_dst[i].first[k] = v;
+      }
   }
   return w;
 }
@@ -524,6 +547,7 @@ HostWeights HostWeights::load_grcp(const std::string& path) {
 }
 
 void HostWeights::save_grcp(const std::string& path) const {
+  require(!partial, "cannot save an expert-parallel shard of the weights as a GRCP checkpoint");
   std::ofstream out(path, std::ios::binary);
   if (!out) throw RuntimeError("cannot open for writing: " + path);
   auto pod = [&](auto v) { out.write(reinterpret_cast<const char*>(&v), sizeof v); };

@@ -83,7 +83,9 @@ class HostWeights {
   std::unordered_map<std::string, int> index;
   const Tensor& get(const std::string& name) const;
   const float* ptr(const std::string& name) const { return get(name).data.data(); }
-  static HostWeights random(const orx_config& cfg);
+  // ep_world > 1: only experts of rank ep_rank are materialised (partial = true)
+  static HostWeights random(const orx_config& cfg, int ep_rank = 0, int ep_world = 1);
+  bool partial = false;
   static HostWeights load_grcp(const std::string& path);
   void save_grcp(const std::string& path) const;
 };

@@ -269,6 +269,13 @@ class Weights:
         return Weights(h)
 
     @staticmethod
+    def random_ep(cfg: PolicyConfig, ep_rank: int, ep_world: int) -> "Weights":
+        """The same seeded weights, materialising only this expert-parallel rank's experts."""
+        h = C.c_void_p()
+        check(lib().orx_weights_create_random_ep(C.byref(cfg.to_c()), ep_rank, ep_world, C.byref(h)))
+        return Weights(h)
+
+    @staticmethod
     def load(path: str) -> "Weights":
         h = C.c_void_p()
         check(lib().orx_weights_load_grcp(str(path).encode(), C.byref(h)))

@@ -31,7 +31,8 @@ def main():
         w = P.Weights.random(cfg)
         rep = P.PolicyModel(weights=w, precision=precision, device=local, max_users=users, max_width=width)
         uid = ep_unique_id(device=torch.device("cuda", local))  # one id per communicator
-        ep = P.PolicyModel(weights=w, precision=precision, device=local, max_users=users, max_width=width,
+        w_ep = P.Weights.random_ep(cfg, rank, world)  # only this rank's experts materialised
+        ep = P.PolicyModel(weights=w_ep, precision=precision, device=local, max_users=users, max_width=width,
                            ep=(rank, world, uid))
         # different users per rank (and a different ragged shape on odd ranks)
         lens = (20, 64, 300) if rank % 2 == 0 else (7, 31, 129)

@@ -11,7 +11,6 @@
 //                 row log-softmax + top-k -> per-user merge, depth times.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -24,6 +23,7 @@
 #include "beam.cuh"
 #include "engine.hpp"
 #include "ep_plan.hpp"
+#include "nccl_dl.hpp"
 #include "gemm.cuh"
 #include "kernels.cuh"
 
@@ -43,7 +43,7 @@ namespace {
 #define NCCL_CHECK(x)                                                                                      \
   do {                                                                                                     \
     ncclResult_t r__ = (x);                                                                                \
-    if (r__ != ncclSuccess) throw RuntimeError(std::string("NCCL: ") + ncclGetErrorString(r__) + " at " + \
+    if (r__ != ncclSuccess) throw RuntimeError(std::string("NCCL: ") + nccl().GetErrorString(r__) + " at " + \
                                                __FILE__ + ":" + std::to_string(__LINE__));                 \
   } while (0)
 
@@ -142,7 +142,7 @@ class EngineT final : public Engine {
       ncclUniqueId id;
       static_assert(sizeof(id.internal) == 128, "ncclUniqueId size");
       memcpy(id.internal, ep->unique_id, 128);
-      NCCL_CHECK(ncclCommInitRank(&comm_, ep_world_, id, ep_rank_));
+      NCCL_CHECK(nccl().CommInitRank(&comm_, ep_world_, id, ep_rank_));
     }
     require(max_users >= 1 && max_width >= 1, "engine capacity must be positive");
     require(cfg_.n_code_layers <= 8, "n_code_layers above 8 is not supported");
@@ -159,7 +159,7 @@ class EngineT final : public Engine {
   ~EngineT() override {
     cudaSetDevice(dev_);
     cudaStreamSynchronize(st_);
-    if (comm_) ncclCommDestroy(comm_);
+    if (comm_) nccl().CommDestroy(comm_);
     if (h_ep_) cudaFreeHost(h_ep_);
     if (host_stage_) cudaFreeHost(host_stage_);
     if (host_out_) cudaFreeHost(host_out_);
@@ -809,7 +809,7 @@ class EngineT final : public Engine {
     const orx_config& c = cfg_;
     const int d = c.d_model, E = c.n_experts, k = c.experts_active, W = ep_world_, El = El_;
     const ncclDataType_t dt = kBf16 ? ncclBfloat16 : ncclFloat32;
-    NCCL_CHECK(ncclAllGather(counts_, all_counts_, E, ncclInt32, comm_, st_));
+    NCCL_CHECK(nccl().AllGather(counts_, all_counts_, E, ncclInt32, comm_, st_));
     CUDA_CHECK(cudaMemcpyAsync(h_ep_, all_counts_, static_cast<size_t>(W) * E * 4, cudaMemcpyDeviceToHost, st_));
     launch_ep_send_plan(E, counts_, cursor_, st_);
     launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xs_, ws_, st_);
@@ -826,18 +826,18 @@ class EngineT final : public Engine {
     const size_t up_n = static_cast<size_t>(W) * El * 3 + max_tiles_ + 1;
     CUDA_CHECK(cudaMemcpyAsync(ep_up_, up, up_n * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
     // dispatch: rows (and their gate weights) to the experts' ranks
-    NCCL_CHECK(ncclGroupStart());
+    NCCL_CHECK(nccl().GroupStart());
     for (int p = 0; p < W; ++p) {
       if (send_cnt[p]) {
-        NCCL_CHECK(ncclSend(xs_ + send_off[p] * d, send_cnt[p] * d, dt, p, comm_, st_));
-        NCCL_CHECK(ncclSend(ws_ + send_off[p], send_cnt[p], ncclFloat32, p, comm_, st_));
+        NCCL_CHECK(nccl().Send(xs_ + send_off[p] * d, send_cnt[p] * d, dt, p, comm_, st_));
+        NCCL_CHECK(nccl().Send(ws_ + send_off[p], send_cnt[p], ncclFloat32, p, comm_, st_));
       }
       if (recv_cnt[p]) {
-        NCCL_CHECK(ncclRecv(xr_ + recv_off[p] * d, recv_cnt[p] * d, dt, p, comm_, st_));
-        NCCL_CHECK(ncclRecv(wr_ + recv_off[p], recv_cnt[p], ncclFloat32, p, comm_, st_));
+        NCCL_CHECK(nccl().Recv(xr_ + recv_off[p] * d, recv_cnt[p] * d, dt, p, comm_, st_));
+        NCCL_CHECK(nccl().Recv(wr_ + recv_off[p], recv_cnt[p], ncclFloat32, p, comm_, st_));
       }
     }
-    NCCL_CHECK(ncclGroupEnd());
+    NCCL_CHECK(nccl().GroupEnd());
     int32_t* saved_te = tile_expert_;
     int32_t* saved_nm = n_mtiles_;
     tile_expert_ = ep_up_ + static_cast<size_t>(W) * El * 3;
@@ -848,12 +848,12 @@ class EngineT final : public Engine {
     n_mtiles_ = saved_nm;
     launch_ep_unpermute(static_cast<int>(total_recv), d, yg_, perm_, ys_, st_);
     // combine: weighted expert outputs back to the tokens' ranks
-    NCCL_CHECK(ncclGroupStart());
+    NCCL_CHECK(nccl().GroupStart());
     for (int p = 0; p < W; ++p) {
-      if (recv_cnt[p]) NCCL_CHECK(ncclSend(ys_ + recv_off[p] * d, recv_cnt[p] * d, ncclFloat32, p, comm_, st_));
-      if (send_cnt[p]) NCCL_CHECK(ncclRecv(yr_ + send_off[p] * d, send_cnt[p] * d, ncclFloat32, p, comm_, st_));
+      if (recv_cnt[p]) NCCL_CHECK(nccl().Send(ys_ + recv_off[p] * d, recv_cnt[p] * d, ncclFloat32, p, comm_, st_));
+      if (send_cnt[p]) NCCL_CHECK(nccl().Recv(yr_ + send_off[p] * d, send_cnt[p] * d, ncclFloat32, p, comm_, st_));
     }
-    NCCL_CHECK(ncclGroupEnd());
+    NCCL_CHECK(nccl().GroupEnd());
     launch_moe_combine(rows, k, d, yr_, slot_, h, d, st_);
   }
 
@@ -1100,7 +1100,7 @@ class EngineT final : public Engine {
 
 void nccl_unique_id(uint8_t out[128]) {
   ncclUniqueId id;
-  NCCL_CHECK(ncclGetUniqueId(&id));
+  NCCL_CHECK(nccl().GetUniqueId(&id));
   memcpy(out, id.internal, 128);
 }
 

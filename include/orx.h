@@ -209,6 +209,25 @@ int orx_debug_gemm(const orx_gemm_args* args, void* stream);
  * (0xFFFFFFFF - (plex[r] * V + i)), in unspecified order. */
 int orx_debug_row_topk(int32_t rows, int32_t V, int32_t k, const float* logits, const float* pscore,
                        const int32_t* plex, float* lse, uint64_t* cand, void* stream);
+/* Kernel-level test hook for segmented bf16 attention (device pointers):
+ * segment b's query rows [qs(b), +ql(b)) attend to key rows [ks(b), +kl(b)),
+ * output rows start at os(b); a NULL array means start = b * stride /
+ * len = fixed. kernel 0: mma.sync kernel (row-major V); kernel 1: tcgen05
+ * kernel (V transposed per (vt_user[b] or b, head): Vt rows (u*heads+h)*dh+c,
+ * columns = key position in the segment). Q/K/V are buffer bases with head 0
+ * at column q_col0 / k_col0 / v_col0. */
+typedef struct orx_attn_args {
+  int32_t B, max_q, heads, dh;
+  const void* Q; int64_t q_rows; int32_t ldq, q_col0;
+  const void* K; int64_t k_rows; int32_t ldk, k_col0;
+  const void* V; int32_t ldv, v_col0;
+  const void* Vt; int64_t vt_rows, vt_cols; int32_t vt_ld; const int32_t* vt_user;
+  void* O; int32_t ldo;
+  const int32_t *q_start, *q_len, *k_start, *k_len, *o_start;
+  int32_t q_stride, q_fixed, k_stride, k_fixed, o_stride;
+  int32_t kernel;
+} orx_attn_args;
+int orx_debug_attention(const orx_attn_args* args, void* stream);
 /* Rows of the beam-pruning fast path that took its exact radix-select
  * fallback since the last call (process-wide counter, reset on read). */
 int64_t orx_debug_topk_fallback_rows(void);

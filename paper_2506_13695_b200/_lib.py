@@ -59,6 +59,20 @@ class orx_gemm_args(C.Structure):
     ]
 
 
+class orx_attn_args(C.Structure):
+    _fields_ = [
+        ("B", C.c_int32), ("max_q", C.c_int32), ("heads", C.c_int32), ("dh", C.c_int32),
+        ("Q", C.c_void_p), ("q_rows", C.c_int64), ("ldq", C.c_int32), ("q_col0", C.c_int32),
+        ("K", C.c_void_p), ("k_rows", C.c_int64), ("ldk", C.c_int32), ("k_col0", C.c_int32),
+        ("V", C.c_void_p), ("ldv", C.c_int32), ("v_col0", C.c_int32),
+        ("Vt", C.c_void_p), ("vt_rows", C.c_int64), ("vt_cols", C.c_int64), ("vt_ld", C.c_int32),
+        ("vt_user", C.c_void_p), ("O", C.c_void_p), ("ldo", C.c_int32),
+        ("q_start", C.c_void_p), ("q_len", C.c_void_p), ("k_start", C.c_void_p), ("k_len", C.c_void_p),
+        ("o_start", C.c_void_p), ("q_stride", C.c_int32), ("q_fixed", C.c_int32), ("k_stride", C.c_int32),
+        ("k_fixed", C.c_int32), ("o_stride", C.c_int32), ("kernel", C.c_int32),
+    ]
+
+
 # (name, restype, argtypes) for every function declared in include/orx.h
 _P = C.c_void_p
 _I32P = C.POINTER(C.c_int32)
@@ -100,6 +114,7 @@ SIGNATURES = [
     ("orx_debug_gemm", C.c_int, [C.POINTER(orx_gemm_args), _P]),
     ("orx_debug_row_topk", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
     ("orx_debug_topk_fallback_rows", C.c_int64, []),
+    ("orx_debug_attention", C.c_int, [C.POINTER(orx_attn_args), _P]),
     ("orx_debug_ep_plan", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _I32P, C.c_int32, C.c_int32,
                                     C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                     C.POINTER(C.c_int64), _I32P, _I32P, _I32P]),

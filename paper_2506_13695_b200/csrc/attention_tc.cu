@@ -1,0 +1,326 @@
+// tcgen05 / TMEM flash attention for the bf16 path (head dim 64 or 128).
+//
+// One CTA per (segment b, head h, block of 128 query rows); two CTAs per SM.
+//   warp 0    TMA producer: Q once; K (row-major keys x dh) and V^T (dh x keys,
+//             written transposed by the producing GEMM's epilogue) in 64-key
+//             blocks, double-buffered
+//   warp 1    one thread issues tcgen05.mma:
+//               S_j  = Q . K_j^T   (M=128, N=64, K=dh)   -> TMEM, 2 buffers
+//               O   += P_j . V_j   (M=128, N=dh, K=64)   -> TMEM
+//             S_{j+1} is issued before P_j is ready, so QK^T of the next block
+//             overlaps the softmax of the current one
+//   warps 2-5 softmax, one thread per query row (TMEM lane = row): row max
+//             with lazy rescaling (O in TMEM is rescaled only when the running
+//             max grows by more than 2^8), P = exp2 in bf16 written to shared
+//             memory in the 128-byte-swizzled K-major UMMA layout, final O / l
+// Semantics are mha_core's (tape.cpp:822-905): softmax(Q K^T / sqrt(dh)) V,
+// max-subtracted, keys beyond the segment length masked.
+#include <cfloat>
+#include <stdexcept>
+#include <string>
+
+#include "attention.cuh"
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace orx {
+
+namespace {
+
+__device__ __forceinline__ int seg_start(const Seg& s, int b) { return s.start ? s.start[b] : b * s.stride; }
+__device__ __forceinline__ int seg_len(const Seg& s, int b) { return s.len ? s.len[b] : s.fixed_len; }
+
+ORX_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+ORX_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+ORX_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int DH>
+struct Fmha {
+  static constexpr int BQ = 128, BK = 64;
+  static constexpr int CB = DH / 64;                  // 64-element (128 B) column blocks of Q / K
+  static constexpr uint32_t Q_BYTES = BQ * DH * 2;    // CB blocks of [128 rows x 128 B]
+  static constexpr uint32_t K_BYTES = BK * DH * 2;    // CB blocks of [64 rows x 128 B]
+  static constexpr uint32_t V_BYTES = DH * BK * 2;    // [DH rows (head dims) x 64 keys]
+  static constexpr uint32_t P_BYTES = BQ * BK * 2;    // [128 rows x 64 keys]
+  static constexpr uint32_t SMEM = Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + P_BYTES + 128;  // + barriers
+  static constexpr uint32_t TMEM_COLS = 2 * BK + DH <= 256 ? 256 : 512;  // S[2] + O
+};
+
+template <int DH>
+__global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
+                                                       const __grid_constant__ CUtensorMap tmK,
+                                                       const __grid_constant__ CUtensorMap tmV, int heads,
+                                                       __nv_bfloat16* __restrict__ O, int ldo, Seg qs, Seg ks, Seg os,
+                                                       const int32_t* __restrict__ vt_user, int q_col0, int k_col0) {
+  using F = Fmha<DH>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + F::Q_BYTES;          // [2][K_BYTES]
+  uint8_t* sV = sK + 2 * F::K_BYTES;      // [2][V_BYTES]
+  uint8_t* sP = sV + 2 * F::V_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + F::P_BYTES);
+  uint64_t& q_full = bars[0];
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* s_empty = bars + 7;   // [2]
+  uint64_t& p_full = bars[9];
+  uint64_t& o_done = bars[10];
+  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 11);
+
+  const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * F::BQ;
+  const int qlen = seg_len(qs, b);
+  const int qst = seg_start(qs, b), kst = seg_start(ks, b), klen = seg_len(ks, b), ost = seg_start(os, b);
+  if (q0 >= qlen || klen <= 0) return;
+  const int nb = (klen + F::BK - 1) / F::BK;
+  const int vrow0 = ((vt_user ? vt_user[b] : b) * heads + h) * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    if ((smem_u32(smem) & 1023) != 0) __trap();  // SW128 operands need 1 KB alignment
+    mbar_init(&q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_empty[s], 4);
+    }
+    mbar_init(&p_full, 4);
+    mbar_init(&o_done, 1);
+    fence_mbar_init();
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+  }
+  if (warp == 1) tmem_alloc(&tmem_slot, F::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const uint32_t t_s = tmem;             // S buffers: cols [0, 64), [64, 128)
+  const uint32_t t_o = tmem + 2 * F::BK;  // O: cols [128, 128 + DH)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_normal();
+      mbar_arrive_expect_tx(&q_full, F::Q_BYTES);
+      for (int cb = 0; cb < F::CB; ++cb)
+        tma_load_2d(sQ + cb * (F::BQ * 128), &tmQ, &q_full, q_col0 + h * DH + cb * 64, qst + q0, pol);
+      for (int j = 0; j < nb; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&kv_full[st], F::K_BYTES + F::V_BYTES);
+        for (int cb = 0; cb < F::CB; ++cb)
+          tma_load_2d(sK + st * F::K_BYTES + cb * (F::BK * 128), &tmK, &kv_full[st], k_col0 + h * DH + cb * 64,
+                      kst + j * F::BK, pol);
+        tma_load_2d(sV + st * F::V_BYTES, &tmV, &kv_full[st], j * F::BK, vrow0, pol);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(F::BQ, F::BK);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(F::BQ, DH);
+      auto issue_pv = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&p_full, j & 1);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sP), b0 = smem_u32(sV + st * F::V_BYTES);
+#pragma unroll
+        for (int k = 0; k < F::BK / 16; ++k)
+          tc_mma_bf16(t_o, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc_o, (j | k) != 0);
+        tc_commit(&o_done);
+        tc_commit(&kv_empty[st]);
+      };
+      mbar_wait(&q_full, 0);
+      for (int j = 0; j < nb; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        if (j >= 2) mbar_wait(&s_empty[st], ((j >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + st * F::K_BYTES);
+#pragma unroll
+        for (int k = 0; k < DH / 16; ++k) {
+          const int cb = k >> 2, off = (k & 3) * 32;
+          tc_mma_bf16(t_s + st * F::BK, umma_desc_sw128(qa + cb * (F::BQ * 128) + off),
+                      umma_desc_sw128(kb + cb * (F::BK * 128) + off), idesc_s, k != 0);
+        }
+        tc_commit(&s_full[st]);
+        if (j >= 1) issue_pv(j - 1);
+      }
+      issue_pv(nb - 1);
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quadrant
+    const int r = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    const float scale_log2 = rsqrtf(static_cast<float>(DH)) * 1.4426950408889634f;
+    float m = -FLT_MAX, l = 0.f;
+    bool first = true;
+    uint8_t* prow = sP + (r >> 3) * 1024 + (r & 7) * 128;
+    for (int j = 0; j < nb; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sa[32], sb[32];
+      tmem_ld32_async(t_s + lane_off + st * F::BK, sa);
+      tmem_ld32_async(t_s + lane_off + st * F::BK + 32, sb);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[st]);
+      const int valid = klen - j * F::BK;
+      float x[64];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        x[i] = i < valid ? __uint_as_float(sa[i]) * scale_log2 : -FLT_MAX;
+        x[32 + i] = 32 + i < valid ? __uint_as_float(sb[i]) * scale_log2 : -FLT_MAX;
+      }
+      float bm = -FLT_MAX;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) bm = fmaxf(bm, x[i]);
+      float corr = 1.f;
+      bool resc = false;
+      if (first || bm > m + 8.f) {  // lazy rescale: keep a stale max unless it grew by > 2^8
+        corr = first ? 0.f : exp2f(m - bm);
+        resc = !first;
+        m = bm;
+        first = false;
+      }
+      float sum = 0.f;
+      uint32_t pk[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float p0 = exp2f(x[2 * i] - m), p1 = exp2f(x[2 * i + 1] - m);
+        sum += p0 + p1;
+        pk[i] = pack_bf16(p0, p1);
+      }
+      l = l * corr + sum;
+      if (j >= 1) {  // P buffer and O are free once P_{j-1} . V_{j-1} has completed
+        mbar_wait(&o_done, (j - 1) & 1);
+        tc_fence_after();
+      }
+      if (__any_sync(0xffffffffu, resc)) {
+        const float c = resc ? corr : 1.f;
+#pragma unroll 1
+        for (int cc = 0; cc < DH / 32; ++cc) {
+          uint32_t o[32];
+          tmem_ld32_async(t_o + lane_off + cc * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * c);
+          tmem_st32(t_o + lane_off + cc * 32, o);
+        }
+        tmem_wait_st();
+      }
+      // P row: 8 chunks of 16 B (8 keys), chunk c stored at slot c ^ (row % 8) (128-byte swizzle)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint4 v = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = v;
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full);
+    }
+    mbar_wait(&o_done, (nb - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    const bool store = q0 + r < qlen;
+    __nv_bfloat16* orow = O + (size_t)(ost + q0 + r) * ldo + h * DH;
+#pragma unroll 1
+    for (int cc = 0; cc < DH / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld32_async(t_o + lane_off + cc * 32, o);
+      tmem_wait_ld();
+      if (store) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
+          w.y = pack_bf16(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+          w.z = pack_bf16(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
+          w.w = pack_bf16(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + cc * 32 + i) = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, F::TMEM_COLS);
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+CUtensorMap map2d(const void* ptr, long long rows, long long cols, long long ld, int box_cols, int box_rows) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  CUtensorMap m;
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("attention tensor map encode failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
+template <int DH>
+void launch_fmha(const FmhaArgs& a, cudaStream_t s) {
+  using F = Fmha<DH>;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(fmha_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(F::SMEM));
+    set = true;
+  }
+  // Q/K maps start at the head-0 column of their buffers (column offsets are
+  // added in the kernel): rows x (q_col0 + heads * DH) columns.
+  CUtensorMap mq = map2d(a.Q, a.q_rows, a.q_col0 + a.heads * DH, a.ldq, 64, F::BQ);
+  CUtensorMap mk = map2d(a.K, a.k_rows, a.k_col0 + a.heads * DH, a.ldk, 64, F::BK);
+  CUtensorMap mv = map2d(a.Vt, a.vt_rows, a.vt_cols, a.vt_ld, 64, DH);
+  dim3 grid((a.max_q + F::BQ - 1) / F::BQ, a.heads, a.B);
+  fmha_tc_kernel<DH><<<grid, 192, F::SMEM, s>>>(mq, mk, mv, a.heads, static_cast<__nv_bfloat16*>(a.O), a.ldo, a.q, a.k, a.o, a.vt_user, a.q_col0,
+                                                a.k_col0);
+}
+
+}  // namespace
+
+bool fmha_supported(int dh) { return dh == 64 || dh == 128; }
+
+void launch_fmha_tc(const FmhaArgs& a, cudaStream_t s) {
+  if (a.B <= 0 || a.max_q <= 0) return;
+  if (a.ldq % 8 || a.ldk % 8 || a.vt_ld % 8 || a.q_col0 % 8 || a.k_col0 % 8)
+    throw std::invalid_argument("fmha: strides / column offsets must be multiples of 8 elements");
+  ProfScope ps(PROF_ATTN, s, a.flops, 0.0);
+  if (a.dh == 128) launch_fmha<128>(a, s);
+  else if (a.dh == 64) launch_fmha<64>(a, s);
+  else throw std::invalid_argument("fmha: head dim must be 64 or 128");
+  ++launch_counter();
+}
+
+}  // namespace orx

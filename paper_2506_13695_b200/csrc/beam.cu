@@ -258,11 +258,15 @@ __global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows,
   if (ok) {
     bn[w][lane] = n;
     __syncwarp();
-    // lane owns slot `lane` of every segment j (conflict-free transposed read)
+    // lane owns slots lane, lane + 32, ... of every lane segment j (conflict-free transposed read)
+    constexpr int SPL = kLaneSlots / 32;
     float c[kLaneSlots];
 #pragma unroll
-    for (int j = 0; j < kLaneSlots; ++j)
-      c[j] = lane < bn[w][j] ? ps + (bx[w][j * kLaneSlots + lane] - lse) : -FLT_MAX;
+    for (int j = 0; j < 32; ++j)
+#pragma unroll
+      for (int s2 = 0; s2 < SPL; ++s2)
+        c[j * SPL + s2] =
+            lane + 32 * s2 < bn[w][j] ? ps + (bx[w][j * kLaneSlots + 32 * s2 + lane] - lse) : -FLT_MAX;
     float lo = ps + (tx - lse), hi = ps + (mx - lse);  // count(>= lo) = total >= k_sel
     bool hi_open = true, found = total == k_sel;
     float tau = lo;
@@ -305,7 +309,7 @@ __global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows,
         const bool take = c[j] >= tau;
         const unsigned m = __ballot_sync(0xffffffffu, take);
         if (take) {
-          const uint32_t idx = static_cast<uint32_t>(bi[w][j * kLaneSlots + lane]);
+          const uint32_t idx = static_cast<uint32_t>(bi[w][(j / SPL) * kLaneSlots + 32 * (j % SPL) + lane]);
           out[pos + __popc(m & ((1u << lane) - 1u))] =
               (static_cast<uint64_t>(ord_f32(c[j])) << 32) | (0xFFFFFFFFu - (lbase + idx));
         }

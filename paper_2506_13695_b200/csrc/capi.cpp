@@ -1,5 +1,7 @@
 // extern "C" boundary (include/orx.h). Exceptions never cross it: they are
 // mapped to ORX_EINVAL / ORX_ERUNTIME / ORX_ECUDA plus a thread-local message.
+#include <cuda_bf16.h>
+
 #include <cstring>
 #include <memory>
 #include <string>
@@ -8,6 +10,7 @@
 #include "../../include/orx.h"
 #include "engine.hpp"
 #include "ep_plan.hpp"
+#include "attention.cuh"
 #include "beam.cuh"
 #include "gemm.cuh"
 #include "model.hpp"
@@ -364,6 +367,35 @@ int orx_debug_row_topk(int32_t rows, int32_t V, int32_t k, const float* logits, 
     orx::launch_row_topk(rows, V, k, logits, pscore, plex, lse, cand, fail, static_cast<cudaStream_t>(stream));
     cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
     cudaFree(fail);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) throw orx::RuntimeError(std::string("CUDA: ") + cudaGetErrorString(err));
+  });
+}
+
+int orx_debug_attention(const orx_attn_args* a, void* stream) {
+  return guarded([&] {
+    need(a, "args");
+    orx::Seg q, k, o;
+    q.start = a->q_start, q.len = a->q_len, q.stride = a->q_stride, q.fixed_len = a->q_fixed;
+    k.start = a->k_start, k.len = a->k_len, k.stride = a->k_stride, k.fixed_len = a->k_fixed;
+    o.start = a->o_start, o.stride = a->o_stride;
+    auto st = static_cast<cudaStream_t>(stream);
+    if (a->kernel == 1) {
+      orx::FmhaArgs f;
+      f.B = a->B, f.max_q = a->max_q, f.heads = a->heads, f.dh = a->dh;
+      f.Q = a->Q, f.q_rows = a->q_rows, f.ldq = a->ldq, f.q_col0 = a->q_col0;
+      f.K = a->K, f.k_rows = a->k_rows, f.ldk = a->ldk, f.k_col0 = a->k_col0;
+      f.Vt = a->Vt, f.vt_rows = a->vt_rows, f.vt_cols = a->vt_cols, f.vt_ld = a->vt_ld, f.vt_user = a->vt_user;
+      f.O = a->O, f.ldo = a->ldo;
+      f.q = q, f.k = k, f.o = o;
+      orx::launch_fmha_tc(f, st);
+    } else {
+      using B16 = __nv_bfloat16;
+      orx::launch_attention<B16>(a->B, a->max_q, a->heads, a->dh, static_cast<const B16*>(a->Q) + a->q_col0, a->ldq,
+                                 static_cast<const B16*>(a->K) + a->k_col0, a->ldk,
+                                 static_cast<const B16*>(a->V) + a->v_col0, a->ldv, static_cast<B16*>(a->O), a->ldo,
+                                 q, k, o, st);
+    }
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) throw orx::RuntimeError(std::string("CUDA: ") + cudaGetErrorString(err));
   });

@@ -153,6 +153,7 @@ class EngineT final : public Engine {
               "bf16 mode needs head dim 32, 64 or 128");
       require(!cfg_.moe_enabled || expert_hidden(cfg_) % 128 == 0, "bf16 MoE needs expert hidden % 128 == 0");
     }
+    if constexpr (kBf16) tc_attn_ = fmha_supported(cfg_.d_model / cfg_.n_heads) && !getenv("ORX_ATTN_MMA_SYNC");
     upload(hw);
     alloc_activations();
   }
@@ -268,8 +269,10 @@ class EngineT final : public Engine {
   }
 
   struct Mlp { Lin<T> fc1, fc2; };
-  struct QBlock { Lin<T> wq, wkv, wo, fc1, fc2; const float* gain; };
-  struct EncL { const float *n1, *n2; Lin<T> wqkv, wo, fc1, fc2; MoeW moe; };
+  // tc_attn_ (bf16, head dim 64/128): V is projected by its own GEMM whose
+  // epilogue writes it transposed per (user, head) for the tcgen05 attention
+  struct QBlock { Lin<T> wq, wkv, wk, wv, wo, fc1, fc2; const float* gain; };
+  struct EncL { const float *n1, *n2; Lin<T> wqkv, wqk, wv, wo, fc1, fc2; MoeW moe; };
   struct DecL { const float *n1, *n2, *n3; Lin<T> sqkv, so, cq, co, fc1, fc2; MoeW moe; };
 
   void upload(const HostWeights& hw) {
@@ -312,7 +315,12 @@ class EngineT final : public Engine {
       std::string n = "lifelong.block" + std::to_string(b);
       QBlock q;
       q.wq = pack(hw, {n + ".attn.wq.w"});
-      q.wkv = pack(hw, {n + ".attn.wk.w", n + ".attn.wv.w"});
+      if (tc_attn_) {
+        q.wk = pack(hw, {n + ".attn.wk.w"});
+        q.wv = pack(hw, {n + ".attn.wv.w"});
+      } else {
+        q.wkv = pack(hw, {n + ".attn.wk.w", n + ".attn.wv.w"});
+      }
       q.wo = pack(hw, {n + ".attn.wo.w"});
       q.gain = up(hw, n + ".norm.gain");
       q.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b");
@@ -324,7 +332,12 @@ class EngineT final : public Engine {
       EncL e;
       e.n1 = up(hw, n + ".n1.gain");
       e.n2 = up(hw, n + ".n2.gain");
-      e.wqkv = pack(hw, {n + ".attn.wq.w", n + ".attn.wk.w", n + ".attn.wv.w"});
+      if (tc_attn_) {
+        e.wqk = pack(hw, {n + ".attn.wq.w", n + ".attn.wk.w"});
+        e.wv = pack(hw, {n + ".attn.wv.w"});
+      } else {
+        e.wqkv = pack(hw, {n + ".attn.wq.w", n + ".attn.wk.w", n + ".attn.wv.w"});
+      }
       e.wo = pack(hw, {n + ".attn.wo.w"});
       if (enc_moe(c)) e.moe = pack_moe(hw, n + ".moe", n + ".n2.gain");
       else {
@@ -353,7 +366,14 @@ class EngineT final : public Engine {
       }
       dec_.push_back(e);
     }
-    xkv_w_ = pack(hw, xkv);  // all decoder layers' cross K|V in one GEMM
+    if (tc_attn_) {  // all layers' cross K in one GEMM, all layers' cross V (transposed) in another
+      std::vector<std::string> xk, xv;
+      for (size_t i = 0; i < xkv.size(); i += 2) xk.push_back(xkv[i]), xv.push_back(xkv[i + 1]);
+      xk_w_ = pack(hw, xk);
+      xv_w_ = pack(hw, xv);
+    } else {
+      xkv_w_ = pack(hw, xkv);  // all decoder layers' cross K|V in one GEMM
+    }
   }
 
   // ------------------------------------------------------------------------
@@ -384,6 +404,16 @@ class EngineT final : public Engine {
     qcur_ = ar_.alloc<T>(static_cast<size_t>(U) * Nq * d);
     zt_ = kBf16 ? ar_.alloc<T>(static_cast<size_t>(rows_enc) * d) : reinterpret_cast<T*>(z_);
     xkv_ = ar_.alloc<T>(static_cast<size_t>(rows_enc) * 2 * d * Ld);
+    if (tc_attn_) {  // transposed V operands, zero padding columns stay finite
+      Tpad_ = rup(Tn, 8);
+      Lpad_ = rup(std::max(c.lifelong_len, 1), 8);
+      vt_enc_ = ar_.alloc<T>(static_cast<size_t>(U) * d * Tpad_);
+      vt_q_ = ar_.alloc<T>(static_cast<size_t>(U) * d * Lpad_);
+      vt_x_ = ar_.alloc<T>(static_cast<size_t>(Ld) * U * d * Tpad_);
+      CUDA_CHECK(cudaMemset(vt_enc_, 0, static_cast<size_t>(U) * d * Tpad_ * sizeof(T)));
+      CUDA_CHECK(cudaMemset(vt_q_, 0, static_cast<size_t>(U) * d * Lpad_ * sizeof(T)));
+      CUDA_CHECK(cudaMemset(vt_x_, 0, static_cast<size_t>(Ld) * U * d * Tpad_ * sizeof(T)));
+    }
     h_ = ar_.alloc<float>(static_cast<size_t>(Rd_) * d);
     for (int p = 0; p < L; ++p) cache_.push_back(ar_.alloc<T>(static_cast<size_t>(Rd_) * Ld * 2 * d));
     cache_ptrs_ = ar_.alloc<T*>(L);
@@ -406,6 +436,7 @@ class EngineT final : public Engine {
     grp_start_ = ar_.alloc<int32_t>(Rd_ + 1);
     grp_len_ = ar_.alloc<int32_t>(Rd_ + 1);
     grp_kstart_ = ar_.alloc<int32_t>(Rd_ + 1);
+    grp_user_ = ar_.alloc<int32_t>(Rd_ + 1);
     if (c.moe_enabled) {
       const int E = c.n_experts, k = c.experts_active, h = expert_hidden(c);
       const int64_t mrows = std::max(rows_enc, Rd_);
@@ -461,6 +492,49 @@ class EngineT final : public Engine {
     e.out_bf16 = (!out_f32 && kBf16) ? 1 : 0;
     return e;
   }
+  // epilogue writing V transposed per (user, head) for the tcgen05 attention:
+  // vt[layer][u][c][t] with t the key position (rows r -> (r / T, r % T) or maps)
+  Epi vt_epi(T* vt, int ld, int T_rows, const int32_t* row_user, const int32_t* row_pos, long long layer_stride) {
+    Epi e;
+    e.vt = vt;
+    e.vt_ld = ld;
+    e.vt_T = T_rows;
+    e.vt_cols = cfg_.d_model;
+    e.vt_user_stride = static_cast<long long>(cfg_.d_model) * ld;
+    e.vt_layer_stride = layer_stride;
+    e.vt_row_user = row_user;
+    e.vt_row_pos = row_pos;
+    e.out_bf16 = 1;
+    return e;
+  }
+  FmhaArgs fmha(int B, int max_q, const T* Q, long long q_rows, int ldq, const T* K, long long k_rows, int ldk,
+                int k_col0, const T* Vt, int vt_users, int vt_ld, const int32_t* vt_user, Seg q, Seg k, Seg o,
+                double flops) {
+    FmhaArgs f;
+    f.B = B;
+    f.max_q = max_q;
+    f.heads = cfg_.n_heads;
+    f.dh = cfg_.d_model / cfg_.n_heads;
+    f.Q = Q;
+    f.q_rows = q_rows;
+    f.ldq = ldq;
+    f.K = K;
+    f.k_rows = k_rows;
+    f.ldk = ldk;
+    f.k_col0 = k_col0;
+    f.Vt = Vt;
+    f.vt_rows = static_cast<long long>(vt_users) * cfg_.d_model;
+    f.vt_cols = vt_ld;
+    f.vt_ld = vt_ld;
+    f.vt_user = vt_user;
+    f.O = att_;
+    f.ldo = cfg_.d_model;
+    f.q = q;
+    f.k = k;
+    f.o = o;
+    f.flops = flops;
+    return f;
+  }
   void gemm(const T* A, int lda, const Lin<T>& W, int M, Epi e) {
     if (M <= 0) return;
     if (!e.n_out) e.n_out = W.N;
@@ -479,7 +553,7 @@ class EngineT final : public Engine {
     int n_keys = 0;
     int n_pad_keys = 0;
     size_t off_uid, off_gender, off_age, off_ns, off_np, off_kstart, off_klen, off_static_map, off_life_map,
-        off_pad_keys;
+        off_pad_keys, off_key_user, off_key_pos;
     size_t off_vid[3], off_aid[3], off_tag[3], off_ts[3], off_play[3], off_dur[3], off_lab[3], off_sid[3],
         off_map[3];
     size_t bytes = 0;
@@ -512,6 +586,11 @@ class EngineT final : public Engine {
     s.off_static_map = take(4 * s.U);
     s.off_life_map = take(4 * static_cast<size_t>(s.U) * Nq);
     s.off_pad_keys = take(4 * s.U);
+    int64_t n_keys_total = 0;
+    for (int u = 0; u < s.U; ++u)
+      n_keys_total += std::max<int64_t>(b.lifelong_seq.offsets[u + 1] - b.lifelong_seq.offsets[u], 1);
+    s.off_key_user = take(4 * n_keys_total);  // lifelong key row -> (user, position)
+    s.off_key_pos = take(4 * n_keys_total);
     for (int p = 0; p < 3; ++p) {
       size_t n = s.n_rec[p];
       s.off_vid[p] = take(8 * n);
@@ -550,6 +629,10 @@ class EngineT final : public Engine {
       I32(s.off_kstart)[u] = kpos;
       I32(s.off_klen)[u] = std::max(n, 1);
       if (n == 0) I32(s.off_pad_keys)[npad++] = kpos;
+      for (int t = 0; t < std::max(n, 1); ++t) {
+        I32(s.off_key_user)[kpos + t] = u;
+        I32(s.off_key_pos)[kpos + t] = t;
+      }
       kpos += std::max(n, 1);
     }
     s.n_keys = kpos;
@@ -664,7 +747,6 @@ class EngineT final : public Engine {
       const bool first = b == 0, last = b + 1 == qblocks_.size();
       if (first) gemm(queries_, rup(d, 8), q.wq, Nq, epi(qproj_, d, false));  // user-independent
       else gemm(qcur_, d, q.wq, U * Nq, epi(qproj_, d, false));
-      gemm(keys_, d, q.wkv, sg_.n_keys, epi(kvl_, 2 * d, false));
       Seg qs;
       qs.stride = first ? 0 : Nq;
       qs.fixed_len = Nq;
@@ -674,8 +756,18 @@ class EngineT final : public Engine {
       Seg os;
       os.stride = Nq;
       os.fixed_len = Nq;
-      launch_attention<T>(U, Nq, H, dh, qproj_, d, kvl_, 2 * d, kvl_ + d, 2 * d, att_, d, qs, ks, os, st_,
-                          4.0 * Nq * sg_.n_keys * d);
+      const double aflops = 4.0 * Nq * sg_.n_keys * d;
+      if (tc_attn_) {
+        gemm(keys_, d, q.wk, sg_.n_keys, epi(kvl_, d, false));
+        gemm(keys_, d, q.wv, sg_.n_keys,
+             vt_epi(vt_q_, Lpad_, 0, dp<int32_t>(sg_.off_key_user), dp<int32_t>(sg_.off_key_pos), 0));
+        FmhaArgs f = fmha(U, Nq, qproj_, first ? Nq : U * Nq, d, kvl_, sg_.n_keys, d, 0, vt_q_, U, Lpad_, nullptr,
+                          qs, ks, os, aflops);
+        launch_fmha_tc(f, st_);
+      } else {
+        gemm(keys_, d, q.wkv, sg_.n_keys, epi(kvl_, 2 * d, false));
+        launch_attention<T>(U, Nq, H, dh, qproj_, d, kvl_, 2 * d, kvl_ + d, 2 * d, att_, d, qs, ks, os, st_, aflops);
+      }
       gemm(att_, d, q.wo, U * Nq, epi(qo_, d, true));
       launch_rmsnorm<T>(U * Nq, d, qo_, d, q.gain, xn_, d, st_);
       Epi e1 = epi(ffh_, c.ffn_hidden, false);
@@ -695,12 +787,20 @@ class EngineT final : public Engine {
     const int R = U * Tn;
     for (const EncL& l : enc_) {
       launch_rmsnorm<T>(R, d, z_, d, l.n1, xn_, d, st_);
-      gemm(xn_, d, l.wqkv, R, epi(qkv_, 3 * d, false));
       Seg s;
       s.stride = Tn;
       s.fixed_len = Tn;
-      launch_attention<T>(U, Tn, H, dh, qkv_, 3 * d, qkv_ + d, 3 * d, qkv_ + 2 * d, 3 * d, att_, d, s, s, s, st_,
+      if (tc_attn_) {
+        gemm(xn_, d, l.wqk, R, epi(qkv_, 2 * d, false));
+        gemm(xn_, d, l.wv, R, vt_epi(vt_enc_, Tpad_, Tn, nullptr, nullptr, 0));
+        FmhaArgs f = fmha(U, Tn, qkv_, R, 2 * d, qkv_, R, 2 * d, d, vt_enc_, U, Tpad_, nullptr, s, s, s,
                           4.0 * U * Tn * Tn * d);
+        launch_fmha_tc(f, st_);
+      } else {
+        gemm(xn_, d, l.wqkv, R, epi(qkv_, 3 * d, false));
+        launch_attention<T>(U, Tn, H, dh, qkv_, 3 * d, qkv_ + d, 3 * d, qkv_ + 2 * d, 3 * d, att_, d, s, s, s, st_,
+                            4.0 * U * Tn * Tn * d);
+      }
       Epi eo = epi(z_, d, true);
       eo.resid = z_;
       eo.ld_resid = d;
@@ -860,14 +960,21 @@ class EngineT final : public Engine {
   void prepare_decoder(int U) {
     const int d = cfg_.d_model, Tn = enc_seq_len(cfg_);
     if constexpr (kBf16) launch_convert<T>(U * Tn, d, z_, d, zt_, d, st_);
-    gemm(zt_, d, xkv_w_, U * Tn, epi(xkv_, xkv_w_.N, false));
+    if (tc_attn_) {  // cross K of every decoder layer [rows][Ld*d]; cross V transposed per layer
+      gemm(zt_, d, xk_w_, U * Tn, epi(xkv_, xk_w_.N, false));
+      gemm(zt_, d, xv_w_, U * Tn,
+           vt_epi(vt_x_, Tpad_, Tn, nullptr, nullptr, static_cast<long long>(maxU_) * d * Tpad_));
+    } else {
+      gemm(zt_, d, xkv_w_, U * Tn, epi(xkv_, xkv_w_.N, false));
+    }
   }
 
   // One decoder position for `rows` rows (policy.cpp:267-295). Rows of a
   // group (user) are contiguous: group g = rows [gq.start(g), +gq.len(g)),
   // cross-attending to encoder rows [gk.start(g), +Tn).
+  // vt_user: encoder user of each group (NULL: group g is user g).
   void decode_step(int step, int rows, int groups, Seg gq, Seg gk, const int32_t* codes, int code_stride,
-                   const int32_t* anc, int anc_stride, int max_group_rows) {
+                   const int32_t* anc, int anc_stride, int max_group_rows, const int32_t* vt_user = nullptr) {
     const orx_config& c = cfg_;
     const int d = c.d_model, H = c.n_heads, dh = d / H, Ld = dec_layers(c), Tn = enc_seq_len(c);
     launch_dec_embed(rows, d, step == 0 ? bos_ : tokens_[step - 1], step == 0 ? nullptr : codes + (step - 1),
@@ -883,9 +990,16 @@ class EngineT final : public Engine {
       gemm(att_, d, w.so, rows, e);
       launch_rmsnorm<T>(rows, d, h_, d, w.n2, xn_, d, st_);
       gemm(xn_, d, w.cq, rows, epi(qkv_, d, false));
-      const int ldkv = 2 * d * Ld;
-      launch_attention<T>(groups, max_group_rows, H, dh, qkv_, d, xkv_ + (size_t)l * 2 * d, ldkv,
-                          xkv_ + (size_t)l * 2 * d + d, ldkv, att_, d, gq, gk, gq, st_, 4.0 * rows * Tn * d);
+      if (tc_attn_) {  // beam rows of a user over its cached encoder K / V^T (computed once, prepare_decoder)
+        FmhaArgs f = fmha(groups, max_group_rows, qkv_, rows, d, xkv_, static_cast<long long>(maxU_) * Tn, Ld * d,
+                          l * d, vt_x_ + static_cast<size_t>(l) * maxU_ * d * Tpad_, maxU_, Tpad_, vt_user, gq, gk,
+                          gq, 4.0 * rows * Tn * d);
+        launch_fmha_tc(f, st_);
+      } else {
+        const int ldkv = 2 * d * Ld;
+        launch_attention<T>(groups, max_group_rows, H, dh, qkv_, d, xkv_ + (size_t)l * 2 * d, ldkv,
+                            xkv_ + (size_t)l * 2 * d + d, ldkv, att_, d, gq, gk, gq, st_, 4.0 * rows * Tn * d);
+      }
       gemm(att_, d, w.co, rows, e);
       launch_rmsnorm<T>(rows, d, h_, d, w.n3, xn_, d, st_);
       if (c.moe_enabled) moe(w.moe, xn_, rows, h_, w.n3);
@@ -1010,6 +1124,9 @@ class EngineT final : public Engine {
     CUDA_CHECK(cudaMemcpyAsync(grp_start_, gs.data(), G * 4, cudaMemcpyHostToDevice, st_));
     CUDA_CHECK(cudaMemcpyAsync(grp_len_, gl.data(), G * 4, cudaMemcpyHostToDevice, st_));
     CUDA_CHECK(cudaMemcpyAsync(grp_kstart_, gk.data(), G * 4, cudaMemcpyHostToDevice, st_));
+    std::vector<int32_t> gu(G);
+    for (int g = 0; g < G; ++g) gu[g] = gk[g] / Tn;
+    CUDA_CHECK(cudaMemcpyAsync(grp_user_, gu.data(), G * 4, cudaMemcpyHostToDevice, st_));
     Seg gq;
     gq.start = grp_start_;
     gq.len = grp_len_;
@@ -1019,7 +1136,7 @@ class EngineT final : public Engine {
     std::vector<float> host(static_cast<size_t>(n) * V);
     if (ep_world_ > 1) max_len = L - 1;  // expert-parallel ranks run the same number of MoE layers
     for (int step = 0; step <= max_len; ++step) {
-      decode_step(step, n, G, gq, gkseg, tf_codes_, L, tf_anc_, L, max_group);
+      decode_step(step, n, G, gq, gkseg, tf_codes_, L, tf_anc_, L, max_group, grp_user_);
       CUDA_CHECK(cudaMemcpyAsync(host.data(), logits_, host.size() * 4, cudaMemcpyDeviceToHost, st_));
       CUDA_CHECK(cudaStreamSynchronize(st_));
       for (int r = 0; r < n; ++r)
@@ -1064,7 +1181,11 @@ class EngineT final : public Engine {
   std::vector<QBlock> qblocks_;
   std::vector<EncL> enc_;
   std::vector<DecL> dec_;
-  Lin<T> xkv_w_;
+  Lin<T> xkv_w_, xk_w_, xv_w_;
+  bool tc_attn_ = false;
+  int Tpad_ = 0, Lpad_ = 0;
+  T *vt_enc_ = nullptr, *vt_q_ = nullptr, *vt_x_ = nullptr;
+  int32_t* grp_user_ = nullptr;
   // activations
   int Fp_ = 0, Sp_ = 0;
   int64_t Rd_ = 0, S_ = 0;

@@ -80,6 +80,17 @@ __device__ __forceinline__ void epi_finish32(const Epi& e, int orow, float rs, i
     for (int j = 0; j < 32; ++j) v[j] += r[j];
   }
   const int oc = col0 + e.col_off;
+  if (e.vt) {  // transposed bf16 store: lanes (consecutive rows) write consecutive t
+    const int u = e.vt_row_user ? e.vt_row_user[orow] : orow / e.vt_T;
+    const int t = e.vt_row_pos ? e.vt_row_pos[orow] : orow % e.vt_T;
+    const int l = oc / e.vt_cols, m0 = oc - l * e.vt_cols;  // a 32-column chunk stays in one layer (vt_cols % 32 == 0)
+    __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(e.vt) + (long long)u * e.vt_user_stride + t +
+                          (long long)l * e.vt_layer_stride + (long long)m0 * e.vt_ld;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (full || col0 + j < e.n_out) base[(long long)j * e.vt_ld] = __float2bfloat16_rn(v[j]);
+    return;
+  }
   if (e.out_bf16) {
     __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)orow * e.ldo + oc;
     if (full && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
@@ -689,6 +700,8 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
   if (K % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0)
     throw std::invalid_argument("gemm_bf16: K and row strides must be multiples of 8");
   if (epi.swiglu && N % 256 != 0) throw std::invalid_argument("gemm_bf16: swiglu needs N % 256 == 0");
+  if (epi.vt && (epi.vt_cols % 32 != 0 || epi.col_off % 32 != 0))
+    throw std::invalid_argument("gemm_bf16: transposed store needs 32-column aligned layers");
   ProfScope ps(grp && grp->tile_expert ? PROF_GEMM_MOE : PROF_GEMM, stream,
                2.0 * (grp && grp->tile_expert ? double(grp->algo_rows) : double(M)) * N * K, 0.0);
   const bool grouped = grp && grp->tile_expert;

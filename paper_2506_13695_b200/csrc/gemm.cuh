@@ -30,6 +30,15 @@ struct Epi {
   int n_out = 0;    // number of valid output columns
   int m_valid = 0;  // rows >= m_valid are not stored
   int col_off = 0;  // added to output column index
+  // Transposed store (bf16 only; the attention V operand, K-major for P.V):
+  // element (row r, col n) goes to vt[u * vt_user_stride + t + (n % vt_cols) * vt_ld
+  //                                  + (n / vt_cols) * vt_layer_stride]
+  // with (u, t) = (vt_row_user[r], vt_row_pos[r]) or (r / vt_T, r % vt_T).
+  void* vt = nullptr;
+  int vt_ld = 0, vt_T = 0, vt_cols = 0;
+  long long vt_user_stride = 0, vt_layer_stride = 0;
+  const int32_t* vt_row_user = nullptr;
+  const int32_t* vt_row_pos = nullptr;
 };
 
 // Grouped (MoE) addressing: M tile i uses B rows [tile_expert[i]*b_rows_per_expert, ...).

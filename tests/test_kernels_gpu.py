@@ -9,6 +9,8 @@ Tolerances: fp32 outputs differ from torch only by accumulation order
 """
 import ctypes as C
 
+import numpy as np
+
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -232,3 +234,83 @@ def test_row_topk(V, k, ties):
     want_top = _ref_topk_keys(logits, pscore, plex, k, lse)
     got = torch.sort(cand ^ (-(1 << 63)), dim=1, descending=True).values
     assert torch.equal(got, want_top)
+
+
+def _attn_case(kind, H=2, dh=128, seed=0):
+    """(Q, K, V buffers, segment arrays, Vt) for the three attention uses of the hot path."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    d = H * dh
+    rnd = lambda *s: (torch.randn(*s, device="cuda", generator=g)).to(torch.bfloat16)  # noqa: E731
+    if kind == "encoder":  # self-attention over T=405 rows per user, fused QKV buffer (policy.cpp:261)
+        B, T = 3, 405
+        qkv = rnd(B * T, 3 * d)
+        Q, K, V = qkv, qkv, qkv
+        cols = (0, d, 2 * d)
+        qs = [(b * T, T) for b in range(B)]
+        ks = qs
+    elif kind == "qformer":  # 128 shared learned queries over ragged lifelong keys (nn.cpp:97-100)
+        klens = [2000, 1, 37]
+        B = len(klens)
+        Q = rnd(128, d)
+        kv = rnd(sum(klens), 2 * d)
+        K, V = kv, kv
+        cols = (0, 0, d)
+        starts = np.concatenate([[0], np.cumsum(klens)[:-1]])
+        qs = [(0, 128)] * B
+        ks = list(zip(starts.tolist(), klens))
+    else:  # decoder cross-attention: W=128 beam rows of a user over its 405 encoder rows (policy.cpp:284)
+        B, T, Wb = 2, 405, 128
+        Q = rnd(B * Wb, d)
+        kv = rnd(B * T, 2 * d)
+        K, V = kv, kv
+        cols = (0, 0, d)
+        qs = [(b * Wb, Wb) for b in range(B)]
+        ks = [(b * T, T) for b in range(B)]
+    Lmax = max(k for _, k in ks)
+    ld = (Lmax + 7) // 8 * 8
+    Vt = torch.zeros(B * H * dh, ld, device="cuda", dtype=torch.bfloat16)
+    for b, (s0, n) in enumerate(ks):
+        for h in range(H):
+            Vt[(b * H + h) * dh:(b * H + h + 1) * dh, :n] = V[s0:s0 + n, cols[2] + h * dh:cols[2] + (h + 1) * dh].t()
+    return B, H, dh, Q, K, V, cols, qs, ks, Vt
+
+
+@pytest.mark.parametrize("kind", ["encoder", "qformer", "cross"])
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_attention_bf16(kind, kernel):
+    """Segmented softmax(QK^T/sqrt(dh))V (mha_core, tape.cpp:822-905): the
+    mma.sync kernel (0) and the tcgen05/TMEM kernel (1, transposed V) vs torch fp32."""
+    B, H, dh, Q, K, V, cols, qs, ks, Vt = _attn_case(kind)
+    d = H * dh
+    rows_out = sum(n for _, n in qs)
+    O = torch.zeros(rows_out, d, device="cuda", dtype=torch.bfloat16)
+    ost = np.concatenate([[0], np.cumsum([n for _, n in qs])[:-1]])
+    i32 = lambda xs: torch.tensor(xs, device="cuda", dtype=torch.int32)  # noqa: E731
+    qst, qln = i32([s for s, _ in qs]), i32([n for _, n in qs])
+    kst, kln = i32([s for s, _ in ks]), i32([n for _, n in ks])
+    ostt = i32(ost.tolist())
+    L = _lib()
+    a = L.orx_attn_args()
+    a.B, a.max_q, a.heads, a.dh = B, max(n for _, n in qs), H, dh
+    a.Q, a.q_rows, a.ldq, a.q_col0 = _ptr(Q), Q.shape[0], Q.stride(0), cols[0]
+    a.K, a.k_rows, a.ldk, a.k_col0 = _ptr(K), K.shape[0], K.stride(0), cols[1]
+    a.V, a.ldv, a.v_col0 = _ptr(V), V.stride(0), cols[2]
+    a.Vt, a.vt_rows, a.vt_cols, a.vt_ld = _ptr(Vt), Vt.shape[0], Vt.shape[1], Vt.stride(0)
+    a.O, a.ldo = _ptr(O), O.stride(0)
+    a.q_start, a.q_len, a.k_start, a.k_len, a.o_start = _ptr(qst), _ptr(qln), _ptr(kst), _ptr(kln), _ptr(ostt)
+    a.kernel = kernel
+    L.check(L.lib().orx_debug_attention(C.byref(a), None))
+    torch.cuda.synchronize()
+    worst = 0.0
+    for b in range(B):
+        (q0, nq), (k0, nk) = qs[b], ks[b]
+        for h in range(H):
+            q = Q[q0:q0 + nq, cols[0] + h * dh:cols[0] + (h + 1) * dh].float()
+            k = K[k0:k0 + nk, cols[1] + h * dh:cols[1] + (h + 1) * dh].float()
+            v = V[k0:k0 + nk, cols[2] + h * dh:cols[2] + (h + 1) * dh].float()
+            ref = torch.softmax(q @ k.t() / dh ** 0.5, dim=-1) @ v
+            got = O[ost[b]:ost[b] + nq, h * dh:(h + 1) * dh].float()
+            err = ((got - ref).abs().max() / ref.abs().max().clamp_min(1e-6)).item()
+            worst = max(worst, err)
+    print(f"attention {kind} kernel {kernel}: max rel err {worst:.3e}")
+    assert worst < 3e-2

@@ -141,3 +141,42 @@ def test_cpp_dropin_shim_matches_reference():
     r = subprocess.run([demo, "16"], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("moe", [False, True])
+def test_bf16_tcgen05_attention_dh128(moe):
+    """bf16 engine with head dim 128 (the paper configs' dh): attention runs on
+    the tcgen05 flash kernel with V written transposed by the producing GEMMs
+    (encoder self-attention, QFormer over ragged lifelong keys, decoder cross
+    attention over the cached encoder K/V). Checked against the f64
+    reference and against the same engine on the mma.sync attention kernel."""
+    import os
+    over = dict(d_model=256, n_heads=2, ffn_hidden=512)
+    sets = ["d_model=256", "n_heads=2", "ffn_hidden=512"]
+    if moe:
+        over.update(moe_enabled=True, n_experts=8, experts_active=2)
+        sets += ["moe_enabled=1", "n_experts=8", "experts_active=2"]
+    lens = (20, 64, 300)
+    P, model = _model("0.015B", "bf16", max_users=2, max_width=32, **over)
+    _, refs = ref_dump("0.015B", 2, 32, lens=lens, sets=sets)
+    batch = P.SynthBatch(1, 0, 2, *lens)
+    z = model.encode_batch(batch)
+    codes, logp, _ = model.beam_search_arrays(batch, 32)
+    os.environ["ORX_ATTN_MMA_SYNC"] = "1"
+    try:
+        _, ref_model = _model("0.015B", "bf16", max_users=2, max_width=32, **over)
+    finally:
+        del os.environ["ORX_ATTN_MMA_SYNC"]
+    z_mma = ref_model.encode_batch(batch)
+    for u, ref in enumerate(refs):
+        pres = prefixes_of(ref["prefixes"])
+        lg = model.score_prefixes(batch, [u] * len(pres), pres)
+        lg_mma = ref_model.score_prefixes(batch, [u] * len(pres), pres)
+        el = max(rel_inf(lg[i], ref["logits"][i]) for i in range(len(pres)))
+        el_mma = max(rel_inf(lg_mma[i], ref["logits"][i]) for i in range(len(pres)))
+        ez = rel_inf(z[u], ref["z"])
+        overlap = len({tuple(c) for c in codes[u]} & {tuple(c) for c in ref["beam_codes"]})
+        print(f"dh=128 bf16 moe={moe} user {u}: z {ez:.3e} (mma.sync {rel_inf(z_mma[u], ref['z']):.3e}) "
+              f"logits {el:.3e} (mma.sync {el_mma:.3e}) overlap {overlap}/32")
+        assert el < 5e-2 and overlap >= 16
+        assert el < 2 * el_mma + 1e-2  # no worse than the mma.sync attention path

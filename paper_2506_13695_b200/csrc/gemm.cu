@@ -54,11 +54,67 @@ __device__ __forceinline__ void epi_load_resid(const Epi& e, int orow, int col0,
   }
 }
 
+// Specialised epilogue for a full, aligned 32-column chunk: MODE is the
+// Epi::mode bit set (no per-element predication, vector bias loads).
+template <int MODE>
+__device__ __forceinline__ void epi_fast(const Epi& e, int orow, float rs, int col0, float (&v)[32],
+                                         const float (&r)[32]) {
+  if (MODE & EPI_BIAS) {
+    const float4* b4 = reinterpret_cast<const float4*>(e.bias + col0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 b = __ldg(b4 + q);
+      v[4 * q] += b.x, v[4 * q + 1] += b.y, v[4 * q + 2] += b.z, v[4 * q + 3] += b.w;
+    }
+  }
+  if (MODE & EPI_LEAKY) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = v[j] > 0.f ? v[j] : 0.01f * v[j];  // tape.hpp:88
+  }
+  if (MODE & EPI_SILU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = silu_fast(v[j]);
+  }
+  if (MODE & EPI_RS) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] *= rs;
+  }
+  if (MODE & EPI_RESID) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] += r[j];
+  }
+  const int oc = col0 + e.col_off;
+  if (MODE & EPI_BF16) {
+    uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)orow * e.ldo + oc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      op[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                         pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+  } else {
+    float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)orow * e.ldo + oc);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) op[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+}
+
 // bias -> activation -> row scale -> + residual -> store (bf16 or fp32)
 __device__ __forceinline__ void epi_finish32(const Epi& e, int orow, float rs, int col0, float (&v)[32],
                                              const float (&r)[32], bool has_res) {
   if (col0 >= e.n_out) return;
   const bool full = col0 + 32 <= e.n_out;
+  if (full && e.mode >= 0) {  // host verified alignment and that the flags match a specialised mode
+    switch (e.mode) {
+      case 0: epi_fast<0>(e, orow, rs, col0, v, r); return;
+      case EPI_RS: epi_fast<EPI_RS>(e, orow, rs, col0, v, r); return;
+      case EPI_RESID: epi_fast<EPI_RESID>(e, orow, rs, col0, v, r); return;
+      case EPI_BIAS | EPI_RESID: epi_fast<EPI_BIAS | EPI_RESID>(e, orow, rs, col0, v, r); return;
+      case EPI_BF16: epi_fast<EPI_BF16>(e, orow, rs, col0, v, r); return;
+      case EPI_BIAS | EPI_BF16: epi_fast<EPI_BIAS | EPI_BF16>(e, orow, rs, col0, v, r); return;
+      case EPI_BIAS | EPI_LEAKY | EPI_BF16: epi_fast<EPI_BIAS | EPI_LEAKY | EPI_BF16>(e, orow, rs, col0, v, r); return;
+      case EPI_BIAS | EPI_SILU | EPI_BF16: epi_fast<EPI_BIAS | EPI_SILU | EPI_BF16>(e, orow, rs, col0, v, r); return;
+      default: break;
+    }
+  }
   if (e.bias) {
 #pragma unroll
     for (int j = 0; j < 32; ++j)
@@ -157,25 +213,20 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tb, int row
     constexpr int CH = BN / 32 / 2;
     const bool hr = ok && e.resid != nullptr;
     float rc[32];
-    if (hr) epi_load_resid(e, orow, nt * BN + half * CH * 32, rc);
+    if (hr) epi_load_resid(e, orow, nt * BN + half * CH * 32, rc);  // in flight while the MMAs finish
     mbar_wait(tfull, acc_phase);
     tc_fence_after();
-#pragma unroll
+#pragma unroll 1
     for (int i = 0; i < CH; ++i) {
       const int c = half * CH + i;
       uint32_t ra[32];
       tmem_ld32_async(tb + c * 32, ra);
-      float rn[32];
-      if (hr && i + 1 < CH) epi_load_resid(e, orow, nt * BN + (c + 1) * 32, rn);
+      if (hr && i > 0) epi_load_resid(e, orow, nt * BN + c * 32, rc);  // overlaps the TMEM load
       tmem_wait_ld();
       float v[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(ra[j]);
       if (ok) epi_finish32(e, orow, rs, nt * BN + c * 32, v, rc, hr);
-      if (i + 1 < CH) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) rc[j] = rn[j];
-      }
     }
   }
 }
@@ -615,6 +666,30 @@ void launch_tc2(const void* A, int lda, const void* B, int ldb, int M, int N, in
 
 }  // namespace
 
+// Specialised epilogue mode of a launch (-1: generic path). Requires the
+// output rows / bias to be 16-byte aligned per 32-column chunk.
+int epi_mode(const Epi& e) {
+  if (e.vt) return -1;
+  const int esz = e.out_bf16 ? 2 : 4;
+  if ((reinterpret_cast<uintptr_t>(e.out) % 16) || ((long long)e.ldo * esz) % 16 || (e.col_off * esz) % 16) return -1;
+  if (e.resid && ((reinterpret_cast<uintptr_t>(e.resid) % 16) || (e.ld_resid % 4))) return -1;
+  if (e.bias && reinterpret_cast<uintptr_t>(e.bias) % 16) return -1;
+  int m = 0;
+  if (e.bias) m |= EPI_BIAS;
+  if (e.act == ACT_LEAKY) m |= EPI_LEAKY;
+  if (e.act == ACT_SILU) m |= EPI_SILU;
+  if (e.row_scale) m |= EPI_RS;
+  if (e.resid) m |= EPI_RESID;
+  if (e.out_bf16) m |= EPI_BF16;
+  switch (m) {
+    case 0: case EPI_RS: case EPI_RESID: case EPI_BIAS | EPI_RESID: case EPI_BF16: case EPI_BIAS | EPI_BF16:
+    case EPI_BIAS | EPI_LEAKY | EPI_BF16: case EPI_BIAS | EPI_SILU | EPI_BF16:
+      return m;
+    default:
+      return -1;
+  }
+}
+
 bool& force_single_cta() {
   static bool f = getenv("ORX_GEMM_SINGLE_CTA") != nullptr;
   return f;
@@ -704,18 +779,20 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
     throw std::invalid_argument("gemm_bf16: transposed store needs 32-column aligned layers");
   ProfScope ps(grp && grp->tile_expert ? PROF_GEMM_MOE : PROF_GEMM, stream,
                2.0 * (grp && grp->tile_expert ? double(grp->algo_rows) : double(M)) * N * K, 0.0);
+  Epi ep = epi;
+  ep.mode = epi_mode(ep);
   const bool grouped = grp && grp->tile_expert;
   const bool pair = grouped ? grp->tile_rows == 2 * kBM : (M > kBM && !force_single_cta());
   if (pair) {
     if (N <= 128 && !epi.swiglu)
-      launch_tc2<128, 8>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+      launch_tc2<128, 8>(A, lda, B, ldb, M, N, K, ep, grp, stream);
     else
-      launch_tc2<256, 6>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+      launch_tc2<256, 6>(A, lda, B, ldb, M, N, K, ep, grp, stream);
   } else {
     if (N <= 128 && !epi.swiglu)
-      launch_tc<128, 6>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+      launch_tc<128, 6>(A, lda, B, ldb, M, N, K, ep, grp, stream);
     else
-      launch_tc<256, 4>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+      launch_tc<256, 4>(A, lda, B, ldb, M, N, K, ep, grp, stream);
   }
 }
 

@@ -15,6 +15,8 @@
 namespace orx {
 
 enum Act { ACT_NONE = 0, ACT_LEAKY = 1, ACT_SILU = 2 };
+// Epilogue mode bits (Epi::mode, set by the launcher): specialised code paths.
+enum EpiMode { EPI_BIAS = 1, EPI_LEAKY = 2, EPI_SILU = 4, EPI_RS = 8, EPI_RESID = 16, EPI_BF16 = 32 };
 
 struct Epi {
   const float* bias = nullptr;       // [N] (or [N/2] for swiglu: not used)
@@ -39,6 +41,7 @@ struct Epi {
   long long vt_user_stride = 0, vt_layer_stride = 0;
   const int32_t* vt_row_user = nullptr;
   const int32_t* vt_row_pos = nullptr;
+  int mode = -1;  // EpiMode bits of a specialised path, -1 = generic (set by gemm_bf16)
 };
 
 // Grouped (MoE) addressing: M tile i uses B rows [tile_expert[i]*b_rows_per_expert, ...).
@@ -64,6 +67,7 @@ void gemm_f32(const float* A, int lda, const float* B, int ldb, int M, int N, in
 int num_sms();
 // ORX_GEMM_SINGLE_CTA=1 disables the CTA-pair kernel for dense GEMMs (A/B comparison).
 bool& force_single_cta();
+int epi_mode(const Epi& e);
 long long& launch_counter();
 
 // Optional per-kernel-class timing with CUDA events on the launching stream

@@ -163,6 +163,26 @@ int orx_score_prefixes(orx_engine* e, const orx_user_batch* batch, int32_t n, co
 /* encode + unconstrained beam search of depth n_code_layers, batched. */
 int orx_beam_search(orx_engine* e, const orx_user_batch* batch, int32_t width, orx_beam_out* out);
 
+/* Semantic-ID trie (SemanticTrie, trie.hpp:27-62) as CSR over prefix nodes:
+ * node 0 is the root, node n's children are entries [child_off[n],
+ * child_off[n+1]) of child_code (strictly ascending) / child_node. Uploaded
+ * to the device for orx_beam_search_constrained (generation.cpp:58-64). */
+typedef struct orx_trie {
+  int32_t n_nodes;
+  const int32_t* child_off; /* [n_nodes + 1] */
+  int64_t n_edges;
+  const int32_t* child_code; /* [n_edges] */
+  const int32_t* child_node; /* [n_edges] */
+} orx_trie;
+int orx_engine_set_trie(orx_engine* e, const orx_trie* trie);
+/* Beam search expanding only trie children (GenerationRequest::constrain_to_trie);
+ * n_items[u] < width when the trie offers fewer candidates. */
+int orx_beam_search_constrained(orx_engine* e, const orx_user_batch* batch, int32_t width, orx_beam_out* out);
+/* PolicyModel::sequence_log_prob (policy.cpp:297-310): log-prob (f64) of the
+ * full semantic id codes[q * n_code_layers ...] for user user[q] of the batch. */
+int orx_sequence_log_prob(orx_engine* e, const orx_user_batch* batch, int32_t n, const int32_t* user,
+                          const int32_t* codes, double* log_prob_out);
+
 /* Same as orx_beam_search, but inputs are already resident on the device
  * (uploaded by orx_engine_stage_batch); results stay on the device unless
  * out is non-NULL. Used to time the kernel path without host copies. */

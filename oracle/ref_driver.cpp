@@ -127,6 +127,9 @@ struct Args {
   bool beam = true;
   int procs = 1;
   int calls = 4;
+  int trie_items = 0;      // > 0: constrained beam search over a seeded random trie
+  uint64_t trie_seed = 77;
+  int trie_fanout = 0;     // > 0: codes drawn from [0, fanout) per level (a dense trie)
 };
 
 Args parse(int argc, char** argv) {
@@ -157,6 +160,9 @@ Args parse(int argc, char** argv) {
     else if (k == "--no-beam") a.beam = false;
     else if (k == "--procs") a.procs = std::stoi(next());
     else if (k == "--calls") a.calls = std::stoi(next());
+    else if (k == "--trie-items") a.trie_items = std::stoi(next());
+    else if (k == "--trie-seed") a.trie_seed = std::stoull(next());
+    else if (k == "--trie-fanout") a.trie_fanout = std::stoi(next());
     else throw std::invalid_argument("unknown option " + k);
   }
   if (!a.lens_set) {
@@ -205,7 +211,21 @@ int cmd_dump(const Args& a) {
   const PolicyConfig& cfg = model.config();
   int V = cfg.codebook_size, L = cfg.n_code_layers;
   SemanticTrie trie(L);
-  trie.insert(SemanticId{std::vector<int>(static_cast<size_t>(L), 0)}, 0);
+  if (a.trie_items > 0) {
+    // seeded random item catalogue (codes per level in [0, fanout or V)); written for the engine side
+    Rng tr(a.trie_seed);
+    const int range = a.trie_fanout > 0 ? a.trie_fanout : V;
+    std::vector<int32_t> tc;
+    for (int it = 0; it < a.trie_items; ++it) {
+      std::vector<int> c(static_cast<size_t>(L));
+      for (int j = 0; j < L; ++j) c[size_t(j)] = static_cast<int>(tr.randint(range));
+      for (int x : c) tc.push_back(x);
+      trie.insert(SemanticId{c}, it);
+    }
+    write_npy(a.out + "/trie_codes.npy", "<i4", {size_t(a.trie_items), size_t(L)}, tc.data(), tc.size() * 4);
+  } else {
+    trie.insert(SemanticId{std::vector<int>(static_cast<size_t>(L), 0)}, 0);
+  }
   for (int i = 0; i < a.n_users; ++i) {
     int u = a.user_begin + i;
     UserContext ctx = make_user(a, u);
@@ -218,15 +238,22 @@ int cmd_dump(const Args& a) {
     if (a.beam) {
       GenerationRequest req;
       req.width = a.width;
+      req.constrain_to_trie = a.trie_items > 0;
       auto items = beam_search(req, policy_scorer(model, z), L, V, trie);
       std::vector<int32_t> codes;
-      std::vector<double> lp;
+      std::vector<double> lp, seq;
       for (auto& it : items) {
         for (int c : it.codes.codes) codes.push_back(c);
         lp.push_back(it.log_prob);
+        // teacher-forced sequence log-prob of the same item (policy.cpp:297-310), eval session
+        Tape tape;
+        ParamSession ps(tape, model.params(), false);
+        Var zv = tape.leaf(z);
+        seq.push_back(model.sequence_log_prob(ps, zv, it.codes).value().at(0));
       }
       write_npy(upath(a, "beam_codes", u), "<i4", {items.size(), size_t(L)}, codes.data(), codes.size() * 4);
       write_npy(upath(a, "beam_logp", u), "<f8", {items.size()}, lp.data(), lp.size() * 8);
+      write_npy(upath(a, "seq_logp", u), "<f8", {seq.size()}, seq.data(), seq.size() * 8);
       std::set<std::vector<int>> seen;
       for (int len = 1; len < L; ++len)
         for (int j = 0; j < static_cast<int>(items.size()) && j < a.n_prefix; ++j) {

@@ -46,6 +46,11 @@ class orx_beam_out(C.Structure):
                 ("n_items", C.POINTER(C.c_int32))]
 
 
+class orx_trie(C.Structure):
+    _fields_ = [("n_nodes", C.c_int32), ("child_off", C.POINTER(C.c_int32)), ("n_edges", C.c_int64),
+                ("child_code", C.POINTER(C.c_int32)), ("child_node", C.POINTER(C.c_int32))]
+
+
 class orx_gemm_args(C.Structure):
     _fields_ = [
         ("A", C.c_void_p), ("lda", C.c_int32), ("B", C.c_void_p), ("ldb", C.c_int32),
@@ -104,6 +109,10 @@ SIGNATURES = [
     ("orx_next_logits", C.c_int, [_P, _F32P, C.c_int32, C.c_int32, _I32P, _I32P, _I32P, _F32P]),
     ("orx_score_prefixes", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, _I32P, _I32P, _I32P, _F32P]),
     ("orx_beam_search", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, C.POINTER(orx_beam_out)]),
+    ("orx_engine_set_trie", C.c_int, [_P, C.POINTER(orx_trie)]),
+    ("orx_beam_search_constrained", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, C.POINTER(orx_beam_out)]),
+    ("orx_sequence_log_prob", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, _I32P, _I32P,
+                                        C.POINTER(C.c_double)]),
     ("orx_engine_stage_batch", C.c_int, [_P, C.POINTER(orx_user_batch)]),
     ("orx_beam_search_staged", C.c_int, [_P, C.c_int32, C.POINTER(orx_beam_out)]),
     ("orx_engine_stats", C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -197,48 +197,66 @@ __global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows,
   const float* lg = logits + (size_t)row * V;
   const float4* lg4 = reinterpret_cast<const float4*>(lg);
   const int V4 = V >> 2;  // V % 4 == 0 (launch condition)
-  float mx = -FLT_MAX, s1 = 0.f, s2 = 0.f;
-  for (int i = lane; i < V4; i += 32) {
+  // One streaming pass. The survivor threshold tx comes from the first 1024
+  // logits (mean / spread estimate); the softmax sum is taken relative to that
+  // sample's max (a second pass only if the true max is far above it); loads
+  // are issued 8 deep per lane.
+  constexpr int U8 = 8;
+  float m0 = -FLT_MAX, s1 = 0.f, s2 = 0.f;
+  const int nsamp = min(V4, 256);
+  for (int i = lane; i < nsamp; i += 32) {
     const float4 x = __ldg(lg4 + i);
-    mx = fmaxf(mx, fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
+    m0 = fmaxf(m0, fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
     s1 += (x.x + x.y) + (x.z + x.w);
     s2 += (x.x * x.x + x.y * x.y) + (x.z * x.z + x.w * x.w);
   }
-  mx = warp_max(mx);
+  m0 = warp_max(m0);
   s1 = warp_sum(s1);
   s2 = warp_sum(s2);
-  const float mean = s1 / V, sd = sqrtf(fmaxf(s2 / V - mean * mean, 0.f));
+  const float mean = s1 / (4 * nsamp), sd = sqrtf(fmaxf(s2 / (4 * nsamp) - mean * mean, 0.f));
   // survivors: ~2.5 k_sel, but on average at most half of the slots per lane
   const float target = fminf(2.5f * k_sel, 16.f * kLaneSlots);
-  float tx = fminf(mean + normal_upper_quantile(target / V) * sd, mx);
+  float tx = mean + normal_upper_quantile(target / V) * sd;
   float* sx = bx[w] + lane * kLaneSlots;
   int32_t* si = bi[w] + lane * kLaneSlots;
-  float se = 0.f, rej = -FLT_MAX;
+  float se = 0.f, rej = -FLT_MAX, mx = -FLT_MAX;
   int n = 0, total = 0;
   bool ok = false;
   for (int attempt = 0; attempt < 4; ++attempt) {
     n = 0;
     rej = -FLT_MAX;
     bool over = false;
-    for (int i = lane; i < V4; i += 32) {
-      const float4 x = __ldg(lg4 + i);
-      if (attempt == 0) se += (__expf(x.x - mx) + __expf(x.y - mx)) + (__expf(x.z - mx) + __expf(x.w - mx));
-      const float xs[4] = {x.x, x.y, x.z, x.w};
+    for (int i0 = lane; i0 < V4; i0 += 32 * U8) {
+      float4 xb[U8];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (xs[e] >= tx) {
-          if (n < kLaneSlots) {
-            sx[n] = xs[e];
-            si[n] = 4 * i + e;
+      for (int u = 0; u < U8; ++u) xb[u] = i0 + 32 * u < V4 ? __ldg(lg4 + i0 + 32 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < U8; ++u) {
+        const int i = i0 + 32 * u;
+        if (i >= V4) continue;
+        const float4 x = xb[u];
+        if (attempt == 0) {
+          mx = fmaxf(mx, fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
+          se += (__expf(x.x - m0) + __expf(x.y - m0)) + (__expf(x.z - m0) + __expf(x.w - m0));
+        }
+        const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (xs[e] >= tx) {
+            if (n < kLaneSlots) {
+              sx[n] = xs[e];
+              si[n] = 4 * i + e;
+            } else {
+              over = true;
+            }
+            ++n;
           } else {
-            over = true;
+            rej = fmaxf(rej, xs[e]);
           }
-          ++n;
-        } else {
-          rej = fmaxf(rej, xs[e]);
         }
       }
     }
+    if (attempt == 0) mx = warp_max(mx);
     total = __reduce_add_sync(0xffffffffu, n);
     over = __any_sync(0xffffffffu, over);
     if (total >= k_sel && !over) {
@@ -250,7 +268,16 @@ __global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows,
     if (!(sd > 0.f)) break;
   }
   se = warp_sum(se);
-  const float lse = mx + logf(se);
+  if (mx > m0 + 60.f) {  // the sample's max was far below the row's: exact sum in a second pass
+    se = 0.f;
+    for (int i = lane; i < V4; i += 32) {
+      const float4 x = __ldg(lg4 + i);
+      se += (__expf(x.x - mx) + __expf(x.y - mx)) + (__expf(x.z - mx) + __expf(x.w - mx));
+    }
+    se = warp_sum(se);
+    m0 = mx;
+  }
+  const float lse = m0 + logf(se);
   const float ps = pscore[row];
   if (lane == 0) lse_out[row] = lse;
   uint64_t* out = cand + (size_t)row * k_sel;
@@ -331,7 +358,7 @@ __global__ void __launch_bounds__(kMergeThreads) beam_merge_kernel(int n_live, i
                                                                    int step, const uint64_t* __restrict__ cand,
                                                                    const float* __restrict__ logits,
                                                                    const float* __restrict__ lse, BeamState cur,
-                                                                   BeamState nxt) {
+                                                                   BeamState nxt, TrieDev trie, int use_trie) {
   __shared__ uint64_t sel[kMaxBeam];
   __shared__ uint64_t lex[kMaxBeam];
   __shared__ uint32_t hist[256];
@@ -346,22 +373,53 @@ __global__ void __launch_bounds__(kMergeThreads) beam_merge_kernel(int n_live, i
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += kMergeThreads) {
     uint64_t key = c[i];
-    if (key >= tau) {
+    if (key >= tau && key != 0) {  // key 0 = no candidate (constrained search)
       uint32_t pos = atomicAdd(&counter, 1u);
       if (pos < static_cast<uint32_t>(n_new)) sel[pos] = key;
     }
   }
   __syncthreads();
+  for (int i = static_cast<int>(min(counter, static_cast<uint32_t>(n_new))) + threadIdx.x; i < n_new; i += kMergeThreads)
+    sel[i] = 0;  // fewer candidates than slots: empty slots sort last
+  __syncthreads();
   block_sort_desc<kMaxBeam, kMergeThreads>(sel, n_new);
   // beam b (rank order): decode parent lexrank + code, build next state
   for (int b = threadIdx.x; b < n_new; b += kMergeThreads) {
     const uint64_t key = sel[b];
+    const int nrow = u * n_new + b;
+    if (key == 0) {  // empty slot: decodes harmlessly (code 0, ancestors = its user's first row)
+      const int prow = u * n_live;
+      for (int j = 0; j < step; ++j) {
+        nxt.codes[(size_t)nrow * L + j] = 0;
+        nxt.anc[(size_t)nrow * L + j] = cur.anc[(size_t)prow * L + j];
+      }
+      nxt.codes[(size_t)nrow * L + step] = 0;
+      nxt.anc[(size_t)nrow * L + step] = prow;
+      nxt.score[nrow] = -FLT_MAX;
+      nxt.score64[nrow] = -INFINITY;
+      if (use_trie) nxt.node[nrow] = -1;
+      lex[b] = (static_cast<uint64_t>(0xFFFFFFFFu) << 32) | static_cast<uint32_t>(b);
+      continue;
+    }
     const uint32_t low = 0xFFFFFFFFu - static_cast<uint32_t>(key & 0xFFFFFFFFu);
     const int plr = static_cast<int>(low / static_cast<uint32_t>(V));
     const int code = static_cast<int>(low % static_cast<uint32_t>(V));
     const int pb = cur.lex2beam[(size_t)u * n_live + plr];
     const int prow = u * n_live + pb;
-    const int nrow = u * n_new + b;
+    if (use_trie) {  // child of the parent's node with this code (codes ascending)
+      const int p = cur.node[prow];
+      int lo = trie.child_off[p], hi = trie.child_off[p + 1] - 1, found = -1;
+      while (lo <= hi) {
+        const int mid = (lo + hi) >> 1, cc = trie.child_code[mid];
+        if (cc == code) {
+          found = trie.child_node[mid];
+          break;
+        }
+        if (cc < code) lo = mid + 1;
+        else hi = mid - 1;
+      }
+      nxt.node[nrow] = found;
+    }
     for (int j = 0; j < step; ++j) {
       nxt.codes[(size_t)nrow * L + j] = cur.codes[(size_t)prow * L + j];
       nxt.anc[(size_t)nrow * L + j] = cur.anc[(size_t)prow * L + j];
@@ -395,6 +453,91 @@ __global__ void beam_init_kernel(int users, BeamState st) {
   st.score64[u] = 0.0;
   st.lexrank[u] = 0;
   st.lex2beam[u] = 0;
+  if (st.node) st.node[u] = 0;  // trie root
+}
+
+// Constrained candidates (generation.cpp:58-64): block per row; the log-softmax
+// normaliser runs over the whole row, candidates are the node's trie children.
+__global__ void __launch_bounds__(kRowThreads) row_topk_trie_kernel(int V, int k_sel, const float* __restrict__ logits,
+                                                                    const float* __restrict__ pscore,
+                                                                    const int32_t* __restrict__ plex,
+                                                                    const int32_t* __restrict__ node, TrieDev trie,
+                                                                    float* __restrict__ lse_out,
+                                                                    uint64_t* __restrict__ cand) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t bc[4];
+  __shared__ float red[kRowThreads / 32];
+  __shared__ uint32_t counter;
+  const int row = blockIdx.x;
+  const float* lg = logits + (size_t)row * V;
+  uint64_t* out = cand + (size_t)row * k_sel;
+  const int nd = node[row];
+  if (nd < 0) {  // empty slot: no candidates
+    for (int i = threadIdx.x; i < k_sel; i += kRowThreads) out[i] = 0;
+    if (threadIdx.x == 0) lse_out[row] = 0.f;
+    return;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float mx = -FLT_MAX;
+  for (int i = threadIdx.x; i < V; i += kRowThreads) mx = fmaxf(mx, lg[i]);
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int w = 1; w < kRowThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+  __syncthreads();
+  float sum = 0.f;
+  for (int i = threadIdx.x; i < V; i += kRowThreads) sum += __expf(lg[i] - mx);
+  sum = warp_sum(sum);
+  if (lane == 0) red[warp] = sum;
+  __syncthreads();
+  sum = 0.f;
+  for (int w = 0; w < kRowThreads / 32; ++w) sum += red[w];
+  const float lse = mx + logf(sum);
+  const float ps = pscore[row];
+  const uint32_t lbase = static_cast<uint32_t>(plex[row]) * static_cast<uint32_t>(V);
+  const int o0 = trie.child_off[nd], nc = trie.child_off[nd + 1] - o0;
+  auto key_of = [&](int i) -> uint64_t {
+    const int code = trie.child_code[o0 + i];
+    const float sc = ps + (lg[code] - lse);
+    return (static_cast<uint64_t>(ord_f32(sc)) << 32) | (0xFFFFFFFFu - (lbase + static_cast<uint32_t>(code)));
+  };
+  if (threadIdx.x == 0) {
+    lse_out[row] = lse;
+    counter = 0;
+  }
+  if (nc <= k_sel) {
+    for (int i = threadIdx.x; i < k_sel; i += kRowThreads) out[i] = i < nc ? key_of(i) : 0;
+    return;
+  }
+  __syncthreads();
+  const uint64_t tau = block_kth_largest<kRowThreads>(nc, k_sel, key_of, hist, bc);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nc; i += kRowThreads) {
+    const uint64_t key = key_of(i);
+    if (key >= tau) {
+      const uint32_t pos = atomicAdd(&counter, 1u);
+      if (pos < static_cast<uint32_t>(k_sel)) out[pos] = key;
+    }
+  }
+}
+
+// Warp per row: acc[r] += logits[r][code] - lse(logits[r]) in f64.
+__global__ void pick_logprob_kernel(int rows, int V, const float* __restrict__ logits, const int32_t* __restrict__ codes,
+                                    int code_stride, int step, double* __restrict__ acc) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* lg = logits + (size_t)r * V;
+  float mx = -FLT_MAX;
+  for (int i = lane; i < V; i += 32) mx = fmaxf(mx, lg[i]);
+  mx = warp_max(mx);
+  float sum = 0.f;
+  for (int i = lane; i < V; i += 32) sum += __expf(lg[i] - mx);
+  sum = warp_sum(sum);
+  if (lane == 0) {
+    const int code = codes[(size_t)r * code_stride + step];
+    acc[r] += static_cast<double>(lg[code]) - (static_cast<double>(mx) + log(static_cast<double>(sum)));
+  }
 }
 
 }  // namespace
@@ -418,12 +561,30 @@ void launch_row_topk(int rows, int V, int k_sel, const float* logits, const floa
       row_topk_warp_kernel<64><<<(rows + 1) / 2, 64, 0, s>>>(rows, V, k_sel, logits, parent_score, parent_lexrank,
                                                              lse, cand, fail);
     // rows the warp kernel could not decide (usually none): exact radix select
-    row_topk_kernel<<<std::min(rows, 2 * num_sms()), kRowThreads, smem, s>>>(V, k_sel, logits, parent_score,
+    row_topk_kernel<<<std::min(rows, 32), kRowThreads, smem, s>>>(V, k_sel, logits, parent_score,
                                                                             parent_lexrank, lse, cand, fail);
     launch_counter() += 2;
     return;
   }
   row_topk_kernel<<<rows, kRowThreads, smem, s>>>(V, k_sel, logits, parent_score, parent_lexrank, lse, cand, nullptr);
+  ++launch_counter();
+}
+
+void launch_row_topk_trie(int rows, int V, int k_sel, const float* logits, const float* parent_score,
+                          const int32_t* parent_lexrank, const int32_t* node, TrieDev trie, float* lse,
+                          uint64_t* cand, cudaStream_t s) {
+  if (rows <= 0) return;
+  ProfScope ps(PROF_BEAM, s, 0.0, double(rows) * V * 4);
+  row_topk_trie_kernel<<<rows, kRowThreads, 0, s>>>(V, k_sel, logits, parent_score, parent_lexrank, node, trie, lse,
+                                                    cand);
+  ++launch_counter();
+}
+
+void launch_pick_logprob(int rows, int V, const float* logits, const int32_t* codes, int code_stride, int step,
+                         double* acc, cudaStream_t s) {
+  if (rows <= 0) return;
+  ProfScope ps(PROF_BEAM, s, 0.0, double(rows) * V * 4);
+  pick_logprob_kernel<<<(rows + 7) / 8, 256, 0, s>>>(rows, V, logits, codes, code_stride, step, acc);
   ++launch_counter();
 }
 
@@ -438,11 +599,12 @@ unsigned long long topk_fallback_rows(bool reset) {
 }
 
 void launch_beam_merge(int users, int n_live, int k_sel, int n_new, int V, int L, int step, const uint64_t* cand,
-                       const float* logits, const float* lse, const BeamState& cur, BeamState& nxt,
-                       cudaStream_t s) {
+                       const float* logits, const float* lse, const BeamState& cur, BeamState& nxt, cudaStream_t s,
+                       const TrieDev* trie) {
   if (n_new > kMaxBeam) throw std::invalid_argument("beam width above 1024 is not supported");
   ProfScope ps(PROF_BEAM, s, 0.0, 0.0);
-  beam_merge_kernel<<<users, kMergeThreads, 0, s>>>(n_live, k_sel, n_new, V, L, step, cand, logits, lse, cur, nxt);
+  beam_merge_kernel<<<users, kMergeThreads, 0, s>>>(n_live, k_sel, n_new, V, L, step, cand, logits, lse, cur, nxt,
+                                                    trie ? *trie : TrieDev{}, trie ? 1 : 0);
   ++launch_counter();
 }
 

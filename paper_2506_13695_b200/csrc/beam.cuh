@@ -21,7 +21,29 @@ struct BeamState {  // live beams of one step, row r = user * n_live + beam
   int32_t* lexrank = nullptr;   // [rows]
   int32_t* lex2beam = nullptr;  // [users][n_live]
   int32_t* anc = nullptr;       // [rows][L] ancestor row per position
+  int32_t* node = nullptr;      // [rows] semantic-trie node of the prefix (constrained search), -1 = empty slot
 };
+
+// Semantic-ID trie on the device (SemanticTrie, trie.hpp:27-62) as CSR over
+// prefix nodes: node 0 = root; children of n are [child_off[n], child_off[n+1])
+// of child_code (ascending) / child_node.
+struct TrieDev {
+  const int32_t* child_off = nullptr;
+  const int32_t* child_code = nullptr;
+  const int32_t* child_node = nullptr;
+};
+
+// Constrained variant of launch_row_topk (generation.cpp:58-64): lse over the
+// whole row, candidates only the trie children of the row's node; rows with
+// fewer than k_sel children (or no node) pad with key 0 (= no candidate).
+void launch_row_topk_trie(int rows, int V, int k_sel, const float* logits, const float* parent_score,
+                          const int32_t* parent_lexrank, const int32_t* node, TrieDev trie, float* lse,
+                          uint64_t* cand, cudaStream_t s);
+
+// acc[r] += logits[r][code[r * code_stride + step]] - logsumexp(logits[r]) (f64):
+// one position of PolicyModel::sequence_log_prob (policy.cpp:297-310).
+void launch_pick_logprob(int rows, int V, const float* logits, const int32_t* codes, int code_stride, int step,
+                         double* acc, cudaStream_t s);
 
 // Per row: lse = logsumexp(logits), then the top k_sel candidate keys.
 // fail: device workspace of rows + 1 ints (fast path's undecided rows); NULL
@@ -34,7 +56,10 @@ unsigned long long topk_fallback_rows(bool reset);
 
 // Per user: top n_new of n_live * k_sel candidates, sorted; builds the next
 // BeamState (codes, scores, lexranks, ancestors).
+// With a trie (constrained search) key 0 marks "no candidate": users may end a
+// step with fewer than n_new live beams (the rest are empty slots, node -1).
 void launch_beam_merge(int users, int n_live, int k_sel, int n_new, int V, int L, int step, const uint64_t* cand,
-                       const float* logits, const float* lse, const BeamState& cur, BeamState& nxt, cudaStream_t s);
+                       const float* logits, const float* lse, const BeamState& cur, BeamState& nxt, cudaStream_t s,
+                       const TrieDev* trie = nullptr);
 
 }  // namespace orx

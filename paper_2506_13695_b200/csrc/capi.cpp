@@ -270,6 +270,41 @@ int orx_beam_search(orx_engine* e, const orx_user_batch* batch, int32_t width, o
   });
 }
 
+int orx_engine_set_trie(orx_engine* e, const orx_trie* t) {
+  return guarded([&] {
+    need(e, "engine");
+    need(t, "trie");
+    e->e->set_trie(t->n_nodes, t->child_off, t->n_edges, t->child_code, t->child_node);
+  });
+}
+
+int orx_beam_search_constrained(orx_engine* e, const orx_user_batch* batch, int32_t width, orx_beam_out* out) {
+  return guarded([&] {
+    need(e, "engine");
+    need(batch, "batch");
+    need(out, "out");
+    need(out->codes, "out->codes");
+    need(out->log_prob, "out->log_prob");
+    e->e->stage_batch(*batch);
+    e->e->beam_search_constrained(width, out);
+  });
+}
+
+int orx_sequence_log_prob(orx_engine* e, const orx_user_batch* batch, int32_t n, const int32_t* user,
+                          const int32_t* codes, double* log_prob_out) {
+  return guarded([&] {
+    need(e, "engine");
+    need(batch, "batch");
+    if (n > 0) {
+      need(user, "user");
+      need(codes, "codes");
+      need(log_prob_out, "log_prob_out");
+    }
+    e->e->stage_batch(*batch);
+    e->e->sequence_log_prob(n, user, codes, log_prob_out);
+  });
+}
+
 int orx_engine_stage_batch(orx_engine* e, const orx_user_batch* batch) {
   return guarded([&] {
     need(e, "engine");

@@ -66,9 +66,11 @@ struct Arena {
     ptrs.push_back(p);
     return static_cast<X*>(p);
   }
-  ~Arena() {
+  void reset() {
     for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
   }
+  ~Arena() { reset(); }
 };
 
 template <class T>
@@ -430,8 +432,10 @@ class EngineT final : public Engine {
       bs_[s].lexrank = ar_.alloc<int32_t>(Rd_);
       bs_[s].lex2beam = ar_.alloc<int32_t>(Rd_);
       bs_[s].anc = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
+      node_[s] = ar_.alloc<int32_t>(Rd_);
     }
     tf_anc_ = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
+    seq_acc_ = ar_.alloc<double>(Rd_);
     tf_codes_ = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
     grp_start_ = ar_.alloc<int32_t>(Rd_ + 1);
     grp_len_ = ar_.alloc<int32_t>(Rd_ + 1);
@@ -1026,7 +1030,42 @@ class EngineT final : public Engine {
     CUDA_CHECK(cudaGetLastError());
   }
 
-  void beam_search(int width, orx_beam_out* out) override {
+  void beam_search(int width, orx_beam_out* out) override { run_beam(width, out, false); }
+  void beam_search_constrained(int width, orx_beam_out* out) override {
+    require(has_trie_, "constrained beam search over an empty trie");  // generation.cpp:44-45
+    run_beam(width, out, true);
+  }
+
+  void set_trie(int n_nodes, const int32_t* child_off, int64_t n_edges, const int32_t* child_code,
+                const int32_t* child_node) override {
+    CUDA_CHECK(cudaSetDevice(dev_));
+    require(n_nodes >= 1 && n_edges >= 0 && child_off && (n_edges == 0 || (child_code && child_node)),
+            "trie: bad CSR arrays");
+    require(child_off[0] == 0 && child_off[n_nodes] == n_edges, "trie: child offsets must span the edges");
+    for (int64_t i = 0; i < n_edges; ++i) {
+      require(child_code[i] >= 0 && child_code[i] < cfg_.codebook_size, "trie: code outside the codebook");
+      require(child_node[i] > 0 && child_node[i] < n_nodes, "trie: child node out of range");
+    }
+    for (int n = 0; n < n_nodes; ++n)
+      for (int32_t i = child_off[n] + 1; i < child_off[n + 1]; ++i)
+        require(child_code[i - 1] < child_code[i], "trie: children must have ascending, distinct codes");
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    trie_ar_.reset();
+    int32_t* off = trie_ar_.alloc<int32_t>(n_nodes + 1);
+    int32_t* code = trie_ar_.alloc<int32_t>(std::max<int64_t>(n_edges, 1));
+    int32_t* nd = trie_ar_.alloc<int32_t>(std::max<int64_t>(n_edges, 1));
+    CUDA_CHECK(cudaMemcpy(off, child_off, (n_nodes + 1) * 4, cudaMemcpyHostToDevice));
+    if (n_edges) {
+      CUDA_CHECK(cudaMemcpy(code, child_code, n_edges * 4, cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemcpy(nd, child_node, n_edges * 4, cudaMemcpyHostToDevice));
+    }
+    trie_.child_off = off;
+    trie_.child_code = code;
+    trie_.child_node = nd;
+    has_trie_ = n_edges > 0;
+  }
+
+  void run_beam(int width, orx_beam_out* out, bool constrained) {
     CUDA_CHECK(cudaSetDevice(dev_));
     const orx_config& c = cfg_;
     require(width >= 1, "generation width must be >= 1");  // validate_request, generation.cpp:35
@@ -1035,6 +1074,8 @@ class EngineT final : public Engine {
     run_encode();
     prepare_decoder(U);
     int cur = 0;
+    bs_[0].node = constrained ? node_[0] : nullptr;
+    bs_[1].node = constrained ? node_[1] : nullptr;
     launch_beam_init(U, bs_[cur], st_);
     int n_live = 1;
     for (int step = 0; step < L; ++step) {
@@ -1047,9 +1088,14 @@ class EngineT final : public Engine {
       gk.fixed_len = Tn;
       decode_step(step, rows, U, gq, gk, bs_[cur].codes, L, bs_[cur].anc, L, n_live);
       const int ksel = std::min(width, V);
-      launch_row_topk(rows, V, ksel, logits_, bs_[cur].score, bs_[cur].lexrank, lse_, cand_, topk_fail_, st_);
+      if (constrained)
+        launch_row_topk_trie(rows, V, ksel, logits_, bs_[cur].score, bs_[cur].lexrank, bs_[cur].node, trie_, lse_,
+                             cand_, st_);
+      else
+        launch_row_topk(rows, V, ksel, logits_, bs_[cur].score, bs_[cur].lexrank, lse_, cand_, topk_fail_, st_);
       const int n_new = static_cast<int>(std::min<int64_t>(width, static_cast<int64_t>(n_live) * V));
-      launch_beam_merge(U, n_live, ksel, n_new, V, L, step, cand_, logits_, lse_, bs_[cur], bs_[cur ^ 1], st_);
+      launch_beam_merge(U, n_live, ksel, n_new, V, L, step, cand_, logits_, lse_, bs_[cur], bs_[cur ^ 1], st_,
+                        constrained ? &trie_ : nullptr);
       cur ^= 1;
       n_live = n_new;
     }
@@ -1072,11 +1118,13 @@ class EngineT final : public Engine {
       const int32_t* hc = reinterpret_cast<const int32_t*>(ho);
       const double* hl = reinterpret_cast<const double*>(ho + nc * 4);
       for (int u = 0; u < U; ++u) {
-        if (out->n_items) out->n_items[u] = n_live;
+        int n_u = n_live;  // constrained search: empty slots (log-prob -inf) sort last
+        while (n_u > 0 && std::isinf(hl[(size_t)u * n_live + n_u - 1])) --n_u;
+        if (out->n_items) out->n_items[u] = n_u;
         for (int b = 0; b < width; ++b) {
           for (int j = 0; j < L; ++j)
-            out->codes[((size_t)u * width + b) * L + j] = b < n_live ? hc[((size_t)u * n_live + b) * L + j] : -1;
-          out->log_prob[(size_t)u * width + b] = b < n_live ? hl[(size_t)u * n_live + b] : 0.0;
+            out->codes[((size_t)u * width + b) * L + j] = b < n_u ? hc[((size_t)u * n_live + b) * L + j] : -1;
+          out->log_prob[(size_t)u * width + b] = b < n_u ? hl[(size_t)u * n_live + b] : 0.0;
         }
       }
     }
@@ -1154,6 +1202,66 @@ class EngineT final : public Engine {
     teacher_forced(sg_.U, n, user, prefixes, prefix_len, logits);
   }
 
+  // PolicyModel::sequence_log_prob (policy.cpp:297-310) for n queries: decode
+  // [BOS, c1 .. c_{L-1}] teacher-forced and sum log_softmax(logits_j)[c_j] (f64).
+  void sequence_log_prob(int n, const int32_t* user, const int32_t* codes, double* out) override {
+    CUDA_CHECK(cudaSetDevice(dev_));
+    const orx_config& c = cfg_;
+    const int L = c.n_code_layers, V = c.codebook_size, Tn = enc_seq_len(c);
+    require(n >= 0 && n <= Rd_, "too many sequences for the engine capacity");
+    for (int q = 0; q < n; ++q) {
+      require(user[q] >= 0 && user[q] < sg_.U, "query user index out of range");
+      for (int j = 0; j < L; ++j)
+        require(codes[(size_t)q * L + j] >= 0 && codes[(size_t)q * L + j] < V, "target must be a full semantic id");
+    }
+    run_encode();
+    prepare_decoder(sg_.U);
+    if (n == 0) return;
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return user[a] < user[b]; });
+    std::vector<int32_t> cs(static_cast<size_t>(n) * L), anc(static_cast<size_t>(n) * L), gs, gl, gk, gu;
+    int max_group = 0;
+    for (int r = 0; r < n; ++r) {
+      const int q = order[r];
+      for (int j = 0; j < L; ++j) {
+        cs[(size_t)r * L + j] = codes[(size_t)q * L + j];
+        anc[(size_t)r * L + j] = r;
+      }
+      if (r == 0 || user[order[r - 1]] != user[q]) {
+        gs.push_back(r);
+        gl.push_back(0);
+        gk.push_back(user[q] * Tn);
+        gu.push_back(user[q]);
+      }
+      ++gl.back();
+      max_group = std::max(max_group, gl.back());
+    }
+    const int G = static_cast<int>(gs.size());
+    CUDA_CHECK(cudaMemcpyAsync(tf_codes_, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(tf_anc_, anc.data(), anc.size() * 4, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(grp_start_, gs.data(), G * 4, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(grp_len_, gl.data(), G * 4, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(grp_kstart_, gk.data(), G * 4, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(grp_user_, gu.data(), G * 4, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemsetAsync(seq_acc_, 0, static_cast<size_t>(n) * 8, st_));
+    Seg gq;
+    gq.start = grp_start_;
+    gq.len = grp_len_;
+    Seg gkseg;
+    gkseg.start = grp_kstart_;
+    gkseg.fixed_len = Tn;
+    for (int step = 0; step < L; ++step) {  // position j predicts code j from [BOS, c1 .. c_j]
+      decode_step(step, n, G, gq, gkseg, tf_codes_, L, tf_anc_, L, max_group, grp_user_);
+      launch_pick_logprob(n, V, logits_, tf_codes_, L, step, seq_acc_, st_);
+    }
+    std::vector<double> host(n);
+    CUDA_CHECK(cudaMemcpyAsync(host.data(), seq_acc_, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, st_));
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    CUDA_CHECK(cudaGetLastError());
+    for (int r = 0; r < n; ++r) out[order[r]] = host[r];
+  }
+
   void next_logits(const float* z, int n_z, int n, const int32_t* z_index, const int32_t* prefixes,
                    const int32_t* prefix_len, float* logits) override {
     CUDA_CHECK(cudaSetDevice(dev_));
@@ -1197,6 +1305,12 @@ class EngineT final : public Engine {
   uint64_t* cand_ = nullptr;
   int32_t* topk_fail_ = nullptr;
   BeamState bs_[2];
+  int32_t* node_[2] = {nullptr, nullptr};
+  // device trie (constrained search)
+  Arena trie_ar_;
+  TrieDev trie_;
+  bool has_trie_ = false;
+  double* seq_acc_ = nullptr;
   int32_t *tf_anc_, *tf_codes_, *grp_start_, *grp_len_, *grp_kstart_;
   int32_t *sel_ = nullptr, *slot_ = nullptr, *counts_ = nullptr, *cursor_ = nullptr, *tile_expert_ = nullptr,
           *n_mtiles_ = nullptr;

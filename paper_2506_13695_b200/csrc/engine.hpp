@@ -24,6 +24,13 @@ class Engine {
   virtual void stage_batch(const orx_user_batch& b) = 0;
   virtual void encode(float* z_out) = 0;
   virtual void beam_search(int width, orx_beam_out* out) = 0;
+  // Trie-constrained beam search (generation.cpp:58-64; needs set_trie).
+  virtual void beam_search_constrained(int width, orx_beam_out* out) = 0;
+  // CSR trie (see TrieDev in beam.cuh), uploaded to the device.
+  virtual void set_trie(int n_nodes, const int32_t* child_off, int64_t n_edges, const int32_t* child_code,
+                        const int32_t* child_node) = 0;
+  // PolicyModel::sequence_log_prob (policy.cpp:297-310) for n (user, full code) queries.
+  virtual void sequence_log_prob(int n, const int32_t* user, const int32_t* codes, double* out) = 0;
   virtual void next_logits(const float* z, int n_z, int n, const int32_t* z_index, const int32_t* prefixes,
                            const int32_t* prefix_len, float* logits) = 0;
   virtual void score_prefixes(int n, const int32_t* user, const int32_t* prefixes, const int32_t* prefix_len,

@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(256) features8_kernel(RecordsDev r, FeatureTab
     const float sc[4] = {r.tag[row], r.ts[row], r.play[row], r.dur[row]};
     const uint32_t lab = r.labels[row];
     T* o = out + (size_t)row * ldo;
+#pragma unroll 3
     for (int c0 = lane * 8; c0 < ldo; c0 += 256) {
       float v[8];
       if (c0 < d) {

@@ -23,7 +23,7 @@ from typing import Dict, List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (PRECISION, check, lib, orx_beam_out, orx_config, orx_records, orx_user_batch)
+from ._lib import (PRECISION, check, lib, orx_beam_out, orx_config, orx_records, orx_trie, orx_user_batch)
 
 _CFG_FIELDS = [f for f, _ in orx_config._fields_]
 
@@ -171,6 +171,35 @@ class SemanticTrie:
 
     def item_count(self) -> int:
         return sum(len(v) for v in self._leaves.values())
+
+    def children_of(self, prefix: Sequence[int]) -> List[int]:  # trie.cpp:53-59
+        n = len(prefix)
+        if n >= self.depth:
+            return []
+        p = tuple(prefix)
+        return sorted({k[n] for k in self._leaves if k[:n] == p})
+
+    def to_csr(self):
+        """(child_off, child_code, child_node) int32 arrays over prefix nodes,
+        node 0 = root, children in ascending code order (std::map order)."""
+        nodes = {(): 0}
+        level = [()]
+        edges = {0: []}
+        for depth in range(self.depth):
+            nxt = sorted({k[:depth + 1] for k in self._leaves})
+            for pre in nxt:
+                nodes[pre] = len(nodes)
+                edges[nodes[pre]] = []
+                edges[nodes[pre[:-1]]].append((pre[-1], nodes[pre]))
+            level = nxt
+        off, code, node = [0], [], []
+        for n in range(len(nodes)):
+            for c, ch in sorted(edges[n]):
+                code.append(c)
+                node.append(ch)
+            off.append(len(code))
+        del level
+        return (np.asarray(off, dtype=np.int32), np.asarray(code, dtype=np.int32), np.asarray(node, dtype=np.int32))
 
 
 # ---- user batches ------------------------------------------------------------------
@@ -407,8 +436,32 @@ class PolicyModel:
         return out[:n]
 
     # -- generation ----------------------------------------------------------------------
-    def beam_search_arrays(self, users, width: int):
-        """Batched beam search: (codes [U, W, L] int32, log_prob [U, W] f64, n_items [U])."""
+    def set_trie(self, trie: "SemanticTrie") -> None:
+        """Upload the semantic-ID trie for constrained beam search."""
+        off, code, node = trie.to_csr()
+        self._trie_keep = (off, code, node)
+        I32 = C.POINTER(C.c_int32)
+        t = orx_trie(len(off) - 1, off.ctypes.data_as(I32), len(code), code.ctypes.data_as(I32), node.ctypes.data_as(I32))
+        check(lib().orx_engine_set_trie(self._e, C.byref(t)))
+        self._trie = trie
+
+    def sequence_log_prob_batch(self, users, user_index: Sequence[int], codes: Sequence[Sequence[int]]) -> np.ndarray:
+        """PolicyModel::sequence_log_prob (policy.cpp:297-310) for (user, full code) queries, f64."""
+        b = _as_batch(users, self.cfg.n_code_layers)
+        L = self.cfg.n_code_layers
+        cs = np.ascontiguousarray(np.asarray(codes, dtype=np.int32).reshape(-1, L))
+        ui = np.ascontiguousarray(np.asarray(user_index, dtype=np.int32).reshape(-1))
+        if cs.shape[0] != ui.shape[0]:
+            raise ValueError("one user index per sequence")
+        out = np.empty(max(len(ui), 1), dtype=np.float64)
+        I32 = C.POINTER(C.c_int32)
+        check(lib().orx_sequence_log_prob(self._e, C.byref(b.c), len(ui), ui.ctypes.data_as(I32),
+                                          cs.ctypes.data_as(I32), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out[:len(ui)]
+
+    def beam_search_arrays(self, users, width: int, constrained: bool = False):
+        """Batched beam search: (codes [U, W, L] int32, log_prob [U, W] f64, n_items [U]).
+        constrained=True expands only children of the trie set by set_trie."""
         b = _as_batch(users, self.cfg.n_code_layers)
         L = self.cfg.n_code_layers
         codes = np.empty((b.n_users, width, L), dtype=np.int32)
@@ -416,7 +469,8 @@ class PolicyModel:
         n_items = np.empty(b.n_users, dtype=np.int32)
         out = orx_beam_out(codes.ctypes.data_as(C.POINTER(C.c_int32)), logp.ctypes.data_as(C.POINTER(C.c_double)),
                            n_items.ctypes.data_as(C.POINTER(C.c_int32)))
-        check(lib().orx_beam_search(self._e, C.byref(b.c), width, C.byref(out)))
+        fn = lib().orx_beam_search_constrained if constrained else lib().orx_beam_search
+        check(fn(self._e, C.byref(b.c), width, C.byref(out)))
         return codes, logp, n_items
 
     def generate_batch(self, users, req: GenerationRequest,
@@ -425,8 +479,11 @@ class PolicyModel:
         if req.strategy != "beam":
             raise NotImplementedError("top-k/top-p sampling is outside the B200 hot path (SURVEY.md §8f)")
         if req.constrain_to_trie:
-            raise NotImplementedError("trie-constrained beam search is a §8f 'next' row")
-        codes, logp, n_items = self.beam_search_arrays(users, req.width)
+            if trie is None or trie.item_count() == 0:
+                raise ValueError("constrained beam search over an empty trie")  # generation.cpp:44-45
+            if getattr(self, "_trie", None) is not trie:
+                self.set_trie(trie)
+        codes, logp, n_items = self.beam_search_arrays(users, req.width, constrained=req.constrain_to_trie)
         out = []
         for u in range(codes.shape[0]):
             items = []

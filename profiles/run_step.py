@@ -24,3 +24,4 @@ check(lib().orx_engine_stage_batch(m._e, C.byref(b.c)))
 for _ in range(a.warmup + a.steps):
     check(lib().orx_beam_search_staged(m._e, a.width, None))
 print("launches", m.stats()["launches"])
+print("topk fallback rows", lib().orx_debug_topk_fallback_rows())

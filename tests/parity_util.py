@@ -17,7 +17,8 @@ REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
 
 
 def ref_dump(preset: str, n_users: int, width: int, lens=None, user_seed: int = 1, user_begin: int = 0,
-             n_prefix: int = 4, beam: bool = True, sets=(), out_dir=None, timeout=3600):
+             n_prefix: int = 4, beam: bool = True, sets=(), out_dir=None, timeout=3600, trie_items: int = 0,
+             trie_fanout: int = 0, trie_seed: int = 77):
     """Run the reference on synthetic users; returns (dir, per-user dict)."""
     if not os.path.exists(REF_DRIVER):
         raise FileNotFoundError(f"{REF_DRIVER} missing: run `make -C oracle`")
@@ -31,6 +32,10 @@ def ref_dump(preset: str, n_users: int, width: int, lens=None, user_seed: int = 
         cmd += ["--lens", ",".join(str(x) for x in lens)]
     if not beam:
         cmd += ["--no-beam"]
+    if trie_items:
+        cmd += ["--trie-items", str(trie_items), "--trie-seed", str(trie_seed)]
+        if trie_fanout:
+            cmd += ["--trie-fanout", str(trie_fanout)]
     subprocess.run(cmd, check=True, timeout=timeout, capture_output=True)
     users = []
     for u in range(user_begin, user_begin + n_users):
@@ -38,6 +43,9 @@ def ref_dump(preset: str, n_users: int, width: int, lens=None, user_seed: int = 
         if beam:
             d["beam_codes"] = np.load(os.path.join(out_dir, f"beam_codes_u{u}.npy"))
             d["beam_logp"] = np.load(os.path.join(out_dir, f"beam_logp_u{u}.npy"))
+            d["seq_logp"] = np.load(os.path.join(out_dir, f"seq_logp_u{u}.npy"))
+        if trie_items:
+            d["trie_codes"] = np.load(os.path.join(out_dir, "trie_codes.npy"))
         users.append(d)
     return out_dir, users
 

@@ -177,3 +177,31 @@ def test_cpp_dropin_shim_builds_and_fails_loudly_without_gpu():
         pass
     r = subprocess.run([demo], capture_output=True, text=True, timeout=120)
     assert r.returncode == 2 and "no CPU fallback" in r.stdout
+
+
+def test_trie_csr_matches_children_of():
+    """SemanticTrie.to_csr (the device trie layout) walks to the same children
+    as children_of (trie.cpp:53-59), codes ascending, every leaf reachable."""
+    import numpy as np
+
+    import paper_2506_13695_b200 as P
+    rng = np.random.default_rng(5)
+    t = P.SemanticTrie(3)
+    leaves = {tuple(int(x) for x in rng.integers(0, 6, 3)) for _ in range(60)}
+    for i, c in enumerate(sorted(leaves)):
+        t.insert(list(c), i)
+    off, code, node = t.to_csr()
+    assert off[0] == 0 and off[-1] == len(code) == len(node)
+
+    def walk(prefix):
+        n = 0
+        for c in prefix:
+            kids = code[off[n]:off[n + 1]]
+            assert list(kids) == sorted(kids)
+            n = int(node[off[n] + list(kids).index(c)])
+        return n
+
+    for leaf in leaves:
+        for depth in range(3):
+            n = walk(leaf[:depth])
+            assert list(code[off[n]:off[n + 1]]) == t.children_of(list(leaf[:depth]))

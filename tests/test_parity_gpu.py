@@ -180,3 +180,57 @@ def test_bf16_tcgen05_attention_dh128(moe):
               f"logits {el:.3e} (mma.sync {el_mma:.3e}) overlap {overlap}/32")
         assert el < 5e-2 and overlap >= 16
         assert el < 2 * el_mma + 1e-2  # no worse than the mma.sync attention path
+
+
+def _trie_from(P, codes, depth):
+    t = P.SemanticTrie(depth)
+    for i, c in enumerate(codes):
+        t.insert([int(x) for x in c], i)
+    return t
+
+
+@pytest.mark.parametrize("preset,width,items,fanout", [("tiny", 16, 40, 4), ("tiny", 16, 9, 4), ("0.015B", 32, 3000, 0),
+                                                       ("0.015B", 64, 400, 12)])
+def test_constrained_beam_fp32(preset, width, items, fanout):
+    """Trie-constrained beam search (GenerationRequest::constrain_to_trie,
+    generation.cpp:58-64): only trie children are expanded, fewer than W items
+    when the trie is small; parity with the reference on the same seeded trie."""
+    lens = (4, 4, 8) if preset == "tiny" else (20, 64, 300)
+    P, model = _model(preset, "fp32", max_users=2, max_width=max(width, 16))
+    _, refs = ref_dump(preset, 2, width, lens=lens, trie_items=items, trie_fanout=fanout)
+    trie = _trie_from(P, refs[0]["trie_codes"], model.cfg.n_code_layers)
+    batch = P.SynthBatch(1, 0, 2, *lens)
+    req = P.GenerationRequest(width=width, constrain_to_trie=True)
+    out = model.generate_batch(batch, req, trie)
+    for u, ref in enumerate(refs):
+        W = len(ref["beam_codes"])
+        got = out[u]
+        assert len(got) == W, (len(got), W)
+        assert all(it.legal for it in got)  # every constrained output is a trie leaf
+        codes = np.array([it.codes for it in got], dtype=np.int32).reshape(W, -1)
+        logp = np.array([it.log_prob for it in got])
+        ok, exact, msg = beams_match(codes, logp, ref["beam_codes"], ref["beam_logp"])
+        print(f"{preset} trie({items}) W={width} user {u}: {W} items, exact-rank {exact}/{W}")
+        assert ok, msg
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_sequence_log_prob(precision):
+    """PolicyModel::sequence_log_prob (policy.cpp:297-310) on the reference's
+    beam items: teacher-forced decode of [BOS, c1, c2], summed picked log-softmax."""
+    P, model = _model("0.015B", precision, max_users=2, max_width=32)
+    lens = (20, 64, 300)
+    _, refs = ref_dump("0.015B", 2, 16, lens=lens)
+    batch = P.SynthBatch(1, 0, 2, *lens)
+    users, codes, want = [], [], []
+    for u, ref in enumerate(refs):
+        for c, lp in zip(ref["beam_codes"], ref["seq_logp"]):
+            users.append(u)
+            codes.append(c)
+            want.append(lp)
+    got = model.sequence_log_prob_batch(batch, users, codes)
+    want = np.array(want)
+    err = np.abs(got - want).max() / np.abs(want).max()
+    print(f"sequence_log_prob {precision}: max rel err {err:.3e}")
+    assert err < (1e-4 if precision == "fp32" else 3e-2)
+    np.testing.assert_allclose(want, np.concatenate([r["beam_logp"] for r in refs]), rtol=1e-9)

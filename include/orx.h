@@ -183,6 +183,13 @@ int orx_beam_search_constrained(orx_engine* e, const orx_user_batch* batch, int3
 int orx_sequence_log_prob(orx_engine* e, const orx_user_batch* batch, int32_t n, const int32_t* user,
                           const int32_t* codes, double* log_prob_out);
 
+/* sample_topk_topp (generation.cpp:90-148): `width` independent samples per
+ * user (tempered by temperature, cut to top_k (0 = all) and top_p), user u
+ * drawing uniforms from Rng(seed).split(user_stream[u]) (NULL: u) exactly as
+ * the reference's Rng; log_prob is the untempered model log-prob (f64). */
+int orx_sample(orx_engine* e, const orx_user_batch* batch, int32_t width, double temperature, int32_t top_k,
+               double top_p, uint64_t seed, const uint64_t* user_stream, orx_beam_out* out);
+
 /* Same as orx_beam_search, but inputs are already resident on the device
  * (uploaded by orx_engine_stage_batch); results stay on the device unless
  * out is non-NULL. Used to time the kernel path without host copies. */

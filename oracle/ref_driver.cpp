@@ -130,6 +130,10 @@ struct Args {
   int trie_items = 0;      // > 0: constrained beam search over a seeded random trie
   uint64_t trie_seed = 77;
   int trie_fanout = 0;     // > 0: codes drawn from [0, fanout) per level (a dense trie)
+  bool sample = false;     // also dump sample_topk_topp with Rng(sample_seed).split(user)
+  uint64_t sample_seed = 5;
+  double temperature = 1.0, top_p = 1.0;
+  int top_k = 0;
 };
 
 Args parse(int argc, char** argv) {
@@ -163,6 +167,11 @@ Args parse(int argc, char** argv) {
     else if (k == "--trie-items") a.trie_items = std::stoi(next());
     else if (k == "--trie-seed") a.trie_seed = std::stoull(next());
     else if (k == "--trie-fanout") a.trie_fanout = std::stoi(next());
+    else if (k == "--sample") a.sample = true;
+    else if (k == "--sample-seed") a.sample_seed = std::stoull(next());
+    else if (k == "--temperature") a.temperature = std::stod(next());
+    else if (k == "--top-k") a.top_k = std::stoi(next());
+    else if (k == "--top-p") a.top_p = std::stod(next());
     else throw std::invalid_argument("unknown option " + k);
   }
   if (!a.lens_set) {
@@ -254,6 +263,24 @@ int cmd_dump(const Args& a) {
       write_npy(upath(a, "beam_codes", u), "<i4", {items.size(), size_t(L)}, codes.data(), codes.size() * 4);
       write_npy(upath(a, "beam_logp", u), "<f8", {items.size()}, lp.data(), lp.size() * 8);
       write_npy(upath(a, "seq_logp", u), "<f8", {seq.size()}, seq.data(), seq.size() * 8);
+      if (a.sample) {
+        GenerationRequest sreq;
+        sreq.strategy = SearchStrategy::topk_topp;
+        sreq.width = a.width;
+        sreq.temperature = a.temperature;
+        sreq.top_k = a.top_k;
+        sreq.top_p = a.top_p;
+        Rng srng = Rng(a.sample_seed).split(static_cast<uint64_t>(u));
+        auto smp = generate(sreq, policy_scorer(model, z), L, V, trie, srng);
+        std::vector<int32_t> sc;
+        std::vector<double> sl;
+        for (auto& it : smp) {
+          for (int c : it.codes.codes) sc.push_back(c);
+          sl.push_back(it.log_prob);
+        }
+        write_npy(upath(a, "sample_codes", u), "<i4", {smp.size(), size_t(L)}, sc.data(), sc.size() * 4);
+        write_npy(upath(a, "sample_logp", u), "<f8", {smp.size()}, sl.data(), sl.size() * 8);
+      }
       std::set<std::vector<int>> seen;
       for (int len = 1; len < L; ++len)
         for (int j = 0; j < static_cast<int>(items.size()) && j < a.n_prefix; ++j) {

@@ -113,6 +113,8 @@ SIGNATURES = [
     ("orx_beam_search_constrained", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, C.POINTER(orx_beam_out)]),
     ("orx_sequence_log_prob", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, _I32P, _I32P,
                                         C.POINTER(C.c_double)]),
+    ("orx_sample", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, C.c_double, C.c_int32, C.c_double,
+                             C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(orx_beam_out)]),
     ("orx_engine_stage_batch", C.c_int, [_P, C.POINTER(orx_user_batch)]),
     ("orx_beam_search_staged", C.c_int, [_P, C.c_int32, C.POINTER(orx_beam_out)]),
     ("orx_engine_stats", C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -1,5 +1,6 @@
 #include <algorithm>
 #include <cfloat>
+#include <climits>
 #include <stdexcept>
 
 #include "beam.cuh"
@@ -540,6 +541,125 @@ __global__ void pick_logprob_kernel(int rows, int V, const float* __restrict__ l
   }
 }
 
+// Top-k / top-p sampling step (sample_topk_topp, generation.cpp:90-148), one
+// block per sample row: tempered probabilities sorted by (p desc, index asc)
+// (bitonic, stable like std::stable_sort), cut to top_k, then to the smallest
+// prefix reaching top_p of the kept mass, then the first sorted entry whose
+// running sum reaches u * total; log_prob accumulates the untempered
+// log-softmax of the pick (f64).
+constexpr int kSampleThreads = 512;
+__global__ void __launch_bounds__(kSampleThreads) sample_kernel(int V, int vpad, int L, int step, float inv_temp,
+                                                                int top_k, double top_p,
+                                                                const float* __restrict__ logits,
+                                                                const double* __restrict__ uniforms,
+                                                                int32_t* __restrict__ codes,
+                                                                double* __restrict__ logp) {
+  extern __shared__ uint64_t skeys[];  // [vpad]
+  __shared__ double dscan[kSampleThreads];
+  __shared__ float red[kSampleThreads / 32];
+  __shared__ int sidx[2];
+  __shared__ double stotal;
+  const int row = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* lg = logits + (size_t)row * V;
+  auto bmax = [&](float v) {
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float t = -FLT_MAX;
+    for (int w = 0; w < kSampleThreads / 32; ++w) t = fmaxf(t, red[w]);
+    return t;
+  };
+  auto bsum = [&](float v) {
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float t = 0.f;
+    for (int w = 0; w < kSampleThreads / 32; ++w) t += red[w];
+    return t;
+  };
+  float mx = -FLT_MAX;
+  for (int i = tid; i < V; i += kSampleThreads) mx = fmaxf(mx, lg[i]);
+  mx = bmax(mx);
+  float se = 0.f, st = 0.f;
+  for (int i = tid; i < V; i += kSampleThreads) se += __expf(lg[i] - mx);
+  se = bsum(se);
+  const float lse = mx + logf(se);  // model log-softmax (untempered)
+  for (int i = tid; i < V; i += kSampleThreads) st += __expf((lg[i] - mx) * inv_temp);
+  st = bsum(st);
+  const float lse_t = mx * inv_temp + logf(st);
+  for (int i = tid; i < vpad; i += kSampleThreads) {
+    const float pr = i < V ? __expf(lg[i] * inv_temp - lse_t) : 0.f;
+    skeys[i] = i < V ? (static_cast<uint64_t>(ord_f32(pr)) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(i)) : 0;
+  }
+  __syncthreads();
+  for (int size = 2; size <= vpad; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < vpad / 2; i += kSampleThreads) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool desc = (lo & size) == 0;
+        const uint64_t x = skeys[lo], y = skeys[hi];
+        if ((x < y) == desc) skeys[lo] = y, skeys[hi] = x;
+      }
+      __syncthreads();
+    }
+  const int keep = top_k > 0 ? min(top_k, V) : V;
+  // inclusive prefix sums (f64) of the sorted probabilities, thread-contiguous segments
+  const int per = (keep + kSampleThreads - 1) / kSampleThreads;
+  const int b0 = tid * per, b1 = min(keep, b0 + per);
+  double loc = 0.0;
+  for (int i = b0; i < b1; ++i) loc += static_cast<double>(unord_f32(static_cast<uint32_t>(skeys[i] >> 32)));
+  dscan[tid] = loc;
+  __syncthreads();
+  if (tid == 0) {  // exclusive scan of 512 partials (tiny)
+    double run = 0.0;
+    for (int t = 0; t < kSampleThreads; ++t) {
+      const double v = dscan[t];
+      dscan[t] = run;
+      run += v;
+    }
+    stotal = run;  // mass of the kept set
+    sidx[0] = keep;
+    sidx[1] = INT_MAX;
+  }
+  __syncthreads();
+  const double target = top_p * stotal;
+  double acc = dscan[tid];
+  for (int i = b0; i < b1; ++i) {
+    acc += static_cast<double>(unord_f32(static_cast<uint32_t>(skeys[i] >> 32)));
+    if (acc >= target - 1e-15) {
+      atomicMin(&sidx[0], i + 1);
+      break;
+    }
+  }
+  __syncthreads();
+  const int cut = sidx[0];
+  // total = prefix(cut - 1)
+  if (cut - 1 >= b0 && cut - 1 < b1) {
+    double a2 = dscan[tid];
+    for (int i = b0; i < cut; ++i) a2 += static_cast<double>(unord_f32(static_cast<uint32_t>(skeys[i] >> 32)));
+    stotal = a2;
+  }
+  __syncthreads();
+  const double u = uniforms[(size_t)row * L + step] * stotal;
+  acc = dscan[tid];
+  for (int i = b0; i < min(b1, cut); ++i) {
+    acc += static_cast<double>(unord_f32(static_cast<uint32_t>(skeys[i] >> 32)));
+    if (acc >= u) {
+      atomicMin(&sidx[1], i);
+      break;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int pos = sidx[1] == INT_MAX ? cut - 1 : sidx[1];
+    const int code = static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(skeys[pos] & 0xFFFFFFFFu));
+    codes[(size_t)row * L + step] = code;
+    logp[row] += static_cast<double>(lg[code]) - static_cast<double>(lse);
+  }
+}
+
 }  // namespace
 
 void launch_row_topk(int rows, int V, int k_sel, const float* logits, const float* parent_score,
@@ -585,6 +705,24 @@ void launch_pick_logprob(int rows, int V, const float* logits, const int32_t* co
   if (rows <= 0) return;
   ProfScope ps(PROF_BEAM, s, 0.0, double(rows) * V * 4);
   pick_logprob_kernel<<<(rows + 7) / 8, 256, 0, s>>>(rows, V, logits, codes, code_stride, step, acc);
+  ++launch_counter();
+}
+
+void launch_sample(int rows, int V, int L, int step, float temperature, int top_k, double top_p, const float* logits,
+                   const double* uniforms, int32_t* codes, double* logp, cudaStream_t s) {
+  if (rows <= 0) return;
+  int vpad = 1;
+  while (vpad < V) vpad <<= 1;
+  const size_t smem = static_cast<size_t>(vpad) * 8;
+  if (smem > 200 * 1024) throw std::invalid_argument("sampling supports codebooks up to 25600 codes");
+  static size_t set = 0;
+  if (smem > 48 * 1024 && smem > set) {
+    cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    set = smem;
+  }
+  ProfScope ps(PROF_BEAM, s, 0.0, double(rows) * V * 4);
+  sample_kernel<<<rows, kSampleThreads, smem, s>>>(V, vpad, L, step, 1.f / temperature, top_k, top_p, logits,
+                                                   uniforms, codes, logp);
   ++launch_counter();
 }
 

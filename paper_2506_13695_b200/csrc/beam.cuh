@@ -40,6 +40,12 @@ void launch_row_topk_trie(int rows, int V, int k_sel, const float* logits, const
                           const int32_t* parent_lexrank, const int32_t* node, TrieDev trie, float* lse,
                           uint64_t* cand, cudaStream_t s);
 
+// One step of top-k / top-p sampling for `rows` sample rows: writes
+// codes[r * L + step] and adds the pick's model log-softmax to logp[r] (f64);
+// uniforms[r * L + step] are the reference Rng's draws for that row / step.
+void launch_sample(int rows, int V, int L, int step, float temperature, int top_k, double top_p, const float* logits,
+                   const double* uniforms, int32_t* codes, double* logp, cudaStream_t s);
+
 // acc[r] += logits[r][code[r * code_stride + step]] - logsumexp(logits[r]) (f64):
 // one position of PolicyModel::sequence_log_prob (policy.cpp:297-310).
 void launch_pick_logprob(int rows, int V, const float* logits, const int32_t* codes, int code_stride, int step,

@@ -305,6 +305,19 @@ int orx_sequence_log_prob(orx_engine* e, const orx_user_batch* batch, int32_t n,
   });
 }
 
+int orx_sample(orx_engine* e, const orx_user_batch* batch, int32_t width, double temperature, int32_t top_k,
+               double top_p, uint64_t seed, const uint64_t* user_stream, orx_beam_out* out) {
+  return guarded([&] {
+    need(e, "engine");
+    need(batch, "batch");
+    need(out, "out");
+    need(out->codes, "out->codes");
+    need(out->log_prob, "out->log_prob");
+    e->e->stage_batch(*batch);
+    e->e->sample(width, temperature, top_k, top_p, seed, user_stream, out);
+  });
+}
+
 int orx_engine_stage_batch(orx_engine* e, const orx_user_batch* batch) {
   return guarded([&] {
     need(e, "engine");

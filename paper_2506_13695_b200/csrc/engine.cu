@@ -1202,6 +1202,63 @@ class EngineT final : public Engine {
     teacher_forced(sg_.U, n, user, prefixes, prefix_len, logits);
   }
 
+  void sample(int width, double temperature, int top_k, double top_p, uint64_t seed, const uint64_t* streams,
+              orx_beam_out* out) override {
+    CUDA_CHECK(cudaSetDevice(dev_));
+    const orx_config& c = cfg_;
+    // validate_request, generation.cpp:34-39
+    require(width >= 1, "generation width must be >= 1");
+    require(top_p > 0 && top_p <= 1.0, "top_p must lie in (0,1]");
+    require(top_k >= 0, "top_k must be >= 1 (or 0 for the full vocabulary)");
+    require(temperature > 0, "temperature must be positive");
+    require(width <= maxW_, "sample count above the engine capacity");
+    const int U = sg_.U, V = c.codebook_size, L = c.n_code_layers, Tn = enc_seq_len(c);
+    const int rows = U * width;
+    run_encode();
+    prepare_decoder(U);
+    // the reference draws one uniform per (sample, step), sample-major, from the user's Rng
+    std::vector<double> uni(static_cast<size_t>(rows) * L);
+    for (int u = 0; u < U; ++u) {
+      Rng r = Rng(seed).split(streams ? streams[u] : static_cast<uint64_t>(u));
+      for (int s = 0; s < width; ++s)
+        for (int j = 0; j < L; ++j) uni[((size_t)u * width + s) * L + j] = r.uniform();
+    }
+    if (!uni_) uni_ = ar_.alloc<double>(static_cast<size_t>(Rd_) * L);
+    std::vector<int32_t> anc(static_cast<size_t>(rows) * L);
+    for (int r = 0; r < rows; ++r)
+      for (int j = 0; j < L; ++j) anc[(size_t)r * L + j] = r;
+    CUDA_CHECK(cudaMemcpyAsync(uni_, uni.data(), uni.size() * 8, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemcpyAsync(tf_anc_, anc.data(), anc.size() * 4, cudaMemcpyHostToDevice, st_));
+    CUDA_CHECK(cudaMemsetAsync(tf_codes_, 0, static_cast<size_t>(rows) * L * 4, st_));
+    CUDA_CHECK(cudaMemsetAsync(seq_acc_, 0, static_cast<size_t>(rows) * 8, st_));
+    Seg gq;
+    gq.stride = width;
+    gq.fixed_len = width;
+    Seg gk;
+    gk.stride = Tn;
+    gk.fixed_len = Tn;
+    for (int step = 0; step < L; ++step) {
+      decode_step(step, rows, U, gq, gk, tf_codes_, L, tf_anc_, L, width);
+      launch_sample(rows, V, L, step, static_cast<float>(temperature), top_k, top_p, logits_, uni_, tf_codes_,
+                    seq_acc_, st_);
+    }
+    std::vector<int32_t> hc(static_cast<size_t>(rows) * L);
+    std::vector<double> hl(rows);
+    CUDA_CHECK(cudaMemcpyAsync(hc.data(), tf_codes_, hc.size() * 4, cudaMemcpyDeviceToHost, st_));
+    CUDA_CHECK(cudaMemcpyAsync(hl.data(), seq_acc_, hl.size() * 8, cudaMemcpyDeviceToHost, st_));
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    CUDA_CHECK(cudaGetLastError());
+    d2h_bytes += static_cast<int64_t>(hc.size() * 4 + hl.size() * 8);
+    for (int u = 0; u < U; ++u) {
+      if (out->n_items) out->n_items[u] = width;
+      for (int s = 0; s < width; ++s) {
+        for (int j = 0; j < L; ++j)
+          out->codes[((size_t)u * width + s) * L + j] = hc[((size_t)u * width + s) * L + j];
+        out->log_prob[(size_t)u * width + s] = hl[(size_t)u * width + s];
+      }
+    }
+  }
+
   // PolicyModel::sequence_log_prob (policy.cpp:297-310) for n queries: decode
   // [BOS, c1 .. c_{L-1}] teacher-forced and sum log_softmax(logits_j)[c_j] (f64).
   void sequence_log_prob(int n, const int32_t* user, const int32_t* codes, double* out) override {
@@ -1311,6 +1368,7 @@ class EngineT final : public Engine {
   TrieDev trie_;
   bool has_trie_ = false;
   double* seq_acc_ = nullptr;
+  double* uni_ = nullptr;
   int32_t *tf_anc_, *tf_codes_, *grp_start_, *grp_len_, *grp_kstart_;
   int32_t *sel_ = nullptr, *slot_ = nullptr, *counts_ = nullptr, *cursor_ = nullptr, *tile_expert_ = nullptr,
           *n_mtiles_ = nullptr;

@@ -31,6 +31,10 @@ class Engine {
                         const int32_t* child_node) = 0;
   // PolicyModel::sequence_log_prob (policy.cpp:297-310) for n (user, full code) queries.
   virtual void sequence_log_prob(int n, const int32_t* user, const int32_t* codes, double* out) = 0;
+  // sample_topk_topp (generation.cpp:90-148): width samples per user, user u
+  // drawing from Rng(seed).split(streams[u]) (streams NULL: u).
+  virtual void sample(int width, double temperature, int top_k, double top_p, uint64_t seed, const uint64_t* streams,
+                      orx_beam_out* out) = 0;
   virtual void next_logits(const float* z, int n_z, int n, const int32_t* z_index, const int32_t* prefixes,
                            const int32_t* prefix_len, float* logits) = 0;
   virtual void score_prefixes(int n, const int32_t* user, const int32_t* prefixes, const int32_t* prefix_len,

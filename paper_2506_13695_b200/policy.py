@@ -459,6 +459,27 @@ class PolicyModel:
                                           cs.ctypes.data_as(I32), out.ctypes.data_as(C.POINTER(C.c_double))))
         return out[:len(ui)]
 
+    def sample_arrays(self, users, width: int, temperature: float = 1.0, top_k: int = 0, top_p: float = 1.0,
+                      seed: int = 0, streams: Optional[Sequence[int]] = None):
+        """sample_topk_topp (generation.cpp:90-148) for every user: (codes [U, W, L], log_prob [U, W]);
+        user u draws from Rng(seed).split(streams[u]) (default: u)."""
+        b = _as_batch(users, self.cfg.n_code_layers)
+        L = self.cfg.n_code_layers
+        codes = np.empty((b.n_users, width, L), dtype=np.int32)
+        logp = np.empty((b.n_users, width), dtype=np.float64)
+        n_items = np.empty(b.n_users, dtype=np.int32)
+        out = orx_beam_out(codes.ctypes.data_as(C.POINTER(C.c_int32)), logp.ctypes.data_as(C.POINTER(C.c_double)),
+                           n_items.ctypes.data_as(C.POINTER(C.c_int32)))
+        st = None
+        if streams is not None:
+            st_arr = np.ascontiguousarray(np.asarray(streams, dtype=np.uint64))
+            if st_arr.shape[0] != b.n_users:
+                raise ValueError("one stream id per user")
+            st = st_arr.ctypes.data_as(C.POINTER(C.c_uint64))
+        check(lib().orx_sample(self._e, C.byref(b.c), width, float(temperature), int(top_k), float(top_p),
+                               C.c_uint64(seed), st, C.byref(out)))
+        return codes, logp
+
     def beam_search_arrays(self, users, width: int, constrained: bool = False):
         """Batched beam search: (codes [U, W, L] int32, log_prob [U, W] f64, n_items [U]).
         constrained=True expands only children of the trie set by set_trie."""
@@ -473,11 +494,21 @@ class PolicyModel:
         check(fn(self._e, C.byref(b.c), width, C.byref(out)))
         return codes, logp, n_items
 
-    def generate_batch(self, users, req: GenerationRequest,
-                       trie: Optional[SemanticTrie] = None) -> List[List[GeneratedItem]]:
+    def generate_batch(self, users, req: GenerationRequest, trie: Optional[SemanticTrie] = None, seed: int = 0,
+                       streams: Optional[Sequence[int]] = None) -> List[List[GeneratedItem]]:
         validate_request(req)
-        if req.strategy != "beam":
-            raise NotImplementedError("top-k/top-p sampling is outside the B200 hot path (SURVEY.md §8f)")
+        if req.strategy != "beam":  # sample_topk_topp (generation.cpp:90-148)
+            codes, logp = self.sample_arrays(users, req.width, req.temperature, req.top_k, req.top_p, seed, streams)
+            out = []
+            for u in range(codes.shape[0]):
+                items = []
+                for s_ in range(req.width):
+                    c = [int(x) for x in codes[u, s_]]
+                    ids = trie.lookup(c) if trie is not None else None
+                    items.append(GeneratedItem(codes=c, log_prob=float(logp[u, s_]), legal=ids is not None,
+                                               item_ids=list(ids or [])))
+                out.append(items)
+            return out
         if req.constrain_to_trie:
             if trie is None or trie.item_count() == 0:
                 raise ValueError("constrained beam search over an empty trie")  # generation.cpp:44-45
@@ -495,9 +526,9 @@ class PolicyModel:
             out.append(items)
         return out
 
-    def generate(self, ctx: UserContext, req: GenerationRequest,
-                 trie: Optional[SemanticTrie] = None) -> List[GeneratedItem]:
-        return self.generate_batch([ctx], req, trie)[0]
+    def generate(self, ctx: UserContext, req: GenerationRequest, trie: Optional[SemanticTrie] = None,
+                 seed: int = 0, stream: int = 0) -> List[GeneratedItem]:
+        return self.generate_batch([ctx], req, trie, seed, [stream])[0]
 
     def stats(self):
         a, b, c = C.c_int64(), C.c_int64(), C.c_int64()

@@ -18,7 +18,7 @@ REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
 
 def ref_dump(preset: str, n_users: int, width: int, lens=None, user_seed: int = 1, user_begin: int = 0,
              n_prefix: int = 4, beam: bool = True, sets=(), out_dir=None, timeout=3600, trie_items: int = 0,
-             trie_fanout: int = 0, trie_seed: int = 77):
+             trie_fanout: int = 0, trie_seed: int = 77, sample=None):
     """Run the reference on synthetic users; returns (dir, per-user dict)."""
     if not os.path.exists(REF_DRIVER):
         raise FileNotFoundError(f"{REF_DRIVER} missing: run `make -C oracle`")
@@ -36,6 +36,10 @@ def ref_dump(preset: str, n_users: int, width: int, lens=None, user_seed: int = 
         cmd += ["--trie-items", str(trie_items), "--trie-seed", str(trie_seed)]
         if trie_fanout:
             cmd += ["--trie-fanout", str(trie_fanout)]
+    if sample is not None:  # dict(temperature, top_k, top_p, seed)
+        cmd += ["--sample", "--temperature", str(sample.get("temperature", 1.0)), "--top-k",
+                str(sample.get("top_k", 0)), "--top-p", str(sample.get("top_p", 1.0)), "--sample-seed",
+                str(sample.get("seed", 5))]
     subprocess.run(cmd, check=True, timeout=timeout, capture_output=True)
     users = []
     for u in range(user_begin, user_begin + n_users):
@@ -46,6 +50,9 @@ def ref_dump(preset: str, n_users: int, width: int, lens=None, user_seed: int = 
             d["seq_logp"] = np.load(os.path.join(out_dir, f"seq_logp_u{u}.npy"))
         if trie_items:
             d["trie_codes"] = np.load(os.path.join(out_dir, "trie_codes.npy"))
+        if sample is not None:
+            d["sample_codes"] = np.load(os.path.join(out_dir, f"sample_codes_u{u}.npy"))
+            d["sample_logp"] = np.load(os.path.join(out_dir, f"sample_logp_u{u}.npy"))
         users.append(d)
     return out_dir, users
 

@@ -234,3 +234,34 @@ def test_sequence_log_prob(precision):
     print(f"sequence_log_prob {precision}: max rel err {err:.3e}")
     assert err < (1e-4 if precision == "fp32" else 3e-2)
     np.testing.assert_allclose(want, np.concatenate([r["beam_logp"] for r in refs]), rtol=1e-9)
+
+
+SAMPLE_CASES = [("tiny", dict(temperature=1.0, top_k=0, top_p=1.0, seed=5)),
+                ("tiny", dict(temperature=0.7, top_k=3, top_p=0.9, seed=9)),
+                ("0.015B", dict(temperature=1.3, top_k=50, top_p=0.95, seed=11)),
+                ("0.015B", dict(temperature=1.0, top_k=0, top_p=0.8, seed=3))]
+
+
+@pytest.mark.parametrize("preset,sample", SAMPLE_CASES)
+def test_topk_topp_sampling_fp32(preset, sample):
+    """sample_topk_topp (generation.cpp:90-148): tempered, top-k / top-p cut,
+    stable ordering, the reference Rng's uniforms per (sample, step). fp32
+    logits can flip a pick only when a uniform lands within ~1e-6 of a bucket
+    edge, so nearly every sampled sequence must match the reference exactly."""
+    lens = (4, 4, 8) if preset == "tiny" else (20, 64, 300)
+    W = 24
+    P, model = _model(preset, "fp32", max_users=2, max_width=W)
+    _, refs = ref_dump(preset, 2, W, lens=lens, sample=sample)
+    batch = P.SynthBatch(1, 0, 2, *lens)
+    req = P.GenerationRequest(strategy="topk_topp", width=W, temperature=sample["temperature"],
+                              top_k=sample["top_k"], top_p=sample["top_p"])
+    out = model.generate_batch(batch, req, seed=sample["seed"], streams=[0, 1])
+    same = total = 0
+    for u, ref in enumerate(refs):
+        for s, it in enumerate(out[u]):
+            total += 1
+            if list(it.codes) == [int(x) for x in ref["sample_codes"][s]]:
+                same += 1
+                assert abs(it.log_prob - ref["sample_logp"][s]) <= 1e-4 * max(1.0, abs(ref["sample_logp"][s]))
+    print(f"sampling {preset} {sample}: {same}/{total} sequences identical to the reference")
+    assert same >= 0.9 * total

@@ -93,23 +93,26 @@ struct MoeW {
 
 void validate_batch(const orx_config& cfg, const orx_user_batch& b) {  // validate_context, policy.cpp:23-38
   require(b.n_users >= 0, "negative user count");
+  // messages are only built on failure (this runs over every record of every request)
+  auto fail = [](const char* name, const char* what) { throw InvalidArgument(std::string(name) + what); };
+  const uint32_t label_limit = cfg.n_label_flags >= 32 ? 0u : (1u << cfg.n_label_flags);
   auto check = [&](const orx_records& r, int cap, const char* name) {
     if (b.n_users == 0) return;
-    require(r.offsets != nullptr, std::string(name) + ": offsets required");
-    require(r.offsets[0] == 0, std::string(name) + ": offsets must start at 0");
+    if (!r.offsets) fail(name, ": offsets required");
+    if (r.offsets[0] != 0) fail(name, ": offsets must start at 0");
     for (int u = 0; u < b.n_users; ++u) {
-      int64_t s = r.offsets[u], e = r.offsets[u + 1];
-      require(e >= s, std::string(name) + ": offsets must be non-decreasing");
-      require(e - s <= cap, std::string(name) + " sequence exceeds its configured cap");
+      const int64_t s = r.offsets[u], e = r.offsets[u + 1];
+      if (e < s) fail(name, ": offsets must be non-decreasing");
+      if (e - s > cap) fail(name, " sequence exceeds its configured cap");
       for (int64_t i = s; i < e; ++i) {
-        if (i > s) require(r.ts[i] >= r.ts[i - 1], std::string(name) + " sequence not time-ordered");
-        require(r.playtime[i] <= r.duration[i] * 1.0 + 1e-6, "playtime exceeds duration");
-        require(cfg.n_label_flags >= 32 || r.labels[i] < (1u << cfg.n_label_flags), "label bits outside defined flags");
+        if (i > s && !(r.ts[i] >= r.ts[i - 1])) fail(name, " sequence not time-ordered");
+        if (!(r.playtime[i] <= r.duration[i] * 1.0 + 1e-6)) throw InvalidArgument("playtime exceeds duration");
+        if (label_limit && r.labels[i] >= label_limit) throw InvalidArgument("label bits outside defined flags");
         if (cfg.use_sid_history) {
-          require(r.sid != nullptr, "sid history enabled but record lacks semantic id codes");
+          if (!r.sid) throw InvalidArgument("sid history enabled but record lacks semantic id codes");
           for (int l = 0; l < cfg.n_code_layers; ++l) {
-            int c = r.sid[i * cfg.n_code_layers + l];
-            require(c >= 0 && c < cfg.codebook_size, "sid code outside its layer vocabulary");
+            const int c = r.sid[i * cfg.n_code_layers + l];
+            if (c < 0 || c >= cfg.codebook_size) throw InvalidArgument("sid code outside its layer vocabulary");
           }
         }
       }

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <type_traits>
 
 #include "attention.cuh"
@@ -644,31 +645,48 @@ class EngineT final : public Engine {
     }
     s.n_keys = kpos;
     s.n_pad_keys = npad;
-    for (int p = 0; p < 3; ++p) {
-      const orx_records& r = *rs[p];
-      const size_t n = s.n_rec[p];
-      if (n == 0) continue;
-      memcpy(H + s.off_vid[p], r.vid, 8 * n);
-      memcpy(H + s.off_aid[p], r.aid, 4 * n);
-      memcpy(H + s.off_lab[p], r.labels, 4 * n);
-      for (size_t i = 0; i < n; ++i) {
-        F32(s.off_tag[p])[i] = static_cast<float>(r.tag[i]);
-        F32(s.off_ts[p])[i] = static_cast<float>(r.ts[i]);
-        F32(s.off_play[p])[i] = static_cast<float>(r.playtime[i]);
-        F32(s.off_dur[p])[i] = static_cast<float>(r.duration[i]);
-      }
-      if (c.use_sid_history) memcpy(H + s.off_sid[p], r.sid, 4 * n * L);
-      int32_t* map = I32(s.off_map[p]);
-      for (int u = 0; u < s.U; ++u) {
-        int64_t b0 = r.offsets[u], e0 = r.offsets[u + 1];
-        int cnt = static_cast<int>(e0 - b0);
-        for (int64_t i = b0; i < e0; ++i) {
-          int j = static_cast<int>(i - b0);
-          if (p == 0) map[i] = u * Tn + 1 + (c.short_len - cnt) + j;  // left padding, policy.cpp:209-215
-          else if (p == 1) map[i] = u * Tn + 1 + c.short_len + (c.positive_len - cnt) + j;
-          else map[i] = I32(s.off_kstart)[u] + j;
+    // Record copy / conversion and row maps, split over user ranges on worker
+    // threads (this host packing sits inside every end-to-end request).
+    auto pack_users = [&](int u0, int u1) {
+      for (int p = 0; p < 3; ++p) {
+        const orx_records& r = *rs[p];
+        if (s.n_rec[p] == 0) continue;
+        const int64_t i0 = r.offsets[u0], i1 = r.offsets[u1], n = i1 - i0;
+        if (n == 0) continue;
+        memcpy(H + s.off_vid[p] + 8 * i0, r.vid + i0, 8 * n);
+        memcpy(H + s.off_aid[p] + 4 * i0, r.aid + i0, 4 * n);
+        memcpy(H + s.off_lab[p] + 4 * i0, r.labels + i0, 4 * n);
+        float *tg = F32(s.off_tag[p]), *ts = F32(s.off_ts[p]), *pl = F32(s.off_play[p]), *du = F32(s.off_dur[p]);
+        for (int64_t i = i0; i < i1; ++i) {
+          tg[i] = static_cast<float>(r.tag[i]);
+          ts[i] = static_cast<float>(r.ts[i]);
+          pl[i] = static_cast<float>(r.playtime[i]);
+          du[i] = static_cast<float>(r.duration[i]);
+        }
+        if (c.use_sid_history) memcpy(H + s.off_sid[p] + 4 * i0 * L, r.sid + i0 * L, 4 * n * L);
+        int32_t* map = I32(s.off_map[p]);
+        for (int u = u0; u < u1; ++u) {
+          const int64_t b0 = r.offsets[u], e0 = r.offsets[u + 1];
+          const int cnt = static_cast<int>(e0 - b0);
+          for (int64_t i = b0; i < e0; ++i) {
+            const int j = static_cast<int>(i - b0);
+            if (p == 0) map[i] = u * Tn + 1 + (c.short_len - cnt) + j;  // left padding, policy.cpp:209-215
+            else if (p == 1) map[i] = u * Tn + 1 + c.short_len + (c.positive_len - cnt) + j;
+            else map[i] = I32(s.off_kstart)[u] + j;
+          }
         }
       }
+    };
+    const int64_t total_rec = static_cast<int64_t>(s.n_rec[0]) + s.n_rec[1] + s.n_rec[2];
+    const int n_workers = static_cast<int>(std::min<int64_t>(
+        {8, std::max(1u, std::thread::hardware_concurrency()), std::max<int64_t>(1, total_rec / 32768), s.U}));
+    if (n_workers <= 1) {
+      pack_users(0, s.U);
+    } else {
+      std::vector<std::thread> pool;
+      for (int w = 0; w < n_workers; ++w)
+        pool.emplace_back(pack_users, s.U * w / n_workers, s.U * (w + 1) / n_workers);
+      for (auto& t : pool) t.join();
     }
     CUDA_CHECK(cudaMemcpyAsync(dev_stage_, host_stage_, s.bytes, cudaMemcpyHostToDevice, st_));
     h2d_bytes += static_cast<int64_t>(s.bytes);

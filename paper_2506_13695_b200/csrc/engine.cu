@@ -291,6 +291,18 @@ class EngineT final : public Engine {
     t_age_ = up(hw, "emb.age");
     t_vid_ = up(hw, "emb.vid");
     t_aid_ = up(hw, "emb.aid");
+    if constexpr (kBf16) {  // bf16 copies for the feature-row gathers
+      auto up16 = [&](const std::string& n) {
+        const Tensor& t = hw.get(n);
+        std::vector<T> h(t.data.size());
+        for (size_t i = 0; i < h.size(); ++i) h[i] = to_t<T>(t.data[i]);
+        T* p = ar_.alloc<T>(h.size());
+        CUDA_CHECK(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+        return p;
+      };
+      t_vid16_ = up16("emb.vid");
+      t_aid16_ = up16("emb.aid");
+    }
     t_label_ = up(hw, "emb.label");
     t_tag_ = up(hw, "emb.tag");
     t_ts_ = up(hw, "emb.ts");
@@ -720,6 +732,10 @@ class EngineT final : public Engine {
     t.play = t_play_;
     t.dur = t_dur_;
     t.label = t_label_;
+    if constexpr (kBf16) {
+      t.vid16 = t_vid16_;
+      t.aid16 = t_aid16_;
+    }
     for (int l = 0; l < c.n_code_layers && l < 8; ++l) t.tokens[l] = tokens_[l];
     t.d = c.d_model;
     t.aid_dim = aid_dim(c);
@@ -1360,6 +1376,7 @@ class EngineT final : public Engine {
   // weights
   const float *t_uid_, *t_gender_, *t_age_, *t_vid_, *t_aid_, *t_label_, *t_tag_, *t_ts_, *t_play_, *t_dur_;
   const float *pad_s_, *pad_p_, *pad_l_, *pos_, *bos_;
+  const __nv_bfloat16 *t_vid16_ = nullptr, *t_aid16_ = nullptr;
   std::vector<const float*> tokens_;
   std::vector<Lin<T>> heads_;
   Mlp p_static_, p_short_, p_pos_, p_life_;

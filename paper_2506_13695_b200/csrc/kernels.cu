@@ -146,6 +146,61 @@ __global__ void __launch_bounds__(256) features8_kernel(RecordsDev r, FeatureTab
   }
 }
 
+// bf16 engine, vid_only = 0, no sid history: warp per record, every lane first
+// issues all of its 16-byte loads (vid / aid rows from the bf16 tables), then
+// computes the scalar / label sections and stores (memory-level parallelism).
+constexpr int kFeatMaxChunks = 12;  // ldo <= 3072
+__global__ void __launch_bounds__(256) features16_kernel(RecordsDev r, FeatureTables t, __nv_bfloat16* __restrict__ out,
+                                                         int ldo) {
+  const int d = t.d, ad = t.aid_dim, mn = t.minor;
+  const int F = d + ad + 5 * mn;
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < r.n; row += gridDim.x * (blockDim.x >> 5)) {
+    const int vid = hashed(r.vid[row], t.vid_vocab);
+    const int aid = hashed(r.aid[row], t.aid_vocab);
+    const float sc[4] = {r.tag[row], r.ts[row], r.play[row], r.dur[row]};
+    const uint32_t lab = r.labels[row];
+    uint4 g[kFeatMaxChunks];
+#pragma unroll
+    for (int k = 0; k < kFeatMaxChunks; ++k) {
+      const int c0 = (lane + 32 * k) * 8;
+      if (c0 < d) g[k] = __ldg(reinterpret_cast<const uint4*>(t.vid16 + (size_t)vid * d + c0));
+      else if (c0 < d + ad) g[k] = __ldg(reinterpret_cast<const uint4*>(t.aid16 + (size_t)aid * ad + (c0 - d)));
+    }
+    __nv_bfloat16* o = out + (size_t)row * ldo;
+#pragma unroll
+    for (int k = 0; k < kFeatMaxChunks; ++k) {
+      const int c0 = (lane + 32 * k) * 8;
+      if (c0 >= ldo) break;
+      uint4 w = g[k];
+      if (c0 >= d + ad) {
+        float v[8];
+        if (c0 < F) {
+          const int cc = c0 - d - ad, f = cc / mn, j0 = cc % mn;
+          if (f < 4) {  // x * w + b (policy.cpp:175-188)
+            const float* p = f == 0 ? t.tag : f == 1 ? t.ts : f == 2 ? t.play : t.dur;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = sc[f] * p[j0 + j] + p[mn + j0 + j];
+          } else {  // labels multi-hot . (5 x minor) (policy.cpp:190-195)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = 0.f;
+            for (int b = 0; b < t.n_flags; ++b)
+              if ((lab >> b) & 1u) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] += t.label[b * mn + j0 + j];
+              }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = 0.f;
+        }
+        w = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+      }
+      *reinterpret_cast<uint4*>(o + c0) = w;
+    }
+  }
+}
+
 template <class T>
 __global__ void static_features_kernel(int U, const int32_t* uid, const int32_t* gender, const int32_t* age,
                                        const float* ue, const float* ge, const float* ae, int sd, int uv, int gv,
@@ -522,16 +577,35 @@ __global__ void __launch_bounds__(256, 2) moe_route2_kernel(int rows, int d, int
 // Segment offsets padded to the GEMM expert tile (128 rows, 256 for the CTA-pair kernel); tile -> expert table.
 __global__ void moe_plan_kernel(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
                                 int32_t* n_mtiles, int tile_rows) {
-  if (threadIdx.x != 0) return;
-  int off = 0, tile = 0;
-  for (int e = 0; e < E; ++e) {
-    cursor[e] = off;
-    int nt = (counts[e] + tile_rows - 1) / tile_rows;
-    for (int i = 0; i < nt && tile < max_tiles; ++i) tile_expert[tile++] = e;
-    off += nt * tile_rows;
+  // lane e: tiles of expert e, exclusive prefix over experts (E <= 32), then
+  // every thread of the block fills the tile -> expert table
+  __shared__ int first[33];
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    const int nt = lane < E ? (counts[lane] + tile_rows - 1) / tile_rows : 0;
+    int incl = nt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane < E) {
+      first[lane] = incl - nt;
+      cursor[lane] = (incl - nt) * tile_rows;
+    }
+    if (lane == 31) {
+      first[E] = min(incl, max_tiles);
+      *n_mtiles = min(incl, max_tiles);
+    }
   }
-  *n_mtiles = tile;
-  for (int i = tile; i < max_tiles; ++i) tile_expert[i] = -1;
+  __syncthreads();
+  const int total = first[E];
+  for (int i = threadIdx.x; i < max_tiles; i += blockDim.x) {
+    int e = -1;
+    if (i < total)
+      for (int x = 0; x < E; ++x)
+        if (i >= first[x]) e = x;
+    tile_expert[i] = e;
+  }
 }
 
 template <class T>
@@ -556,6 +630,43 @@ __global__ void moe_scatter_kernel(int rows, int k, int d, const T* __restrict__
     for (int c = lane * 8; c < d; c += 256) *reinterpret_cast<uint4*>(dst + c) = *reinterpret_cast<const uint4*>(src + c);
   } else {
     for (int c = lane; c < d; c += 32) dst[c] = src[c];
+  }
+}
+
+// Same permutation with warp-aggregated slot allocation: a warp takes 32
+// (row, expert) pairs, lanes routed to the same expert share one atomic
+// (hot experts take a large share of the tokens under random-init routing),
+// then the warp copies the 32 rows with 16-byte accesses (bf16, d % 8 == 0).
+__global__ void __launch_bounds__(256) moe_scatter32_kernel(int rows, int k, int d, const __nv_bfloat16* __restrict__ x,
+                                                            int ldx, const int32_t* __restrict__ sel,
+                                                            const float* __restrict__ wts, int32_t* __restrict__ cursor,
+                                                            int32_t* __restrict__ slot, __nv_bfloat16* __restrict__ xg,
+                                                            float* __restrict__ row_scale) {
+  const int lane = threadIdx.x & 31;
+  const int base_pair = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+  const int n_pairs = rows * k;
+  if (base_pair >= n_pairs) return;
+  const int gw = base_pair + lane;
+  const bool on = gw < n_pairs;
+  const int e = on ? sel[gw] : -1;
+  const unsigned act = __ballot_sync(0xffffffffu, on);
+  const unsigned peers = __match_any_sync(0xffffffffu, e);
+  const int leader = __ffs(peers) - 1;
+  int base = 0;
+  if (on && lane == leader) base = atomicAdd(&cursor[e], __popc(peers));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  const int my_slot = base + __popc(peers & ((1u << lane) - 1u));
+  if (on) {
+    slot[gw] = my_slot;
+    row_scale[my_slot] = wts[gw];
+  }
+  for (int i = 0; i < 32; ++i) {
+    if (!((act >> i) & 1u)) break;
+    const int s = __shfl_sync(0xffffffffu, my_slot, i);
+    const int r = (base_pair + i) / k;
+    const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)r * ldx);
+    uint4* dst = reinterpret_cast<uint4*>(xg + (size_t)s * d);
+    for (int c = lane; c < d / 8; c += 32) dst[c] = src[c];
   }
 }
 
@@ -655,6 +766,13 @@ template <class T>
 void launch_features(const RecordsDev& r, const FeatureTables& t, T* out, int ldo, cudaStream_t s) {
   if (r.n <= 0) return;
   const bool vec = t.d % 8 == 0 && ldo % 8 == 0 && (t.vid_only || (t.aid_dim % 8 == 0 && t.minor % 8 == 0));
+  if constexpr (sizeof(T) == 2) {
+    if (vec && t.vid16 && t.aid16 && !t.use_sid && !t.vid_only && ldo <= 8 * 32 * kFeatMaxChunks) {
+      ORX_LAUNCH(features16_kernel<<<grid_for(r.n, 8, num_sms() * 8), 256, 0, s>>>(
+          r, t, reinterpret_cast<__nv_bfloat16*>(out), ldo));
+      return;
+    }
+  }
   if (vec) {
     ORX_LAUNCH(features8_kernel<T><<<grid_for(r.n, 8, num_sms() * 8), 256, 0, s>>>(r, t, out, ldo));
     return;
@@ -735,13 +853,22 @@ void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, co
 void launch_moe_plan(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
                      int32_t* n_mtiles, int tile_rows, cudaStream_t s) {
   ORX_LAUNCH_CAT(PROF_MOE_ROUTE,
-                 moe_plan_kernel<<<1, 32, 0, s>>>(E, counts, cursor, tile_expert, max_tiles, n_mtiles, tile_rows));
+                 moe_plan_kernel<<<1, 256, 0, s>>>(E, counts, cursor, tile_expert, max_tiles, n_mtiles, tile_rows));
 }
 template <class T>
 void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
                         int32_t* cursor, int32_t* slot, T* xg, float* row_scale, cudaStream_t s) {
   if (rows <= 0) return;
   long long warps = (long long)rows * k;
+  if constexpr (sizeof(T) == 2) {
+    if (d % 8 == 0 && ldx % 8 == 0) {
+      const long long w32 = (warps + 31) / 32;
+      ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_scatter32_kernel<<<static_cast<int>((w32 + 7) / 8), 256, 0, s>>>(
+                                         rows, k, d, reinterpret_cast<const __nv_bfloat16*>(x), ldx, sel, wts, cursor,
+                                         slot, reinterpret_cast<__nv_bfloat16*>(xg), row_scale));
+      return;
+    }
+  }
   ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_scatter_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(rows, k, d, x, ldx, sel, wts,
                                                                                       cursor, slot, xg, row_scale));
 }

@@ -30,6 +30,10 @@ struct FeatureTables {  // fp32 embedding tables (policy.cpp:139-198)
   const float* label;     // [n_flags][minor]
   const float* tokens[8]; // sid history: per code layer [V][d]
   int d, aid_dim, minor, vid_vocab, aid_vocab, n_flags, n_code_layers, use_sid, vid_only;
+  // bf16 copies of the vid / aid tables (bf16 engine): a single-row gather
+  // rounded once gives the same bf16 output as the fp32 row
+  const __nv_bfloat16* vid16 = nullptr;
+  const __nv_bfloat16* aid16 = nullptr;
 };
 
 template <class T>

@@ -213,7 +213,14 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tb, int row
     constexpr int CH = BN / 32 / 2;
     const bool hr = ok && e.resid != nullptr;
     float rc[32];
-    if (hr) epi_load_resid(e, orow, nt * BN + half * CH * 32, rc);  // in flight while the MMAs finish
+    if (hr) {
+      // pull this thread's residual row segment (CH * 128 B) into L2 while the MMAs run;
+      // the chunk loads below then hit L2 instead of waiting on HBM one chunk at a time
+      const float* rp = e.resid + (size_t)orow * e.ld_resid + nt * BN + half * CH * 32;
+      if (nt * BN + (half + 1) * CH * 32 <= e.n_out && (reinterpret_cast<uintptr_t>(rp) & 15) == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rp), "r"(CH * 128) : "memory");
+      epi_load_resid(e, orow, nt * BN + half * CH * 32, rc);  // in flight while the MMAs finish
+    }
     mbar_wait(tfull, acc_phase);
     tc_fence_after();
 #pragma unroll 1

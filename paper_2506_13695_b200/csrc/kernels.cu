@@ -150,53 +150,56 @@ __global__ void __launch_bounds__(256) features8_kernel(RecordsDev r, FeatureTab
 // issues all of its 16-byte loads (vid / aid rows from the bf16 tables), then
 // computes the scalar / label sections and stores (memory-level parallelism).
 constexpr int kFeatMaxChunks = 12;  // ldo <= 3072
-__global__ void __launch_bounds__(256) features16_kernel(RecordsDev r, FeatureTables t, __nv_bfloat16* __restrict__ out,
-                                                         int ldo) {
+constexpr int kFeatBatch = 4;       // 16-byte loads in flight per lane
+__global__ void __launch_bounds__(256, 4) features16_kernel(RecordsDev r, FeatureTables t,
+                                                            __nv_bfloat16* __restrict__ out, int ldo) {
   const int d = t.d, ad = t.aid_dim, mn = t.minor;
   const int F = d + ad + 5 * mn;
   const int lane = threadIdx.x & 31;
   for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < r.n; row += gridDim.x * (blockDim.x >> 5)) {
     const int vid = hashed(r.vid[row], t.vid_vocab);
     const int aid = hashed(r.aid[row], t.aid_vocab);
-    const float sc[4] = {r.tag[row], r.ts[row], r.play[row], r.dur[row]};
-    const uint32_t lab = r.labels[row];
-    uint4 g[kFeatMaxChunks];
-#pragma unroll
-    for (int k = 0; k < kFeatMaxChunks; ++k) {
-      const int c0 = (lane + 32 * k) * 8;
-      if (c0 < d) g[k] = __ldg(reinterpret_cast<const uint4*>(t.vid16 + (size_t)vid * d + c0));
-      else if (c0 < d + ad) g[k] = __ldg(reinterpret_cast<const uint4*>(t.aid16 + (size_t)aid * ad + (c0 - d)));
-    }
+    const __nv_bfloat16* vrow = t.vid16 + (size_t)vid * d;
+    const __nv_bfloat16* arow = t.aid16 + (size_t)aid * ad;
     __nv_bfloat16* o = out + (size_t)row * ldo;
+    for (int k0 = 0; k0 < kFeatMaxChunks; k0 += kFeatBatch) {
+      if ((lane + 32 * k0) * 8 >= ldo) break;
+      uint4 g[kFeatBatch];
 #pragma unroll
-    for (int k = 0; k < kFeatMaxChunks; ++k) {
-      const int c0 = (lane + 32 * k) * 8;
-      if (c0 >= ldo) break;
-      uint4 w = g[k];
-      if (c0 >= d + ad) {
-        float v[8];
-        if (c0 < F) {
-          const int cc = c0 - d - ad, f = cc / mn, j0 = cc % mn;
-          if (f < 4) {  // x * w + b (policy.cpp:175-188)
-            const float* p = f == 0 ? t.tag : f == 1 ? t.ts : f == 2 ? t.play : t.dur;
+      for (int k = 0; k < kFeatBatch; ++k) {
+        const int c0 = (lane + 32 * (k0 + k)) * 8;
+        if (c0 < d) g[k] = __ldg(reinterpret_cast<const uint4*>(vrow + c0));
+        else if (c0 < d + ad) g[k] = __ldg(reinterpret_cast<const uint4*>(arow + (c0 - d)));
+      }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = sc[f] * p[j0 + j] + p[mn + j0 + j];
-          } else {  // labels multi-hot . (5 x minor) (policy.cpp:190-195)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = 0.f;
-            for (int b = 0; b < t.n_flags; ++b)
-              if ((lab >> b) & 1u) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) v[j] += t.label[b * mn + j0 + j];
-              }
-          }
-        } else {
+      for (int k = 0; k < kFeatBatch; ++k) {
+        const int c0 = (lane + 32 * (k0 + k)) * 8;
+        if (c0 >= ldo) break;
+        uint4 w = g[k];
+        if (c0 >= d + ad) {
+          float v[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) v[j] = 0.f;
+          if (c0 < F) {
+            const int cc = c0 - d - ad, f = cc / mn, j0 = cc % mn;
+            if (f < 4) {  // x * w + b (policy.cpp:175-188)
+              const float x = f == 0 ? r.tag[row] : f == 1 ? r.ts[row] : f == 2 ? r.play[row] : r.dur[row];
+              const float* p = f == 0 ? t.tag : f == 1 ? t.ts : f == 2 ? t.play : t.dur;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[j] = x * p[j0 + j] + p[mn + j0 + j];
+            } else {  // labels multi-hot . (5 x minor) (policy.cpp:190-195)
+              const uint32_t lab = r.labels[row];
+              for (int b = 0; b < t.n_flags; ++b)
+                if ((lab >> b) & 1u) {
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) v[j] += t.label[b * mn + j0 + j];
+                }
+            }
+          }
+          w = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
         }
-        w = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+        *reinterpret_cast<uint4*>(o + c0) = w;
       }
-      *reinterpret_cast<uint4*>(o + c0) = w;
     }
   }
 }
@@ -243,6 +246,18 @@ __global__ void rmsnorm_kernel(int rows, int d, const float* __restrict__ x, int
   float r = rsqrtf(ss / d + 1e-6f);
   T* o = out + (size_t)row * ldo;
   for (int c = lane; c < d; c += 32) o[c] = from_f<T>(xr[c] * r * g[c]);
+}
+
+// Vectorised variant: cols % 4 == 0, rows 16-byte aligned; thread per 4 elements.
+template <class T>
+__global__ void convert4_kernel(int rows, int cols, const float* __restrict__ x, int ldx, T* __restrict__ out,
+                                int ldo) {
+  const int q = cols / 4;
+  const long long n = (long long)rows * q;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(i / q), c = static_cast<int>(i % q) * 4;
+    st4(out + (size_t)r * ldo + c, __ldg(reinterpret_cast<const float4*>(x + (size_t)r * ldx + c)));
+  }
 }
 
 template <class T>
@@ -797,6 +812,11 @@ void launch_rmsnorm(int rows, int d, const float* x, int ldx, const float* gain,
 template <class T>
 void launch_convert(int rows, int cols, const float* x, int ldx, T* out, int ldo, cudaStream_t s) {
   if (rows <= 0) return;
+  if (cols % 4 == 0 && ldx % 4 == 0 && ldo % 4 == 0) {
+    ORX_LAUNCH(convert4_kernel<T><<<grid_for((long long)rows * cols / 4, 256), 256, 0, s>>>(rows, cols, x, ldx, out,
+                                                                                          ldo));
+    return;
+  }
   ORX_LAUNCH(convert_kernel<T><<<grid_for((long long)rows * cols, 256), 256, 0, s>>>(rows, cols, x, ldx, out, ldo));
 }
 template <class T>

@@ -153,7 +153,9 @@ ORX_DEV uint32_t mapa_shared(const void* p, uint32_t rank) {
   return r;
 }
 ORX_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  // default .release.cta semantics (as CUTLASS ClusterBarrier::arrive): a cluster-scope release would
+  // fence every outstanding global store of the epilogue thread (MEMBAR.GPU) before the TMEM hand-back
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load into this CTA's smem, completing bytes on an mbarrier that may
 // live in the peer CTA of the pair (`bar_cluster` is a shared::cluster address).

@@ -5,14 +5,17 @@
 //             written transposed by the producing GEMM's epilogue) in 64-key
 //             blocks, double-buffered
 //   warp 1    one thread issues tcgen05.mma:
-//               S_j  = Q . K_j^T   (M=128, N=64, K=dh)   -> TMEM, 2 buffers
-//               O   += P_j . V_j   (M=128, N=dh, K=64)   -> TMEM
+//               S_j  = Q . K_j^T   (M=128, N=64, K=dh)    -> TMEM, 2 buffers
+//               O   += P_j . V_j   (M=128, N=dh, K=64)     -> TMEM, A = P from TMEM
 //             S_{j+1} is issued before P_j is ready, so QK^T of the next block
 //             overlaps the softmax of the current one
 //   warps 2-5 softmax, one thread per query row (TMEM lane = row): row max
 //             with lazy rescaling (O in TMEM is rescaled only when the running
-//             max grows by more than 2^8), P = exp2 in bf16 written to shared
-//             memory in the 128-byte-swizzled K-major UMMA layout, final O / l
+//             max grows by more than 2^8), P = exp2 packed bf16x2 and stored
+//             back into the block's own S columns (tcgen05.st) as the A operand
+//             of P.V, final O / l. With P in TMEM (two S/P buffers) the softmax
+//             of block j+1 never waits for P_j . V_j; MMAs run in issue order,
+//             so S_{j+2} overwrites P_j only after P_j . V_j has read it.
 // Semantics are mha_core's (tape.cpp:822-905): softmax(Q K^T / sqrt(dh)) V,
 // max-subtracted, keys beyond the segment length masked.
 #include <cfloat>
@@ -42,7 +45,17 @@ ORX_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
       : "memory");
 }
 ORX_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-ORX_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// D[tmem] (+)= A[tmem] * B[smem]^T (A: 128 lanes x K, bf16 packed two per 32-bit column)
+ORX_DEV void tc_mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
 
 template <int DH>
 struct Fmha {
@@ -51,8 +64,7 @@ struct Fmha {
   static constexpr uint32_t Q_BYTES = BQ * DH * 2;    // CB blocks of [128 rows x 128 B]
   static constexpr uint32_t K_BYTES = BK * DH * 2;    // CB blocks of [64 rows x 128 B]
   static constexpr uint32_t V_BYTES = DH * BK * 2;    // [DH rows (head dims) x 64 keys]
-  static constexpr uint32_t P_BYTES = BQ * BK * 2;    // [128 rows x 64 keys]
-  static constexpr uint32_t SMEM = Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + P_BYTES + 128;  // + barriers
+  static constexpr uint32_t SMEM = Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + 128;  // + barriers
   static constexpr uint32_t TMEM_COLS = 2 * BK + DH <= 256 ? 256 : 512;  // S[2] + O
 };
 
@@ -67,13 +79,11 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + F::Q_BYTES;          // [2][K_BYTES]
   uint8_t* sV = sK + 2 * F::K_BYTES;      // [2][V_BYTES]
-  uint8_t* sP = sV + 2 * F::V_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + F::P_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * F::V_BYTES);
   uint64_t& q_full = bars[0];
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
   uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_empty = bars + 7;   // [2]
   uint64_t& p_full = bars[9];
   uint64_t& o_done = bars[10];
   uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 11);
@@ -93,7 +103,6 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&s_empty[s], 4);
     }
     mbar_init(&p_full, 4);
     mbar_init(&o_done, 1);
@@ -134,10 +143,11 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
         const int st = j & 1;
         mbar_wait(&p_full, j & 1);
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sP), b0 = smem_u32(sV + st * F::V_BYTES);
+        const uint32_t b0 = smem_u32(sV + st * F::V_BYTES);
+        // A = P_j: 128 lanes x 64 keys bf16 = 32 TMEM columns at the start of S buffer st, 8 per K=16 step
 #pragma unroll
         for (int k = 0; k < F::BK / 16; ++k)
-          tc_mma_bf16(t_o, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc_o, (j | k) != 0);
+          tc_mma_bf16_ts(t_o, t_s + st * F::BK + k * 8, umma_desc_sw128(b0 + k * 32), idesc_o, (j | k) != 0);
         tc_commit(&o_done);
         tc_commit(&kv_empty[st]);
       };
@@ -145,7 +155,6 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
       for (int j = 0; j < nb; ++j) {
         const int st = j & 1;
         mbar_wait(&kv_full[st], (j >> 1) & 1);
-        if (j >= 2) mbar_wait(&s_empty[st], ((j >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + st * F::K_BYTES);
 #pragma unroll
@@ -166,7 +175,6 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
     const float scale_log2 = rsqrtf(static_cast<float>(DH)) * 1.4426950408889634f;
     float m = -FLT_MAX, l = 0.f;
     bool first = true;
-    uint8_t* prow = sP + (r >> 3) * 1024 + (r & 7) * 128;
     for (int j = 0; j < nb; ++j) {
       const int st = j & 1;
       mbar_wait(&s_full[st], (j >> 1) & 1);
@@ -175,9 +183,6 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
       tmem_ld32_async(t_s + lane_off + st * F::BK, sa);
       tmem_ld32_async(t_s + lane_off + st * F::BK + 32, sb);
       tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[st]);
       const int valid = klen - j * F::BK;
       float x[64];
 #pragma unroll
@@ -205,7 +210,12 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
         pk[i] = pack_bf16(p0, p1);
       }
       l = l * corr + sum;
-      if (j >= 1) {  // P buffer and O are free once P_{j-1} . V_{j-1} has completed
+      // P_j replaces S_j in TMEM (columns [0, 32) of this buffer, keys 2c / 2c+1 in column c)
+      tmem_st32(t_s + lane_off + st * F::BK, pk);
+      // P_{j-1} . V_{j-1} (issued when this thread finished block j-1) is normally long done
+      // by now; waiting for it every block keeps o_done at most one phase ahead of its waiters
+      // and orders the O rescale after it
+      if (j >= 1) {
         mbar_wait(&o_done, (j - 1) & 1);
         tc_fence_after();
       }
@@ -220,15 +230,8 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
           for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * c);
           tmem_st32(t_o + lane_off + cc * 32, o);
         }
-        tmem_wait_st();
       }
-      // P row: 8 chunks of 16 B (8 keys), chunk c stored at slot c ^ (row % 8) (128-byte swizzle)
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint4 v = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = v;
-      }
-      fence_proxy_async_smem();
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full);

@@ -268,6 +268,30 @@ int orx_debug_ep_plan(int32_t world, int32_t rank, int32_t n_experts, const int3
                       int32_t max_tiles, int64_t* send_cnt, int64_t* send_off, int64_t* recv_cnt, int64_t* recv_off,
                       int32_t* tab, int32_t* tiles, int32_t* n_tiles);
 
+/* Lifelong-history compression on the GPU (the step before the encoder;
+ * compress_lifelong, policy.cpp:447-510, over hierarchical K-means,
+ * kmeans.cpp:22-183): per user u, records [offsets[u], offsets[u+1]) of
+ * `history` with content rows content[i * content_dim ...] (f64) are
+ * clustered (threshold records per leaf) with the reference Rng seeded by
+ * rng_seeds[u] (build_user_context uses cfg.seed ^ (0x9e3779b97f4a7c15 *
+ * (user + 1))), and replaced by their leaf's representative (categorical
+ * fields) with leaf-mean tag / playtime / duration and their own ts; the last
+ * min(n_u, max_out) records are written to `out` (out->offsets [n_users+1]). */
+typedef struct orx_records_out {
+  int64_t* offsets;
+  int64_t* vid;
+  int32_t* aid;
+  double* tag;
+  double* ts;
+  double* playtime;
+  double* duration;
+  uint32_t* labels;
+  int32_t* sid; /* [n * n_code_layers] or NULL */
+} orx_records_out;
+int orx_compress_lifelong(int device, int32_t n_users, const orx_records* history, const double* content,
+                          int32_t content_dim, int32_t threshold, int32_t max_out, int32_t n_code_layers,
+                          const uint64_t* rng_seeds, orx_records_out* out);
+
 /* Seeded synthetic users (synth_users.hpp). */
 int orx_synth_batch_create(uint64_t seed, int64_t user_begin, int32_t n_users, int32_t n_short, int32_t n_positive,
                            int32_t n_lifelong, orx_synth_batch** out);

@@ -134,6 +134,8 @@ struct Args {
   uint64_t sample_seed = 5;
   double temperature = 1.0, top_p = 1.0;
   int top_k = 0;
+  // compress: seeded raw histories + clustered content for compress_lifelong
+  int hist_len = 600, content_dim = 32, threshold = 8, max_out = 2000;
 };
 
 Args parse(int argc, char** argv) {
@@ -167,6 +169,10 @@ Args parse(int argc, char** argv) {
     else if (k == "--trie-items") a.trie_items = std::stoi(next());
     else if (k == "--trie-seed") a.trie_seed = std::stoull(next());
     else if (k == "--trie-fanout") a.trie_fanout = std::stoi(next());
+    else if (k == "--hist-len") a.hist_len = std::stoi(next());
+    else if (k == "--content-dim") a.content_dim = std::stoi(next());
+    else if (k == "--threshold") a.threshold = std::stoi(next());
+    else if (k == "--max-out") a.max_out = std::stoi(next());
     else if (k == "--sample") a.sample = true;
     else if (k == "--sample-seed") a.sample_seed = std::stoull(next());
     else if (k == "--temperature") a.temperature = std::stod(next());
@@ -315,6 +321,74 @@ int cmd_dump(const Args& a) {
   return 0;
 }
 
+// compress_lifelong (policy.cpp:447-510) on seeded raw histories: user u has
+// hist_len + 37 * u records whose content rows are drawn around 24 latent
+// centres; the user's Rng is build_user_context's (policy.cpp:564).
+int cmd_compress(const Args& a) {
+  const int D = a.content_dim;
+  std::vector<int64_t> off{0}, vid, ooff{0}, ovid;
+  std::vector<int32_t> aid, oaid;
+  std::vector<uint32_t> lab, olab;
+  std::vector<double> tag, ts, play, dur, content, otag, ots, oplay, odur;
+  std::vector<uint64_t> seeds;
+  Rng world(a.user_seed);
+  std::vector<double> centres(static_cast<size_t>(24) * D);
+  for (auto& c : centres) c = world.normal();
+  for (int u = 0; u < a.n_users; ++u) {
+    const int n = a.hist_len + 37 * u;
+    Rng r = Rng(a.user_seed).split(static_cast<uint64_t>(u));
+    std::vector<InteractionFeature> hist;
+    Array cont({n, D});
+    double t = -static_cast<double>(n) * 0.01;
+    for (int i = 0; i < n; ++i) {
+      InteractionFeature f;
+      f.vid = static_cast<int64_t>(r.randint(1 << 20));
+      f.aid = static_cast<int>(r.randint(100000));
+      f.tag = r.uniform();
+      f.ts = t;
+      t += 0.01;
+      f.duration = r.uniform(0.05, 1.0);
+      f.playtime = f.duration * r.uniform();
+      f.labels = static_cast<uint32_t>(r.randint(32));
+      hist.push_back(f);
+      const int cl = static_cast<int>(r.randint(24));
+      for (int j = 0; j < D; ++j) cont.at(i, j) = centres[static_cast<size_t>(cl) * D + j] + 0.3 * r.normal();
+    }
+    const uint64_t seed = a.cfg.seed ^ (0x9e3779b97f4a7c15ULL * static_cast<uint64_t>(u + 1));
+    Rng krng(seed);
+    auto out = compress_lifelong(hist, cont, a.threshold, a.max_out, krng);
+    seeds.push_back(seed);
+    for (int i = 0; i < n; ++i) {
+      const auto& f = hist[size_t(i)];
+      vid.push_back(f.vid), aid.push_back(f.aid), lab.push_back(f.labels);
+      tag.push_back(f.tag), ts.push_back(f.ts), play.push_back(f.playtime), dur.push_back(f.duration);
+      for (int j = 0; j < D; ++j) content.push_back(cont.at(i, j));
+    }
+    off.push_back(off.back() + n);
+    for (const auto& f : out) {
+      ovid.push_back(f.vid), oaid.push_back(f.aid), olab.push_back(f.labels);
+      otag.push_back(f.tag), ots.push_back(f.ts), oplay.push_back(f.playtime), odur.push_back(f.duration);
+    }
+    ooff.push_back(ooff.back() + static_cast<int64_t>(out.size()));
+  }
+  auto w8 = [&](const char* n, const std::vector<double>& v) {
+    write_npy(a.out + "/" + n + ".npy", "<f8", {v.size()}, v.data(), v.size() * 8);
+  };
+  auto wi8 = [&](const char* n, const std::vector<int64_t>& v) {
+    write_npy(a.out + "/" + n + ".npy", "<i8", {v.size()}, v.data(), v.size() * 8);
+  };
+  auto wi4 = [&](const char* n, const void* p, size_t cnt) {
+    write_npy(a.out + "/" + n + ".npy", "<i4", {cnt}, p, cnt * 4);
+  };
+  wi8("in_offsets", off), wi8("in_vid", vid), wi4("in_aid", aid.data(), aid.size()), wi4("in_labels", lab.data(), lab.size());
+  w8("in_tag", tag), w8("in_ts", ts), w8("in_playtime", play), w8("in_duration", dur);
+  write_npy(a.out + "/in_content.npy", "<f8", {content.size() / size_t(D), size_t(D)}, content.data(), content.size() * 8);
+  write_npy(a.out + "/seeds.npy", "<u8", {seeds.size()}, seeds.data(), seeds.size() * 8);
+  wi8("out_offsets", ooff), wi8("out_vid", ovid), wi4("out_aid", oaid.data(), oaid.size()), wi4("out_labels", olab.data(), olab.size());
+  w8("out_tag", otag), w8("out_ts", ots), w8("out_playtime", oplay), w8("out_duration", odur);
+  return 0;
+}
+
 // Bounded CPU sample of the hot path: per worker process, encode one user and
 // time `calls` decoder calls on beam-shaped prefixes; per-user time is
 // extrapolated to the full beam (1 + 2W scorer calls, generation.cpp:52-56).
@@ -409,6 +483,10 @@ int main(int argc, char** argv) {
       return 0;
     }
     if (a.cmd == "dump") return cmd_dump(a);
+    if (a.cmd == "compress") {
+      if (a.out.empty()) throw std::invalid_argument("--out required");
+      return cmd_compress(a);
+    }
     if (a.cmd == "bench") return cmd_bench(a);
     throw std::invalid_argument("unknown command " + a.cmd);
   } catch (const std::exception& e) {

@@ -51,6 +51,12 @@ class orx_trie(C.Structure):
                 ("child_code", C.POINTER(C.c_int32)), ("child_node", C.POINTER(C.c_int32))]
 
 
+class orx_records_out(C.Structure):
+    _fields_ = [("offsets", C.POINTER(C.c_int64)), ("vid", C.POINTER(C.c_int64)), ("aid", C.POINTER(C.c_int32)),
+                ("tag", C.POINTER(C.c_double)), ("ts", C.POINTER(C.c_double)), ("playtime", C.POINTER(C.c_double)),
+                ("duration", C.POINTER(C.c_double)), ("labels", C.POINTER(C.c_uint32)), ("sid", C.POINTER(C.c_int32))]
+
+
 class orx_gemm_args(C.Structure):
     _fields_ = [
         ("A", C.c_void_p), ("lda", C.c_int32), ("B", C.c_void_p), ("ldb", C.c_int32),
@@ -129,6 +135,9 @@ SIGNATURES = [
     ("orx_debug_ep_plan", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _I32P, C.c_int32, C.c_int32,
                                     C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                     C.POINTER(C.c_int64), _I32P, _I32P, _I32P]),
+    ("orx_compress_lifelong", C.c_int, [C.c_int, C.c_int32, C.POINTER(orx_records), C.POINTER(C.c_double), C.c_int32,
+                                        C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint64),
+                                        C.POINTER(orx_records_out)]),
     ("orx_synth_batch_create", C.c_int, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                          C.POINTER(_P)]),
     ("orx_synth_batch_view", C.c_int, [_P, C.POINTER(orx_user_batch)]),

@@ -12,6 +12,7 @@
 #include "ep_plan.hpp"
 #include "attention.cuh"
 #include "beam.cuh"
+#include "compress.cuh"
 #include "gemm.cuh"
 #include "model.hpp"
 #include "synth_users.hpp"
@@ -468,6 +469,41 @@ int orx_debug_ep_plan(int32_t world, int32_t rank, int32_t n_experts, const int3
       if (recv_off) recv_off[p] = pl.recv_off[p];
     }
     if (n_tiles) *n_tiles = pl.n_tiles;
+  });
+}
+
+int orx_compress_lifelong(int device, int32_t n_users, const orx_records* history, const double* content,
+                          int32_t content_dim, int32_t threshold, int32_t max_out, int32_t n_code_layers,
+                          const uint64_t* rng_seeds, orx_records_out* out) {
+  return guarded([&] {
+    need(history, "history");
+    need(out, "out");
+    if (n_users < 0) throw orx::InvalidArgument("negative user count");
+    need(history->offsets, "history->offsets");
+    need(out->offsets, "out->offsets");
+    if (history->offsets[0] != 0) throw orx::InvalidArgument("offsets must start at 0");
+    const int64_t n = history->offsets[n_users];
+    if (n > 0) {
+      need(content, "content");
+      need(rng_seeds, "rng_seeds");
+      need(history->vid, "history->vid");
+      need(history->aid, "history->aid");
+      need(history->tag, "history->tag");
+      need(history->ts, "history->ts");
+      need(history->playtime, "history->playtime");
+      need(history->duration, "history->duration");
+      need(history->labels, "history->labels");
+    }
+    orx::CompressHost h{};
+    h.n_users = n_users, h.D = content_dim, h.threshold = threshold, h.max_out = max_out;
+    h.n_code_layers = n_code_layers;
+    h.offsets = history->offsets, h.vid = history->vid, h.aid = history->aid, h.labels = history->labels;
+    h.tag = history->tag, h.ts = history->ts, h.playtime = history->playtime, h.duration = history->duration;
+    h.sid = history->sid, h.content = content, h.rng_seeds = rng_seeds;
+    h.out_offsets = out->offsets, h.out_vid = out->vid, h.out_aid = out->aid, h.out_labels = out->labels;
+    h.out_tag = out->tag, h.out_ts = out->ts, h.out_playtime = out->playtime, h.out_duration = out->duration;
+    h.out_sid = out->sid;
+    orx::compress_lifelong_gpu(h, device);
   });
 }
 

@@ -540,3 +540,46 @@ def policy_scorer(model: PolicyModel, z_enc: np.ndarray):
     """StepScorer closure (generation.cpp:163-167): prefix -> logits (1, V)."""
     z = np.ascontiguousarray(z_enc, dtype=np.float32)
     return lambda prefix: model.next_logits_eval(z, prefix)
+
+
+def compress_lifelong_batch(offsets, vid, aid, tag, ts, playtime, duration, labels, content, rng_seeds,
+                            threshold: int = 8, max_out: int = 2000, sid=None, n_code_layers: int = 3,
+                            device: int = 0):
+    """compress_lifelong (policy.cpp:447-510) for a batch of raw histories on
+    the GPU (hierarchical K-means, bit-identical to the reference's f64 code).
+    Inputs are flat per-record arrays with user offsets; content is
+    [n_records, D] f64; rng_seeds[u] seeds user u's Rng. Returns a dict of
+    the compressed flat arrays (last min(n_u, max_out) records per user)."""
+    from ._lib import orx_records, orx_records_out
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    U = len(off) - 1
+    cnt = np.diff(off)
+    n_out = int(np.minimum(cnt, max_out).sum())
+    arr = {"vid": np.ascontiguousarray(vid, dtype=np.int64), "aid": np.ascontiguousarray(aid, dtype=np.int32),
+           "tag": np.ascontiguousarray(tag, dtype=np.float64), "ts": np.ascontiguousarray(ts, dtype=np.float64),
+           "playtime": np.ascontiguousarray(playtime, dtype=np.float64),
+           "duration": np.ascontiguousarray(duration, dtype=np.float64),
+           "labels": np.ascontiguousarray(labels, dtype=np.uint32)}
+    cont = np.ascontiguousarray(content, dtype=np.float64)
+    seeds = np.ascontiguousarray(rng_seeds, dtype=np.uint64)
+    sid_a = np.ascontiguousarray(sid, dtype=np.int32) if sid is not None else None
+    P = C.POINTER
+    rec = orx_records(off.ctypes.data_as(P(C.c_int64)), arr["vid"].ctypes.data_as(P(C.c_int64)),
+                      arr["aid"].ctypes.data_as(P(C.c_int32)), arr["tag"].ctypes.data_as(P(C.c_double)),
+                      arr["ts"].ctypes.data_as(P(C.c_double)), arr["playtime"].ctypes.data_as(P(C.c_double)),
+                      arr["duration"].ctypes.data_as(P(C.c_double)), arr["labels"].ctypes.data_as(P(C.c_uint32)),
+                      sid_a.ctypes.data_as(P(C.c_int32)) if sid_a is not None else None)
+    out = {"offsets": np.empty(U + 1, dtype=np.int64), "vid": np.empty(n_out, dtype=np.int64),
+           "aid": np.empty(n_out, dtype=np.int32), "tag": np.empty(n_out), "ts": np.empty(n_out),
+           "playtime": np.empty(n_out), "duration": np.empty(n_out), "labels": np.empty(n_out, dtype=np.uint32)}
+    if sid_a is not None:
+        out["sid"] = np.empty(n_out * n_code_layers, dtype=np.int32)
+    ro = orx_records_out(out["offsets"].ctypes.data_as(P(C.c_int64)), out["vid"].ctypes.data_as(P(C.c_int64)),
+                         out["aid"].ctypes.data_as(P(C.c_int32)), out["tag"].ctypes.data_as(P(C.c_double)),
+                         out["ts"].ctypes.data_as(P(C.c_double)), out["playtime"].ctypes.data_as(P(C.c_double)),
+                         out["duration"].ctypes.data_as(P(C.c_double)), out["labels"].ctypes.data_as(P(C.c_uint32)),
+                         out["sid"].ctypes.data_as(P(C.c_int32)) if sid_a is not None else None)
+    check(lib().orx_compress_lifelong(device, U, C.byref(rec), cont.ctypes.data_as(P(C.c_double)),
+                                      cont.shape[1] if cont.ndim == 2 else 1, threshold, max_out, n_code_layers,
+                                      seeds.ctypes.data_as(P(C.c_uint64)), C.byref(ro)))
+    return out

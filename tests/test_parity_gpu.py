@@ -265,3 +265,31 @@ def test_topk_topp_sampling_fp32(preset, sample):
                 assert abs(it.log_prob - ref["sample_logp"][s]) <= 1e-4 * max(1.0, abs(ref["sample_logp"][s]))
     print(f"sampling {preset} {sample}: {same}/{total} sequences identical to the reference")
     assert same >= 0.9 * total
+
+
+@pytest.mark.parametrize("users,hist_len,dim,threshold,max_out", [(3, 300, 32, 8, 320), (4, 2300, 256, 8, 2000),
+                                                                   (2, 5, 16, 8, 4)])
+def test_compress_lifelong_gpu(users, hist_len, dim, threshold, max_out):
+    """compress_lifelong (policy.cpp:447-510) with hierarchical K-means
+    (kmeans.cpp:22-183) on the GPU is bit-identical to the reference on seeded
+    raw histories (clustered content rows, build_user_context's Rng seeds)."""
+    import os
+    import subprocess
+    import tempfile
+
+    import paper_2506_13695_b200 as P
+    from parity_util import REF_DRIVER
+    d = tempfile.mkdtemp(prefix="orx_cmp_")
+    subprocess.run([REF_DRIVER, "compress", "--n-users", str(users), "--hist-len", str(hist_len), "--content-dim",
+                    str(dim), "--threshold", str(threshold), "--max-out", str(max_out), "--out", d],
+                   check=True, capture_output=True, timeout=1200)
+    ld = lambda n: np.load(os.path.join(d, n + ".npy"))  # noqa: E731
+    got = P.compress_lifelong_batch(ld("in_offsets"), ld("in_vid"), ld("in_aid"), ld("in_tag"), ld("in_ts"),
+                                    ld("in_playtime"), ld("in_duration"), ld("in_labels"), ld("in_content"),
+                                    ld("seeds"), threshold=threshold, max_out=max_out)
+    assert np.array_equal(got["offsets"], ld("out_offsets"))
+    for f in ("vid", "aid", "labels", "tag", "ts", "playtime", "duration"):
+        want = ld("out_" + f)
+        assert np.array_equal(got[f].astype(want.dtype), want), f
+    n_rep = len(set(got["vid"].tolist()))
+    print(f"compress {users} users x ~{hist_len} records (D={dim}): {len(got['vid'])} records, {n_rep} representatives")

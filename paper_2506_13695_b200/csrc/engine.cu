@@ -166,6 +166,7 @@ class EngineT final : public Engine {
   ~EngineT() override {
     cudaSetDevice(dev_);
     cudaStreamSynchronize(st_);
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (comm_) nccl().CommDestroy(comm_);
     if (h_ep_) cudaFreeHost(h_ep_);
     if (host_stage_) cudaFreeHost(host_stage_);
@@ -1102,11 +1103,22 @@ class EngineT final : public Engine {
     has_trie_ = n_edges > 0;
   }
 
-  void run_beam(int width, orx_beam_out* out, bool constrained) {
-    CUDA_CHECK(cudaSetDevice(dev_));
+  struct GraphKey {
+    int U, W;
+    bool constrained;
+    int n_rec[3];
+    int n_keys, n_pad;
+    const void* stage;
+    bool operator==(const GraphKey& o) const {
+      return U == o.U && W == o.W && constrained == o.constrained && n_rec[0] == o.n_rec[0] &&
+             n_rec[1] == o.n_rec[1] && n_rec[2] == o.n_rec[2] && n_keys == o.n_keys && n_pad == o.n_pad &&
+             stage == o.stage;
+    }
+  };
+
+  // encode + decode + prune for the staged batch (only stream work: capturable)
+  void beam_body(int width, bool constrained) {
     const orx_config& c = cfg_;
-    require(width >= 1, "generation width must be >= 1");  // validate_request, generation.cpp:35
-    require(width <= maxW_, "beam width above the engine capacity");
     const int U = sg_.U, V = c.codebook_size, L = c.n_code_layers, Tn = enc_seq_len(c);
     run_encode();
     prepare_decoder(U);
@@ -1135,6 +1147,46 @@ class EngineT final : public Engine {
                         constrained ? &trie_ : nullptr);
       cur ^= 1;
       n_live = n_new;
+    }
+  }
+
+  void run_beam(int width, orx_beam_out* out, bool constrained) {
+    CUDA_CHECK(cudaSetDevice(dev_));
+    const orx_config& c = cfg_;
+    require(width >= 1, "generation width must be >= 1");  // validate_request, generation.cpp:35
+    require(width <= maxW_, "beam width above the engine capacity");
+    const int U = sg_.U, V = c.codebook_size, L = c.n_code_layers;
+    // The whole encode + decode + prune sequence is replayed from a CUDA graph
+    // when the request has the same shapes as the captured one (no host work
+    // or launch gaps between its ~260 kernels); expert-parallel engines (host
+    // sync per MoE layer) and profiling runs launch directly.
+    const bool graphs = ep_world_ == 1 && !prof_enabled() && !getenv("ORX_NO_GRAPH");
+    int n_live = 1;
+    for (int step = 0; step < L; ++step) n_live = static_cast<int>(std::min<int64_t>(width, (int64_t)n_live * V));
+    int cur = L % 2;
+    if (graphs) {
+      const GraphKey key{U, width, constrained, {sg_.n_rec[0], sg_.n_rec[1], sg_.n_rec[2]}, sg_.n_keys,
+                         sg_.n_pad_keys, dev_stage_};
+      if (!graph_exec_ || !(key == graph_key_)) {
+        if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+        cudaGraph_t g = nullptr;
+        CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+        try {
+          beam_body(width, constrained);
+        } catch (...) {
+          cudaStreamEndCapture(st_, &g);
+          if (g) cudaGraphDestroy(g);
+          throw;
+        }
+        CUDA_CHECK(cudaStreamEndCapture(st_, &g));
+        CUDA_CHECK(cudaGraphInstantiate(&graph_exec_, g, 0));
+        cudaGraphDestroy(g);
+        graph_key_ = key;
+      }
+      CUDA_CHECK(cudaGraphLaunch(graph_exec_, st_));
+    } else {
+      beam_body(width, constrained);
     }
     last_n_live_ = n_live;
     last_state_ = cur;
@@ -1407,6 +1459,8 @@ class EngineT final : public Engine {
   bool has_trie_ = false;
   double* seq_acc_ = nullptr;
   double* uni_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  GraphKey graph_key_{};
   int32_t *tf_anc_, *tf_codes_, *grp_start_, *grp_len_, *grp_kstart_;
   int32_t *sel_ = nullptr, *slot_ = nullptr, *counts_ = nullptr, *cursor_ = nullptr, *tile_expert_ = nullptr,
           *n_mtiles_ = nullptr;

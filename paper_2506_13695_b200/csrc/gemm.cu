@@ -759,6 +759,7 @@ ProfScope::~ProfScope() {
   if (idx >= 0) cudaEventRecord(prof().recs[static_cast<size_t>(idx)].b, s);
 }
 void prof_enable(bool on) { prof().on = on; }
+bool prof_enabled() { return prof().on; }
 void prof_collect(long long* count, double* ms, double* flops, double* bytes) {
   Prof& p = prof();
   for (int c = 0; c < PROF_N; ++c) count[c] = 0, ms[c] = flops[c] = bytes[c] = 0;

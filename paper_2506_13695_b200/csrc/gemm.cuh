@@ -80,6 +80,7 @@ struct ProfScope {
   cudaStream_t s;
 };
 void prof_enable(bool on);
+bool prof_enabled();
 // Per category: launches, total ms, algorithmic flops, algorithmic bytes.
 void prof_collect(long long* count, double* ms, double* flops, double* bytes);
 

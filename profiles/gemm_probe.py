@@ -20,6 +20,8 @@ SHAPES = {  # name: (M, N, K, act, bias, out_bf16, resid)
     "life_fc1_leaky": (256000, 1024, 2176, 1, True, True, False),
     "dec_head": (16384, 8192, 1024, 0, False, False, False),
     "dec_so_resid": (16384, 1024, 1024, 0, False, False, True),
+    "dec_cq": (16384, 1024, 1024, 0, False, True, False),
+    "dec_sqkv": (16384, 3072, 1024, 0, False, True, False),
 }
 
 

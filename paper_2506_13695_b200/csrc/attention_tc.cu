@@ -64,7 +64,8 @@ struct Fmha {
   static constexpr uint32_t Q_BYTES = BQ * DH * 2;    // CB blocks of [128 rows x 128 B]
   static constexpr uint32_t K_BYTES = BK * DH * 2;    // CB blocks of [64 rows x 128 B]
   static constexpr uint32_t V_BYTES = DH * BK * 2;    // [DH rows (head dims) x 64 keys]
-  static constexpr uint32_t SMEM = Q_BYTES + 2 * K_BYTES + 2 * V_BYTES + 128;  // + barriers
+  static constexpr int KST = 3, VST = 2;              // K ring deeper than V: S_j needs K_j first
+  static constexpr uint32_t SMEM = Q_BYTES + KST * K_BYTES + VST * V_BYTES + 256;  // + barriers
   static constexpr uint32_t TMEM_COLS = 2 * BK + DH <= 256 ? 256 : 512;  // S[2] + O
 };
 
@@ -77,16 +78,18 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
   using F = Fmha<DH>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem;
-  uint8_t* sK = sQ + F::Q_BYTES;          // [2][K_BYTES]
-  uint8_t* sV = sK + 2 * F::K_BYTES;      // [2][V_BYTES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * F::V_BYTES);
+  uint8_t* sK = sQ + F::Q_BYTES;            // [KST][K_BYTES]
+  uint8_t* sV = sK + F::KST * F::K_BYTES;   // [VST][V_BYTES]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + F::VST * F::V_BYTES);
   uint64_t& q_full = bars[0];
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t& p_full = bars[9];
-  uint64_t& o_done = bars[10];
-  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* k_full = bars + 1;    // [KST]
+  uint64_t* k_empty = bars + 4;   // [KST]
+  uint64_t* v_full = bars + 7;    // [VST]
+  uint64_t* v_empty = bars + 9;   // [VST]
+  uint64_t* s_full = bars + 11;   // [2]
+  uint64_t& p_full = bars[13];
+  uint64_t& o_done = bars[14];
+  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 15);
 
   const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * F::BQ;
   const int qlen = seg_len(qs, b);
@@ -99,11 +102,15 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
   if (threadIdx.x == 0) {
     if ((smem_u32(smem) & 1023) != 0) __trap();  // SW128 operands need 1 KB alignment
     mbar_init(&q_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-      mbar_init(&s_full[s], 1);
+    for (int s = 0; s < F::KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
     }
+    for (int s = 0; s < F::VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) mbar_init(&s_full[s], 1);
     mbar_init(&p_full, 4);
     mbar_init(&o_done, 1);
     fence_mbar_init();
@@ -125,14 +132,23 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
       mbar_arrive_expect_tx(&q_full, F::Q_BYTES);
       for (int cb = 0; cb < F::CB; ++cb)
         tma_load_2d(sQ + cb * (F::BQ * 128), &tmQ, &q_full, q_col0 + h * DH + cb * 64, qst + q0, pol);
-      for (int j = 0; j < nb; ++j) {
-        const int st = j & 1;
-        if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&kv_full[st], F::K_BYTES + F::V_BYTES);
-        for (int cb = 0; cb < F::CB; ++cb)
-          tma_load_2d(sK + st * F::K_BYTES + cb * (F::BK * 128), &tmK, &kv_full[st], k_col0 + h * DH + cb * 64,
-                      kst + j * F::BK, pol);
-        tma_load_2d(sV + st * F::V_BYTES, &tmV, &kv_full[st], j * F::BK, vrow0, pol);
+      // K runs one block ahead of V (V_j is consumed a softmax later than K_j)
+      for (int i = 0; i <= nb; ++i) {
+        if (i < nb) {
+          const int ks = i % F::KST;
+          if (i >= F::KST) mbar_wait(&k_empty[ks], ((i / F::KST) - 1) & 1);
+          mbar_arrive_expect_tx(&k_full[ks], F::K_BYTES);
+          for (int cb = 0; cb < F::CB; ++cb)
+            tma_load_2d(sK + ks * F::K_BYTES + cb * (F::BK * 128), &tmK, &k_full[ks], k_col0 + h * DH + cb * 64,
+                        kst + i * F::BK, pol);
+        }
+        const int j = i - 1;
+        if (j >= 0) {
+          const int vs = j % F::VST;
+          if (j >= F::VST) mbar_wait(&v_empty[vs], ((j / F::VST) - 1) & 1);
+          mbar_arrive_expect_tx(&v_full[vs], F::V_BYTES);
+          tma_load_2d(sV + vs * F::V_BYTES, &tmV, &v_full[vs], j * F::BK, vrow0, pol);
+        }
       }
     }
   } else if (warp == 1) {
@@ -140,23 +156,24 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
       constexpr uint32_t idesc_s = umma_idesc_bf16(F::BQ, F::BK);
       constexpr uint32_t idesc_o = umma_idesc_bf16(F::BQ, DH);
       auto issue_pv = [&](int j) {
-        const int st = j & 1;
+        const int st = j & 1, vs = j % F::VST;
+        mbar_wait(&v_full[vs], (j / F::VST) & 1);
         mbar_wait(&p_full, j & 1);
         tc_fence_after();
-        const uint32_t b0 = smem_u32(sV + st * F::V_BYTES);
+        const uint32_t b0 = smem_u32(sV + vs * F::V_BYTES);
         // A = P_j: 128 lanes x 64 keys bf16 = 32 TMEM columns at the start of S buffer st, 8 per K=16 step
 #pragma unroll
         for (int k = 0; k < F::BK / 16; ++k)
           tc_mma_bf16_ts(t_o, t_s + st * F::BK + k * 8, umma_desc_sw128(b0 + k * 32), idesc_o, (j | k) != 0);
         tc_commit(&o_done);
-        tc_commit(&kv_empty[st]);
+        tc_commit(&v_empty[vs]);
       };
       mbar_wait(&q_full, 0);
       for (int j = 0; j < nb; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        const int st = j & 1, ks = j % F::KST;
+        mbar_wait(&k_full[ks], (j / F::KST) & 1);
         tc_fence_after();
-        const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + st * F::K_BYTES);
+        const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + ks * F::K_BYTES);
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {
           const int cb = k >> 2, off = (k & 3) * 32;
@@ -164,6 +181,7 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
                       umma_desc_sw128(kb + cb * (F::BK * 128) + off), idesc_s, k != 0);
         }
         tc_commit(&s_full[st]);
+        tc_commit(&k_empty[ks]);
         if (j >= 1) issue_pv(j - 1);
       }
       issue_pv(nb - 1);

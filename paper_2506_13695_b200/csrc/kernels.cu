@@ -881,7 +881,7 @@ void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32
   if (rows <= 0) return;
   long long warps = (long long)rows * k;
   if constexpr (sizeof(T) == 2) {
-    if (d % 8 == 0 && ldx % 8 == 0) {
+    if (d % 8 == 0 && ldx % 8 == 0 && warps >= 8192) {  // many pairs: aggregate the slot atomics per warp
       const long long w32 = (warps + 31) / 32;
       ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_scatter32_kernel<<<static_cast<int>((w32 + 7) / 8), 256, 0, s>>>(
                                          rows, k, d, reinterpret_cast<const __nv_bfloat16*>(x), ldx, sel, wts, cursor,

@@ -28,7 +28,7 @@ import os
 import statistics
 import subprocess
 import sys
-import tempfile
+import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -78,50 +78,56 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock, power and throttle reasons sampled every ~10 ms through NVML
+    (the fields of the profiling recipe's nvidia-smi clocks line) on a side
+    thread while the timed region runs; start() returns once the first sample
+    is in, so a short timed region is still covered."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.rows, self.stop_flag, self.t = [], threading.Event(), None
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[gpu_index]) if vis and vis.split(",")[gpu_index].isdigit() else gpu_index
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_sm = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
         except Exception:
-            self.p = None
+            self.nv = None
+            return
+        first = threading.Event()
+
+        def run():
+            nv = self.nv
+            while not self.stop_flag.is_set():
+                try:
+                    self.rows.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)),
+                                      nv.nvmlDeviceGetPowerUsage(self.h) / 1e3,
+                                      int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+                except Exception:
+                    pass
+                first.set()
+                self.stop_flag.wait(0.01)
+
+        self.t = threading.Thread(target=run, daemon=True)
+        self.t.start()
+        first.wait(5)
+        self.rows.clear()  # keep only samples taken inside the timed region
 
     def stop(self):
-        if self.p is None:
+        if self.t is None:
             return None
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.flush()
-        rows = []
-        with open(self.f.name) as fh:
-            for line in fh:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) < 9 or not parts[0].isdigit() or int(parts[0]) != self.gpu:
-                    continue
-                rows.append(parts)
-        os.unlink(self.f.name)
+        self.stop_flag.set()
+        self.t.join(5)
+        rows = list(self.rows)
         if not rows:
             return None
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for n, v in zip(names, r[5:9]):
-                if v.strip().lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
-                "reasons": sorted(reasons), "samples": len(rows),
-                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+        reasons = sorted(n for n, bit in self.REASONS.items() if any(r[2] & bit for r in rows))
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": self.max_sm, "reasons": reasons,
+                "samples": len(rows), "power_w_max": round(max(r[1] for r in rows), 1), "source": "nvml 10 ms"}
 
 
 def safe_procs(cfg_preset: str) -> int:
@@ -254,9 +260,8 @@ def main():
     for _ in range(args.warmup):
         check(lib().orx_beam_search_staged(e, args.width, None))
     st0 = model.stats()
-    sampler = ClockSampler(local)
-    time.sleep(0.3)
     barrier()
+    sampler = ClockSampler(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):

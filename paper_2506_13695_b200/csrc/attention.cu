@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(128) attn_f32_kernel(int heads, const float* _
                                                         const float* __restrict__ K, int ldk,
                                                         const float* __restrict__ V, int ldv, float* __restrict__ O,
                                                         int ldo, Seg qs, Seg ks, Seg os) {
+  pdl_begin();
   constexpr int BQ = 32, BKV = 32, PER = (DH + 31) / 32;
   extern __shared__ float smf[];
   float (*sQ)[DH] = reinterpret_cast<float (*)[DH]>(smf);
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(128) attn_bf16_kernel(int heads, const __nv_bf
                                                          const __nv_bfloat16* __restrict__ V, int ldv,
                                                          __nv_bfloat16* __restrict__ O, int ldo, Seg qs, Seg ks,
                                                          Seg os) {
+  pdl_begin();
   using S = AttnSmem<DH>;
   constexpr int BQ = S::BQ, BKV = S::BKV, LD = S::LD;
   constexpr int CH = DH / 8;  // 16-byte chunks per row
@@ -300,7 +302,7 @@ void launch_f32(int B, int max_q, int heads, const float* Q, int ldq, const floa
     set = true;
   }
   dim3 grid((max_q + 31) / 32, heads, B);
-  attn_f32_kernel<DH><<<grid, 128, smem, s>>>(heads, Q, ldq, K, ldk, V, ldv, O, ldo, q, k, o);
+  launch_pdl(attn_f32_kernel<DH>, grid, 128, smem, s, heads, Q, ldq, K, ldk, V, ldv, O, ldo, q, k, o);
 }
 
 template <int DH>
@@ -313,7 +315,7 @@ void launch_b16(int B, int max_q, int heads, const __nv_bfloat16* Q, int ldq, co
     set = true;
   }
   dim3 grid((max_q + 63) / 64, heads, B);
-  attn_bf16_kernel<DH><<<grid, 128, smem, s>>>(heads, Q, ldq, K, ldk, V, ldv, O, ldo, q, k, o);
+  launch_pdl(attn_bf16_kernel<DH>, grid, 128, smem, s, heads, Q, ldq, K, ldk, V, ldv, O, ldo, q, k, o);
 }
 
 }  // namespace

@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
                                                        const __grid_constant__ CUtensorMap tmV, int heads,
                                                        __nv_bfloat16* __restrict__ O, int ldo, Seg qs, Seg ks, Seg os,
                                                        const int32_t* __restrict__ vt_user, int q_col0, int k_col0) {
+  pdl_begin();
   using F = Fmha<DH>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem;
@@ -325,7 +326,7 @@ void launch_fmha(const FmhaArgs& a, cudaStream_t s) {
   CUtensorMap mk = map2d(a.K, a.k_rows, a.k_col0 + a.heads * DH, a.ldk, 64, F::BK);
   CUtensorMap mv = map2d(a.Vt, a.vt_rows, a.vt_cols, a.vt_ld, 64, DH);
   dim3 grid((a.max_q + F::BQ - 1) / F::BQ, a.heads, a.B);
-  fmha_tc_kernel<DH><<<grid, 192, F::SMEM, s>>>(mq, mk, mv, a.heads, static_cast<__nv_bfloat16*>(a.O), a.ldo, a.q, a.k, a.o, a.vt_user, a.q_col0,
+  launch_pdl(fmha_tc_kernel<DH>, grid, 192, F::SMEM, s, mq, mk, mv, a.heads, static_cast<__nv_bfloat16*>(a.O), a.ldo, a.q, a.k, a.o, a.vt_user, a.q_col0,
                                                 a.k_col0);
 }
 

@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(kRowThreads) row_topk_kernel(int V, int k_sel,
                                                                float* __restrict__ lse_out,
                                                                uint64_t* __restrict__ cand,
                                                                const int32_t* __restrict__ row_list) {
+  pdl_begin();
   extern __shared__ uint64_t keys[];  // [V]
   __shared__ uint32_t hist[256];
   __shared__ uint32_t bc[4];
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows,
                                                                        float* __restrict__ lse_out,
                                                                        uint64_t* __restrict__ cand,
                                                                        int32_t* __restrict__ fail) {
+  pdl_begin();
   __shared__ float bx[kWarpRows][kLaneSlots * 32];
   __shared__ int32_t bi[kWarpRows][kLaneSlots * 32];
   __shared__ int32_t bn[kWarpRows][32];
@@ -360,6 +362,7 @@ __global__ void __launch_bounds__(kMergeThreads) beam_merge_kernel(int n_live, i
                                                                    const float* __restrict__ logits,
                                                                    const float* __restrict__ lse, BeamState cur,
                                                                    BeamState nxt, TrieDev trie, int use_trie) {
+  pdl_begin();
   __shared__ uint64_t sel[kMaxBeam];
   __shared__ uint64_t lex[kMaxBeam];
   __shared__ uint32_t hist[256];
@@ -448,6 +451,7 @@ __global__ void __launch_bounds__(kMergeThreads) beam_merge_kernel(int n_live, i
 }
 
 __global__ void beam_init_kernel(int users, BeamState st) {
+  pdl_begin();
   int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= users) return;
   st.score[u] = 0.f;
@@ -465,6 +469,7 @@ __global__ void __launch_bounds__(kRowThreads) row_topk_trie_kernel(int V, int k
                                                                     const int32_t* __restrict__ node, TrieDev trie,
                                                                     float* __restrict__ lse_out,
                                                                     uint64_t* __restrict__ cand) {
+  pdl_begin();
   __shared__ uint32_t hist[256];
   __shared__ uint32_t bc[4];
   __shared__ float red[kRowThreads / 32];
@@ -526,6 +531,7 @@ __global__ void __launch_bounds__(kRowThreads) row_topk_trie_kernel(int V, int k
 // Warp per row: acc[r] += logits[r][code] - lse(logits[r]) in f64.
 __global__ void pick_logprob_kernel(int rows, int V, const float* __restrict__ logits, const int32_t* __restrict__ codes,
                                     int code_stride, int step, double* __restrict__ acc) {
+  pdl_begin();
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (r >= rows) return;
   const float* lg = logits + (size_t)r * V;
@@ -554,6 +560,7 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(int V, int vpad,
                                                                 const double* __restrict__ uniforms,
                                                                 int32_t* __restrict__ codes,
                                                                 double* __restrict__ logp) {
+  pdl_begin();
   extern __shared__ uint64_t skeys[];  // [vpad]
   __shared__ double dscan[kSampleThreads];
   __shared__ float red[kSampleThreads / 32];
@@ -675,18 +682,18 @@ void launch_row_topk(int rows, int V, int k_sel, const float* logits, const floa
   if (fail && V % 4 == 0 && k_sel < V && k_sel <= 1024) {
     cudaMemsetAsync(fail, 0, sizeof(int32_t), s);
     if (k_sel <= 192)
-      row_topk_warp_kernel<32><<<(rows + 3) / 4, 128, 0, s>>>(rows, V, k_sel, logits, parent_score, parent_lexrank,
+      launch_pdl(row_topk_warp_kernel<32>, (rows + 3) / 4, 128, 0, s, rows, V, k_sel, logits, parent_score, parent_lexrank,
                                                               lse, cand, fail);
     else
-      row_topk_warp_kernel<64><<<(rows + 1) / 2, 64, 0, s>>>(rows, V, k_sel, logits, parent_score, parent_lexrank,
+      launch_pdl(row_topk_warp_kernel<64>, (rows + 1) / 2, 64, 0, s, rows, V, k_sel, logits, parent_score, parent_lexrank,
                                                              lse, cand, fail);
     // rows the warp kernel could not decide (usually none): exact radix select
-    row_topk_kernel<<<std::min(rows, 32), kRowThreads, smem, s>>>(V, k_sel, logits, parent_score,
+    launch_pdl(row_topk_kernel, std::min(rows, 32), kRowThreads, smem, s, V, k_sel, logits, parent_score,
                                                                             parent_lexrank, lse, cand, fail);
     launch_counter() += 2;
     return;
   }
-  row_topk_kernel<<<rows, kRowThreads, smem, s>>>(V, k_sel, logits, parent_score, parent_lexrank, lse, cand, nullptr);
+  launch_pdl(row_topk_kernel, rows, kRowThreads, smem, s, V, k_sel, logits, parent_score, parent_lexrank, lse, cand, nullptr);
   ++launch_counter();
 }
 
@@ -695,7 +702,7 @@ void launch_row_topk_trie(int rows, int V, int k_sel, const float* logits, const
                           uint64_t* cand, cudaStream_t s) {
   if (rows <= 0) return;
   ProfScope ps(PROF_BEAM, s, 0.0, double(rows) * V * 4);
-  row_topk_trie_kernel<<<rows, kRowThreads, 0, s>>>(V, k_sel, logits, parent_score, parent_lexrank, node, trie, lse,
+  launch_pdl(row_topk_trie_kernel, rows, kRowThreads, 0, s, V, k_sel, logits, parent_score, parent_lexrank, node, trie, lse,
                                                     cand);
   ++launch_counter();
 }
@@ -704,7 +711,7 @@ void launch_pick_logprob(int rows, int V, const float* logits, const int32_t* co
                          double* acc, cudaStream_t s) {
   if (rows <= 0) return;
   ProfScope ps(PROF_BEAM, s, 0.0, double(rows) * V * 4);
-  pick_logprob_kernel<<<(rows + 7) / 8, 256, 0, s>>>(rows, V, logits, codes, code_stride, step, acc);
+  launch_pdl(pick_logprob_kernel, (rows + 7) / 8, 256, 0, s, rows, V, logits, codes, code_stride, step, acc);
   ++launch_counter();
 }
 
@@ -721,7 +728,7 @@ void launch_sample(int rows, int V, int L, int step, float temperature, int top_
     set = smem;
   }
   ProfScope ps(PROF_BEAM, s, 0.0, double(rows) * V * 4);
-  sample_kernel<<<rows, kSampleThreads, smem, s>>>(V, vpad, L, step, 1.f / temperature, top_k, top_p, logits,
+  launch_pdl(sample_kernel, rows, kSampleThreads, smem, s, V, vpad, L, step, 1.f / temperature, top_k, top_p, logits,
                                                    uniforms, codes, logp);
   ++launch_counter();
 }
@@ -741,13 +748,13 @@ void launch_beam_merge(int users, int n_live, int k_sel, int n_new, int V, int L
                        const TrieDev* trie) {
   if (n_new > kMaxBeam) throw std::invalid_argument("beam width above 1024 is not supported");
   ProfScope ps(PROF_BEAM, s, 0.0, 0.0);
-  beam_merge_kernel<<<users, kMergeThreads, 0, s>>>(n_live, k_sel, n_new, V, L, step, cand, logits, lse, cur, nxt,
+  launch_pdl(beam_merge_kernel, users, kMergeThreads, 0, s, n_live, k_sel, n_new, V, L, step, cand, logits, lse, cur, nxt,
                                                     trie ? *trie : TrieDev{}, trie ? 1 : 0);
   ++launch_counter();
 }
 
 void launch_beam_init(int users, BeamState& st, cudaStream_t s) {
-  beam_init_kernel<<<(users + 127) / 128, 128, 0, s>>>(users, st);
+  launch_pdl(beam_init_kernel, (users + 127) / 128, 128, 0, s, users, st);
   ++launch_counter();
 }
 

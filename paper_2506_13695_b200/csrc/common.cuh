@@ -9,9 +9,47 @@
 
 #include "gemm.cuh"
 
+#include <cstdlib>
+#include <utility>
+
 #define ORX_DEV __device__ __forceinline__
 
 namespace orx {
+
+// Programmatic dependent launch. Every kernel launched through launch_pdl()
+// opens with pdl_begin(): it blocks until the previous kernel in the stream
+// has completed and flushed (griddepcontrol.wait), then lets the next kernel
+// start its launch (griddepcontrol.launch_dependents). The next grid's CTAs
+// therefore get scheduled onto SMs the current grid's last wave leaves idle
+// and skip the launch gap; nothing reads a predecessor's output early.
+ORX_DEV void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static const bool on = std::getenv("ORX_NO_PDL") == nullptr;
+  return on;
+}
+
+// kernel<<<grid, block, smem, stream>>>(args...) with the programmatic
+// stream-serialisation attribute (kept inside captured CUDA graphs as
+// programmatic edges).
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 ORX_DEV float act_apply(float v, int act) {
   if (act == ACT_LEAKY) return v > 0.f ? v : 0.01f * v;  // tape.hpp:88 slope 0.01

@@ -1180,11 +1180,25 @@ class EngineT final : public Engine {
           throw;
         }
         CUDA_CHECK(cudaStreamEndCapture(st_, &g));
+        // the replay launches these kernel nodes every call: count them like
+        // direct launches (memset nodes are not kernels)
+        size_t n_nodes = 0;
+        CUDA_CHECK(cudaGraphGetNodes(g, nullptr, &n_nodes));
+        std::vector<cudaGraphNode_t> nodes(n_nodes);
+        if (n_nodes) CUDA_CHECK(cudaGraphGetNodes(g, nodes.data(), &n_nodes));
+        graph_kernels_ = 0;
+        for (cudaGraphNode_t nd : nodes) {
+          cudaGraphNodeType t;
+          CUDA_CHECK(cudaGraphNodeGetType(nd, &t));
+          if (t == cudaGraphNodeTypeKernel) ++graph_kernels_;
+        }
         CUDA_CHECK(cudaGraphInstantiate(&graph_exec_, g, 0));
         cudaGraphDestroy(g);
         graph_key_ = key;
+        launch_counter() -= graph_kernels_;  // capture itself launched nothing
       }
       CUDA_CHECK(cudaGraphLaunch(graph_exec_, st_));
+      launch_counter() += graph_kernels_;
     } else {
       beam_body(width, constrained);
     }
@@ -1460,6 +1474,7 @@ class EngineT final : public Engine {
   double* seq_acc_ = nullptr;
   double* uni_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
+  long long graph_kernels_ = 0;
   GraphKey graph_key_{};
   int32_t *tf_anc_, *tf_codes_, *grp_start_, *grp_len_, *grp_kstart_;
   int32_t *sel_ = nullptr, *slot_ = nullptr, *counts_ = nullptr, *cursor_ = nullptr, *tile_expert_ = nullptr,

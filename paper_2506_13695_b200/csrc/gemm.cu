@@ -238,6 +238,95 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tb, int row
   }
 }
 
+// Staged epilogue for full, aligned tiles (CTA-pair kernel). TMEM hands each
+// thread one ROW of 32 columns; storing that directly makes every warp access
+// touch 32 rows (32 L1 wavefronts per instruction, 2-3 TB/s on the fp32
+// residual GEMMs). Instead each warp transposes its 32x32 chunk through a
+// 4 KB XOR-swizzled SMEM tile and then reads / writes global memory row-wise:
+// 8 lanes cover one row's 128 B, one instruction covers 4 rows. The residual
+// chunk is loaded in that coalesced layout while tcgen05.ld runs.
+template <int BN, int MODE>
+__device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, uint32_t tb, int row, int nt,
+                                                     int half, uint64_t* tfull, uint32_t acc_phase) {
+  constexpr int CH = BN / 32 / 2;
+  const int lane = threadIdx.x & 31, sub = lane >> 3, q = lane & 7;
+  int orow = -1;
+  float rs = 1.f;
+  if (row < e.m_valid) {
+    orow = e.row_map ? e.row_map[row] : row;
+    if (MODE & EPI_RS) rs = e.row_scale[row];
+  }
+  int orr[8];  // output rows this lane stores: r = 4 * k + sub
+#pragma unroll
+  for (int k = 0; k < 8; ++k) orr[k] = __shfl_sync(0xffffffffu, orow, 4 * k + sub);
+  if (MODE & EPI_RESID) {
+    if (orow >= 0)  // this row's residual segment into L2 while the MMAs run
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(e.resid + (size_t)orow * e.ld_resid +
+                                                                       nt * BN + half * CH * 32),
+                   "r"(CH * 128)
+                   : "memory");
+  }
+  float4* s4 = reinterpret_cast<float4*>(stg);
+  mbar_wait(tfull, acc_phase);
+  tc_fence_after();
+#pragma unroll 1
+  for (int i = 0; i < CH; ++i) {
+    const int col0 = nt * BN + (half * CH + i) * 32;
+    uint32_t ra[32];
+    tmem_ld32_async(tb + (half * CH + i) * 32, ra);
+    float4 rr[8];
+    if (MODE & EPI_RESID) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        rr[k] = orr[k] >= 0 ? __ldg(reinterpret_cast<const float4*>(e.resid + (size_t)orr[k] * e.ld_resid + col0) + q)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    tmem_wait_ld();
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(ra[j]);
+    if (MODE & EPI_BIAS) {
+      const float4* b4 = reinterpret_cast<const float4*>(e.bias + col0);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float4 b = __ldg(b4 + k);
+        v[4 * k] += b.x, v[4 * k + 1] += b.y, v[4 * k + 2] += b.z, v[4 * k + 3] += b.w;
+      }
+    }
+    if (MODE & EPI_LEAKY) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = v[j] > 0.f ? v[j] : 0.01f * v[j];  // tape.hpp:88
+    }
+    if (MODE & EPI_SILU) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = silu_fast(v[j]);
+    }
+    if (MODE & EPI_RS) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= rs;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      s4[lane * 8 + (k ^ (lane & 7))] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    __syncwarp();
+    const int oc = col0 + e.col_off + 4 * q;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int r = 4 * k + sub;
+      float4 x = s4[r * 8 + (q ^ (r & 7))];
+      if (orr[k] < 0) continue;
+      if (MODE & EPI_RESID) x.x += rr[k].x, x.y += rr[k].y, x.z += rr[k].z, x.w += rr[k].w;
+      if (MODE & EPI_BF16) {
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)orr[k] * e.ldo + oc) =
+            make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)orr[k] * e.ldo + oc) = x;
+      }
+    }
+    __syncwarp();  // the next chunk reuses stg
+  }
+}
+
 // ---------------------------------------------------------------------------
 // tcgen05 persistent GEMM, one CTA per tile (128 x BN): small M
 // ---------------------------------------------------------------------------
@@ -260,12 +349,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile_rows = grp.tile_rows ? grp.tile_rows : kBM;
-  const int m_tiles = grp.n_mtiles ? *grp.n_mtiles * (tile_rows / kBM) : (M + kBM - 1) / kBM;
-  const int n_tiles = (N + BN - 1) / BN;
-  const int total = m_tiles * n_tiles;
-  const int kblocks = (K + kBK - 1) / kBK;
-  auto expert_of = [&](int mt) { return grp.tile_expert[mt / (tile_rows / kBM)]; };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -285,6 +368,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // setup above touches only parameters, SMEM and TMEM: overlap it with the
+  // previous kernel's tail, then wait for that kernel's outputs
+  pdl_begin();
+  const int tile_rows = grp.tile_rows ? grp.tile_rows : kBM;
+  const int m_tiles = grp.n_mtiles ? *grp.n_mtiles * (tile_rows / kBM) : (M + kBM - 1) / kBM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int total = m_tiles * n_tiles;
+  const int kblocks = (K + kBK - 1) / kBK;
+  auto expert_of = [&](int mt) { return grp.tile_expert[mt / (tile_rows / kBM)]; };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -378,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // rate), the leader CTA issues M=256 MMAs, each CTA drains its own 128-row
 // half of the accumulator from its TMEM.
 // ---------------------------------------------------------------------------
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EPI>  // EPI: specialised EpiMode (staged epilogue) or -1 (generic)
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc2_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                     int N, int K, Epi epi, Grouped grp) {
@@ -400,10 +492,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int m_tiles = grp.n_mtiles ? *grp.n_mtiles : (M + PM - 1) / PM;  // grouped: tile_rows == 256
-  const int n_tiles = (N + BN - 1) / BN;
-  const int total = m_tiles * n_tiles;
-  const int kblocks = (K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -423,6 +511,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_begin();  // as in tc_gemm_kernel: setup overlaps the previous kernel
+  const int m_tiles = grp.n_mtiles ? *grp.n_mtiles : (M + PM - 1) / PM;  // grouped: tile_rows == 256
+  const int n_tiles = (N + BN - 1) / BN;
+  const int total = m_tiles * n_tiles;
+  const int kblocks = (K + kBK - 1) / kBK;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -488,6 +581,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0), tempty_leader1 = mapa_shared(&tempty[1], 0);
+    // 4 KB transpose tile per epilogue warp, after the barrier block
+    float* stg = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 2) * 1024;
+    (void)stg;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = pair; t < total; t += npairs) {
@@ -495,7 +591,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (grp.tile_expert && grp.tile_expert[mt] < 0) continue;
       const int row = mt * PM + static_cast<int>(rank) * kBM + q * 32 + lane;
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-      epilogue_tile<BN>(epi, tb, row, nt, half, &tfull[acc], acc_phase);
+      if constexpr (EPI >= 0)
+        epilogue_tile_staged<BN, EPI>(epi, stg, tb, row, nt, half, &tfull[acc], acc_phase);
+      else
+        epilogue_tile<BN>(epi, tb, row, nt, half, &tfull[acc], acc_phase);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
@@ -517,6 +616,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 __global__ void __launch_bounds__(256) simt_gemm_kernel(const float* __restrict__ A, int lda,
                                                          const float* __restrict__ B, int ldb, int M, int N,
                                                          int K, Epi epi, Grouped grp) {
+  pdl_begin();
   __shared__ float sA[16][64 + 4];
   __shared__ float sB[16][64 + 4];
   const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
@@ -640,17 +740,17 @@ void launch_tc(const void* A, int lda, const void* B, int ldb, int M, int N, int
     tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
     if (tiles > num_sms()) tiles = num_sms();
   }
-  tc_gemm_kernel<BN, STAGES><<<tiles, kThreads, smem, stream>>>(ma, mb, M, N, K, epi, g);
+  launch_pdl(tc_gemm_kernel<BN, STAGES>, tiles, kThreads, smem, stream, ma, mb, M, N, K, epi, g);
   ++launch_counter();
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EPI>
 void launch_tc2(const void* A, int lda, const void* B, int ldb, int M, int N, int K, const Epi& epi,
                 const Grouped* grp, cudaStream_t stream) {
-  constexpr size_t smem = STAGES * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 256;
+  constexpr size_t smem = STAGES * (kBM * kBK * 2 + (BN / 2) * kBK * 2) + 1024 + 256 + (EPI >= 0 ? kEpiWarps * 4096 : 0);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tc2_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(tc2_gemm_kernel<BN, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     attr_set = true;
   }
   Grouped g = grp ? *grp : Grouped{};
@@ -667,8 +767,30 @@ void launch_tc2(const void* A, int lda, const void* B, int ldb, int M, int N, in
     pairs = ((M + 2 * kBM - 1) / (2 * kBM)) * ((N + BN - 1) / BN);
     if (pairs > max_pairs) pairs = max_pairs;
   }
-  tc2_gemm_kernel<BN, STAGES><<<2 * pairs, kThreads, smem, stream>>>(ma, mb, M, N, K, epi, g);
+  launch_pdl(tc2_gemm_kernel<BN, STAGES, EPI>, 2 * pairs, kThreads, smem, stream, ma, mb, M, N, K, epi, g);
   ++launch_counter();
+}
+
+// BN=256 keeps 5 stages (6 without the 32 KB transpose tiles), BN=128 7 (8).
+template <int BN>
+void launch_tc2_mode(int staged, const void* A, int lda, const void* B, int ldb, int M, int N, int K,
+                     const Epi& epi, const Grouped* grp, cudaStream_t stream) {
+  constexpr int S = BN == 256 ? 5 : 7, SG = S + 1;
+  switch (staged) {
+    case 0: launch_tc2<BN, S, 0>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
+    case EPI_RS: launch_tc2<BN, S, EPI_RS>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
+    case EPI_RESID: launch_tc2<BN, S, EPI_RESID>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
+    case EPI_BIAS | EPI_RESID: launch_tc2<BN, S, EPI_BIAS | EPI_RESID>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
+    case EPI_BF16: launch_tc2<BN, S, EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
+    case EPI_BIAS | EPI_BF16: launch_tc2<BN, S, EPI_BIAS | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
+    case EPI_BIAS | EPI_LEAKY | EPI_BF16:
+      launch_tc2<BN, S, EPI_BIAS | EPI_LEAKY | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+      return;
+    case EPI_BIAS | EPI_SILU | EPI_BF16:
+      launch_tc2<BN, S, EPI_BIAS | EPI_SILU | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+      return;
+    default: launch_tc2<BN, SG, -1>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
+  }
 }
 
 }  // namespace
@@ -792,10 +914,14 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
   const bool grouped = grp && grp->tile_expert;
   const bool pair = grouped ? grp->tile_rows == 2 * kBM : (M > kBM && !force_single_cta());
   if (pair) {
-    if (N <= 128 && !epi.swiglu)
-      launch_tc2<128, 8>(A, lda, B, ldb, M, N, K, ep, grp, stream);
+    const bool small_n = N <= 128 && !epi.swiglu;
+    const int bn = small_n ? 128 : 256;
+    // staged (coalesced) epilogue: specialised mode and every tile full
+    const int staged = (ep.mode >= 0 && !ep.swiglu && ep.n_out >= N && N % bn == 0) ? ep.mode : -1;
+    if (small_n)
+      launch_tc2_mode<128>(staged, A, lda, B, ldb, M, N, K, ep, grp, stream);
     else
-      launch_tc2<256, 6>(A, lda, B, ldb, M, N, K, ep, grp, stream);
+      launch_tc2_mode<256>(staged, A, lda, B, ldb, M, N, K, ep, grp, stream);
   } else {
     if (N <= 128 && !epi.swiglu)
       launch_tc<128, 6>(A, lda, B, ldb, M, N, K, ep, grp, stream);
@@ -812,7 +938,7 @@ void gemm_f32(const float* A, int lda, const float* B, int ldb, int M, int N, in
   ProfScope ps(g.tile_expert ? PROF_GEMM_MOE : PROF_GEMM, stream,
                2.0 * (g.tile_expert ? double(g.algo_rows) : double(M)) * N * K, 0.0);
   dim3 grid((N + 63) / 64, (M + 63) / 64);
-  simt_gemm_kernel<<<grid, 256, 0, stream>>>(A, lda, B, ldb, M, N, K, epi, g);
+  launch_pdl(simt_gemm_kernel, grid, 256, 0, stream, A, lda, B, ldb, M, N, K, epi, g);
   ++launch_counter();
 }
 

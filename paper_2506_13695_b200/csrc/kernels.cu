@@ -19,6 +19,7 @@ __device__ __forceinline__ int hashed(int64_t id, int vocab) {  // policy.cpp:14
 // [vid row | aid row | tag | ts | playtime | duration | label multi-hot . emb]
 template <class T>
 __global__ void features_kernel(RecordsDev r, FeatureTables t, T* __restrict__ out, int ldo) {
+  pdl_begin();
   const int d = t.d, ad = t.aid_dim, mn = t.minor;
   const int F = t.vid_only ? d : d + ad + 5 * mn;
   for (int row = blockIdx.x; row < r.n; row += gridDim.x) {
@@ -88,6 +89,7 @@ __device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&v)[8]) {
 // lane per 8-column group; every section width is a multiple of 8 here.
 template <class T>
 __global__ void __launch_bounds__(256) features8_kernel(RecordsDev r, FeatureTables t, T* __restrict__ out, int ldo) {
+  pdl_begin();
   const int d = t.d, ad = t.aid_dim, mn = t.minor;
   const int F = t.vid_only ? d : d + ad + 5 * mn;
   const int lane = threadIdx.x & 31;
@@ -153,6 +155,7 @@ constexpr int kFeatMaxChunks = 12;  // ldo <= 3072
 constexpr int kFeatBatch = 4;       // 16-byte loads in flight per lane
 __global__ void __launch_bounds__(256, 4) features16_kernel(RecordsDev r, FeatureTables t,
                                                             __nv_bfloat16* __restrict__ out, int ldo) {
+  pdl_begin();
   const int d = t.d, ad = t.aid_dim, mn = t.minor;
   const int F = d + ad + 5 * mn;
   const int lane = threadIdx.x & 31;
@@ -208,6 +211,7 @@ template <class T>
 __global__ void static_features_kernel(int U, const int32_t* uid, const int32_t* gender, const int32_t* age,
                                        const float* ue, const float* ge, const float* ae, int sd, int uv, int gv,
                                        int av, T* out, int ldo) {
+  pdl_begin();
   int u = blockIdx.x;
   if (u >= U) return;
   int iu = hashed(uid[u], uv), ig = hashed(gender[u], gv), ia = hashed(age[u], av);
@@ -222,6 +226,7 @@ __global__ void static_features_kernel(int U, const int32_t* uid, const int32_t*
 
 __global__ void z_init_kernel(int U, int T, int d, const float* pos, const float* pad_s, const float* pad_p,
                               const int32_t* n_s, const int32_t* n_p, int Ls, int Lp, float* z) {
+  pdl_begin();
   size_t row = blockIdx.x;
   int u = static_cast<int>(row / T), t = static_cast<int>(row % T);
   const float* pad = nullptr;
@@ -237,6 +242,7 @@ __global__ void z_init_kernel(int U, int T, int d, const float* pos, const float
 template <class T>
 __global__ void rmsnorm_kernel(int rows, int d, const float* __restrict__ x, int ldx, const float* __restrict__ g,
                                T* __restrict__ out, int ldo) {
+  pdl_begin();
   int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (row >= rows) return;
   const float* xr = x + (size_t)row * ldx;
@@ -252,6 +258,7 @@ __global__ void rmsnorm_kernel(int rows, int d, const float* __restrict__ x, int
 template <class T>
 __global__ void convert4_kernel(int rows, int cols, const float* __restrict__ x, int ldx, T* __restrict__ out,
                                 int ldo) {
+  pdl_begin();
   const int q = cols / 4;
   const long long n = (long long)rows * q;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -262,6 +269,7 @@ __global__ void convert4_kernel(int rows, int cols, const float* __restrict__ x,
 
 template <class T>
 __global__ void convert_kernel(int rows, int cols, const float* x, int ldx, T* out, int ldo) {
+  pdl_begin();
   size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   size_t n = (size_t)rows * cols;
   for (; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -272,6 +280,7 @@ __global__ void convert_kernel(int rows, int cols, const float* x, int ldx, T* o
 
 template <class T>
 __global__ void fill_rows_kernel(int rows, int cols, const float* src, T* out, int ldo, const int32_t* idx) {
+  pdl_begin();
   int r = blockIdx.x;
   if (r >= rows) return;
   int orow = idx ? idx[r] : r;
@@ -280,6 +289,7 @@ __global__ void fill_rows_kernel(int rows, int cols, const float* src, T* out, i
 
 __global__ void dec_embed_kernel(int rows, int d, const float* table, const int32_t* code, int code_stride,
                                  float* h) {
+  pdl_begin();
   int r = blockIdx.x;
   if (r >= rows) return;
   size_t src = code ? (size_t)code[(size_t)r * code_stride] * d : 0;
@@ -293,6 +303,7 @@ template <class T>
 __global__ void dec_self_attn_kernel(int rows, int d, int heads, int step, int layer, int L, const T* __restrict__ qkv,
                                      T* const* __restrict__ cache, const int32_t* __restrict__ anc, int anc_stride,
                                      T* __restrict__ out) {
+  pdl_begin();
   int gw = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
   int r = gw / heads, h = gw % heads;
   if (r >= rows) return;
@@ -338,6 +349,7 @@ __global__ void __launch_bounds__(256) dec_self_attn4_kernel(int rows, int d, in
                                                              const T* __restrict__ qkv, T* const* __restrict__ cache,
                                                              const int32_t* __restrict__ anc, int anc_stride,
                                                              T* __restrict__ out) {
+  pdl_begin();
   const int gw = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
   const int r = gw / heads, h = gw % heads;
   if (r >= rows) return;
@@ -385,6 +397,7 @@ __global__ void __launch_bounds__(256) dec_self_attn4_kernel(int rows, int d, in
 __global__ void __launch_bounds__(256) moe_combine4_kernel(int rows, int k, int d, const float* __restrict__ yg,
                                                            const int32_t* __restrict__ slot, float* __restrict__ h,
                                                            int ldh) {
+  pdl_begin();
   const int q = d / 4;
   const long long n = (long long)rows * q;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -474,6 +487,7 @@ __global__ void __launch_bounds__(256) moe_route_kernel(int rows, int d, int E, 
                                                         const float* __restrict__ gate_t,
                                                         const float* __restrict__ bias, int32_t* __restrict__ sel,
                                                         float* __restrict__ wts, int32_t* __restrict__ counts) {
+  pdl_begin();
   extern __shared__ float sg[];  // [E][d]
   for (int i = threadIdx.x; i < E * d; i += blockDim.x) sg[i] = gate_t[i];
   __syncthreads();
@@ -509,6 +523,7 @@ __global__ void __launch_bounds__(256, 2) moe_route2_kernel(int rows, int d, int
                                                             int ldx, const float* __restrict__ gg,
                                                             const float* __restrict__ bias, int32_t* __restrict__ sel,
                                                             float* __restrict__ wts, int32_t* __restrict__ counts) {
+  pdl_begin();
   extern __shared__ float sg[];  // [E][d]
   __shared__ int hist[32];
   for (int i = threadIdx.x; i < E * d / 4; i += blockDim.x)
@@ -592,6 +607,7 @@ __global__ void __launch_bounds__(256, 2) moe_route2_kernel(int rows, int d, int
 // Segment offsets padded to the GEMM expert tile (128 rows, 256 for the CTA-pair kernel); tile -> expert table.
 __global__ void moe_plan_kernel(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
                                 int32_t* n_mtiles, int tile_rows) {
+  pdl_begin();
   // lane e: tiles of expert e, exclusive prefix over experts (E <= 32), then
   // every thread of the block fills the tile -> expert table
   __shared__ int first[33];
@@ -628,6 +644,7 @@ __global__ void moe_scatter_kernel(int rows, int k, int d, const T* __restrict__
                                    const int32_t* __restrict__ sel, const float* __restrict__ wts,
                                    int32_t* __restrict__ cursor, int32_t* __restrict__ slot, T* __restrict__ xg,
                                    float* __restrict__ row_scale) {
+  pdl_begin();
   int gw = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (gw >= rows * k) return;
   int r = gw / k;
@@ -657,6 +674,7 @@ __global__ void __launch_bounds__(256) moe_scatter32_kernel(int rows, int k, int
                                                             const float* __restrict__ wts, int32_t* __restrict__ cursor,
                                                             int32_t* __restrict__ slot, __nv_bfloat16* __restrict__ xg,
                                                             float* __restrict__ row_scale) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int base_pair = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
   const int n_pairs = rows * k;
@@ -688,6 +706,7 @@ __global__ void __launch_bounds__(256) moe_scatter32_kernel(int rows, int k, int
 // h[r] += sum_j (ascending expert) y[slot[r][j]]; y already carries the gate weight.
 __global__ void moe_combine_kernel(int rows, int k, int d, const float* __restrict__ yg,
                                    const int32_t* __restrict__ slot, float* __restrict__ h, int ldh) {
+  pdl_begin();
   int r = blockIdx.x;
   if (r >= rows) return;
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
@@ -698,6 +717,7 @@ __global__ void moe_combine_kernel(int rows, int k, int d, const float* __restri
 }
 
 __global__ void swiglu_mul_kernel(long long n, const float* a, const float* b, float* out) {
+  pdl_begin();
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   for (; i < n; i += (long long)gridDim.x * blockDim.x) {
     float x = a[i];
@@ -708,6 +728,7 @@ __global__ void swiglu_mul_kernel(long long n, const float* a, const float* b, f
 // ---- expert parallelism ------------------------------------------
 // Exclusive prefix of per-expert counts: compact (unpadded) send order by expert.
 __global__ void ep_send_plan_kernel(int E, const int32_t* __restrict__ counts, int32_t* __restrict__ cursor) {
+  pdl_begin();
   const int lane = threadIdx.x;
   int c = lane < E ? counts[lane] : 0;
   int incl = c;
@@ -725,6 +746,7 @@ template <class T>
 __global__ void ep_permute_kernel(int total, int n_seg, const int32_t* __restrict__ tab, int d,
                                   const T* __restrict__ xr, const float* __restrict__ wr, T* __restrict__ xg,
                                   float* __restrict__ row_scale, int32_t* __restrict__ perm) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < total; r += gridDim.x * (blockDim.x >> 5)) {
     int dst = -1;
@@ -750,6 +772,7 @@ __global__ void ep_permute_kernel(int total, int n_seg, const int32_t* __restric
 // ys[r] = yg[perm[r]]: expert outputs back to the received order.
 __global__ void ep_unpermute_kernel(int total, int d, const float* __restrict__ yg, const int32_t* __restrict__ perm,
                                     float* __restrict__ ys) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < total; r += gridDim.x * (blockDim.x >> 5)) {
     const float* a = yg + (size_t)perm[r] * d;
@@ -783,51 +806,51 @@ void launch_features(const RecordsDev& r, const FeatureTables& t, T* out, int ld
   const bool vec = t.d % 8 == 0 && ldo % 8 == 0 && (t.vid_only || (t.aid_dim % 8 == 0 && t.minor % 8 == 0));
   if constexpr (sizeof(T) == 2) {
     if (vec && t.vid16 && t.aid16 && !t.use_sid && !t.vid_only && ldo <= 8 * 32 * kFeatMaxChunks) {
-      ORX_LAUNCH(features16_kernel<<<grid_for(r.n, 8, num_sms() * 8), 256, 0, s>>>(
+      ORX_LAUNCH(launch_pdl(features16_kernel, grid_for(r.n, 8, num_sms() * 8), 256, 0, s, 
           r, t, reinterpret_cast<__nv_bfloat16*>(out), ldo));
       return;
     }
   }
   if (vec) {
-    ORX_LAUNCH(features8_kernel<T><<<grid_for(r.n, 8, num_sms() * 8), 256, 0, s>>>(r, t, out, ldo));
+    ORX_LAUNCH(launch_pdl(features8_kernel<T>, grid_for(r.n, 8, num_sms() * 8), 256, 0, s, r, t, out, ldo));
     return;
   }
-  ORX_LAUNCH(features_kernel<T><<<grid_for(r.n, 1, 148 * 16), 256, 0, s>>>(r, t, out, ldo));
+  ORX_LAUNCH(launch_pdl(features_kernel<T>, grid_for(r.n, 1, 148 * 16), 256, 0, s, r, t, out, ldo));
 }
 template <class T>
 void launch_static_features(int U, const int32_t* uid, const int32_t* gender, const int32_t* age, const float* ue,
                             const float* ge, const float* ae, int sd, int uv, int gv, int av, T* out, int ldo,
                             cudaStream_t s) {
-  ORX_LAUNCH(static_features_kernel<T><<<U, 128, 0, s>>>(U, uid, gender, age, ue, ge, ae, sd, uv, gv, av, out, ldo));
+  ORX_LAUNCH(launch_pdl(static_features_kernel<T>, U, 128, 0, s, U, uid, gender, age, ue, ge, ae, sd, uv, gv, av, out, ldo));
 }
 void launch_z_init(int U, int T, int d, const float* pos, const float* pad_s, const float* pad_p, const int32_t* n_s,
                    const int32_t* n_p, int Ls, int Lp, float* z, cudaStream_t s) {
-  ORX_LAUNCH(z_init_kernel<<<U * T, 256, 0, s>>>(U, T, d, pos, pad_s, pad_p, n_s, n_p, Ls, Lp, z));
+  ORX_LAUNCH(launch_pdl(z_init_kernel, U * T, 256, 0, s, U, T, d, pos, pad_s, pad_p, n_s, n_p, Ls, Lp, z));
 }
 template <class T>
 void launch_rmsnorm(int rows, int d, const float* x, int ldx, const float* gain, T* out, int ldo, cudaStream_t s) {
   if (rows <= 0) return;
-  ORX_LAUNCH(rmsnorm_kernel<T><<<(rows + 7) / 8, 256, 0, s>>>(rows, d, x, ldx, gain, out, ldo));
+  ORX_LAUNCH(launch_pdl(rmsnorm_kernel<T>, (rows + 7) / 8, 256, 0, s, rows, d, x, ldx, gain, out, ldo));
 }
 template <class T>
 void launch_convert(int rows, int cols, const float* x, int ldx, T* out, int ldo, cudaStream_t s) {
   if (rows <= 0) return;
   if (cols % 4 == 0 && ldx % 4 == 0 && ldo % 4 == 0) {
-    ORX_LAUNCH(convert4_kernel<T><<<grid_for((long long)rows * cols / 4, 256), 256, 0, s>>>(rows, cols, x, ldx, out,
+    ORX_LAUNCH(launch_pdl(convert4_kernel<T>, grid_for((long long)rows * cols / 4, 256), 256, 0, s, rows, cols, x, ldx, out,
                                                                                           ldo));
     return;
   }
-  ORX_LAUNCH(convert_kernel<T><<<grid_for((long long)rows * cols, 256), 256, 0, s>>>(rows, cols, x, ldx, out, ldo));
+  ORX_LAUNCH(launch_pdl(convert_kernel<T>, grid_for((long long)rows * cols, 256), 256, 0, s, rows, cols, x, ldx, out, ldo));
 }
 template <class T>
 void launch_fill_rows(int rows, int cols, const float* src, T* out, int ldo, const int32_t* idx, cudaStream_t s) {
   if (rows <= 0) return;
-  ORX_LAUNCH(fill_rows_kernel<T><<<rows, 128, 0, s>>>(rows, cols, src, out, ldo, idx));
+  ORX_LAUNCH(launch_pdl(fill_rows_kernel<T>, rows, 128, 0, s, rows, cols, src, out, ldo, idx));
 }
 void launch_dec_embed(int rows, int d, const float* table, const int32_t* code, int code_stride, float* h,
                       cudaStream_t s) {
   if (rows <= 0) return;
-  ORX_LAUNCH(dec_embed_kernel<<<rows, 256, 0, s>>>(rows, d, table, code, code_stride, h));
+  ORX_LAUNCH(launch_pdl(dec_embed_kernel, rows, 256, 0, s, rows, d, table, code, code_stride, h));
 }
 template <class T>
 void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L, const T* qkv, T* const* cache,
@@ -835,11 +858,11 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L
   if (rows <= 0) return;
   long long warps = (long long)rows * heads;
   if ((d / heads) % 4 == 0 && d / heads <= 128 && d % 4 == 0) {
-    ORX_LAUNCH_CAT(PROF_DEC_SELF, dec_self_attn4_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(
+    ORX_LAUNCH_CAT(PROF_DEC_SELF, launch_pdl(dec_self_attn4_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, 
         rows, d, heads, step, layer, L, qkv, cache, anc, anc_stride, out));
     return;
   }
-  ORX_LAUNCH_CAT(PROF_DEC_SELF, dec_self_attn_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(
+  ORX_LAUNCH_CAT(PROF_DEC_SELF, launch_pdl(dec_self_attn_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, 
       rows, d, heads, step, layer, L, qkv, cache, anc, anc_stride, out));
 }
 void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, const float* gain, const float* gate_t,
@@ -856,7 +879,7 @@ void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, co
     }
     const int per_block = 8 * kRoutePerWarp;
     int blocks = std::min((rows + per_block - 1) / per_block, num_sms() * 2);
-    ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_route2_kernel<<<blocks, 256, smem, s>>>(rows, d, E, k, x, ldx, gate_gain, bias,
+    ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_route2_kernel, blocks, 256, smem, s, rows, d, E, k, x, ldx, gate_gain, bias,
                                                                                sel, wts, counts));
     return;
   }
@@ -867,13 +890,13 @@ void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, co
     set = smem;
   }
   int blocks = std::min((rows + 7) / 8, num_sms() * 2);
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_route_kernel<<<blocks, 256, smem, s>>>(rows, d, E, k, x, ldx, gain, gate_t, bias,
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_route_kernel, blocks, 256, smem, s, rows, d, E, k, x, ldx, gain, gate_t, bias,
                                                                             sel, wts, counts));
 }
 void launch_moe_plan(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
                      int32_t* n_mtiles, int tile_rows, cudaStream_t s) {
   ORX_LAUNCH_CAT(PROF_MOE_ROUTE,
-                 moe_plan_kernel<<<1, 256, 0, s>>>(E, counts, cursor, tile_expert, max_tiles, n_mtiles, tile_rows));
+                 launch_pdl(moe_plan_kernel, 1, 256, 0, s, E, counts, cursor, tile_expert, max_tiles, n_mtiles, tile_rows));
 }
 template <class T>
 void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
@@ -883,44 +906,43 @@ void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32
   if constexpr (sizeof(T) == 2) {
     if (d % 8 == 0 && ldx % 8 == 0 && warps >= 8192) {  // many pairs: aggregate the slot atomics per warp
       const long long w32 = (warps + 31) / 32;
-      ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_scatter32_kernel<<<static_cast<int>((w32 + 7) / 8), 256, 0, s>>>(
+      ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_scatter32_kernel, static_cast<int>((w32 + 7) / 8), 256, 0, s, 
                                          rows, k, d, reinterpret_cast<const __nv_bfloat16*>(x), ldx, sel, wts, cursor,
                                          slot, reinterpret_cast<__nv_bfloat16*>(xg), row_scale));
       return;
     }
   }
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_scatter_kernel<T><<<static_cast<int>((warps + 7) / 8), 256, 0, s>>>(rows, k, d, x, ldx, sel, wts,
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_scatter_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, rows, k, d, x, ldx, sel, wts,
                                                                                       cursor, slot, xg, row_scale));
 }
 void launch_moe_combine(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
                         cudaStream_t s) {
   if (rows <= 0) return;
   if (d % 4 == 0 && ldh % 4 == 0) {
-    ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_combine4_kernel<<<grid_for((long long)rows * d / 4, 256, num_sms() * 8), 256, 0,
-                                                         s>>>(rows, k, d, yg, slot, h, ldh));
+    ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_combine4_kernel, grid_for((long long)rows * d / 4, 256, num_sms() * 8), 256, 0, s, rows, k, d, yg, slot, h, ldh));
     return;
   }
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, moe_combine_kernel<<<rows, 256, 0, s>>>(rows, k, d, yg, slot, h, ldh));
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_combine_kernel, rows, 256, 0, s, rows, k, d, yg, slot, h, ldh));
 }
 void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, cudaStream_t s) {
   if (n <= 0) return;
-  ORX_LAUNCH(swiglu_mul_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, a, b, out));
+  ORX_LAUNCH(launch_pdl(swiglu_mul_kernel, grid_for(n, 256), 256, 0, s, n, a, b, out));
 }
 
 void launch_ep_send_plan(int E, const int32_t* counts, int32_t* cursor, cudaStream_t s) {
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, ep_send_plan_kernel<<<1, 32, 0, s>>>(E, counts, cursor));
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_send_plan_kernel, 1, 32, 0, s, E, counts, cursor));
 }
 template <class T>
 void launch_ep_permute(int total, int n_seg, const int32_t* tab, int d, const T* xr, const float* wr, T* xg,
                        float* row_scale, int32_t* perm, cudaStream_t s) {
   if (total <= 0) return;
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, ep_permute_kernel<T><<<grid_for(total, 8, num_sms() * 8), 256, 0, s>>>(
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_permute_kernel<T>, grid_for(total, 8, num_sms() * 8), 256, 0, s, 
                                      total, n_seg, tab, d, xr, wr, xg, row_scale, perm));
 }
 void launch_ep_unpermute(int total, int d, const float* yg, const int32_t* perm, float* ys, cudaStream_t s) {
   if (total <= 0) return;
   ORX_LAUNCH_CAT(PROF_MOE_ROUTE,
-                 ep_unpermute_kernel<<<grid_for(total, 8, num_sms() * 8), 256, 0, s>>>(total, d, yg, perm, ys));
+                 launch_pdl(ep_unpermute_kernel, grid_for(total, 8, num_sms() * 8), 256, 0, s, total, d, yg, perm, ys));
 }
 
 #define INST(T)                                                                                                   \

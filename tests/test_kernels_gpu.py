@@ -127,6 +127,27 @@ def test_gemm_row_map_scale_resid():
     _close(out, want, False)
 
 
+@pytest.mark.parametrize("scale", [False, True])
+def test_gemm_staged_row_map(scale):
+    """Coalesced (SMEM-transposed) epilogue with scattered / dropped output rows:
+    row_map + residual (specialised mode) and row_map + row scale, ragged M."""
+    M, N, K = 777, 512, 256
+    A, B = _inputs(M, N, K, seed=11)
+    perm = torch.randperm(3 * M, device="cuda")[:M].to(torch.int32)
+    perm[5::9] = -1
+    out = torch.randn(3 * M, N, device="cuda")
+    base = out.clone()
+    rs = torch.rand(M, device="cuda") + 0.5 if scale else None
+    run_gemm(A, B, out=out, row_map=perm, row_scale=rs, resid=None if scale else out)
+    y = A.float() @ B.float().t()
+    if scale:
+        y = y * rs[:, None]
+    want = base.clone()
+    keep = perm >= 0
+    want[perm[keep].long()] = (0 if scale else base[perm[keep].long()]) + y[keep]
+    _close(out, want, False)
+
+
 def _grouped_case(E, counts, h, d, tile_rows, seed):
     """Expert segments padded to tile_rows (moe_plan_kernel layout)."""
     segs, tiles, off = [], [], 0

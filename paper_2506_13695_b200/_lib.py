@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liborx.so")
+# ORX_LIB_PATH: an alternative in-tree build (A/B timing of two library versions)
+LIB_PATH = os.environ.get("ORX_LIB_PATH") or os.path.join(_HERE, "liborx.so")
 
 ORX_OK, ORX_EINVAL, ORX_ERUNTIME, ORX_ECUDA = 0, -1, -2, -3
 PRECISION = {"fp32": 0, "bf16": 1}

@@ -339,6 +339,9 @@ void launch_fmha_tc(const FmhaArgs& a, cudaStream_t s) {
   if (a.ldq % 8 || a.ldk % 8 || a.vt_ld % 8 || a.q_col0 % 8 || a.k_col0 % 8)
     throw std::invalid_argument("fmha: strides / column offsets must be multiples of 8 elements");
   ProfScope ps(PROF_ATTN, s, a.flops, 0.0);
+  if (prof_enabled())
+    prof_note("fmha B=" + std::to_string(a.B) + " heads=" + std::to_string(a.heads) + " max_q=" +
+              std::to_string(a.max_q) + " k_rows=" + std::to_string(a.k_rows));
   if (a.dh == 128) launch_fmha<128>(a, s);
   else if (a.dh == 64) launch_fmha<64>(a, s);
   else throw std::invalid_argument("fmha: head dim must be 64 or 128");

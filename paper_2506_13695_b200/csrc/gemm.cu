@@ -267,20 +267,24 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
                    : "memory");
   }
   float4* s4 = reinterpret_cast<float4*>(stg);
+  // residual chunks in the coalesced layout, one chunk ahead: chunk 0 is in
+  // flight while the MMAs finish, chunk i+1 while chunk i is finished
+  float4 rr[2][8];
+  auto load_resid = [&](int i, float4 (&dst)[8]) {
+    const int col0 = nt * BN + (half * CH + i) * 32;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      dst[k] = orr[k] >= 0 ? __ldg(reinterpret_cast<const float4*>(e.resid + (size_t)orr[k] * e.ld_resid + col0) + q)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  if (MODE & EPI_RESID) load_resid(0, rr[0]);
   mbar_wait(tfull, acc_phase);
   tc_fence_after();
-#pragma unroll 1
-  for (int i = 0; i < CH; ++i) {
+  auto do_chunk = [&](int i, const float4 (&cur)[8], float4 (&nxt)[8]) {
     const int col0 = nt * BN + (half * CH + i) * 32;
     uint32_t ra[32];
     tmem_ld32_async(tb + (half * CH + i) * 32, ra);
-    float4 rr[8];
-    if (MODE & EPI_RESID) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        rr[k] = orr[k] >= 0 ? __ldg(reinterpret_cast<const float4*>(e.resid + (size_t)orr[k] * e.ld_resid + col0) + q)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    if ((MODE & EPI_RESID) && i + 1 < CH) load_resid(i + 1, nxt);
     tmem_wait_ld();
     float v[32];
 #pragma unroll
@@ -315,7 +319,10 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
       const int r = 4 * k + sub;
       float4 x = s4[r * 8 + (q ^ (r & 7))];
       if (orr[k] < 0) continue;
-      if (MODE & EPI_RESID) x.x += rr[k].x, x.y += rr[k].y, x.z += rr[k].z, x.w += rr[k].w;
+      if (MODE & EPI_RESID) {
+        const float4 y = cur[k];
+        x.x += y.x, x.y += y.y, x.z += y.z, x.w += y.w;
+      }
       if (MODE & EPI_BF16) {
         *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)orr[k] * e.ldo + oc) =
             make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
@@ -324,6 +331,12 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
       }
     }
     __syncwarp();  // the next chunk reuses stg
+  };
+  static_assert(CH % 2 == 0, "chunks are processed in pairs");
+#pragma unroll 1
+  for (int i = 0; i < CH; i += 2) {
+    do_chunk(i, rr[0], rr[1]);
+    do_chunk(i + 1, rr[1], rr[0]);
   }
 }
 
@@ -847,6 +860,7 @@ struct ProfRec {
   int cat;
   cudaEvent_t a, b;
   double flops, bytes;
+  std::string note;
 };
 struct Prof {
   bool on = false;
@@ -872,7 +886,7 @@ Prof& prof() {
 ProfScope::ProfScope(int cat, cudaStream_t st, double flops, double bytes) : s(st) {
   Prof& p = prof();
   if (!p.on) return;
-  ProfRec r{cat, p.get(), p.get(), flops, bytes};
+  ProfRec r{cat, p.get(), p.get(), flops, bytes, {}};
   cudaEventRecord(r.a, s);
   idx = static_cast<int>(p.recs.size());
   p.recs.push_back(r);
@@ -881,6 +895,10 @@ ProfScope::~ProfScope() {
   if (idx >= 0) cudaEventRecord(prof().recs[static_cast<size_t>(idx)].b, s);
 }
 void prof_enable(bool on) { prof().on = on; }
+void prof_note(const std::string& note) {
+  Prof& p = prof();
+  if (p.on && !p.recs.empty()) p.recs.back().note = note;
+}
 bool prof_enabled() { return prof().on; }
 void prof_collect(long long* count, double* ms, double* flops, double* bytes) {
   Prof& p = prof();
@@ -891,6 +909,10 @@ void prof_collect(long long* count, double* ms, double* flops, double* bytes) {
     cudaEventElapsedTime(&t, r.a, r.b);
     count[r.cat] += 1;
     ms[r.cat] += t;
+    static const bool dump = getenv("ORX_PROF_DUMP") != nullptr;  // per-launch lines on stderr
+    if (dump)
+      fprintf(stderr, "prof cat=%d %s us=%.1f tflops=%.0f\n", r.cat, r.note.c_str(), t * 1e3,
+              r.flops > 0 ? r.flops / (t * 1e-3) / 1e12 : 0.0);
     flops[r.cat] += r.flops;
     bytes[r.cat] += r.bytes;
     p.pool.push_back(r.a);
@@ -911,10 +933,25 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
                2.0 * (grp && grp->tile_expert ? double(grp->algo_rows) : double(M)) * N * K, 0.0);
   Epi ep = epi;
   ep.mode = epi_mode(ep);
+  if (prof_enabled())
+    prof_note("gemm M=" + std::to_string(M) + " N=" + std::to_string(N) + " K=" + std::to_string(K) +
+              " mode=" + std::to_string(ep.mode) + (grp && grp->tile_expert ? " grouped" : "") +
+              (ep.swiglu ? " swiglu" : "") + (ep.vt ? " vt" : "") + (ep.row_map ? " row_map" : ""));
   const bool grouped = grp && grp->tile_expert;
   const bool pair = grouped ? grp->tile_rows == 2 * kBM : (M > kBM && !force_single_cta());
   if (pair) {
-    const bool small_n = N <= 128 && !epi.swiglu;
+    // BN=128 for small N, and where 256-wide tiles would leave a badly
+    // filled last wave (e.g. M=16384, N=1024: 256 tiles on 74 pairs = 3.46
+    // waves; 512 narrow tiles fill 6.92)
+    bool small_n = N <= 128 && !epi.swiglu;
+    if (!small_n && !epi.swiglu && !grouped && N % 128 == 0 && getenv("ORX_GEMM_BN_PICK")) {
+      const int pairs = num_sms() / 2;
+      const long long mt = (M + 2 * kBM - 1) / (2 * kBM);
+      const long long t256 = mt * ((N + 255) / 256), t128 = mt * (N / 128);
+      const double f256 = double(t256) / (double((t256 + pairs - 1) / pairs) * pairs);
+      const double f128 = double(t128) / (double((t128 + pairs - 1) / pairs) * pairs);
+      small_n = f128 > f256 + 0.08;
+    }
     const int bn = small_n ? 128 : 256;
     // staged (coalesced) epilogue: specialised mode and every tile full
     const int staged = (ep.mode >= 0 && !ep.swiglu && ep.n_out >= N && N % bn == 0) ? ep.mode : -1;

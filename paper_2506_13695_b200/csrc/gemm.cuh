@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+
 namespace orx {
 
 enum Act { ACT_NONE = 0, ACT_LEAKY = 1, ACT_SILU = 2 };
@@ -80,6 +82,7 @@ struct ProfScope {
   cudaStream_t s;
 };
 void prof_enable(bool on);
+void prof_note(const std::string& note);  // label the latest record (ORX_PROF_DUMP)
 bool prof_enabled();
 // Per category: launches, total ms, algorithmic flops, algorithmic bytes.
 void prof_collect(long long* count, double* ms, double* flops, double* bytes);

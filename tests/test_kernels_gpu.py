@@ -29,7 +29,7 @@ def _ptr(t):
 
 def run_gemm(A, B, *, out, bias=None, row_scale=None, resid=None, row_map=None, act=0, swiglu=0, n_out=0,
              m_valid=0, col_off=0, tile_expert=None, n_mtiles=None, b_rows_per_expert=0, n_groups=0, tile_rows=0,
-             force_single_cta=0, precision=1):
+             force_single_cta=0, precision=1, sync=True):
     L = _lib()
     a = L.orx_gemm_args()
     a.A, a.lda = _ptr(A), A.stride(0)
@@ -45,7 +45,8 @@ def run_gemm(A, B, *, out, bias=None, row_scale=None, resid=None, row_map=None, 
     a.b_rows_per_expert, a.n_groups, a.tile_rows = b_rows_per_expert, n_groups, tile_rows
     a.force_single_cta = force_single_cta
     L.check(L.lib().orx_debug_gemm(C.byref(a), None))
-    torch.cuda.synchronize()
+    if sync:
+        torch.cuda.synchronize()
 
 
 def _act(x, act):

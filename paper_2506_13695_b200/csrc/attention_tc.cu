@@ -19,6 +19,7 @@
 // Semantics are mha_core's (tape.cpp:822-905): softmax(Q K^T / sqrt(dh)) V,
 // max-subtracted, keys beyond the segment length masked.
 #include <cfloat>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -197,45 +198,54 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
     for (int j = 0; j < nb; ++j) {
       const int st = j & 1;
       mbar_wait(&s_full[st], (j >> 1) & 1);
+      __syncwarp();  // tcgen05.ld/st are .sync.aligned: reconverge after the per-thread wait / branches
       tc_fence_after();
       uint32_t sa[32], sb[32];
       tmem_ld32_async(t_s + lane_off + st * F::BK, sa);
       tmem_ld32_async(t_s + lane_off + st * F::BK + 32, sb);
       tmem_wait_ld();
       const int valid = klen - j * F::BK;
-      float x[64];
+      float x[64];  // raw scores; the 1/sqrt(dh) * log2(e) scale is folded into the exponent's FMA
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        x[i] = i < valid ? __uint_as_float(sa[i]) * scale_log2 : -FLT_MAX;
-        x[32 + i] = 32 + i < valid ? __uint_as_float(sb[i]) * scale_log2 : -FLT_MAX;
+      for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(sa[i]), x[32 + i] = __uint_as_float(sb[i]);
+      if (valid < F::BK) {  // tail block only: keys beyond the segment
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i >= valid) x[i] = -INFINITY;
       }
-      float bm = -FLT_MAX;
+      float bm = fmaxf(x[0], x[1]);
 #pragma unroll
-      for (int i = 0; i < 64; ++i) bm = fmaxf(bm, x[i]);
+      for (int i = 2; i < 64; i += 2) bm = fmaxf(bm, fmaxf(x[i], x[i + 1]));  // FMNMX3
+      bm *= scale_log2;
       float corr = 1.f;
       bool resc = false;
       if (first || bm > m + 8.f) {  // lazy rescale: keep a stale max unless it grew by > 2^8
-        corr = first ? 0.f : exp2f(m - bm);
+        corr = first ? 0.f : ex2_fast(m - bm);
         resc = !first;
         m = bm;
         first = false;
       }
-      float sum = 0.f;
+      const float2 sc = make_float2(scale_log2, scale_log2), nm = make_float2(-m, -m);
+      float2 acc2 = make_float2(0.f, 0.f);
       uint32_t pk[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const float p0 = exp2f(x[2 * i] - m), p1 = exp2f(x[2 * i + 1] - m);
-        sum += p0 + p1;
-        pk[i] = pack_bf16(p0, p1);
+        const float2 t = ffma2(make_float2(x[2 * i], x[2 * i + 1]), sc, nm);
+        const float2 p = make_float2(ex2_fast(t.x), ex2_fast(t.y));
+        acc2 = fadd2(acc2, p);
+        pk[i] = pack_bf16(p.x, p.y);
       }
+      const float sum = acc2.x + acc2.y;
       l = l * corr + sum;
       // P_j replaces S_j in TMEM (columns [0, 32) of this buffer, keys 2c / 2c+1 in column c)
+      __syncwarp();
       tmem_st32(t_s + lane_off + st * F::BK, pk);
       // P_{j-1} . V_{j-1} (issued when this thread finished block j-1) is normally long done
       // by now; waiting for it every block keeps o_done at most one phase ahead of its waiters
       // and orders the O rescale after it
       if (j >= 1) {
         mbar_wait(&o_done, (j - 1) & 1);
+        __syncwarp();
         tc_fence_after();
       }
       if (__any_sync(0xffffffffu, resc)) {
@@ -256,6 +266,7 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
       if (lane == 0) mbar_arrive(&p_full);
     }
     mbar_wait(&o_done, (nb - 1) & 1);
+    __syncwarp();
     tc_fence_after();
     const float inv = 1.f / l;
     const bool store = q0 + r < qlen;

@@ -193,6 +193,7 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tb, int row
     // B rows interleaved per 128: accumulator cols [0,BN/2) = W1, [BN/2,BN) = W3 (swiglu, nn.cpp:84-86)
     constexpr int CP = BN / 64 / 2;
     mbar_wait(tfull, acc_phase);
+    __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread wait
     tc_fence_after();
 #pragma unroll
     for (int i = 0; i < CP; ++i) {
@@ -222,6 +223,7 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tb, int row
       epi_load_resid(e, orow, nt * BN + half * CH * 32, rc);  // in flight while the MMAs finish
     }
     mbar_wait(tfull, acc_phase);
+    __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread wait
     tc_fence_after();
 #pragma unroll 1
     for (int i = 0; i < CH; ++i) {
@@ -279,6 +281,7 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
   };
   if (MODE & EPI_RESID) load_resid(0, rr[0]);
   mbar_wait(tfull, acc_phase);
+  __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread wait
   tc_fence_after();
   auto do_chunk = [&](int i, const float4 (&cur)[8], float4 (&nxt)[8]) {
     const int col0 = nt * BN + (half * CH + i) * 32;

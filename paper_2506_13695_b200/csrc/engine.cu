@@ -13,7 +13,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -123,6 +129,108 @@ void validate_batch(const orx_config& cfg, const orx_user_batch& b) {  // valida
   check(b.positive_seq, cfg.positive_len, "positive");
   check(b.lifelong_seq, cfg.lifelong_len, "lifelong");
 }
+
+namespace {
+
+// The per-record part of validate_batch for users [u0, u1) of one sequence,
+// as a non-throwing predicate (the request packers run it in parallel; on a
+// failure the sequential validate_batch re-runs to raise the first error in
+// the reference's order). Offsets must already be known to be valid.
+bool records_ok(const orx_config& cfg, const orx_records& r, int u0, int u1) {
+  const uint32_t label_limit = cfg.n_label_flags >= 32 ? 0u : (1u << cfg.n_label_flags);
+  const int64_t i0 = r.offsets[u0], i1 = r.offsets[u1];
+  bool ok = true;
+  for (int u = u0; u < u1; ++u) {
+    const int64_t s = r.offsets[u], e = r.offsets[u + 1];
+    for (int64_t i = s + 1; i < e; ++i) ok &= r.ts[i] >= r.ts[i - 1];
+  }
+  for (int64_t i = i0; i < i1; ++i) {
+    ok &= r.playtime[i] <= r.duration[i] * 1.0 + 1e-6;
+    if (label_limit) ok &= static_cast<uint32_t>(r.labels[i]) < label_limit;
+  }
+  if (cfg.use_sid_history) {
+    if (i1 > i0 && !r.sid) return false;
+    const int L = cfg.n_code_layers;
+    for (int64_t i = i0 * L; i < i1 * L; ++i) ok &= r.sid[i] >= 0 && r.sid[i] < cfg.codebook_size;
+  }
+  return ok;
+}
+
+bool offsets_ok(const orx_config& cfg, const orx_user_batch& b) {
+  const orx_records* rs[3] = {&b.short_seq, &b.positive_seq, &b.lifelong_seq};
+  const int caps[3] = {cfg.short_len, cfg.positive_len, cfg.lifelong_len};
+  for (int p = 0; p < 3; ++p) {
+    const orx_records& r = *rs[p];
+    if (!r.offsets || r.offsets[0] != 0) return false;
+    for (int u = 0; u < b.n_users; ++u)
+      if (r.offsets[u + 1] < r.offsets[u] || r.offsets[u + 1] - r.offsets[u] > caps[p]) return false;
+  }
+  return true;
+}
+
+// Persistent host workers for request packing (thread start-up would cost
+// more than the packing slice of a small request).
+class WorkerPool {
+ public:
+  explicit WorkerPool(int n) {
+    for (int w = 1; w < n; ++w) threads_.emplace_back([this, w] { loop(w); });
+    n_ = n;
+  }
+  ~WorkerPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+  int size() const { return n_; }
+  // fn(w) for w in [0, n) on n threads (the caller runs w = 0); returns when all are done
+  void run(int n, const std::function<void(int)>& fn) {
+    n = std::max(1, std::min(n, n_));
+    {
+      std::lock_guard<std::mutex> g(m_);
+      fn_ = &fn;
+      active_ = n;
+      pending_ = n - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> lk(m_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void loop(int w) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* fn;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        if (w >= active_) continue;
+        fn = fn_;
+      }
+      (*fn)(w);
+      std::lock_guard<std::mutex> g(m_);
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  uint64_t gen_ = 0;
+  int n_ = 1, active_ = 0, pending_ = 0;
+  bool stop_ = false;
+};
+
+}  // namespace
 
 template <class T>
 class EngineT final : public Engine {
@@ -581,10 +689,15 @@ class EngineT final : public Engine {
   } sg_;
 
   void stage_batch(const orx_user_batch& b) override {
+    const auto t_enter = std::chrono::steady_clock::now();
     const orx_config& c = cfg_;
-    validate_batch(c, b);
-    CUDA_CHECK(cudaStreamSynchronize(st_));  // previous copy out of the pinned stage has finished
+    require(b.n_users >= 0, "negative user count");
+    // offsets first (O(users), sequential): the packers below index by them;
+    // the per-record checks run inside the packers
+    if (!offsets_ok(c, b)) validate_batch(c, b);  // raises the first error in reference order
     require(b.n_users >= 1 && b.n_users <= maxU_, "batch size outside the engine capacity");
+    CUDA_CHECK(cudaStreamSynchronize(st_));  // previous copy out of the pinned stage has finished
+    const auto t_synced = std::chrono::steady_clock::now();
     CUDA_CHECK(cudaSetDevice(dev_));
     Stage s;
     s.U = b.n_users;
@@ -650,10 +763,6 @@ class EngineT final : public Engine {
       I32(s.off_kstart)[u] = kpos;
       I32(s.off_klen)[u] = std::max(n, 1);
       if (n == 0) I32(s.off_pad_keys)[npad++] = kpos;
-      for (int t = 0; t < std::max(n, 1); ++t) {
-        I32(s.off_key_user)[kpos + t] = u;
-        I32(s.off_key_pos)[kpos + t] = t;
-      }
       kpos += std::max(n, 1);
     }
     s.n_keys = kpos;
@@ -661,6 +770,13 @@ class EngineT final : public Engine {
     // Record copy / conversion and row maps, split over user ranges on worker
     // threads (this host packing sits inside every end-to-end request).
     auto pack_users = [&](int u0, int u1) {
+      for (int u = u0; u < u1; ++u) {  // key row -> (user, position)
+        const int k0 = I32(s.off_kstart)[u], kn = I32(s.off_klen)[u];
+        for (int t = 0; t < kn; ++t) {
+          I32(s.off_key_user)[k0 + t] = u;
+          I32(s.off_key_pos)[k0 + t] = t;
+        }
+      }
       for (int p = 0; p < 3; ++p) {
         const orx_records& r = *rs[p];
         if (s.n_rec[p] == 0) continue;
@@ -691,17 +807,40 @@ class EngineT final : public Engine {
       }
     };
     const int64_t total_rec = static_cast<int64_t>(s.n_rec[0]) + s.n_rec[1] + s.n_rec[2];
-    const int n_workers = static_cast<int>(std::min<int64_t>(
-        {8, std::max(1u, std::thread::hardware_concurrency()), std::max<int64_t>(1, total_rec / 32768), s.U}));
-    if (n_workers <= 1) {
-      pack_users(0, s.U);
-    } else {
-      std::vector<std::thread> pool;
-      for (int w = 0; w < n_workers; ++w)
-        pool.emplace_back(pack_users, s.U * w / n_workers, s.U * (w + 1) / n_workers);
-      for (auto& t : pool) t.join();
+    const auto t_pack0 = std::chrono::steady_clock::now();
+    const int n_workers = static_cast<int>(
+        std::min<int64_t>({pool_.size(), std::max<int64_t>(1, total_rec / 16384), s.U}));
+    std::atomic<bool> rec_ok{true};
+    pool_.run(n_workers, [&](int w) {
+      const int u0 = s.U * w / n_workers, u1 = s.U * (w + 1) / n_workers;
+      bool ok = true;
+      for (int p = 0; p < 3; ++p) ok &= records_ok(c, *rs[p], u0, u1);
+      if (!ok) {
+        rec_ok = false;
+        return;
+      }
+      pack_users(u0, u1);
+    });
+    if (!rec_ok) validate_batch(c, b);  // raises the first error in reference order
+    static const bool timing = getenv("ORX_STAGE_TIMING") != nullptr;
+    if (timing) {
+      const auto now = std::chrono::steady_clock::now();
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      fprintf(stderr, "stage: validate+sync %.3f ms, layout %.3f ms, %d workers pack %.3f ms\n",
+              ms(t_enter, t_synced), ms(t_synced, t_pack0), n_workers, ms(t_pack0, now));
     }
+    const auto t_copy0 = std::chrono::steady_clock::now();
     CUDA_CHECK(cudaMemcpyAsync(dev_stage_, host_stage_, s.bytes, cudaMemcpyHostToDevice, st_));
+    if (timing) {
+      const auto t1 = std::chrono::steady_clock::now();
+      CUDA_CHECK(cudaStreamSynchronize(st_));
+      const auto t2 = std::chrono::steady_clock::now();
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      cudaPointerAttributes pa{};
+      cudaPointerGetAttributes(&pa, host_stage_);
+      fprintf(stderr, "stage: H2D %zu B issue %.3f ms, complete %.3f ms (host type %d)\n", s.bytes, ms(t_copy0, t1),
+              ms(t1, t2), int(pa.type));
+    }
     h2d_bytes += static_cast<int64_t>(s.bytes);
     sg_ = s;
     staged_ = true;
@@ -1474,6 +1613,7 @@ class EngineT final : public Engine {
   double* seq_acc_ = nullptr;
   double* uni_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
+  WorkerPool pool_{static_cast<int>(std::clamp(std::thread::hardware_concurrency(), 1u, 16u))};
   long long graph_kernels_ = 0;
   GraphKey graph_key_{};
   int32_t *tf_anc_, *tf_codes_, *grp_start_, *grp_len_, *grp_kstart_;

@@ -156,6 +156,22 @@ bool records_ok(const orx_config& cfg, const orx_records& r, int u0, int u1) {
   return ok;
 }
 
+// Write back and evict [p, p + n) from the CPU caches. The pinned stage is
+// packed by many cores; a DMA read of lines still dirty in several cores'
+// caches runs at ~6 GB/s on the B200 hosts, after a flush at ~53 GB/s
+// (12.6 MB: 2.2 ms -> 0.24 ms, measured with build/probe/h2d_nt.cu).
+#if defined(__x86_64__)
+__attribute__((target("clflushopt"))) void flush_lines(const void* p, size_t n) {
+  const char* c = static_cast<const char*>(p);
+  const char* e = c + n;
+  for (c = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(c) & ~uintptr_t(63)); c < e; c += 64)
+    __builtin_ia32_clflushopt(c);
+  __builtin_ia32_sfence();
+}
+#else
+void flush_lines(const void*, size_t) {}
+#endif
+
 bool offsets_ok(const orx_config& cfg, const orx_user_batch& b) {
   const orx_records* rs[3] = {&b.short_seq, &b.positive_seq, &b.lifelong_seq};
   const int caps[3] = {cfg.short_len, cfg.positive_len, cfg.lifelong_len};
@@ -822,6 +838,11 @@ class EngineT final : public Engine {
       pack_users(u0, u1);
     });
     if (!rec_ok) validate_batch(c, b);  // raises the first error in reference order
+    const int n_flush = static_cast<int>(std::min<int64_t>(pool_.size(), std::max<size_t>(1, s.bytes >> 19)));
+    pool_.run(n_flush, [&](int w) {  // stage lines out of the CPU caches before the DMA reads them
+      const size_t a = (s.bytes * w / n_flush) & ~size_t(63), e = w + 1 == n_flush ? s.bytes : (s.bytes * (w + 1) / n_flush) & ~size_t(63);
+      flush_lines(H + a, e - a);
+    });
     static const bool timing = getenv("ORX_STAGE_TIMING") != nullptr;
     if (timing) {
       const auto now = std::chrono::steady_clock::now();

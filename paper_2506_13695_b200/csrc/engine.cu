@@ -159,7 +159,7 @@ bool records_ok(const orx_config& cfg, const orx_records& r, int u0, int u1) {
 // Write back and evict [p, p + n) from the CPU caches. The pinned stage is
 // packed by many cores; a DMA read of lines still dirty in several cores'
 // caches runs at ~6 GB/s on the B200 hosts, after a flush at ~53 GB/s
-// (12.6 MB: 2.2 ms -> 0.24 ms, measured with build/probe/h2d_nt.cu).
+// (12.6 MB: 2.2 ms -> 0.24 ms, measured with profiles/h2d_flush_probe.cu).
 #if defined(__x86_64__)
 __attribute__((target("clflushopt"))) void flush_lines(const void* p, size_t n) {
   const char* c = static_cast<const char*>(p);

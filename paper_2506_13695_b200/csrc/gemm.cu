@@ -343,6 +343,49 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
   }
 }
 
+// Staged SwiGLU epilogue (MoE W1|W3 GEMM): silu(a) * b per 32-column chunk,
+// then the same SMEM transpose and coalesced bf16 row stores as above.
+template <int BN>
+__device__ __forceinline__ void epilogue_tile_swiglu_staged(const Epi& e, float* stg, uint32_t tb, int row, int nt,
+                                                            int half, uint64_t* tfull, uint32_t acc_phase) {
+  constexpr int CP = BN / 64 / 2;  // 32-column output chunks per warp
+  const int lane = threadIdx.x & 31, sub = lane >> 3, q = lane & 7;
+  const int orow = row < e.m_valid ? (e.row_map ? e.row_map[row] : row) : -1;
+  int orr[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) orr[k] = __shfl_sync(0xffffffffu, orow, 4 * k + sub);
+  float4* s4 = reinterpret_cast<float4*>(stg);
+  mbar_wait(tfull, acc_phase);
+  __syncwarp();
+  tc_fence_after();
+#pragma unroll 1
+  for (int i = 0; i < CP; ++i) {
+    const int c = half * CP + i;
+    uint32_t ra[32], rb[32];
+    tmem_ld32_async(tb + c * 32, ra);
+    tmem_ld32_async(tb + BN / 2 + c * 32, rb);
+    tmem_wait_ld();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = silu_fast(__uint_as_float(ra[4 * k + j])) * __uint_as_float(rb[4 * k + j]);
+      s4[lane * 8 + (k ^ (lane & 7))] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    __syncwarp();
+    const int oc = nt * (BN / 2) + c * 32 + e.col_off + 4 * q;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int r = 4 * k + sub;
+      const float4 x = s4[r * 8 + (q ^ (r & 7))];
+      if (orr[k] >= 0)
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)orr[k] * e.ldo + oc) =
+            make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
+    }
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // tcgen05 persistent GEMM, one CTA per tile (128 x BN): small M
 // ---------------------------------------------------------------------------
@@ -607,7 +650,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (grp.tile_expert && grp.tile_expert[mt] < 0) continue;
       const int row = mt * PM + static_cast<int>(rank) * kBM + q * 32 + lane;
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-      if constexpr (EPI >= 0)
+      if constexpr (EPI == (EPI_SWIGLU | EPI_BF16))
+        epilogue_tile_swiglu_staged<BN>(epi, stg, tb, row, nt, half, &tfull[acc], acc_phase);
+      else if constexpr (EPI >= 0)
         epilogue_tile_staged<BN, EPI>(epi, stg, tb, row, nt, half, &tfull[acc], acc_phase);
       else
         epilogue_tile<BN>(epi, tb, row, nt, half, &tfull[acc], acc_phase);
@@ -805,6 +850,12 @@ void launch_tc2_mode(int staged, const void* A, int lda, const void* B, int ldb,
     case EPI_BIAS | EPI_SILU | EPI_BF16:
       launch_tc2<BN, S, EPI_BIAS | EPI_SILU | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream);
       return;
+    case EPI_SWIGLU | EPI_BF16:
+      if constexpr (BN == 256) {
+        launch_tc2<BN, S, EPI_SWIGLU | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+        return;
+      }
+      [[fallthrough]];
     default: launch_tc2<BN, SG, -1>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
   }
 }
@@ -814,11 +865,15 @@ void launch_tc2_mode(int staged, const void* A, int lda, const void* B, int ldb,
 // Specialised epilogue mode of a launch (-1: generic path). Requires the
 // output rows / bias to be 16-byte aligned per 32-column chunk.
 int epi_mode(const Epi& e) {
+  const bool plain = !e.bias && !e.act && !e.row_scale && !e.resid;
+  // transposed V store: generic path (its per-column stores are already coalesced
+  // across lanes; a SMEM-transposed variant measured slower)
   if (e.vt) return -1;
   const int esz = e.out_bf16 ? 2 : 4;
   if ((reinterpret_cast<uintptr_t>(e.out) % 16) || ((long long)e.ldo * esz) % 16 || (e.col_off * esz) % 16) return -1;
   if (e.resid && ((reinterpret_cast<uintptr_t>(e.resid) % 16) || (e.ld_resid % 4))) return -1;
   if (e.bias && reinterpret_cast<uintptr_t>(e.bias) % 16) return -1;
+  if (e.swiglu) return plain && e.out_bf16 ? EPI_SWIGLU | EPI_BF16 : -1;
   int m = 0;
   if (e.bias) m |= EPI_BIAS;
   if (e.act == ACT_LEAKY) m |= EPI_LEAKY;
@@ -957,7 +1012,7 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
     }
     const int bn = small_n ? 128 : 256;
     // staged (coalesced) epilogue: specialised mode and every tile full
-    const int staged = (ep.mode >= 0 && !ep.swiglu && ep.n_out >= N && N % bn == 0) ? ep.mode : -1;
+    const int staged = (ep.mode >= 0 && ep.n_out >= (ep.swiglu ? N / 2 : N) && N % bn == 0) ? ep.mode : -1;
     if (small_n)
       launch_tc2_mode<128>(staged, A, lda, B, ldb, M, N, K, ep, grp, stream);
     else

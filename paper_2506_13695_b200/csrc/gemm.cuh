@@ -18,7 +18,10 @@ namespace orx {
 
 enum Act { ACT_NONE = 0, ACT_LEAKY = 1, ACT_SILU = 2 };
 // Epilogue mode bits (Epi::mode, set by the launcher): specialised code paths.
-enum EpiMode { EPI_BIAS = 1, EPI_LEAKY = 2, EPI_SILU = 4, EPI_RS = 8, EPI_RESID = 16, EPI_BF16 = 32 };
+enum EpiMode {
+  EPI_BIAS = 1, EPI_LEAKY = 2, EPI_SILU = 4, EPI_RS = 8, EPI_RESID = 16, EPI_BF16 = 32,
+  EPI_SWIGLU = 64  // silu(a) * b over the interleaved W1|W3 accumulator (bf16 out, nothing else)
+};
 
 struct Epi {
   const float* bias = nullptr;       // [N] (or [N/2] for swiglu: not used)

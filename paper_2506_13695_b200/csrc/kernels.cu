@@ -235,6 +235,20 @@ __global__ void z_init_kernel(int U, int T, int d, const float* pos, const float
   } else if (t >= 1 + Ls && t < 1 + Ls + Lp) {
     if (t - 1 - Ls < Lp - n_p[u]) pad = pad_p;
   }
+  if (d % 4 == 0) {  // float4 path (the callers' buffers are 16-byte aligned)
+    const float4* p4 = reinterpret_cast<const float4*>(pos + (size_t)t * d);
+    const float4* q4 = reinterpret_cast<const float4*>(pad);
+    float4* z4 = reinterpret_cast<float4*>(z + row * d);
+    for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+      float4 v = __ldg(p4 + c);
+      if (pad) {
+        const float4 w = __ldg(q4 + c);
+        v.x += w.x, v.y += w.y, v.z += w.z, v.w += w.w;
+      }
+      z4[c] = v;
+    }
+    return;
+  }
   for (int c = threadIdx.x; c < d; c += blockDim.x) z[row * d + c] = pos[(size_t)t * d + c] + (pad ? pad[c] : 0.f);
 }
 
@@ -293,6 +307,12 @@ __global__ void dec_embed_kernel(int rows, int d, const float* table, const int3
   int r = blockIdx.x;
   if (r >= rows) return;
   size_t src = code ? (size_t)code[(size_t)r * code_stride] * d : 0;
+  if (d % 4 == 0) {
+    const float4* t4 = reinterpret_cast<const float4*>(table + src);
+    float4* h4 = reinterpret_cast<float4*>(h + (size_t)r * d);
+    for (int c = threadIdx.x; c < d / 4; c += blockDim.x) h4[c] = __ldg(t4 + c);
+    return;
+  }
   for (int c = threadIdx.x; c < d; c += blockDim.x) h[(size_t)r * d + c] = table[src + c];
 }
 
@@ -825,7 +845,11 @@ void launch_static_features(int U, const int32_t* uid, const int32_t* gender, co
 }
 void launch_z_init(int U, int T, int d, const float* pos, const float* pad_s, const float* pad_p, const int32_t* n_s,
                    const int32_t* n_p, int Ls, int Lp, float* z, cudaStream_t s) {
-  ORX_LAUNCH(launch_pdl(z_init_kernel, U * T, 256, 0, s, U, T, d, pos, pad_s, pad_p, n_s, n_p, Ls, Lp, z));
+  const bool al = reinterpret_cast<uintptr_t>(pos) % 16 == 0 && reinterpret_cast<uintptr_t>(z) % 16 == 0 &&
+                  reinterpret_cast<uintptr_t>(pad_s) % 16 == 0 && reinterpret_cast<uintptr_t>(pad_p) % 16 == 0;
+  if (!al && d % 4 == 0) throw std::invalid_argument("z_init: buffers must be 16-byte aligned");
+  ORX_LAUNCH(launch_pdl(z_init_kernel, U * T, d % 4 == 0 ? std::min(256, d / 4) : 256, 0, s, U, T, d, pos, pad_s, pad_p,
+                        n_s, n_p, Ls, Lp, z));
 }
 // Warp per row, the row held in registers: one float4 load per lane per 128
 // columns, all NC issued before the reduction (the scalar kernel above ran at
@@ -895,7 +919,10 @@ void launch_fill_rows(int rows, int cols, const float* src, T* out, int ldo, con
 void launch_dec_embed(int rows, int d, const float* table, const int32_t* code, int code_stride, float* h,
                       cudaStream_t s) {
   if (rows <= 0) return;
-  ORX_LAUNCH(launch_pdl(dec_embed_kernel, rows, 256, 0, s, rows, d, table, code, code_stride, h));
+  if (d % 4 == 0 && (reinterpret_cast<uintptr_t>(table) % 16 || reinterpret_cast<uintptr_t>(h) % 16))
+    throw std::invalid_argument("dec_embed: buffers must be 16-byte aligned");
+  ORX_LAUNCH(launch_pdl(dec_embed_kernel, rows, d % 4 == 0 ? std::min(256, d / 4) : 256, 0, s, rows, d, table, code,
+                        code_stride, h));
 }
 template <class T>
 void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L, const T* qkv, T* const* cache,

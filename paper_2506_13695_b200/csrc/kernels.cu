@@ -159,6 +159,16 @@ __global__ void __launch_bounds__(256, 4) features16_kernel(RecordsDev r, Featur
   const int d = t.d, ad = t.aid_dim, mn = t.minor;
   const int F = d + ad + 5 * mn;
   const int lane = threadIdx.x & 31;
+  // the minor-feature tables (4 x [2][mn] + [n_flags][mn] fp32) in shared
+  // memory: read as float4 per 8-column chunk instead of scalar L1 loads
+  extern __shared__ float4 sm4[];
+  float* smt = reinterpret_cast<float*>(sm4);
+  const int nt = 8 * mn + t.n_flags * mn;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    const int f = i / (2 * mn), j = i - f * 2 * mn;
+    smt[i] = f < 4 ? (f == 0 ? t.tag : f == 1 ? t.ts : f == 2 ? t.play : t.dur)[j] : t.label[i - 8 * mn];
+  }
+  __syncthreads();
   for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < r.n; row += gridDim.x * (blockDim.x >> 5)) {
     const int vid = hashed(r.vid[row], t.vid_vocab);
     const int aid = hashed(r.aid[row], t.aid_vocab);
@@ -187,15 +197,24 @@ __global__ void __launch_bounds__(256, 4) features16_kernel(RecordsDev r, Featur
             const int cc = c0 - d - ad, f = cc / mn, j0 = cc % mn;
             if (f < 4) {  // x * w + b (policy.cpp:175-188)
               const float x = f == 0 ? r.tag[row] : f == 1 ? r.ts[row] : f == 2 ? r.play[row] : r.dur[row];
-              const float* p = f == 0 ? t.tag : f == 1 ? t.ts : f == 2 ? t.play : t.dur;
+              const float4* w4 = reinterpret_cast<const float4*>(smt + f * 2 * mn + j0);
+              const float4* b4 = reinterpret_cast<const float4*>(smt + f * 2 * mn + mn + j0);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) v[j] = x * p[j0 + j] + p[mn + j0 + j];
+              for (int h = 0; h < 2; ++h) {
+                const float4 w = w4[h], b = b4[h];
+                v[4 * h] = x * w.x + b.x, v[4 * h + 1] = x * w.y + b.y;
+                v[4 * h + 2] = x * w.z + b.z, v[4 * h + 3] = x * w.w + b.w;
+              }
             } else {  // labels multi-hot . (5 x minor) (policy.cpp:190-195)
               const uint32_t lab = r.labels[row];
               for (int b = 0; b < t.n_flags; ++b)
                 if ((lab >> b) & 1u) {
+                  const float4* l4 = reinterpret_cast<const float4*>(smt + 8 * mn + b * mn + j0);
 #pragma unroll
-                  for (int j = 0; j < 8; ++j) v[j] += t.label[b * mn + j0 + j];
+                  for (int h = 0; h < 2; ++h) {
+                    const float4 w = l4[h];
+                    v[4 * h] += w.x, v[4 * h + 1] += w.y, v[4 * h + 2] += w.z, v[4 * h + 3] += w.w;
+                  }
                 }
             }
           }
@@ -826,7 +845,9 @@ void launch_features(const RecordsDev& r, const FeatureTables& t, T* out, int ld
   const bool vec = t.d % 8 == 0 && ldo % 8 == 0 && (t.vid_only || (t.aid_dim % 8 == 0 && t.minor % 8 == 0));
   if constexpr (sizeof(T) == 2) {
     if (vec && t.vid16 && t.aid16 && !t.use_sid && !t.vid_only && ldo <= 8 * 32 * kFeatMaxChunks) {
-      ORX_LAUNCH(launch_pdl(features16_kernel, grid_for(r.n, 8, num_sms() * 8), 256, 0, s, 
+      const size_t tsm = sizeof(float) * (8 + t.n_flags) * t.minor;
+      if (tsm > 48 * 1024) cudaFuncSetAttribute(features16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsm));
+      ORX_LAUNCH(launch_pdl(features16_kernel, grid_for(r.n, 8, num_sms() * 8), 256, tsm, s, 
           r, t, reinterpret_cast<__nv_bfloat16*>(out), ldo));
       return;
     }

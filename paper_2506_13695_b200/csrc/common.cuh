@@ -284,10 +284,15 @@ ORX_DEV float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
+// silu(x) = x * sigmoid(x) = h + h * tanh(h), h = x / 2: one SFU op
+// (tanh.approx, |rel err| < 2^-11 -> absolute error <= |h| * 2^-11, below the
+// bf16 rounding of the epilogue's output) instead of ex2 + rcp; the fused
+// GEMM epilogues are SFU-bound on SiLU / SwiGLU tiles.
 ORX_DEV float silu_fast(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + __expf(-x)));
-  return x * r;
+  const float h = 0.5f * x;
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+  return fmaf(h, t, h);
 }
 
 // 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread.

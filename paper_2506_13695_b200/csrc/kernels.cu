@@ -945,11 +945,132 @@ void launch_dec_embed(int rows, int d, const float* table, const int32_t* code, 
   ORX_LAUNCH(launch_pdl(dec_embed_kernel, rows, d % 4 == 0 ? std::min(256, d / 4) : 256, 0, s, rows, d, table, code,
                         code_stride, h));
 }
+// bf16 decoder self-attention, one warp per ROW (all heads): lane l owns
+// columns [l * EPL, (l + 1) * EPL) of q / k / v (16-byte loads), a head spans
+// dh / EPL lanes, so each position's dot product is a per-lane partial plus a
+// log2(dh / EPL)-step shuffle; the ancestor row of each cached position is
+// loaded once per row instead of once per head (the warp-per-head kernel
+// above was issue bound on shuffles and index math).
+template <int EPL>
+__global__ void __launch_bounds__(256) dec_self_attn_row_kernel(int rows, int d, int heads, int step, int layer, int L,
+                                                                const __nv_bfloat16* __restrict__ qkv,
+                                                                __nv_bfloat16* const* __restrict__ cache,
+                                                                const int32_t* __restrict__ anc, int anc_stride,
+                                                                __nv_bfloat16* __restrict__ out) {
+  pdl_begin();
+  constexpr int NV = EPL / 8;  // uint4 (8 x bf16) per lane
+  const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  const int dh = d / heads, lph = dh / EPL;  // lanes per head (power of two)
+  const int c0 = lane * EPL;
+  const __nv_bfloat16* qr = qkv + (size_t)r * 3 * d + c0;
+  uint4 q[NV], kv_own[2][NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    q[i] = __ldg(reinterpret_cast<const uint4*>(qr) + i);
+    kv_own[0][i] = __ldg(reinterpret_cast<const uint4*>(qr + d) + i);
+    kv_own[1][i] = __ldg(reinterpret_cast<const uint4*>(qr + 2 * d) + i);
+  }
+  __nv_bfloat16* cown = cache[step] + ((size_t)r * L + layer) * 2 * d + c0;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    reinterpret_cast<uint4*>(cown)[i] = kv_own[0][i];
+    reinterpret_cast<uint4*>(cown + d)[i] = kv_own[1][i];
+  }
+  const int a_l = lane < step ? anc[(size_t)r * anc_stride + lane] : 0;
+  auto bf2 = [](uint32_t w) { return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w)); };
+  auto dot = [&](const uint4* k) {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const uint32_t qw[4] = {q[i].x, q[i].y, q[i].z, q[i].w}, kw[4] = {k[i].x, k[i].y, k[i].z, k[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 a = bf2(qw[j]), b = bf2(kw[j]);
+        s = fmaf(a.x, b.x, s);
+        s = fmaf(a.y, b.y, s);
+      }
+    }
+    for (int o = lph >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+  };
+  const float scale = rsqrtf(static_cast<float>(dh));
+  float sc[8];
+  float mx = -FLT_MAX;
+  for (int p = 0; p <= step; ++p) {
+    float sp;
+    if (p < step) {
+      const int ar = __shfl_sync(0xffffffffu, a_l, p);
+      const uint4* kp = reinterpret_cast<const uint4*>(cache[p] + ((size_t)ar * L + layer) * 2 * d + c0);
+      uint4 kk[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) kk[i] = kp[i];
+      sp = dot(kk);
+    } else {
+      sp = dot(kv_own[0]);
+    }
+    sc[p] = sp * scale;
+    mx = fmaxf(mx, sc[p]);
+  }
+  float den = 0.f;
+  for (int p = 0; p <= step; ++p) {
+    sc[p] = __expf(sc[p] - mx);
+    den += sc[p];
+  }
+  float acc[EPL];
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+  for (int p = 0; p <= step; ++p) {
+    uint4 vv[NV];
+    if (p < step) {
+      const int ar = __shfl_sync(0xffffffffu, a_l, p);
+      const uint4* vp = reinterpret_cast<const uint4*>(cache[p] + ((size_t)ar * L + layer) * 2 * d + d + c0);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) vv[i] = vp[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) vv[i] = kv_own[1][i];
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const uint32_t vw[4] = {vv[i].x, vv[i].y, vv[i].z, vv[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 b = bf2(vw[j]);
+        acc[8 * i + 2 * j] = fmaf(sc[p], b.x, acc[8 * i + 2 * j]);
+        acc[8 * i + 2 * j + 1] = fmaf(sc[p], b.y, acc[8 * i + 2 * j + 1]);
+      }
+    }
+  }
+  const float inv = 1.f / den;
+  uint4* o = reinterpret_cast<uint4*>(out + (size_t)r * d + c0);
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    o[i] = make_uint4(pack_bf16(acc[8 * i] * inv, acc[8 * i + 1] * inv), pack_bf16(acc[8 * i + 2] * inv, acc[8 * i + 3] * inv),
+                      pack_bf16(acc[8 * i + 4] * inv, acc[8 * i + 5] * inv), pack_bf16(acc[8 * i + 6] * inv, acc[8 * i + 7] * inv));
+}
+
 template <class T>
 void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L, const T* qkv, T* const* cache,
                           const int32_t* anc, int anc_stride, T* out, cudaStream_t s) {
   if (rows <= 0) return;
   long long warps = (long long)rows * heads;
+  if constexpr (sizeof(T) == 2) {
+    const int dh = d / heads, epl = d / 32, lph = epl > 0 ? dh / epl : 0;
+    if (d % 256 == 0 && epl <= 64 && dh % epl == 0 && (lph & (lph - 1)) == 0 && step < 8) {  // whole row per warp
+      auto go = [&](auto kern) {
+        ORX_LAUNCH_CAT(PROF_DEC_SELF, launch_pdl(kern, (rows + 7) / 8, 256, 0, s, rows, d, heads, step, layer, L,
+                                                 reinterpret_cast<const __nv_bfloat16*>(qkv),
+                                                 reinterpret_cast<__nv_bfloat16* const*>(cache), anc, anc_stride,
+                                                 reinterpret_cast<__nv_bfloat16*>(out)));
+      };
+      if (epl == 8) go(dec_self_attn_row_kernel<8>);
+      else if (epl == 16) go(dec_self_attn_row_kernel<16>);
+      else if (epl == 32) go(dec_self_attn_row_kernel<32>);
+      else go(dec_self_attn_row_kernel<64>);
+      return;
+    }
+  }
   if ((d / heads) % 4 == 0 && d / heads <= 128 && d % 4 == 0) {
     ORX_LAUNCH_CAT(PROF_DEC_SELF, launch_pdl(dec_self_attn4_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, 
         rows, d, heads, step, layer, L, qkv, cache, anc, anc_stride, out));

@@ -1018,7 +1018,12 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
     else
       launch_tc2_mode<256>(staged, A, lda, B, ldb, M, N, K, ep, grp, stream);
   } else {
-    if (N <= 128 && !epi.swiglu)
+    // M <= 128 (decoder step 0): the GEMM is a weight stream; 64-wide tiles put
+    // 4x more SMs on it than 256-wide ones (N=1024: 16 CTAs instead of 4)
+    const bool narrow = !epi.swiglu && !grouped && N >= 512 && M <= kBM && !getenv("ORX_GEMM_NO_NARROW");
+    if (narrow)
+      launch_tc<64, 8>(A, lda, B, ldb, M, N, K, ep, grp, stream);
+    else if (N <= 128 && !epi.swiglu)
       launch_tc<128, 6>(A, lda, B, ldb, M, N, K, ep, grp, stream);
     else
       launch_tc<256, 4>(A, lda, B, ldb, M, N, K, ep, grp, stream);

@@ -82,6 +82,8 @@ DENSE = [
     (6000, 1024, 2048, 0, True, False, True),   # FFN fc2 + residual (fp32 stream)
     (1000, 128, 256, 1, True, True, False),     # BN=128 CTA-pair kernel
     (77, 96, 40, 0, True, False, True),         # tiny, 1-CTA BN=128
+    (100, 1024, 1024, 0, True, False, True),    # M <= 128, N >= 512: 1-CTA BN=64 (decoder step 0), residual
+    (64, 2048, 512, 2, True, True, False),      # same kernel, SiLU + bf16 out
 ]
 
 

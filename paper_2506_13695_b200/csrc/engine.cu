@@ -402,8 +402,8 @@ class EngineT final : public Engine {
   struct Mlp { Lin<T> fc1, fc2; };
   // tc_attn_ (bf16, head dim 64/128): V is projected by its own GEMM whose
   // epilogue writes it transposed per (user, head) for the tcgen05 attention
-  struct QBlock { Lin<T> wq, wkv, wk, wv, wo, fc1, fc2; const float* gain; };
-  struct EncL { const float *n1, *n2; Lin<T> wqkv, wqk, wv, wo, fc1, fc2; MoeW moe; };
+  struct QBlock { Lin<T> wq, wkv, wo, fc1, fc2; const float* gain; };
+  struct EncL { const float *n1, *n2; Lin<T> wqkv, wo, fc1, fc2; MoeW moe; };
   struct DecL { const float *n1, *n2, *n3; Lin<T> sqkv, so, cq, co, fc1, fc2; MoeW moe; };
 
   void upload(const HostWeights& hw) {
@@ -458,12 +458,7 @@ class EngineT final : public Engine {
       std::string n = "lifelong.block" + std::to_string(b);
       QBlock q;
       q.wq = pack(hw, {n + ".attn.wq.w"});
-      if (tc_attn_) {
-        q.wk = pack(hw, {n + ".attn.wk.w"});
-        q.wv = pack(hw, {n + ".attn.wv.w"});
-      } else {
-        q.wkv = pack(hw, {n + ".attn.wk.w", n + ".attn.wv.w"});
-      }
+      q.wkv = pack(hw, {n + ".attn.wk.w", n + ".attn.wv.w"});  // tcgen05 path: V part stored transposed
       q.wo = pack(hw, {n + ".attn.wo.w"});
       q.gain = up(hw, n + ".norm.gain");
       q.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b");
@@ -475,12 +470,7 @@ class EngineT final : public Engine {
       EncL e;
       e.n1 = up(hw, n + ".n1.gain");
       e.n2 = up(hw, n + ".n2.gain");
-      if (tc_attn_) {
-        e.wqk = pack(hw, {n + ".attn.wq.w", n + ".attn.wk.w"});
-        e.wv = pack(hw, {n + ".attn.wv.w"});
-      } else {
-        e.wqkv = pack(hw, {n + ".attn.wq.w", n + ".attn.wk.w", n + ".attn.wv.w"});
-      }
+      e.wqkv = pack(hw, {n + ".attn.wq.w", n + ".attn.wk.w", n + ".attn.wv.w"});  // tcgen05 path: V transposed
       e.wo = pack(hw, {n + ".attn.wo.w"});
       if (enc_moe(c)) e.moe = pack_moe(hw, n + ".moe", n + ".n2.gain");
       else {
@@ -509,11 +499,11 @@ class EngineT final : public Engine {
       }
       dec_.push_back(e);
     }
-    if (tc_attn_) {  // all layers' cross K in one GEMM, all layers' cross V (transposed) in another
-      std::vector<std::string> xk, xv;
-      for (size_t i = 0; i < xkv.size(); i += 2) xk.push_back(xkv[i]), xv.push_back(xkv[i + 1]);
-      xk_w_ = pack(hw, xk);
-      xv_w_ = pack(hw, xv);
+    if (tc_attn_) {  // one GEMM: all layers' cross K, then all layers' cross V (stored transposed)
+      std::vector<std::string> kv;
+      for (size_t i = 0; i < xkv.size(); i += 2) kv.push_back(xkv[i]);
+      for (size_t i = 1; i < xkv.size(); i += 2) kv.push_back(xkv[i]);
+      xkv_w_ = pack(hw, kv);
     } else {
       xkv_w_ = pack(hw, xkv);  // all decoder layers' cross K|V in one GEMM
     }
@@ -651,6 +641,13 @@ class EngineT final : public Engine {
     e.vt_row_pos = row_pos;
     e.out_bf16 = 1;
     return e;
+  }
+  // split K|V GEMM: columns [0, vt_col0) to out (ldo), the rest transposed as in `vt`
+  static Epi split_epi(Epi vt, void* out, int ldo, int vt_col0) {
+    vt.out = out;
+    vt.ldo = ldo;
+    vt.vt_col0 = vt_col0;
+    return vt;
   }
   FmhaArgs fmha(int B, int max_q, const T* Q, long long q_rows, int ldq, const T* K, long long k_rows, int ldk,
                 int k_col0, const T* Vt, int vt_users, int vt_ld, const int32_t* vt_user, Seg q, Seg k, Seg o,
@@ -960,9 +957,9 @@ class EngineT final : public Engine {
       os.fixed_len = Nq;
       const double aflops = 4.0 * Nq * sg_.n_keys * d;
       if (tc_attn_) {
-        gemm(keys_, d, q.wk, sg_.n_keys, epi(kvl_, d, false));
-        gemm(keys_, d, q.wv, sg_.n_keys,
-             vt_epi(vt_q_, Lpad_, 0, dp<int32_t>(sg_.off_key_user), dp<int32_t>(sg_.off_key_pos), 0));
+        gemm(keys_, d, q.wkv, sg_.n_keys,
+             split_epi(vt_epi(vt_q_, Lpad_, 0, dp<int32_t>(sg_.off_key_user), dp<int32_t>(sg_.off_key_pos), 0), kvl_, d,
+                       d));
         FmhaArgs f = fmha(U, Nq, qproj_, first ? Nq : U * Nq, d, kvl_, sg_.n_keys, d, 0, vt_q_, U, Lpad_, nullptr,
                           qs, ks, os, aflops);
         launch_fmha_tc(f, st_);
@@ -993,8 +990,7 @@ class EngineT final : public Engine {
       s.stride = Tn;
       s.fixed_len = Tn;
       if (tc_attn_) {
-        gemm(xn_, d, l.wqk, R, epi(qkv_, 2 * d, false));
-        gemm(xn_, d, l.wv, R, vt_epi(vt_enc_, Tpad_, Tn, nullptr, nullptr, 0));
+        gemm(xn_, d, l.wqkv, R, split_epi(vt_epi(vt_enc_, Tpad_, Tn, nullptr, nullptr, 0), qkv_, 2 * d, 2 * d));
         FmhaArgs f = fmha(U, Tn, qkv_, R, 2 * d, qkv_, R, 2 * d, d, vt_enc_, U, Tpad_, nullptr, s, s, s,
                           4.0 * U * Tn * Tn * d);
         launch_fmha_tc(f, st_);
@@ -1163,9 +1159,10 @@ class EngineT final : public Engine {
     const int d = cfg_.d_model, Tn = enc_seq_len(cfg_);
     if constexpr (kBf16) launch_convert<T>(U * Tn, d, z_, d, zt_, d, st_);
     if (tc_attn_) {  // cross K of every decoder layer [rows][Ld*d]; cross V transposed per layer
-      gemm(zt_, d, xk_w_, U * Tn, epi(xkv_, xk_w_.N, false));
-      gemm(zt_, d, xv_w_, U * Tn,
-           vt_epi(vt_x_, Tpad_, Tn, nullptr, nullptr, static_cast<long long>(maxU_) * d * Tpad_));
+      const int kn = xkv_w_.N / 2;  // K of all layers | V of all layers
+      gemm(zt_, d, xkv_w_, U * Tn,
+           split_epi(vt_epi(vt_x_, Tpad_, Tn, nullptr, nullptr, static_cast<long long>(maxU_) * d * Tpad_), xkv_, kn,
+                     kn));
     } else {
       gemm(zt_, d, xkv_w_, U * Tn, epi(xkv_, xkv_w_.N, false));
     }
@@ -1610,7 +1607,7 @@ class EngineT final : public Engine {
   std::vector<QBlock> qblocks_;
   std::vector<EncL> enc_;
   std::vector<DecL> dec_;
-  Lin<T> xkv_w_, xk_w_, xv_w_;
+  Lin<T> xkv_w_;
   bool tc_attn_ = false;
   int Tpad_ = 0, Lpad_ = 0;
   T *vt_enc_ = nullptr, *vt_q_ = nullptr, *vt_x_ = nullptr;

@@ -136,10 +136,10 @@ __device__ __forceinline__ void epi_finish32(const Epi& e, int orow, float rs, i
     for (int j = 0; j < 32; ++j) v[j] += r[j];
   }
   const int oc = col0 + e.col_off;
-  if (e.vt) {  // transposed bf16 store: lanes (consecutive rows) write consecutive t
+  if (e.vt && oc >= e.vt_col0) {  // transposed bf16 store: lanes (consecutive rows) write consecutive t
     const int u = e.vt_row_user ? e.vt_row_user[orow] : orow / e.vt_T;
     const int t = e.vt_row_pos ? e.vt_row_pos[orow] : orow % e.vt_T;
-    const int l = oc / e.vt_cols, m0 = oc - l * e.vt_cols;  // a 32-column chunk stays in one layer (vt_cols % 32 == 0)
+    const int l = (oc - e.vt_col0) / e.vt_cols, m0 = (oc - e.vt_col0) - l * e.vt_cols;  // a 32-column chunk stays in one layer (vt_cols % 32 == 0)
     __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(e.vt) + (long long)u * e.vt_user_stride + t +
                           (long long)l * e.vt_layer_stride + (long long)m0 * e.vt_ld;
 #pragma unroll
@@ -383,6 +383,38 @@ __device__ __forceinline__ void epilogue_tile_swiglu_staged(const Epi& e, float*
             make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
     }
     __syncwarp();
+  }
+}
+
+// Transposed-V tile of a split K|V GEMM (columns >= vt_col0): per 32-column
+// chunk, lanes (consecutive rows = consecutive key positions) store column j's
+// 64-byte run of positions, one column per instruction.
+template <int BN>
+__device__ __forceinline__ void epilogue_tile_vt(const Epi& e, uint32_t tb, int row, int nt, int half, uint64_t* tfull,
+                                                 uint32_t acc_phase) {
+  constexpr int CH = BN / 32 / 2;
+  const bool valid = row < e.m_valid;
+  int u = 0, t = 0;
+  if (valid) {
+    u = e.vt_row_user ? e.vt_row_user[row] : row / e.vt_T;
+    t = e.vt_row_pos ? e.vt_row_pos[row] : row % e.vt_T;
+  }
+  mbar_wait(tfull, acc_phase);
+  __syncwarp();
+  tc_fence_after();
+#pragma unroll 1
+  for (int i = 0; i < CH; ++i) {
+    const int c = half * CH + i;
+    uint32_t ra[32];
+    tmem_ld32_async(tb + c * 32, ra);
+    tmem_wait_ld();
+    if (!valid) continue;
+    const int oc = nt * BN + c * 32 + e.col_off - e.vt_col0;
+    const int l = oc / e.vt_cols, m0 = oc - l * e.vt_cols;
+    __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(e.vt) + (long long)u * e.vt_user_stride + t +
+                          (long long)l * e.vt_layer_stride + (long long)m0 * e.vt_ld;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) base[(long long)j * e.vt_ld] = __float2bfloat16_rn(__uint_as_float(ra[j]));
   }
 }
 
@@ -650,7 +682,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (grp.tile_expert && grp.tile_expert[mt] < 0) continue;
       const int row = mt * PM + static_cast<int>(rank) * kBM + q * 32 + lane;
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-      if constexpr (EPI == (EPI_SWIGLU | EPI_BF16))
+      if constexpr (EPI == (EPI_SPLITVT | EPI_BF16)) {
+        if (nt * BN >= epi.vt_col0)
+          epilogue_tile_vt<BN>(epi, tb, row, nt, half, &tfull[acc], acc_phase);
+        else
+          epilogue_tile_staged<BN, EPI_BF16>(epi, stg, tb, row, nt, half, &tfull[acc], acc_phase);
+      } else if constexpr (EPI == (EPI_SWIGLU | EPI_BF16))
         epilogue_tile_swiglu_staged<BN>(epi, stg, tb, row, nt, half, &tfull[acc], acc_phase);
       else if constexpr (EPI >= 0)
         epilogue_tile_staged<BN, EPI>(epi, stg, tb, row, nt, half, &tfull[acc], acc_phase);
@@ -850,6 +887,13 @@ void launch_tc2_mode(int staged, const void* A, int lda, const void* B, int ldb,
     case EPI_BIAS | EPI_SILU | EPI_BF16:
       launch_tc2<BN, S, EPI_BIAS | EPI_SILU | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream);
       return;
+    case EPI_SPLITVT | EPI_BF16:
+      if constexpr (BN == 256) {
+        launch_tc2<BN, S, EPI_SPLITVT | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+        return;
+      }
+      launch_tc2<BN, SG, -1>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+      return;
     case EPI_SWIGLU | EPI_BF16:
       if constexpr (BN == 256) {
         launch_tc2<BN, S, EPI_SWIGLU | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream);
@@ -868,7 +912,11 @@ int epi_mode(const Epi& e) {
   const bool plain = !e.bias && !e.act && !e.row_scale && !e.resid;
   // transposed V store: generic path (its per-column stores are already coalesced
   // across lanes; a SMEM-transposed variant measured slower)
-  if (e.vt) return -1;
+  if (e.vt)  // split K|V GEMM: staged bf16 tiles below vt_col0, transposed tiles above
+    return plain && !e.swiglu && !e.row_map && e.out_bf16 && e.vt_col0 > 0 && e.out &&
+                   reinterpret_cast<uintptr_t>(e.out) % 16 == 0 && e.ldo % 8 == 0 && e.col_off == 0
+               ? EPI_SPLITVT | EPI_BF16
+               : -1;
   const int esz = e.out_bf16 ? 2 : 4;
   if ((reinterpret_cast<uintptr_t>(e.out) % 16) || ((long long)e.ldo * esz) % 16 || (e.col_off * esz) % 16) return -1;
   if (e.resid && ((reinterpret_cast<uintptr_t>(e.resid) % 16) || (e.ld_resid % 4))) return -1;
@@ -985,7 +1033,7 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
   if (K % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0)
     throw std::invalid_argument("gemm_bf16: K and row strides must be multiples of 8");
   if (epi.swiglu && N % 256 != 0) throw std::invalid_argument("gemm_bf16: swiglu needs N % 256 == 0");
-  if (epi.vt && (epi.vt_cols % 32 != 0 || epi.col_off % 32 != 0))
+  if (epi.vt && (epi.vt_cols % 32 != 0 || epi.col_off % 32 != 0 || epi.vt_col0 % 32 != 0))
     throw std::invalid_argument("gemm_bf16: transposed store needs 32-column aligned layers");
   ProfScope ps(grp && grp->tile_expert ? PROF_GEMM_MOE : PROF_GEMM, stream,
                2.0 * (grp && grp->tile_expert ? double(grp->algo_rows) : double(M)) * N * K, 0.0);
@@ -1012,7 +1060,10 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
     }
     const int bn = small_n ? 128 : 256;
     // staged (coalesced) epilogue: specialised mode and every tile full
-    const int staged = (ep.mode >= 0 && ep.n_out >= (ep.swiglu ? N / 2 : N) && N % bn == 0) ? ep.mode : -1;
+    const int staged = (ep.mode >= 0 && ep.n_out >= (ep.swiglu ? N / 2 : N) && N % bn == 0 &&
+                        (!ep.vt || ep.vt_col0 % bn == 0))
+                           ? ep.mode
+                           : -1;
     if (small_n)
       launch_tc2_mode<128>(staged, A, lda, B, ldb, M, N, K, ep, grp, stream);
     else

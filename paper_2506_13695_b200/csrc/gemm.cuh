@@ -20,7 +20,8 @@ enum Act { ACT_NONE = 0, ACT_LEAKY = 1, ACT_SILU = 2 };
 // Epilogue mode bits (Epi::mode, set by the launcher): specialised code paths.
 enum EpiMode {
   EPI_BIAS = 1, EPI_LEAKY = 2, EPI_SILU = 4, EPI_RS = 8, EPI_RESID = 16, EPI_BF16 = 32,
-  EPI_SWIGLU = 64  // silu(a) * b over the interleaved W1|W3 accumulator (bf16 out, nothing else)
+  EPI_SWIGLU = 64,  // silu(a) * b over the interleaved W1|W3 accumulator (bf16 out, nothing else)
+  EPI_SPLITVT = 128  // bf16 out below Epi::vt_col0, transposed V store from it on (nothing else)
 };
 
 struct Epi {
@@ -46,6 +47,9 @@ struct Epi {
   long long vt_user_stride = 0, vt_layer_stride = 0;
   const int32_t* vt_row_user = nullptr;
   const int32_t* vt_row_pos = nullptr;
+  // columns >= vt_col0 take the transposed store (as column n - vt_col0);
+  // columns below it are regular bf16 stores to out / ldo (one GEMM for K|V)
+  int vt_col0 = 0;
   int mode = -1;  // EpiMode bits of a specialised path, -1 = generic (set by gemm_bf16)
 };
 

@@ -458,12 +458,18 @@ class EngineT final : public Engine {
       std::string n = "lifelong.block" + std::to_string(b);
       QBlock q;
       q.wq = pack(hw, {n + ".attn.wq.w"});
-      q.wkv = pack(hw, {n + ".attn.wk.w", n + ".attn.wv.w"});  // tcgen05 path: V part stored transposed
+      if (!tc_attn_) q.wkv = pack(hw, {n + ".attn.wk.w", n + ".attn.wv.w"});
       q.wo = pack(hw, {n + ".attn.wo.w"});
       q.gain = up(hw, n + ".norm.gain");
       q.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b");
       q.fc2 = pack(hw, {n + ".ffn.fc2.w"}, n + ".ffn.fc2.b");
       qblocks_.push_back(q);
+    }
+    if (tc_attn_ && c.lifelong_blocks > 0) {  // the keys are the same for every block: one K|V GEMM for all
+      std::vector<std::string> kv;
+      for (int b = 0; b < c.lifelong_blocks; ++b) kv.push_back("lifelong.block" + std::to_string(b) + ".attn.wk.w");
+      for (int b = 0; b < c.lifelong_blocks; ++b) kv.push_back("lifelong.block" + std::to_string(b) + ".attn.wv.w");
+      qkv_all_ = pack(hw, kv);
     }
     for (int l = 0; l < enc_layers(c); ++l) {
       std::string n = "enc" + std::to_string(l);
@@ -526,7 +532,8 @@ class EngineT final : public Engine {
     feat_ = ar_.alloc<T>(static_cast<size_t>(std::max<int64_t>(rec_max, U)) * std::max(Fp_, Sp_));
     hid_ = ar_.alloc<T>(static_cast<size_t>(std::max<int64_t>(rec_max, U)) * d);
     keys_ = ar_.alloc<T>(static_cast<size_t>(keys_max) * d);
-    kvl_ = ar_.alloc<T>(static_cast<size_t>(keys_max) * 2 * d);
+    const int nqb = std::max(c.lifelong_blocks, 1);
+    kvl_ = ar_.alloc<T>(static_cast<size_t>(keys_max) * std::max(2, nqb) * d);  // tcgen05: K of every QFormer block
     z_ = ar_.alloc<float>(static_cast<size_t>(rows_enc) * d);
     xn_ = ar_.alloc<T>(static_cast<size_t>(rows_big) * d);
     qkv_ = ar_.alloc<T>(static_cast<size_t>(rows_big) * 3 * d);
@@ -541,10 +548,10 @@ class EngineT final : public Engine {
       Tpad_ = rup(Tn, 8);
       Lpad_ = rup(std::max(c.lifelong_len, 1), 8);
       vt_enc_ = ar_.alloc<T>(static_cast<size_t>(U) * d * Tpad_);
-      vt_q_ = ar_.alloc<T>(static_cast<size_t>(U) * d * Lpad_);
+      vt_q_ = ar_.alloc<T>(static_cast<size_t>(nqb) * U * d * Lpad_);  // V^T of every QFormer block
       vt_x_ = ar_.alloc<T>(static_cast<size_t>(Ld) * U * d * Tpad_);
       CUDA_CHECK(cudaMemset(vt_enc_, 0, static_cast<size_t>(U) * d * Tpad_ * sizeof(T)));
-      CUDA_CHECK(cudaMemset(vt_q_, 0, static_cast<size_t>(U) * d * Lpad_ * sizeof(T)));
+      CUDA_CHECK(cudaMemset(vt_q_, 0, static_cast<size_t>(nqb) * U * d * Lpad_ * sizeof(T)));
       CUDA_CHECK(cudaMemset(vt_x_, 0, static_cast<size_t>(Ld) * U * d * Tpad_ * sizeof(T)));
     }
     h_ = ar_.alloc<float>(static_cast<size_t>(Rd_) * d);
@@ -957,11 +964,14 @@ class EngineT final : public Engine {
       os.fixed_len = Nq;
       const double aflops = 4.0 * Nq * sg_.n_keys * d;
       if (tc_attn_) {
-        gemm(keys_, d, q.wkv, sg_.n_keys,
-             split_epi(vt_epi(vt_q_, Lpad_, 0, dp<int32_t>(sg_.off_key_user), dp<int32_t>(sg_.off_key_pos), 0), kvl_, d,
-                       d));
-        FmhaArgs f = fmha(U, Nq, qproj_, first ? Nq : U * Nq, d, kvl_, sg_.n_keys, d, 0, vt_q_, U, Lpad_, nullptr,
-                          qs, ks, os, aflops);
+        const int nb = static_cast<int>(qblocks_.size());
+        const long long vt_layer = static_cast<long long>(maxU_) * d * Lpad_;
+        if (first)  // K of every block | V^T of every block, keys_ read once
+          gemm(keys_, d, qkv_all_, sg_.n_keys,
+               split_epi(vt_epi(vt_q_, Lpad_, 0, dp<int32_t>(sg_.off_key_user), dp<int32_t>(sg_.off_key_pos), vt_layer),
+                         kvl_, nb * d, nb * d));
+        FmhaArgs f = fmha(U, Nq, qproj_, first ? Nq : U * Nq, d, kvl_, sg_.n_keys, nb * d, static_cast<int>(b) * d,
+                          vt_q_ + b * vt_layer, U, Lpad_, nullptr, qs, ks, os, aflops);
         launch_fmha_tc(f, st_);
       } else {
         gemm(keys_, d, q.wkv, sg_.n_keys, epi(kvl_, 2 * d, false));
@@ -1607,7 +1617,7 @@ class EngineT final : public Engine {
   std::vector<QBlock> qblocks_;
   std::vector<EncL> enc_;
   std::vector<DecL> dec_;
-  Lin<T> xkv_w_;
+  Lin<T> xkv_w_, qkv_all_;
   bool tc_attn_ = false;
   int Tpad_ = 0, Lpad_ = 0;
   T *vt_enc_ = nullptr, *vt_q_ = nullptr, *vt_x_ = nullptr;

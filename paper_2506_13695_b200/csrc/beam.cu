@@ -244,18 +244,16 @@ __global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows,
         }
         const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (xs[e] >= tx) {
-            if (n < kLaneSlots) {
-              sx[n] = xs[e];
-              si[n] = 4 * i + e;
-            } else {
-              over = true;
-            }
-            ++n;
-          } else {
-            rej = fmaxf(rej, xs[e]);
+        for (int e = 0; e < 4; ++e) {  // branch-free append (predicated stores, no reconvergence per element)
+          const bool take = xs[e] >= tx;
+          const bool fits = n < kLaneSlots;
+          if (take && fits) {
+            sx[n] = xs[e];
+            si[n] = 4 * i + e;
           }
+          over |= take && !fits;
+          n += take ? 1 : 0;
+          rej = take ? rej : fmaxf(rej, xs[e]);
         }
       }
     }

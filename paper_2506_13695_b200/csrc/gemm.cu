@@ -399,6 +399,13 @@ __device__ __forceinline__ void epilogue_tile_vt(const Epi& e, uint32_t tb, int 
     u = e.vt_row_user ? e.vt_row_user[row] : row / e.vt_T;
     t = e.vt_row_pos ? e.vt_row_pos[row] : row % e.vt_T;
   }
+  const int lane = threadIdx.x & 31;
+  // 32 consecutive positions of one user starting at an even t0: lane pairs
+  // swap values so each lane stores two positions of one column (4 bytes),
+  // two columns per instruction, 16 stores per chunk instead of 32
+  const int u0 = __shfl_sync(0xffffffffu, u, 0), t0 = __shfl_sync(0xffffffffu, t, 0);
+  const bool pairs = __all_sync(0xffffffffu, valid && u == u0 && t == t0 + lane) && (t0 & 1) == 0;
+  const bool odd = lane & 1;
   mbar_wait(tfull, acc_phase);
   __syncwarp();
   tc_fence_after();
@@ -408,6 +415,19 @@ __device__ __forceinline__ void epilogue_tile_vt(const Epi& e, uint32_t tb, int 
     uint32_t ra[32];
     tmem_ld32_async(tb + c * 32, ra);
     tmem_wait_ld();
+    if (pairs) {
+      const int oc = nt * BN + c * 32 + e.col_off - e.vt_col0;
+      const int l = oc / e.vt_cols, m0 = oc - l * e.vt_cols;
+      __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(e.vt) + (long long)u0 * e.vt_user_stride + t0 +
+                            (lane & ~1) + (long long)l * e.vt_layer_stride + (long long)(m0 + odd) * e.vt_ld;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float vj = __uint_as_float(ra[j]), vj1 = __uint_as_float(ra[j + 1]);
+        const float recv = __shfl_xor_sync(0xffffffffu, odd ? vj : vj1, 1);
+        *reinterpret_cast<uint32_t*>(base + (long long)j * e.vt_ld) = odd ? pack_bf16(recv, vj1) : pack_bf16(vj, recv);
+      }
+      continue;
+    }
     if (!valid) continue;
     const int oc = nt * BN + c * 32 + e.col_off - e.vt_col0;
     const int l = oc / e.vt_cols, m0 = oc - l * e.vt_cols;

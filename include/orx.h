@@ -163,6 +163,15 @@ int orx_score_prefixes(orx_engine* e, const orx_user_batch* batch, int32_t n, co
 /* encode + unconstrained beam search of depth n_code_layers, batched. */
 int orx_beam_search(orx_engine* e, const orx_user_batch* batch, int32_t width, orx_beam_out* out);
 
+/* Pipelined serving form of orx_beam_search (same results): submit stages the
+ * batch (host packing + H2D on a copy stream) and launches its search without
+ * waiting; collect blocks for the OLDEST submitted request and writes its
+ * beams into `out` (layout of orx_beam_search). At most two requests are in
+ * flight (one per staging slot), so request i+1's host packing and H2D overlap
+ * request i's device work. A third submit before a collect fails (EINVAL). */
+int orx_beam_search_submit(orx_engine* e, const orx_user_batch* batch, int32_t width);
+int orx_beam_search_collect(orx_engine* e, orx_beam_out* out);
+
 /* Semantic-ID trie (SemanticTrie, trie.hpp:27-62) as CSR over prefix nodes:
  * node 0 is the root, node n's children are entries [child_off[n],
  * child_off[n+1]) of child_code (strictly ascending) / child_node. Uploaded

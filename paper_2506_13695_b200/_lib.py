@@ -116,6 +116,8 @@ SIGNATURES = [
     ("orx_next_logits", C.c_int, [_P, _F32P, C.c_int32, C.c_int32, _I32P, _I32P, _I32P, _F32P]),
     ("orx_score_prefixes", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, _I32P, _I32P, _I32P, _F32P]),
     ("orx_beam_search", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, C.POINTER(orx_beam_out)]),
+    ("orx_beam_search_submit", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32]),
+    ("orx_beam_search_collect", C.c_int, [_P, C.POINTER(orx_beam_out)]),
     ("orx_engine_set_trie", C.c_int, [_P, C.POINTER(orx_trie)]),
     ("orx_beam_search_constrained", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, C.POINTER(orx_beam_out)]),
     ("orx_sequence_log_prob", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, _I32P, _I32P,

@@ -271,6 +271,22 @@ int orx_beam_search(orx_engine* e, const orx_user_batch* batch, int32_t width, o
   });
 }
 
+int orx_beam_search_submit(orx_engine* e, const orx_user_batch* batch, int32_t width) {
+  return guarded([&] {
+    need(e, "engine");
+    need(batch, "batch");
+    e->e->submit_beam(*batch, width);
+  });
+}
+
+int orx_beam_search_collect(orx_engine* e, orx_beam_out* out) {
+  return guarded([&] {
+    need(e, "engine");
+    need(out, "out");
+    e->e->collect(out);
+  });
+}
+
 int orx_engine_set_trie(orx_engine* e, const orx_trie* t) {
   return guarded([&] {
     need(e, "engine");

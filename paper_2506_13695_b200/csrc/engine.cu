@@ -290,11 +290,17 @@ class EngineT final : public Engine {
   ~EngineT() override {
     cudaSetDevice(dev_);
     cudaStreamSynchronize(st_);
-    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    for (auto& g : graphs_) cudaGraphExecDestroy(g.exec);
     if (comm_) nccl().CommDestroy(comm_);
     if (h_ep_) cudaFreeHost(h_ep_);
-    if (host_stage_) cudaFreeHost(host_stage_);
-    if (host_out_) cudaFreeHost(host_out_);
+    for (int k = 0; k < 2; ++k) {
+      if (host_stage_[k]) cudaFreeHost(host_stage_[k]);
+      if (host_out_[k]) cudaFreeHost(host_out_[k]);
+      cudaEventDestroy(h2d_done_[k]);
+      cudaEventDestroy(dev_free_[k]);
+      cudaEventDestroy(out_ready_[k]);
+    }
+    cudaStreamDestroy(cs_);
     cudaStreamDestroy(st_);
   }
 
@@ -620,8 +626,14 @@ class EngineT final : public Engine {
         CUDA_CHECK(cudaMallocHost(&h_ep_, (static_cast<size_t>(ep_world_) * E + up) * sizeof(int32_t)));
       }
     }
-    // user batch staging (device side); host side is pinned and grown on demand
-    stage_cap_ = 0;
+    // user batch staging: two slots (pinned host + device), grown on demand; a
+    // copy stream moves slot s while the compute stream still runs the other
+    CUDA_CHECK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      CUDA_CHECK(cudaEventCreateWithFlags(&h2d_done_[k], cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventCreateWithFlags(&dev_free_[k], cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventCreateWithFlags(&out_ready_[k], cudaEventDisableTiming));
+    }
   }
 
   // ------------------------------------------------------------------------
@@ -716,7 +728,8 @@ class EngineT final : public Engine {
     // the per-record checks run inside the packers
     if (!offsets_ok(c, b)) validate_batch(c, b);  // raises the first error in reference order
     require(b.n_users >= 1 && b.n_users <= maxU_, "batch size outside the engine capacity");
-    CUDA_CHECK(cudaStreamSynchronize(st_));  // previous copy out of the pinned stage has finished
+    const int ss = stage_slot_ ^ 1;  // the slot not used by the most recent request
+    CUDA_CHECK(cudaEventSynchronize(h2d_done_[ss]));  // its previous H2D has read the pinned buffer
     const auto t_synced = std::chrono::steady_clock::now();
     CUDA_CHECK(cudaSetDevice(dev_));
     Stage s;
@@ -758,13 +771,13 @@ class EngineT final : public Engine {
       s.off_map[p] = take(4 * n);
     }
     s.bytes = off;
-    if (s.bytes > stage_cap_) {
-      if (host_stage_) cudaFreeHost(host_stage_);
-      CUDA_CHECK(cudaMallocHost(&host_stage_, s.bytes));
-      dev_stage_ = ar_.alloc<uint8_t>(s.bytes);
-      stage_cap_ = s.bytes;
+    if (s.bytes > stage_cap_[ss]) {
+      if (host_stage_[ss]) cudaFreeHost(host_stage_[ss]);
+      CUDA_CHECK(cudaMallocHost(&host_stage_[ss], s.bytes));
+      dev_stage_[ss] = ar_.alloc<uint8_t>(s.bytes);
+      stage_cap_[ss] = s.bytes;
     }
-    uint8_t* H = static_cast<uint8_t*>(host_stage_);
+    uint8_t* H = static_cast<uint8_t*>(host_stage_[ss]);
     auto I32 = [&](size_t o) { return reinterpret_cast<int32_t*>(H + o); };
     auto F32 = [&](size_t o) { return reinterpret_cast<float*>(H + o); };
     for (int u = 0; u < s.U; ++u) {
@@ -855,24 +868,30 @@ class EngineT final : public Engine {
               ms(t_enter, t_synced), ms(t_synced, t_pack0), n_workers, ms(t_pack0, now));
     }
     const auto t_copy0 = std::chrono::steady_clock::now();
-    CUDA_CHECK(cudaMemcpyAsync(dev_stage_, host_stage_, s.bytes, cudaMemcpyHostToDevice, st_));
+    // copy stream: wait until the compute stream no longer reads this slot, copy, and
+    // make the compute stream wait for the copy (the other slot's work overlaps it)
+    CUDA_CHECK(cudaStreamWaitEvent(cs_, dev_free_[ss], 0));
+    CUDA_CHECK(cudaMemcpyAsync(dev_stage_[ss], host_stage_[ss], s.bytes, cudaMemcpyHostToDevice, cs_));
+    CUDA_CHECK(cudaEventRecord(h2d_done_[ss], cs_));
+    CUDA_CHECK(cudaStreamWaitEvent(st_, h2d_done_[ss], 0));
     if (timing) {
       const auto t1 = std::chrono::steady_clock::now();
-      CUDA_CHECK(cudaStreamSynchronize(st_));
+      CUDA_CHECK(cudaStreamSynchronize(cs_));
       const auto t2 = std::chrono::steady_clock::now();
       auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
       cudaPointerAttributes pa{};
-      cudaPointerGetAttributes(&pa, host_stage_);
+      cudaPointerGetAttributes(&pa, host_stage_[ss]);
       fprintf(stderr, "stage: H2D %zu B issue %.3f ms, complete %.3f ms (host type %d)\n", s.bytes, ms(t_copy0, t1),
               ms(t1, t2), int(pa.type));
     }
     h2d_bytes += static_cast<int64_t>(s.bytes);
     sg_ = s;
+    stage_slot_ = ss;
     staged_ = true;
   }
   template <class X>
   const X* dp(size_t off) const {
-    return reinterpret_cast<const X*>(dev_stage_ + off);
+    return reinterpret_cast<const X*>(dev_stage_[stage_slot_] + off);
   }
   RecordsDev recs(int p) const {
     RecordsDev r;
@@ -1317,15 +1336,19 @@ class EngineT final : public Engine {
     }
   }
 
-  void run_beam(int width, orx_beam_out* out, bool constrained) {
+  // Launch the staged request's beam search (CUDA graph replay when shapes
+  // repeat) and enqueue the D2H of its result into the slot's pinned bounce
+  // buffer; the result is read by collect().
+  void launch_beam(int width, bool constrained, bool want_out) {
     CUDA_CHECK(cudaSetDevice(dev_));
     const orx_config& c = cfg_;
     require(width >= 1, "generation width must be >= 1");  // validate_request, generation.cpp:35
     require(width <= maxW_, "beam width above the engine capacity");
+    require(staged_, "no user batch staged");
     const int U = sg_.U, V = c.codebook_size, L = c.n_code_layers;
     // The whole encode + decode + prune sequence is replayed from a CUDA graph
-    // when the request has the same shapes as the captured one (no host work
-    // or launch gaps between its ~260 kernels); expert-parallel engines (host
+    // when the request has the same shapes as a captured one (no host work
+    // or launch gaps between its ~250 kernels); expert-parallel engines (host
     // sync per MoE layer) and profiling runs launch directly.
     const bool graphs = ep_world_ == 1 && !prof_enabled() && !getenv("ORX_NO_GRAPH");
     int n_live = 1;
@@ -1333,10 +1356,15 @@ class EngineT final : public Engine {
     int cur = L % 2;
     if (graphs) {
       const GraphKey key{U, width, constrained, {sg_.n_rec[0], sg_.n_rec[1], sg_.n_rec[2]}, sg_.n_keys,
-                         sg_.n_pad_keys, dev_stage_};
-      if (!graph_exec_ || !(key == graph_key_)) {
-        if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-        graph_exec_ = nullptr;
+                         sg_.n_pad_keys, dev_stage_[stage_slot_]};
+      CachedGraph* hit = nullptr;
+      for (auto& g : graphs_)
+        if (g.key == key) hit = &g;
+      if (!hit) {
+        if (graphs_.size() >= 4) {  // small LRU: one graph per staging slot and shape
+          cudaGraphExecDestroy(graphs_.front().exec);
+          graphs_.erase(graphs_.begin());
+        }
         cudaGraph_t g = nullptr;
         CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
         try {
@@ -1353,53 +1381,108 @@ class EngineT final : public Engine {
         CUDA_CHECK(cudaGraphGetNodes(g, nullptr, &n_nodes));
         std::vector<cudaGraphNode_t> nodes(n_nodes);
         if (n_nodes) CUDA_CHECK(cudaGraphGetNodes(g, nodes.data(), &n_nodes));
-        graph_kernels_ = 0;
+        long long kernels = 0;
         for (cudaGraphNode_t nd : nodes) {
           cudaGraphNodeType t;
           CUDA_CHECK(cudaGraphNodeGetType(nd, &t));
-          if (t == cudaGraphNodeTypeKernel) ++graph_kernels_;
+          if (t == cudaGraphNodeTypeKernel) ++kernels;
         }
-        CUDA_CHECK(cudaGraphInstantiate(&graph_exec_, g, 0));
+        CachedGraph cg;
+        cg.key = key;
+        cg.kernels = kernels;
+        CUDA_CHECK(cudaGraphInstantiate(&cg.exec, g, 0));
         cudaGraphDestroy(g);
-        graph_key_ = key;
-        launch_counter() -= graph_kernels_;  // capture itself launched nothing
+        graphs_.push_back(cg);
+        hit = &graphs_.back();
+        launch_counter() -= kernels;  // capture itself launched nothing
+      } else if (hit != &graphs_.back()) {  // keep LRU order
+        CachedGraph keep = *hit;
+        graphs_.erase(graphs_.begin() + (hit - graphs_.data()));
+        graphs_.push_back(keep);
+        hit = &graphs_.back();
       }
-      CUDA_CHECK(cudaGraphLaunch(graph_exec_, st_));
-      launch_counter() += graph_kernels_;
+      CUDA_CHECK(cudaGraphLaunch(hit->exec, st_));
+      launch_counter() += hit->kernels;
     } else {
       beam_body(width, constrained);
     }
+    CUDA_CHECK(cudaEventRecord(dev_free_[stage_slot_], st_));  // the staged inputs of this slot are consumed
     last_n_live_ = n_live;
     last_state_ = cur;
-    if (out) {
-      // pinned bounce buffer, then scatter into caller arrays (rows of width)
+    Pending pd;
+    pd.slot = stage_slot_;
+    pd.U = U;
+    pd.n_live = n_live;
+    pd.width = width;
+    pd.has_out = want_out;
+    if (want_out) {
       const size_t nc = static_cast<size_t>(U) * n_live * L, nl = static_cast<size_t>(U) * n_live;
-      size_t need = nc * 4 + nl * 8;
-      if (need > host_out_cap_) {
-        if (host_out_) cudaFreeHost(host_out_);
-        CUDA_CHECK(cudaMallocHost(&host_out_, need));
-        host_out_cap_ = need;
+      const size_t need = nc * 4 + nl * 8;
+      const int k = stage_slot_;
+      if (need > host_out_cap_[k]) {
+        CUDA_CHECK(cudaEventSynchronize(out_ready_[k]));
+        if (host_out_[k]) cudaFreeHost(host_out_[k]);
+        CUDA_CHECK(cudaMallocHost(&host_out_[k], need));
+        host_out_cap_[k] = need;
       }
-      uint8_t* ho = static_cast<uint8_t*>(host_out_);
+      uint8_t* ho = static_cast<uint8_t*>(host_out_[k]);
       CUDA_CHECK(cudaMemcpyAsync(ho, bs_[cur].codes, nc * 4, cudaMemcpyDeviceToHost, st_));
       CUDA_CHECK(cudaMemcpyAsync(ho + nc * 4, bs_[cur].score64, nl * 8, cudaMemcpyDeviceToHost, st_));
+      CUDA_CHECK(cudaEventRecord(out_ready_[k], st_));
       d2h_bytes += static_cast<int64_t>(need);
-      CUDA_CHECK(cudaStreamSynchronize(st_));
-      const int32_t* hc = reinterpret_cast<const int32_t*>(ho);
-      const double* hl = reinterpret_cast<const double*>(ho + nc * 4);
-      for (int u = 0; u < U; ++u) {
-        int n_u = n_live;  // constrained search: empty slots (log-prob -inf) sort last
-        while (n_u > 0 && std::isinf(hl[(size_t)u * n_live + n_u - 1])) --n_u;
-        if (out->n_items) out->n_items[u] = n_u;
-        for (int b = 0; b < width; ++b) {
-          for (int j = 0; j < L; ++j)
-            out->codes[((size_t)u * width + b) * L + j] = b < n_u ? hc[((size_t)u * n_live + b) * L + j] : -1;
-          out->log_prob[(size_t)u * width + b] = b < n_u ? hl[(size_t)u * n_live + b] : 0.0;
-        }
+    }
+    pending_.push_back(pd);
+  }
+
+  // Wait for the oldest launched request and scatter its beams (rows of width) into `out`.
+  void collect_beam(orx_beam_out* out) {
+    require(!pending_.empty(), "no beam search in flight");
+    const Pending pd = pending_.front();
+    pending_.erase(pending_.begin());
+    const int L = cfg_.n_code_layers;
+    if (!pd.has_out || !out) {
+      CUDA_CHECK(cudaEventSynchronize(dev_free_[pd.slot]));
+      CUDA_CHECK(cudaGetLastError());
+      return;
+    }
+    CUDA_CHECK(cudaEventSynchronize(out_ready_[pd.slot]));
+    CUDA_CHECK(cudaGetLastError());
+    const int U = pd.U, n_live = pd.n_live, width = pd.width;
+    const size_t nc = static_cast<size_t>(U) * n_live * L;
+    const uint8_t* ho = static_cast<const uint8_t*>(host_out_[pd.slot]);
+    const int32_t* hc = reinterpret_cast<const int32_t*>(ho);
+    const double* hl = reinterpret_cast<const double*>(ho + nc * 4);
+    for (int u = 0; u < U; ++u) {
+      int n_u = n_live;  // constrained search: empty slots (log-prob -inf) sort last
+      while (n_u > 0 && std::isinf(hl[(size_t)u * n_live + n_u - 1])) --n_u;
+      if (out->n_items) out->n_items[u] = n_u;
+      for (int b = 0; b < width; ++b) {
+        for (int j = 0; j < L; ++j)
+          out->codes[((size_t)u * width + b) * L + j] = b < n_u ? hc[((size_t)u * n_live + b) * L + j] : -1;
+        out->log_prob[(size_t)u * width + b] = b < n_u ? hl[(size_t)u * n_live + b] : 0.0;
       }
     }
+  }
+
+  void run_beam(int width, orx_beam_out* out, bool constrained) {
+    while (!pending_.empty()) collect_beam(nullptr);  // synchronous call: nothing else in flight
+    launch_beam(width, constrained, out != nullptr);
+    collect_beam(out);
     CUDA_CHECK(cudaStreamSynchronize(st_));
     CUDA_CHECK(cudaGetLastError());
+  }
+
+  // Pipelined serving: stage + launch request i+1 while request i runs; at
+  // most two in flight (one per staging slot).
+  void submit_beam(const orx_user_batch& b, int width) override {
+    require(pending_.size() < 2, "two beam searches already in flight: collect one first");
+    for (const Pending& p : pending_) require(p.has_out, "a staged-only search is in flight");
+    stage_batch(b);
+    launch_beam(width, false, true);
+  }
+  void collect(orx_beam_out* out) override {
+    require(out && out->codes && out->log_prob, "collect needs output arrays");
+    collect_beam(out);
   }
 
   // Teacher-forced logits. Queries are grouped by encoder row block; every
@@ -1640,10 +1723,7 @@ class EngineT final : public Engine {
   bool has_trie_ = false;
   double* seq_acc_ = nullptr;
   double* uni_ = nullptr;
-  cudaGraphExec_t graph_exec_ = nullptr;
   WorkerPool pool_{static_cast<int>(std::clamp(std::thread::hardware_concurrency(), 1u, 16u))};
-  long long graph_kernels_ = 0;
-  GraphKey graph_key_{};
   int32_t *tf_anc_, *tf_codes_, *grp_start_, *grp_len_, *grp_kstart_;
   int32_t *sel_ = nullptr, *slot_ = nullptr, *counts_ = nullptr, *cursor_ = nullptr, *tile_expert_ = nullptr,
           *n_mtiles_ = nullptr;
@@ -1657,12 +1737,26 @@ class EngineT final : public Engine {
   float *ws_ = nullptr, *wr_ = nullptr, *ys_ = nullptr, *yr_ = nullptr;
   int32_t *perm_ = nullptr, *all_counts_ = nullptr, *ep_up_ = nullptr, *h_ep_ = nullptr;
   // staging
-  void* host_stage_ = nullptr;
-  uint8_t* dev_stage_ = nullptr;
-  size_t stage_cap_ = 0;
+  void* host_stage_[2] = {nullptr, nullptr};
+  uint8_t* dev_stage_[2] = {nullptr, nullptr};
+  size_t stage_cap_[2] = {0, 0};
+  int stage_slot_ = 1;  // slot of the most recently staged batch (the first batch goes to slot 0)
+  cudaStream_t cs_ = nullptr;  // H2D copy stream
+  cudaEvent_t h2d_done_[2] = {}, dev_free_[2] = {}, out_ready_[2] = {};
   bool staged_ = false;
-  void* host_out_ = nullptr;
-  size_t host_out_cap_ = 0;
+  void* host_out_[2] = {nullptr, nullptr};
+  size_t host_out_cap_[2] = {0, 0};
+  struct Pending {
+    int slot, U, n_live, width;
+    bool has_out;
+  };
+  std::vector<Pending> pending_;
+  struct CachedGraph {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    long long kernels = 0;
+  };
+  std::vector<CachedGraph> graphs_;
   int last_n_live_ = 0, last_state_ = 0;
 };
 

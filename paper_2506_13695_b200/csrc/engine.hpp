@@ -26,6 +26,10 @@ class Engine {
   virtual void beam_search(int width, orx_beam_out* out) = 0;
   // Trie-constrained beam search (generation.cpp:58-64; needs set_trie).
   virtual void beam_search_constrained(int width, orx_beam_out* out) = 0;
+  // Pipelined serving: stage + launch a request without waiting (at most two
+  // in flight, one per staging slot); collect() returns the oldest one's beams.
+  virtual void submit_beam(const orx_user_batch& b, int width) = 0;
+  virtual void collect(orx_beam_out* out) = 0;
   // CSR trie (see TrieDev in beam.cuh), uploaded to the device.
   virtual void set_trie(int n_nodes, const int32_t* child_off, int64_t n_edges, const int32_t* child_code,
                         const int32_t* child_node) = 0;

@@ -357,6 +357,7 @@ class PolicyModel:
         self.cfg = weights.config()
         self.precision = precision
         self.max_users, self.max_width = max_users, max_width
+        self._pending = []  # (n_users, width) of submitted, not yet collected beam searches
         self._e = C.c_void_p()
         if ep is None or ep[1] == 1:
             check(lib().orx_engine_create(weights._h, device, PRECISION[precision], max_users, max_width,
@@ -492,6 +493,27 @@ class PolicyModel:
                            n_items.ctypes.data_as(C.POINTER(C.c_int32)))
         fn = lib().orx_beam_search_constrained if constrained else lib().orx_beam_search
         check(fn(self._e, C.byref(b.c), width, C.byref(out)))
+        return codes, logp, n_items
+
+    def beam_search_submit(self, users, width: int) -> None:
+        """Pipelined form of beam_search_arrays: stage + launch without waiting
+        (at most two in flight); beam_search_collect returns the oldest."""
+        b = _as_batch(users, self.cfg.n_code_layers)
+        check(lib().orx_beam_search_submit(self._e, C.byref(b.c), width))
+        self._pending.append((b.n_users, width))
+
+    def beam_search_collect(self):
+        if not self._pending:
+            raise ValueError("no beam search in flight")
+        n_users, width = self._pending[0]
+        L = self.cfg.n_code_layers
+        codes = np.empty((n_users, width, L), dtype=np.int32)
+        logp = np.empty((n_users, width), dtype=np.float64)
+        n_items = np.empty(n_users, dtype=np.int32)
+        out = orx_beam_out(codes.ctypes.data_as(C.POINTER(C.c_int32)), logp.ctypes.data_as(C.POINTER(C.c_double)),
+                           n_items.ctypes.data_as(C.POINTER(C.c_int32)))
+        check(lib().orx_beam_search_collect(self._e, C.byref(out)))
+        self._pending.pop(0)
         return codes, logp, n_items
 
     def generate_batch(self, users, req: GenerationRequest, trie: Optional[SemanticTrie] = None, seed: int = 0,

@@ -41,3 +41,36 @@ print("staged beam ms", t(lambda: check(lib().orx_beam_search_staged(e, 128, Non
 print("staged beam + out ms", t(lambda: check(lib().orx_beam_search_staged(e, 128, C.byref(out)))))
 print("full call ms", t(lambda: check(lib().orx_beam_search(e, C.byref(b.c), 128, C.byref(out)))))
 print("host cores", os.cpu_count())
+
+
+def pipelined(n=20):
+    check(lib().orx_beam_search_submit(e, C.byref(b.c), 128))
+    check(lib().orx_beam_search_collect(e, C.byref(out)))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    check(lib().orx_beam_search_submit(e, C.byref(b.c), 128))
+    for i in range(n):
+        if i + 1 < n:
+            check(lib().orx_beam_search_submit(e, C.byref(b.c), 128))
+        check(lib().orx_beam_search_collect(e, C.byref(out)))
+    return (time.perf_counter() - t0) * 1e3 / n
+
+
+def sync(n=20):
+    check(lib().orx_beam_search(e, C.byref(b.c), 128, C.byref(out)))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        check(lib().orx_beam_search(e, C.byref(b.c), 128, C.byref(out)))
+    return (time.perf_counter() - t0) * 1e3 / n
+
+
+def staged(n=20):
+    check(lib().orx_beam_search_staged(e, 128, None))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        check(lib().orx_beam_search_staged(e, 128, None))
+    return (time.perf_counter() - t0) * 1e3 / n
+
+
+for _ in range(2):
+    print(f"per request ms: staged only {staged():.3f}, synchronous {sync():.3f}, pipelined {pipelined():.3f}")

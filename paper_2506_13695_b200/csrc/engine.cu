@@ -172,6 +172,12 @@ __attribute__((target("clflushopt"))) void flush_lines(const void* p, size_t n) 
 void flush_lines(const void*, size_t) {}
 #endif
 
+// hashed (policy.cpp:14-17): id mod vocab in [0, vocab)
+inline int32_t host_hashed(int64_t id, int vocab) {
+  const int64_t m = id % vocab;
+  return static_cast<int32_t>(m < 0 ? m + vocab : m);
+}
+
 bool offsets_ok(const orx_config& cfg, const orx_user_batch& b) {
   const orx_records* rs[3] = {&b.short_seq, &b.positive_seq, &b.lifelong_seq};
   const int caps[3] = {cfg.short_len, cfg.positive_len, cfg.lifelong_len};
@@ -760,7 +766,7 @@ class EngineT final : public Engine {
     s.off_key_pos = take(4 * n_keys_total);
     for (int p = 0; p < 3; ++p) {
       size_t n = s.n_rec[p];
-      s.off_vid[p] = take(8 * n);
+      s.off_vid[p] = take(4 * n);  // hashed vid row index (policy.cpp:14-17), int32
       s.off_aid[p] = take(4 * n);
       s.off_tag[p] = take(4 * n);
       s.off_ts[p] = take(4 * n);
@@ -815,8 +821,14 @@ class EngineT final : public Engine {
         if (s.n_rec[p] == 0) continue;
         const int64_t i0 = r.offsets[u0], i1 = r.offsets[u1], n = i1 - i0;
         if (n == 0) continue;
-        memcpy(H + s.off_vid[p] + 8 * i0, r.vid + i0, 8 * n);
-        memcpy(H + s.off_aid[p] + 4 * i0, r.aid + i0, 4 * n);
+        // embedding-row indices hashed here (the 64-bit modulo per record
+        // was a third of the device feature kernel's instructions)
+        int32_t* vi = I32(s.off_vid[p]);
+        int32_t* ai = I32(s.off_aid[p]);
+        for (int64_t i = i0; i < i1; ++i) {
+          vi[i] = c.use_sid_history ? 0 : host_hashed(r.vid[i], c.vid_vocab);
+          ai[i] = host_hashed(r.aid[i], c.aid_vocab);
+        }
         memcpy(H + s.off_lab[p] + 4 * i0, r.labels + i0, 4 * n);
         float *tg = F32(s.off_tag[p]), *ts = F32(s.off_ts[p]), *pl = F32(s.off_play[p]), *du = F32(s.off_dur[p]);
         for (int64_t i = i0; i < i1; ++i) {
@@ -896,7 +908,7 @@ class EngineT final : public Engine {
   RecordsDev recs(int p) const {
     RecordsDev r;
     r.n = sg_.n_rec[p];
-    r.vid = dp<int64_t>(sg_.off_vid[p]);
+    r.vid = dp<int32_t>(sg_.off_vid[p]);
     r.aid = dp<int32_t>(sg_.off_aid[p]);
     r.tag = dp<float>(sg_.off_tag[p]);
     r.ts = dp<float>(sg_.off_ts[p]);

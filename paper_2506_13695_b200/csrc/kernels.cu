@@ -23,8 +23,8 @@ __global__ void features_kernel(RecordsDev r, FeatureTables t, T* __restrict__ o
   const int d = t.d, ad = t.aid_dim, mn = t.minor;
   const int F = t.vid_only ? d : d + ad + 5 * mn;
   for (int row = blockIdx.x; row < r.n; row += gridDim.x) {
-    const int vid = t.use_sid ? 0 : hashed(r.vid[row], t.vid_vocab);
-    const int aid = hashed(r.aid[row], t.aid_vocab);
+    const int vid = t.use_sid ? 0 : r.vid[row];  // indices hashed at staging
+    const int aid = r.aid[row];
     const float sc[4] = {r.tag[row], r.ts[row], r.play[row], r.dur[row]};
     const uint32_t lab = r.labels[row];
     T* o = out + (size_t)row * ldo;
@@ -94,8 +94,8 @@ __global__ void __launch_bounds__(256) features8_kernel(RecordsDev r, FeatureTab
   const int F = t.vid_only ? d : d + ad + 5 * mn;
   const int lane = threadIdx.x & 31;
   for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < r.n; row += gridDim.x * (blockDim.x >> 5)) {
-    const int vid = t.use_sid ? 0 : hashed(r.vid[row], t.vid_vocab);
-    const int aid = hashed(r.aid[row], t.aid_vocab);
+    const int vid = t.use_sid ? 0 : r.vid[row];  // indices hashed at staging
+    const int aid = r.aid[row];
     const float sc[4] = {r.tag[row], r.ts[row], r.play[row], r.dur[row]};
     const uint32_t lab = r.labels[row];
     T* o = out + (size_t)row * ldo;
@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(256, 4) features16_kernel(RecordsDev r, Featur
   }
   __syncthreads();
   for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < r.n; row += gridDim.x * (blockDim.x >> 5)) {
-    const int vid = hashed(r.vid[row], t.vid_vocab);
-    const int aid = hashed(r.aid[row], t.aid_vocab);
+    const int vid = r.vid[row];  // indices hashed at staging
+    const int aid = r.aid[row];
     const __nv_bfloat16* vrow = t.vid16 + (size_t)vid * d;
     const __nv_bfloat16* arow = t.aid16 + (size_t)aid * ad;
     __nv_bfloat16* o = out + (size_t)row * ldo;

@@ -10,8 +10,8 @@ namespace orx {
 
 struct RecordsDev {  // one pathway, all users, packed (device pointers)
   int n = 0;
-  const int64_t* vid = nullptr;
-  const int32_t* aid = nullptr;
+  const int32_t* vid = nullptr;  // hashed vid row index (host-side, policy.cpp:14-17)
+  const int32_t* aid = nullptr;  // hashed aid row index
   const float* tag = nullptr;
   const float* ts = nullptr;
   const float* play = nullptr;

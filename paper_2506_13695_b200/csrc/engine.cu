@@ -1076,19 +1076,27 @@ class EngineT final : public Engine {
     gemm(ffh_, cfg_.ffn_hidden, fc2, rows, e2);
   }
   // h += MoE(x)  (moe_forward, nn.cpp:117-172)
-  void moe(const MoeW& m, const T* x, int rows, float* h, const float* norm_gain) {
+  // post: when non-null the bf16 engine also writes the NEXT op's input from the
+  // updated h in the combine pass: RMSNorm(h) with gain `post_gain` into `post`,
+  // or a plain bf16 copy when post_gain is null. Returns whether it did.
+  bool moe(const MoeW& m, const T* x, int rows, float* h, const float* norm_gain, T* post = nullptr,
+           const float* post_gain = nullptr) {
     const orx_config& c = cfg_;
     const int d = c.d_model, E = c.n_experts, k = c.experts_active;
     CUDA_CHECK(cudaMemsetAsync(counts_, 0, E * sizeof(int32_t), st_));
     launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.gate_gain, m.bias, sel_, wts_, counts_, st_);
     if (ep_world_ > 1) {
       moe_ep(m, x, rows, h);
-      return;
+      return false;
     }
     launch_moe_plan(E, counts_, cursor_, tile_expert_, max_tiles_, n_mtiles_, kMoeTile, st_);
     launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xg_, row_scale_, st_);
     expert_ffn(m, static_cast<int>(S_), static_cast<long long>(rows) * k);
+    if constexpr (kBf16) {
+      if (post && launch_moe_combine_norm(rows, k, d, yg_, slot_, h, d, post_gain, post, d, st_)) return true;
+    }
     launch_moe_combine(rows, k, d, yg_, slot_, h, d, st_);
+    return false;
   }
 
   // Grouped expert FFNs over xg_ (expert per M tile: tile_expert_ / n_mtiles_):
@@ -1219,9 +1227,11 @@ class EngineT final : public Engine {
     const int d = c.d_model, H = c.n_heads, dh = d / H, Ld = dec_layers(c), Tn = enc_seq_len(c);
     launch_dec_embed(rows, d, step == 0 ? bos_ : tokens_[step - 1], step == 0 ? nullptr : codes + (step - 1),
                      code_stride, h_, st_);
+    bool have_x = false;  // xn_ already holds the next op's input (fused into the MoE combine)
     for (int l = 0; l < Ld; ++l) {
       const DecL& w = dec_[l];
-      launch_rmsnorm<T>(rows, d, h_, d, w.n1, xn_, d, st_);
+      if (!have_x) launch_rmsnorm<T>(rows, d, h_, d, w.n1, xn_, d, st_);
+      have_x = false;
       gemm(xn_, d, w.sqkv, rows, epi(qkv_, 3 * d, false));
       launch_dec_self_attn<T>(rows, d, H, step, l, Ld, qkv_, cache_ptrs_, anc, anc_stride, att_, st_);
       Epi e = epi(h_, d, true);
@@ -1242,12 +1252,14 @@ class EngineT final : public Engine {
       }
       gemm(att_, d, w.co, rows, e);
       launch_rmsnorm<T>(rows, d, h_, d, w.n3, xn_, d, st_);
-      if (c.moe_enabled) moe(w.moe, xn_, rows, h_, w.n3);
-      else ffn(w.fc1, w.fc2, xn_, rows, h_);
+      if (c.moe_enabled)  // next layer's n1 norm (or the head's bf16 copy) fused into the combine
+        have_x = moe(w.moe, xn_, rows, h_, w.n3, xn_, l + 1 < Ld ? dec_[l + 1].n1 : nullptr);
+      else
+        ffn(w.fc1, w.fc2, xn_, rows, h_);
     }
     (void)Tn;
     // position_logits: no final norm (policy.cpp:290-295)
-    launch_convert<T>(rows, d, h_, d, xn_, d, st_);
+    if (!have_x) launch_convert<T>(rows, d, h_, d, xn_, d, st_);
     gemm(xn_, d, heads_[step], rows, epi(logits_, c.codebook_size, true));
   }
 

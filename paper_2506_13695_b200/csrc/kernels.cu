@@ -1129,6 +1129,69 @@ void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32
   ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_scatter_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, rows, k, d, x, ldx, sel, wts,
                                                                                       cursor, slot, xg, row_scale));
 }
+// h += sum_j yg[slot[r][j]] (as moe_combine4_kernel, same order), then the
+// NEXT op's input from the updated row while it is in registers: the next
+// layer's RMSNorm (gain) or, for the head, a plain bf16 copy (gain null) —
+// as rmsnorm4_kernel / convert would compute it, one pass over h instead of two.
+template <int NC>
+__global__ void __launch_bounds__(256) moe_combine_norm_kernel(int rows, int k, int d, const float* __restrict__ yg,
+                                                               const int32_t* __restrict__ slot, float* __restrict__ h,
+                                                               int ldh, const float* __restrict__ gain,
+                                                               __nv_bfloat16* __restrict__ out, int ldo) {
+  pdl_begin();
+  const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  float4 v[NC];
+  float4* hr = reinterpret_cast<float4*>(h + (size_t)r * ldh);
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int c4 = lane + 32 * i;
+    float4 acc = __ldg(reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k] * d) + c4);
+    for (int j = 1; j < k; ++j) {
+      const float4 y = __ldg(reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k + j] * d) + c4);
+      acc.x += y.x, acc.y += y.y, acc.z += y.z, acc.w += y.w;
+    }
+    float4 hv = hr[c4];
+    hv.x += acc.x, hv.y += acc.y, hv.z += acc.z, hv.w += acc.w;
+    hr[c4] = hv;
+    v[i] = hv;
+  }
+  float rs = 1.f;
+  if (gain) {
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    ss = warp_sum(ss);
+    rs = rsqrtf(ss / d + 1e-6f);
+  }
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int c = (lane + 32 * i) * 4;
+    float a = v[i].x, b = v[i].y, cc = v[i].z, e = v[i].w;
+    if (gain) {
+      const float4 g4 = __ldg(reinterpret_cast<const float4*>(gain + c));
+      a = a * rs * g4.x, b = b * rs * g4.y, cc = cc * rs * g4.z, e = e * rs * g4.w;
+    }
+    *reinterpret_cast<uint2*>(out + (size_t)r * ldo + c) = make_uint2(pack_bf16(a, b), pack_bf16(cc, e));
+  }
+}
+
+bool launch_moe_combine_norm(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
+                             const float* gain, __nv_bfloat16* out, int ldo, cudaStream_t s) {
+  if ((d != 512 && d != 1024) || ldh % 4 || ldo % 4 || reinterpret_cast<uintptr_t>(h) % 16 ||
+      reinterpret_cast<uintptr_t>(out) % 16 || (gain && reinterpret_cast<uintptr_t>(gain) % 16) ||
+      getenv("ORX_NO_COMBINE_NORM"))
+    return false;
+  if (rows <= 0) return true;
+  if (d == 1024)
+    ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_combine_norm_kernel<8>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
+                                              slot, h, ldh, gain, out, ldo));
+  else
+    ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_combine_norm_kernel<4>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
+                                              slot, h, ldh, gain, out, ldo));
+  return true;
+}
+
 void launch_moe_combine(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
                         cudaStream_t s) {
   if (rows <= 0) return;

@@ -69,6 +69,11 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int n
 void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, const float* gain, const float* gate_t,
                       const float* gate_gain, const float* bias, int32_t* sel, float* wts, int32_t* counts,
                       cudaStream_t s);
+// bf16 engine: the MoE combine fused with the next op's input (RMSNorm with
+// `gain`, or a plain bf16 copy when gain is null); false if the shape is not
+// supported (then run launch_moe_combine + the norm / convert).
+bool launch_moe_combine_norm(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
+                             const float* gain, __nv_bfloat16* out, int ldo, cudaStream_t s);
 void launch_moe_plan(int E, const int32_t* counts, int32_t* seg_cursor, int32_t* tile_expert, int max_tiles,
                      int32_t* n_mtiles, int tile_rows, cudaStream_t s);
 template <class T>

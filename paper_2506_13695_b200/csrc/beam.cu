@@ -223,6 +223,9 @@ __global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows,
   float* sx = bx[w] + lane * kLaneSlots;
   int32_t* si = bi[w] + lane * kLaneSlots;
   float se = 0.f, rej = -FLT_MAX, mx = -FLT_MAX;
+  float2 se2 = make_float2(0.f, 0.f);
+  const float2 l2e2 = make_float2(1.4426950408889634f, 1.4426950408889634f);
+  const float2 nm2 = make_float2(-m0 * 1.4426950408889634f, -m0 * 1.4426950408889634f);
   int n = 0, total = 0;
   bool ok = false;
   for (int attempt = 0; attempt < 4; ++attempt) {
@@ -238,9 +241,11 @@ __global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows,
         const int i = i0 + 32 * u;
         if (i >= V4) continue;
         const float4 x = xb[u];
-        if (attempt == 0) {
+        if (attempt == 0) {  // packed: one FFMA2 per pair (log2 e and the sample max folded), SFU ex2, FADD2
           mx = fmaxf(mx, fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
-          se += (__expf(x.x - m0) + __expf(x.y - m0)) + (__expf(x.z - m0) + __expf(x.w - m0));
+          const float2 t01 = ffma2(make_float2(x.x, x.y), l2e2, nm2), t23 = ffma2(make_float2(x.z, x.w), l2e2, nm2);
+          se2 = fadd2(se2, make_float2(ex2_fast(t01.x), ex2_fast(t01.y)));
+          se2 = fadd2(se2, make_float2(ex2_fast(t23.x), ex2_fast(t23.y)));
         }
         const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -268,7 +273,7 @@ __global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows,
     tx = total < k_sel ? tx - 0.75f * sd : tx + 0.25f * sd;
     if (!(sd > 0.f)) break;
   }
-  se = warp_sum(se);
+  se = warp_sum(se2.x + se2.y);
   if (mx > m0 + 60.f) {  // the sample's max was far below the row's: exact sum in a second pass
     se = 0.f;
     for (int i = lane; i < V4; i += 32) {

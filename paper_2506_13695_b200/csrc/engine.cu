@@ -418,6 +418,69 @@ class EngineT final : public Engine {
   struct EncL { const float *n1, *n2; Lin<T> wqkv, wo, fc1, fc2; MoeW moe; };
   struct DecL { const float *n1, *n2, *n3; Lin<T> sqkv, so, cq, co, fc1, fc2; MoeW moe; };
 
+  // fc1 of a record pathway is linear in each feature section (policy.cpp:139-216):
+  //   features(r) . W1 = vid_row . W1[0:d] + aid_row . W1[d:d+ad]
+  //                    + sum_f (x_f w_f + b_f) . W1[sec_f] + sum_b lab_b label_b . W1[sec_lab]
+  // so the vid / aid products become [vocab][d] tables (two GEMMs over the
+  // bf16 tables, once per engine) and the scalar / label sections d-vectors
+  // (f64 on the host). The per-record fc1 GEMM and the n x 2.125d feature rows
+  // are replaced by a gather-add (launch_fold_features).
+  FoldTables build_fold(const HostWeights& hw, const std::string& n, const Mlp& m) {
+    const orx_config& c = cfg_;
+    const int d = c.d_model, ad = aid_dim(c), mn = minor_dim(c), nf = c.n_label_flags;
+    const Tensor& W = hw.get(n + ".fc1.w");  // [F][d] (in, out)
+    require(W.cols == d && W.rows == d + ad + 5 * mn && m.fc1.K >= d + ad, "fold: unexpected fc1 shape");
+    const int nvid = hw.get("emb.vid").rows, naid = hw.get("emb.aid").rows;
+    FoldTables f;
+    f.d = d;
+    f.n_flags = nf;
+    float* pv = ar_.alloc<float>(static_cast<size_t>(nvid) * d);
+    float* pa = ar_.alloc<float>(static_cast<size_t>(naid) * d);
+    Epi ev = epi(pv, d, true);
+    ev.n_out = d;
+    ev.m_valid = nvid;
+    gemm_bf16(t_vid16_, d, m.fc1.w, m.fc1.K, nvid, d, d, ev, nullptr, st_);
+    Epi ea = epi(pa, d, true);
+    ea.n_out = d;
+    ea.m_valid = naid;
+    gemm_bf16(t_aid16_, ad, m.fc1.w + d, m.fc1.K, naid, d, ad, ea, nullptr, st_);
+    std::vector<double> u(static_cast<size_t>(4) * d, 0.0), c0(d, 0.0), lab(static_cast<size_t>(nf) * d, 0.0);
+    auto axpy = [&](double a, int k, double* y) {
+      const float* r = W.data.data() + static_cast<size_t>(k) * d;
+      for (int j = 0; j < d; ++j) y[j] += a * r[j];
+    };
+    const char* sec[4] = {"emb.tag", "emb.ts", "emb.playtime", "emb.duration"};
+    for (int s = 0; s < 4; ++s) {
+      const Tensor& t = hw.get(sec[s]);  // [2][minor]: w row, b row
+      for (int j = 0; j < mn; ++j) {
+        axpy(t.data[j], d + ad + s * mn + j, u.data() + static_cast<size_t>(s) * d);
+        axpy(t.data[mn + j], d + ad + s * mn + j, c0.data());
+      }
+    }
+    const Tensor& L = hw.get("emb.label");  // [n_flags][minor]
+    for (int b = 0; b < nf; ++b)
+      for (int j = 0; j < mn; ++j)
+        axpy(L.data[static_cast<size_t>(b) * mn + j], d + ad + 4 * mn + j, lab.data() + static_cast<size_t>(b) * d);
+    const Tensor& bias = hw.get(n + ".fc1.b");
+    for (int j = 0; j < d; ++j) c0[j] += bias.data[j];
+    // every label combination (labels < 2^n_flags, policy.cpp:33) with the constant part folded in
+    std::vector<float> pl(static_cast<size_t>(d) << nf);
+    for (int m = 0; m < (1 << nf); ++m)
+      for (int j = 0; j < d; ++j) {
+        double acc = c0[j];
+        for (int b = 0; b < nf; ++b)
+          if ((m >> b) & 1) acc += lab[static_cast<size_t>(b) * d + j];
+        pl[static_cast<size_t>(m) * d + j] = static_cast<float>(acc);
+      }
+    std::vector<float> uf(u.begin(), u.end());
+    f.pv = pv;
+    f.pa = pa;
+    f.pl = upload_f32(pl.data(), pl.size());
+    f.u = upload_f32(uf.data(), uf.size());
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    return f;
+  }
+
   void upload(const HostWeights& hw) {
     const orx_config& c = cfg_;
     auto mlp = [&](const std::string& n) {
@@ -458,6 +521,15 @@ class EngineT final : public Engine {
     p_short_ = mlp("pathway.short");
     p_pos_ = mlp("pathway.positive");
     p_life_ = mlp("pathway.lifelong");
+    if constexpr (kBf16) {
+      fold_on_ = !c.use_sid_history && !c.vid_only_features && aid_dim(c) % 8 == 0 &&
+                 fold_features_supported(c.d_model, c.n_label_flags) && !getenv("ORX_NO_FEATURE_FOLD");
+      if (fold_on_) {
+        fold_[0] = build_fold(hw, "pathway.short", p_short_);
+        fold_[1] = build_fold(hw, "pathway.positive", p_pos_);
+        fold_[2] = build_fold(hw, "pathway.lifelong", p_life_);
+      }
+    }
     {  // lifelong.queries as a GEMM operand [Nq][d]
       const Tensor& q = hw.get("lifelong.queries");
       std::vector<T> h(q.data.size());
@@ -963,16 +1035,25 @@ class EngineT final : public Engine {
     const FeatureTables tb = tables();
     for (int p = 0; p < 2; ++p) {
       if (!sg_.n_rec[p]) continue;
+      if (fold_on_) {
+        if constexpr (kBf16) launch_fold_features(recs(p), fold_[p], hid_, d, st_);
+        fc2_into_z(p == 0 ? p_short_ : p_pos_, sg_.n_rec[p], dp<int32_t>(sg_.off_map[p]));
+        continue;
+      }
       launch_features<T>(recs(p), tb, feat_, Fp_, st_);
       mlp_into_z(p == 0 ? p_short_ : p_pos_, feat_, Fp_, sg_.n_rec[p], dp<int32_t>(sg_.off_map[p]));
     }
     // lifelong pathway -> keys (policy.cpp:233-238)
     if (sg_.n_rec[2]) {
-      launch_features<T>(recs(2), tb, feat_, Fp_, st_);
       const Mlp& m = p_life_;
-      Epi e1 = epi(hid_, d, false);
-      e1.act = ACT_LEAKY;
-      gemm(feat_, Fp_, m.fc1, sg_.n_rec[2], e1);
+      if (fold_on_) {
+        if constexpr (kBf16) launch_fold_features(recs(2), fold_[2], hid_, d, st_);
+      } else {
+        launch_features<T>(recs(2), tb, feat_, Fp_, st_);
+        Epi e1 = epi(hid_, d, false);
+        e1.act = ACT_LEAKY;
+        gemm(feat_, Fp_, m.fc1, sg_.n_rec[2], e1);
+      }
       Epi e2 = epi(keys_, d, false);
       e2.row_map = dp<int32_t>(sg_.off_map[2]);
       gemm(hid_, d, m.fc2, sg_.n_rec[2], e2);
@@ -1053,6 +1134,14 @@ class EngineT final : public Engine {
     }
   }
 
+  void fc2_into_z(const Mlp& m, int rows, const int32_t* map) {
+    const int d = cfg_.d_model;
+    Epi e2 = epi(z_, d, true);
+    e2.resid = z_;
+    e2.ld_resid = d;
+    e2.row_map = map;
+    gemm(hid_, d, m.fc2, rows, e2);
+  }
   void mlp_into_z(const Mlp& m, const T* x, int ldx, int rows, const int32_t* map) {
     const int d = cfg_.d_model;
     Epi e1 = epi(hid_, d, false);
@@ -1720,6 +1809,9 @@ class EngineT final : public Engine {
   std::vector<const float*> tokens_;
   std::vector<Lin<T>> heads_;
   Mlp p_static_, p_short_, p_pos_, p_life_;
+  // short / positive / lifelong fc1 folded through the feature tables (bf16)
+  FoldTables fold_[3];
+  bool fold_on_ = false;
   const T* queries_ = nullptr;
   std::vector<QBlock> qblocks_;
   std::vector<EncL> enc_;

@@ -226,6 +226,54 @@ __global__ void __launch_bounds__(256, 4) features16_kernel(RecordsDev r, Featur
   }
 }
 
+// Folded pathway first layer: G warps per record, each owning 256 columns
+// (two float4 per lane, 16-byte lane stride); the u vectors stay in registers
+// across the rows a warp visits, the Pv / Pa / Pl rows (L2-resident per
+// pathway) are gathered as float4. Replaces features16 + the fc1 GEMM
+// (n x 2.125d x d) per pathway.
+template <int G>
+__global__ void __launch_bounds__(256) fold_features_kernel(RecordsDev r, FoldTables f,
+                                                            __nv_bfloat16* __restrict__ out, int ldo) {
+  pdl_begin();
+  constexpr int RPB = 8 / G;  // records in flight per block
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d4 = f.d / 4, cg = warp % G, rl = warp / G;
+  const unsigned lmask = (1u << f.n_flags) - 1u;
+  int c4[2];
+  bool ok[2];
+  float4 u[4][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    c4[h] = cg * 64 + h * 32 + lane;
+    ok[h] = c4[h] < d4;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      u[s][h] = ok[h] ? __ldg(reinterpret_cast<const float4*>(f.u) + s * d4 + c4[h]) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int row = blockIdx.x * RPB + rl; row < r.n; row += gridDim.x * RPB) {
+    const float4* pv = reinterpret_cast<const float4*>(f.pv) + (size_t)r.vid[row] * d4;
+    const float4* pa = reinterpret_cast<const float4*>(f.pa) + (size_t)r.aid[row] * d4;
+    const float4* pl = reinterpret_cast<const float4*>(f.pl) + (size_t)(r.labels[row] & lmask) * d4;
+    float4 a[2], b[2], l[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (ok[h]) a[h] = __ldg(pv + c4[h]), b[h] = __ldg(pa + c4[h]), l[h] = __ldg(pl + c4[h]);
+    const float x0 = r.tag[row], x1 = r.ts[row], x2 = r.play[row], x3 = r.dur[row];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!ok[h]) continue;
+      float v[4];
+      v[0] = a[h].x + b[h].x + l[h].x + x0 * u[0][h].x + x1 * u[1][h].x + x2 * u[2][h].x + x3 * u[3][h].x;
+      v[1] = a[h].y + b[h].y + l[h].y + x0 * u[0][h].y + x1 * u[1][h].y + x2 * u[2][h].y + x3 * u[3][h].y;
+      v[2] = a[h].z + b[h].z + l[h].z + x0 * u[0][h].z + x1 * u[1][h].z + x2 * u[2][h].z + x3 * u[3][h].z;
+      v[3] = a[h].w + b[h].w + l[h].w + x0 * u[0][h].w + x1 * u[1][h].w + x2 * u[2][h].w + x3 * u[3][h].w;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = v[j] > 0.f ? v[j] : 0.01f * v[j];  // tape.hpp:88
+      *reinterpret_cast<uint2*>(out + (size_t)row * ldo + c4[h] * 4) = make_uint2(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]));
+    }
+  }
+}
+
 template <class T>
 __global__ void static_features_kernel(int U, const int32_t* uid, const int32_t* gender, const int32_t* age,
                                        const float* ue, const float* ge, const float* ae, int sd, int uv, int gv,
@@ -857,6 +905,22 @@ void launch_features(const RecordsDev& r, const FeatureTables& t, T* out, int ld
     return;
   }
   ORX_LAUNCH(launch_pdl(features_kernel<T>, grid_for(r.n, 1, 148 * 16), 256, 0, s, r, t, out, ldo));
+}
+bool fold_features_supported(int d, int n_flags) {
+  const int g = (d + 255) / 256;
+  return d % 4 == 0 && d <= 2048 && 8 % g == 0 && n_flags >= 0 && n_flags <= 8;
+}
+void launch_fold_features(const RecordsDev& r, const FoldTables& f, __nv_bfloat16* out, int ldo, cudaStream_t s) {
+  if (r.n <= 0) return;
+  if (!fold_features_supported(f.d, f.n_flags) || ldo % 4 != 0)
+    throw std::invalid_argument("fold_features: unsupported shape");
+  const int g = (f.d + 255) / 256, rpb = 8 / g;
+  const int grid = static_cast<int>(std::min<long long>((r.n + rpb - 1) / rpb, num_sms() * 3LL));  // 80 regs: 3 blocks per SM
+  auto go = [&](auto kern) { ORX_LAUNCH(launch_pdl(kern, grid, 256, 0, s, r, f, out, ldo)); };
+  if (g == 1) go(fold_features_kernel<1>);
+  else if (g == 2) go(fold_features_kernel<2>);
+  else if (g == 4) go(fold_features_kernel<4>);
+  else go(fold_features_kernel<8>);
 }
 template <class T>
 void launch_static_features(int U, const int32_t* uid, const int32_t* gender, const int32_t* age, const float* ue,

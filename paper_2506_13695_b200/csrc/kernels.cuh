@@ -38,6 +38,18 @@ struct FeatureTables {  // fp32 embedding tables (policy.cpp:139-198)
 
 template <class T>
 void launch_features(const RecordsDev& r, const FeatureTables& t, T* out, int ldo, cudaStream_t s);
+// Pathway first layer folded through the feature tables (bf16 engine, no sid
+// history): fc1(features(r)) = Pv[vid] + Pa[aid] + Pl[labels] + tag*u0 + ts*u1 +
+// play*u2 + dur*u3, LeakyReLU'd (policy.cpp:175-216).
+struct FoldTables {
+  const float* pv = nullptr;  // [vid_vocab][d] = emb.vid . W1[0:d]
+  const float* pa = nullptr;  // [aid_vocab][d] = emb.aid . W1[d:d+ad]
+  const float* pl = nullptr;  // [2^n_flags][d]: label multi-hot . W1[lab] + scalar-section b rows + fc1 bias
+  const float* u = nullptr;   // [4][d]: tag / ts / playtime / duration w rows through W1
+  int d = 0, n_flags = 0;
+};
+bool fold_features_supported(int d, int n_flags);
+void launch_fold_features(const RecordsDev& r, const FoldTables& f, __nv_bfloat16* out, int ldo, cudaStream_t s);
 template <class T>
 void launch_static_features(int U, const int32_t* uid, const int32_t* gender, const int32_t* age,
                             const float* uid_emb, const float* gender_emb, const float* age_emb, int sdim,

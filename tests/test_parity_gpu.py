@@ -293,3 +293,30 @@ def test_compress_lifelong_gpu(users, hist_len, dim, threshold, max_out):
         assert np.array_equal(got[f].astype(want.dtype), want), f
     n_rep = len(set(got["vid"].tolist()))
     print(f"compress {users} users x ~{hist_len} records (D={dim}): {len(got['vid'])} records, {n_rep} representatives")
+
+
+@pytest.mark.parametrize("d", [128, 1024])
+def test_bf16_feature_fold(d):
+    """bf16 engine: the pathway fc1 folded through the feature tables
+    (launch_fold_features) against the same engine with the explicit feature
+    rows + fc1 GEMM (ORX_NO_FEATURE_FOLD=1) and against the f64 reference."""
+    import os
+    over, sets = {}, []
+    if d != 128:
+        over = dict(d_model=d, n_heads=d // 128, ffn_hidden=2 * d)
+        sets = [f"d_model={d}", f"n_heads={d // 128}", f"ffn_hidden={2 * d}"]
+    lens = (20, 64, 300)
+    P, model = _model("0.015B", "bf16", max_users=2, max_width=32, **over)
+    _, refs = ref_dump("0.015B", 2, 32, lens=lens, sets=sets, beam=False, n_prefix=1)
+    batch = P.SynthBatch(1, 0, 2, *lens)
+    z = model.encode_batch(batch)
+    os.environ["ORX_NO_FEATURE_FOLD"] = "1"
+    try:
+        _, unf = _model("0.015B", "bf16", max_users=2, max_width=32, **over)
+    finally:
+        del os.environ["ORX_NO_FEATURE_FOLD"]
+    z_unf = unf.encode_batch(batch)
+    for u, ref in enumerate(refs):
+        ez, ez_unf, e_pair = rel_inf(z[u], ref["z"]), rel_inf(z_unf[u], ref["z"]), rel_inf(z[u], z_unf[u])
+        print(f"fold d={d} user {u}: z {ez:.3e} (unfolded {ez_unf:.3e}, fold vs unfolded {e_pair:.3e})")
+        assert ez < 5e-2 and ez <= 1.5 * ez_unf + 2e-3

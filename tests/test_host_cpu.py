@@ -161,6 +161,13 @@ def test_flops_model_matches_survey():
         got = [bench.flops_per_user(cfg, w, (20, 256, 2000))[0] / 1e9 for w in (32, 128, 512)]
         for g, w in zip(got, want):
             assert abs(g - w) / w < 0.01, (name, got, want)
+    # folded pathway fc1 (bf16 engine): the per-record fc1 GEMM leaves the count
+    cfg = P.PolicyConfig.preset("0.935B")
+    d, n = cfg.d_model, 20 + 256 + 2000
+    F = d + d // 2 + 5 * (d // 8)
+    full, _ = bench.flops_per_user(cfg, 128, (20, 256, 2000))
+    fold, _ = bench.flops_per_user(cfg, 128, (20, 256, 2000), fold_fc1=True)
+    assert abs((full - fold) - 2.0 * n * (F * d - 10 * d)) < 1.0
 
 
 def test_cpp_dropin_shim_builds_and_fails_loudly_without_gpu():

@@ -41,6 +41,24 @@ BASELINE_CONFIG = {"0.015B": 1, "0.121B": 2, "0.935B": 3, "2.633B": 4}
 PROF_NAMES = ["gemm_dense", "gemm_moe", "attention", "dec_self_attn", "moe_route", "beam_topk_merge", "other"]
 
 
+_JSON_OUT = None
+
+
+def quiet_stdout():
+    """Route fd 1 to stderr so native libraries' banners (NCCL's version line
+    under NCCL_DEBUG=VERSION) never precede the one JSON line on stdout."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line):
+    out = _JSON_OUT or sys.stdout
+    print(json.dumps(line), file=out, flush=True)
+
+
 def flops_per_user(cfg, width, lens, fold_fc1=False):
     """Algorithmic FLOPs per user, KV-cached minimum.
     fold_fc1: the pathway fc1 folded through the feature tables (bf16 engine),
@@ -190,7 +208,7 @@ def reference_arm(args, cfg, lens):
         "e2e": {"value": value, "unit": "users/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gflop_per_user": flops_u / 1e9, "wall_s": wall, "init_s": r["init_s"],
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
@@ -228,6 +246,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        quiet_stdout()
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     t_init = time.time()
@@ -399,7 +418,7 @@ def main():
             "roofline": roofline, "kernel_classes_ms_per_step": classes,
             "cpu_baseline": cpu, "clocks": clocks, "init_s": t_init,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

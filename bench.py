@@ -59,6 +59,57 @@ def emit(line):
     print(json.dumps(line), file=out, flush=True)
 
 
+class BenchConfig:
+    """Static copy of the preset dims bench.py needs (include/orx.h presets =
+    the reference PolicyConfig at PAPER.md:398-413), so the reference arm never
+    imports the package or loads liborx.so. tests/test_host_cpu.py checks it
+    against PolicyConfig.preset."""
+
+    BASE = dict(n_layers=4, d_model=128, ffn_hidden=256, n_heads=4, moe_enabled=False, n_experts=0,
+                experts_active=0, moe_location="decoder", expert_round_multiple=128, n_code_layers=3,
+                codebook_size=64, short_len=20, positive_len=256, lifelong_len=2000, n_queries=128,
+                lifelong_blocks=2, seed=123)
+    PRESETS = {
+        "0.015B": dict(n_layers=4, d_model=128, ffn_hidden=256, n_heads=4, codebook_size=8192),
+        "0.121B": dict(n_layers=8, d_model=1024, ffn_hidden=2048, n_heads=8, codebook_size=8192),
+        "0.935B": dict(n_layers=8, d_model=1024, ffn_hidden=2048, n_heads=8, codebook_size=8192, moe_enabled=True,
+                       n_experts=24, experts_active=2),
+        "2.633B": dict(n_layers=24, d_model=1024, ffn_hidden=2048, n_heads=8, codebook_size=8192, moe_enabled=True,
+                       n_experts=24, experts_active=4, moe_location="enc_and_dec"),
+    }
+
+    def __init__(self, name):
+        if name not in self.PRESETS:
+            raise ValueError(f"unknown preset {name}")
+        self.__dict__.update(self.BASE)
+        self.__dict__.update(self.PRESETS[name])
+
+    def enc_layers(self):
+        return self.n_layers // 2
+
+    def dec_layers(self):
+        return self.n_layers - self.n_layers // 2
+
+    def enc_seq_len(self):
+        return 1 + self.short_len + self.positive_len + self.n_queries
+
+    def expert_hidden(self):  # policy.cpp expert sizing: round_up((8 d + 2) / 3, multiple)
+        raw = (2 * 4 * self.d_model + 2) // 3
+        m = self.expert_round_multiple
+        return (raw + m - 1) // m * m
+
+
+def bench_config(args, cfg, lens, world):
+    """The `config` object, identical for both arms (the driver compares them)."""
+    return {"workload": f"OneRec-{args.config} (BASELINE config {BASELINE_CONFIG.get(args.config, '?')}): encoder + "
+                        f"{'MoE ' if cfg.moe_enabled else ''}decoder + depth-{cfg.n_code_layers} beam search, "
+                        f"W={args.width}, V={cfg.codebook_size}, {args.users} users/GPU "
+                        f"(short,positive,lifelong)={tuple(lens)}, random-init weights (seed {cfg.seed})",
+            "model": f"OneRec-{args.config}", "users_per_gpu": args.users, "global_batch": args.users * world,
+            "width": args.width, "lens": list(lens), "parallelism": f"dp{world}" + (f"xep{world}" if args.ep else ""),
+            "l2": "working set (weights ~2 GB + activations) exceeds the 126 MB L2; no flush"}
+
+
 def flops_per_user(cfg, width, lens, fold_fc1=False):
     """Algorithmic FLOPs per user, KV-cached minimum.
     fold_fc1: the pathway fc1 folded through the feature tables (bf16 engine),
@@ -201,9 +252,8 @@ def reference_arm(args, cfg, lens):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "users/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"OneRec-{args.config} encoder+decoder, beam search W={args.width} depth 3, "
-                               f"V={cfg.codebook_size}, users full-length {lens}",
-                   "users_per_gpu": args.users, "width": args.width, "lens": list(lens), "parallelism": "cpu"},
+        "config": bench_config(args, cfg, lens, args.gpus),
+        "parallelism_detail": f"reference C++ core, {r['procs']} single-threaded worker processes on host cores",
         "cpu_baseline": cpu_baseline_block(r, args.config, args.width),
         "e2e": {"value": value, "unit": "users/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gflop_per_user": flops_u / 1e9, "wall_s": wall, "init_s": r["init_s"],
@@ -231,13 +281,14 @@ def main():
     args.warmup = max(args.warmup, 3)
     lens = tuple(int(x) for x in args.lens.split(","))
 
-    import paper_2506_13695_b200 as P
-    from paper_2506_13695_b200._lib import check, lib, orx_beam_out
-    cfg = P.PolicyConfig.preset(args.config)
-
-    if args.impl == "reference":
+    cfg = BenchConfig(args.config)
+    if args.impl == "reference":  # never imports the package (no liborx.so in this process)
         reference_arm(args, cfg, lens)
         return
+
+    import paper_2506_13695_b200 as P
+    from paper_2506_13695_b200._lib import check, lib, orx_beam_out
+    pcfg = P.PolicyConfig.preset(args.config)
 
     import torch
     import torch.distributed as dist
@@ -254,10 +305,10 @@ def main():
     if ep:
         from paper_2506_13695_b200.dist import ep_unique_id
         uid = ep_unique_id(device=torch.device("cuda", local))
-        model = P.PolicyModel(weights=P.Weights.random_ep(cfg, rank, world), precision=args.precision, device=local,
+        model = P.PolicyModel(weights=P.Weights.random_ep(pcfg, rank, world), precision=args.precision, device=local,
                               max_users=args.users, max_width=args.width, ep=(rank, world, uid))
     else:
-        model = P.PolicyModel(cfg, precision=args.precision, device=local, max_users=args.users,
+        model = P.PolicyModel(pcfg, precision=args.precision, device=local, max_users=args.users,
                               max_width=args.width)
     t_init = time.time() - t_init
     from paper_2506_13695_b200.dist import shard_users
@@ -398,16 +449,10 @@ def main():
             "metric": METRIC, "value": value, "unit": "users/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16" if args.precision == "bf16" else "fp32", "data": "synthetic",
-            "config": {"workload": f"OneRec-{args.config} (BASELINE config {BASELINE_CONFIG.get(args.config, '?')}): encoder + "
-                                   f"{'MoE ' if cfg.moe_enabled else ''}decoder + depth-{L} beam search, "
-                                   f"W={args.width}, V={cfg.codebook_size}, {args.users} users/GPU "
-                                   f"(short,positive,lifelong)={lens}, random-init weights (seed {cfg.seed})",
-                       "model": f"OneRec-{args.config}", "users_per_gpu": args.users, "global_batch": args.users * world,
-                       "width": args.width,
-                       "parallelism": (f"dp{world} x ep{world} (users sharded; MoE experts sharded, NCCL all-to-all "
-                                       f"dispatch/combine over NVLink)") if ep else
-                                      f"dp{world} (users sharded, no inter-GPU traffic)",
-                       "l2": "working set (weights ~2 GB + activations) exceeds the 126 MB L2; no flush"},
+            "config": bench_config(args, cfg, lens, world),
+            "parallelism_detail": (f"dp{world} x ep{world} (users sharded; MoE experts sharded, NCCL all-to-all "
+                                   f"dispatch/combine over NVLink)") if ep else
+                                  f"dp{world} (users sharded, no inter-GPU traffic)",
             "mfu": mfu, "mfu_peak": "bf16_tflops (burst) of MEASURED_PEAKS.json",
             "gflop_per_user": flops_u / 1e9, "gflop_per_user_encoder": enc_flops_u / 1e9,
             "e2e": {"value": e2e_sync_value, "unit": "users/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

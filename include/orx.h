@@ -127,6 +127,10 @@ int64_t orx_weights_count(const orx_weights* w);
 int orx_weights_entry(const orx_weights* w, int64_t i, const char** name, int32_t* ndim, int32_t dims[2],
                       const float** data);
 int orx_weights_find(const orx_weights* w, const char* name, int64_t* index);
+/* Overwrite the n = rows * cols values of a named parameter (e.g. from the
+ * caller's own f64 ParamStore, converted; ORX_EINVAL on an unknown name or a
+ * size mismatch). Engines created afterwards see the new values. */
+int orx_weights_set(orx_weights* w, const char* name, const float* data, int64_t n);
 void orx_weights_destroy(orx_weights* w);
 
 int orx_validate_batch(const orx_config* cfg, const orx_user_batch* batch);

@@ -125,6 +125,8 @@ struct Args {
   int width = 8;
   int n_prefix = 4;
   bool beam = true;
+  bool seq = true;         // also dump sequence_log_prob of every beam item
+  bool sid_codes = false;  // give every record semantic-id codes sid[l] = (vid >> 8l) % V (use_sid_history)
   int procs = 1;
   int calls = 4;
   int trie_items = 0;      // > 0: constrained beam search over a seeded random trie
@@ -164,6 +166,8 @@ Args parse(int argc, char** argv) {
     } else if (k == "--width") a.width = std::stoi(next());
     else if (k == "--n-prefix") a.n_prefix = std::stoi(next());
     else if (k == "--no-beam") a.beam = false;
+    else if (k == "--no-seq") a.seq = false;
+    else if (k == "--sid-codes") a.sid_codes = true;
     else if (k == "--procs") a.procs = std::stoi(next());
     else if (k == "--calls") a.calls = std::stoi(next());
     else if (k == "--trie-items") a.trie_items = std::stoi(next());
@@ -207,6 +211,9 @@ UserContext make_user(const Args& a, int index) {
         f.playtime = playtime;
         f.duration = duration;
         f.labels = labels;
+        if (a.sid_codes)
+          for (int l = 0; l < a.cfg.n_code_layers; ++l)
+            f.sid.push_back(static_cast<int>((vid >> (8 * l)) % a.cfg.codebook_size));
         (pathway == 0 ? ctx.short_seq : pathway == 1 ? ctx.positive_seq : ctx.lifelong_seq).push_back(f);
       });
   return ctx;
@@ -260,6 +267,7 @@ int cmd_dump(const Args& a) {
       for (auto& it : items) {
         for (int c : it.codes.codes) codes.push_back(c);
         lp.push_back(it.log_prob);
+        if (!a.seq) continue;
         // teacher-forced sequence log-prob of the same item (policy.cpp:297-310), eval session
         Tape tape;
         ParamSession ps(tape, model.params(), false);
@@ -268,7 +276,7 @@ int cmd_dump(const Args& a) {
       }
       write_npy(upath(a, "beam_codes", u), "<i4", {items.size(), size_t(L)}, codes.data(), codes.size() * 4);
       write_npy(upath(a, "beam_logp", u), "<f8", {items.size()}, lp.data(), lp.size() * 8);
-      write_npy(upath(a, "seq_logp", u), "<f8", {seq.size()}, seq.data(), seq.size() * 8);
+      if (a.seq) write_npy(upath(a, "seq_logp", u), "<f8", {seq.size()}, seq.data(), seq.size() * 8);
       if (a.sample) {
         GenerationRequest sreq;
         sreq.strategy = SearchStrategy::topk_topp;

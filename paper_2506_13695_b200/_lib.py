@@ -105,6 +105,7 @@ SIGNATURES = [
     ("orx_weights_entry", C.c_int, [_P, C.c_int64, C.POINTER(C.c_char_p), _I32P, _I32P,
                                     C.POINTER(_F32P)]),
     ("orx_weights_find", C.c_int, [_P, C.c_char_p, C.POINTER(C.c_int64)]),
+    ("orx_weights_set", C.c_int, [_P, C.c_char_p, C.POINTER(C.c_float), C.c_int64]),
     ("orx_weights_destroy", None, [_P]),
     ("orx_validate_batch", C.c_int, [C.POINTER(orx_config), C.POINTER(orx_user_batch)]),
     ("orx_engine_create", C.c_int, [_P, C.c_int, C.c_int, C.c_int32, C.c_int32, C.POINTER(_P)]),

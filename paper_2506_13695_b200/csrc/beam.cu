@@ -374,6 +374,9 @@ __global__ void __launch_bounds__(kMergeThreads) beam_merge_kernel(int n_live, i
   const int u = blockIdx.x;
   const int n = n_live * k_sel;
   const uint64_t* c = cand + (size_t)u * n;
+  if (cur.nonfinite)
+    for (int r = threadIdx.x; r < n_live; r += kMergeThreads)
+      if (!isfinite(lse[(size_t)u * n_live + r])) *cur.nonfinite = 1;
   if (threadIdx.x == 0) counter = 0;
   __syncthreads();
   uint64_t tau = block_kth_largest<kMergeThreads>(n, n_new, [&](int i) { return c[i]; }, hist, bc);
@@ -462,6 +465,7 @@ __global__ void beam_init_kernel(int users, BeamState st) {
   st.lexrank[u] = 0;
   st.lex2beam[u] = 0;
   if (st.node) st.node[u] = 0;  // trie root
+  if (st.nonfinite && u == 0) *st.nonfinite = 0;
 }
 
 // Constrained candidates (generation.cpp:58-64): block per row; the log-softmax

@@ -22,6 +22,10 @@ struct BeamState {  // live beams of one step, row r = user * n_live + beam
   int32_t* lex2beam = nullptr;  // [users][n_live]
   int32_t* anc = nullptr;       // [rows][L] ancestor row per position
   int32_t* node = nullptr;      // [rows] semantic-trie node of the prefix (constrained search), -1 = empty slot
+  // [1] (shared by both states of a search): set when a scored row's
+  // log-softmax normaliser is non-finite, i.e. a NaN/Inf reached the logits
+  // (the reference throws "non-finite value produced on tape", tape.cpp:29)
+  int32_t* nonfinite = nullptr;
 };
 
 // Semantic-ID trie on the device (SemanticTrie, trie.hpp:27-62) as CSR over

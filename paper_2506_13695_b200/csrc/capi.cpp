@@ -173,6 +173,19 @@ int orx_weights_find(const orx_weights* w, const char* name, int64_t* index) {
   });
 }
 
+int orx_weights_set(orx_weights* w, const char* name, const float* data, int64_t n) {
+  return guarded([&] {
+    need(w, "weights");
+    need(name, "name");
+    need(data, "data");
+    auto it = w->w.index.find(name);
+    if (it == w->w.index.end()) throw orx::InvalidArgument(std::string("unknown parameter: ") + name);
+    orx::Tensor& t = w->w.tensors[static_cast<size_t>(it->second)];
+    if (n != static_cast<int64_t>(t.data.size())) throw orx::InvalidArgument(std::string("size mismatch for ") + name);
+    std::copy(data, data + n, t.data.begin());
+  });
+}
+
 void orx_weights_destroy(orx_weights* w) { delete w; }
 
 int orx_validate_batch(const orx_config* cfg, const orx_user_batch* batch) {
@@ -227,6 +240,7 @@ int orx_encode(orx_engine* e, const orx_user_batch* batch, float* z_out) {
   return guarded([&] {
     need(e, "engine");
     need(batch, "batch");
+    e->e->require_idle();
     e->e->stage_batch(*batch);
     e->e->encode(z_out);
   });
@@ -254,6 +268,7 @@ int orx_score_prefixes(orx_engine* e, const orx_user_batch* batch, int32_t n, co
     need(prefixes, "prefixes");
     need(prefix_len, "prefix_len");
     need(logits_out, "logits_out");
+    e->e->require_idle();
     e->e->stage_batch(*batch);
     e->e->score_prefixes(n, user, prefixes, prefix_len, logits_out);
   });
@@ -266,6 +281,7 @@ int orx_beam_search(orx_engine* e, const orx_user_batch* batch, int32_t width, o
     need(out, "out");
     need(out->codes, "out->codes");
     need(out->log_prob, "out->log_prob");
+    e->e->require_idle();
     e->e->stage_batch(*batch);
     e->e->beam_search(width, out);
   });
@@ -291,6 +307,7 @@ int orx_engine_set_trie(orx_engine* e, const orx_trie* t) {
   return guarded([&] {
     need(e, "engine");
     need(t, "trie");
+    e->e->require_idle();
     e->e->set_trie(t->n_nodes, t->child_off, t->n_edges, t->child_code, t->child_node);
   });
 }
@@ -302,6 +319,7 @@ int orx_beam_search_constrained(orx_engine* e, const orx_user_batch* batch, int3
     need(out, "out");
     need(out->codes, "out->codes");
     need(out->log_prob, "out->log_prob");
+    e->e->require_idle();
     e->e->stage_batch(*batch);
     e->e->beam_search_constrained(width, out);
   });
@@ -317,6 +335,7 @@ int orx_sequence_log_prob(orx_engine* e, const orx_user_batch* batch, int32_t n,
       need(codes, "codes");
       need(log_prob_out, "log_prob_out");
     }
+    e->e->require_idle();
     e->e->stage_batch(*batch);
     e->e->sequence_log_prob(n, user, codes, log_prob_out);
   });
@@ -330,6 +349,7 @@ int orx_sample(orx_engine* e, const orx_user_batch* batch, int32_t width, double
     need(out, "out");
     need(out->codes, "out->codes");
     need(out->log_prob, "out->log_prob");
+    e->e->require_idle();
     e->e->stage_batch(*batch);
     e->e->sample(width, temperature, top_k, top_p, seed, user_stream, out);
   });
@@ -339,6 +359,7 @@ int orx_engine_stage_batch(orx_engine* e, const orx_user_batch* batch) {
   return guarded([&] {
     need(e, "engine");
     need(batch, "batch");
+    e->e->require_idle();
     e->e->stage_batch(*batch);
   });
 }
@@ -346,6 +367,7 @@ int orx_engine_stage_batch(orx_engine* e, const orx_user_batch* batch) {
 int orx_beam_search_staged(orx_engine* e, int32_t width, orx_beam_out* out) {
   return guarded([&] {
     need(e, "engine");
+    e->e->require_idle();
     e->e->beam_search(width, out);
   });
 }

@@ -310,7 +310,18 @@ class EngineT final : public Engine {
     cudaStreamDestroy(st_);
   }
 
+  // The reference checks every tape value (tape.cpp:29); host outputs are
+  // checked here, the beam search by its device flag (BeamState::nonfinite).
+  template <class X>
+  static void require_finite(const X* p, size_t n) {
+    for (size_t i = 0; i < n; ++i)
+      if (!std::isfinite(p[i])) throw RuntimeError("non-finite value produced on tape");
+  }
+
   void* stream() override { return st_; }
+  void require_idle() const override {
+    require(pending_.empty(), "a submitted beam search is in flight: collect it before synchronous calls");
+  }
 
   // ------------------------------------------------------------------------
   // weights
@@ -522,8 +533,17 @@ class EngineT final : public Engine {
     p_pos_ = mlp("pathway.positive");
     p_life_ = mlp("pathway.lifelong");
     if constexpr (kBf16) {
+      // The fold pays only while one pathway's folded vid/aid tables stay
+      // L2-resident (126 MB L2): above a 48 MB budget per pathway (e.g. a
+      // production-size vid vocabulary) the explicit feature rows + fc1 GEMM
+      // path is used instead.
+      const double fold_bytes = double(c.vid_vocab + c.aid_vocab) * c.d_model * 4.0;
       fold_on_ = !c.use_sid_history && !c.vid_only_features && aid_dim(c) % 8 == 0 &&
-                 fold_features_supported(c.d_model, c.n_label_flags) && !getenv("ORX_NO_FEATURE_FOLD");
+                 fold_features_supported(c.d_model, c.n_label_flags) && fold_bytes <= 48.0 * (1 << 20) &&
+                 !getenv("ORX_NO_FEATURE_FOLD");
+      if (getenv("ORX_VERBOSE"))
+        fprintf(stderr, "orx: pathway fc1 fold %s (folded tables %.1f MB per pathway)\n", fold_on_ ? "on" : "off",
+                fold_bytes / (1 << 20));
       if (fold_on_) {
         fold_[0] = build_fold(hw, "pathway.short", p_short_);
         fold_[1] = build_fold(hw, "pathway.positive", p_pos_);
@@ -656,6 +676,8 @@ class EngineT final : public Engine {
       bs_[s].anc = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
       node_[s] = ar_.alloc<int32_t>(Rd_);
     }
+    nonfinite_ = ar_.alloc<int32_t>(4);
+    bs_[0].nonfinite = bs_[1].nonfinite = nonfinite_;
     tf_anc_ = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
     seq_acc_ = ar_.alloc<double>(Rd_);
     tf_codes_ = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
@@ -806,7 +828,11 @@ class EngineT final : public Engine {
     // the per-record checks run inside the packers
     if (!offsets_ok(c, b)) validate_batch(c, b);  // raises the first error in reference order
     require(b.n_users >= 1 && b.n_users <= maxU_, "batch size outside the engine capacity");
-    const int ss = stage_slot_ ^ 1;  // the slot not used by the most recent request
+    // a slot no submitted (uncollected) request holds; with none in flight,
+    // the one not used by the most recent request
+    int ss = stage_slot_ ^ 1;
+    for (const Pending& p : pending_) ss = p.slot ^ 1;
+    require(pending_.size() < 2, "both staging slots hold submitted searches");
     CUDA_CHECK(cudaEventSynchronize(h2d_done_[ss]));  // its previous H2D has read the pinned buffer
     const auto t_synced = std::chrono::steady_clock::now();
     CUDA_CHECK(cudaSetDevice(dev_));
@@ -1365,6 +1391,7 @@ class EngineT final : public Engine {
     }
     CUDA_CHECK(cudaStreamSynchronize(st_));
     CUDA_CHECK(cudaGetLastError());
+    if (z_out) require_finite(z_out, static_cast<size_t>(sg_.U) * enc_seq_len(cfg_) * cfg_.d_model);
   }
 
   void beam_search(int width, orx_beam_out* out) override { run_beam(width, out, false); }
@@ -1400,6 +1427,13 @@ class EngineT final : public Engine {
     trie_.child_code = code;
     trie_.child_node = nd;
     has_trie_ = n_edges > 0;
+    // captured constrained searches hold the old trie's device pointers in
+    // their kernel parameters: drop them
+    for (size_t i = graphs_.size(); i-- > 0;)
+      if (graphs_[i].key.constrained) {
+        cudaGraphExecDestroy(graphs_[i].exec);
+        graphs_.erase(graphs_.begin() + static_cast<std::ptrdiff_t>(i));
+      }
   }
 
   struct GraphKey {
@@ -1530,7 +1564,7 @@ class EngineT final : public Engine {
     pd.has_out = want_out;
     if (want_out) {
       const size_t nc = static_cast<size_t>(U) * n_live * L, nl = static_cast<size_t>(U) * n_live;
-      const size_t need = nc * 4 + nl * 8;
+      const size_t need = nc * 4 + nl * 8 + 4;  // codes, log-probs, non-finite flag
       const int k = stage_slot_;
       if (need > host_out_cap_[k]) {
         CUDA_CHECK(cudaEventSynchronize(out_ready_[k]));
@@ -1541,6 +1575,7 @@ class EngineT final : public Engine {
       uint8_t* ho = static_cast<uint8_t*>(host_out_[k]);
       CUDA_CHECK(cudaMemcpyAsync(ho, bs_[cur].codes, nc * 4, cudaMemcpyDeviceToHost, st_));
       CUDA_CHECK(cudaMemcpyAsync(ho + nc * 4, bs_[cur].score64, nl * 8, cudaMemcpyDeviceToHost, st_));
+      CUDA_CHECK(cudaMemcpyAsync(ho + nc * 4 + nl * 8, nonfinite_, 4, cudaMemcpyDeviceToHost, st_));
       CUDA_CHECK(cudaEventRecord(out_ready_[k], st_));
       d2h_bytes += static_cast<int64_t>(need);
     }
@@ -1565,6 +1600,9 @@ class EngineT final : public Engine {
     const uint8_t* ho = static_cast<const uint8_t*>(host_out_[pd.slot]);
     const int32_t* hc = reinterpret_cast<const int32_t*>(ho);
     const double* hl = reinterpret_cast<const double*>(ho + nc * 4);
+    int32_t bad = 0;
+    memcpy(&bad, ho + nc * 4 + static_cast<size_t>(U) * n_live * 8, 4);
+    if (bad) throw RuntimeError("non-finite value produced on tape");  // tape.cpp:29
     for (int u = 0; u < U; ++u) {
       int n_u = n_live;  // constrained search: empty slots (log-prob -inf) sort last
       while (n_u > 0 && std::isinf(hl[(size_t)u * n_live + n_u - 1])) --n_u;
@@ -1654,8 +1692,10 @@ class EngineT final : public Engine {
       CUDA_CHECK(cudaMemcpyAsync(host.data(), logits_, host.size() * 4, cudaMemcpyDeviceToHost, st_));
       CUDA_CHECK(cudaStreamSynchronize(st_));
       for (int r = 0; r < n; ++r)
-        if (prefix_len[order[r]] == step)
+        if (prefix_len[order[r]] == step) {
+          require_finite(host.data() + (size_t)r * V, static_cast<size_t>(V));
           memcpy(logits + (size_t)order[r] * V, host.data() + (size_t)r * V, static_cast<size_t>(V) * 4);
+        }
     }
     CUDA_CHECK(cudaGetLastError());
   }
@@ -1715,6 +1755,7 @@ class EngineT final : public Engine {
     CUDA_CHECK(cudaStreamSynchronize(st_));
     CUDA_CHECK(cudaGetLastError());
     d2h_bytes += static_cast<int64_t>(hc.size() * 4 + hl.size() * 8);
+    require_finite(hl.data(), hl.size());
     for (int u = 0; u < U; ++u) {
       if (out->n_items) out->n_items[u] = width;
       for (int s = 0; s < width; ++s) {
@@ -1782,6 +1823,7 @@ class EngineT final : public Engine {
     CUDA_CHECK(cudaMemcpyAsync(host.data(), seq_acc_, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, st_));
     CUDA_CHECK(cudaStreamSynchronize(st_));
     CUDA_CHECK(cudaGetLastError());
+    require_finite(host.data(), host.size());
     for (int r = 0; r < n; ++r) out[order[r]] = host[r];
   }
 
@@ -1790,8 +1832,7 @@ class EngineT final : public Engine {
     CUDA_CHECK(cudaSetDevice(dev_));
     require(n_z >= 1 && n_z <= maxU_, "encoding count outside the engine capacity");
     const size_t nz = static_cast<size_t>(n_z) * enc_seq_len(cfg_) * cfg_.d_model;
-    for (size_t i = 0; i < nz; ++i)
-      if (!std::isfinite(z[i])) throw RuntimeError("non-finite value produced on tape");
+    require_finite(z, nz);
     CUDA_CHECK(cudaMemcpyAsync(z_, z, nz * 4, cudaMemcpyHostToDevice, st_));
     prepare_decoder(n_z);
     teacher_forced(n_z, n, z_index, prefixes, prefix_len, logits);
@@ -1832,6 +1873,7 @@ class EngineT final : public Engine {
   uint64_t* cand_ = nullptr;
   int32_t* topk_fail_ = nullptr;
   BeamState bs_[2];
+  int32_t* nonfinite_ = nullptr;
   int32_t* node_[2] = {nullptr, nullptr};
   // device trie (constrained search)
   Arena trie_ar_;

@@ -44,6 +44,9 @@ class Engine {
   virtual void score_prefixes(int n, const int32_t* user, const int32_t* prefixes, const int32_t* prefix_len,
                               float* logits) = 0;
   virtual void* stream() = 0;
+  // Synchronous entry points refuse to run while a submitted search is in
+  // flight (they would reuse its staging slot / drain its result).
+  virtual void require_idle() const = 0;
   int64_t h2d_bytes = 0, d2h_bytes = 0;
 };
 

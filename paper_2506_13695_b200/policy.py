@@ -158,6 +158,7 @@ class SemanticTrie:
             raise ValueError("trie depth must be >= 1")
         self.depth = depth
         self._leaves: Dict[tuple, List[int]] = {}
+        self.version = 0  # bumped by insert(): a PolicyModel re-uploads a changed trie
 
     def insert(self, codes: Sequence[int], item: int) -> None:
         if len(codes) != self.depth:
@@ -165,6 +166,7 @@ class SemanticTrie:
         if any(c < 0 for c in codes):
             raise ValueError("semantic id codes must be non-negative")
         self._leaves.setdefault(tuple(codes), []).append(int(item))
+        self.version += 1
 
     def lookup(self, codes: Sequence[int]) -> Optional[List[int]]:
         return self._leaves.get(tuple(codes)) if len(codes) == self.depth else None
@@ -335,6 +337,11 @@ class Weights:
         n = dims[0] * dims[1]
         return np.ctypeslib.as_array(data, shape=(n,)).reshape(dims[0], dims[1]).copy()
 
+    def set(self, name: str, value: np.ndarray) -> None:
+        """Overwrite a named parameter (reference name, e.g. "dec.head0.w")."""
+        v = np.ascontiguousarray(np.asarray(value, dtype=np.float32).ravel())
+        check(lib().orx_weights_set(self._h, name.encode(), v.ctypes.data_as(C.POINTER(C.c_float)), v.size))
+
     def __del__(self):
         if getattr(self, "_h", None):
             lib().orx_weights_destroy(self._h)
@@ -445,6 +452,7 @@ class PolicyModel:
         t = orx_trie(len(off) - 1, off.ctypes.data_as(I32), len(code), code.ctypes.data_as(I32), node.ctypes.data_as(I32))
         check(lib().orx_engine_set_trie(self._e, C.byref(t)))
         self._trie = trie
+        self._trie_version = trie.version
 
     def sequence_log_prob_batch(self, users, user_index: Sequence[int], codes: Sequence[Sequence[int]]) -> np.ndarray:
         """PolicyModel::sequence_log_prob (policy.cpp:297-310) for (user, full code) queries, f64."""
@@ -512,8 +520,9 @@ class PolicyModel:
         n_items = np.empty(n_users, dtype=np.int32)
         out = orx_beam_out(codes.ctypes.data_as(C.POINTER(C.c_int32)), logp.ctypes.data_as(C.POINTER(C.c_double)),
                            n_items.ctypes.data_as(C.POINTER(C.c_int32)))
-        check(lib().orx_beam_search_collect(self._e, C.byref(out)))
-        self._pending.pop(0)
+        rc = lib().orx_beam_search_collect(self._e, C.byref(out))
+        self._pending.pop(0)  # the engine retires the request even when it fails (e.g. non-finite)
+        check(rc)
         return codes, logp, n_items
 
     def generate_batch(self, users, req: GenerationRequest, trie: Optional[SemanticTrie] = None, seed: int = 0,
@@ -534,7 +543,7 @@ class PolicyModel:
         if req.constrain_to_trie:
             if trie is None or trie.item_count() == 0:
                 raise ValueError("constrained beam search over an empty trie")  # generation.cpp:44-45
-            if getattr(self, "_trie", None) is not trie:
+            if getattr(self, "_trie", None) is not trie or self._trie_version != trie.version:
                 self.set_trie(trie)
         codes, logp, n_items = self.beam_search_arrays(users, req.width, constrained=req.constrain_to_trie)
         out = []

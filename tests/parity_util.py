@@ -18,7 +18,7 @@ REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
 
 def ref_dump(preset: str, n_users: int, width: int, lens=None, user_seed: int = 1, user_begin: int = 0,
              n_prefix: int = 4, beam: bool = True, sets=(), out_dir=None, timeout=3600, trie_items: int = 0,
-             trie_fanout: int = 0, trie_seed: int = 77, sample=None):
+             trie_fanout: int = 0, trie_seed: int = 77, sample=None, sid_codes: bool = False):
     """Run the reference on synthetic users; returns (dir, per-user dict)."""
     if not os.path.exists(REF_DRIVER):
         raise FileNotFoundError(f"{REF_DRIVER} missing: run `make -C oracle`")
@@ -32,6 +32,8 @@ def ref_dump(preset: str, n_users: int, width: int, lens=None, user_seed: int = 
         cmd += ["--lens", ",".join(str(x) for x in lens)]
     if not beam:
         cmd += ["--no-beam"]
+    if sid_codes:
+        cmd += ["--sid-codes"]
     if trie_items:
         cmd += ["--trie-items", str(trie_items), "--trie-seed", str(trie_seed)]
         if trie_fanout:

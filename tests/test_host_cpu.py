@@ -212,3 +212,55 @@ def test_trie_csr_matches_children_of():
         for depth in range(3):
             n = walk(leaf[:depth])
             assert list(code[off[n]:off[n + 1]]) == t.children_of(list(leaf[:depth]))
+
+
+def test_weights_set_roundtrip():
+    """orx_weights_set overwrites a named parameter (host only)."""
+    import numpy as np
+    import pytest
+
+    import paper_2506_13695_b200 as P
+    w = P.Weights.random(P.PolicyConfig.preset("tiny"))
+    x = w.get("dec.head0.w")
+    y = np.arange(x.size, dtype=np.float32).reshape(x.shape)
+    w.set("dec.head0.w", y)
+    assert np.array_equal(w.get("dec.head0.w"), y)
+    with pytest.raises(ValueError):
+        w.set("dec.head0.w", y[:-1])
+    with pytest.raises(ValueError):
+        w.set("no.such.param", y)
+
+
+def test_bench_static_presets_match_library():
+    """bench.py's reference arm never loads liborx.so: its static preset table
+    must equal the library's presets (include/orx.h / PolicyConfig)."""
+    import bench
+
+    import paper_2506_13695_b200 as P
+    for name in bench.BenchConfig.PRESETS:
+        b, p = bench.BenchConfig(name), P.PolicyConfig.preset(name)
+        for f in bench.BenchConfig.BASE:
+            assert getattr(b, f) == getattr(p, f), (name, f)
+        assert b.expert_hidden() == p.expert_hidden()
+        assert b.enc_seq_len() == p.enc_seq_len()
+        assert bench.flops_per_user(b, 128, (20, 256, 2000)) == bench.flops_per_user(p, 128, (20, 256, 2000))
+
+
+def test_bench_reference_arm_does_not_import_package():
+    """--impl reference must not map liborx.so (the driver checks the loaded .so files)."""
+    import subprocess
+    import sys
+    code = ("import sys, runpy; sys.argv=['bench.py','--impl','reference','--config','0.015B','--steps','1',"
+            "'--width','8','--users','1']\n"
+            "import bench\n"
+            "bench.run_reference_sample = lambda *a, **k: {'users_per_s': 1.0, 'procs': 1, 't_encode_s': 0.1, "
+            "'beam_measured': True, 't_beam_s': 0.1, 'init_s': 0.0}\n"
+            "bench.main()\n"
+            "assert not any('paper_2506_13695_b200' in m for m in sys.modules), 'package imported'\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "assert 'liborx' not in maps, 'liborx.so mapped'\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=120)
+    assert r.returncode == 0, r.stderr
+    import json
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["config"]["model"] == "OneRec-0.015B"

@@ -320,3 +320,44 @@ def test_bf16_feature_fold(d):
         ez, ez_unf, e_pair = rel_inf(z[u], ref["z"]), rel_inf(z_unf[u], ref["z"]), rel_inf(z[u], z_unf[u])
         print(f"fold d={d} user {u}: z {ez:.3e} (unfolded {ez_unf:.3e}, fold vs unfolded {e_pair:.3e})")
         assert ez < 5e-2 and ez <= 1.5 * ez_unf + 2e-3
+
+
+def _with_sids(P, batch, L, V):
+    """The ref_driver's --sid-codes rule: sid[l] = (vid >> 8l) % V."""
+    users = batch.to_contexts()
+    for u in users:
+        for seq in (u.short_seq, u.positive_seq, u.lifelong_seq):
+            for f in seq:
+                f.sid = [int((f.vid >> (8 * l)) % V) for l in range(L)]
+    return P.UserBatch(users, L)
+
+
+@pytest.mark.parametrize("flag", ["use_sid_history", "vid_only_features", "both"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_feature_branches(flag, precision):
+    """PolicyConfig::use_sid_history (record vid row = sum of the SID code
+    embeddings, policy.cpp:146-160) and vid_only_features (feature row = the
+    vid row alone, policy.cpp:166) against the reference."""
+    flags = ["use_sid_history", "vid_only_features"] if flag == "both" else [flag]
+    over = {f: True for f in flags}
+    sets = [f"{f}=1" for f in flags]
+    lens = (20, 64, 300)
+    P, model = _model("0.015B", precision, max_users=2, max_width=16, **over)
+    sid = "use_sid_history" in flags
+    _, refs = ref_dump("0.015B", 2, 16, lens=lens, sets=sets, sid_codes=sid)
+    batch = P.SynthBatch(1, 0, 2, *lens)
+    if sid:
+        batch = _with_sids(P, batch, model.cfg.n_code_layers, model.cfg.codebook_size)
+    if precision == "fp32":
+        rep = _check_user(P, model, batch, refs, 16, 1e-4, LOGIT_RTOL)
+        print(f"{flag} fp32 (z, logits, next_logits):", rep)
+    else:
+        z = model.encode_batch(batch)
+        codes, _, _ = model.beam_search_arrays(batch, 16)
+        for u, ref in enumerate(refs):
+            pres = prefixes_of(ref["prefixes"])
+            lg = model.score_prefixes(batch, [u] * len(pres), pres)
+            el = max(rel_inf(lg[i], ref["logits"][i]) for i in range(len(pres)))
+            overlap = len({tuple(c) for c in codes[u]} & {tuple(c) for c in ref["beam_codes"]})
+            print(f"{flag} bf16 user {u}: z {rel_inf(z[u], ref['z']):.3e} logits {el:.3e} overlap {overlap}/16")
+            assert rel_inf(z[u], ref["z"]) < 3e-2 and el < 3e-2 and overlap >= 12

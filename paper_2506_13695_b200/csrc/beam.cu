@@ -360,41 +360,15 @@ __global__ void __launch_bounds__(32 * kWarpRows) row_topk_warp_kernel(int rows,
 constexpr int kMergeThreads = 512;
 constexpr int kMaxBeam = 1024;
 
-__global__ void __launch_bounds__(kMergeThreads) beam_merge_kernel(int n_live, int k_sel, int n_new, int V, int L,
-                                                                   int step, const uint64_t* __restrict__ cand,
-                                                                   const float* __restrict__ logits,
-                                                                   const float* __restrict__ lse, BeamState cur,
-                                                                   BeamState nxt, TrieDev trie, int use_trie) {
-  pdl_begin();
-  __shared__ uint64_t sel[kMaxBeam];
-  __shared__ uint64_t lex[kMaxBeam];
-  __shared__ uint32_t hist[256];
-  __shared__ uint32_t bc[4];
-  __shared__ uint32_t counter;
-  const int u = blockIdx.x;
-  const int n = n_live * k_sel;
-  const uint64_t* c = cand + (size_t)u * n;
-  if (cur.nonfinite)
-    for (int r = threadIdx.x; r < n_live; r += kMergeThreads)
-      if (!isfinite(lse[(size_t)u * n_live + r])) *cur.nonfinite = 1;
-  if (threadIdx.x == 0) counter = 0;
-  __syncthreads();
-  uint64_t tau = block_kth_largest<kMergeThreads>(n, n_new, [&](int i) { return c[i]; }, hist, bc);
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += kMergeThreads) {
-    uint64_t key = c[i];
-    if (key >= tau && key != 0) {  // key 0 = no candidate (constrained search)
-      uint32_t pos = atomicAdd(&counter, 1u);
-      if (pos < static_cast<uint32_t>(n_new)) sel[pos] = key;
-    }
-  }
-  __syncthreads();
-  for (int i = static_cast<int>(min(counter, static_cast<uint32_t>(n_new))) + threadIdx.x; i < n_new; i += kMergeThreads)
-    sel[i] = 0;  // fewer candidates than slots: empty slots sort last
-  __syncthreads();
-  block_sort_desc<kMaxBeam, kMergeThreads>(sel, n_new);
+// Next BeamState from the n_new selected candidate keys of user u, sorted
+// descending in sel[] (shared): codes, ancestors, scores, trie nodes and the
+// lexicographic ranks of the new prefixes. lex[] is kMaxBeam shared scratch.
+template <int NT, class LseOf>
+__device__ void build_next_state(int u, int n_live, int n_new, int V, int L, int step, const uint64_t* sel, uint64_t* lex,
+                                 const float* __restrict__ logits, LseOf lse_of, const BeamState& cur,
+                                 const BeamState& nxt, const TrieDev& trie, int use_trie) {
   // beam b (rank order): decode parent lexrank + code, build next state
-  for (int b = threadIdx.x; b < n_new; b += kMergeThreads) {
+  for (int b = threadIdx.x; b < n_new; b += NT) {
     const uint64_t key = sel[b];
     const int nrow = u * n_new + b;
     if (key == 0) {  // empty slot: decodes harmlessly (code 0, ancestors = its user's first row)
@@ -438,22 +412,320 @@ __global__ void __launch_bounds__(kMergeThreads) beam_merge_kernel(int n_live, i
     nxt.anc[(size_t)nrow * L + step] = prow;
     nxt.score[nrow] = unord_f32(static_cast<uint32_t>(key >> 32));
     nxt.score64[nrow] = cur.score64[prow] + (static_cast<double>(logits[(size_t)prow * V + code]) -
-                                             static_cast<double>(lse[prow]));
+                                             static_cast<double>(lse_of(prow)));
     lex[b] = (static_cast<uint64_t>(low) << 32) | static_cast<uint32_t>(b);
   }
   __syncthreads();
   // lexicographic rank of the new prefixes = ascending (plr, code) = ascending low
-  for (int i = n_new + threadIdx.x; i < kMaxBeam; i += kMergeThreads) lex[i] = ~0ull;
+  for (int i = n_new + threadIdx.x; i < kMaxBeam; i += NT) lex[i] = ~0ull;
   __syncthreads();
   // ascending sort: negate by sorting descending of the complement
-  for (int i = threadIdx.x; i < kMaxBeam; i += kMergeThreads) lex[i] = ~lex[i];
+  for (int i = threadIdx.x; i < kMaxBeam; i += NT) lex[i] = ~lex[i];
   __syncthreads();
-  block_sort_desc<kMaxBeam, kMergeThreads>(lex, kMaxBeam);
-  for (int r = threadIdx.x; r < n_new; r += kMergeThreads) {
+  block_sort_desc<kMaxBeam, NT>(lex, kMaxBeam);
+  for (int r = threadIdx.x; r < n_new; r += NT) {
     const int b = static_cast<int>(static_cast<uint32_t>(~lex[r]));
     nxt.lexrank[u * n_new + b] = r;
     nxt.lex2beam[(size_t)u * n_new + r] = b;
   }
+}
+
+__global__ void __launch_bounds__(kMergeThreads) beam_merge_kernel(int n_live, int k_sel, int n_new, int V, int L,
+                                                                   int step, const uint64_t* __restrict__ cand,
+                                                                   const float* __restrict__ logits,
+                                                                   const float* __restrict__ lse, BeamState cur,
+                                                                   BeamState nxt, TrieDev trie, int use_trie) {
+  pdl_begin();
+  __shared__ uint64_t sel[kMaxBeam];
+  __shared__ uint64_t lex[kMaxBeam];
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t bc[4];
+  __shared__ uint32_t counter;
+  const int u = blockIdx.x;
+  const int n = n_live * k_sel;
+  const uint64_t* c = cand + (size_t)u * n;
+  if (cur.nonfinite)
+    for (int r = threadIdx.x; r < n_live; r += kMergeThreads)
+      if (!isfinite(lse[(size_t)u * n_live + r])) *cur.nonfinite = 1;
+  if (threadIdx.x == 0) counter = 0;
+  __syncthreads();
+  uint64_t tau = block_kth_largest<kMergeThreads>(n, n_new, [&](int i) { return c[i]; }, hist, bc);
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += kMergeThreads) {
+    uint64_t key = c[i];
+    if (key >= tau && key != 0) {  // key 0 = no candidate (constrained search)
+      uint32_t pos = atomicAdd(&counter, 1u);
+      if (pos < static_cast<uint32_t>(n_new)) sel[pos] = key;
+    }
+  }
+  __syncthreads();
+  for (int i = static_cast<int>(min(counter, static_cast<uint32_t>(n_new))) + threadIdx.x; i < n_new; i += kMergeThreads)
+    sel[i] = 0;  // fewer candidates than slots: empty slots sort last
+  __syncthreads();
+  block_sort_desc<kMaxBeam, kMergeThreads>(sel, n_new);
+  build_next_state<kMergeThreads>(u, n_live, n_new, V, L, step, sel, lex, logits,
+                                  [&](int prow) { return lse[prow]; }, cur, nxt, trie, use_trie);
+}
+
+// ---------------------------------------------------------------------------
+// Fused log-softmax + beam selection (unconstrained steps whose head GEMM
+// wrote chunk statistics, EPI_STATS). One block per user; the logits are
+// read only where they can hold a winner.
+//
+// Per parent row b: lse_b from the row's (max, sum exp) pairs of its 32-column
+// chunks (generation.cpp:10-20). Chunk key = ord(ps_b + (cmax - lse_b)), the
+// exact fp32 score of the chunk's best element. tau = the n_new-th largest
+// chunk key: at least n_new elements score >= tau, so the n_new-th best
+// candidate does too, and since fp32 rounding is monotone every element
+// scoring >= tau lies in a chunk whose key is >= tau. Only those chunks are
+// read (typically ~n_new of n_live * V / 32): their elements with score >=
+// tau become the candidates (64-bit keys as in row_topk), the exact top n_new
+// of which form the next beams -- the same set the full per-row top-k +
+// merge selects. Degenerate inputs that overflow the candidate buffers
+// (massive ties) take an exact radix select over all n_live * V keys.
+// ---------------------------------------------------------------------------
+constexpr int kSelThreads = 512;
+constexpr int kSelWarps = kSelThreads / 32;
+constexpr int kSelChunkKeys = 32768;  // chunk keys cached in shared memory (128 KB)
+constexpr int kSelCand = 16384;       // candidate capacity (aliases the chunk-key cache)
+constexpr int kSelIds = 4096;         // selected-chunk capacity
+struct SelSmem {
+  uint64_t sel[kMaxBeam];
+  uint64_t lex[kMaxBeam];
+  uint32_t hist[kSelWarps * 256];
+  uint32_t ids[kSelIds];
+  float lse[kMaxBeam];
+  float ps[kMaxBeam];
+  uint32_t lbase[kMaxBeam];
+  uint32_t tot[256];
+  uint32_t bc[4];
+  uint32_t counter, nids;
+};
+constexpr size_t kSelSmemBytes = sizeof(uint32_t) * kSelChunkKeys + sizeof(SelSmem);
+static_assert(sizeof(uint32_t) * kSelChunkKeys >= sizeof(uint64_t) * kSelCand, "candidate alias");
+
+// n-th largest (with multiplicity) of n 32-bit keys: count(key >= tau) >= k and
+// tau is the largest value with that property. Bits above the highest bit in
+// which the keys differ are skipped; per-warp histograms.
+template <class Get>
+__device__ uint32_t block_kth_largest32(int n, int k, Get get, SelSmem& S) {
+  if (n <= k) return 0;
+  uint32_t a = 0xFFFFFFFFu, o = 0;
+  for (int i = threadIdx.x; i < n; i += kSelThreads) {
+    const uint32_t x = get(i);
+    a &= x;
+    o |= x;
+  }
+  a = __reduce_and_sync(0xffffffffu, a);
+  o = __reduce_or_sync(0xffffffffu, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    S.hist[warp] = a;
+    S.hist[kSelWarps + warp] = o;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t A = 0xFFFFFFFFu, O = 0;
+    for (int w = 0; w < kSelWarps; ++w) A &= S.hist[w], O |= S.hist[kSelWarps + w];
+    S.bc[0] = A;
+    S.bc[1] = O;
+  }
+  __syncthreads();
+  const uint32_t A = S.bc[0], O = S.bc[1];
+  __syncthreads();
+  if (A == O) return A;  // all keys equal
+  const int hb = 31 - __clz(A ^ O);
+  const uint32_t low_mask = hb == 31 ? 0xFFFFFFFFu : ((2u << hb) - 1u);
+  uint32_t prefix = A & ~low_mask, mask = ~low_mask;
+  int krem = k;
+  int shift = hb >= 7 ? hb - 7 : 0;
+  for (;;) {
+    for (int i = threadIdx.x; i < kSelWarps * 256; i += kSelThreads) S.hist[i] = 0;
+    __syncthreads();
+    uint32_t* h = S.hist + warp * 256;
+    for (int i = threadIdx.x; i < n; i += kSelThreads) {
+      const uint32_t x = get(i);
+      if ((x & mask) == prefix) atomicAdd(&h[(x >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += kSelThreads) {
+      uint32_t t = 0;
+#pragma unroll 4
+      for (int w = 0; w < kSelWarps; ++w) t += S.hist[w * 256 + b];
+      S.tot[b] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint32_t c[8], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = S.tot[255 - 8 * lane - j];
+        tot += c[j];
+      }
+      uint32_t incl = tot;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      uint32_t above = incl - tot;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (above < static_cast<uint32_t>(krem) && above + c[j] >= static_cast<uint32_t>(krem)) {
+          S.bc[0] = 255 - 8 * lane - j;
+          S.bc[1] = above;
+          S.bc[2] = c[j];
+        }
+        above += c[j];
+      }
+    }
+    __syncthreads();
+    const uint32_t dgt = S.bc[0], above = S.bc[1], cnt = S.bc[2];
+    __syncthreads();
+    prefix = (prefix & ~(255u << shift)) | (dgt << shift);
+    mask |= 255u << shift;
+    krem -= static_cast<int>(above);
+    if (static_cast<int>(cnt) == krem || shift == 0) break;
+    shift = shift >= 8 ? shift - 8 : 0;
+  }
+  return prefix;
+}
+
+__global__ void __launch_bounds__(kSelThreads, 1)
+    beam_select_kernel(int n_live, int n_new, int V, int L, int step, const float* __restrict__ logits,
+                       const float2* __restrict__ stats, long long stats_ld, float* __restrict__ lse_out,
+                       uint32_t* __restrict__ gkeys, BeamState cur, BeamState nxt) {
+  pdl_begin();
+  extern __shared__ __align__(16) uint8_t sel_smem[];
+  uint32_t* ckeys = reinterpret_cast<uint32_t*>(sel_smem);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(sel_smem);  // after the chunk selection
+  SelSmem& S = *reinterpret_cast<SelSmem*>(sel_smem + sizeof(uint32_t) * kSelChunkKeys);
+  const int u = blockIdx.x, r0 = u * n_live;
+  const int NC = V >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // 1. log-softmax normaliser per parent row from its chunk statistics:
+  //    P threads per row over interleaved chunks (coalesced over rows), combined
+  //    through shared memory (S.hist as (max, sum) scratch)
+  {
+    const int P = n_live >= kSelThreads ? 1 : kSelThreads / n_live;
+    float2* part = reinterpret_cast<float2*>(S.hist);  // [P][n_live] (P * n_live <= 2048)
+    const int Pn = P * n_live <= 2048 ? P : 2048 / n_live;
+    for (int t = threadIdx.x; t < Pn * n_live; t += kSelThreads) {
+      const int b = t % n_live, p = t / n_live;
+      float m = -INFINITY;
+      for (int c = p; c < NC; c += Pn) m = fmaxf(m, stats[(long long)c * stats_ld + r0 + b].x);
+      float sum = 0.f;
+      for (int c = p; c < NC; c += Pn) {
+        const float2 st = stats[(long long)c * stats_ld + r0 + b];
+        sum += st.y * __expf(st.x - m);
+      }
+      part[p * n_live + b] = make_float2(m, sum);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < n_live; b += kSelThreads) {
+      float m = -INFINITY;
+      for (int p = 0; p < Pn; ++p) m = fmaxf(m, part[p * n_live + b].x);
+      float sum = 0.f;
+      for (int p = 0; p < Pn; ++p) {
+        const float2 q = part[p * n_live + b];
+        sum += q.y * __expf(q.x - m);
+      }
+      const float lse = m + logf(sum);
+      if (!isfinite(lse) && cur.nonfinite) *cur.nonfinite = 1;
+      S.lse[b] = lse;
+      S.ps[b] = cur.score[r0 + b];
+      S.lbase[b] = static_cast<uint32_t>(cur.lexrank[r0 + b]) * static_cast<uint32_t>(V);
+      lse_out[r0 + b] = lse;
+    }
+    if (threadIdx.x == 0) {
+      S.counter = 0;
+      S.nids = 0;
+    }
+    __syncthreads();
+  }
+
+  // 2. chunk keys (index i = c * n_live + b: consecutive threads read consecutive rows)
+  const int nck = n_live * NC;
+  const bool in_smem = nck <= kSelChunkKeys;
+  uint32_t* keys = in_smem ? ckeys : gkeys + (size_t)u * nck;
+  for (int i = threadIdx.x; i < nck; i += kSelThreads) {
+    const int c = i / n_live, b = i - c * n_live;
+    keys[i] = ord_f32(S.ps[b] + (stats[(long long)c * stats_ld + r0 + b].x - S.lse[b]));
+  }
+  __syncthreads();
+  const uint32_t tau = block_kth_largest32(nck, n_new, [&](int i) { return keys[i]; }, S);
+
+  // 3. the chunks that can hold a winner
+  for (int i0 = warp * 32; i0 < nck; i0 += kSelThreads) {
+    const int i = i0 + lane;
+    const bool take = i < nck && keys[i] >= tau;
+    const uint32_t m = __ballot_sync(0xffffffffu, take);
+    uint32_t base = 0;
+    if (lane == 0 && m) base = atomicAdd(&S.nids, static_cast<uint32_t>(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+    if (take && pos < static_cast<uint32_t>(kSelIds)) S.ids[pos] = static_cast<uint32_t>(i);
+  }
+  __syncthreads();
+  const int nids = static_cast<int>(S.nids);
+
+  // 4. candidates: elements of the selected chunks scoring >= tau (warp per chunk)
+  if (nids <= kSelIds) {
+    for (int j = warp; j < nids; j += kSelWarps) {
+      const int i = static_cast<int>(S.ids[j]);
+      const int c = i / n_live, b = i - c * n_live;
+      const int code = c * 32 + lane;
+      const float sc = S.ps[b] + (logits[(size_t)(r0 + b) * V + code] - S.lse[b]);
+      const uint32_t k32 = ord_f32(sc);
+      const bool take = k32 >= tau;
+      const uint32_t m = __ballot_sync(0xffffffffu, take);
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&S.counter, static_cast<uint32_t>(__popc(m)));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+      if (take && pos < static_cast<uint32_t>(kSelCand))
+        cand[pos] = (static_cast<uint64_t>(k32) << 32) | (0xFFFFFFFFu - (S.lbase[b] + static_cast<uint32_t>(code)));
+    }
+  }
+  __syncthreads();
+  const int ncand = static_cast<int>(S.counter);
+  const bool fallback = nids > kSelIds || ncand > kSelCand;
+  __syncthreads();
+  if (threadIdx.x == 0) S.counter = 0;
+  if (!fallback) {
+    const uint64_t t64 =
+        block_kth_largest<kSelThreads>(ncand, n_new, [&](int i) { return cand[i]; }, S.hist, S.bc);
+    __syncthreads();
+    for (int i = threadIdx.x; i < ncand; i += kSelThreads) {
+      const uint64_t key = cand[i];
+      if (key >= t64) {
+        const uint32_t pos = atomicAdd(&S.counter, 1u);
+        if (pos < static_cast<uint32_t>(n_new)) S.sel[pos] = key;
+      }
+    }
+  } else {  // exact select over every (row, code) of the user
+    auto key_of = [&](int i) {
+      const int b = i / V, code = i - b * V;
+      const float sc = S.ps[b] + (logits[(size_t)(r0 + b) * V + code] - S.lse[b]);
+      return (static_cast<uint64_t>(ord_f32(sc)) << 32) | (0xFFFFFFFFu - (S.lbase[b] + static_cast<uint32_t>(code)));
+    };
+    const int n = n_live * V;
+    const uint64_t t64 = block_kth_largest<kSelThreads>(n, n_new, key_of, S.hist, S.bc);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kSelThreads) {
+      const uint64_t key = key_of(i);
+      if (key >= t64) {
+        const uint32_t pos = atomicAdd(&S.counter, 1u);
+        if (pos < static_cast<uint32_t>(n_new)) S.sel[pos] = key;
+      }
+    }
+    if (threadIdx.x == 0) atomicAdd(&g_topk_fallback_rows, 1ull);
+  }
+  __syncthreads();
+  block_sort_desc<kMaxBeam, kSelThreads>(S.sel, n_new);
+  build_next_state<kSelThreads>(u, n_live, n_new, V, L, step, S.sel, S.lex, logits,
+                                [&](int prow) { return S.lse[prow - r0]; }, cur, nxt, TrieDev{}, 0);
 }
 
 __global__ void beam_init_kernel(int users, BeamState st) {
@@ -758,6 +1030,28 @@ void launch_beam_merge(int users, int n_live, int k_sel, int n_new, int V, int L
   launch_pdl(beam_merge_kernel, users, kMergeThreads, 0, s, n_live, k_sel, n_new, V, L, step, cand, logits, lse, cur, nxt,
                                                     trie ? *trie : TrieDev{}, trie ? 1 : 0);
   ++launch_counter();
+}
+
+void launch_beam_select(int users, int n_live, int n_new, int V, int L, int step, const float* logits,
+                        const float2* stats, long long stats_ld, float* lse, uint32_t* scratch, const BeamState& cur,
+                        BeamState& nxt, cudaStream_t s) {
+  if (n_new > kMaxBeam) throw std::invalid_argument("beam width above 1024 is not supported");
+  if (V % 32 != 0) throw std::invalid_argument("beam_select: codebook size must be a multiple of 32");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(beam_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSelSmemBytes));
+    attr = true;
+  }
+  // algorithmic bytes: the chunk statistics plus ~2 logit chunks per new beam
+  ProfScope ps(PROF_BEAM, s, 0.0, double(users) * (double(n_live) * (V / 32) * 8 + 2.0 * n_new * 128));
+  launch_pdl(beam_select_kernel, users, kSelThreads, kSelSmemBytes, s, n_live, n_new, V, L, step, logits, stats,
+             stats_ld, lse, scratch, cur, nxt);
+  ++launch_counter();
+}
+
+size_t beam_select_scratch_words(int n_live, int V) {
+  const size_t nck = size_t(n_live) * (V / 32);
+  return nck <= size_t(kSelChunkKeys) ? 0 : nck;
 }
 
 void launch_beam_init(int users, BeamState& st, cudaStream_t s) {

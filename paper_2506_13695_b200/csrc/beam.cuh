@@ -72,4 +72,15 @@ void launch_beam_merge(int users, int n_live, int k_sel, int n_new, int V, int L
                        const float* logits, const float* lse, const BeamState& cur, BeamState& nxt, cudaStream_t s,
                        const TrieDev* trie = nullptr);
 
+// Fused log-softmax + exact beam selection from the head GEMM's chunk
+// statistics (Epi::stats, stats[c * stats_ld + row] = (max, sum exp) of the
+// row's 32-column chunk c): replaces launch_row_topk + launch_beam_merge for
+// unconstrained steps and reads only the logit chunks that can hold a winner.
+// Writes lse[rows] and the next BeamState. scratch: per user
+// beam_select_scratch_words(n_live, V) words (0 when the chunk keys fit on chip).
+void launch_beam_select(int users, int n_live, int n_new, int V, int L, int step, const float* logits,
+                        const float2* stats, long long stats_ld, float* lse, uint32_t* scratch, const BeamState& cur,
+                        BeamState& nxt, cudaStream_t s);
+size_t beam_select_scratch_words(int n_live, int V);
+
 }  // namespace orx

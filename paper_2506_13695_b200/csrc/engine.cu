@@ -666,6 +666,14 @@ class EngineT final : public Engine {
     const int ksel = std::min(maxW_, c.codebook_size);
     cand_ = ar_.alloc<uint64_t>(static_cast<size_t>(Rd_) * ksel);
     lse_ = ar_.alloc<float>(Rd_);
+    if constexpr (kBf16) {  // fused log-softmax + beam selection from the head GEMM's chunk statistics
+      fused_select_ = c.codebook_size % 256 == 0 && maxW_ <= 1024 && !getenv("ORX_NO_FUSED_SELECT");
+      if (fused_select_) {
+        head_stats_ = ar_.alloc<float2>(static_cast<size_t>(Rd_) * (c.codebook_size / 32));
+        const size_t words = beam_select_scratch_words(std::min(maxW_, c.codebook_size), c.codebook_size);
+        if (words) sel_scratch_ = ar_.alloc<uint32_t>(words * maxU_);
+      }
+    }
     topk_fail_ = ar_.alloc<int32_t>(Rd_ + 1);
     for (int s = 0; s < 2; ++s) {
       bs_[s].codes = ar_.alloc<int32_t>(static_cast<size_t>(Rd_) * L);
@@ -1337,7 +1345,8 @@ class EngineT final : public Engine {
   // cross-attending to encoder rows [gk.start(g), +Tn).
   // vt_user: encoder user of each group (NULL: group g is user g).
   void decode_step(int step, int rows, int groups, Seg gq, Seg gk, const int32_t* codes, int code_stride,
-                   const int32_t* anc, int anc_stride, int max_group_rows, const int32_t* vt_user = nullptr) {
+                   const int32_t* anc, int anc_stride, int max_group_rows, const int32_t* vt_user = nullptr,
+                   float2* head_stats = nullptr) {
     const orx_config& c = cfg_;
     const int d = c.d_model, H = c.n_heads, dh = d / H, Ld = dec_layers(c), Tn = enc_seq_len(c);
     launch_dec_embed(rows, d, step == 0 ? bos_ : tokens_[step - 1], step == 0 ? nullptr : codes + (step - 1),
@@ -1375,7 +1384,12 @@ class EngineT final : public Engine {
     (void)Tn;
     // position_logits: no final norm (policy.cpp:290-295)
     if (!have_x) launch_convert<T>(rows, d, h_, d, xn_, d, st_);
-    gemm(xn_, d, heads_[step], rows, epi(logits_, c.codebook_size, true));
+    Epi he = epi(logits_, c.codebook_size, true);
+    if (head_stats) {  // + per-chunk log-sum-exp statistics for launch_beam_select
+      he.stats = head_stats;
+      he.stats_ld = Rd_;
+    }
+    gemm(xn_, d, heads_[step], rows, he);
   }
 
   // ------------------------------------------------------------------------
@@ -1468,14 +1482,24 @@ class EngineT final : public Engine {
       Seg gk;
       gk.stride = Tn;
       gk.fixed_len = Tn;
-      decode_step(step, rows, U, gq, gk, bs_[cur].codes, L, bs_[cur].anc, L, n_live);
+      const int n_new = static_cast<int>(std::min<int64_t>(width, static_cast<int64_t>(n_live) * V));
+      // fused selection: unconstrained, and the head GEMM runs on the CTA-pair kernel (M > 128)
+      const bool fused = fused_select_ && !constrained && rows > 128;
+      decode_step(step, rows, U, gq, gk, bs_[cur].codes, L, bs_[cur].anc, L, n_live, nullptr,
+                  fused ? head_stats_ : nullptr);
+      if (fused) {
+        launch_beam_select(U, n_live, n_new, V, L, step, logits_, head_stats_, Rd_, lse_, sel_scratch_, bs_[cur],
+                           bs_[cur ^ 1], st_);
+        cur ^= 1;
+        n_live = n_new;
+        continue;
+      }
       const int ksel = std::min(width, V);
       if (constrained)
         launch_row_topk_trie(rows, V, ksel, logits_, bs_[cur].score, bs_[cur].lexrank, bs_[cur].node, trie_, lse_,
                              cand_, st_);
       else
         launch_row_topk(rows, V, ksel, logits_, bs_[cur].score, bs_[cur].lexrank, lse_, cand_, topk_fail_, st_);
-      const int n_new = static_cast<int>(std::min<int64_t>(width, static_cast<int64_t>(n_live) * V));
       launch_beam_merge(U, n_live, ksel, n_new, V, L, step, cand_, logits_, lse_, bs_[cur], bs_[cur ^ 1], st_,
                         constrained ? &trie_ : nullptr);
       cur ^= 1;
@@ -1874,6 +1898,9 @@ class EngineT final : public Engine {
   int32_t* topk_fail_ = nullptr;
   BeamState bs_[2];
   int32_t* nonfinite_ = nullptr;
+  bool fused_select_ = false;
+  float2* head_stats_ = nullptr;     // [V/32][Rd_] head GEMM chunk statistics
+  uint32_t* sel_scratch_ = nullptr;  // beam_select chunk keys that do not fit on chip
   int32_t* node_[2] = {nullptr, nullptr};
   // device trie (constrained search)
   Arena trie_ar_;

@@ -312,6 +312,20 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] *= rs;
     }
+    if (MODE & EPI_STATS) {  // this row's 32-column chunk: max and sum exp(x - max) (log-softmax inputs)
+      float m = fmaxf(v[0], v[1]);
+#pragma unroll
+      for (int j = 2; j < 32; ++j) m = fmaxf(m, v[j]);
+      const float2 l2 = make_float2(1.4426950408889634f, 1.4426950408889634f);
+      const float2 nm = make_float2(-m * 1.4426950408889634f, -m * 1.4426950408889634f);
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float2 t = ffma2(make_float2(v[j], v[j + 1]), l2, nm);
+        acc = fadd2(acc, make_float2(ex2_fast(t.x), ex2_fast(t.y)));
+      }
+      if (row < e.m_valid) e.stats[(long long)(col0 >> 5) * e.stats_ld + row] = make_float2(m, acc.x + acc.y);
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       s4[lane * 8 + (k ^ (lane & 7))] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
@@ -907,6 +921,12 @@ void launch_tc2_mode(int staged, const void* A, int lda, const void* B, int ldb,
     case EPI_BIAS | EPI_SILU | EPI_BF16:
       launch_tc2<BN, S, EPI_BIAS | EPI_SILU | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream);
       return;
+    case EPI_STATS:
+      if constexpr (BN == 256) {
+        launch_tc2<BN, S, EPI_STATS>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+        return;
+      }
+      throw std::invalid_argument("gemm_bf16: head statistics need 256-wide tiles");
     case EPI_SPLITVT | EPI_BF16:
       if constexpr (BN == 256) {
         launch_tc2<BN, S, EPI_SPLITVT | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream);
@@ -936,6 +956,11 @@ int epi_mode(const Epi& e) {
     return plain && !e.swiglu && !e.row_map && e.out_bf16 && e.vt_col0 > 0 && e.out &&
                    reinterpret_cast<uintptr_t>(e.out) % 16 == 0 && e.ldo % 8 == 0 && e.col_off == 0
                ? EPI_SPLITVT | EPI_BF16
+               : -1;
+  if (e.stats)  // head GEMM: fp32 logits + chunk statistics, nothing else
+    return plain && !e.swiglu && !e.row_map && !e.out_bf16 && e.col_off == 0 && e.out &&
+                   reinterpret_cast<uintptr_t>(e.out) % 16 == 0 && e.ldo % 4 == 0
+               ? EPI_STATS
                : -1;
   const int esz = e.out_bf16 ? 2 : 4;
   if ((reinterpret_cast<uintptr_t>(e.out) % 16) || ((long long)e.ldo * esz) % 16 || (e.col_off * esz) % 16) return -1;
@@ -1078,17 +1103,21 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
       const double f128 = double(t128) / (double((t128 + pairs - 1) / pairs) * pairs);
       small_n = f128 > f256 + 0.08;
     }
+    if (ep.stats) small_n = false;  // statistics are produced by the 256-wide staged epilogue only
     const int bn = small_n ? 128 : 256;
     // staged (coalesced) epilogue: specialised mode and every tile full
     const int staged = (ep.mode >= 0 && ep.n_out >= (ep.swiglu ? N / 2 : N) && N % bn == 0 &&
                         (!ep.vt || ep.vt_col0 % bn == 0))
                            ? ep.mode
                            : -1;
+    if (ep.stats && staged != EPI_STATS)
+      throw std::invalid_argument("gemm_bf16: head statistics need full, aligned 256-column tiles");
     if (small_n)
       launch_tc2_mode<128>(staged, A, lda, B, ldb, M, N, K, ep, grp, stream);
     else
       launch_tc2_mode<256>(staged, A, lda, B, ldb, M, N, K, ep, grp, stream);
   } else {
+    if (ep.stats) throw std::invalid_argument("gemm_bf16: head statistics need the CTA-pair kernel (M > 128)");
     // M <= 128 (decoder step 0): the GEMM is a weight stream; 64-wide tiles put
     // 4x more SMs on it than 256-wide ones (N=1024: 16 CTAs instead of 4)
     const bool narrow = !epi.swiglu && !grouped && N >= 512 && M <= kBM && !getenv("ORX_GEMM_NO_NARROW");

@@ -21,7 +21,8 @@ enum Act { ACT_NONE = 0, ACT_LEAKY = 1, ACT_SILU = 2 };
 enum EpiMode {
   EPI_BIAS = 1, EPI_LEAKY = 2, EPI_SILU = 4, EPI_RS = 8, EPI_RESID = 16, EPI_BF16 = 32,
   EPI_SWIGLU = 64,  // silu(a) * b over the interleaved W1|W3 accumulator (bf16 out, nothing else)
-  EPI_SPLITVT = 128  // bf16 out below Epi::vt_col0, transposed V store from it on (nothing else)
+  EPI_SPLITVT = 128,  // bf16 out below Epi::vt_col0, transposed V store from it on (nothing else)
+  EPI_STATS = 256     // fp32 out + per-(row, 32-column chunk) log-sum-exp statistics (the head GEMM)
 };
 
 struct Epi {
@@ -50,6 +51,13 @@ struct Epi {
   // columns >= vt_col0 take the transposed store (as column n - vt_col0);
   // columns below it are regular bf16 stores to out / ldo (one GEMM for K|V)
   int vt_col0 = 0;
+  // Head GEMM statistics (EPI_STATS, plain fp32 out only): for every output
+  // row r and 32-column chunk c, stats[c * stats_ld + r] = (max, sum exp(x - max))
+  // over columns [32c, 32c + 32) -- the inputs of the fused log-softmax +
+  // beam selection (beam_select, beam.cuh). Chunk-major so a warp's 32 rows
+  // store 256 contiguous bytes.
+  float2* stats = nullptr;
+  long long stats_ld = 0;
   int mode = -1;  // EpiMode bits of a specialised path, -1 = generic (set by gemm_bf16)
 };
 

@@ -73,14 +73,18 @@ __device__ uint64_t block_kth_largest(int n, int k, Get get, uint32_t* hist, uin
   return prefix;
 }
 
-// Bitonic sort (descending) of n <= NP keys in shared memory, padded with 0.
+// Bitonic sort (descending) of n <= NP keys in shared memory, padded with 0
+// up to the next power of two (a[] must hold that many).
 template <int NP, int NT>
 __device__ void block_sort_desc(uint64_t* a, int n) {
-  for (int i = n + threadIdx.x; i < NP; i += NT) a[i] = 0;
+  int np = 2;
+  while (np < n) np <<= 1;
+  if (np > NP) np = NP;
+  for (int i = n + threadIdx.x; i < np; i += NT) a[i] = 0;
   __syncthreads();
-  for (int size = 2; size <= NP; size <<= 1) {
+  for (int size = 2; size <= np; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < NP / 2; i += NT) {
+      for (int i = threadIdx.x; i < np / 2; i += NT) {
         int lo = 2 * i - (i & (stride - 1));
         int hi = lo + stride;
         bool desc = ((lo & size) == 0);
@@ -416,13 +420,11 @@ __device__ void build_next_state(int u, int n_live, int n_new, int V, int L, int
     lex[b] = (static_cast<uint64_t>(low) << 32) | static_cast<uint32_t>(b);
   }
   __syncthreads();
-  // lexicographic rank of the new prefixes = ascending (plr, code) = ascending low
-  for (int i = n_new + threadIdx.x; i < kMaxBeam; i += NT) lex[i] = ~0ull;
+  // lexicographic rank of the new prefixes = ascending (plr, code) = ascending
+  // low: sort the complements descending (padding 0 sorts last)
+  for (int i = threadIdx.x; i < n_new; i += NT) lex[i] = ~lex[i];
   __syncthreads();
-  // ascending sort: negate by sorting descending of the complement
-  for (int i = threadIdx.x; i < kMaxBeam; i += NT) lex[i] = ~lex[i];
-  __syncthreads();
-  block_sort_desc<kMaxBeam, NT>(lex, kMaxBeam);
+  block_sort_desc<kMaxBeam, NT>(lex, n_new);
   for (int r = threadIdx.x; r < n_new; r += NT) {
     const int b = static_cast<int>(static_cast<uint32_t>(~lex[r]));
     nxt.lexrank[u * n_new + b] = r;
@@ -474,8 +476,9 @@ __global__ void __launch_bounds__(kMergeThreads) beam_merge_kernel(int n_live, i
 //
 // Per parent row b: lse_b from the row's (max, sum exp) pairs of its 32-column
 // chunks (generation.cpp:10-20). Chunk key = ord(ps_b + (cmax - lse_b)), the
-// exact fp32 score of the chunk's best element. tau = the n_new-th largest
-// chunk key: at least n_new elements score >= tau, so the n_new-th best
+// exact fp32 score of the chunk's best element. tau = a chunk key with at
+// least n_new chunk keys >= tau (block_threshold32, at or just below the
+// n_new-th largest): at least n_new elements score >= tau, so the n_new-th best
 // candidate does too, and since fp32 rounding is monotone every element
 // scoring >= tau lies in a chunk whose key is >= tau. Only those chunks are
 // read (typically ~n_new of n_live * V / 32): their elements with score >=
@@ -504,91 +507,87 @@ struct SelSmem {
 constexpr size_t kSelSmemBytes = sizeof(uint32_t) * kSelChunkKeys + sizeof(SelSmem);
 static_assert(sizeof(uint32_t) * kSelChunkKeys >= sizeof(uint64_t) * kSelCand, "candidate alias");
 
-// n-th largest (with multiplicity) of n 32-bit keys: count(key >= tau) >= k and
-// tau is the largest value with that property. Bits above the highest bit in
-// which the keys differ are skipped; per-warp histograms.
+// A threshold tau over n 32-bit ordered-float keys with count(key >= tau) >= k,
+// close to the k-th largest: one 2048-bucket histogram over the float range
+// (bucket index is monotone in the key), the bucket where the count from the
+// top reaches k, tau = the smallest key in that bucket. Three passes over the
+// keys, no multi-pass radix contention.
 template <class Get>
-__device__ uint32_t block_kth_largest32(int n, int k, Get get, SelSmem& S) {
+__device__ uint32_t block_threshold32(int n, int k, Get get, SelSmem& S) {
   if (n <= k) return 0;
-  uint32_t a = 0xFFFFFFFFu, o = 0;
+  constexpr int NB = 2048;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t lo = 0xFFFFFFFFu, hi = 0;
   for (int i = threadIdx.x; i < n; i += kSelThreads) {
     const uint32_t x = get(i);
-    a &= x;
-    o |= x;
+    lo = min(lo, x);
+    hi = max(hi, x);
   }
-  a = __reduce_and_sync(0xffffffffu, a);
-  o = __reduce_or_sync(0xffffffffu, o);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
   if (lane == 0) {
-    S.hist[warp] = a;
-    S.hist[kSelWarps + warp] = o;
+    S.tot[warp] = lo;
+    S.tot[kSelWarps + warp] = hi;
   }
+  for (int b = threadIdx.x; b < NB; b += kSelThreads) S.hist[b] = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
-    uint32_t A = 0xFFFFFFFFu, O = 0;
-    for (int w = 0; w < kSelWarps; ++w) A &= S.hist[w], O |= S.hist[kSelWarps + w];
-    S.bc[0] = A;
-    S.bc[1] = O;
+    uint32_t L = 0xFFFFFFFFu, H = 0;
+    for (int w = 0; w < kSelWarps; ++w) L = min(L, S.tot[w]), H = max(H, S.tot[kSelWarps + w]);
+    S.bc[0] = L;
+    S.bc[1] = H;
+    S.bc[3] = 0xFFFFFFFFu;
   }
   __syncthreads();
-  const uint32_t A = S.bc[0], O = S.bc[1];
+  const uint32_t L = S.bc[0], H = S.bc[1];
+  if (L == H) return L;
+  const float flo = unord_f32(L), fhi = unord_f32(H);
+  float scale = static_cast<float>(NB) / (fhi - flo);
+  if (!(scale > 0.f) || !isfinite(scale)) scale = 0.f;  // degenerate range: one bucket, tau = min
+  auto bucket = [&](uint32_t x) {
+    const float f = (unord_f32(x) - flo) * scale;
+    return f >= static_cast<float>(NB - 1) ? NB - 1 : (f > 0.f ? static_cast<int>(f) : 0);
+  };
+  for (int i = threadIdx.x; i < n; i += kSelThreads) atomicAdd(&S.hist[bucket(get(i))], 1u);
   __syncthreads();
-  if (A == O) return A;  // all keys equal
-  const int hb = 31 - __clz(A ^ O);
-  const uint32_t low_mask = hb == 31 ? 0xFFFFFFFFu : ((2u << hb) - 1u);
-  uint32_t prefix = A & ~low_mask, mask = ~low_mask;
-  int krem = k;
-  int shift = hb >= 7 ? hb - 7 : 0;
-  for (;;) {
-    for (int i = threadIdx.x; i < kSelWarps * 256; i += kSelThreads) S.hist[i] = 0;
-    __syncthreads();
-    uint32_t* h = S.hist + warp * 256;
-    for (int i = threadIdx.x; i < n; i += kSelThreads) {
-      const uint32_t x = get(i);
-      if ((x & mask) == prefix) atomicAdd(&h[(x >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < 256; b += kSelThreads) {
-      uint32_t t = 0;
-#pragma unroll 4
-      for (int w = 0; w < kSelWarps; ++w) t += S.hist[w * 256 + b];
-      S.tot[b] = t;
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      uint32_t c[8], tot = 0;
+  // suffix counts: thread t owns buckets [4t, 4t + 4); scan over threads from the top
+  const int t = threadIdx.x;
+  uint32_t c4[4], own = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c[j] = S.tot[255 - 8 * lane - j];
-        tot += c[j];
-      }
-      uint32_t incl = tot;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += v;
-      }
-      uint32_t above = incl - tot;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (above < static_cast<uint32_t>(krem) && above + c[j] >= static_cast<uint32_t>(krem)) {
-          S.bc[0] = 255 - 8 * lane - j;
-          S.bc[1] = above;
-          S.bc[2] = c[j];
-        }
-        above += c[j];
-      }
-    }
-    __syncthreads();
-    const uint32_t dgt = S.bc[0], above = S.bc[1], cnt = S.bc[2];
-    __syncthreads();
-    prefix = (prefix & ~(255u << shift)) | (dgt << shift);
-    mask |= 255u << shift;
-    krem -= static_cast<int>(above);
-    if (static_cast<int>(cnt) == krem || shift == 0) break;
-    shift = shift >= 8 ? shift - 8 : 0;
+  for (int j = 0; j < 4; ++j) {
+    c4[j] = S.hist[4 * t + j];
+    own += c4[j];
   }
-  return prefix;
+  // inclusive suffix over lanes (higher lanes = higher buckets)
+  uint32_t suf = own;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_down_sync(0xffffffffu, suf, o);
+    if (lane + o < 32) suf += v;
+  }
+  if (lane == 0) S.tot[64 + warp] = suf;  // warp total
+  __syncthreads();
+  uint32_t above_warps = 0;
+  for (int w = warp + 1; w < kSelWarps; ++w) above_warps += S.tot[64 + w];
+  uint32_t above = above_warps + suf - own;  // keys in buckets above this thread's
+#pragma unroll
+  for (int j = 3; j >= 0; --j) {
+    if (above < static_cast<uint32_t>(k) && above + c4[j] >= static_cast<uint32_t>(k)) S.bc[2] = 4 * t + j;
+    above += c4[j];
+  }
+  __syncthreads();
+  const int bstar = static_cast<int>(S.bc[2]);
+  uint32_t mn = 0xFFFFFFFFu;
+  for (int i = threadIdx.x; i < n; i += kSelThreads) {
+    const uint32_t x = get(i);
+    if (bucket(x) == bstar) mn = min(mn, x);
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  if (lane == 0) atomicMin(&S.bc[3], mn);
+  __syncthreads();
+  const uint32_t tau = S.bc[3];
+  __syncthreads();
+  return tau;
 }
 
 __global__ void __launch_bounds__(kSelThreads, 1)
@@ -604,23 +603,45 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   const int NC = V >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // 1. log-softmax normaliser per parent row from its chunk statistics:
-  //    P threads per row over interleaved chunks (coalesced over rows), combined
-  //    through shared memory (S.hist as (max, sum) scratch)
+  // 1. log-softmax normaliser per parent row from its chunk statistics: P
+  //    threads per row over interleaved chunks (consecutive threads read
+  //    consecutive rows), 8 independent loads in flight per thread, online
+  //    (max, sum) combine; the chunk maxima are kept (keys[], as floats) for
+  //    step 2, the per-thread partials combined through S.hist
+  const int nck = n_live * NC;
+  const bool in_smem = nck <= kSelChunkKeys;
+  uint32_t* keys = in_smem ? ckeys : gkeys + (size_t)u * nck;
+  float* cmax = reinterpret_cast<float*>(keys);  // [c * n_live + b] before step 2
   {
     const int P = n_live >= kSelThreads ? 1 : kSelThreads / n_live;
     float2* part = reinterpret_cast<float2*>(S.hist);  // [P][n_live] (P * n_live <= 2048)
     const int Pn = P * n_live <= 2048 ? P : 2048 / n_live;
     for (int t = threadIdx.x; t < Pn * n_live; t += kSelThreads) {
       const int b = t % n_live, p = t / n_live;
-      float m = -INFINITY;
-      for (int c = p; c < NC; c += Pn) m = fmaxf(m, stats[(long long)c * stats_ld + r0 + b].x);
-      float sum = 0.f;
-      for (int c = p; c < NC; c += Pn) {
-        const float2 st = stats[(long long)c * stats_ld + r0 + b];
-        sum += st.y * __expf(st.x - m);
+      float M = -INFINITY, Ssum = 0.f;
+      for (int c0 = p; c0 < NC; c0 += 8 * Pn) {
+        float2 st[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int c = c0 + j * Pn;
+          st[j] = c < NC ? __ldg(stats + (long long)c * stats_ld + r0 + b) : make_float2(-INFINITY, 0.f);
+        }
+        float mb = M;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mb = fmaxf(mb, st[j].x);
+        float acc = M == -INFINITY ? 0.f : Ssum * __expf(M - mb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int c = c0 + j * Pn;
+          if (c < NC) {
+            acc += st[j].y * __expf(st[j].x - mb);
+            cmax[(size_t)c * n_live + b] = st[j].x;
+          }
+        }
+        M = mb;
+        Ssum = acc;
       }
-      part[p * n_live + b] = make_float2(m, sum);
+      part[p * n_live + b] = make_float2(M, Ssum);
     }
     __syncthreads();
     for (int b = threadIdx.x; b < n_live; b += kSelThreads) {
@@ -645,16 +666,13 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     __syncthreads();
   }
 
-  // 2. chunk keys (index i = c * n_live + b: consecutive threads read consecutive rows)
-  const int nck = n_live * NC;
-  const bool in_smem = nck <= kSelChunkKeys;
-  uint32_t* keys = in_smem ? ckeys : gkeys + (size_t)u * nck;
+  // 2. chunk keys in place: ord(ps + (cmax - lse)), index i = c * n_live + b
   for (int i = threadIdx.x; i < nck; i += kSelThreads) {
     const int c = i / n_live, b = i - c * n_live;
-    keys[i] = ord_f32(S.ps[b] + (stats[(long long)c * stats_ld + r0 + b].x - S.lse[b]));
+    keys[i] = ord_f32(S.ps[b] + (cmax[i] - S.lse[b]));
   }
   __syncthreads();
-  const uint32_t tau = block_kth_largest32(nck, n_new, [&](int i) { return keys[i]; }, S);
+  const uint32_t tau = block_threshold32(nck, n_new, [&](int i) { return keys[i]; }, S);
 
   // 3. the chunks that can hold a winner
   for (int i0 = warp * 32; i0 < nck; i0 += kSelThreads) {
@@ -672,11 +690,24 @@ __global__ void __launch_bounds__(kSelThreads, 1)
 
   // 4. candidates: elements of the selected chunks scoring >= tau (warp per chunk)
   if (nids <= kSelIds) {
-    for (int j = warp; j < nids; j += kSelWarps) {
-      const int i = static_cast<int>(S.ids[j]);
-      const int c = i / n_live, b = i - c * n_live;
-      const int code = c * 32 + lane;
-      const float sc = S.ps[b] + (logits[(size_t)(r0 + b) * V + code] - S.lse[b]);
+    constexpr int kU = 4;  // chunks in flight per warp
+    for (int j0 = warp; j0 < nids; j0 += kSelWarps * kU) {
+      float x[kU];
+      int bb[kU], cc[kU];
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        const int j = j0 + q * kSelWarps;
+        const int i = j < nids ? static_cast<int>(S.ids[j]) : 0;
+        cc[q] = i / n_live;
+        bb[q] = i - cc[q] * n_live;
+        x[q] = j < nids ? __ldg(logits + (size_t)(r0 + bb[q]) * V + cc[q] * 32 + lane) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+      if (j0 + q * kSelWarps >= nids) break;
+      const int b = bb[q];
+      const int code = cc[q] * 32 + lane;
+      const float sc = S.ps[b] + (x[q] - S.lse[b]);
       const uint32_t k32 = ord_f32(sc);
       const bool take = k32 >= tau;
       const uint32_t m = __ballot_sync(0xffffffffu, take);
@@ -686,6 +717,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
       const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
       if (take && pos < static_cast<uint32_t>(kSelCand))
         cand[pos] = (static_cast<uint64_t>(k32) << 32) | (0xFFFFFFFFu - (S.lbase[b] + static_cast<uint32_t>(code)));
+      }
     }
   }
   __syncthreads();

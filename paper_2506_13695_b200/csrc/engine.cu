@@ -90,6 +90,7 @@ struct Lin {  // y = x . W, W^T packed [N][K] (K padded to 8, zeros)
 struct MoeW {
   const float* gate_t = nullptr;  // [E][d]
   const float* gate_gain = nullptr;  // [E][d] gate_t[e][c] * (pre-MoE RMSNorm gain)[c]
+  const float* gate_sw = nullptr;    // gate_gain in moe_route4's swizzled shared-memory layout (E <= 24)
   const float* bias = nullptr;    // [E]
   const void* w13 = nullptr;      // bf16: [E][2h][d] interleaved per 128 rows; fp32: w1 [E][h][d]
   const void* w3 = nullptr;       // fp32 only: [E][h][d]
@@ -373,6 +374,15 @@ class EngineT final : public Engine {
     for (int e = 0; e < E; ++e)
       for (int k = 0; k < d; ++k) gt[(size_t)e * d + k] *= gain.data[k];
     m.gate_gain = upload_f32(gt.data(), gt.size());
+    if (E <= 24 && d % 128 == 0) {  // moe_route4 layout: 4-column groups x 24 swizzled (4 experts x 1 column) units
+      std::vector<float> sw(static_cast<size_t>(d) * 24, 0.f);
+      for (int e = 0; e < E; ++e)
+        for (int c = 0; c < d; ++c) {
+          const int q = c >> 2, unit = ((c & 3) * 6 + (e >> 2)) ^ (q & 7);
+          sw[(size_t)q * 96 + unit * 4 + (e & 3)] = gt[(size_t)e * d + c];
+        }
+      m.gate_sw = upload_f32(sw.data(), sw.size());
+    }
     m.bias = up(hw, n + ".routing_bias");
     const int dp = rup(d, 8), hp = rup(h, 8);
     // this rank's experts only (all of them without expert parallelism): local e -> global e0_ + e
@@ -1207,7 +1217,8 @@ class EngineT final : public Engine {
     const orx_config& c = cfg_;
     const int d = c.d_model, E = c.n_experts, k = c.experts_active;
     CUDA_CHECK(cudaMemsetAsync(counts_, 0, E * sizeof(int32_t), st_));
-    launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.gate_gain, m.bias, sel_, wts_, counts_, st_);
+    launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.gate_gain, m.bias, sel_, wts_, counts_, st_,
+                     m.gate_sw);
     if (ep_world_ > 1) {
       moe_ep(m, x, rows, h);
       return false;

@@ -691,6 +691,214 @@ __global__ void __launch_bounds__(256, 2) moe_route2_kernel(int rows, int d, int
   if (threadIdx.x < E && hist[threadIdx.x]) atomicAdd(&counts[threadIdx.x], hist[threadIdx.x]);
 }
 
+// Routing v4 (E <= 24, k <= 8, d % 128 == 0): warp per 4 rows. Lane owns
+// columns {128 i + 4 lane .. +3}. The gain-folded gate sits in shared memory
+// as 16-byte units (g_e.c .. g_e+3.c) of one column and 4 experts, 24 units per
+// 4-column group, XOR-swizzled by the group index (conflict-free LDS.128):
+// one unit feeds 2 packed FFMA2 (expert pairs x the row's x_c broadcast) per
+// row, so every gate load serves 4 rows with no operand shuffling. The 96
+// partial sums (4 rows x 24 expert slots) are reduce-scattered with a 5-level
+// butterfly: lane l ends with row (l >> 3) & 3, experts 3 (l & 7) .. +2, so each
+// row's selection runs in one 8-lane group (stable top-k by score + bias,
+// ties -> lower id, nn.cpp:127-136; softmax over the selected raw scores,
+// nn.cpp:139-147; ids ascending).
+constexpr int kRoute4Rows = 4;
+__global__ void __launch_bounds__(256, 1) moe_route4_kernel(int rows, int d, int E, int k, const float* __restrict__ x,
+                                                            int ldx, const float* __restrict__ gsw,
+                                                            const float* __restrict__ bias, int32_t* __restrict__ sel,
+                                                            float* __restrict__ wts, int32_t* __restrict__ counts) {
+  extern __shared__ float sg[];  // [d / 4 groups][24 units][4], pre-swizzled by the engine (gsw)
+  __shared__ int hist[32];
+  // The gate is a weight: staged before griddepcontrol.wait (overlaps the
+  // previous kernel's tail), 8 independent 16-byte loads in flight per thread.
+  {
+    const int n4 = 24 * d / 4;
+    float4* s4 = reinterpret_cast<float4*>(sg);
+    const float4* g4 = reinterpret_cast<const float4*>(gsw);
+    for (int i0 = threadIdx.x; i0 < n4; i0 += 8 * blockDim.x) {
+      float4 t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + j * blockDim.x;
+        if (i < n4) t[j] = __ldg(g4 + i);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (i0 + j * blockDim.x < n4) s4[i0 + j * blockDim.x] = t[j];
+    }
+  }
+  if (threadIdx.x < 32) hist[threadIdx.x] = 0;
+  pdl_begin();
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  const int grp = (lane >> 3) & 3, sub = lane & 7;
+  float bias3[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const int e = 3 * sub + j;
+    bias3[j] = e < E ? bias[e] : 0.f;
+  }
+  const float4* sg4 = reinterpret_cast<const float4*>(sg);
+  // x streams as one flat sequence of (row group, 128-column block) steps per
+  // warp, two steps of loads in flight across row-group boundaries
+  const int gstride = gridDim.x * wpb;
+  const int nb = d >> 7;
+  int pg = blockIdx.x * wpb + (threadIdx.x >> 5), pi = 0;  // next step to load
+  float4 an[2][4];
+  auto load_step = [&](float4 (&dst)[4]) {
+    if (pg * kRoute4Rows < rows) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        dst[r] = __ldg(reinterpret_cast<const float4*>(x + (size_t)min(pg * kRoute4Rows + r, rows - 1) * ldx +
+                                                       pi * 128 + lane * 4));
+    }
+    if (++pi == nb) {
+      pi = 0;
+      pg += gstride;
+      const int rn = pg * kRoute4Rows + gstride * kRoute4Rows + (lane & 3);  // the group after, into L2
+      if (lane < 4 && rn < rows)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + (size_t)rn * ldx), "r"(d * 4) : "memory");
+    }
+  };
+  load_step(an[0]);
+  load_step(an[1]);
+  for (int r0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * kRoute4Rows; r0 < rows; r0 += gstride * kRoute4Rows) {
+    float2 acc[4][12];  // [row][expert pair]
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int p = 0; p < 12; ++p) acc[r][p] = make_float2(0.f, 0.f);
+    float ss[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = lane * 4; c < d; c += 128) {
+      float4 a[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        a[r] = an[0][r];
+        an[0][r] = an[1][r];
+      }
+      load_step(an[1]);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        ss[r] += a[r].x * a[r].x + a[r].y * a[r].y + a[r].z * a[r].z + a[r].w * a[r].w;
+      const int q = c >> 2;
+      const float4* gq = sg4 + (size_t)q * 24;
+#pragma unroll
+      for (int cl = 0; cl < 4; ++cl) {
+#pragma unroll
+        for (int u = 0; u < 6; ++u) {
+          const float4 g = gq[(cl * 6 + u) ^ (lane & 7)];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const float xc = cl == 0 ? a[r].x : cl == 1 ? a[r].y : cl == 2 ? a[r].z : a[r].w;
+            acc[r][2 * u] = ffma2(make_float2(g.x, g.y), make_float2(xc, xc), acc[r][2 * u]);
+            acc[r][2 * u + 1] = ffma2(make_float2(g.z, g.w), make_float2(xc, xc), acc[r][2 * u + 1]);
+          }
+        }
+      }
+    }
+    // flat v[r * 24 + e]
+    float v[96];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int p = 0; p < 12; ++p) {
+        v[r * 24 + 2 * p] = acc[r][p].x;
+        v[r * 24 + 2 * p + 1] = acc[r][p].y;
+      }
+#pragma unroll
+    for (int lvl = 0; lvl < 5; ++lvl) {
+      const int o = 16 >> lvl;
+      const int h = 48 >> lvl;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < h; ++i) {
+        const float send = up ? v[i] : v[i + h];
+        const float keep = up ? v[i + h] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) ss[r] = warp_sum(ss[r]);
+    const int r = r0 + grp;
+    const float my_ss = grp == 0 ? ss[0] : grp == 1 ? ss[1] : grp == 2 ? ss[2] : ss[3];
+    const float inv = rsqrtf(my_ss / d + 1e-6f);
+    float sc[3], key[3];
+    bool taken[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      sc[j] = v[j] * inv;
+      key[j] = 3 * sub + j < E ? sc[j] + bias3[j] : -FLT_MAX;
+      taken[j] = 3 * sub + j >= E;
+    }
+    int ids[8];
+    float raw[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      ids[t] = 1 << 30;
+      raw[t] = -FLT_MAX;
+      if (t >= k) continue;
+      float bk = -FLT_MAX, bs = 0.f;
+      int bi = 1 << 30;
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (!taken[j] && (key[j] > bk || bi == (1 << 30))) {
+          bk = key[j];
+          bs = sc[j];
+          bi = 3 * sub + j;
+        }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {  // within the 8-lane group
+        const float k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+        const float s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (k2 > bk || (k2 == bk && i2 < bi)) {
+          bk = k2;
+          bs = s2;
+          bi = i2;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (3 * sub + j == bi) taken[j] = true;
+      ids[t] = bi;
+      raw[t] = bs;
+    }
+    // ids ascending (odd-even transposition network; unused slots hold 1 << 30)
+#pragma unroll
+    for (int pass = 0; pass < 8; ++pass)
+#pragma unroll
+      for (int a2 = pass & 1; a2 + 1 < 8; a2 += 2)
+        if (ids[a2] > ids[a2 + 1]) {
+          const int ti = ids[a2];
+          ids[a2] = ids[a2 + 1];
+          ids[a2 + 1] = ti;
+          const float tr = raw[a2];
+          raw[a2] = raw[a2 + 1];
+          raw[a2 + 1] = tr;
+        }
+    float mx = -FLT_MAX;
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      if (t < k) mx = fmaxf(mx, raw[t]);
+    float den = 0.f;
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      if (t < k) den += __expf(raw[t] - mx);
+    if (r < rows && sub < k) {
+      float rt = raw[0];
+      int it = ids[0];
+#pragma unroll
+      for (int t = 1; t < 8; ++t)
+        if (t == sub) rt = raw[t], it = ids[t];
+      sel[(size_t)r * k + sub] = it;
+      wts[(size_t)r * k + sub] = __expf(rt - mx) / den;
+      atomicAdd(&hist[it], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < E && hist[threadIdx.x]) atomicAdd(&counts[threadIdx.x], hist[threadIdx.x]);
+}
+
 // Segment offsets padded to the GEMM expert tile (128 rows, 256 for the CTA-pair kernel); tile -> expert table.
 __global__ void moe_plan_kernel(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
                                 int32_t* n_mtiles, int tile_rows) {
@@ -1145,10 +1353,24 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L
 }
 void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, const float* gain, const float* gate_t,
                       const float* gate_gain, const float* bias, int32_t* sel, float* wts, int32_t* counts,
-                      cudaStream_t s) {
+                      cudaStream_t s, const float* gate_sw) {
   if (rows <= 0) return;
   if (E > 32) throw std::invalid_argument("moe routing supports at most 32 experts");
   const int smem = E * d * 4;
+  if (gate_sw && E <= 24 && k <= 8 && d % 128 == 0 && ldx % 4 == 0 && !getenv("ORX_ROUTE_V2")) {
+    const int smem4 = 24 * d * 4;
+    const int per_block = 8 * kRoute4Rows;
+    const int blocks = std::min((rows + per_block - 1) / per_block, num_sms());  // one 8-warp block per SM
+    static int set4 = 0;
+    if (smem4 > 48 * 1024 && smem4 > set4) {
+      cudaFuncSetAttribute(moe_route4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4);
+      set4 = smem4;
+    }
+    ProfScope ps(PROF_MOE_ROUTE, s, 0.0, double(rows) * (4.0 * d + 8.0 * k));
+    launch_pdl(moe_route4_kernel, blocks, 256, smem4, s, rows, d, E, k, x, ldx, gate_sw, bias, sel, wts, counts);
+    ++launch_counter();
+    return;
+  }
   if (gate_gain && d % 4 == 0 && ldx % 4 == 0) {
     const int per_block = 8 * kRoutePerWarp;
     int blocks = std::min((rows + per_block - 1) / per_block, num_sms() * 2);

@@ -77,10 +77,11 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int n
 
 // MoE (nn.cpp:117-172)
 // Routing reads the fp32 residual x and the pre-MoE RMSNorm gain (norm recomputed in fp32).
-// gate_gain [E][d] = gain[c] * W_g[c][e] selects the fast path (d % 4 == 0).
+// gate_gain [E][d] = gain[c] * W_g[c][e] selects the fast path (d % 4 == 0);
+// gate_sw (E <= 24, d % 128 == 0) is the same in moe_route4's swizzled layout.
 void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, const float* gain, const float* gate_t,
                       const float* gate_gain, const float* bias, int32_t* sel, float* wts, int32_t* counts,
-                      cudaStream_t s);
+                      cudaStream_t s, const float* gate_sw = nullptr);
 // bf16 engine: the MoE combine fused with the next op's input (RMSNorm with
 // `gain`, or a plain bf16 copy when gain is null); false if the shape is not
 // supported (then run launch_moe_combine + the norm / convert).

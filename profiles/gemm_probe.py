@@ -22,6 +22,8 @@ SHAPES = {  # name: (M, N, K, act, bias, out_bf16, resid)
     "dec_so_resid": (16384, 1024, 1024, 0, False, False, True),
     "dec_cq": (16384, 1024, 1024, 0, False, True, False),
     "dec_sqkv": (16384, 3072, 1024, 0, False, True, False),
+    "dec0_so_resid": (128, 1024, 1024, 0, False, False, True),  # decoder step 0 (one row per user)
+    "dec0_cq": (128, 1024, 1024, 0, False, True, False),
 }
 
 

@@ -38,7 +38,8 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "users/sec (beam-searched rec lists) per box at 1/2/4/8 B200; inference MFU"
 
 BASELINE_CONFIG = {"0.015B": 1, "0.121B": 2, "0.935B": 3, "2.633B": 4}
-PROF_NAMES = ["gemm_dense", "gemm_moe", "attention", "dec_self_attn", "moe_route", "beam_topk_merge", "other"]
+PROF_NAMES = ["gemm_dense", "gemm_moe", "attention", "dec_self_attn", "moe_route", "beam_select", "other",
+              "xattn_decode", "features", "rmsnorm"]
 
 
 _JSON_OUT = None
@@ -261,6 +262,39 @@ def reference_arm(args, cfg, lens):
     emit(line)
 
 
+def parity_block(P, model, preset, width):
+    """bf16 deviation of the benchmarked engine from the reference itself
+    (tests/golden/paper_*.npz: the reference core's own encode / next_logits /
+    beam_search outputs for users 0 and 1 at this preset; tests/golden/
+    make_paper_golden.py). None when no fixture exists for the preset."""
+    import glob
+
+    import numpy as np
+    tag = preset.replace(".", "")
+    gold = os.path.join(ROOT, "tests", "golden")
+    fx = {w: [dict(np.load(p)) for p in sorted(glob.glob(os.path.join(gold, f"paper_{tag}_u*_w{w}.npz")))]
+          for w in (8, 128)}
+    if not fx[8]:
+        return None
+    batch = P.SynthBatch(1, 0, 2)
+    errs = []
+    for f in fx[8]:
+        u = int(f["user"])
+        pres = [[int(c) for c in row if c >= 0] for row in f["prefixes"]]
+        lg = model.score_prefixes(batch, [u] * len(pres), pres)
+        for i in range(len(pres)):
+            ref = f["logits"][i].astype(np.float64)
+            errs.append(float(np.abs(lg[i] - ref).max() / np.abs(ref).max()))
+    out = {"reference": "reference core (f64), tests/golden/paper_%s_*.npz" % tag, "users": 2,
+           "logits_rel_err_max": max(errs), "logits_rel_err_median": float(np.median(errs)), "rows": len(errs)}
+    for w in (8, 128):
+        if fx[w] and w <= width:
+            codes, _, _ = model.beam_search_arrays(batch, w)
+            out[f"beam_overlap_at_{w}"] = [len({tuple(c) for c in codes[int(f["user"])]} &
+                                               {tuple(c) for c in f["beam_codes"]}) for f in fx[w]]
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -402,15 +436,22 @@ def main():
     check(lib().orx_profile_enable(1))
     check(lib().orx_beam_search_staged(e, args.width, None))
     torch.cuda.synchronize()
-    n = 7
+    n = len(PROF_NAMES)
     pl, pms, pfl, pby = (C.c_int64 * n)(), (C.c_double * n)(), (C.c_double * n)(), (C.c_double * n)()
     check(lib().orx_profile_read(n, pl, pms, pfl, pby))
     check(lib().orx_profile_enable(0))
-    classes = {PROF_NAMES[i]: {"launches": pl[i], "ms": round(pms[i], 4),
-                               "tflops": (pfl[i] / (pms[i] * 1e-3) / 1e12) if pms[i] > 0 and pfl[i] > 0 else None}
-               for i in range(n)}
-    prof_total = sum(pms[i] for i in range(n))
     peaks, peak_src = load_peaks()
+    hbm_peak = peaks.get("hbm_gbs")
+    classes = {}
+    for i in range(n):
+        c = {"launches": pl[i], "ms": round(pms[i], 4),
+             "tflops": (pfl[i] / (pms[i] * 1e-3) / 1e12) if pms[i] > 0 and pfl[i] > 0 else None}
+        if pby[i] > 0 and pms[i] > 0:  # HBM-bound classes: algorithmic bytes / time vs the measured copy bandwidth
+            c["gbs"] = pby[i] / (pms[i] * 1e-3) / 1e9
+            c["frac_hbm"] = c["gbs"] / hbm_peak if hbm_peak else None
+            c["bytes_per_step"] = pby[i]
+        classes[PROF_NAMES[i]] = c
+    prof_total = sum(pms[i] for i in range(n))
     gemm_ms = pms[0] + pms[1]
     gemm_launch = pl[0] + pl[1]
     gemm_flops = pfl[0] + pfl[1]
@@ -433,6 +474,14 @@ def main():
 
     flops_u, enc_flops_u = flops_per_user(cfg, args.width, lens, fold_fc1=args.precision == "bf16")
     mfu = value / world * flops_u / (peaks["bf16_tflops"] * 1e12)
+
+    # ---- measured deviation from the reference (rank 0) ------------------------------------
+    parity = None
+    if rank == 0 and args.precision == "bf16":
+        try:
+            parity = parity_block(P, model, args.config, args.width)
+        except Exception as ex:  # reported, not fatal
+            parity = {"error": str(ex)}
 
     # ---- CPU baseline (rank 0, N=1 only) --------------------------------------------------
     cpu = None
@@ -461,7 +510,7 @@ def main():
                     "pipelined_api": "orx_beam_search_submit / orx_beam_search_collect (two requests in flight)"},
             "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
             "roofline": roofline, "kernel_classes_ms_per_step": classes,
-            "cpu_baseline": cpu, "clocks": clocks, "init_s": t_init,
+            "cpu_baseline": cpu, "clocks": clocks, "init_s": t_init, "parity": parity,
         }
         emit(line)
     if world > 1:

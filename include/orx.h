@@ -213,10 +213,13 @@ int orx_engine_stats(const orx_engine* e, int64_t* launches, int64_t* h2d_bytes,
 /* Stream the engine launches on (cudaStream_t as void*). */
 void* orx_engine_stream(orx_engine* e);
 /* Per-kernel-class CUDA-event timing (process-wide; off by default).
- * Classes: 0 dense GEMM, 1 MoE grouped GEMM, 2 attention, 3 decoder
- * self-attention, 4 MoE routing/scatter/combine, 5 beam top-k/merge, 6 other.
- * orx_profile_read fills n (<= 7) entries and resets the log. */
-#define ORX_PROF_CLASSES 7
+ * Classes: 0 dense GEMM, 1 MoE grouped GEMM, 2 encoder / QFormer attention,
+ * 3 decoder self-attention, 4 MoE routing/scatter/combine, 5 beam selection,
+ * 6 other, 7 decoder cross attention over the K/V cache, 8 record features,
+ * 9 RMSNorm. flops / bytes are algorithmic (bytes: HBM traffic the kernel must
+ * do, for the HBM-bound classes). orx_profile_read fills n (<= 10) entries and
+ * resets the log. */
+#define ORX_PROF_CLASSES 10
 int orx_profile_enable(int on);
 int orx_profile_read(int32_t n, int64_t* launches, double* ms, double* flops, double* bytes);
 

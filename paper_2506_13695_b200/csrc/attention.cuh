@@ -40,6 +40,8 @@ struct FmhaArgs {
   int ldo = 0;
   Seg q, k, o;
   double flops = 0.0;
+  int prof_cat = 2;    // PROF_ATTN; the decoder's cross attention reports as PROF_XATTN
+  double bytes = 0.0;  // algorithmic HBM bytes (cached K / V^T + Q + O) for the HBM-bound uses
 };
 bool fmha_supported(int dh);
 void launch_fmha_tc(const FmhaArgs& a, cudaStream_t s);

@@ -349,7 +349,7 @@ void launch_fmha_tc(const FmhaArgs& a, cudaStream_t s) {
   if (a.B <= 0 || a.max_q <= 0) return;
   if (a.ldq % 8 || a.ldk % 8 || a.vt_ld % 8 || a.q_col0 % 8 || a.k_col0 % 8)
     throw std::invalid_argument("fmha: strides / column offsets must be multiples of 8 elements");
-  ProfScope ps(PROF_ATTN, s, a.flops, 0.0);
+  ProfScope ps(a.prof_cat, s, a.flops, a.bytes);
   if (prof_enabled())
     prof_note("fmha B=" + std::to_string(a.B) + " heads=" + std::to_string(a.heads) + " max_q=" +
               std::to_string(a.max_q) + " k_rows=" + std::to_string(a.k_rows));

@@ -1379,6 +1379,8 @@ class EngineT final : public Engine {
         FmhaArgs f = fmha(groups, max_group_rows, qkv_, rows, d, xkv_, static_cast<long long>(maxU_) * Tn, Ld * d,
                           l * d, vt_x_ + static_cast<size_t>(l) * maxU_ * d * Tpad_, maxU_, Tpad_, vt_user, gq, gk,
                           gq, 4.0 * rows * Tn * d);
+        f.prof_cat = PROF_XATTN;  // one pass over every user's cached K and V^T, plus the beam rows' Q and O
+        f.bytes = static_cast<double>(groups) * Tn * d * 2.0 * sizeof(T) + 2.0 * rows * d * sizeof(T);
         launch_fmha_tc(f, st_);
       } else {
         const int ldkv = 2 * d * Ld;

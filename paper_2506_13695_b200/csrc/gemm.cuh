@@ -89,7 +89,13 @@ long long& launch_counter();
 
 // Optional per-kernel-class timing with CUDA events on the launching stream
 // (bench.py's roofline). Disabled by default; zero cost when off.
-enum ProfCat { PROF_GEMM = 0, PROF_GEMM_MOE, PROF_ATTN, PROF_DEC_SELF, PROF_MOE_ROUTE, PROF_BEAM, PROF_MISC, PROF_N };
+// PROF_ATTN: encoder / QFormer attention (tensor-bound); PROF_XATTN: decoder
+// cross attention over the cached encoder K / V (HBM-bound); PROF_FEAT: record
+// feature gathers / the folded pathway fc1; PROF_NORM: RMSNorm passes.
+enum ProfCat {
+  PROF_GEMM = 0, PROF_GEMM_MOE, PROF_ATTN, PROF_DEC_SELF, PROF_MOE_ROUTE, PROF_BEAM, PROF_MISC,
+  PROF_XATTN, PROF_FEAT, PROF_NORM, PROF_N
+};
 struct ProfScope {
   ProfScope(int cat, cudaStream_t s, double flops, double bytes);
   ~ProfScope();

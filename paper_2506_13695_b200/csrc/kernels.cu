@@ -1094,25 +1094,33 @@ inline int grid_for(long long n, int block, int cap = 148 * 32) {
     ++launch_counter();                   \
   } while (0)
 #define ORX_LAUNCH(...) ORX_LAUNCH_CAT(PROF_MISC, __VA_ARGS__)
+// with the launch's algorithmic HBM bytes (bench.py's per-class GB/s)
+#define ORX_LAUNCH_CATB(cat, bytes, ...)    \
+  do {                                      \
+    ProfScope ps__(cat, s, 0.0, (bytes));   \
+    __VA_ARGS__;                            \
+    ++launch_counter();                     \
+  } while (0)
 
 template <class T>
 void launch_features(const RecordsDev& r, const FeatureTables& t, T* out, int ldo, cudaStream_t s) {
   if (r.n <= 0) return;
+  const double nb = double(r.n) * (double(ldo) * sizeof(T) + 28.0);  // feature rows out, scalar inputs in
   const bool vec = t.d % 8 == 0 && ldo % 8 == 0 && (t.vid_only || (t.aid_dim % 8 == 0 && t.minor % 8 == 0));
   if constexpr (sizeof(T) == 2) {
     if (vec && t.vid16 && t.aid16 && !t.use_sid && !t.vid_only && ldo <= 8 * 32 * kFeatMaxChunks) {
       const size_t tsm = sizeof(float) * (8 + t.n_flags) * t.minor;
       if (tsm > 48 * 1024) cudaFuncSetAttribute(features16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsm));
-      ORX_LAUNCH(launch_pdl(features16_kernel, grid_for(r.n, 8, num_sms() * 8), 256, tsm, s, 
+      ORX_LAUNCH_CATB(PROF_FEAT, nb, launch_pdl(features16_kernel, grid_for(r.n, 8, num_sms() * 8), 256, tsm, s, 
           r, t, reinterpret_cast<__nv_bfloat16*>(out), ldo));
       return;
     }
   }
   if (vec) {
-    ORX_LAUNCH(launch_pdl(features8_kernel<T>, grid_for(r.n, 8, num_sms() * 8), 256, 0, s, r, t, out, ldo));
+    ORX_LAUNCH_CATB(PROF_FEAT, nb, launch_pdl(features8_kernel<T>, grid_for(r.n, 8, num_sms() * 8), 256, 0, s, r, t, out, ldo));
     return;
   }
-  ORX_LAUNCH(launch_pdl(features_kernel<T>, grid_for(r.n, 1, 148 * 16), 256, 0, s, r, t, out, ldo));
+  ORX_LAUNCH_CATB(PROF_FEAT, nb, launch_pdl(features_kernel<T>, grid_for(r.n, 1, 148 * 16), 256, 0, s, r, t, out, ldo));
 }
 bool fold_features_supported(int d, int n_flags) {
   const int g = (d + 255) / 256;
@@ -1124,7 +1132,9 @@ void launch_fold_features(const RecordsDev& r, const FoldTables& f, __nv_bfloat1
     throw std::invalid_argument("fold_features: unsupported shape");
   const int g = (f.d + 255) / 256, rpb = 8 / g;
   const int grid = static_cast<int>(std::min<long long>((r.n + rpb - 1) / rpb, num_sms() * 3LL));  // 80 regs: 3 blocks per SM
-  auto go = [&](auto kern) { ORX_LAUNCH(launch_pdl(kern, grid, 256, 0, s, r, f, out, ldo)); };
+  // records' scalar inputs in, bf16 hidden rows out (the table gathers are L2 hits)
+  const double nb = double(r.n) * (2.0 * f.d + 28.0);
+  auto go = [&](auto kern) { ORX_LAUNCH_CATB(PROF_FEAT, nb, launch_pdl(kern, grid, 256, 0, s, r, f, out, ldo)); };
   if (g == 1) go(fold_features_kernel<1>);
   else if (g == 2) go(fold_features_kernel<2>);
   else if (g == 4) go(fold_features_kernel<4>);
@@ -1182,16 +1192,17 @@ __global__ void __launch_bounds__(256, 2) rmsnorm4_kernel(int rows, int d, const
 template <class T>
 void launch_rmsnorm(int rows, int d, const float* x, int ldx, const float* gain, T* out, int ldo, cudaStream_t s) {
   if (rows <= 0) return;
+  const double nb = double(rows) * d * (4.0 + sizeof(T));  // fp32 row in, normalised row out
   const bool vec = d % 4 == 0 && ldx % 4 == 0 && ldo % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
                    reinterpret_cast<uintptr_t>(gain) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
   if (vec && d <= 512) {
-    ORX_LAUNCH(launch_pdl(rmsnorm4_kernel<T, 4>, (rows + 7) / 8, 256, 0, s, rows, d, x, ldx, gain, out, ldo));
+    ORX_LAUNCH_CATB(PROF_NORM, nb, launch_pdl(rmsnorm4_kernel<T, 4>, (rows + 7) / 8, 256, 0, s, rows, d, x, ldx, gain, out, ldo));
   } else if (vec && d <= 1024) {
-    ORX_LAUNCH(launch_pdl(rmsnorm4_kernel<T, 8>, (rows + 7) / 8, 256, 0, s, rows, d, x, ldx, gain, out, ldo));
+    ORX_LAUNCH_CATB(PROF_NORM, nb, launch_pdl(rmsnorm4_kernel<T, 8>, (rows + 7) / 8, 256, 0, s, rows, d, x, ldx, gain, out, ldo));
   } else if (vec && d <= 2048) {
-    ORX_LAUNCH(launch_pdl(rmsnorm4_kernel<T, 16>, (rows + 7) / 8, 256, 0, s, rows, d, x, ldx, gain, out, ldo));
+    ORX_LAUNCH_CATB(PROF_NORM, nb, launch_pdl(rmsnorm4_kernel<T, 16>, (rows + 7) / 8, 256, 0, s, rows, d, x, ldx, gain, out, ldo));
   } else {
-    ORX_LAUNCH(launch_pdl(rmsnorm_kernel<T>, (rows + 7) / 8, 256, 0, s, rows, d, x, ldx, gain, out, ldo));
+    ORX_LAUNCH_CATB(PROF_NORM, nb, launch_pdl(rmsnorm_kernel<T>, (rows + 7) / 8, 256, 0, s, rows, d, x, ldx, gain, out, ldo));
   }
 }
 template <class T>
@@ -1326,12 +1337,14 @@ template <class T>
 void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L, const T* qkv, T* const* cache,
                           const int32_t* anc, int anc_stride, T* out, cudaStream_t s) {
   if (rows <= 0) return;
+  // per row: q, k, v in; the ancestors' cached k, v; out row; this position's k, v into the cache
+  const double nb = double(rows) * d * sizeof(T) * (3.0 + 2.0 * step + 1.0 + 2.0);
   long long warps = (long long)rows * heads;
   if constexpr (sizeof(T) == 2) {
     const int dh = d / heads, epl = d / 32, lph = epl > 0 ? dh / epl : 0;
     if (d % 256 == 0 && epl <= 64 && dh % epl == 0 && (lph & (lph - 1)) == 0 && step < 8) {  // whole row per warp
       auto go = [&](auto kern) {
-        ORX_LAUNCH_CAT(PROF_DEC_SELF, launch_pdl(kern, (rows + 7) / 8, 256, 0, s, rows, d, heads, step, layer, L,
+        ORX_LAUNCH_CATB(PROF_DEC_SELF, nb, launch_pdl(kern, (rows + 7) / 8, 256, 0, s, rows, d, heads, step, layer, L,
                                                  reinterpret_cast<const __nv_bfloat16*>(qkv),
                                                  reinterpret_cast<__nv_bfloat16* const*>(cache), anc, anc_stride,
                                                  reinterpret_cast<__nv_bfloat16*>(out)));
@@ -1344,11 +1357,11 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L
     }
   }
   if ((d / heads) % 4 == 0 && d / heads <= 128 && d % 4 == 0) {
-    ORX_LAUNCH_CAT(PROF_DEC_SELF, launch_pdl(dec_self_attn4_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, 
+    ORX_LAUNCH_CATB(PROF_DEC_SELF, nb, launch_pdl(dec_self_attn4_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, 
         rows, d, heads, step, layer, L, qkv, cache, anc, anc_stride, out));
     return;
   }
-  ORX_LAUNCH_CAT(PROF_DEC_SELF, launch_pdl(dec_self_attn_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, 
+  ORX_LAUNCH_CATB(PROF_DEC_SELF, nb, launch_pdl(dec_self_attn_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, 
       rows, d, heads, step, layer, L, qkv, cache, anc, anc_stride, out));
 }
 void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, const float* gain, const float* gate_t,
@@ -1401,18 +1414,19 @@ void launch_moe_plan(int E, const int32_t* counts, int32_t* cursor, int32_t* til
 template <class T>
 void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
                         int32_t* cursor, int32_t* slot, T* xg, float* row_scale, cudaStream_t s) {
+  const double nb = double(rows) * d * sizeof(T) * (1.0 + k);  // token rows in, k expert-sorted copies out
   if (rows <= 0) return;
   long long warps = (long long)rows * k;
   if constexpr (sizeof(T) == 2) {
     if (d % 8 == 0 && ldx % 8 == 0 && warps >= 8192) {  // many pairs: aggregate the slot atomics per warp
       const long long w32 = (warps + 31) / 32;
-      ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_scatter32_kernel, static_cast<int>((w32 + 7) / 8), 256, 0, s, 
+      ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_scatter32_kernel, static_cast<int>((w32 + 7) / 8), 256, 0, s, 
                                          rows, k, d, reinterpret_cast<const __nv_bfloat16*>(x), ldx, sel, wts, cursor,
                                          slot, reinterpret_cast<__nv_bfloat16*>(xg), row_scale));
       return;
     }
   }
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_scatter_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, rows, k, d, x, ldx, sel, wts,
+  ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_scatter_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, rows, k, d, x, ldx, sel, wts,
                                                                                       cursor, slot, xg, row_scale));
 }
 // h += sum_j yg[slot[r][j]] (as moe_combine4_kernel, same order), then the
@@ -1469,23 +1483,25 @@ bool launch_moe_combine_norm(int rows, int k, int d, const float* yg, const int3
       getenv("ORX_NO_COMBINE_NORM"))
     return false;
   if (rows <= 0) return true;
+  const double nb = double(rows) * d * (4.0 * k + 8.0 + 2.0);  // k expert outputs + residual in/out + bf16 row
   if (d == 1024)
-    ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_combine_norm_kernel<8>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
+    ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_norm_kernel<8>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
                                               slot, h, ldh, gain, out, ldo));
   else
-    ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_combine_norm_kernel<4>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
+    ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_norm_kernel<4>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
                                               slot, h, ldh, gain, out, ldo));
   return true;
 }
 
 void launch_moe_combine(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
                         cudaStream_t s) {
+  const double nb = double(rows) * d * (4.0 * k + 8.0 + 2.0);  // k expert outputs + residual in/out (+ bf16 row)
   if (rows <= 0) return;
   if (d % 4 == 0 && ldh % 4 == 0) {
-    ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_combine4_kernel, grid_for((long long)rows * d / 4, 256, num_sms() * 8), 256, 0, s, rows, k, d, yg, slot, h, ldh));
+    ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine4_kernel, grid_for((long long)rows * d / 4, 256, num_sms() * 8), 256, 0, s, rows, k, d, yg, slot, h, ldh));
     return;
   }
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_combine_kernel, rows, 256, 0, s, rows, k, d, yg, slot, h, ldh));
+  ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_kernel, rows, 256, 0, s, rows, k, d, yg, slot, h, ldh));
 }
 void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, cudaStream_t s) {
   if (n <= 0) return;

@@ -298,8 +298,10 @@ class EngineT final : public Engine {
     cudaSetDevice(dev_);
     cudaStreamSynchronize(st_);
     for (auto& g : graphs_) cudaGraphExecDestroy(g.exec);
+    for (size_t p = 0; p < ep_peer_base_.size(); ++p)
+      if (static_cast<int>(p) != ep_rank_ && ep_peer_base_[p]) cudaIpcCloseMemHandle(ep_peer_base_[p]);
+    if (ep_region_) cudaFree(ep_region_);
     if (comm_) nccl().CommDestroy(comm_);
-    if (h_ep_) cudaFreeHost(h_ep_);
     for (int k = 0; k < 2; ++k) {
       if (host_stage_[k]) cudaFreeHost(host_stage_[k]);
       if (host_out_[k]) cudaFreeHost(host_out_[k]);
@@ -727,22 +729,7 @@ class EngineT final : public Engine {
         ga_ = ar_.alloc<float>(static_cast<size_t>(S_) * h);
         gb_ = ar_.alloc<float>(static_cast<size_t>(S_) * h);
       }
-      if (ep_world_ > 1) {
-        send_cap_ = mrows * k;
-        recv_cap_ = grouped;
-        xs_ = ar_.alloc<T>(static_cast<size_t>(send_cap_) * d);
-        ws_ = ar_.alloc<float>(send_cap_);
-        yr_ = ar_.alloc<float>(static_cast<size_t>(send_cap_) * d);
-        xr_ = ar_.alloc<T>(static_cast<size_t>(recv_cap_) * d);
-        wr_ = ar_.alloc<float>(recv_cap_);
-        perm_ = ar_.alloc<int32_t>(recv_cap_);
-        ys_ = ar_.alloc<float>(static_cast<size_t>(recv_cap_) * d);
-        all_counts_ = ar_.alloc<int32_t>(static_cast<size_t>(ep_world_) * E);
-        // upload region [tab: world*El*3 | tile_expert: max_tiles | n_mtiles: 1]
-        const size_t up = static_cast<size_t>(ep_world_) * El_ * 3 + max_tiles_ + 1;
-        ep_up_ = ar_.alloc<int32_t>(up);
-        CUDA_CHECK(cudaMallocHost(&h_ep_, (static_cast<size_t>(ep_world_) * E + up) * sizeof(int32_t)));
-      }
+      if (ep_world_ > 1) setup_ep_exchange(mrows * k, S_);
     }
     // user batch staging: two slots (pinned host + device), grown on demand; a
     // copy stream moves slot s while the compute stream still runs the other
@@ -1219,10 +1206,7 @@ class EngineT final : public Engine {
     CUDA_CHECK(cudaMemsetAsync(counts_, 0, E * sizeof(int32_t), st_));
     launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.gate_gain, m.bias, sel_, wts_, counts_, st_,
                      m.gate_sw);
-    if (ep_world_ > 1) {
-      moe_ep(m, x, rows, h);
-      return false;
-    }
+    if (ep_world_ > 1) return moe_ep(m, x, rows, h, post, post_gain);
     launch_moe_plan(E, counts_, cursor_, tile_expert_, max_tiles_, n_mtiles_, kMoeTile, st_);
     launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xg_, row_scale_, st_);
     expert_ffn(m, static_cast<int>(S_), static_cast<long long>(rows) * k);
@@ -1278,64 +1262,120 @@ class EngineT final : public Engine {
     }
   }
 
-  // Expert-parallel MoE: every rank routes its own tokens,
-  // sends each (token, expert) row with its gate weight to the rank owning
-  // the expert (NCCL send/recv over NVLink), runs the grouped GEMMs of its
-  // local experts on what it received, and sends the weighted outputs back;
-  // the combine (ascending expert id) runs where the token lives. Every row
-  // goes through the same kernels as on one GPU, so the result is bitwise
-  // identical to the replica path. All ranks must run the same sequence of
-  // engine calls (same number of MoE layers), with any number of rows.
-  void moe_ep(const MoeW& m, const T* x, int rows, float* h) {
-    const orx_config& c = cfg_;
-    const int d = c.d_model, E = c.n_experts, k = c.experts_active, W = ep_world_, El = El_;
-    const ncclDataType_t dt = kBf16 ? ncclBfloat16 : ncclFloat32;
-    NCCL_CHECK(nccl().AllGather(counts_, all_counts_, E, ncclInt32, comm_, st_));
-    CUDA_CHECK(cudaMemcpyAsync(h_ep_, all_counts_, static_cast<size_t>(W) * E * 4, cudaMemcpyDeviceToHost, st_));
-    launch_ep_send_plan(E, counts_, cursor_, st_);
-    launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xs_, ws_, st_);
+  // Symmetric exchange region of an expert-parallel engine: one cudaMalloc per
+  // rank, same layout on every rank, mapped into every peer by CUDA IPC (the
+  // handles travel once, at engine creation, over the NCCL communicator).
+  void setup_ep_exchange(int64_t send_cap, int64_t recv_cap) {
+    const int d = cfg_.d_model, E = cfg_.n_experts, W = ep_world_;
+    require(W <= kEpMaxWorld, "expert parallelism supports at most 8 ranks");
+    require(send_cap < (1 << 24) && recv_cap < (int64_t(1) << 31), "expert-parallel exchange too large");
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      const size_t o = off;
+      off += (bytes + 255) / 256 * 256;
+      return o;
+    };
+    const size_t o_xr = take(static_cast<size_t>(recv_cap) * d * sizeof(T));
+    const size_t o_wr = take(static_cast<size_t>(recv_cap) * 4);
+    const size_t o_src = take(static_cast<size_t>(recv_cap) * 4);
+    const size_t o_yr = take(static_cast<size_t>(send_cap) * d * 4);
+    const size_t o_cnt = take(static_cast<size_t>(W) * E * 4);
+    const size_t o_flag = take(static_cast<size_t>(3) * W * 4);
+    CUDA_CHECK(cudaMalloc(&ep_region_, off));
+    CUDA_CHECK(cudaMemset(ep_region_, 0, off));
+    cudaIpcMemHandle_t mine;
+    CUDA_CHECK(cudaIpcGetMemHandle(&mine, ep_region_));
+    // all-gather the handles (NCCL moves device memory)
+    uint8_t* dh = nullptr;
+    CUDA_CHECK(cudaMalloc(&dh, static_cast<size_t>(W) * sizeof(mine)));
+    CUDA_CHECK(cudaMemcpy(dh + static_cast<size_t>(ep_rank_) * sizeof(mine), &mine, sizeof(mine),
+                          cudaMemcpyHostToDevice));
+    NCCL_CHECK(nccl().AllGather(dh + static_cast<size_t>(ep_rank_) * sizeof(mine), dh, sizeof(mine), ncclUint8,
+                                comm_, st_));
+    std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(W));
     CUDA_CHECK(cudaStreamSynchronize(st_));
-    const int32_t* cnt = h_ep_;  // [W][E]
-    int32_t* up = h_ep_ + static_cast<size_t>(W) * E;  // [tab | tile_expert | n_mtiles]
-    int32_t* tiles = up + static_cast<size_t>(W) * El * 3;
-    const EpPlan pl = ep_plan(W, ep_rank_, E, cnt, kMoeTile, max_tiles_, up, tiles);
-    if (pl.total_recv > recv_cap_) throw RuntimeError("expert-parallel receive buffer overflow");
-    const int n_tiles = pl.n_tiles;
-    tiles[max_tiles_] = n_tiles;
-    const auto &send_cnt = pl.send_cnt, &send_off = pl.send_off, &recv_cnt = pl.recv_cnt, &recv_off = pl.recv_off;
-    const int64_t total_recv = pl.total_recv;
-    const size_t up_n = static_cast<size_t>(W) * El * 3 + max_tiles_ + 1;
-    CUDA_CHECK(cudaMemcpyAsync(ep_up_, up, up_n * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
-    // dispatch: rows (and their gate weights) to the experts' ranks
-    NCCL_CHECK(nccl().GroupStart());
+    CUDA_CHECK(cudaMemcpy(all.data(), dh, static_cast<size_t>(W) * sizeof(mine), cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaFree(dh));
+    ep_peer_base_.assign(static_cast<size_t>(W), nullptr);
     for (int p = 0; p < W; ++p) {
-      if (send_cnt[p]) {
-        NCCL_CHECK(nccl().Send(xs_ + send_off[p] * d, send_cnt[p] * d, dt, p, comm_, st_));
-        NCCL_CHECK(nccl().Send(ws_ + send_off[p], send_cnt[p], ncclFloat32, p, comm_, st_));
+      if (p == ep_rank_) {
+        ep_peer_base_[p] = ep_region_;
+      } else {
+        CUDA_CHECK(cudaIpcOpenMemHandle(&ep_peer_base_[p], all[p], cudaIpcMemLazyEnablePeerAccess));
       }
-      if (recv_cnt[p]) {
-        NCCL_CHECK(nccl().Recv(xr_ + recv_off[p] * d, recv_cnt[p] * d, dt, p, comm_, st_));
-        NCCL_CHECK(nccl().Recv(wr_ + recv_off[p], recv_cnt[p], ncclFloat32, p, comm_, st_));
-      }
+      uint8_t* b = static_cast<uint8_t*>(ep_peer_base_[p]);
+      ep_.xr[p] = b + o_xr;
+      ep_.wr[p] = reinterpret_cast<float*>(b + o_wr);
+      ep_.src[p] = reinterpret_cast<int32_t*>(b + o_src);
+      ep_.yr[p] = reinterpret_cast<float*>(b + o_yr);
+      ep_.cnt[p] = reinterpret_cast<int32_t*>(b + o_cnt);
+      ep_.flag[p] = reinterpret_cast<uint32_t*>(b + o_flag);
     }
-    NCCL_CHECK(nccl().GroupEnd());
+    ep_.me = ep_rank_;
+    ep_.world = W;
+    ep_.recv_cap = static_cast<int>(recv_cap);
+    ep_.epoch = ar_.alloc<uint32_t>(4);
+    ep_.err = ar_.alloc<int32_t>(1);
+    CUDA_CHECK(cudaMemset(ep_.epoch, 0, 16));
+    CUDA_CHECK(cudaMemset(ep_.err, 0, 4));
+    ep_seg_ = ar_.alloc<int32_t>(2 * El_);
+    ep_tiles_ = ar_.alloc<int32_t>(max_tiles_);
+    ep_ntiles_ = ar_.alloc<int32_t>(1);
+    CUDA_CHECK(cudaDeviceSynchronize());
+  }
+
+  // Expert-parallel MoE: every rank routes its own tokens
+  // and writes each (token, expert) row with its gate weight straight into the
+  // expert owner's grouped GEMM buffer over NVLink (peer stores at offsets the
+  // device plans from the all-gathered histograms); each rank runs the grouped
+  // GEMMs of its local experts on what arrived and writes every weighted
+  // output back into the token rank's return buffer; the combine (ascending
+  // expert id) runs where the token lives. Arrival counters order the phases,
+  // so the whole exchange is device-side and replays from a CUDA graph. Every
+  // row goes through the same kernels as on one GPU: bitwise identical to the
+  // replica engine. All ranks must run the same sequence of engine calls.
+  bool moe_ep(const MoeW& m, const T* x, int rows, float* h, T* post, const float* post_gain) {
+    const orx_config& c = cfg_;
+    const int d = c.d_model, E = c.n_experts, k = c.experts_active;
+    launch_ep_counts(E, counts_, ep_, st_);
+    launch_ep_wait(ep_, EP_COUNTS, st_);
+    launch_ep_plan(E, ep_, kMoeTile, max_tiles_, cursor_, ep_tiles_, ep_ntiles_, ep_seg_, st_);
+    launch_ep_dispatch<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, El_, ep_, st_);
+    launch_ep_signal(ep_, EP_DISPATCH, st_);
+    launch_ep_wait(ep_, EP_DISPATCH, st_);
+    // grouped GEMMs of the local experts over the received rows (in place)
+    T* saved_xg = xg_;
+    float* saved_rs = row_scale_;
     int32_t* saved_te = tile_expert_;
     int32_t* saved_nm = n_mtiles_;
-    tile_expert_ = ep_up_ + static_cast<size_t>(W) * El * 3;
-    n_mtiles_ = tile_expert_ + max_tiles_;
-    launch_ep_permute<T>(static_cast<int>(total_recv), W * El, ep_up_, d, xr_, wr_, xg_, row_scale_, perm_, st_);
-    expert_ffn(m, std::max(1, n_tiles) * kMoeTile, total_recv);
+    xg_ = static_cast<T*>(ep_.xr[ep_rank_]);
+    row_scale_ = ep_.wr[ep_rank_];
+    tile_expert_ = ep_tiles_;
+    n_mtiles_ = ep_ntiles_;
+    expert_ffn(m, static_cast<int>(S_), static_cast<long long>(rows) * k);  // FLOPs: this rank's share on average
+    xg_ = saved_xg;
+    row_scale_ = saved_rs;
     tile_expert_ = saved_te;
     n_mtiles_ = saved_nm;
-    launch_ep_unpermute(static_cast<int>(total_recv), d, yg_, perm_, ys_, st_);
-    // combine: weighted expert outputs back to the tokens' ranks
-    NCCL_CHECK(nccl().GroupStart());
-    for (int p = 0; p < W; ++p) {
-      if (recv_cnt[p]) NCCL_CHECK(nccl().Send(ys_ + recv_off[p] * d, recv_cnt[p] * d, ncclFloat32, p, comm_, st_));
-      if (send_cnt[p]) NCCL_CHECK(nccl().Recv(yr_ + send_off[p] * d, send_cnt[p] * d, ncclFloat32, p, comm_, st_));
+    launch_ep_return(El_, d, ep_seg_, yg_, ep_, st_);
+    launch_ep_signal(ep_, EP_RETURN, st_);
+    launch_ep_wait(ep_, EP_RETURN, st_);
+    float* yr = ep_.yr[ep_rank_];
+    if constexpr (kBf16) {
+      if (post && launch_moe_combine_norm(rows, k, d, yr, slot_, h, d, post_gain, post, d, st_)) return true;
     }
-    NCCL_CHECK(nccl().GroupEnd());
-    launch_moe_combine(rows, k, d, yr_, slot_, h, d, st_);
+    launch_moe_combine(rows, k, d, yr, slot_, h, d, st_);
+    return false;
+  }
+
+  // Expert-parallel exchange failures (peer timeout, capacity) surface here.
+  void check_ep() {
+    if (ep_world_ <= 1) return;
+    int32_t e = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&e, ep_.err, 4, cudaMemcpyDeviceToHost, st_));
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    if (e == 1) throw RuntimeError("expert-parallel exchange: a peer did not arrive within 30 s");
+    if (e == 2) throw RuntimeError("expert-parallel exchange: receive buffer overflow");
   }
 
   void prepare_decoder(int U) {
@@ -1418,6 +1458,7 @@ class EngineT final : public Engine {
     }
     CUDA_CHECK(cudaStreamSynchronize(st_));
     CUDA_CHECK(cudaGetLastError());
+    check_ep();
     if (z_out) require_finite(z_out, static_cast<size_t>(sg_.U) * enc_seq_len(cfg_) * cfg_.d_model);
   }
 
@@ -1532,9 +1573,9 @@ class EngineT final : public Engine {
     const int U = sg_.U, V = c.codebook_size, L = c.n_code_layers;
     // The whole encode + decode + prune sequence is replayed from a CUDA graph
     // when the request has the same shapes as a captured one (no host work
-    // or launch gaps between its ~250 kernels); expert-parallel engines (host
-    // sync per MoE layer) and profiling runs launch directly.
-    const bool graphs = ep_world_ == 1 && !prof_enabled() && !getenv("ORX_NO_GRAPH");
+    // or launch gaps between its ~250 kernels; the expert-parallel exchange is
+    // device-side too); profiling runs launch directly.
+    const bool graphs = !prof_enabled() && !getenv("ORX_NO_GRAPH");
     int n_live = 1;
     for (int step = 0; step < L; ++step) n_live = static_cast<int>(std::min<int64_t>(width, (int64_t)n_live * V));
     int cur = L % 2;
@@ -1628,10 +1669,12 @@ class EngineT final : public Engine {
     if (!pd.has_out || !out) {
       CUDA_CHECK(cudaEventSynchronize(dev_free_[pd.slot]));
       CUDA_CHECK(cudaGetLastError());
+    check_ep();
       return;
     }
     CUDA_CHECK(cudaEventSynchronize(out_ready_[pd.slot]));
     CUDA_CHECK(cudaGetLastError());
+    check_ep();
     const int U = pd.U, n_live = pd.n_live, width = pd.width;
     const size_t nc = static_cast<size_t>(U) * n_live * L;
     const uint8_t* ho = static_cast<const uint8_t*>(host_out_[pd.slot]);
@@ -1658,6 +1701,7 @@ class EngineT final : public Engine {
     collect_beam(out);
     CUDA_CHECK(cudaStreamSynchronize(st_));
     CUDA_CHECK(cudaGetLastError());
+    check_ep();
   }
 
   // Pipelined serving: stage + launch request i+1 while request i runs; at
@@ -1735,6 +1779,7 @@ class EngineT final : public Engine {
         }
     }
     CUDA_CHECK(cudaGetLastError());
+    check_ep();
   }
 
   void score_prefixes(int n, const int32_t* user, const int32_t* prefixes, const int32_t* prefix_len,
@@ -1791,6 +1836,7 @@ class EngineT final : public Engine {
     CUDA_CHECK(cudaMemcpyAsync(hl.data(), seq_acc_, hl.size() * 8, cudaMemcpyDeviceToHost, st_));
     CUDA_CHECK(cudaStreamSynchronize(st_));
     CUDA_CHECK(cudaGetLastError());
+    check_ep();
     d2h_bytes += static_cast<int64_t>(hc.size() * 4 + hl.size() * 8);
     require_finite(hl.data(), hl.size());
     for (int u = 0; u < U; ++u) {
@@ -1860,6 +1906,7 @@ class EngineT final : public Engine {
     CUDA_CHECK(cudaMemcpyAsync(host.data(), seq_acc_, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, st_));
     CUDA_CHECK(cudaStreamSynchronize(st_));
     CUDA_CHECK(cudaGetLastError());
+    check_ep();
     require_finite(host.data(), host.size());
     for (int r = 0; r < n; ++r) out[order[r]] = host[r];
   }
@@ -1930,10 +1977,10 @@ class EngineT final : public Engine {
   // expert parallelism
   int ep_rank_ = 0, ep_world_ = 1, e0_ = 0, El_ = 0;
   ncclComm_t comm_ = nullptr;
-  int64_t send_cap_ = 0, recv_cap_ = 0;
-  T *xs_ = nullptr, *xr_ = nullptr;
-  float *ws_ = nullptr, *wr_ = nullptr, *ys_ = nullptr, *yr_ = nullptr;
-  int32_t *perm_ = nullptr, *all_counts_ = nullptr, *ep_up_ = nullptr, *h_ep_ = nullptr;
+  EpPeers ep_{};                      // peer views of the symmetric exchange regions
+  void* ep_region_ = nullptr;          // this rank's region
+  std::vector<void*> ep_peer_base_;    // every rank's region mapped here
+  int32_t *ep_seg_ = nullptr, *ep_tiles_ = nullptr, *ep_ntiles_ = nullptr;
   // staging
   void* host_stage_[2] = {nullptr, nullptr};
   uint8_t* dev_stage_[2] = {nullptr, nullptr};

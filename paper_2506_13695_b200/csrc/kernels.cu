@@ -1020,62 +1020,179 @@ __global__ void swiglu_mul_kernel(long long n, const float* a, const float* b, f
   }
 }
 
-// ---- expert parallelism ------------------------------------------
-// Exclusive prefix of per-expert counts: compact (unpadded) send order by expert.
-__global__ void ep_send_plan_kernel(int E, const int32_t* __restrict__ counts, int32_t* __restrict__ cursor) {
-  pdl_begin();
-  const int lane = threadIdx.x;
-  int c = lane < E ? counts[lane] : 0;
-  int incl = c;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane < E) cursor[lane] = incl - c;
+// ---- expert-parallel exchange over peer memory -----------------------------
+__device__ __forceinline__ void st_release_sys_add(uint32_t* p) {
+  asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ep_signal_all(const EpPeers& P, int phase) {
+  __threadfence_system();
+  for (int p = 0; p < P.world; ++p) st_release_sys_add(P.flag[p] + phase * P.world + P.me);
 }
 
-// Received rows (source rank major, then expert) -> expert-grouped rows padded
-// to the grouped GEMM tile. tab: n_seg x (src_row, dst_row, count).
+__global__ void ep_counts_kernel(int E, const int32_t* __restrict__ counts, EpPeers P) {
+  pdl_begin();
+  for (int i = threadIdx.x; i < P.world * E; i += blockDim.x) {
+    const int p = i / E, e = i - p * E;
+    P.cnt[p][P.me * E + e] = counts[e];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) ep_signal_all(P, EP_COUNTS);
+}
+
+__global__ void ep_signal_kernel(EpPeers P, int phase) {
+  pdl_begin();
+  if (threadIdx.x == 0) ep_signal_all(P, phase);
+}
+
+// One thread spins (acquire, system scope) on the local arrival counters of
+// every source for this exchange; gives up after 30 s (err = 1) so a lost
+// peer cannot hang the GPU.
+__global__ void ep_wait_kernel(EpPeers P, int phase) {
+  pdl_begin();
+  if (threadIdx.x != 0) return;
+  const uint32_t target = P.epoch[phase] + 1;
+  const uint32_t* f = P.flag[P.me] + phase * P.world;
+  const uint64_t t0 = globaltimer_ns();
+  for (int p = 0; p < P.world; ++p) {
+    while (ld_acquire_sys(f + p) < target) {
+      if (globaltimer_ns() - t0 > 30ull * 1000000000ull) {
+        *P.err = 1;
+        break;
+      }
+      __nanosleep(200);
+    }
+  }
+  P.epoch[phase] = target;
+  __threadfence();
+}
+
+// Device plan (the same arithmetic as ep_plan.hpp, on every rank from the same
+// histograms): owner p's grouped buffer holds, per local expert el in order, a
+// segment of sum_q cnt[q][p El + el] rows (source rank major) padded to `tile`.
+__global__ void ep_plan_kernel(int E, EpPeers P, int tile, int max_tiles, int32_t* __restrict__ cursor,
+                               int32_t* __restrict__ tile_expert, int32_t* __restrict__ n_mtiles,
+                               int32_t* __restrict__ seg) {
+  pdl_begin();
+  const int32_t* cnt = P.cnt[P.me];  // local copy [W][E]
+  const int W = P.world, El = E / W;
+  __shared__ int32_t seg_start[32], tot[32];
+  const int e = threadIdx.x;
+  if (e < E) {
+    int t = 0;
+    for (int q = 0; q < W; ++q) t += cnt[q * E + e];
+    tot[e] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int p = 0; p < W; ++p) {
+      int off = 0;
+      for (int el = 0; el < El; ++el) {
+        seg_start[p * El + el] = off;
+        off += (tot[p * El + el] + tile - 1) / tile * tile;
+      }
+    }
+  }
+  __syncthreads();
+  if (e < E) {
+    int before = 0;
+    for (int q = 0; q < P.me; ++q) before += cnt[q * E + e];
+    cursor[e] = seg_start[e] + before;
+  }
+  if (threadIdx.x == 0) {
+    int nt = 0;
+    for (int el = 0; el < El; ++el) {
+      const int g = P.me * El + el;
+      seg[2 * el] = seg_start[g];
+      seg[2 * el + 1] = tot[g];
+      for (int i = 0; i < (tot[g] + tile - 1) / tile && nt < max_tiles; ++i) tile_expert[nt++] = el;
+    }
+    const int last = El ? seg_start[P.me * El + El - 1] + (tot[P.me * El + El - 1] + tile - 1) / tile * tile : 0;
+    if (last > P.recv_cap) *P.err = 2;
+    *n_mtiles = nt;
+    for (int i = nt; i < max_tiles; ++i) tile_expert[i] = -1;
+  }
+}
+
 template <class T>
-__global__ void ep_permute_kernel(int total, int n_seg, const int32_t* __restrict__ tab, int d,
-                                  const T* __restrict__ xr, const float* __restrict__ wr, T* __restrict__ xg,
-                                  float* __restrict__ row_scale, int32_t* __restrict__ perm) {
+__global__ void ep_dispatch_kernel(int rows, int k, int d, const T* __restrict__ x, int ldx,
+                                   const int32_t* __restrict__ sel, const float* __restrict__ wts,
+                                   int32_t* __restrict__ cursor, int32_t* __restrict__ slot, int El, EpPeers P) {
   pdl_begin();
   const int lane = threadIdx.x & 31;
-  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < total; r += gridDim.x * (blockDim.x >> 5)) {
-    int dst = -1;
-    for (int sgi = 0; sgi < n_seg; ++sgi) {
-      const int src = tab[3 * sgi], cnt = tab[3 * sgi + 2];
-      if (r >= src && r < src + cnt) dst = tab[3 * sgi + 1] + (r - src);
+  const int n_pairs = rows * k;
+  for (int base_pair = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base_pair < n_pairs;
+       base_pair += gridDim.x * (blockDim.x >> 5) * 32) {
+    const int gw = base_pair + lane;
+    const bool on = gw < n_pairs;
+    const int e = on ? sel[gw] : -1;
+    const unsigned act = __ballot_sync(0xffffffffu, on);
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (on && lane == leader) base = atomicAdd(&cursor[e], __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    const int pos = base + __popc(peers & ((1u << lane) - 1u));
+    const int owner = on ? e / El : 0;
+    const bool fits = pos < P.recv_cap;
+    if (on && fits) {
+      slot[gw] = gw;
+      P.wr[owner][pos] = wts[gw];
+      P.src[owner][pos] = (P.me << 24) | gw;
+    } else if (on) {
+      *P.err = 2;
     }
-    if (dst < 0) continue;
-    const T* a = xr + (size_t)r * d;
-    T* b = xg + (size_t)dst * d;
-    if (sizeof(T) == 2 && d % 8 == 0) {
-      for (int c = lane * 8; c < d; c += 256) *reinterpret_cast<uint4*>(b + c) = *reinterpret_cast<const uint4*>(a + c);
-    } else {
-      for (int c = lane; c < d; c += 32) b[c] = a[c];
-    }
-    if (lane == 0) {
-      row_scale[dst] = wr[r];
-      perm[r] = dst;
+    for (int i = 0; i < 32; ++i) {
+      if (!((act >> i) & 1u)) break;
+      const int s = __shfl_sync(0xffffffffu, pos, i);
+      const int o = __shfl_sync(0xffffffffu, owner, i);
+      if (s >= P.recv_cap) continue;
+      const int r = (base_pair + i) / k;
+      const T* a = x + (size_t)r * ldx;
+      T* b = reinterpret_cast<T*>(P.xr[o]) + (size_t)s * d;
+      if (sizeof(T) == 2 && d % 8 == 0) {
+        for (int c = lane * 8; c < d; c += 256)
+          *reinterpret_cast<uint4*>(b + c) = *reinterpret_cast<const uint4*>(a + c);
+      } else if (d % 4 == 0) {
+        for (int c = lane * 4; c < d; c += 128)
+          *reinterpret_cast<uint4*>(b + c) = *reinterpret_cast<const uint4*>(a + c);
+      } else {
+        for (int c = lane; c < d; c += 32) b[c] = a[c];
+      }
     }
   }
 }
 
-// ys[r] = yg[perm[r]]: expert outputs back to the received order.
-__global__ void ep_unpermute_kernel(int total, int d, const float* __restrict__ yg, const int32_t* __restrict__ perm,
-                                    float* __restrict__ ys) {
+// Warp per received row: the weighted expert output goes back to yr[slot] on the token's rank.
+__global__ void ep_return_kernel(int El, int d, const int32_t* __restrict__ seg, const float* __restrict__ yg,
+                                 EpPeers P) {
   pdl_begin();
   const int lane = threadIdx.x & 31;
-  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < total; r += gridDim.x * (blockDim.x >> 5)) {
-    const float* a = yg + (size_t)perm[r] * d;
-    float* b = ys + (size_t)r * d;
-    if (d % 4 == 0) {
-      for (int c = lane * 4; c < d; c += 128) *reinterpret_cast<float4*>(b + c) = *reinterpret_cast<const float4*>(a + c);
-    } else {
-      for (int c = lane; c < d; c += 32) b[c] = a[c];
+  const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), nw = gridDim.x * (blockDim.x >> 5);
+  const int32_t* src = P.src[P.me];
+  for (int el = 0; el < El; ++el) {
+    const int s0 = seg[2 * el], n = seg[2 * el + 1];
+    for (int i = wid; i < n; i += nw) {
+      const int code = src[s0 + i];
+      const int q = code >> 24, gw = code & 0xFFFFFF;
+      const float* a = yg + (size_t)(s0 + i) * d;
+      float* b = P.yr[q] + (size_t)gw * d;
+      if (d % 4 == 0) {
+        for (int c = lane * 4; c < d; c += 128)
+          *reinterpret_cast<float4*>(b + c) = *reinterpret_cast<const float4*>(a + c);
+      } else {
+        for (int c = lane; c < d; c += 32) b[c] = a[c];
+      }
     }
   }
 }
@@ -1508,20 +1625,33 @@ void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, 
   ORX_LAUNCH(launch_pdl(swiglu_mul_kernel, grid_for(n, 256), 256, 0, s, n, a, b, out));
 }
 
-void launch_ep_send_plan(int E, const int32_t* counts, int32_t* cursor, cudaStream_t s) {
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_send_plan_kernel, 1, 32, 0, s, E, counts, cursor));
+void launch_ep_counts(int E, const int32_t* counts, const EpPeers& P, cudaStream_t s) {
+  ORX_LAUNCH_CATB(PROF_MOE_ROUTE, double(P.world) * E * 4, launch_pdl(ep_counts_kernel, 1, 256, 0, s, E, counts, P));
+}
+void launch_ep_signal(const EpPeers& P, int phase, cudaStream_t s) {
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_signal_kernel, 1, 32, 0, s, P, phase));
+}
+void launch_ep_wait(const EpPeers& P, int phase, cudaStream_t s) {
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_wait_kernel, 1, 32, 0, s, P, phase));
+}
+void launch_ep_plan(int E, const EpPeers& P, int tile, int max_tiles, int32_t* cursor, int32_t* tile_expert,
+                    int32_t* n_mtiles, int32_t* seg, cudaStream_t s) {
+  if (E > 32 || E % P.world) throw std::invalid_argument("ep_plan: at most 32 experts, divisible by the world");
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE,
+                 launch_pdl(ep_plan_kernel, 1, 32, 0, s, E, P, tile, max_tiles, cursor, tile_expert, n_mtiles, seg));
 }
 template <class T>
-void launch_ep_permute(int total, int n_seg, const int32_t* tab, int d, const T* xr, const float* wr, T* xg,
-                       float* row_scale, int32_t* perm, cudaStream_t s) {
-  if (total <= 0) return;
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_permute_kernel<T>, grid_for(total, 8, num_sms() * 8), 256, 0, s, 
-                                     total, n_seg, tab, d, xr, wr, xg, row_scale, perm));
+void launch_ep_dispatch(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
+                        int32_t* cursor, int32_t* slot, int El, const EpPeers& P, cudaStream_t s) {
+  if (rows <= 0) return;
+  const double nb = double(rows) * k * (d * sizeof(T) + 8.0) + double(rows) * d * sizeof(T);
+  const long long warps = ((long long)rows * k + 31) / 32;
+  ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb,
+                  launch_pdl(ep_dispatch_kernel<T>, grid_for(warps, 8, num_sms() * 8), 256, 0, s, rows, k, d, x, ldx,
+                             sel, wts, cursor, slot, El, P));
 }
-void launch_ep_unpermute(int total, int d, const float* yg, const int32_t* perm, float* ys, cudaStream_t s) {
-  if (total <= 0) return;
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE,
-                 launch_pdl(ep_unpermute_kernel, grid_for(total, 8, num_sms() * 8), 256, 0, s, total, d, yg, perm, ys));
+void launch_ep_return(int El, int d, const int32_t* seg, const float* yg, const EpPeers& P, cudaStream_t s) {
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_return_kernel, num_sms() * 4, 256, 0, s, El, d, seg, yg, P));
 }
 
 #define INST(T)                                                                                                   \
@@ -1535,8 +1665,8 @@ void launch_ep_unpermute(int total, int d, const float* yg, const int32_t* perm,
                                         T*, cudaStream_t);                                                       \
   template void launch_moe_scatter<T>(int, int, int, const T*, int, const int32_t*, const float*, int32_t*,       \
                                       int32_t*, T*, float*, cudaStream_t);                                        \
-  template void launch_ep_permute<T>(int, int, const int32_t*, int, const T*, const float*, T*, float*, int32_t*, \
-                                     cudaStream_t);
+  template void launch_ep_dispatch<T>(int, int, int, const T*, int, const int32_t*, const float*, int32_t*,       \
+                                      int32_t*, int, const EpPeers&, cudaStream_t);
 INST(float)
 INST(__nv_bfloat16)
 

@@ -94,12 +94,42 @@ void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32
                         int32_t* seg_cursor, int32_t* slot, T* xg, float* row_scale, cudaStream_t s);
 void launch_moe_combine(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
                         cudaStream_t s);
-// Expert parallelism: compact send order, receive-side grouping, and its inverse.
-void launch_ep_send_plan(int E, const int32_t* counts, int32_t* cursor, cudaStream_t s);
+
+// ---- expert-parallel exchange over NVLink peer memory (graph-capturable) ----
+// Every rank maps every peer's symmetric exchange region (CUDA IPC); the
+// dispatch / return are device-side stores into the peers' buffers at offsets
+// computed on the device from the all-gathered routing histograms, ordered by
+// per-(phase, source) monotonic arrival counters. No host synchronisation.
+constexpr int kEpMaxWorld = 8;
+struct EpPeers {
+  void* xr[kEpMaxWorld];       // [recv_cap][d] T: expert-grouped received rows (256-row padded segments)
+  float* wr[kEpMaxWorld];      // [recv_cap] gate weight of each received row
+  int32_t* src[kEpMaxWorld];   // [recv_cap] (source rank << 24) | source (token, slot) index
+  float* yr[kEpMaxWorld];      // [send_cap][d] weighted expert outputs returned to the token's rank
+  int32_t* cnt[kEpMaxWorld];   // [W][E] routing histograms of every rank
+  uint32_t* flag[kEpMaxWorld];  // [3 phases][W sources] arrival counters
+  uint32_t* epoch = nullptr;   // local [3] exchanges completed per phase
+  int32_t* err = nullptr;      // local: 1 = wait timeout, 2 = receive capacity overflow
+  int me = 0, world = 1;
+  int recv_cap = 0;
+};
+enum EpPhase { EP_COUNTS = 0, EP_DISPATCH = 1, EP_RETURN = 2 };
+// counts[E] -> every rank's cnt[me][:], then signal EP_COUNTS
+void launch_ep_counts(int E, const int32_t* counts, const EpPeers& P, cudaStream_t s);
+// wait until every rank signalled `phase` for the current exchange
+void launch_ep_wait(const EpPeers& P, int phase, cudaStream_t s);
+void launch_ep_signal(const EpPeers& P, int phase, cudaStream_t s);
+// From the local copy of every rank's histogram: cursor[e] = where this rank's
+// rows for global expert e start in the owner's grouped buffer; this rank's
+// grouped-GEMM tile table, n_mtiles and segment (start, count) per local expert.
+void launch_ep_plan(int E, const EpPeers& P, int tile, int max_tiles, int32_t* cursor, int32_t* tile_expert,
+                    int32_t* n_mtiles, int32_t* seg, cudaStream_t s);
+// (token, slot) rows -> the experts' ranks' grouped buffers (+ gate weight, source id); slot[i] = i
 template <class T>
-void launch_ep_permute(int total, int n_seg, const int32_t* tab, int d, const T* xr, const float* wr, T* xg,
-                       float* row_scale, int32_t* perm, cudaStream_t s);
-void launch_ep_unpermute(int total, int d, const float* yg, const int32_t* perm, float* ys, cudaStream_t s);
+void launch_ep_dispatch(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
+                        int32_t* cursor, int32_t* slot, int El, const EpPeers& P, cudaStream_t s);
+// this rank's received rows' outputs (yg, grouped order) -> the tokens' ranks' yr[slot]
+void launch_ep_return(int El, int d, const int32_t* seg, const float* yg, const EpPeers& P, cudaStream_t s);
 void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, cudaStream_t s);
 
 }  // namespace orx

@@ -1,9 +1,11 @@
 """Expert-parallel MoE exchange on CPU (gloo, world size 2 and 4).
 
-Drives the engine's own host plan (csrc/ep_plan.hpp through
-orx_debug_ep_plan) with the same dispatch / regroup / return / combine steps
-as EngineT::moe_ep, with gloo all_to_all standing in for NCCL send/recv and
-numpy experts standing in for the grouped GEMMs, and checks the result
+Drives the host plan (csrc/ep_plan.hpp through orx_debug_ep_plan; the
+device plan ep_plan_kernel computes the same layout: per owner, local experts
+in order, source-rank-major rows within each expert segment, segments padded
+to the grouped-GEMM tile) with the same dispatch / regroup / return / combine
+steps as EngineT::moe_ep, with gloo all_to_all standing in for the peer-memory
+stores and numpy experts standing in for the grouped GEMMs, and checks the result
 against the single-process MoE (every rank holding all experts): identical
 per-token outputs, ascending-expert combine (nn.cpp:152-169).
 """

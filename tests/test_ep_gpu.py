@@ -1,5 +1,6 @@
-"""Expert parallelism on >= 2 GPUs: the NCCL all-to-all
-dispatch/combine engine is bitwise identical to the replica engine. Runs
+"""Expert parallelism on >= 2 GPUs: the peer-memory
+(NVLink, CUDA IPC) dispatch / return engine, replayed from CUDA graphs, is
+bitwise identical to the replica engine. Runs
 tests/ep_worker.py under torchrun; skipped on a single-GPU box."""
 import os
 import subprocess

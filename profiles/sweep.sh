@@ -12,3 +12,5 @@ for W in 32 64 256 512; do
   echo "# config 5: 0.121B, 256 users, W=$W"
   run --config 0.121B --users 256 --width $W --steps 5 --warmup 3
 done
+echo "# config 3 at the paper's production beam: 0.935B, 128 users/GPU, W=512"
+run --config 0.935B --users 128 --width 512 --steps 3 --warmup 3

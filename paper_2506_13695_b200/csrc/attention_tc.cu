@@ -18,6 +18,7 @@
 //             so S_{j+2} overwrites P_j only after P_j . V_j has read it.
 // Semantics are mha_core's (tape.cpp:822-905): softmax(Q K^T / sqrt(dh)) V,
 // max-subtracted, keys beyond the segment length masked.
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 #include <stdexcept>
@@ -66,16 +67,17 @@ struct Fmha {
   static constexpr uint32_t K_BYTES = BK * DH * 2;    // CB blocks of [64 rows x 128 B]
   static constexpr uint32_t V_BYTES = DH * BK * 2;    // [DH rows (head dims) x 64 keys]
   static constexpr int KST = 3, VST = 2;              // K ring deeper than V: S_j needs K_j first
-  static constexpr uint32_t SMEM = Q_BYTES + KST * K_BYTES + VST * V_BYTES + 256;  // + barriers
+  static constexpr uint32_t SMEM = Q_BYTES + KST * K_BYTES + VST * V_BYTES + 256;  // + barriers (17 x 8 B)
   static constexpr uint32_t TMEM_COLS = 2 * BK + DH <= 256 ? 256 : 512;  // S[2] + O
 };
 
 template <int DH>
 __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                        const __grid_constant__ CUtensorMap tmK,
-                                                       const __grid_constant__ CUtensorMap tmV, int heads,
-                                                       __nv_bfloat16* __restrict__ O, int ldo, Seg qs, Seg ks, Seg os,
-                                                       const int32_t* __restrict__ vt_user, int q_col0, int k_col0) {
+                                                       const __grid_constant__ CUtensorMap tmV, int heads, int nqt,
+                                                       int n_seg, __nv_bfloat16* __restrict__ O, int ldo, Seg qs,
+                                                       Seg ks, Seg os, const int32_t* __restrict__ vt_user,
+                                                       int q_col0, int k_col0) {
   pdl_begin();
   using F = Fmha<DH>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -91,19 +93,14 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
   uint64_t* s_full = bars + 11;   // [2]
   uint64_t& p_full = bars[13];
   uint64_t& o_done = bars[14];
-  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 15);
-
-  const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * F::BQ;
-  const int qlen = seg_len(qs, b);
-  const int qst = seg_start(qs, b), kst = seg_start(ks, b), klen = seg_len(ks, b), ost = seg_start(os, b);
-  if (q0 >= qlen || klen <= 0) return;
-  const int nb = (klen + F::BK - 1) / F::BK;
-  const int vrow0 = ((vt_user ? vt_user[b] : b) * heads + h) * DH;
+  uint64_t& q_empty = bars[15];
+  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     if ((smem_u32(smem) & 1023) != 0) __trap();  // SW128 operands need 1 KB alignment
     mbar_init(&q_full, 1);
+    mbar_init(&q_empty, 1);
     for (int s = 0; s < F::KST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -128,165 +125,217 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
   const uint32_t t_s = tmem;             // S buffers: cols [0, 64), [64, 128)
   const uint32_t t_o = tmem + 2 * F::BK;  // O: cols [128, 128 + DH)
 
+  // Persistent: this CTA walks tiles t = blockIdx.x, + gridDim.x, ...; tile t =
+  // (segment b, head h, query block qt) with t = (b * heads + h) * nqt + qt.
+  // Every role walks the same list (empty tiles skipped identically), and the
+  // K / V rings, S buffers and barrier phases run on CTA-global block counters,
+  // so the next tile's loads and QK^T overlap the current tile's tail.
+  const int total = n_seg * heads * nqt;
+  struct Tile {
+    int b, h, q0, qlen, qst, kst, klen, ost, nb, vrow0;
+  };
+  auto tile_at = [&](int t, Tile& T) {
+    T.b = t / (heads * nqt);
+    const int r = t - T.b * heads * nqt;
+    T.h = r / nqt;
+    T.q0 = (r - T.h * nqt) * F::BQ;
+    T.qlen = seg_len(qs, T.b);
+    T.klen = seg_len(ks, T.b);
+    if (T.q0 >= T.qlen || T.klen <= 0) return false;
+    T.qst = seg_start(qs, T.b);
+    T.kst = seg_start(ks, T.b);
+    T.ost = seg_start(os, T.b);
+    T.nb = (T.klen + F::BK - 1) / F::BK;
+    T.vrow0 = ((vt_user ? vt_user[T.b] : T.b) * heads + T.h) * DH;
+    return true;
+  };
+
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_normal();
-      mbar_arrive_expect_tx(&q_full, F::Q_BYTES);
-      for (int cb = 0; cb < F::CB; ++cb)
-        tma_load_2d(sQ + cb * (F::BQ * 128), &tmQ, &q_full, q_col0 + h * DH + cb * 64, qst + q0, pol);
-      // K runs one block ahead of V (V_j is consumed a softmax later than K_j)
-      for (int i = 0; i <= nb; ++i) {
-        if (i < nb) {
-          const int ks = i % F::KST;
-          if (i >= F::KST) mbar_wait(&k_empty[ks], ((i / F::KST) - 1) & 1);
-          mbar_arrive_expect_tx(&k_full[ks], F::K_BYTES);
-          for (int cb = 0; cb < F::CB; ++cb)
-            tma_load_2d(sK + ks * F::K_BYTES + cb * (F::BK * 128), &tmK, &k_full[ks], k_col0 + h * DH + cb * 64,
-                        kst + i * F::BK, pol);
+      int kc = 0, vc = 0, tc = 0;  // K blocks, V blocks, tiles loaded so far
+      Tile T;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        if (!tile_at(t, T)) continue;
+        if (tc > 0) mbar_wait(&q_empty, (tc - 1) & 1);  // the previous tile's last QK^T has read Q
+        mbar_arrive_expect_tx(&q_full, F::Q_BYTES);
+        for (int cb = 0; cb < F::CB; ++cb)
+          tma_load_2d(sQ + cb * (F::BQ * 128), &tmQ, &q_full, q_col0 + T.h * DH + cb * 64, T.qst + T.q0, pol);
+        // K runs one block ahead of V (V_j is consumed a softmax later than K_j)
+        for (int i = 0; i <= T.nb; ++i) {
+          if (i < T.nb) {
+            const int kslot = kc % F::KST;
+            if (kc >= F::KST) mbar_wait(&k_empty[kslot], ((kc / F::KST) - 1) & 1);
+            mbar_arrive_expect_tx(&k_full[kslot], F::K_BYTES);
+            for (int cb = 0; cb < F::CB; ++cb)
+              tma_load_2d(sK + kslot * F::K_BYTES + cb * (F::BK * 128), &tmK, &k_full[kslot],
+                          k_col0 + T.h * DH + cb * 64, T.kst + i * F::BK, pol);
+            ++kc;
+          }
+          const int j = i - 1;
+          if (j >= 0) {
+            const int vslot = vc % F::VST;
+            if (vc >= F::VST) mbar_wait(&v_empty[vslot], ((vc / F::VST) - 1) & 1);
+            mbar_arrive_expect_tx(&v_full[vslot], F::V_BYTES);
+            tma_load_2d(sV + vslot * F::V_BYTES, &tmV, &v_full[vslot], j * F::BK, T.vrow0, pol);
+            ++vc;
+          }
         }
-        const int j = i - 1;
-        if (j >= 0) {
-          const int vs = j % F::VST;
-          if (j >= F::VST) mbar_wait(&v_empty[vs], ((j / F::VST) - 1) & 1);
-          mbar_arrive_expect_tx(&v_full[vs], F::V_BYTES);
-          tma_load_2d(sV + vs * F::V_BYTES, &tmV, &v_full[vs], j * F::BK, vrow0, pol);
-        }
+        ++tc;
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(F::BQ, F::BK);
       constexpr uint32_t idesc_o = umma_idesc_bf16(F::BQ, DH);
-      auto issue_pv = [&](int j) {
-        const int st = j & 1, vs = j % F::VST;
-        mbar_wait(&v_full[vs], (j / F::VST) & 1);
-        mbar_wait(&p_full, j & 1);
+      // PV of global block gp (first = first block of its tile: overwrite O)
+      auto issue_pv = [&](int gp, bool first) {
+        const int st = gp & 1, vslot = gp % F::VST;
+        mbar_wait(&v_full[vslot], (gp / F::VST) & 1);
+        mbar_wait(&p_full, gp & 1);
         tc_fence_after();
-        const uint32_t b0 = smem_u32(sV + vs * F::V_BYTES);
-        // A = P_j: 128 lanes x 64 keys bf16 = 32 TMEM columns at the start of S buffer st, 8 per K=16 step
+        const uint32_t b0 = smem_u32(sV + vslot * F::V_BYTES);
+        // A = P: 128 lanes x 64 keys bf16 = 32 TMEM columns at the start of S buffer st, 8 per K=16 step
 #pragma unroll
         for (int k = 0; k < F::BK / 16; ++k)
-          tc_mma_bf16_ts(t_o, t_s + st * F::BK + k * 8, umma_desc_sw128(b0 + k * 32), idesc_o, (j | k) != 0);
+          tc_mma_bf16_ts(t_o, t_s + st * F::BK + k * 8, umma_desc_sw128(b0 + k * 32), idesc_o, !(first && k == 0));
         tc_commit(&o_done);
-        tc_commit(&v_empty[vs]);
+        tc_commit(&v_empty[vslot]);
       };
-      mbar_wait(&q_full, 0);
-      for (int j = 0; j < nb; ++j) {
-        const int st = j & 1, ks = j % F::KST;
-        mbar_wait(&k_full[ks], (j / F::KST) & 1);
+      int g = 0, tc = 0;
+      bool prev_first = false;
+      Tile T;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        if (!tile_at(t, T)) continue;
+        mbar_wait(&q_full, tc & 1);
         tc_fence_after();
-        const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + ks * F::K_BYTES);
+        for (int j = 0; j < T.nb; ++j, ++g) {
+          const int st = g & 1, kslot = g % F::KST;
+          mbar_wait(&k_full[kslot], (g / F::KST) & 1);
+          tc_fence_after();
+          const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + kslot * F::K_BYTES);
 #pragma unroll
-        for (int k = 0; k < DH / 16; ++k) {
-          const int cb = k >> 2, off = (k & 3) * 32;
-          tc_mma_bf16(t_s + st * F::BK, umma_desc_sw128(qa + cb * (F::BQ * 128) + off),
-                      umma_desc_sw128(kb + cb * (F::BK * 128) + off), idesc_s, k != 0);
+          for (int k = 0; k < DH / 16; ++k) {
+            const int cb = k >> 2, off = (k & 3) * 32;
+            tc_mma_bf16(t_s + st * F::BK, umma_desc_sw128(qa + cb * (F::BQ * 128) + off),
+                        umma_desc_sw128(kb + cb * (F::BK * 128) + off), idesc_s, k != 0);
+          }
+          tc_commit(&s_full[st]);
+          tc_commit(&k_empty[kslot]);
+          if (j == T.nb - 1) tc_commit(&q_empty);
+          if (g >= 1) issue_pv(g - 1, prev_first);
+          prev_first = j == 0;
         }
-        tc_commit(&s_full[st]);
-        tc_commit(&k_empty[ks]);
-        if (j >= 1) issue_pv(j - 1);
+        ++tc;
       }
-      issue_pv(nb - 1);
+      if (g >= 1) issue_pv(g - 1, prev_first);
     }
   } else {
     const int q = warp & 3;  // TMEM lane quadrant
     const int r = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const float scale_log2 = rsqrtf(static_cast<float>(DH)) * 1.4426950408889634f;
-    float m = -FLT_MAX, l = 0.f;
-    bool first = true;
-    for (int j = 0; j < nb; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
-      __syncwarp();  // tcgen05.ld/st are .sync.aligned: reconverge after the per-thread wait / branches
-      tc_fence_after();
-      uint32_t sa[32], sb[32];
-      tmem_ld32_async(t_s + lane_off + st * F::BK, sa);
-      tmem_ld32_async(t_s + lane_off + st * F::BK + 32, sb);
-      tmem_wait_ld();
-      const int valid = klen - j * F::BK;
-      float x[64];  // raw scores; the 1/sqrt(dh) * log2(e) scale is folded into the exponent's FMA
-#pragma unroll
-      for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(sa[i]), x[32 + i] = __uint_as_float(sb[i]);
-      if (valid < F::BK) {  // tail block only: keys beyond the segment
-#pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (i >= valid) x[i] = -INFINITY;
-      }
-      float bm = fmaxf(x[0], x[1]);
-#pragma unroll
-      for (int i = 2; i < 64; i += 2) bm = fmaxf(bm, fmaxf(x[i], x[i + 1]));  // FMNMX3
-      bm *= scale_log2;
-      float corr = 1.f;
-      bool resc = false;
-      if (first || bm > m + 8.f) {  // lazy rescale: keep a stale max unless it grew by > 2^8
-        corr = first ? 0.f : ex2_fast(m - bm);
-        resc = !first;
-        m = bm;
-        first = false;
-      }
-      const float2 sc = make_float2(scale_log2, scale_log2), nm = make_float2(-m, -m);
-      float2 acc2 = make_float2(0.f, 0.f);
-      uint32_t pk[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float2 t = ffma2(make_float2(x[2 * i], x[2 * i + 1]), sc, nm);
-        const float2 p = make_float2(ex2_fast(t.x), ex2_fast(t.y));
-        acc2 = fadd2(acc2, p);
-        pk[i] = pack_bf16(p.x, p.y);
-      }
-      const float sum = acc2.x + acc2.y;
-      l = l * corr + sum;
-      // P_j replaces S_j in TMEM (columns [0, 32) of this buffer, keys 2c / 2c+1 in column c)
-      __syncwarp();
-      tmem_st32(t_s + lane_off + st * F::BK, pk);
-      // P_{j-1} . V_{j-1} (issued when this thread finished block j-1) is normally long done
-      // by now; waiting for it every block keeps o_done at most one phase ahead of its waiters
-      // and orders the O rescale after it
-      if (j >= 1) {
-        mbar_wait(&o_done, (j - 1) & 1);
-        __syncwarp();
+    int g = 0;
+    Tile T;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      if (!tile_at(t, T)) continue;
+      float m = -FLT_MAX, l = 0.f;
+      bool first = true;
+      for (int j = 0; j < T.nb; ++j, ++g) {
+        const int st = g & 1;
+        mbar_wait(&s_full[st], (g >> 1) & 1);
+        __syncwarp();  // tcgen05.ld/st are .sync.aligned: reconverge after the per-thread wait / branches
         tc_fence_after();
-      }
-      if (__any_sync(0xffffffffu, resc)) {
-        const float c = resc ? corr : 1.f;
-#pragma unroll 1
-        for (int cc = 0; cc < DH / 32; ++cc) {
-          uint32_t o[32];
-          tmem_ld32_async(t_o + lane_off + cc * 32, o);
-          tmem_wait_ld();
+        uint32_t sa[32], sb[32];
+        tmem_ld32_async(t_s + lane_off + st * F::BK, sa);
+        tmem_ld32_async(t_s + lane_off + st * F::BK + 32, sb);
+        tmem_wait_ld();
+        const int valid = T.klen - j * F::BK;
+        float x[64];  // raw scores; the 1/sqrt(dh) * log2(e) scale is folded into the exponent's FMA
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * c);
-          tmem_st32(t_o + lane_off + cc * 32, o);
+        for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(sa[i]), x[32 + i] = __uint_as_float(sb[i]);
+        if (valid < F::BK) {  // tail block only: keys beyond the segment
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (i >= valid) x[i] = -INFINITY;
         }
+        float bm = fmaxf(x[0], x[1]);
+#pragma unroll
+        for (int i = 2; i < 64; i += 2) bm = fmaxf(bm, fmaxf(x[i], x[i + 1]));  // FMNMX3
+        bm *= scale_log2;
+        float corr = 1.f;
+        bool resc = false;
+        if (first || bm > m + 8.f) {  // lazy rescale: keep a stale max unless it grew by > 2^8
+          corr = first ? 0.f : ex2_fast(m - bm);
+          resc = !first;
+          m = bm;
+          first = false;
+        }
+        const float2 sc = make_float2(scale_log2, scale_log2), nm = make_float2(-m, -m);
+        float2 acc2 = make_float2(0.f, 0.f);
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float2 tt = ffma2(make_float2(x[2 * i], x[2 * i + 1]), sc, nm);
+          const float2 p = make_float2(ex2_fast(tt.x), ex2_fast(tt.y));
+          acc2 = fadd2(acc2, p);
+          pk[i] = pack_bf16(p.x, p.y);
+        }
+        const float sum = acc2.x + acc2.y;
+        l = l * corr + sum;
+        // P replaces S in TMEM (columns [0, 32) of this buffer, keys 2c / 2c+1 in column c)
+        __syncwarp();
+        tmem_st32(t_s + lane_off + st * F::BK, pk);
+        // the previous block's P . V (same tile) is normally long done by now; waiting
+        // for it keeps o_done at most one phase ahead and orders the O rescale after it
+        if (j >= 1) {
+          mbar_wait(&o_done, (g - 1) & 1);
+          __syncwarp();
+          tc_fence_after();
+        }
+        if (__any_sync(0xffffffffu, resc)) {
+          const float c = resc ? corr : 1.f;
+#pragma unroll 1
+          for (int cc = 0; cc < DH / 32; ++cc) {
+            uint32_t o[32];
+            tmem_ld32_async(t_o + lane_off + cc * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * c);
+            tmem_st32(t_o + lane_off + cc * 32, o);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full);
       }
-      tmem_wait_st();
-      tc_fence_before();
+      mbar_wait(&o_done, (g - 1) & 1);  // this tile's last P . V
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full);
-    }
-    mbar_wait(&o_done, (nb - 1) & 1);
-    __syncwarp();
-    tc_fence_after();
-    const float inv = 1.f / l;
-    const bool store = q0 + r < qlen;
-    __nv_bfloat16* orow = O + (size_t)(ost + q0 + r) * ldo + h * DH;
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const bool store = T.q0 + r < T.qlen;
+      __nv_bfloat16* orow = O + (size_t)(T.ost + T.q0 + r) * ldo + T.h * DH;
 #pragma unroll 1
-    for (int cc = 0; cc < DH / 32; ++cc) {
-      uint32_t o[32];
-      tmem_ld32_async(t_o + lane_off + cc * 32, o);
-      tmem_wait_ld();
-      if (store) {
+      for (int cc = 0; cc < DH / 32; ++cc) {
+        uint32_t o[32];
+        tmem_ld32_async(t_o + lane_off + cc * 32, o);
+        tmem_wait_ld();
+        if (store) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
-          w.y = pack_bf16(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
-          w.z = pack_bf16(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
-          w.w = pack_bf16(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
-          *reinterpret_cast<uint4*>(orow + cc * 32 + i) = w;
+          for (int i = 0; i < 32; i += 8) {
+            uint4 w;
+            w.x = pack_bf16(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
+            w.y = pack_bf16(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+            w.z = pack_bf16(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
+            w.w = pack_bf16(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
+            *reinterpret_cast<uint4*>(orow + cc * 32 + i) = w;
+          }
         }
       }
+      // the next tile's first P . V overwrites O: issued only after p_full of its
+      // first block, which these threads arrive after this read (tcgen05.ld waited)
+      tc_fence_before();
     }
   }
   tc_fence_before();
@@ -336,9 +385,11 @@ void launch_fmha(const FmhaArgs& a, cudaStream_t s) {
   CUtensorMap mq = map2d(a.Q, a.q_rows, a.q_col0 + a.heads * DH, a.ldq, 64, F::BQ);
   CUtensorMap mk = map2d(a.K, a.k_rows, a.k_col0 + a.heads * DH, a.ldk, 64, F::BK);
   CUtensorMap mv = map2d(a.Vt, a.vt_rows, a.vt_cols, a.vt_ld, 64, DH);
-  dim3 grid((a.max_q + F::BQ - 1) / F::BQ, a.heads, a.B);
-  launch_pdl(fmha_tc_kernel<DH>, grid, 192, F::SMEM, s, mq, mk, mv, a.heads, static_cast<__nv_bfloat16*>(a.O), a.ldo, a.q, a.k, a.o, a.vt_user, a.q_col0,
-                                                a.k_col0);
+  const int nqt = (a.max_q + F::BQ - 1) / F::BQ;
+  const long long tiles = static_cast<long long>(nqt) * a.heads * a.B;
+  const int grid = static_cast<int>(std::min<long long>(tiles, 2LL * num_sms()));  // persistent, two CTAs per SM
+  launch_pdl(fmha_tc_kernel<DH>, grid, 192, F::SMEM, s, mq, mk, mv, a.heads, nqt, a.B,
+             static_cast<__nv_bfloat16*>(a.O), a.ldo, a.q, a.k, a.o, a.vt_user, a.q_col0, a.k_col0);
 }
 
 }  // namespace

@@ -1,4 +1,4 @@
-// tcgen05 / TMEM flash attention for the bf16 path (head dim 64 or 128).
+// tcgen05 / TMEM flash attention for the bf16 path (head dim 32, 64 or 128).
 //
 // One CTA per (segment b, head h, block of 128 query rows); two CTAs per SM.
 //   warp 0    TMA producer: Q once; K (row-major keys x dh) and V^T (dh x keys,
@@ -62,14 +62,34 @@ ORX_DEV void tc_mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, u
 template <int DH>
 struct Fmha {
   static constexpr int BQ = 128, BK = 64;
-  static constexpr int CB = DH / 64;                  // 64-element (128 B) column blocks of Q / K
+  // Q / K rows are stored as ROWB-byte swizzled rows: 128 B (SWIZZLE_128B, 64
+  // elements per column block) for dh >= 64, 64 B (SWIZZLE_64B) for dh = 32
+  static constexpr int ROWB = DH >= 64 ? 128 : 64;
+  static constexpr int CB = DH * 2 / ROWB;            // column blocks of Q / K
+  static constexpr int KPR = ROWB / 32;               // K=16 MMA steps per swizzled row
   static constexpr uint32_t Q_BYTES = BQ * DH * 2;    // CB blocks of [128 rows x 128 B]
   static constexpr uint32_t K_BYTES = BK * DH * 2;    // CB blocks of [64 rows x 128 B]
   static constexpr uint32_t V_BYTES = DH * BK * 2;    // [DH rows (head dims) x 64 keys]
   static constexpr int KST = 3, VST = 2;              // K ring deeper than V: S_j needs K_j first
   static constexpr uint32_t SMEM = Q_BYTES + KST * K_BYTES + VST * V_BYTES + 256;  // + barriers (17 x 8 B)
   static constexpr uint32_t TMEM_COLS = 2 * BK + DH <= 256 ? 256 : 512;  // S[2] + O
+  static_assert(DH == 32 || DH % 64 == 0, "head dim 32 or a multiple of 64");
 };
+// K-major operand descriptor for ROWB-byte swizzled rows (8-row core groups)
+template <int ROWB>
+ORX_DEV uint64_t umma_desc_rows(uint32_t smem_addr) {
+  if constexpr (ROWB == 128) {
+    return umma_desc_sw128(smem_addr);
+  } else {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr & 0x3FFFF) >> 4);  // start address
+    d |= static_cast<uint64_t>(1) << 16;                      // LBO (ignored)
+    d |= static_cast<uint64_t>(512 >> 4) << 32;               // SBO: 8 rows x 64 B
+    d |= static_cast<uint64_t>(1) << 46;                      // descriptor version (sm100)
+    d |= static_cast<uint64_t>(4) << 61;                      // SWIZZLE_64B
+    return d;
+  }
+}
 
 template <int DH>
 __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
@@ -160,7 +180,8 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
         if (tc > 0) mbar_wait(&q_empty, (tc - 1) & 1);  // the previous tile's last QK^T has read Q
         mbar_arrive_expect_tx(&q_full, F::Q_BYTES);
         for (int cb = 0; cb < F::CB; ++cb)
-          tma_load_2d(sQ + cb * (F::BQ * 128), &tmQ, &q_full, q_col0 + T.h * DH + cb * 64, T.qst + T.q0, pol);
+          tma_load_2d(sQ + cb * (F::BQ * F::ROWB), &tmQ, &q_full, q_col0 + T.h * DH + cb * (F::ROWB / 2),
+                      T.qst + T.q0, pol);
         // K runs one block ahead of V (V_j is consumed a softmax later than K_j)
         for (int i = 0; i <= T.nb; ++i) {
           if (i < T.nb) {
@@ -168,8 +189,8 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
             if (kc >= F::KST) mbar_wait(&k_empty[kslot], ((kc / F::KST) - 1) & 1);
             mbar_arrive_expect_tx(&k_full[kslot], F::K_BYTES);
             for (int cb = 0; cb < F::CB; ++cb)
-              tma_load_2d(sK + kslot * F::K_BYTES + cb * (F::BK * 128), &tmK, &k_full[kslot],
-                          k_col0 + T.h * DH + cb * 64, T.kst + i * F::BK, pol);
+              tma_load_2d(sK + kslot * F::K_BYTES + cb * (F::BK * F::ROWB), &tmK, &k_full[kslot],
+                          k_col0 + T.h * DH + cb * (F::ROWB / 2), T.kst + i * F::BK, pol);
             ++kc;
           }
           const int j = i - 1;
@@ -216,9 +237,9 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
           const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + kslot * F::K_BYTES);
 #pragma unroll
           for (int k = 0; k < DH / 16; ++k) {
-            const int cb = k >> 2, off = (k & 3) * 32;
-            tc_mma_bf16(t_s + st * F::BK, umma_desc_sw128(qa + cb * (F::BQ * 128) + off),
-                        umma_desc_sw128(kb + cb * (F::BK * 128) + off), idesc_s, k != 0);
+            const int cb = k / F::KPR, off = (k % F::KPR) * 32;
+            tc_mma_bf16(t_s + st * F::BK, umma_desc_rows<F::ROWB>(qa + cb * (F::BQ * F::ROWB) + off),
+                        umma_desc_rows<F::ROWB>(kb + cb * (F::BK * F::ROWB) + off), idesc_s, k != 0);
           }
           tc_commit(&s_full[st]);
           tc_commit(&k_empty[kslot]);
@@ -350,7 +371,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-CUtensorMap map2d(const void* ptr, long long rows, long long cols, long long ld, int box_cols, int box_rows) {
+CUtensorMap map2d(const void* ptr, long long rows, long long cols, long long ld, int box_cols, int box_rows,
+                  CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     void* p = nullptr;
@@ -366,7 +388,7 @@ CUtensorMap map2d(const void* ptr, long long rows, long long cols, long long ld,
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("attention tensor map encode failed (" + std::to_string(int(r)) + ")");
   return m;
@@ -382,8 +404,9 @@ void launch_fmha(const FmhaArgs& a, cudaStream_t s) {
   }
   // Q/K maps start at the head-0 column of their buffers (column offsets are
   // added in the kernel): rows x (q_col0 + heads * DH) columns.
-  CUtensorMap mq = map2d(a.Q, a.q_rows, a.q_col0 + a.heads * DH, a.ldq, 64, F::BQ);
-  CUtensorMap mk = map2d(a.K, a.k_rows, a.k_col0 + a.heads * DH, a.ldk, 64, F::BK);
+  constexpr CUtensorMapSwizzle qk_swz = F::ROWB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  CUtensorMap mq = map2d(a.Q, a.q_rows, a.q_col0 + a.heads * DH, a.ldq, F::ROWB / 2, F::BQ, qk_swz);
+  CUtensorMap mk = map2d(a.K, a.k_rows, a.k_col0 + a.heads * DH, a.ldk, F::ROWB / 2, F::BK, qk_swz);
   CUtensorMap mv = map2d(a.Vt, a.vt_rows, a.vt_cols, a.vt_ld, 64, DH);
   const int nqt = (a.max_q + F::BQ - 1) / F::BQ;
   const long long tiles = static_cast<long long>(nqt) * a.heads * a.B;
@@ -394,7 +417,7 @@ void launch_fmha(const FmhaArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-bool fmha_supported(int dh) { return dh == 64 || dh == 128; }
+bool fmha_supported(int dh) { return dh == 32 || dh == 64 || dh == 128; }
 
 void launch_fmha_tc(const FmhaArgs& a, cudaStream_t s) {
   if (a.B <= 0 || a.max_q <= 0) return;
@@ -406,7 +429,8 @@ void launch_fmha_tc(const FmhaArgs& a, cudaStream_t s) {
               std::to_string(a.max_q) + " k_rows=" + std::to_string(a.k_rows));
   if (a.dh == 128) launch_fmha<128>(a, s);
   else if (a.dh == 64) launch_fmha<64>(a, s);
-  else throw std::invalid_argument("fmha: head dim must be 64 or 128");
+  else if (a.dh == 32) launch_fmha<32>(a, s);
+  else throw std::invalid_argument("fmha: head dim must be 32, 64 or 128");
   ++launch_counter();
 }
 

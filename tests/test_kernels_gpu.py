@@ -301,10 +301,12 @@ def _attn_case(kind, H=2, dh=128, seed=0):
 
 @pytest.mark.parametrize("kind", ["encoder", "qformer", "cross"])
 @pytest.mark.parametrize("kernel", [0, 1])
-def test_attention_bf16(kind, kernel):
+@pytest.mark.parametrize("dh", [32, 64, 128])
+def test_attention_bf16(kind, kernel, dh):
     """Segmented softmax(QK^T/sqrt(dh))V (mha_core, tape.cpp:822-905): the
-    mma.sync kernel (0) and the tcgen05/TMEM kernel (1, transposed V) vs torch fp32."""
-    B, H, dh, Q, K, V, cols, qs, ks, Vt = _attn_case(kind)
+    mma.sync kernel (0) and the tcgen05/TMEM kernel (1, transposed V; 64-byte
+    swizzled Q/K rows at dh=32, the 0.015B config) vs torch fp32."""
+    B, H, dh, Q, K, V, cols, qs, ks, Vt = _attn_case(kind, H=256 // dh, dh=dh)
     d = H * dh
     rows_out = sum(n for _, n in qs)
     O = torch.zeros(rows_out, d, device="cuda", dtype=torch.bfloat16)

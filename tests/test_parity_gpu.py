@@ -112,8 +112,13 @@ def test_moe_small(kind, precision):
             overlap = len({tuple(c) for c in codes[u]} & {tuple(c) for c in ref["beam_codes"]})
             print(f"MoE {kind} bf16 user {u}: z max {zr.max():.3e} median {np.median(zr):.3e} "
                   f"p95 {np.percentile(zr, 95):.3e} logits {el:.3e} overlap {overlap}/32")
-            assert np.median(zr) < 3e-2 and zr.max() < 1.0
-            assert el < 0.25 and overlap >= 16
+            # measured (round 2): dec logits ~6e-3, overlap 31-32/32; enc_and_dec (MoE in every
+            # layer, more routing flips) logits 0.07-0.10, overlap 27-29/32, median z row 8e-3
+            assert np.median(zr) < 2e-2 and zr.max() < 0.6
+            if kind == "dec":
+                assert el < 2e-2 and overlap >= 28
+            else:
+                assert el < 0.2 and overlap >= 24
 
 
 def test_0015b_bf16_deviation():
@@ -129,7 +134,7 @@ def test_0015b_bf16_deviation():
         el = max(rel_inf(lg[i], ref["logits"][i]) for i in range(len(pres)))
         overlap = len({tuple(c) for c in codes[u]} & {tuple(c) for c in ref["beam_codes"]})
         print(f"0.015B bf16 user {u}: z rel {ez:.3e} logits rel {el:.3e} beam overlap {overlap}/128")
-        assert ez < 5e-2 and el < 5e-2 and overlap >= 64
+        assert ez < 2e-2 and el < 2e-2 and overlap >= 120  # measured: 6e-3, 6e-3, 126-127
 
 
 def test_cpp_dropin_shim_matches_reference():
@@ -178,7 +183,7 @@ def test_bf16_tcgen05_attention_dh128(moe):
         overlap = len({tuple(c) for c in codes[u]} & {tuple(c) for c in ref["beam_codes"]})
         print(f"dh=128 bf16 moe={moe} user {u}: z {ez:.3e} (mma.sync {rel_inf(z_mma[u], ref['z']):.3e}) "
               f"logits {el:.3e} (mma.sync {el_mma:.3e}) overlap {overlap}/32")
-        assert el < 5e-2 and overlap >= 16
+        assert el < 2e-2 and overlap >= 28  # measured: 7e-3 .. 9e-3, 30-32/32
         assert el < 2 * el_mma + 1e-2  # no worse than the mma.sync attention path
 
 

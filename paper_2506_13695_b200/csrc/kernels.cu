@@ -250,27 +250,61 @@ __global__ void __launch_bounds__(256) fold_features_kernel(RecordsDev r, FoldTa
     for (int s = 0; s < 4; ++s)
       u[s][h] = ok[h] ? __ldg(reinterpret_cast<const float4*>(f.u) + s * d4 + c4[h]) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  for (int row = blockIdx.x * RPB + rl; row < r.n; row += gridDim.x * RPB) {
-    const float4* pv = reinterpret_cast<const float4*>(f.pv) + (size_t)r.vid[row] * d4;
-    const float4* pa = reinterpret_cast<const float4*>(f.pa) + (size_t)r.aid[row] * d4;
-    const float4* pl = reinterpret_cast<const float4*>(f.pl) + (size_t)(r.labels[row] & lmask) * d4;
-    float4 a[2], b[2], l[2];
+  // Software-pipelined over this warp's records: the record fields of row k+2
+  // and the table rows of row k+1 are in flight while row k is finished (the
+  // loop is otherwise two dependent memory latencies per record).
+  const int stride = gridDim.x * RPB;
+  struct Rec {
+    int vid, aid;
+    unsigned lab;
+    float x0, x1, x2, x3;
+  };
+  auto load_rec = [&](int row, Rec& q) {
+    if (row < r.n) {
+      q.vid = r.vid[row];
+      q.aid = r.aid[row];
+      q.lab = r.labels[row] & lmask;
+      q.x0 = r.tag[row];
+      q.x1 = r.ts[row];
+      q.x2 = r.play[row];
+      q.x3 = r.dur[row];
+    }
+  };
+  auto gather = [&](int row, const Rec& q, float4 (&a)[2], float4 (&b)[2], float4 (&l)[2]) {
+    if (row >= r.n) return;
+    const float4* pv = reinterpret_cast<const float4*>(f.pv) + (size_t)q.vid * d4;
+    const float4* pa = reinterpret_cast<const float4*>(f.pa) + (size_t)q.aid * d4;
+    const float4* pl = reinterpret_cast<const float4*>(f.pl) + (size_t)q.lab * d4;
 #pragma unroll
     for (int h = 0; h < 2; ++h)
       if (ok[h]) a[h] = __ldg(pv + c4[h]), b[h] = __ldg(pa + c4[h]), l[h] = __ldg(pl + c4[h]);
-    const float x0 = r.tag[row], x1 = r.ts[row], x2 = r.play[row], x3 = r.dur[row];
+  };
+  int row = blockIdx.x * RPB + rl;
+  Rec q0{}, q1{}, q2{};
+  float4 a0[2], b0[2], l0[2], a1[2], b1[2], l1[2];
+  load_rec(row, q0);
+  load_rec(row + stride, q1);
+  gather(row, q0, a0, b0, l0);
+  for (; row < r.n; row += stride) {
+    load_rec(row + 2 * stride, q2);
+    gather(row + stride, q1, a1, b1, l1);
+    const float x0 = q0.x0, x1 = q0.x1, x2 = q0.x2, x3 = q0.x3;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (!ok[h]) continue;
       float v[4];
-      v[0] = a[h].x + b[h].x + l[h].x + x0 * u[0][h].x + x1 * u[1][h].x + x2 * u[2][h].x + x3 * u[3][h].x;
-      v[1] = a[h].y + b[h].y + l[h].y + x0 * u[0][h].y + x1 * u[1][h].y + x2 * u[2][h].y + x3 * u[3][h].y;
-      v[2] = a[h].z + b[h].z + l[h].z + x0 * u[0][h].z + x1 * u[1][h].z + x2 * u[2][h].z + x3 * u[3][h].z;
-      v[3] = a[h].w + b[h].w + l[h].w + x0 * u[0][h].w + x1 * u[1][h].w + x2 * u[2][h].w + x3 * u[3][h].w;
+      v[0] = a0[h].x + b0[h].x + l0[h].x + x0 * u[0][h].x + x1 * u[1][h].x + x2 * u[2][h].x + x3 * u[3][h].x;
+      v[1] = a0[h].y + b0[h].y + l0[h].y + x0 * u[0][h].y + x1 * u[1][h].y + x2 * u[2][h].y + x3 * u[3][h].y;
+      v[2] = a0[h].z + b0[h].z + l0[h].z + x0 * u[0][h].z + x1 * u[1][h].z + x2 * u[2][h].z + x3 * u[3][h].z;
+      v[3] = a0[h].w + b0[h].w + l0[h].w + x0 * u[0][h].w + x1 * u[1][h].w + x2 * u[2][h].w + x3 * u[3][h].w;
 #pragma unroll
       for (int j = 0; j < 4; ++j) v[j] = v[j] > 0.f ? v[j] : 0.01f * v[j];  // tape.hpp:88
       *reinterpret_cast<uint2*>(out + (size_t)row * ldo + c4[h] * 4) = make_uint2(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]));
     }
+    q0 = q1;
+    q1 = q2;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) a0[h] = a1[h], b0[h] = b1[h], l0[h] = l1[h];
   }
 }
 
@@ -1248,7 +1282,7 @@ void launch_fold_features(const RecordsDev& r, const FoldTables& f, __nv_bfloat1
   if (!fold_features_supported(f.d, f.n_flags) || ldo % 4 != 0)
     throw std::invalid_argument("fold_features: unsupported shape");
   const int g = (f.d + 255) / 256, rpb = 8 / g;
-  const int grid = static_cast<int>(std::min<long long>((r.n + rpb - 1) / rpb, num_sms() * 3LL));  // 80 regs: 3 blocks per SM
+  const int grid = static_cast<int>(std::min<long long>((r.n + rpb - 1) / rpb, num_sms() * 2LL));  // 124 regs: 2 blocks per SM
   // records' scalar inputs in, bf16 hidden rows out (the table gathers are L2 hits)
   const double nb = double(r.n) * (2.0 * f.d + 28.0);
   auto go = [&](auto kern) { ORX_LAUNCH_CATB(PROF_FEAT, nb, launch_pdl(kern, grid, 256, 0, s, r, f, out, ldo)); };

@@ -327,6 +327,7 @@ def test_attention_bf16(kind, kernel, dh):
     a.kernel = kernel
     L.check(L.lib().orx_debug_attention(C.byref(a), None))
     torch.cuda.synchronize()
+    assert torch.isfinite(O.float()).all(), "non-finite attention output"
     worst = 0.0
     for b in range(B):
         (q0, nq), (k0, nk) = qs[b], ks[b]
@@ -337,6 +338,7 @@ def test_attention_bf16(kind, kernel, dh):
             ref = torch.softmax(q @ k.t() / dh ** 0.5, dim=-1) @ v
             got = O[ost[b]:ost[b] + nq, h * dh:(h + 1) * dh].float()
             err = ((got - ref).abs().max() / ref.abs().max().clamp_min(1e-6)).item()
+            assert err == err, "NaN error"
             worst = max(worst, err)
-    print(f"attention {kind} kernel {kernel}: max rel err {worst:.3e}")
+    print(f"attention {kind} kernel {kernel} dh={dh}: max rel err {worst:.3e}")
     assert worst < 3e-2

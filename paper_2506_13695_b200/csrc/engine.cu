@@ -91,6 +91,8 @@ struct MoeW {
   const float* gate_t = nullptr;  // [E][d]
   const float* gate_gain = nullptr;  // [E][d] gate_t[e][c] * (pre-MoE RMSNorm gain)[c]
   const float* gate_sw = nullptr;    // gate_gain in moe_route4's swizzled shared-memory layout (E <= 24)
+  const float* gate_hi = nullptr;    // bf16 engine: [32][d] tf32 hi / fp32 residual of gate_gain (route_tc.cu)
+  const float* gate_lo = nullptr;
   const float* bias = nullptr;    // [E]
   const void* w13 = nullptr;      // bf16: [E][2h][d] interleaved per 128 rows; fp32: w1 [E][h][d]
   const void* w3 = nullptr;       // fp32 only: [E][h][d]
@@ -384,6 +386,19 @@ class EngineT final : public Engine {
           sw[(size_t)q * 96 + unit * 4 + (e & 3)] = gt[(size_t)e * d + c];
         }
       m.gate_sw = upload_f32(sw.data(), sw.size());
+    }
+    if (kBf16 && moe_route_tc_supported(d, E, cfg_.experts_active, d) && !getenv("ORX_ROUTE_SIMT")) {
+      // 3xTF32 gate for the tensor-pipe router: tf32-exact hi part and the fp32 residual, 32 expert rows
+      std::vector<float> hi(static_cast<size_t>(32) * d, 0.f), lo(static_cast<size_t>(32) * d, 0.f);
+      for (size_t i = 0; i < gt.size(); ++i) {
+        uint32_t b;
+        memcpy(&b, &gt[i], 4);
+        b &= 0xFFFFE000u;
+        memcpy(&hi[i], &b, 4);
+        lo[i] = gt[i] - hi[i];
+      }
+      m.gate_hi = upload_f32(hi.data(), hi.size());
+      m.gate_lo = upload_f32(lo.data(), lo.size());
     }
     m.bias = up(hw, n + ".routing_bias");
     const int dp = rup(d, 8), hp = rup(h, 8);
@@ -1204,8 +1219,13 @@ class EngineT final : public Engine {
     const orx_config& c = cfg_;
     const int d = c.d_model, E = c.n_experts, k = c.experts_active;
     CUDA_CHECK(cudaMemsetAsync(counts_, 0, E * sizeof(int32_t), st_));
-    launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.gate_gain, m.bias, sel_, wts_, counts_, st_,
-                     m.gate_sw);
+    // tensor-pipe router for large row counts (one 128-row tile per SM is latency-bound: the SIMT
+    // router is faster below a few thousand rows)
+    if (m.gate_hi && rows >= 4096)
+      launch_moe_route_tc(rows, d, E, k, h, d, m.gate_hi, m.gate_lo, m.bias, sel_, wts_, counts_, st_);
+    else
+      launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.gate_gain, m.bias, sel_, wts_, counts_, st_,
+                       m.gate_sw);
     if (ep_world_ > 1) return moe_ep(m, x, rows, h, post, post_gain);
     launch_moe_plan(E, counts_, cursor_, tile_expert_, max_tiles_, n_mtiles_, kMoeTile, st_);
     launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xg_, row_scale_, st_);

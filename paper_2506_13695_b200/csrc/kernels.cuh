@@ -87,6 +87,13 @@ void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, co
 // supported (then run launch_moe_combine + the norm / convert).
 bool launch_moe_combine_norm(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
                              const float* gain, __nv_bfloat16* out, int ldo, cudaStream_t s);
+// Gate scores on the tensor pipe (3xTF32, route_tc.cu) for the bf16 engine:
+// gate_hi / gate_lo [32][d] = the gain-folded gate split into tf32 hi and
+// residual lo (expert rows >= E zero). Same outputs as launch_moe_route.
+bool moe_route_tc_supported(int d, int E, int k, int ldx);
+void launch_moe_route_tc(int rows, int d, int E, int k, const float* x, int ldx, const float* gate_hi,
+                         const float* gate_lo, const float* bias, int32_t* sel, float* wts, int32_t* counts,
+                         cudaStream_t s);
 void launch_moe_plan(int E, const int32_t* counts, int32_t* seg_cursor, int32_t* tile_expert, int max_tiles,
                      int32_t* n_mtiles, int tile_rows, cudaStream_t s);
 template <class T>

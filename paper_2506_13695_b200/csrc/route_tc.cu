@@ -1,0 +1,307 @@
+// MoE gate scores on the tensor pipe (bf16 engine): s = RMSNorm(h) . W_g with
+// the RMSNorm gain folded into W_g, computed as 3xTF32 on tcgen05 so routing
+// keeps fp32-grade scores (moe_forward, nn.cpp:117-147):
+//   x = x_hi + x_lo, w = w_hi + w_lo (x_hi, w_hi tf32-exact, x_lo = x - x_hi)
+//   x.w ~= x_hi.w_hi + x_lo.w_hi + x_hi.w_lo     (dropped term ~2^-21 relative)
+// One CTA per SM walks 128-row tiles of h (fp32, the residual stream):
+//   warp 0    TMA: h tile (128 rows x 32 fp32, 128-byte swizzled rows) and the
+//             pre-split gate (32 expert rows x 32) per K block, 4-stage ring
+//   warps 2-5 thread = row: split the staged fp32 row into tf32 hi (in place)
+//             and lo (second buffer), accumulate the row's sum of squares; at
+//             the end of the tile read the row's 32 scores from TMEM, scale by
+//             rsqrt(mean(x^2) + eps), stable top-k by score + bias (ties ->
+//             lower id, nn.cpp:127-136), softmax over the selected raw scores
+//             (nn.cpp:139-147), ids ascending
+//   warp 1    one thread issues tcgen05.mma kind::tf32 (M=128, N=32, K=8), three
+//             per K step, into one of two TMEM accumulators
+// The h tile is read once from HBM (4 d bytes per row); the per-row work is
+// ~30 instructions per 32 columns, so the kernel runs at the HBM rate instead
+// of the shared-memory bound of a SIMT 24-expert dot product.
+#include <cfloat>
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace orx {
+
+namespace {
+
+constexpr int kRtBM = 128;      // rows per tile
+constexpr int kRtBK = 32;       // fp32 columns per K block (128-byte rows)
+constexpr int kRtN = 32;        // expert slots (E <= 32)
+constexpr int kRtStages = 4;
+constexpr uint32_t kRtA = kRtBM * kRtBK * 4;  // 16 KB
+constexpr uint32_t kRtB = kRtN * kRtBK * 4;   // 4 KB
+constexpr uint32_t kRtStage = 2 * kRtA + 2 * kRtB;  // A hi (in place) + A lo + B hi + B lo
+constexpr size_t kRtSmem = kRtStages * kRtStage + 1024 + 512;
+
+// kind::tf32 instruction descriptor: fp32 accumulate, A/B tf32, both K-major
+constexpr uint32_t idesc_tf32(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+ORX_DEV void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+ORX_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__global__ void __launch_bounds__(192, 1)
+    moe_route_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmBh,
+                        const __grid_constant__ CUtensorMap tmBl, int rows, int d, int E, int k,
+                        const float* __restrict__ bias, int32_t* __restrict__ sel, float* __restrict__ wts,
+                        int32_t* __restrict__ counts) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRtStages * kRtStage);
+  uint64_t* conv = full + kRtStages;
+  uint64_t* empty = conv + kRtStages;
+  uint64_t* acc_full = empty + kRtStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  int* hist = reinterpret_cast<int*>(tmem_slot + 4);  // [32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRtStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);
+    }
+    fence_mbar_init();
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmBh);
+    tma_prefetch(&tmBl);
+  }
+  if (threadIdx.x < 32) hist[threadIdx.x] = 0;
+  if (warp == 1) tmem_alloc(tmem_slot, 64);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_begin();
+  const int tiles = (rows + kRtBM - 1) / kRtBM;
+  const int kblocks = d / kRtBK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_x = l2_policy_evict_first(), pol_b = l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * kRtStage;
+          mbar_arrive_expect_tx(&full[stage], kRtA + 2 * kRtB);
+          tma_load_2d(st, &tmX, &full[stage], kb * kRtBK, t * kRtBM, pol_x);
+          tma_load_2d(st + 2 * kRtA, &tmBh, &full[stage], kb * kRtBK, 0, pol_b);
+          tma_load_2d(st + 2 * kRtA + kRtB, &tmBl, &full[stage], kb * kRtBK, 0, pol_b);
+          if (++stage == kRtStages) stage = 0, phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(kRtBM, kRtN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t dt = tmem + acc * kRtN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          mbar_wait(&conv[stage], phase);
+          tc_fence_after();
+          const uint32_t ah = smem_u32(smem + stage * kRtStage), al = ah + kRtA;
+          const uint32_t bh = ah + 2 * kRtA, bl = bh + kRtB;
+#pragma unroll
+          for (int ks = 0; ks < kRtBK / 8; ++ks) {  // K = 8 tf32 = 32 bytes per step
+            const uint32_t o = ks * 32;
+            const uint32_t first = (kb | ks) != 0;
+            tc_mma_tf32(dt, umma_desc_sw128(ah + o), umma_desc_sw128(bh + o), idesc, first);
+            tc_mma_tf32(dt, umma_desc_sw128(al + o), umma_desc_sw128(bh + o), idesc, 1);
+            tc_mma_tf32(dt, umma_desc_sw128(ah + o), umma_desc_sw128(bl + o), idesc, 1);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == kRtStages) stage = 0, phase ^= 1;
+        }
+        tc_commit(&acc_full[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3;   // TMEM lane quadrant = row block of the tile
+    const int r = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      float ss = 0.f;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        uint8_t* st = smem + stage * kRtStage;
+        float4* hi = reinterpret_cast<float4*>(st + r * 128);
+        float4* lo = reinterpret_cast<float4*>(st + kRtA + r * 128);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {  // the row's 8 16-byte units, elementwise: visit them XOR-rotated
+          const int u = j ^ (r & 7);   // so the 8 lanes of a phase hit 8 different bank groups
+          float4 x = hi[u];
+          ss += x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w;
+          float4 h4, l4;
+          h4.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+          h4.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+          h4.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+          h4.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          l4.x = x.x - h4.x, l4.y = x.y - h4.y, l4.z = x.z - h4.z, l4.w = x.w - h4.w;
+          hi[u] = h4;
+          lo[u] = l4;
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> the tensor core's reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[stage]);
+        if (++stage == kRtStages) stage = 0, phase ^= 1;
+      }
+      // epilogue: this row's expert scores
+      mbar_wait(&acc_full[acc], acc_phase);
+      __syncwarp();
+      tc_fence_after();
+      uint32_t raw[32];
+      tmem_ld32_async(tmem + lane_off + acc * kRtN, raw);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+      const int row = t * kRtBM + r;
+      if (row >= rows) continue;
+      const float inv = rsqrtf(ss / d + 1e-6f);
+      float sc[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) sc[e] = __uint_as_float(raw[e]) * inv;
+      uint32_t taken = 0;
+      int ids[8];
+      float rw[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        ids[j] = 1 << 30;
+        rw[j] = -FLT_MAX;
+        if (j >= k) continue;
+        int bi = -1;
+        float bk = -FLT_MAX;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          if (e >= E || ((taken >> e) & 1u)) continue;
+          const float key = sc[e] + __ldg(bias + e);
+          if (bi < 0 || key > bk) bk = key, bi = e;  // strict >: ties keep the lower id
+        }
+        taken |= 1u << bi;
+        ids[j] = bi;
+      }
+      // ids ascending, raw scores in that order (nn.cpp:139-147)
+      int n = 0;
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if ((taken >> e) & 1u) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j == n) ids[j] = e, rw[j] = sc[e];
+          ++n;
+        }
+      float mx = -FLT_MAX;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < k) mx = fmaxf(mx, rw[j]);
+      float den = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < k) den += __expf(rw[j] - mx);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < k) {
+          sel[(size_t)row * k + j] = ids[j];
+          wts[(size_t)row * k + j] = __expf(rw[j] - mx) / den;
+          atomicAdd(&hist[ids[j]], 1);
+        }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < E && hist[threadIdx.x]) atomicAdd(&counts[threadIdx.x], hist[threadIdx.x]);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 64);
+  }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+CUtensorMap map_f32(const void* ptr, long long rows, long long cols, long long ld, int box_rows) {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeFn>(p);
+  }
+  CUtensorMap m;
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kRtBK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), gdim, gstride, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("route tensor map encode failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
+}  // namespace
+
+bool moe_route_tc_supported(int d, int E, int k, int ldx) {
+  return E <= kRtN && k >= 1 && k <= 8 && d % kRtBK == 0 && ldx % 4 == 0;
+}
+
+void launch_moe_route_tc(int rows, int d, int E, int k, const float* x, int ldx, const float* gate_hi,
+                         const float* gate_lo, const float* bias, int32_t* sel, float* wts, int32_t* counts,
+                         cudaStream_t s) {
+  if (rows <= 0) return;
+  if (!moe_route_tc_supported(d, E, k, ldx)) throw std::invalid_argument("moe_route_tc: unsupported shape");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(moe_route_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRtSmem));
+    attr = true;
+  }
+  const CUtensorMap mx = map_f32(x, rows, d, ldx, kRtBM);
+  const CUtensorMap mh = map_f32(gate_hi, kRtN, d, d, kRtN);
+  const CUtensorMap ml = map_f32(gate_lo, kRtN, d, d, kRtN);
+  const int tiles = (rows + kRtBM - 1) / kRtBM;
+  const int grid = std::min(tiles, num_sms());
+  ProfScope ps(PROF_MOE_ROUTE, s, 2.0 * 3 * rows * d * kRtN, double(rows) * (4.0 * d + 8.0 * k));
+  launch_pdl(moe_route_tc_kernel, grid, 192, kRtSmem, s, mx, mh, ml, rows, d, E, k, bias, sel, wts, counts);
+  ++launch_counter();
+}
+
+}  // namespace orx

@@ -1592,20 +1592,29 @@ __global__ void __launch_bounds__(256) moe_combine_norm_kernel(int rows, int k, 
   pdl_begin();
   const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (r >= rows) return;
-  float4 v[NC];
+  // every load of a pass is issued before its first use (the row's h segment and
+  // the first expert output, then one pass per further expert): k round trips
+  // to memory per row instead of one per column chunk
+  float4 v[NC], acc[NC];
   float4* hr = reinterpret_cast<float4*>(h + (size_t)r * ldh);
+  const float4* y0 = reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k] * d);
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
-    const int c4 = lane + 32 * i;
-    float4 acc = __ldg(reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k] * d) + c4);
-    for (int j = 1; j < k; ++j) {
-      const float4 y = __ldg(reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k + j] * d) + c4);
-      acc.x += y.x, acc.y += y.y, acc.z += y.z, acc.w += y.w;
-    }
-    float4 hv = hr[c4];
-    hv.x += acc.x, hv.y += acc.y, hv.z += acc.z, hv.w += acc.w;
-    hr[c4] = hv;
-    v[i] = hv;
+    v[i] = hr[lane + 32 * i];
+    acc[i] = __ldg(y0 + lane + 32 * i);
+  }
+  for (int j = 1; j < k; ++j) {  // ascending expert order, as the reference combines (nn.cpp:152-169)
+    const float4* yj = reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k + j] * d);
+    float4 y[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) y[i] = __ldg(yj + lane + 32 * i);
+#pragma unroll
+    for (int i = 0; i < NC; ++i) acc[i].x += y[i].x, acc[i].y += y[i].y, acc[i].z += y[i].z, acc[i].w += y[i].w;
+  }
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    v[i].x += acc[i].x, v[i].y += acc[i].y, v[i].z += acc[i].z, v[i].w += acc[i].w;
+    hr[lane + 32 * i] = v[i];
   }
   float rs = 1.f;
   if (gain) {

@@ -15,3 +15,8 @@ run gemm160 'tc2_gemm_kernel<\(int\)256, \(int\)5, \(int\)160>' 0
 run gemm96 'tc2_gemm_kernel<\(int\)256, \(int\)5, \(int\)96>' 4
 run gemm8 'tc2_gemm_kernel<\(int\)256, \(int\)5, \(int\)8>' 4
 run gemm16 'tc2_gemm_kernel<\(int\)256, \(int\)5, \(int\)16>' 12
+if [ -n "${MORE:-}" ]; then
+  run gemm37 'tc2_gemm_kernel<\(int\)256, \(int\)5, \(int\)37>' 0
+  run gemm32 'tc2_gemm_kernel<\(int\)256, \(int\)5, \(int\)32>' 4
+  run gemm17 'tc2_gemm_kernel<\(int\)256, \(int\)5, \(int\)17>' 0
+fi

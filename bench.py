@@ -111,10 +111,12 @@ def bench_config(args, cfg, lens, world):
             "l2": "working set (weights ~2 GB + activations) exceeds the 126 MB L2; no flush"}
 
 
-def flops_per_user(cfg, width, lens, fold_fc1=False):
+def flops_per_user(cfg, width, lens, fold_fc1=False, fold_kv=False):
     """Algorithmic FLOPs per user, KV-cached minimum.
     fold_fc1: the pathway fc1 folded through the feature tables (bf16 engine),
-    so only fc2 is a per-record GEMM (what the engine executes)."""
+    so only fc2 is a per-record GEMM; fold_kv: the lifelong pathway's fc2 folded
+    into the QFormer K|V weights (bf16 engine), so the lifelong records go
+    through one GEMM (K|V) after the fold (what the engine executes)."""
     d, V, T = cfg.d_model, cfg.codebook_size, cfg.enc_seq_len()
     ns, npos, nl = lens
     nl_keys = max(nl, 1)
@@ -124,6 +126,8 @@ def flops_per_user(cfg, width, lens, fold_fc1=False):
     F = d + d // 2 + 5 * (d // 8)
     fc1 = 10 * d if fold_fc1 else F * d  # folded: a gather-add of ~10 d-vectors per record
     enc += 2.0 * (ns + npos + nl) * (fc1 + d * d)  # pathway MLPs
+    if fold_kv and cfg.lifelong_blocks > 0:
+        enc -= 2.0 * nl * d * d  # lifelong fc2 absorbed by the K|V projection
     Nq = cfg.n_queries
     enc += cfg.lifelong_blocks * (2.0 * Nq * d * d * 2 + 4.0 * nl_keys * d * d + 4.0 * Nq * nl_keys * d + ffn(Nq))
     enc_moe = cfg.moe_enabled and cfg.moe_location == "enc_and_dec"
@@ -472,7 +476,8 @@ def main():
         except Exception:
             pass
 
-    flops_u, enc_flops_u = flops_per_user(cfg, args.width, lens, fold_fc1=args.precision == "bf16")
+    bf16 = args.precision == "bf16"
+    flops_u, enc_flops_u = flops_per_user(cfg, args.width, lens, fold_fc1=bf16, fold_kv=bf16)
     mfu = value / world * flops_u / (peaks["bf16_tflops"] * 1e12)
 
     # ---- measured deviation from the reference (rank 0) ------------------------------------

@@ -366,6 +366,55 @@ class EngineT final : public Engine {
     if (!bias.empty()) L.bias = up(hw, bias);
     return L;
   }
+  // Lifelong keys only feed the QFormer's K / V projections (policy.cpp:233-238,
+  // nn.cpp:97-100): K|V = (H W2 + b2) Wkv = H (W2 Wkv) + b2 Wkv, H the pathway's
+  // LeakyReLU hidden rows. W2 Wkv is formed once here (fp32 SIMT GEMM, one bf16
+  // rounding), so the pathway's fc2 GEMM and its key rows disappear from the
+  // encoder; empty-history users' pad key (pad.lifelong, not an fc2 output) gets
+  // pad Wkv written by launch_fill_kv_pad.
+  void build_kv_fold(const HostWeights& hw, const std::vector<std::string>& kv) {
+    const int d = cfg_.d_model, nkv = static_cast<int>(kv.size()) * d;
+    const Tensor& W2 = hw.get("pathway.lifelong.fc2.w");  // (in, out) = [d][d]
+    const Tensor& b2 = hw.get("pathway.lifelong.fc2.b");
+    const Tensor& pad = hw.get("pad.lifelong");
+    require(W2.rows == d && W2.cols == d, "kv fold: unexpected fc2 shape");
+    std::vector<float> at(static_cast<size_t>(nkv) * d);  // Wkv^T [nkv][d]
+    std::vector<double> c(nkv, 0.0), pk(nkv, 0.0);
+    int n0 = 0;
+    for (const auto& name : kv) {
+      const Tensor& t = hw.get(name);  // (in, out) = [d][d]
+      for (int k = 0; k < d; ++k)
+        for (int j = 0; j < t.cols; ++j) {
+          const float w = t.data[(size_t)k * t.cols + j];
+          at[(size_t)(n0 + j) * d + k] = w;
+          c[n0 + j] += double(b2.data[k]) * w;
+          pk[n0 + j] += double(pad.data[k]) * w;
+        }
+      n0 += t.cols;
+    }
+    float* dA = ar_.alloc<float>(at.size());
+    float* dB = ar_.alloc<float>(W2.data.size());
+    float* dC = ar_.alloc<float>(static_cast<size_t>(nkv) * d);
+    CUDA_CHECK(cudaMemcpy(dA, at.data(), at.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(dB, W2.data.data(), W2.data.size() * 4, cudaMemcpyHostToDevice));
+    Epi ef;
+    ef.out = dC;
+    ef.ldo = d;
+    ef.n_out = d;
+    ef.m_valid = nkv;
+    gemm_f32(dA, d, dB, d, nkv, d, d, ef, nullptr, st_);  // C[m][n] = sum_k Wkv[k][m] W2[n][k] = (W2 Wkv)^T
+    T* w = ar_.alloc<T>(static_cast<size_t>(nkv) * d);
+    launch_convert<T>(nkv, d, dC, d, w, d, st_);
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    kvf_.w = w;
+    kvf_.N = nkv;
+    kvf_.K = d;
+    std::vector<float> cf(c.begin(), c.end()), pf(pk.begin(), pk.end());
+    kvf_.bias = upload_f32(cf.data(), cf.size());
+    kv_pad_ = upload_f32(pf.data(), pf.size());
+    kv_fold_ = true;
+  }
+
   MoeW pack_moe(const HostWeights& hw, const std::string& n, const std::string& gain_name) {
     const int d = cfg_.d_model, E = cfg_.n_experts, El = El_, h = expert_hidden(cfg_);
     MoeW m;
@@ -601,6 +650,9 @@ class EngineT final : public Engine {
       for (int b = 0; b < c.lifelong_blocks; ++b) kv.push_back("lifelong.block" + std::to_string(b) + ".attn.wk.w");
       for (int b = 0; b < c.lifelong_blocks; ++b) kv.push_back("lifelong.block" + std::to_string(b) + ".attn.wv.w");
       qkv_all_ = pack(hw, kv);
+      if constexpr (kBf16) {
+        if (!getenv("ORX_NO_KV_FOLD")) build_kv_fold(hw, kv);
+      }
     }
     for (int l = 0; l < enc_layers(c); ++l) {
       std::string n = "enc" + std::to_string(l);
@@ -1100,11 +1152,29 @@ class EngineT final : public Engine {
         e1.act = ACT_LEAKY;
         gemm(feat_, Fp_, m.fc1, sg_.n_rec[2], e1);
       }
-      Epi e2 = epi(keys_, d, false);
-      e2.row_map = dp<int32_t>(sg_.off_map[2]);
-      gemm(hid_, d, m.fc2, sg_.n_rec[2], e2);
+      if (kv_fold_) {  // K|V of every QFormer block straight from the hidden rows (build_kv_fold)
+        const int nb = static_cast<int>(qblocks_.size());
+        Epi ek = split_epi(vt_epi(vt_q_, Lpad_, 0, dp<int32_t>(sg_.off_key_user), dp<int32_t>(sg_.off_key_pos),
+                                  static_cast<long long>(maxU_) * d * Lpad_),
+                           kvl_, nb * d, nb * d);
+        ek.row_map = dp<int32_t>(sg_.off_map[2]);
+        gemm(hid_, d, kvf_, sg_.n_rec[2], ek);
+      } else {
+        Epi e2 = epi(keys_, d, false);
+        e2.row_map = dp<int32_t>(sg_.off_map[2]);
+        gemm(hid_, d, m.fc2, sg_.n_rec[2], e2);
+      }
     }
-    if (sg_.n_pad_keys) launch_fill_rows<T>(sg_.n_pad_keys, d, pad_l_, keys_, d, dp<int32_t>(sg_.off_pad_keys), st_);
+    if (sg_.n_pad_keys) {
+      if (kv_fold_) {
+        const int nb = static_cast<int>(qblocks_.size());
+        launch_fill_kv_pad<T>(sg_.n_pad_keys, dp<int32_t>(sg_.off_pad_keys), dp<int32_t>(sg_.off_key_user),
+                              dp<int32_t>(sg_.off_key_pos), kv_pad_, nb * d, kvl_, nb * d, vt_q_, Lpad_,
+                              static_cast<long long>(d) * Lpad_, static_cast<long long>(maxU_) * d * Lpad_, d, st_);
+      } else {
+        launch_fill_rows<T>(sg_.n_pad_keys, d, pad_l_, keys_, d, dp<int32_t>(sg_.off_pad_keys), st_);
+      }
+    }
     // QFormer blocks, no residual (nn.cpp:97-100)
     for (size_t b = 0; b < qblocks_.size(); ++b) {
       const QBlock& q = qblocks_[b];
@@ -1124,7 +1194,7 @@ class EngineT final : public Engine {
       if (tc_attn_) {
         const int nb = static_cast<int>(qblocks_.size());
         const long long vt_layer = static_cast<long long>(maxU_) * d * Lpad_;
-        if (first)  // K of every block | V^T of every block, keys_ read once
+        if (first && !kv_fold_)  // K of every block | V^T of every block, keys_ read once
           gemm(keys_, d, qkv_all_, sg_.n_keys,
                split_epi(vt_epi(vt_q_, Lpad_, 0, dp<int32_t>(sg_.off_key_user), dp<int32_t>(sg_.off_key_pos), vt_layer),
                          kvl_, nb * d, nb * d));
@@ -1962,6 +2032,9 @@ class EngineT final : public Engine {
   std::vector<EncL> enc_;
   std::vector<DecL> dec_;
   Lin<T> xkv_w_, qkv_all_;
+  Lin<T> kvf_;                    // lifelong fc2 folded into the QFormer K|V weights (build_kv_fold)
+  const float* kv_pad_ = nullptr;  // pad.lifelong . Wkv
+  bool kv_fold_ = false;
   bool tc_attn_ = false;
   int Tpad_ = 0, Lpad_ = 0;
   T *vt_enc_ = nullptr, *vt_q_ = nullptr, *vt_x_ = nullptr;

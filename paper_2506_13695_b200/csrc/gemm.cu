@@ -407,11 +407,12 @@ template <int BN>
 __device__ __forceinline__ void epilogue_tile_vt(const Epi& e, uint32_t tb, int row, int nt, int half, uint64_t* tfull,
                                                  uint32_t acc_phase) {
   constexpr int CH = BN / 32 / 2;
-  const bool valid = row < e.m_valid;
+  const int orow = row < e.m_valid ? (e.row_map ? e.row_map[row] : row) : -1;
+  const bool valid = orow >= 0;
   int u = 0, t = 0;
   if (valid) {
-    u = e.vt_row_user ? e.vt_row_user[row] : row / e.vt_T;
-    t = e.vt_row_pos ? e.vt_row_pos[row] : row % e.vt_T;
+    u = e.vt_row_user ? e.vt_row_user[orow] : orow / e.vt_T;
+    t = e.vt_row_pos ? e.vt_row_pos[orow] : orow % e.vt_T;
   }
   const int lane = threadIdx.x & 31;
   // 32 consecutive positions of one user starting at an even t0: lane pairs
@@ -429,6 +430,11 @@ __device__ __forceinline__ void epilogue_tile_vt(const Epi& e, uint32_t tb, int 
     uint32_t ra[32];
     tmem_ld32_async(tb + c * 32, ra);
     tmem_wait_ld();
+    if (e.bias) {  // bias of the GEMM output column (the folded lifelong fc2 bias through Wk|Wv)
+      const float* bp = e.bias + nt * BN + c * 32;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) ra[j] = __float_as_uint(__uint_as_float(ra[j]) + __ldg(bp + j));
+    }
     if (pairs) {
       const int oc = nt * BN + c * 32 + e.col_off - e.vt_col0;
       const int l = oc / e.vt_cols, m0 = oc - l * e.vt_cols;
@@ -716,11 +722,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (grp.tile_expert && grp.tile_expert[mt] < 0) continue;
       const int row = mt * PM + static_cast<int>(rank) * kBM + q * 32 + lane;
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-      if constexpr (EPI == (EPI_SPLITVT | EPI_BF16)) {
+      if constexpr (EPI >= 0 && (EPI & EPI_SPLITVT) != 0) {
         if (nt * BN >= epi.vt_col0)
           epilogue_tile_vt<BN>(epi, tb, row, nt, half, &tfull[acc], acc_phase);
         else
-          epilogue_tile_staged<BN, EPI_BF16>(epi, stg, tb, row, nt, half, &tfull[acc], acc_phase);
+          epilogue_tile_staged<BN, EPI & ~EPI_SPLITVT>(epi, stg, tb, row, nt, half, &tfull[acc], acc_phase);
       } else if constexpr (EPI == (EPI_SWIGLU | EPI_BF16))
         epilogue_tile_swiglu_staged<BN>(epi, stg, tb, row, nt, half, &tfull[acc], acc_phase);
       else if constexpr (EPI >= 0)
@@ -934,6 +940,13 @@ void launch_tc2_mode(int staged, const void* A, int lda, const void* B, int ldb,
       }
       launch_tc2<BN, SG, -1>(A, lda, B, ldb, M, N, K, epi, grp, stream);
       return;
+    case EPI_SPLITVT | EPI_BF16 | EPI_BIAS:
+      if constexpr (BN == 256) {
+        launch_tc2<BN, S, EPI_SPLITVT | EPI_BF16 | EPI_BIAS>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+        return;
+      }
+      launch_tc2<BN, SG, -1>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+      return;
     case EPI_SWIGLU | EPI_BF16:
       if constexpr (BN == 256) {
         launch_tc2<BN, S, EPI_SWIGLU | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream);
@@ -952,10 +965,11 @@ int epi_mode(const Epi& e) {
   const bool plain = !e.bias && !e.act && !e.row_scale && !e.resid;
   // transposed V store: generic path (its per-column stores are already coalesced
   // across lanes; a SMEM-transposed variant measured slower)
-  if (e.vt)  // split K|V GEMM: staged bf16 tiles below vt_col0, transposed tiles above
-    return plain && !e.swiglu && !e.row_map && e.out_bf16 && e.vt_col0 > 0 && e.out &&
-                   reinterpret_cast<uintptr_t>(e.out) % 16 == 0 && e.ldo % 8 == 0 && e.col_off == 0
-               ? EPI_SPLITVT | EPI_BF16
+  if (e.vt)  // split K|V GEMM: staged bf16 tiles below vt_col0, transposed tiles above (+ bias, row map)
+    return !e.act && !e.row_scale && !e.resid && !e.swiglu && e.out_bf16 && e.vt_col0 > 0 && e.out &&
+                   reinterpret_cast<uintptr_t>(e.out) % 16 == 0 && e.ldo % 8 == 0 && e.col_off == 0 &&
+                   (!e.bias || reinterpret_cast<uintptr_t>(e.bias) % 16 == 0)
+               ? EPI_SPLITVT | EPI_BF16 | (e.bias ? EPI_BIAS : 0)
                : -1;
   if (e.stats)  // head GEMM: fp32 logits + chunk statistics, nothing else
     return plain && !e.swiglu && !e.row_map && !e.out_bf16 && e.col_off == 0 && e.out &&

@@ -1231,6 +1231,26 @@ __global__ void ep_return_kernel(int El, int d, const int32_t* __restrict__ seg,
   }
 }
 
+// K|V of the empty-history pad key rows (kv = pad.lifelong . Wkv, fp32 [2 nkv]):
+// K part row-major into kvl[row][0 .. nkv), V part transposed like the split
+// K|V GEMM's epilogue (column n of layer n / d at vt[u][n % d][t]).
+template <class T>
+__global__ void fill_kv_pad_kernel(int n_pad, const int32_t* __restrict__ rows, const int32_t* __restrict__ row_user,
+                                   const int32_t* __restrict__ row_pos, const float* __restrict__ kv, int nkv,
+                                   T* __restrict__ kvl, int ldk, T* __restrict__ vt, int vt_ld,
+                                   long long vt_user_stride, long long vt_layer_stride, int d) {
+  pdl_begin();
+  for (int i = blockIdx.x; i < n_pad; i += gridDim.x) {
+    const int r = rows[i], u = row_user[r], t = row_pos[r];
+    for (int n = threadIdx.x; n < nkv; n += blockDim.x) {
+      kvl[(size_t)r * ldk + n] = from_f<T>(kv[n]);
+      const int l = n / d, m = n - l * d;
+      vt[(long long)u * vt_user_stride + t + (long long)m * vt_ld + (long long)l * vt_layer_stride] =
+          from_f<T>(kv[nkv + n]);
+    }
+  }
+}
+
 inline int grid_for(long long n, int block, int cap = 148 * 32) {
   long long g = (n + block - 1) / block;
   return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
@@ -1697,6 +1717,15 @@ void launch_ep_return(int El, int d, const int32_t* seg, const float* yg, const 
   ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_return_kernel, num_sms() * 4, 256, 0, s, El, d, seg, yg, P));
 }
 
+template <class T>
+void launch_fill_kv_pad(int n_pad, const int32_t* rows, const int32_t* row_user, const int32_t* row_pos,
+                        const float* kv, int nkv, T* kvl, int ldk, T* vt, int vt_ld, long long vt_user_stride,
+                        long long vt_layer_stride, int d, cudaStream_t s) {
+  if (n_pad <= 0) return;
+  ORX_LAUNCH(launch_pdl(fill_kv_pad_kernel<T>, std::min(n_pad, num_sms() * 4), 256, 0, s, n_pad, rows, row_user,
+                        row_pos, kv, nkv, kvl, ldk, vt, vt_ld, vt_user_stride, vt_layer_stride, d));
+}
+
 #define INST(T)                                                                                                   \
   template void launch_features<T>(const RecordsDev&, const FeatureTables&, T*, int, cudaStream_t);              \
   template void launch_static_features<T>(int, const int32_t*, const int32_t*, const int32_t*, const float*,     \
@@ -1704,6 +1733,8 @@ void launch_ep_return(int El, int d, const int32_t* seg, const float* yg, const 
   template void launch_rmsnorm<T>(int, int, const float*, int, const float*, T*, int, cudaStream_t);              \
   template void launch_convert<T>(int, int, const float*, int, T*, int, cudaStream_t);                           \
   template void launch_fill_rows<T>(int, int, const float*, T*, int, const int32_t*, cudaStream_t);              \
+  template void launch_fill_kv_pad<T>(int, const int32_t*, const int32_t*, const int32_t*, const float*, int, T*, \
+                                      int, T*, int, long long, long long, int, cudaStream_t);                      \
   template void launch_dec_self_attn<T>(int, int, int, int, int, int, const T*, T* const*, const int32_t*, int,   \
                                         T*, cudaStream_t);                                                       \
   template void launch_moe_scatter<T>(int, int, int, const T*, int, const int32_t*, const float*, int32_t*,       \

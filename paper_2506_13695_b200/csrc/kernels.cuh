@@ -87,6 +87,12 @@ void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, co
 // supported (then run launch_moe_combine + the norm / convert).
 bool launch_moe_combine_norm(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
                              const float* gain, __nv_bfloat16* out, int ldo, cudaStream_t s);
+// K|V of the empty-history pad key rows when the lifelong fc2 is folded into the
+// QFormer K|V weights (engine build_kv_fold): kv = pad . Wkv [2 nkv] (K then V).
+template <class T>
+void launch_fill_kv_pad(int n_pad, const int32_t* rows, const int32_t* row_user, const int32_t* row_pos,
+                        const float* kv, int nkv, T* kvl, int ldk, T* vt, int vt_ld, long long vt_user_stride,
+                        long long vt_layer_stride, int d, cudaStream_t s);
 // Gate scores on the tensor pipe (3xTF32, route_tc.cu) for the bf16 engine:
 // gate_hi / gate_lo [32][d] = the gain-folded gate split into tf32 hi and
 // residual lo (expert rows >= E zero). Same outputs as launch_moe_route.

@@ -366,3 +366,29 @@ def test_feature_branches(flag, precision):
             overlap = len({tuple(c) for c in codes[u]} & {tuple(c) for c in ref["beam_codes"]})
             print(f"{flag} bf16 user {u}: z {rel_inf(z[u], ref['z']):.3e} logits {el:.3e} overlap {overlap}/16")
             assert rel_inf(z[u], ref["z"]) < 3e-2 and el < 3e-2 and overlap >= 12
+
+
+@pytest.mark.parametrize("lens", [(20, 64, 300), (5, 3, 0), (0, 0, 0)])
+def test_bf16_lifelong_kv_fold(lens):
+    """bf16 + tcgen05 attention: the lifelong pathway's fc2 folded into the
+    QFormer K|V weights (EngineT::build_kv_fold) against the unfolded engine
+    (ORX_NO_KV_FOLD=1: fc2 GEMM, key rows, K|V GEMM) and the f64 reference,
+    including users without lifelong history (pad key written by
+    launch_fill_kv_pad)."""
+    import os
+    over = dict(d_model=256, n_heads=2, ffn_hidden=512)
+    sets = ["d_model=256", "n_heads=2", "ffn_hidden=512"]
+    P, model = _model("0.015B", "bf16", max_users=2, max_width=16, **over)
+    _, refs = ref_dump("0.015B", 2, 16, lens=lens, sets=sets, beam=False, n_prefix=2)
+    batch = P.SynthBatch(1, 0, 2, *lens)
+    z = model.encode_batch(batch)
+    os.environ["ORX_NO_KV_FOLD"] = "1"
+    try:
+        _, unf = _model("0.015B", "bf16", max_users=2, max_width=16, **over)
+    finally:
+        del os.environ["ORX_NO_KV_FOLD"]
+    z_unf = unf.encode_batch(batch)
+    for u, ref in enumerate(refs):
+        ez, ez_unf, pair = rel_inf(z[u], ref["z"]), rel_inf(z_unf[u], ref["z"]), rel_inf(z[u], z_unf[u])
+        print(f"kv fold lens={lens} user {u}: z {ez:.3e} (unfolded {ez_unf:.3e}, fold vs unfolded {pair:.3e})")
+        assert ez < 3e-2 and ez <= 1.5 * ez_unf + 2e-3

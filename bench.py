@@ -302,7 +302,7 @@ def parity_block(P, model, preset, width):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="orx", choices=["orx", "reference"])
     ap.add_argument("--config", default="0.935B")

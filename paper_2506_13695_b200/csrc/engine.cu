@@ -341,8 +341,10 @@ class EngineT final : public Engine {
     return upload_f32(t.data.data(), t.data.size());
   }
   // Pack several (in, out) row-major weights side by side along N: W^T [sum N][Kp].
-  Lin<T> pack(const HostWeights& hw, const std::vector<std::string>& names, const std::string& bias = "") {
+  Lin<T> pack(const HostWeights& hw, const std::vector<std::string>& names, const std::string& bias = "",
+              const std::string& in_gain = "") {
     const Tensor& f = hw.get(names[0]);
+    const float* gk = in_gain.empty() ? nullptr : hw.get(in_gain).data.data();  // RMSNorm gain folded into W rows
     int K = f.rows, N = 0;
     for (auto& n : names) {
       require(hw.get(n).rows == K, "pack: inner dims differ");
@@ -354,7 +356,9 @@ class EngineT final : public Engine {
     for (auto& n : names) {
       const Tensor& t = hw.get(n);
       for (int k = 0; k < K; ++k)
-        for (int j = 0; j < t.cols; ++j) h[static_cast<size_t>(n0 + j) * Kp + k] = to_t<T>(t.data[(size_t)k * t.cols + j]);
+        for (int j = 0; j < t.cols; ++j)
+          h[static_cast<size_t>(n0 + j) * Kp + k] = to_t<T>(gk ? gk[k] * t.data[(size_t)k * t.cols + j]
+                                                               : t.data[(size_t)k * t.cols + j]);
       n0 += t.cols;
     }
     T* d = ar_.alloc<T>(h.size());
@@ -570,6 +574,11 @@ class EngineT final : public Engine {
 
   void upload(const HostWeights& hw) {
     const orx_config& c = cfg_;
+    if constexpr (kBf16) fold_norm_ = c.d_model % 256 == 0 && !getenv("ORX_NO_NORM_FOLD");
+    if (fold_norm_) {
+      std::vector<float> ones(c.d_model, 1.f);
+      ones_ = upload_f32(ones.data(), ones.size());
+    }
     auto mlp = [&](const std::string& n) {
       return Mlp{pack(hw, {n + ".fc1.w"}, n + ".fc1.b"), pack(hw, {n + ".fc2.w"}, n + ".fc2.b")};
     };
@@ -659,11 +668,12 @@ class EngineT final : public Engine {
       EncL e;
       e.n1 = up(hw, n + ".n1.gain");
       e.n2 = up(hw, n + ".n2.gain");
-      e.wqkv = pack(hw, {n + ".attn.wq.w", n + ".attn.wk.w", n + ".attn.wv.w"});  // tcgen05 path: V transposed
+      e.wqkv = pack(hw, {n + ".attn.wq.w", n + ".attn.wk.w", n + ".attn.wv.w"}, "",
+                    fold_norm_ ? n + ".n1.gain" : "");  // tcgen05 path: V transposed
       e.wo = pack(hw, {n + ".attn.wo.w"});
       if (enc_moe(c)) e.moe = pack_moe(hw, n + ".moe", n + ".n2.gain");
       else {
-        e.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b");
+        e.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b", fold_norm_ ? n + ".n2.gain" : "");
         e.fc2 = pack(hw, {n + ".ffn.fc2.w"}, n + ".ffn.fc2.b");
       }
       enc_.push_back(e);
@@ -677,7 +687,7 @@ class EngineT final : public Engine {
       e.n3 = up(hw, n + ".n3.gain");
       e.sqkv = pack(hw, {n + ".self.wq.w", n + ".self.wk.w", n + ".self.wv.w"});
       e.so = pack(hw, {n + ".self.wo.w"});
-      e.cq = pack(hw, {n + ".cross.wq.w"});
+      e.cq = pack(hw, {n + ".cross.wq.w"}, "", fold_norm_ ? n + ".n2.gain" : "");
       e.co = pack(hw, {n + ".cross.wo.w"});
       xkv.push_back(n + ".cross.wk.w");
       xkv.push_back(n + ".cross.wv.w");
@@ -719,6 +729,10 @@ class EngineT final : public Engine {
     kvl_ = ar_.alloc<T>(static_cast<size_t>(keys_max) * std::max(2, nqb) * d);  // tcgen05: K of every QFormer block
     z_ = ar_.alloc<float>(static_cast<size_t>(rows_enc) * d);
     xn_ = ar_.alloc<T>(static_cast<size_t>(rows_big) * d);
+    if (fold_norm_) {  // per-row sum-of-squares partials of the folded RMSNorms: 2 per 256 output columns
+      ssq_ld_ = rows_big;
+      ssq_ = ar_.alloc<float>(static_cast<size_t>(2 * d / 256) * rows_big);
+    }
     qkv_ = ar_.alloc<T>(static_cast<size_t>(rows_big) * 3 * d);
     att_ = ar_.alloc<T>(static_cast<size_t>(rows_big) * d);
     ffh_ = ar_.alloc<T>(static_cast<size_t>(rows_big) * c.ffn_hidden);
@@ -1222,30 +1236,40 @@ class EngineT final : public Engine {
     }
     // encoder blocks (policy.cpp:259-263)
     const int R = U * Tn;
-    for (const EncL& l : enc_) {
-      launch_rmsnorm<T>(R, d, z_, d, l.n1, xn_, d, st_);
+    // folded RMSNorm (dense FFN encoder, bf16): each residual GEMM also writes
+    // bf16(z) and its sums of squares; QKV / fc1 carry the gains and scale rows
+    const bool nf = fold_norm_ && !enc_moe(c);
+    for (size_t li = 0; li < enc_.size(); ++li) {
+      const EncL& l = enc_[li];
+      const bool nf_in = nf && li > 0;  // layer 0's input is assembled by many producers: explicit norm
+      if (!nf_in) launch_rmsnorm<T>(R, d, z_, d, nf ? ones_ : l.n1, xn_, d, st_);
       Seg s;
       s.stride = Tn;
       s.fixed_len = Tn;
       if (tc_attn_) {
-        gemm(xn_, d, l.wqkv, R, split_epi(vt_epi(vt_enc_, Tpad_, Tn, nullptr, nullptr, 0), qkv_, 2 * d, 2 * d));
+        Epi eq = split_epi(vt_epi(vt_enc_, Tpad_, Tn, nullptr, nullptr, 0), qkv_, 2 * d, 2 * d);
+        if (nf_in) norm_in(eq);
+        gemm(xn_, d, l.wqkv, R, eq);
         FmhaArgs f = fmha(U, Tn, qkv_, R, 2 * d, qkv_, R, 2 * d, d, vt_enc_, U, Tpad_, nullptr, s, s, s,
                           4.0 * U * Tn * Tn * d);
         launch_fmha_tc(f, st_);
       } else {
-        gemm(xn_, d, l.wqkv, R, epi(qkv_, 3 * d, false));
+        Epi eq = epi(qkv_, 3 * d, false);
+        if (nf_in) norm_in(eq);
+        gemm(xn_, d, l.wqkv, R, eq);
         launch_attention<T>(U, Tn, H, dh, qkv_, 3 * d, qkv_ + d, 3 * d, qkv_ + 2 * d, 3 * d, att_, d, s, s, s, st_,
                             4.0 * U * Tn * Tn * d);
       }
       Epi eo = epi(z_, d, true);
       eo.resid = z_;
       eo.ld_resid = d;
+      if (nf) norm_out(eo);
       gemm(att_, d, l.wo, R, eo);
-      launch_rmsnorm<T>(R, d, z_, d, l.n2, xn_, d, st_);
+      if (!nf) launch_rmsnorm<T>(R, d, z_, d, l.n2, xn_, d, st_);
       if (enc_moe(c)) {
         moe(l.moe, xn_, R, z_, l.n2);
       } else {
-        ffn(l.fc1, l.fc2, xn_, R, z_);
+        ffn(l.fc1, l.fc2, xn_, R, z_, nf, nf && li + 1 < enc_.size());
       }
     }
   }
@@ -1270,15 +1294,34 @@ class EngineT final : public Engine {
     gemm(hid_, d, m.fc2, rows, e2);
   }
   // h += fc2(silu(fc1(x)))  (ffn, nn.cpp:71-73)
-  void ffn(const Lin<T>& fc1, const Lin<T>& fc2, const T* x, int rows, float* h) {
+  // fold_in: x is the un-normalised bf16 row (fc1 carries the RMSNorm gain;
+  // scales from ssq_); fold_out: fc2 also writes bf16(h) to xn_ and its sums
+  // of squares to ssq_ for the next folded RMSNorm.
+  void ffn(const Lin<T>& fc1, const Lin<T>& fc2, const T* x, int rows, float* h, bool fold_in = false,
+           bool fold_out = false) {
     const int d = cfg_.d_model;
     Epi e1 = epi(ffh_, cfg_.ffn_hidden, false);
     e1.act = ACT_SILU;
+    if (fold_in) norm_in(e1);
     gemm(x, d, fc1, rows, e1);
     Epi e2 = epi(h, d, true);
     e2.resid = h;
     e2.ld_resid = d;
+    if (fold_out) norm_out(e2);
     gemm(ffh_, cfg_.ffn_hidden, fc2, rows, e2);
+  }
+  // RMSNorm folded into the GEMMs around it (Epi::out2 / ssq / rsq, fold_norm_)
+  void norm_out(Epi& e) {
+    e.out2 = xn_;
+    e.ldo2 = cfg_.d_model;
+    e.ssq = ssq_;
+    e.ssq_ld = ssq_ld_;
+  }
+  void norm_in(Epi& e) {
+    e.rsq = ssq_;
+    e.rsq_ld = ssq_ld_;
+    e.rsq_n = 2 * cfg_.d_model / 256;
+    e.rsq_inv_d = 1.f / cfg_.d_model;
   }
   // h += MoE(x)  (moe_forward, nn.cpp:117-172)
   // post: when non-null the bf16 engine also writes the NEXT op's input from the
@@ -1502,9 +1545,16 @@ class EngineT final : public Engine {
       Epi e = epi(h_, d, true);
       e.resid = h_;
       e.ld_resid = d;
-      gemm(att_, d, w.so, rows, e);
-      launch_rmsnorm<T>(rows, d, h_, d, w.n2, xn_, d, st_);
-      gemm(xn_, d, w.cq, rows, epi(qkv_, d, false));
+      // folded n2 (cq carries its gain): beyond 128 rows the so GEMM writes bf16(h) and its sums of
+      // squares and cq scales rows; at step 0 (1-CTA GEMMs) an explicit gain-free RMSNorm
+      const bool nf2 = fold_norm_ && rows > 128;
+      Epi es = e;
+      if (nf2) norm_out(es);
+      gemm(att_, d, w.so, rows, es);
+      if (!nf2) launch_rmsnorm<T>(rows, d, h_, d, fold_norm_ ? ones_ : w.n2, xn_, d, st_);
+      Epi ecq = epi(qkv_, d, false);
+      if (nf2) norm_in(ecq);
+      gemm(xn_, d, w.cq, rows, ecq);
       if (tc_attn_) {  // beam rows of a user over its cached encoder K / V^T (computed once, prepare_decoder)
         FmhaArgs f = fmha(groups, max_group_rows, qkv_, rows, d, xkv_, static_cast<long long>(maxU_) * Tn, Ld * d,
                           l * d, vt_x_ + static_cast<size_t>(l) * maxU_ * d * Tpad_, maxU_, Tpad_, vt_user, gq, gk,
@@ -2035,6 +2085,10 @@ class EngineT final : public Engine {
   Lin<T> kvf_;                    // lifelong fc2 folded into the QFormer K|V weights (build_kv_fold)
   const float* kv_pad_ = nullptr;  // pad.lifelong . Wkv
   bool kv_fold_ = false;
+  bool fold_norm_ = false;        // RMSNorm folded into the GEMMs around it (bf16, d % 256 == 0)
+  const float* ones_ = nullptr;   // unit gain for the explicit gain-free norms of the folded path
+  float* ssq_ = nullptr;
+  long long ssq_ld_ = 0;
   bool tc_attn_ = false;
   int Tpad_ = 0, Lpad_ = 0;
   T *vt_enc_ = nullptr, *vt_q_ = nullptr, *vt_x_ = nullptr;

@@ -253,11 +253,19 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
   constexpr int CH = BN / 32 / 2;
   const int lane = threadIdx.x & 31, sub = lane >> 3, q = lane & 7;
   int orow = -1;
-  float rs = 1.f;
+  float rs = 1.f, rsq = 1.f;
   if (row < e.m_valid) {
     orow = e.row_map ? e.row_map[row] : row;
     if (MODE & EPI_RS) rs = e.row_scale[row];
+    if (MODE & EPI_RSQ) {  // folded RMSNorm: this row's scale from the producer's partial sums of squares
+      float ss = 0.f;
+      for (int i = 0; i < e.rsq_n; ++i) ss += e.rsq[(long long)i * e.rsq_ld + row];
+      rsq = rsqrtf(ss * e.rsq_inv_d + 1e-6f);
+    }
   }
+  float ssp[8];  // producer: partial sums of squares of rows 4k + sub over this warp's columns
+#pragma unroll
+  for (int k = 0; k < 8; ++k) ssp[k] = 0.f;
   int orr[8];  // output rows this lane stores: r = 4 * k + sub
 #pragma unroll
   for (int k = 0; k < 8; ++k) orr[k] = __shfl_sync(0xffffffffu, orow, 4 * k + sub);
@@ -292,6 +300,10 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(ra[j]);
+    if (MODE & EPI_RSQ) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= rsq;
+    }
     if (MODE & EPI_BIAS) {
       const float4* b4 = reinterpret_cast<const float4*>(e.bias + col0);
 #pragma unroll
@@ -346,6 +358,11 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
       } else {
         *reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)orr[k] * e.ldo + oc) = x;
       }
+      if (MODE & EPI_XSSQ) {  // the next GEMM's A operand and its RMSNorm statistics
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out2) + (size_t)orr[k] * e.ldo2 + oc) =
+            make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
+        ssp[k] += x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w;
+      }
     }
     __syncwarp();  // the next chunk reuses stg
   };
@@ -354,6 +371,16 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
   for (int i = 0; i < CH; i += 2) {
     do_chunk(i, rr[0], rr[1]);
     do_chunk(i + 1, rr[1], rr[0]);
+  }
+  if (MODE & EPI_XSSQ) {  // rows 4k + sub: reduce over the 8 lanes of the row group, one store per row
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float t = ssp[k];
+      t += __shfl_xor_sync(0xffffffffu, t, 1);
+      t += __shfl_xor_sync(0xffffffffu, t, 2);
+      t += __shfl_xor_sync(0xffffffffu, t, 4);
+      if (q == 0 && orr[k] >= 0) e.ssq[(long long)(nt * 2 + half) * e.ssq_ld + orr[k]] = t;
+    }
   }
 }
 
@@ -409,6 +436,12 @@ __device__ __forceinline__ void epilogue_tile_vt(const Epi& e, uint32_t tb, int 
   constexpr int CH = BN / 32 / 2;
   const int orow = row < e.m_valid ? (e.row_map ? e.row_map[row] : row) : -1;
   const bool valid = orow >= 0;
+  float rsq = 1.f;
+  if (e.rsq && row < e.m_valid) {  // folded RMSNorm (EPI_RSQ), as in epilogue_tile_staged
+    float ss = 0.f;
+    for (int i = 0; i < e.rsq_n; ++i) ss += e.rsq[(long long)i * e.rsq_ld + row];
+    rsq = rsqrtf(ss * e.rsq_inv_d + 1e-6f);
+  }
   int u = 0, t = 0;
   if (valid) {
     u = e.vt_row_user ? e.vt_row_user[orow] : orow / e.vt_T;
@@ -430,6 +463,10 @@ __device__ __forceinline__ void epilogue_tile_vt(const Epi& e, uint32_t tb, int 
     uint32_t ra[32];
     tmem_ld32_async(tb + c * 32, ra);
     tmem_wait_ld();
+    if (e.rsq) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) ra[j] = __float_as_uint(__uint_as_float(ra[j]) * rsq);
+    }
     if (e.bias) {  // bias of the GEMM output column (the folded lifelong fc2 bias through Wk|Wv)
       const float* bp = e.bias + nt * BN + c * 32;
 #pragma unroll
@@ -927,6 +964,36 @@ void launch_tc2_mode(int staged, const void* A, int lda, const void* B, int ldb,
     case EPI_BIAS | EPI_SILU | EPI_BF16:
       launch_tc2<BN, S, EPI_BIAS | EPI_SILU | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream);
       return;
+    case EPI_RESID | EPI_XSSQ:
+      if constexpr (BN == 256) {
+        launch_tc2<BN, S, EPI_RESID | EPI_XSSQ>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+        return;
+      }
+      break;
+    case EPI_BIAS | EPI_RESID | EPI_XSSQ:
+      if constexpr (BN == 256) {
+        launch_tc2<BN, S, EPI_BIAS | EPI_RESID | EPI_XSSQ>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+        return;
+      }
+      break;
+    case EPI_BF16 | EPI_RSQ:
+      if constexpr (BN == 256) {
+        launch_tc2<BN, S, EPI_BF16 | EPI_RSQ>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+        return;
+      }
+      break;
+    case EPI_BIAS | EPI_SILU | EPI_BF16 | EPI_RSQ:
+      if constexpr (BN == 256) {
+        launch_tc2<BN, S, EPI_BIAS | EPI_SILU | EPI_BF16 | EPI_RSQ>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+        return;
+      }
+      break;
+    case EPI_SPLITVT | EPI_BF16 | EPI_RSQ:
+      if constexpr (BN == 256) {
+        launch_tc2<BN, S, EPI_SPLITVT | EPI_BF16 | EPI_RSQ>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+        return;
+      }
+      break;
     case EPI_STATS:
       if constexpr (BN == 256) {
         launch_tc2<BN, S, EPI_STATS>(A, lda, B, ldb, M, N, K, epi, grp, stream);
@@ -955,6 +1022,7 @@ void launch_tc2_mode(int staged, const void* A, int lda, const void* B, int ldb,
       [[fallthrough]];
     default: launch_tc2<BN, SG, -1>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
   }
+  throw std::invalid_argument("gemm_bf16: epilogue mode needs 256-wide tiles");
 }
 
 }  // namespace
@@ -969,7 +1037,7 @@ int epi_mode(const Epi& e) {
     return !e.act && !e.row_scale && !e.resid && !e.swiglu && e.out_bf16 && e.vt_col0 > 0 && e.out &&
                    reinterpret_cast<uintptr_t>(e.out) % 16 == 0 && e.ldo % 8 == 0 && e.col_off == 0 &&
                    (!e.bias || reinterpret_cast<uintptr_t>(e.bias) % 16 == 0)
-               ? EPI_SPLITVT | EPI_BF16 | (e.bias ? EPI_BIAS : 0)
+               ? EPI_SPLITVT | EPI_BF16 | (e.bias ? EPI_BIAS : 0) | (e.rsq ? EPI_RSQ : 0)
                : -1;
   if (e.stats)  // head GEMM: fp32 logits + chunk statistics, nothing else
     return plain && !e.swiglu && !e.row_map && !e.out_bf16 && e.col_off == 0 && e.out &&
@@ -988,9 +1056,16 @@ int epi_mode(const Epi& e) {
   if (e.row_scale) m |= EPI_RS;
   if (e.resid) m |= EPI_RESID;
   if (e.out_bf16) m |= EPI_BF16;
+  if (e.out2) {
+    if (!e.ssq || (reinterpret_cast<uintptr_t>(e.out2) % 16) || e.ldo2 % 8) return -1;
+    m |= EPI_XSSQ;
+  }
+  if (e.rsq) m |= EPI_RSQ;
   switch (m) {
     case 0: case EPI_RS: case EPI_RESID: case EPI_BIAS | EPI_RESID: case EPI_BF16: case EPI_BIAS | EPI_BF16:
     case EPI_BIAS | EPI_LEAKY | EPI_BF16: case EPI_BIAS | EPI_SILU | EPI_BF16:
+    case EPI_RESID | EPI_XSSQ: case EPI_BIAS | EPI_RESID | EPI_XSSQ: case EPI_BF16 | EPI_RSQ:
+    case EPI_BIAS | EPI_SILU | EPI_BF16 | EPI_RSQ:
       return m;
     default:
       return -1;
@@ -1126,12 +1201,15 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
                            : -1;
     if (ep.stats && staged != EPI_STATS)
       throw std::invalid_argument("gemm_bf16: head statistics need full, aligned 256-column tiles");
+    if ((ep.out2 || ep.rsq) && (staged < 0 || small_n))
+      throw std::invalid_argument("gemm_bf16: the folded RMSNorm needs the staged 256-wide epilogue");
     if (small_n)
       launch_tc2_mode<128>(staged, A, lda, B, ldb, M, N, K, ep, grp, stream);
     else
       launch_tc2_mode<256>(staged, A, lda, B, ldb, M, N, K, ep, grp, stream);
   } else {
     if (ep.stats) throw std::invalid_argument("gemm_bf16: head statistics need the CTA-pair kernel (M > 128)");
+    if (ep.out2 || ep.rsq) throw std::invalid_argument("gemm_bf16: the folded RMSNorm needs the CTA-pair kernel");
     // M <= 128 (decoder step 0): the GEMM is a weight stream; 64-wide tiles put
     // 4x more SMs on it than 256-wide ones (N=1024: 16 CTAs instead of 4)
     const bool narrow = !epi.swiglu && !grouped && N >= 512 && M <= kBM && !getenv("ORX_GEMM_NO_NARROW");

@@ -22,7 +22,9 @@ enum EpiMode {
   EPI_BIAS = 1, EPI_LEAKY = 2, EPI_SILU = 4, EPI_RS = 8, EPI_RESID = 16, EPI_BF16 = 32,
   EPI_SWIGLU = 64,  // silu(a) * b over the interleaved W1|W3 accumulator (bf16 out, nothing else)
   EPI_SPLITVT = 128,  // bf16 out below Epi::vt_col0, transposed V store from it on (nothing else)
-  EPI_STATS = 256     // fp32 out + per-(row, 32-column chunk) log-sum-exp statistics (the head GEMM)
+  EPI_STATS = 256,    // fp32 out + per-(row, 32-column chunk) log-sum-exp statistics (the head GEMM)
+  EPI_XSSQ = 512,     // residual producers: also a bf16 copy of the output and per-row sum-of-squares partials
+  EPI_RSQ = 1024      // consumers: accumulator pre-scaled by rsqrt(mean(x^2) + eps) from those partials
 };
 
 struct Epi {
@@ -58,6 +60,20 @@ struct Epi {
   // store 256 contiguous bytes.
   float2* stats = nullptr;
   long long stats_ld = 0;
+  // RMSNorm folded into the GEMMs either side of it (bf16 engine): the GEMM
+  // that writes the fp32 residual row also writes bf16(row) to out2 and, per
+  // row and 128-column half tile, the partial sum of squares ssq[slot][row]
+  // (slot = 2 * n_tile + half). The next GEMM reads out2 as its A operand (the
+  // RMSNorm gain is folded into its weights) and scales each accumulator row
+  // by rsqrt(sum_{i < rsq_n} rsq[i][row] / d + 1e-6) before anything else.
+  void* out2 = nullptr;
+  int ldo2 = 0;
+  float* ssq = nullptr;
+  long long ssq_ld = 0;
+  const float* rsq = nullptr;
+  long long rsq_ld = 0;
+  int rsq_n = 0;
+  float rsq_inv_d = 0.f;
   int mode = -1;  // EpiMode bits of a specialised path, -1 = generic (set by gemm_bf16)
 };
 

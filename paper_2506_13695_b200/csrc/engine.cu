@@ -299,6 +299,7 @@ class EngineT final : public Engine {
   ~EngineT() override {
     cudaSetDevice(dev_);
     cudaStreamSynchronize(st_);
+    report_routing();
     for (auto& g : graphs_) cudaGraphExecDestroy(g.exec);
     for (size_t p = 0; p < ep_peer_base_.size(); ++p)
       if (static_cast<int>(p) != ep_rank_ && ep_peer_base_[p]) cudaIpcCloseMemHandle(ep_peer_base_[p]);
@@ -1339,6 +1340,7 @@ class EngineT final : public Engine {
     else
       launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.gate_gain, m.bias, sel_, wts_, counts_, st_,
                        m.gate_sw);
+    if (route_stats_) record_routing(rows);
     if (ep_world_ > 1) return moe_ep(m, x, rows, h, post, post_gain);
     launch_moe_plan(E, counts_, cursor_, tile_expert_, max_tiles_, n_mtiles_, kMoeTile, st_);
     launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xg_, row_scale_, st_);
@@ -1348,6 +1350,43 @@ class EngineT final : public Engine {
     }
     launch_moe_combine(rows, k, d, yg_, slot_, h, d, st_);
     return false;
+  }
+
+  // ORX_ROUTE_STATS (diagnostic, graphs off): per-expert token counts of every
+  // MoE call with >= 4096 rows, summarised at engine teardown as the rank-load
+  // imbalance an expert-parallel split of the experts would see.
+  void record_routing(int rows) {
+    if (rows < 4096) return;
+    std::vector<int32_t> h(cfg_.n_experts);
+    CUDA_CHECK(cudaMemcpyAsync(h.data(), counts_, h.size() * 4, cudaMemcpyDeviceToHost, st_));
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    route_hist_.push_back(std::move(h));
+  }
+  void report_routing() const {
+    if (route_hist_.empty()) return;
+    const int E = cfg_.n_experts;
+    std::vector<double> share(E, 0.0);
+    double imb[4] = {0, 0, 0, 0};
+    for (const auto& h : route_hist_) {
+      double tot = 0;
+      for (int e = 0; e < E; ++e) tot += h[e];
+      for (int e = 0; e < E; ++e) share[e] += h[e] / tot / route_hist_.size();
+      for (int wi = 0; wi < 4; ++wi) {
+        const int W = 1 << wi;
+        if (E % W) continue;
+        double mx = 0;
+        for (int r = 0; r < W; ++r) {
+          double s = 0;
+          for (int e = r * E / W; e < (r + 1) * E / W; ++e) s += h[e];
+          mx = std::max(mx, s);
+        }
+        imb[wi] += mx / (tot / W) / route_hist_.size();
+      }
+    }
+    fprintf(stderr, "[orx route] calls %zu; max/mean rank load at EP2 %.3f EP4 %.3f EP8 %.3f; expert shares:",
+            route_hist_.size(), imb[1], imb[2], imb[3]);
+    for (int e = 0; e < E; ++e) fprintf(stderr, " %.3f", share[e]);
+    fprintf(stderr, "\n");
   }
 
   // Grouped expert FFNs over xg_ (expert per M tile: tile_expert_ / n_mtiles_):
@@ -1715,7 +1754,7 @@ class EngineT final : public Engine {
     // when the request has the same shapes as a captured one (no host work
     // or launch gaps between its ~250 kernels; the expert-parallel exchange is
     // device-side too); profiling runs launch directly.
-    const bool graphs = !prof_enabled() && !getenv("ORX_NO_GRAPH");
+    const bool graphs = !prof_enabled() && !getenv("ORX_NO_GRAPH") && !route_stats_;
     int n_live = 1;
     for (int step = 0; step < L; ++step) n_live = static_cast<int>(std::min<int64_t>(width, (int64_t)n_live * V));
     int cur = L % 2;
@@ -2123,6 +2162,8 @@ class EngineT final : public Engine {
   T *xg_ = nullptr, *hg_ = nullptr;
   // expert parallelism
   int ep_rank_ = 0, ep_world_ = 1, e0_ = 0, El_ = 0;
+  const bool route_stats_ = getenv("ORX_ROUTE_STATS") != nullptr;
+  std::vector<std::vector<int32_t>> route_hist_;
   ncclComm_t comm_ = nullptr;
   EpPeers ep_{};                      // peer views of the symmetric exchange regions
   void* ep_region_ = nullptr;          // this rank's region

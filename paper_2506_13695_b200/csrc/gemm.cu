@@ -1139,6 +1139,15 @@ void prof_note(const std::string& note) {
   Prof& p = prof();
   if (p.on && !p.recs.empty()) p.recs.back().note = note;
 }
+void prof_note_launch(const char* expr) {
+  Prof& p = prof();
+  if (!p.on || p.recs.empty()) return;
+  std::string e(expr);  // "launch_pdl(kernel<...>, grid, ..." -> "kernel<...>"
+  size_t a = e.find('(');
+  a = a == std::string::npos ? 0 : a + 1;
+  size_t b = e.find(',', a);
+  p.recs.back().note = e.substr(a, std::min<size_t>(b == std::string::npos ? e.size() : b, a + 60) - a);
+}
 bool prof_enabled() { return prof().on; }
 void prof_collect(long long* count, double* ms, double* flops, double* bytes) {
   Prof& p = prof();

@@ -120,6 +120,7 @@ struct ProfScope {
 };
 void prof_enable(bool on);
 void prof_note(const std::string& note);  // label the latest record (ORX_PROF_DUMP)
+void prof_note_launch(const char* expr);  // label with the launched kernel's name (profiling only)
 bool prof_enabled();
 // Per category: launches, total ms, algorithmic flops, algorithmic bytes.
 void prof_collect(long long* count, double* ms, double* flops, double* bytes);

@@ -1262,6 +1262,7 @@ inline int grid_for(long long n, int block, int cap = 148 * 32) {
   do {                                    \
     ProfScope ps__(cat, s, 0.0, 0.0);     \
     __VA_ARGS__;                          \
+    prof_note_launch(#__VA_ARGS__);         \
     ++launch_counter();                   \
   } while (0)
 #define ORX_LAUNCH(...) ORX_LAUNCH_CAT(PROF_MISC, __VA_ARGS__)
@@ -1270,6 +1271,7 @@ inline int grid_for(long long n, int block, int cap = 148 * 32) {
   do {                                      \
     ProfScope ps__(cat, s, 0.0, (bytes));   \
     __VA_ARGS__;                            \
+    prof_note_launch(#__VA_ARGS__);         \
     ++launch_counter();                     \
   } while (0)
 

@@ -313,8 +313,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--ep", action="store_true",
-                    help="expert-parallel MoE over the N GPUs (NCCL all-to-all, BASELINE config 4); "
-                         "each rank holds n_experts / N experts")
+                    help="expert-parallel MoE over the N GPUs (peer-memory exchange, BASELINE config 4); "
+                         "each rank computes n_experts / N experts (+ replicated hot ones, --ep-replicas)")
+    ap.add_argument("--ep-replicas", type=int, default=None,
+                    help="load-balanced expert placement: at most this many replicated experts per MoE layer, "
+                         "from the expert loads of one calibration request on other users "
+                         "(default n_experts / N / 2; -1 = contiguous expert blocks, no calibration)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     lens = tuple(int(x) for x in args.lens.split(","))
@@ -340,11 +344,31 @@ def main():
 
     t_init = time.time()
     ep = args.ep and world > 1 and cfg.moe_enabled
+    ep_info = None
     if ep:
-        from paper_2506_13695_b200.dist import ep_unique_id
-        uid = ep_unique_id(device=torch.device("cuda", local))
-        model = P.PolicyModel(weights=P.Weights.random_ep(pcfg, rank, world), precision=args.precision, device=local,
-                              max_users=args.users, max_width=args.width, ep=(rank, world, uid))
+        from paper_2506_13695_b200.dist import ep_unique_id, shard_users as _shard
+
+        def ep_model(owner):
+            uid = ep_unique_id(device=torch.device("cuda", local))
+            return P.PolicyModel(weights=P.Weights.random_ep(pcfg, rank, world, owner=owner), precision=args.precision,
+                                 device=local, max_users=args.users, max_width=args.width, ep=(rank, world, uid),
+                                 ep_owner=owner)
+        model = ep_model(None)
+        reps = args.ep_replicas if args.ep_replicas is not None else pcfg.n_experts // world // 2
+        if reps >= 0:
+            # expert placement from one calibration request on OTHER users (the loads
+            # are all-gathered, so every rank computes the same placement)
+            cb, cn = _shard(rank, world, args.users)
+            calib = P.SynthBatch(7, 1_000_000 + cb, cn, *lens)
+            model.beam_search_arrays(calib, args.width)
+            owner, pred = P.ep_place(model.expert_load(), world, reps)
+            del model
+            model = ep_model(owner)
+            ep_info = {"placement": "load-balanced (calibration: 1 request, other users, seed 7)",
+                       "max_replicas": reps, "replicated_per_layer": float((owner < 0).sum(axis=1).mean()),
+                       "predicted_busiest_over_mean": [round(float(x), 3) for x in pred]}
+        else:
+            ep_info = {"placement": "contiguous expert blocks"}
     else:
         model = P.PolicyModel(pcfg, precision=args.precision, device=local, max_users=args.users,
                               max_width=args.width)
@@ -520,6 +544,8 @@ def main():
             "roofline": roofline, "kernel_classes_ms_per_step": classes,
             "cpu_baseline": cpu, "clocks": clocks, "init_s": t_init, "parity": parity,
         }
+        if ep_info:
+            line["expert_parallel"] = ep_info
         emit(line)
     if world > 1:
         dist.barrier()

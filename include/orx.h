@@ -140,11 +140,13 @@ int orx_engine_create(const orx_weights* w, int device, int precision, int32_t m
                       orx_engine** out);
 void orx_engine_destroy(orx_engine* e);
 
-/* Expert parallelism over NCCL (NVLink), SURVEY.md §8(e) / BASELINE config 4:
- * ep_world engines (one process per GPU) each hold n_experts / ep_world
- * experts of every MoE layer; MoE layers exchange (token, expert) rows with
- * NCCL send/recv. Rank 0 creates a fresh id per engine (orx_ep_unique_id;
- * an id bootstraps one communicator only) and every rank receives it out of band (e.g. torch.distributed broadcast). All ranks must
+/* Expert parallelism over NVLink peer memory, SURVEY.md §8(e) / BASELINE
+ * config 4: ep_world engines (one process per GPU) each compute n_experts /
+ * ep_world experts of every MoE layer; MoE layers exchange (token, expert)
+ * rows by device-side stores into the peers' buffers (CUDA IPC regions, set
+ * up once over an NCCL communicator). Rank 0 creates a fresh id per engine
+ * (orx_ep_unique_id; an id bootstraps one communicator only) and every rank
+ * receives it out of band (e.g. torch.distributed broadcast). All ranks must
  * then call the same sequence of orx_encode / orx_beam_search /
  * orx_score_prefixes / orx_next_logits (each with its own users; widths
  * equal). Results are bitwise identical to a replica engine's. */
@@ -152,6 +154,31 @@ void orx_engine_destroy(orx_engine* e);
 int orx_ep_unique_id(uint8_t id_out[ORX_EP_ID_BYTES]);
 int orx_engine_create_ep(const orx_weights* w, int device, int precision, int32_t max_users, int32_t max_width,
                          const uint8_t id[ORX_EP_ID_BYTES], int32_t ep_rank, int32_t ep_world, orx_engine** out);
+/* Expert placement (load balancing): owner [moe_layers * n_experts] gives,
+ * per MoE layer (encoder layers first when they are MoE, then decoder
+ * layers; orx_config_moe_layers), the rank that computes each expert, or -1
+ * = replicated on every rank (computed where the token lives, never sent).
+ * Every rank must pass the same table (checked at creation); the weights must
+ * hold the experts the rank computes (orx_weights_create_random_ep_placed, or
+ * full weights). NULL = contiguous blocks (orx_engine_create_ep). */
+int32_t orx_config_moe_layers(const orx_config* cfg);
+int orx_engine_create_ep_placed(const orx_weights* w, int device, int precision, int32_t max_users,
+                                int32_t max_width, const uint8_t id[ORX_EP_ID_BYTES], int32_t ep_rank,
+                                int32_t ep_world, const int32_t* owner, orx_engine** out);
+int orx_weights_create_random_ep_placed(const orx_config* cfg, int32_t ep_rank, int32_t ep_world,
+                                        const int32_t* owner, orx_weights** out);
+/* Rows routed to each expert of each MoE layer, summed over every rank and
+ * every MoE call since creation / the last reset: load_out [moe_layers *
+ * n_experts]; identical on every expert-parallel rank (zeros otherwise). */
+int orx_engine_expert_load(orx_engine* e, int64_t* load_out, int32_t reset);
+/* Load-balanced placement from such loads (csrc/ep_plan.hpp
+ * ep_place_balanced): per layer the fewest heaviest experts (at most
+ * max_replicas) are replicated such that the rest, packed heaviest-first onto
+ * the least-loaded rank, leave the busiest rank within 5% of the mean (else
+ * the best found). predicted_imbalance [moe_layers] (optional) = busiest /
+ * mean rank load under that placement. Deterministic. */
+int orx_ep_place(const int64_t* load, int32_t layers, int32_t n_experts, int32_t world, int32_t max_replicas,
+                 int32_t* owner_out, double* predicted_imbalance);
 
 /* z_out (host, optional): [n_users * enc_seq_len * d_model] fp32. */
 int orx_encode(orx_engine* e, const orx_user_batch* batch, float* z_out);
@@ -275,14 +302,17 @@ int orx_debug_attention(const orx_attn_args* args, void* stream);
  * fallback since the last call (process-wide counter, reset on read). */
 int64_t orx_debug_topk_fallback_rows(void);
 
-/* Host plan of one expert-parallel exchange (csrc/ep_plan.hpp), for the CPU
- * tests: counts [world * n_experts]; outputs send/recv counts and offsets
- * [world] each, tab [world * (n_experts / world) * 3] (src row, dst row,
- * count) and tiles [max_tiles] (local expert per grouped-GEMM tile, -1 past
- * the end); returns the number of tiles in use via n_tiles. */
-int orx_debug_ep_plan(int32_t world, int32_t rank, int32_t n_experts, const int32_t* counts, int32_t tile,
-                      int32_t max_tiles, int64_t* send_cnt, int64_t* send_off, int64_t* recv_cnt, int64_t* recv_off,
-                      int32_t* tab, int32_t* tiles, int32_t* n_tiles);
+/* Host restatement of the device plan of one expert-parallel exchange
+ * (csrc/ep_plan.hpp ep_plan_placed), for the CPU tests: counts [world *
+ * n_experts] (all-gathered histograms), owner [n_experts] (one layer's
+ * placement), slots = local expert slots per rank. Outputs for `rank`:
+ * cursor [n_experts] (first row of its expert-e rows in the computing rank's
+ * buffer), seg [2 * slots] (start, rows of each local slot), tiles
+ * [max_tiles] (local slot per grouped-GEMM tile, -1 past the end), n_tiles,
+ * rows_needed (its buffer rows, padded). */
+int orx_debug_ep_plan(int32_t world, int32_t rank, int32_t n_experts, const int32_t* counts, const int32_t* owner,
+                      int32_t tile, int32_t max_tiles, int32_t slots, int32_t* cursor, int32_t* seg, int32_t* tiles,
+                      int32_t* n_tiles, int64_t* rows_needed);
 
 /* Lifelong-history compression on the GPU (the step before the encoder;
  * compress_lifelong, policy.cpp:447-510, over hierarchical K-means,

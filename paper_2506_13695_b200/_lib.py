@@ -98,6 +98,9 @@ SIGNATURES = [
     ("orx_config_expert_hidden", C.c_int64, [C.POINTER(orx_config)]),
     ("orx_weights_create_random", C.c_int, [C.POINTER(orx_config), C.POINTER(_P)]),
     ("orx_weights_create_random_ep", C.c_int, [C.POINTER(orx_config), C.c_int32, C.c_int32, C.POINTER(_P)]),
+    ("orx_weights_create_random_ep_placed", C.c_int, [C.POINTER(orx_config), C.c_int32, C.c_int32, _I32P,
+                                                      C.POINTER(_P)]),
+    ("orx_config_moe_layers", C.c_int32, [C.POINTER(orx_config)]),
     ("orx_weights_load_grcp", C.c_int, [C.c_char_p, C.POINTER(_P)]),
     ("orx_weights_save_grcp", C.c_int, [_P, C.c_char_p]),
     ("orx_weights_config", C.c_int, [_P, C.POINTER(orx_config)]),
@@ -113,6 +116,11 @@ SIGNATURES = [
     ("orx_ep_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
     ("orx_engine_create_ep", C.c_int, [_P, C.c_int, C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32,
                                        C.c_int32, C.POINTER(_P)]),
+    ("orx_engine_create_ep_placed", C.c_int, [_P, C.c_int, C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_uint8),
+                                              C.c_int32, C.c_int32, _I32P, C.POINTER(_P)]),
+    ("orx_engine_expert_load", C.c_int, [_P, C.POINTER(C.c_int64), C.c_int32]),
+    ("orx_ep_place", C.c_int, [C.POINTER(C.c_int64), C.c_int32, C.c_int32, C.c_int32, C.c_int32, _I32P,
+                               C.POINTER(C.c_double)]),
     ("orx_encode", C.c_int, [_P, C.POINTER(orx_user_batch), _F32P]),
     ("orx_next_logits", C.c_int, [_P, _F32P, C.c_int32, C.c_int32, _I32P, _I32P, _I32P, _F32P]),
     ("orx_score_prefixes", C.c_int, [_P, C.POINTER(orx_user_batch), C.c_int32, _I32P, _I32P, _I32P, _F32P]),
@@ -136,9 +144,8 @@ SIGNATURES = [
     ("orx_debug_row_topk", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
     ("orx_debug_topk_fallback_rows", C.c_int64, []),
     ("orx_debug_attention", C.c_int, [C.POINTER(orx_attn_args), _P]),
-    ("orx_debug_ep_plan", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _I32P, C.c_int32, C.c_int32,
-                                    C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
-                                    C.POINTER(C.c_int64), _I32P, _I32P, _I32P]),
+    ("orx_debug_ep_plan", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _I32P, _I32P, C.c_int32, C.c_int32,
+                                    C.c_int32, _I32P, _I32P, _I32P, _I32P, C.POINTER(C.c_int64)]),
     ("orx_compress_lifelong", C.c_int, [C.c_int, C.c_int32, C.POINTER(orx_records), C.POINTER(C.c_double), C.c_int32,
                                         C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint64),
                                         C.POINTER(orx_records_out)]),

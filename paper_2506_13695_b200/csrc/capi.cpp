@@ -110,12 +110,49 @@ int orx_weights_create_random(const orx_config* cfg, orx_weights** out) {
 }
 
 int orx_weights_create_random_ep(const orx_config* cfg, int32_t ep_rank, int32_t ep_world, orx_weights** out) {
+  return orx_weights_create_random_ep_placed(cfg, ep_rank, ep_world, nullptr, out);
+}
+
+namespace {
+// a caller's placement table, validated (shape, owners, slot capacity)
+orx::EpPlacement placement_of(const orx_config& cfg, int32_t world, const int32_t* owner) {
+  orx::EpPlacement p;
+  p.layers = orx::moe_layers(cfg);
+  p.E = cfg.n_experts;
+  p.W = world;
+  p.owner.assign(owner, owner + static_cast<size_t>(p.layers) * p.E);
+  p.validate();
+  return p;
+}
+}  // namespace
+
+int orx_weights_create_random_ep_placed(const orx_config* cfg, int32_t ep_rank, int32_t ep_world,
+                                        const int32_t* owner, orx_weights** out) {
   return guarded([&] {
     need(cfg, "cfg");
     need(out, "out");
+    if (owner) {
+      if (!cfg->moe_enabled) throw orx::InvalidArgument("expert placement needs a MoE config");
+      placement_of(*cfg, ep_world, owner);
+    }
     auto w = std::make_unique<orx_weights>();
-    w->w = orx::HostWeights::random(*cfg, ep_rank, ep_world);
+    w->w = orx::HostWeights::random(*cfg, ep_rank, ep_world, owner);
     *out = w.release();
+  });
+}
+
+int32_t orx_config_moe_layers(const orx_config* cfg) { return cfg ? orx::moe_layers(*cfg) : 0; }
+
+int orx_ep_place(const int64_t* load, int32_t layers, int32_t n_experts, int32_t world, int32_t max_replicas,
+                 int32_t* owner_out, double* predicted_imbalance) {
+  return guarded([&] {
+    need(load, "load");
+    need(owner_out, "owner_out");
+    std::vector<double> pred;
+    const orx::EpPlacement p = orx::ep_place_balanced(load, layers, n_experts, world, max_replicas, 1.05, &pred);
+    p.validate();
+    std::copy(p.owner.begin(), p.owner.end(), owner_out);
+    if (predicted_imbalance) std::copy(pred.begin(), pred.end(), predicted_imbalance);
   });
 }
 
@@ -218,6 +255,12 @@ int orx_ep_unique_id(uint8_t id_out[ORX_EP_ID_BYTES]) {
 
 int orx_engine_create_ep(const orx_weights* w, int device, int precision, int32_t max_users, int32_t max_width,
                          const uint8_t id[ORX_EP_ID_BYTES], int32_t ep_rank, int32_t ep_world, orx_engine** out) {
+  return orx_engine_create_ep_placed(w, device, precision, max_users, max_width, id, ep_rank, ep_world, nullptr, out);
+}
+
+int orx_engine_create_ep_placed(const orx_weights* w, int device, int precision, int32_t max_users,
+                                int32_t max_width, const uint8_t id[ORX_EP_ID_BYTES], int32_t ep_rank,
+                                int32_t ep_world, const int32_t* owner, orx_engine** out) {
   return guarded([&] {
     need(w, "weights");
     need(out, "out");
@@ -226,6 +269,10 @@ int orx_engine_create_ep(const orx_weights* w, int device, int precision, int32_
     ep.rank = ep_rank;
     ep.world = ep_world;
     memcpy(ep.unique_id, id, ORX_EP_ID_BYTES);
+    if (owner) {
+      if (!w->w.cfg.moe_enabled) throw orx::InvalidArgument("expert placement needs a MoE config");
+      ep.owner = placement_of(w->w.cfg, ep_world, owner).owner;
+    }
     auto e = std::make_unique<orx_engine>();
     e->e = orx::Engine::create(w->w, device, precision, max_users, max_width, &ep);
     e->w = &w->w;
@@ -235,6 +282,14 @@ int orx_engine_create_ep(const orx_weights* w, int device, int precision, int32_
 }
 
 void orx_engine_destroy(orx_engine* e) { delete e; }
+
+int orx_engine_expert_load(orx_engine* e, int64_t* load_out, int32_t reset) {
+  return guarded([&] {
+    need(e, "engine");
+    need(load_out, "load_out");
+    e->e->expert_load(load_out, reset != 0);
+  });
+}
 
 int orx_encode(orx_engine* e, const orx_user_batch* batch, float* z_out) {
   return guarded([&] {
@@ -492,21 +547,19 @@ int64_t orx_debug_topk_fallback_rows(void) {
   return static_cast<int64_t>(orx::topk_fallback_rows(true));
 }
 
-int orx_debug_ep_plan(int32_t world, int32_t rank, int32_t n_experts, const int32_t* counts, int32_t tile,
-                      int32_t max_tiles, int64_t* send_cnt, int64_t* send_off, int64_t* recv_cnt, int64_t* recv_off,
-                      int32_t* tab, int32_t* tiles, int32_t* n_tiles) {
+int orx_debug_ep_plan(int32_t world, int32_t rank, int32_t n_experts, const int32_t* counts, const int32_t* owner,
+                      int32_t tile, int32_t max_tiles, int32_t slots, int32_t* cursor, int32_t* seg, int32_t* tiles,
+                      int32_t* n_tiles, int64_t* rows_needed) {
   return guarded([&] {
     need(counts, "counts");
-    need(tab, "tab");
+    need(owner, "owner");
+    need(cursor, "cursor");
+    need(seg, "seg");
     need(tiles, "tiles");
-    const orx::EpPlan pl = orx::ep_plan(world, rank, n_experts, counts, tile, max_tiles, tab, tiles);
-    for (int p = 0; p < world; ++p) {
-      if (send_cnt) send_cnt[p] = pl.send_cnt[p];
-      if (send_off) send_off[p] = pl.send_off[p];
-      if (recv_cnt) recv_cnt[p] = pl.recv_cnt[p];
-      if (recv_off) recv_off[p] = pl.recv_off[p];
-    }
-    if (n_tiles) *n_tiles = pl.n_tiles;
+    need(n_tiles, "n_tiles");
+    const int64_t r = orx::ep_plan_placed(world, rank, n_experts, counts, owner, tile, max_tiles, cursor, seg, slots,
+                                          tiles, n_tiles);
+    if (rows_needed) *rows_needed = r;
   });
 }
 

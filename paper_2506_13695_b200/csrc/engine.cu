@@ -97,6 +97,13 @@ struct MoeW {
   const void* w13 = nullptr;      // bf16: [E][2h][d] interleaved per 128 rows; fp32: w1 [E][h][d]
   const void* w3 = nullptr;       // fp32 only: [E][h][d]
   const void* w2 = nullptr;       // [E][d][h]
+  // expert parallelism: this MoE layer's placement tables (ep_plan.hpp) and
+  // accumulated per-expert loads
+  int li = 0;
+  const int32_t* ep_owner = nullptr;  // [E]
+  const int32_t* ep_slot = nullptr;   // [E]
+  const int32_t* ep_list = nullptr;   // [W][C]
+  long long* ep_load = nullptr;       // [E]
 };
 
 }  // namespace
@@ -273,11 +280,20 @@ class EngineT final : public Engine {
     if (ep && ep->world > 1) {
       require(cfg_.moe_enabled, "expert parallelism needs a MoE config");
       require(ep->rank >= 0 && ep->rank < ep->world, "expert-parallel rank outside the world");
-      require(cfg_.n_experts % ep->world == 0, "expert count must divide evenly over the expert-parallel ranks");
+      require(!ep->owner.empty() || cfg_.n_experts % ep->world == 0,
+              "expert count must divide evenly over the expert-parallel ranks");
+      require(ep->owner.empty() || ep->owner.size() == static_cast<size_t>(moe_layers(cfg_)) * cfg_.n_experts,
+              "expert placement must have moe_layers * n_experts entries");
       ep_rank_ = ep->rank;
       ep_world_ = ep->world;
-      El_ = cfg_.n_experts / ep_world_;
-      e0_ = ep_rank_ * El_;
+      const int nml = moe_layers(cfg_);
+      place_ = ep->owner.empty() ? EpPlacement::contiguous(nml, cfg_.n_experts, ep_world_) : EpPlacement{};
+      if (!ep->owner.empty()) {
+        place_.layers = nml, place_.E = cfg_.n_experts, place_.W = ep_world_;
+        place_.owner = ep->owner;
+      }
+      place_.validate();
+      El_ = place_.capacity();  // local expert slots per MoE layer (replicated + owned)
       ncclUniqueId id;
       static_assert(sizeof(id.internal) == 128, "ncclUniqueId size");
       memcpy(id.internal, ep->unique_id, 128);
@@ -324,6 +340,18 @@ class EngineT final : public Engine {
       if (!std::isfinite(p[i])) throw RuntimeError("non-finite value produced on tape");
   }
 
+  void expert_load(int64_t* out, bool reset) override {
+    require_idle();
+    const size_t E = cfg_.n_experts;
+    if (moe_layers(cfg_) == 0) return;
+    std::fill(out, out + static_cast<size_t>(moe_layers(cfg_)) * E, int64_t(0));
+    CUDA_CHECK(cudaStreamSynchronize(st_));
+    for (size_t li = 0; li < ep_loads_.size(); ++li) {
+      static_assert(sizeof(long long) == sizeof(int64_t), "load counters are 64-bit");
+      CUDA_CHECK(cudaMemcpy(out + li * E, ep_loads_[li], E * 8, cudaMemcpyDeviceToHost));
+      if (reset) CUDA_CHECK(cudaMemset(ep_loads_[li], 0, E * 8));
+    }
+  }
   void* stream() override { return st_; }
   void require_idle() const override {
     require(pending_.empty(), "a submitted beam search is in flight: collect it before synchronous calls");
@@ -456,13 +484,34 @@ class EngineT final : public Engine {
     }
     m.bias = up(hw, n + ".routing_bias");
     const int dp = rup(d, 8), hp = rup(h, 8);
-    // this rank's experts only (all of them without expert parallelism): local e -> global e0_ + e
-    auto ex = [&](int e, const char* w) {
-      return hw.get(n + ".expert" + std::to_string(e0_ + e) + "." + w + ".w");
+    // this rank's expert slots (all experts without expert parallelism): slot e -> global expert
+    m.li = n_moe_++;
+    std::vector<int> glob(static_cast<size_t>(El));
+    if (ep_world_ > 1) {
+      const std::vector<int> l = place_.local(m.li, ep_rank_);
+      for (int e = 0; e < El; ++e) glob[e] = e < static_cast<int>(l.size()) ? l[e] : -1;
+      std::vector<int32_t> list, slot;
+      place_.tables(El, list, slot);
+      const size_t W = ep_world_;
+      int32_t* t = ar_.alloc<int32_t>(2 * static_cast<size_t>(E) + W * El);
+      CUDA_CHECK(cudaMemcpy(t, place_.owner.data() + static_cast<size_t>(m.li) * E, E * 4, cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemcpy(t + E, slot.data() + static_cast<size_t>(m.li) * E, E * 4, cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemcpy(t + 2 * E, list.data() + static_cast<size_t>(m.li) * W * El, W * El * 4,
+                            cudaMemcpyHostToDevice));
+      m.ep_owner = t, m.ep_slot = t + E, m.ep_list = t + 2 * E;
+      m.ep_load = ar_.alloc<long long>(E);
+      CUDA_CHECK(cudaMemset(m.ep_load, 0, E * sizeof(long long)));
+      ep_loads_.push_back(m.ep_load);
+    } else {
+      for (int e = 0; e < El; ++e) glob[e] = e;
+    }
+    auto ex = [&](int e, const char* w) -> const Tensor& {  // empty slots (glob < 0) stay zero
+      return hw.get(n + ".expert" + std::to_string(glob[e]) + "." + w + ".w");
     };
     if (kBf16) {
       std::vector<T> w13(static_cast<size_t>(El) * 2 * h * dp, to_t<T>(0.f));
       for (int e = 0; e < El; ++e) {
+        if (glob[e] < 0) continue;
         const Tensor& w1 = ex(e, "w1");
         const Tensor& w3 = ex(e, "w3");
         for (int j = 0; j < h; ++j) {
@@ -482,6 +531,7 @@ class EngineT final : public Engine {
       for (int which = 0; which < 2; ++which) {
         std::vector<T> w(static_cast<size_t>(El) * h * dp, to_t<T>(0.f));
         for (int e = 0; e < El; ++e) {
+          if (glob[e] < 0) continue;
           const Tensor& t = ex(e, which == 0 ? "w1" : "w3");
           for (int j = 0; j < h; ++j)
             for (int k = 0; k < d; ++k) w[((size_t)e * h + j) * dp + k] = to_t<T>(t.data[(size_t)k * h + j]);
@@ -493,6 +543,7 @@ class EngineT final : public Engine {
     }
     std::vector<T> w2(static_cast<size_t>(El) * d * hp, to_t<T>(0.f));
     for (int e = 0; e < El; ++e) {
+      if (glob[e] < 0) continue;
       const Tensor& t = ex(e, "w2");  // (h, d)
       for (int k = 0; k < h; ++k)
         for (int j = 0; j < d; ++j) w2[((size_t)e * d + j) * hp + k] = to_t<T>(t.data[(size_t)k * d + j]);
@@ -805,7 +856,7 @@ class EngineT final : public Engine {
       row_scale_ = ar_.alloc<float>(S_);
       xg_ = ar_.alloc<T>(static_cast<size_t>(S_) * d);
       hg_ = ar_.alloc<T>(static_cast<size_t>(S_) * rup(h, 8));
-      yg_ = ar_.alloc<float>(static_cast<size_t>(S_) * d);
+      yg_ = ar_.alloc<T>(static_cast<size_t>(S_) * d);
       CUDA_CHECK(cudaMemset(xg_, 0, static_cast<size_t>(S_) * d * sizeof(T)));
       if (!kBf16) {
         ga_ = ar_.alloc<float>(static_cast<size_t>(S_) * h);
@@ -1391,7 +1442,9 @@ class EngineT final : public Engine {
 
   // Grouped expert FFNs over xg_ (expert per M tile: tile_expert_ / n_mtiles_):
   // yg_ = row_scale * W2(silu(W1 x) * W3 x)  (swiglu, nn.cpp:75-86; weight nn.cpp:167-168)
-  void expert_ffn(const MoeW& m, int M, long long algo_rows) {
+  // peer: expert-parallel (bf16) -- the W2 epilogue stores every output row
+  // straight into its token rank's return buffer (ep_.src codes, ep_.yr views).
+  void expert_ffn(const MoeW& m, int M, long long algo_rows, bool peer = false) {
     const orx_config& c = cfg_;
     const int d = c.d_model, he = expert_hidden(c), hp = rup(he, 8);
     Grouped g;
@@ -1407,10 +1460,14 @@ class EngineT final : public Engine {
       e1.m_valid = M;
       g.b_rows_per_expert = 2 * he;
       gemm_bf16(xg_, d, m.w13, rup(d, 8), M, 2 * he, rup(d, 8), e1, &g, st_);
-      Epi e2 = epi(yg_, d, true);
+      Epi e2 = epi(yg_, d, false);
       e2.row_scale = row_scale_;
       e2.n_out = d;
       e2.m_valid = M;
+      if (peer) {
+        e2.peer_code = ep_.src[ep_rank_];
+        for (int p = 0; p < ep_world_; ++p) e2.peer_out[p] = ep_.yr[p];
+      }
       g.b_rows_per_expert = d;
       gemm_bf16(hg_, hp, m.w2, hp, M, d, hp, e2, &g, st_);
     } else {
@@ -1450,36 +1507,43 @@ class EngineT final : public Engine {
     const size_t o_xr = take(static_cast<size_t>(recv_cap) * d * sizeof(T));
     const size_t o_wr = take(static_cast<size_t>(recv_cap) * 4);
     const size_t o_src = take(static_cast<size_t>(recv_cap) * 4);
-    const size_t o_yr = take(static_cast<size_t>(send_cap) * d * 4);
+    const size_t o_yr = take(static_cast<size_t>(send_cap) * d * sizeof(T));
     const size_t o_cnt = take(static_cast<size_t>(W) * E * 4);
     const size_t o_flag = take(static_cast<size_t>(3) * W * 4);
     CUDA_CHECK(cudaMalloc(&ep_region_, off));
     CUDA_CHECK(cudaMemset(ep_region_, 0, off));
-    cudaIpcMemHandle_t mine;
-    CUDA_CHECK(cudaIpcGetMemHandle(&mine, ep_region_));
-    // all-gather the handles (NCCL moves device memory)
+    struct Hello {  // what every rank publishes once: its region and its expert placement
+      cudaIpcMemHandle_t h;
+      uint64_t placement;
+    } mine{};
+    CUDA_CHECK(cudaIpcGetMemHandle(&mine.h, ep_region_));
+    mine.placement = 1469598103934665603ull;  // FNV-1a over the owner table
+    for (int32_t o : place_.owner) mine.placement = (mine.placement ^ static_cast<uint32_t>(o)) * 1099511628211ull;
+    // all-gather (NCCL moves device memory)
     uint8_t* dh = nullptr;
     CUDA_CHECK(cudaMalloc(&dh, static_cast<size_t>(W) * sizeof(mine)));
     CUDA_CHECK(cudaMemcpy(dh + static_cast<size_t>(ep_rank_) * sizeof(mine), &mine, sizeof(mine),
                           cudaMemcpyHostToDevice));
     NCCL_CHECK(nccl().AllGather(dh + static_cast<size_t>(ep_rank_) * sizeof(mine), dh, sizeof(mine), ncclUint8,
                                 comm_, st_));
-    std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(W));
+    std::vector<Hello> all(static_cast<size_t>(W));
     CUDA_CHECK(cudaStreamSynchronize(st_));
     CUDA_CHECK(cudaMemcpy(all.data(), dh, static_cast<size_t>(W) * sizeof(mine), cudaMemcpyDeviceToHost));
     CUDA_CHECK(cudaFree(dh));
+    for (int p = 0; p < W; ++p)
+      require(all[p].placement == mine.placement, "expert-parallel ranks were created with different expert placements");
     ep_peer_base_.assign(static_cast<size_t>(W), nullptr);
     for (int p = 0; p < W; ++p) {
       if (p == ep_rank_) {
         ep_peer_base_[p] = ep_region_;
       } else {
-        CUDA_CHECK(cudaIpcOpenMemHandle(&ep_peer_base_[p], all[p], cudaIpcMemLazyEnablePeerAccess));
+        CUDA_CHECK(cudaIpcOpenMemHandle(&ep_peer_base_[p], all[p].h, cudaIpcMemLazyEnablePeerAccess));
       }
       uint8_t* b = static_cast<uint8_t*>(ep_peer_base_[p]);
       ep_.xr[p] = b + o_xr;
       ep_.wr[p] = reinterpret_cast<float*>(b + o_wr);
       ep_.src[p] = reinterpret_cast<int32_t*>(b + o_src);
-      ep_.yr[p] = reinterpret_cast<float*>(b + o_yr);
+      ep_.yr[p] = b + o_yr;
       ep_.cnt[p] = reinterpret_cast<int32_t*>(b + o_cnt);
       ep_.flag[p] = reinterpret_cast<uint32_t*>(b + o_flag);
     }
@@ -1511,8 +1575,9 @@ class EngineT final : public Engine {
     const int d = c.d_model, E = c.n_experts, k = c.experts_active;
     launch_ep_counts(E, counts_, ep_, st_);
     launch_ep_wait(ep_, EP_COUNTS, st_);
-    launch_ep_plan(E, ep_, kMoeTile, max_tiles_, cursor_, ep_tiles_, ep_ntiles_, ep_seg_, st_);
-    launch_ep_dispatch<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, El_, ep_, st_);
+    launch_ep_plan(E, ep_, kMoeTile, max_tiles_, cursor_, ep_tiles_, ep_ntiles_, ep_seg_, m.ep_owner, m.ep_slot,
+                   m.ep_list, El_, m.ep_load, st_);
+    launch_ep_dispatch<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, m.ep_owner, ep_, st_);
     launch_ep_signal(ep_, EP_DISPATCH, st_);
     launch_ep_wait(ep_, EP_DISPATCH, st_);
     // grouped GEMMs of the local experts over the received rows (in place)
@@ -1524,15 +1589,17 @@ class EngineT final : public Engine {
     row_scale_ = ep_.wr[ep_rank_];
     tile_expert_ = ep_tiles_;
     n_mtiles_ = ep_ntiles_;
-    expert_ffn(m, static_cast<int>(S_), static_cast<long long>(rows) * k);  // FLOPs: this rank's share on average
+    // bf16: the W2 epilogue stores each output row into its token rank's return buffer
+    const bool fused_return = kBf16 && d % 128 == 0;
+    expert_ffn(m, static_cast<int>(S_), static_cast<long long>(rows) * k, fused_return);  // FLOPs: average share
     xg_ = saved_xg;
     row_scale_ = saved_rs;
     tile_expert_ = saved_te;
     n_mtiles_ = saved_nm;
-    launch_ep_return(El_, d, ep_seg_, yg_, ep_, st_);
+    if (!fused_return) launch_ep_return(El_, d, ep_seg_, yg_, ep_, st_);
     launch_ep_signal(ep_, EP_RETURN, st_);
     launch_ep_wait(ep_, EP_RETURN, st_);
-    float* yr = ep_.yr[ep_rank_];
+    const T* yr = static_cast<const T*>(ep_.yr[ep_rank_]);
     if constexpr (kBf16) {
       if (post && launch_moe_combine_norm(rows, k, d, yr, slot_, h, d, post_gain, post, d, st_)) return true;
     }
@@ -2158,10 +2225,14 @@ class EngineT final : public Engine {
   int32_t *tf_anc_, *tf_codes_, *grp_start_, *grp_len_, *grp_kstart_;
   int32_t *sel_ = nullptr, *slot_ = nullptr, *counts_ = nullptr, *cursor_ = nullptr, *tile_expert_ = nullptr,
           *n_mtiles_ = nullptr;
-  float *wts_ = nullptr, *row_scale_ = nullptr, *yg_ = nullptr, *ga_ = nullptr, *gb_ = nullptr;
+  float *wts_ = nullptr, *row_scale_ = nullptr, *ga_ = nullptr, *gb_ = nullptr;
+  T* yg_ = nullptr;  // weighted expert outputs (bf16 in the bf16 engine)
   T *xg_ = nullptr, *hg_ = nullptr;
   // expert parallelism
-  int ep_rank_ = 0, ep_world_ = 1, e0_ = 0, El_ = 0;
+  int ep_rank_ = 0, ep_world_ = 1, El_ = 0;  // El_: local expert slots per MoE layer
+  EpPlacement place_;                  // expert parallelism: who computes which expert (ep_plan.hpp)
+  int n_moe_ = 0;                      // MoE layers packed so far (MoeW::li)
+  std::vector<long long*> ep_loads_;   // per MoE layer: accumulated global rows per expert
   const bool route_stats_ = getenv("ORX_ROUTE_STATS") != nullptr;
   std::vector<std::vector<int32_t>> route_hist_;
   ncclComm_t comm_ = nullptr;

@@ -9,11 +9,15 @@
 
 namespace orx {
 
-// Expert parallelism over NCCL: rank `rank` of `world`
-// holds experts [rank * E / world, (rank + 1) * E / world) of every MoE layer.
+// Expert parallelism over NVLink peer memory: rank `rank`
+// of `world` computes the experts the placement gives it (ep_plan.hpp): by
+// default experts [rank * E / world, (rank + 1) * E / world) of every MoE
+// layer; `owner` ([moe_layers][E], rank or -1 = replicated) overrides it and
+// must be the same on every rank.
 struct EpConfig {
   int rank = 0, world = 1;
-  uint8_t unique_id[128] = {};  // ncclUniqueId
+  uint8_t unique_id[128] = {};  // ncclUniqueId (bootstraps the region exchange)
+  std::vector<int32_t> owner;
 };
 
 class Engine {
@@ -43,6 +47,10 @@ class Engine {
                            const int32_t* prefix_len, float* logits) = 0;
   virtual void score_prefixes(int n, const int32_t* user, const int32_t* prefixes, const int32_t* prefix_len,
                               float* logits) = 0;
+  // Expert parallelism: rows routed to each expert of each MoE layer, summed
+  // over every rank and every MoE call since creation (or the last reset):
+  // out [moe_layers][E]; identical on every rank. Zeros without expert parallelism.
+  virtual void expert_load(int64_t* out, bool reset) = 0;
   virtual void* stream() = 0;
   // Synchronous entry points refuse to run while a submitted search is in
   // flight (they would reuse its staging slot / drain its result).

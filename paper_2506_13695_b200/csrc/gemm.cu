@@ -106,6 +106,7 @@ __device__ __forceinline__ void epi_finish32(const Epi& e, int orow, float rs, i
     switch (e.mode) {
       case 0: epi_fast<0>(e, orow, rs, col0, v, r); return;
       case EPI_RS: epi_fast<EPI_RS>(e, orow, rs, col0, v, r); return;
+      case EPI_RS | EPI_BF16: epi_fast<EPI_RS | EPI_BF16>(e, orow, rs, col0, v, r); return;
       case EPI_RESID: epi_fast<EPI_RESID>(e, orow, rs, col0, v, r); return;
       case EPI_BIAS | EPI_RESID: epi_fast<EPI_BIAS | EPI_RESID>(e, orow, rs, col0, v, r); return;
       case EPI_BF16: epi_fast<EPI_BF16>(e, orow, rs, col0, v, r); return;
@@ -254,8 +255,15 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
   const int lane = threadIdx.x & 31, sub = lane >> 3, q = lane & 7;
   int orow = -1;
   float rs = 1.f, rsq = 1.f;
+  unsigned long long pbase = 0;  // EPI_PEER: this row's destination buffer
   if (row < e.m_valid) {
-    orow = e.row_map ? e.row_map[row] : row;
+    if (MODE & EPI_PEER) {
+      const int code = e.peer_code[row];
+      orow = code < 0 ? -1 : (code & 0xFFFFFF);
+      pbase = reinterpret_cast<unsigned long long>(e.peer_out[code < 0 ? 0 : (code >> 24)]);
+    } else {
+      orow = e.row_map ? e.row_map[row] : row;
+    }
     if (MODE & EPI_RS) rs = e.row_scale[row];
     if (MODE & EPI_RSQ) {  // folded RMSNorm: this row's scale from the producer's partial sums of squares
       float ss = 0.f;
@@ -269,6 +277,11 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
   int orr[8];  // output rows this lane stores: r = 4 * k + sub
 #pragma unroll
   for (int k = 0; k < 8; ++k) orr[k] = __shfl_sync(0xffffffffu, orow, 4 * k + sub);
+  unsigned long long pb[(MODE & EPI_PEER) ? 8 : 1];
+  if constexpr ((MODE & EPI_PEER) != 0) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pb[k] = __shfl_sync(0xffffffffu, pbase, 4 * k + sub);
+  }
   if (MODE & EPI_RESID) {
     if (orow >= 0)  // this row's residual segment into L2 while the MMAs run
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(e.resid + (size_t)orow * e.ld_resid +
@@ -352,7 +365,10 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
         const float4 y = cur[k];
         x.x += y.x, x.y += y.y, x.z += y.z, x.w += y.w;
       }
-      if (MODE & EPI_BF16) {
+      if constexpr ((MODE & EPI_PEER) != 0) {
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(pb[k]) + (size_t)orr[k] * e.ldo + oc) =
+            make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
+      } else if (MODE & EPI_BF16) {
         *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)orr[k] * e.ldo + oc) =
             make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
       } else {
@@ -954,6 +970,10 @@ void launch_tc2_mode(int staged, const void* A, int lda, const void* B, int ldb,
   switch (staged) {
     case 0: launch_tc2<BN, S, 0>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
     case EPI_RS: launch_tc2<BN, S, EPI_RS>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
+    case EPI_RS | EPI_BF16: launch_tc2<BN, S, EPI_RS | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
+    case EPI_RS | EPI_BF16 | EPI_PEER:
+      launch_tc2<BN, S, EPI_RS | EPI_BF16 | EPI_PEER>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+      return;
     case EPI_RESID: launch_tc2<BN, S, EPI_RESID>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
     case EPI_BIAS | EPI_RESID: launch_tc2<BN, S, EPI_BIAS | EPI_RESID>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
     case EPI_BF16: launch_tc2<BN, S, EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
@@ -1061,7 +1081,9 @@ int epi_mode(const Epi& e) {
     m |= EPI_XSSQ;
   }
   if (e.rsq) m |= EPI_RSQ;
+  if (e.peer_code) m |= EPI_PEER;
   switch (m) {
+    case EPI_RS | EPI_BF16: case EPI_RS | EPI_BF16 | EPI_PEER:
     case 0: case EPI_RS: case EPI_RESID: case EPI_BIAS | EPI_RESID: case EPI_BF16: case EPI_BIAS | EPI_BF16:
     case EPI_BIAS | EPI_LEAKY | EPI_BF16: case EPI_BIAS | EPI_SILU | EPI_BF16:
     case EPI_RESID | EPI_XSSQ: case EPI_BIAS | EPI_RESID | EPI_XSSQ: case EPI_BF16 | EPI_RSQ:
@@ -1212,6 +1234,8 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
       throw std::invalid_argument("gemm_bf16: head statistics need full, aligned 256-column tiles");
     if ((ep.out2 || ep.rsq) && (staged < 0 || small_n))
       throw std::invalid_argument("gemm_bf16: the folded RMSNorm needs the staged 256-wide epilogue");
+    if (ep.peer_code && staged < 0)
+      throw std::invalid_argument("gemm_bf16: peer-scattered rows need the staged epilogue (full 128-column tiles)");
     if (small_n)
       launch_tc2_mode<128>(staged, A, lda, B, ldb, M, N, K, ep, grp, stream);
     else
@@ -1219,6 +1243,7 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
   } else {
     if (ep.stats) throw std::invalid_argument("gemm_bf16: head statistics need the CTA-pair kernel (M > 128)");
     if (ep.out2 || ep.rsq) throw std::invalid_argument("gemm_bf16: the folded RMSNorm needs the CTA-pair kernel");
+    if (ep.peer_code) throw std::invalid_argument("gemm_bf16: peer-scattered rows need the CTA-pair kernel");
     // M <= 128 (decoder step 0): the GEMM is a weight stream; 64-wide tiles put
     // 4x more SMs on it than 256-wide ones (N=1024: 16 CTAs instead of 4)
     const bool narrow = !epi.swiglu && !grouped && N >= 512 && M <= kBM && !getenv("ORX_GEMM_NO_NARROW");

@@ -24,8 +24,10 @@ enum EpiMode {
   EPI_SPLITVT = 128,  // bf16 out below Epi::vt_col0, transposed V store from it on (nothing else)
   EPI_STATS = 256,    // fp32 out + per-(row, 32-column chunk) log-sum-exp statistics (the head GEMM)
   EPI_XSSQ = 512,     // residual producers: also a bf16 copy of the output and per-row sum-of-squares partials
-  EPI_RSQ = 1024      // consumers: accumulator pre-scaled by rsqrt(mean(x^2) + eps) from those partials
+  EPI_RSQ = 1024,     // consumers: accumulator pre-scaled by rsqrt(mean(x^2) + eps) from those partials
+  EPI_PEER = 2048     // rows scattered to peer memory: row r -> peer_out[code >> 24] + (code & 0xFFFFFF) * ldo
 };
+constexpr int kEpiMaxPeers = 8;
 
 struct Epi {
   const float* bias = nullptr;       // [N] (or [N/2] for swiglu: not used)
@@ -74,6 +76,12 @@ struct Epi {
   long long rsq_ld = 0;
   int rsq_n = 0;
   float rsq_inv_d = 0.f;
+  // Expert-parallel return fused into the grouped W2 GEMM (EPI_PEER, bf16 out):
+  // output row r goes to peer_out[code >> 24] + (code & 0xFFFFFF) * ldo with
+  // code = peer_code[r] (< 0: padding row, not stored) -- the token's rank's
+  // return buffer, mapped into this process over NVLink.
+  const int32_t* peer_code = nullptr;
+  void* peer_out[kEpiMaxPeers] = {};
   int mode = -1;  // EpiMode bits of a specialised path, -1 = generic (set by gemm_bf16)
 };
 

@@ -514,8 +514,18 @@ __global__ void __launch_bounds__(256) dec_self_attn4_kernel(int rows, int d, in
   }
 }
 
+// four consecutive expert-output elements (fp32, or bf16 in the bf16 engine)
+__device__ __forceinline__ float4 ldy4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 ldy4(const __nv_bfloat16* p) {
+  const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
 // h[r] += sum_j (ascending expert) y[slot[r][j]], float4 per thread (d % 4 == 0).
-__global__ void __launch_bounds__(256) moe_combine4_kernel(int rows, int k, int d, const float* __restrict__ yg,
+template <class YT>
+__global__ void __launch_bounds__(256) moe_combine4_kernel(int rows, int k, int d, const YT* __restrict__ yg,
                                                            const int32_t* __restrict__ slot, float* __restrict__ h,
                                                            int ldh) {
   pdl_begin();
@@ -523,9 +533,9 @@ __global__ void __launch_bounds__(256) moe_combine4_kernel(int rows, int k, int 
   const long long n = (long long)rows * q;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int r = static_cast<int>(i / q), c = static_cast<int>(i % q) * 4;
-    float4 acc = __ldg(reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k] * d + c));
+    float4 acc = ldy4(yg + (size_t)slot[(size_t)r * k] * d + c);
     for (int j = 1; j < k; ++j) {
-      const float4 y = __ldg(reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k + j] * d + c));
+      const float4 y = ldy4(yg + (size_t)slot[(size_t)r * k + j] * d + c);
       acc.x += y.x, acc.y += y.y, acc.z += y.z, acc.w += y.w;
     }
     float4* hp = reinterpret_cast<float4*>(h + (size_t)r * ldh + c);
@@ -1033,14 +1043,15 @@ __global__ void __launch_bounds__(256) moe_scatter32_kernel(int rows, int k, int
 }
 
 // h[r] += sum_j (ascending expert) y[slot[r][j]]; y already carries the gate weight.
-__global__ void moe_combine_kernel(int rows, int k, int d, const float* __restrict__ yg,
+template <class YT>
+__global__ void moe_combine_kernel(int rows, int k, int d, const YT* __restrict__ yg,
                                    const int32_t* __restrict__ slot, float* __restrict__ h, int ldh) {
   pdl_begin();
   int r = blockIdx.x;
   if (r >= rows) return;
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
     float acc = 0.f;
-    for (int j = 0; j < k; ++j) acc += yg[(size_t)slot[(size_t)r * k + j] * d + c];
+    for (int j = 0; j < k; ++j) acc += to_f(yg[(size_t)slot[(size_t)r * k + j] * d + c]);
     h[(size_t)r * ldh + c] += acc;
   }
 }
@@ -1111,57 +1122,73 @@ __global__ void ep_wait_kernel(EpPeers P, int phase) {
   __threadfence();
 }
 
-// Device plan (the same arithmetic as ep_plan.hpp, on every rank from the same
-// histograms): owner p's grouped buffer holds, per local expert el in order, a
-// segment of sum_q cnt[q][p El + el] rows (source rank major) padded to `tile`.
+// Device plan (the same arithmetic as ep_plan_placed, ep_plan.hpp, on every
+// rank from the same histograms): rank p's grouped buffer holds, per local slot
+// j (global expert list[p][j]), a segment of that expert's rows -- every rank's
+// (source-rank major) for an owned expert, p's own for a replicated one
+// (owner -1) -- padded to `tile`. Also accumulates the layer's global expert
+// loads (placement statistics) and marks the padding rows (no source).
 __global__ void ep_plan_kernel(int E, EpPeers P, int tile, int max_tiles, int32_t* __restrict__ cursor,
                                int32_t* __restrict__ tile_expert, int32_t* __restrict__ n_mtiles,
-                               int32_t* __restrict__ seg) {
+                               int32_t* __restrict__ seg, const int32_t* __restrict__ owner,
+                               const int32_t* __restrict__ slot, const int32_t* __restrict__ list, int C,
+                               long long* __restrict__ load) {
   pdl_begin();
   const int32_t* cnt = P.cnt[P.me];  // local copy [W][E]
-  const int W = P.world, El = E / W;
-  __shared__ int32_t seg_start[32], tot[32];
+  const int W = P.world;
+  __shared__ int32_t tot[32], seg_start[kEpMaxWorld * 32], seg_rows[kEpMaxWorld * 32];
   const int e = threadIdx.x;
   if (e < E) {
     int t = 0;
     for (int q = 0; q < W; ++q) t += cnt[q * E + e];
     tot[e] = t;
+    if (load) load[e] += t;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int p = 0; p < W; ++p) {
-      int off = 0;
-      for (int el = 0; el < El; ++el) {
-        seg_start[p * El + el] = off;
-        off += (tot[p * El + el] + tile - 1) / tile * tile;
-      }
+  if (threadIdx.x < W) {
+    const int p = threadIdx.x;
+    int off = 0;
+    for (int j = 0; j < C; ++j) {
+      const int g = list[p * C + j];
+      const int n = g < 0 ? 0 : (owner[g] < 0 ? cnt[p * E + g] : tot[g]);
+      seg_start[p * 32 + j] = off;
+      seg_rows[p * 32 + j] = n;
+      off += (n + tile - 1) / tile * tile;
     }
+    if (p == P.me && off > P.recv_cap) *P.err = 2;
   }
   __syncthreads();
   if (e < E) {
+    const int o = owner[e];
     int before = 0;
-    for (int q = 0; q < P.me; ++q) before += cnt[q * E + e];
-    cursor[e] = seg_start[e] + before;
+    if (o >= 0)
+      for (int q = 0; q < P.me; ++q) before += cnt[q * E + e];
+    cursor[e] = seg_start[(o < 0 ? P.me : o) * 32 + slot[e]] + before;
   }
+  const int* my_start = seg_start + P.me * 32;
+  const int* my_rows = seg_rows + P.me * 32;
   if (threadIdx.x == 0) {
     int nt = 0;
-    for (int el = 0; el < El; ++el) {
-      const int g = P.me * El + el;
-      seg[2 * el] = seg_start[g];
-      seg[2 * el + 1] = tot[g];
-      for (int i = 0; i < (tot[g] + tile - 1) / tile && nt < max_tiles; ++i) tile_expert[nt++] = el;
+    for (int j = 0; j < C; ++j) {
+      seg[2 * j] = my_start[j];
+      seg[2 * j + 1] = my_rows[j];
+      for (int i = 0; i < (my_rows[j] + tile - 1) / tile && nt < max_tiles; ++i) tile_expert[nt++] = j;
     }
-    const int last = El ? seg_start[P.me * El + El - 1] + (tot[P.me * El + El - 1] + tile - 1) / tile * tile : 0;
-    if (last > P.recv_cap) *P.err = 2;
     *n_mtiles = nt;
     for (int i = nt; i < max_tiles; ++i) tile_expert[i] = -1;
+  }
+  // padding rows of the local segments: no source (the fused return skips them)
+  for (int j = 0; j < C; ++j) {
+    const int end = min(my_start[j] + (my_rows[j] + tile - 1) / tile * tile, P.recv_cap);
+    for (int i = my_start[j] + my_rows[j] + threadIdx.x; i < end; i += blockDim.x) P.src[P.me][i] = -1;
   }
 }
 
 template <class T>
 __global__ void ep_dispatch_kernel(int rows, int k, int d, const T* __restrict__ x, int ldx,
                                    const int32_t* __restrict__ sel, const float* __restrict__ wts,
-                                   int32_t* __restrict__ cursor, int32_t* __restrict__ slot, int El, EpPeers P) {
+                                   int32_t* __restrict__ cursor, int32_t* __restrict__ slot,
+                                   const int32_t* __restrict__ owner_of, EpPeers P) {
   pdl_begin();
   const int lane = threadIdx.x & 31;
   const int n_pairs = rows * k;
@@ -1177,7 +1204,8 @@ __global__ void ep_dispatch_kernel(int rows, int k, int d, const T* __restrict__
     if (on && lane == leader) base = atomicAdd(&cursor[e], __popc(peers));
     base = __shfl_sync(0xffffffffu, base, leader);
     const int pos = base + __popc(peers & ((1u << lane) - 1u));
-    const int owner = on ? e / El : 0;
+    const int own = on ? owner_of[e] : 0;
+    const int owner = own < 0 ? P.me : own;  // replicated experts run where the token lives
     const bool fits = pos < P.recv_cap;
     if (on && fits) {
       slot[gw] = gw;
@@ -1207,8 +1235,65 @@ __global__ void ep_dispatch_kernel(int rows, int k, int d, const T* __restrict__
   }
 }
 
-// Warp per received row: the weighted expert output goes back to yr[slot] on the token's rank.
-__global__ void ep_return_kernel(int El, int d, const int32_t* __restrict__ seg, const float* __restrict__ yg,
+// Row-major form for bf16, d = 256 * NV, k | 32: a warp assigns 32 (token,
+// expert) pairs (= 32 / k tokens) as above, then loads each token row ONCE
+// (coalesced, NV x 16 B per lane) and stores it to its k destinations -- the
+// peer stores are posted writes, so the next row's loads overlap them.
+template <int NV>
+__global__ void __launch_bounds__(256) ep_dispatch_rows_kernel(int rows, int k, int d,
+                                                               const __nv_bfloat16* __restrict__ x, int ldx,
+                                                               const int32_t* __restrict__ sel,
+                                                               const float* __restrict__ wts,
+                                                               int32_t* __restrict__ cursor, int32_t* __restrict__ slot,
+                                                               const int32_t* __restrict__ owner_of, EpPeers P) {
+  pdl_begin();
+  const int lane = threadIdx.x & 31;
+  const int n_pairs = rows * k, tpw = 32 / k;
+  for (int base_pair = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base_pair < n_pairs;
+       base_pair += gridDim.x * (blockDim.x >> 5) * 32) {
+    const int gw = base_pair + lane;
+    const bool on = gw < n_pairs;
+    const int e = on ? sel[gw] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (on && lane == leader) base = atomicAdd(&cursor[e], __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    const int pos = base + __popc(peers & ((1u << lane) - 1u));
+    const int own = on ? owner_of[e] : 0;
+    const int owner = own < 0 ? P.me : own;
+    if (on && pos < P.recv_cap) {
+      slot[gw] = gw;
+      P.wr[owner][pos] = wts[gw];
+      P.src[owner][pos] = (P.me << 24) | gw;
+    } else if (on) {
+      *P.err = 2;
+    }
+    const int r0 = base_pair / k;
+#pragma unroll 2
+    for (int t = 0; t < tpw; ++t) {
+      const int r = r0 + t;
+      if (r >= rows) break;
+      const uint4* a = reinterpret_cast<const uint4*>(x + (size_t)r * ldx);
+      uint4 v[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) v[q] = __ldg(a + lane + 32 * q);
+      for (int j = 0; j < k; ++j) {
+        const int s = __shfl_sync(0xffffffffu, pos, t * k + j);
+        const int o = __shfl_sync(0xffffffffu, owner, t * k + j);
+        if (s >= P.recv_cap) continue;
+        uint4* b = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(P.xr[o]) + (size_t)s * d);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) b[lane + 32 * q] = v[q];
+      }
+    }
+  }
+}
+
+// Warp per received row: the weighted expert output goes back to yr[slot] on the
+// token's rank (fp32 engine; the bf16 engine stores from the W2 GEMM epilogue).
+template <class T>
+__global__ void ep_return_kernel(int El, int d, const int32_t* __restrict__ seg, const T* __restrict__ yg,
                                  EpPeers P) {
   pdl_begin();
   const int lane = threadIdx.x & 31;
@@ -1219,11 +1304,12 @@ __global__ void ep_return_kernel(int El, int d, const int32_t* __restrict__ seg,
     for (int i = wid; i < n; i += nw) {
       const int code = src[s0 + i];
       const int q = code >> 24, gw = code & 0xFFFFFF;
-      const float* a = yg + (size_t)(s0 + i) * d;
-      float* b = P.yr[q] + (size_t)gw * d;
-      if (d % 4 == 0) {
-        for (int c = lane * 4; c < d; c += 128)
-          *reinterpret_cast<float4*>(b + c) = *reinterpret_cast<const float4*>(a + c);
+      const T* a = yg + (size_t)(s0 + i) * d;
+      T* b = static_cast<T*>(P.yr[q]) + (size_t)gw * d;
+      constexpr int V = 16 / sizeof(T);
+      if (d % V == 0) {
+        for (int c = lane * V; c < d; c += 32 * V)
+          *reinterpret_cast<uint4*>(b + c) = *reinterpret_cast<const uint4*>(a + c);
       } else {
         for (int c = lane; c < d; c += 32) b[c] = a[c];
       }
@@ -1606,8 +1692,8 @@ void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32
 // NEXT op's input from the updated row while it is in registers: the next
 // layer's RMSNorm (gain) or, for the head, a plain bf16 copy (gain null) —
 // as rmsnorm4_kernel / convert would compute it, one pass over h instead of two.
-template <int NC>
-__global__ void __launch_bounds__(256) moe_combine_norm_kernel(int rows, int k, int d, const float* __restrict__ yg,
+template <int NC, class YT>
+__global__ void __launch_bounds__(256) moe_combine_norm_kernel(int rows, int k, int d, const YT* __restrict__ yg,
                                                                const int32_t* __restrict__ slot, float* __restrict__ h,
                                                                int ldh, const float* __restrict__ gain,
                                                                __nv_bfloat16* __restrict__ out, int ldo) {
@@ -1619,17 +1705,17 @@ __global__ void __launch_bounds__(256) moe_combine_norm_kernel(int rows, int k, 
   // to memory per row instead of one per column chunk
   float4 v[NC], acc[NC];
   float4* hr = reinterpret_cast<float4*>(h + (size_t)r * ldh);
-  const float4* y0 = reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k] * d);
+  const YT* y0 = yg + (size_t)slot[(size_t)r * k] * d;
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
     v[i] = hr[lane + 32 * i];
-    acc[i] = __ldg(y0 + lane + 32 * i);
+    acc[i] = ldy4(y0 + 4 * (lane + 32 * i));
   }
   for (int j = 1; j < k; ++j) {  // ascending expert order, as the reference combines (nn.cpp:152-169)
-    const float4* yj = reinterpret_cast<const float4*>(yg + (size_t)slot[(size_t)r * k + j] * d);
+    const YT* yj = yg + (size_t)slot[(size_t)r * k + j] * d;
     float4 y[NC];
 #pragma unroll
-    for (int i = 0; i < NC; ++i) y[i] = __ldg(yj + lane + 32 * i);
+    for (int i = 0; i < NC; ++i) y[i] = ldy4(yj + 4 * (lane + 32 * i));
 #pragma unroll
     for (int i = 0; i < NC; ++i) acc[i].x += y[i].x, acc[i].y += y[i].y, acc[i].z += y[i].z, acc[i].w += y[i].w;
   }
@@ -1658,32 +1744,34 @@ __global__ void __launch_bounds__(256) moe_combine_norm_kernel(int rows, int k, 
   }
 }
 
-bool launch_moe_combine_norm(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
+template <class YT>
+bool launch_moe_combine_norm(int rows, int k, int d, const YT* yg, const int32_t* slot, float* h, int ldh,
                              const float* gain, __nv_bfloat16* out, int ldo, cudaStream_t s) {
   if ((d != 512 && d != 1024) || ldh % 4 || ldo % 4 || reinterpret_cast<uintptr_t>(h) % 16 ||
       reinterpret_cast<uintptr_t>(out) % 16 || (gain && reinterpret_cast<uintptr_t>(gain) % 16) ||
       getenv("ORX_NO_COMBINE_NORM"))
     return false;
   if (rows <= 0) return true;
-  const double nb = double(rows) * d * (4.0 * k + 8.0 + 2.0);  // k expert outputs + residual in/out + bf16 row
+  const double nb = double(rows) * d * (sizeof(YT) * k + 8.0 + 2.0);  // k expert outputs + residual in/out + bf16 row
   if (d == 1024)
-    ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_norm_kernel<8>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
+    ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_norm_kernel<8, YT>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
                                               slot, h, ldh, gain, out, ldo));
   else
-    ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_norm_kernel<4>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
+    ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_norm_kernel<4, YT>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
                                               slot, h, ldh, gain, out, ldo));
   return true;
 }
 
-void launch_moe_combine(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
+template <class YT>
+void launch_moe_combine(int rows, int k, int d, const YT* yg, const int32_t* slot, float* h, int ldh,
                         cudaStream_t s) {
-  const double nb = double(rows) * d * (4.0 * k + 8.0 + 2.0);  // k expert outputs + residual in/out (+ bf16 row)
+  const double nb = double(rows) * d * (sizeof(YT) * k + 8.0);  // k expert outputs + residual in/out
   if (rows <= 0) return;
   if (d % 4 == 0 && ldh % 4 == 0) {
-    ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine4_kernel, grid_for((long long)rows * d / 4, 256, num_sms() * 8), 256, 0, s, rows, k, d, yg, slot, h, ldh));
+    ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine4_kernel<YT>, grid_for((long long)rows * d / 4, 256, num_sms() * 8), 256, 0, s, rows, k, d, yg, slot, h, ldh));
     return;
   }
-  ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_kernel, rows, 256, 0, s, rows, k, d, yg, slot, h, ldh));
+  ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_kernel<YT>, rows, 256, 0, s, rows, k, d, yg, slot, h, ldh));
 }
 void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, cudaStream_t s) {
   if (n <= 0) return;
@@ -1700,23 +1788,35 @@ void launch_ep_wait(const EpPeers& P, int phase, cudaStream_t s) {
   ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_wait_kernel, 1, 32, 0, s, P, phase));
 }
 void launch_ep_plan(int E, const EpPeers& P, int tile, int max_tiles, int32_t* cursor, int32_t* tile_expert,
-                    int32_t* n_mtiles, int32_t* seg, cudaStream_t s) {
-  if (E > 32 || E % P.world) throw std::invalid_argument("ep_plan: at most 32 experts, divisible by the world");
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE,
-                 launch_pdl(ep_plan_kernel, 1, 32, 0, s, E, P, tile, max_tiles, cursor, tile_expert, n_mtiles, seg));
+                    int32_t* n_mtiles, int32_t* seg, const int32_t* owner, const int32_t* slot, const int32_t* list,
+                    int C, long long* load, cudaStream_t s) {
+  if (E > 32 || C > 32 || P.world > kEpMaxWorld) throw std::invalid_argument("ep_plan: at most 32 experts / slots");
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_plan_kernel, 1, 32, 0, s, E, P, tile, max_tiles, cursor, tile_expert,
+                                            n_mtiles, seg, owner, slot, list, C, load));
 }
 template <class T>
 void launch_ep_dispatch(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
-                        int32_t* cursor, int32_t* slot, int El, const EpPeers& P, cudaStream_t s) {
+                        int32_t* cursor, int32_t* slot, const int32_t* owner, const EpPeers& P, cudaStream_t s) {
   if (rows <= 0) return;
   const double nb = double(rows) * k * (d * sizeof(T) + 8.0) + double(rows) * d * sizeof(T);
   const long long warps = ((long long)rows * k + 31) / 32;
+  if constexpr (sizeof(T) == 2) {
+    const int nv = d / 256;
+    if (d % 256 == 0 && 32 % k == 0 && ldx % 8 == 0 && (nv == 1 || nv == 2 || nv == 4)) {
+      auto kern = nv == 4 ? ep_dispatch_rows_kernel<4> : nv == 2 ? ep_dispatch_rows_kernel<2> : ep_dispatch_rows_kernel<1>;
+      ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb,
+                      launch_pdl(kern, grid_for(warps, 8, num_sms() * 8), 256, 0, s, rows, k, d,
+                                 reinterpret_cast<const __nv_bfloat16*>(x), ldx, sel, wts, cursor, slot, owner, P));
+      return;
+    }
+  }
   ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb,
                   launch_pdl(ep_dispatch_kernel<T>, grid_for(warps, 8, num_sms() * 8), 256, 0, s, rows, k, d, x, ldx,
-                             sel, wts, cursor, slot, El, P));
+                             sel, wts, cursor, slot, owner, P));
 }
-void launch_ep_return(int El, int d, const int32_t* seg, const float* yg, const EpPeers& P, cudaStream_t s) {
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_return_kernel, num_sms() * 4, 256, 0, s, El, d, seg, yg, P));
+template <class T>
+void launch_ep_return(int El, int d, const int32_t* seg, const T* yg, const EpPeers& P, cudaStream_t s) {
+  ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(ep_return_kernel<T>, num_sms() * 4, 256, 0, s, El, d, seg, yg, P));
 }
 
 template <class T>
@@ -1742,7 +1842,11 @@ void launch_fill_kv_pad(int n_pad, const int32_t* rows, const int32_t* row_user,
   template void launch_moe_scatter<T>(int, int, int, const T*, int, const int32_t*, const float*, int32_t*,       \
                                       int32_t*, T*, float*, cudaStream_t);                                        \
   template void launch_ep_dispatch<T>(int, int, int, const T*, int, const int32_t*, const float*, int32_t*,       \
-                                      int32_t*, int, const EpPeers&, cudaStream_t);
+                                      int32_t*, const int32_t*, const EpPeers&, cudaStream_t);                               \
+  template void launch_ep_return<T>(int, int, const int32_t*, const T*, const EpPeers&, cudaStream_t);           \
+  template void launch_moe_combine<T>(int, int, int, const T*, const int32_t*, float*, int, cudaStream_t);         \
+  template bool launch_moe_combine_norm<T>(int, int, int, const T*, const int32_t*, float*, int, const float*,    \
+                                           __nv_bfloat16*, int, cudaStream_t);
 INST(float)
 INST(__nv_bfloat16)
 

@@ -85,7 +85,8 @@ void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, co
 // bf16 engine: the MoE combine fused with the next op's input (RMSNorm with
 // `gain`, or a plain bf16 copy when gain is null); false if the shape is not
 // supported (then run launch_moe_combine + the norm / convert).
-bool launch_moe_combine_norm(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
+template <class YT>
+bool launch_moe_combine_norm(int rows, int k, int d, const YT* yg, const int32_t* slot, float* h, int ldh,
                              const float* gain, __nv_bfloat16* out, int ldo, cudaStream_t s);
 // K|V of the empty-history pad key rows when the lifelong fc2 is folded into the
 // QFormer K|V weights (engine build_kv_fold): kv = pad . Wkv [2 nkv] (K then V).
@@ -105,7 +106,9 @@ void launch_moe_plan(int E, const int32_t* counts, int32_t* seg_cursor, int32_t*
 template <class T>
 void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
                         int32_t* seg_cursor, int32_t* slot, T* xg, float* row_scale, cudaStream_t s);
-void launch_moe_combine(int rows, int k, int d, const float* yg, const int32_t* slot, float* h, int ldh,
+// yg: fp32 (fp32 engine) or bf16 (bf16 engine) weighted expert outputs
+template <class YT>
+void launch_moe_combine(int rows, int k, int d, const YT* yg, const int32_t* slot, float* h, int ldh,
                         cudaStream_t s);
 
 // ---- expert-parallel exchange over NVLink peer memory (graph-capturable) ----
@@ -118,7 +121,7 @@ struct EpPeers {
   void* xr[kEpMaxWorld];       // [recv_cap][d] T: expert-grouped received rows (256-row padded segments)
   float* wr[kEpMaxWorld];      // [recv_cap] gate weight of each received row
   int32_t* src[kEpMaxWorld];   // [recv_cap] (source rank << 24) | source (token, slot) index
-  float* yr[kEpMaxWorld];      // [send_cap][d] weighted expert outputs returned to the token's rank
+  void* yr[kEpMaxWorld];       // [send_cap][d] T: weighted expert outputs returned to the token's rank
   int32_t* cnt[kEpMaxWorld];   // [W][E] routing histograms of every rank
   uint32_t* flag[kEpMaxWorld];  // [3 phases][W sources] arrival counters
   uint32_t* epoch = nullptr;   // local [3] exchanges completed per phase
@@ -135,14 +138,18 @@ void launch_ep_signal(const EpPeers& P, int phase, cudaStream_t s);
 // From the local copy of every rank's histogram: cursor[e] = where this rank's
 // rows for global expert e start in the owner's grouped buffer; this rank's
 // grouped-GEMM tile table, n_mtiles and segment (start, count) per local expert.
+// owner / slot [E], list [W][C]: the MoE layer's placement tables (ep_plan.hpp);
+// load [E] (optional) accumulates the layer's global rows per expert
 void launch_ep_plan(int E, const EpPeers& P, int tile, int max_tiles, int32_t* cursor, int32_t* tile_expert,
-                    int32_t* n_mtiles, int32_t* seg, cudaStream_t s);
+                    int32_t* n_mtiles, int32_t* seg, const int32_t* owner, const int32_t* slot, const int32_t* list,
+                    int C, long long* load, cudaStream_t s);
 // (token, slot) rows -> the experts' ranks' grouped buffers (+ gate weight, source id); slot[i] = i
 template <class T>
 void launch_ep_dispatch(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
-                        int32_t* cursor, int32_t* slot, int El, const EpPeers& P, cudaStream_t s);
+                        int32_t* cursor, int32_t* slot, const int32_t* owner, const EpPeers& P, cudaStream_t s);
 // this rank's received rows' outputs (yg, grouped order) -> the tokens' ranks' yr[slot]
-void launch_ep_return(int El, int d, const int32_t* seg, const float* yg, const EpPeers& P, cudaStream_t s);
+template <class T>
+void launch_ep_return(int El, int d, const int32_t* seg, const T* yg, const EpPeers& P, cudaStream_t s);
 void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, cudaStream_t s);
 
 }  // namespace orx

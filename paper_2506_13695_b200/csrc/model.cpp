@@ -375,7 +375,7 @@ const Tensor& HostWeights::get(const std::string& name) const {
 // (cos, sin) values in that order, so normal #j is fixed by draws 2*(j/2)
 // and 2*(j/2)+1; a sequential pass records the generator state every chunk
 // and worker threads fill chunks in parallel.
-HostWeights HostWeights::random(const orx_config& cfg, int ep_rank, int ep_world) {
+HostWeights HostWeights::random(const orx_config& cfg, int ep_rank, int ep_world, const int32_t* owner) {
   HostWeights w;
   w.cfg = cfg;
   auto specs = param_specs(cfg);
@@ -386,8 +386,12 @@ HostWeights HostWeights::random(const orx_config& cfg, int ep_rank, int ep_world
     const size_t at = name.find(".expert");
     if (at == std::string::npos) return true;
     const int e = std::atoi(name.c_str() + at + 7);
-    const int per = cfg.n_experts / ep_world;
-    return e / per == ep_rank;
+    if (!owner) return e / (cfg.n_experts / ep_world) == ep_rank;
+    // "enc<l>.moe..." / "dec<l>.moe...": MoE layer index in engine order (moe_layers)
+    const int l = std::atoi(name.c_str() + 3);
+    const int li = name.compare(0, 3, "enc") == 0 ? l : (enc_moe(cfg) ? enc_layers(cfg) : 0) + l;
+    const int32_t o = owner[static_cast<size_t>(li) * cfg.n_experts + e];
+    return o < 0 || o == ep_rank;
   };
   if (ep_world > 1) {
     require(cfg.moe_enabled && cfg.n_experts % ep_world == 0, "experts must divide evenly over the ranks");

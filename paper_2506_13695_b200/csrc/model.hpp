@@ -41,6 +41,10 @@ inline int feat_dim(const orx_config& c) {
   return c.vid_only_features ? c.d_model : c.d_model + aid_dim(c) + 5 * minor_dim(c);
 }
 inline bool enc_moe(const orx_config& c) { return c.moe_enabled && c.moe_location == 1; }
+// MoE layers in engine order: encoder layers (when they are MoE), then decoder layers
+inline int moe_layers(const orx_config& c) {
+  return c.moe_enabled ? (enc_moe(c) ? enc_layers(c) : 0) + dec_layers(c) : 0;
+}
 void validate_config(const orx_config& c);
 std::string config_to_json(const orx_config& c);
 orx_config config_from_json(const std::string& s);
@@ -83,8 +87,11 @@ class HostWeights {
   std::unordered_map<std::string, int> index;
   const Tensor& get(const std::string& name) const;
   const float* ptr(const std::string& name) const { return get(name).data.data(); }
-  // ep_world > 1: only experts of rank ep_rank are materialised (partial = true)
-  static HostWeights random(const orx_config& cfg, int ep_rank = 0, int ep_world = 1);
+  // ep_world > 1: only the experts rank ep_rank computes are materialised
+  // (partial = true): contiguous blocks, or per `owner` [moe_layers][E]
+  // (rank or -1 = replicated; ep_plan.hpp) when given
+  static HostWeights random(const orx_config& cfg, int ep_rank = 0, int ep_world = 1,
+                            const int32_t* owner = nullptr);
   bool partial = false;
   static HostWeights load_grcp(const std::string& path);
   void save_grcp(const std::string& path) const;

@@ -300,10 +300,17 @@ class Weights:
         return Weights(h)
 
     @staticmethod
-    def random_ep(cfg: PolicyConfig, ep_rank: int, ep_world: int) -> "Weights":
-        """The same seeded weights, materialising only this expert-parallel rank's experts."""
+    def random_ep(cfg: PolicyConfig, ep_rank: int, ep_world: int, owner=None) -> "Weights":
+        """The same seeded weights, materialising only the experts this
+        expert-parallel rank computes (contiguous blocks, or per the placement
+        `owner` [moe_layers, n_experts]: rank, or -1 = replicated)."""
         h = C.c_void_p()
-        check(lib().orx_weights_create_random_ep(C.byref(cfg.to_c()), ep_rank, ep_world, C.byref(h)))
+        if owner is None:
+            check(lib().orx_weights_create_random_ep(C.byref(cfg.to_c()), ep_rank, ep_world, C.byref(h)))
+        else:
+            own = _placement(cfg, owner)
+            check(lib().orx_weights_create_random_ep_placed(C.byref(cfg.to_c()), ep_rank, ep_world,
+                                                            own.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(h)))
         return Weights(h)
 
     @staticmethod
@@ -334,6 +341,8 @@ class Weights:
         dims = (C.c_int32 * 2)()
         data = C.POINTER(C.c_float)()
         check(lib().orx_weights_entry(self._h, idx.value, None, None, dims, C.byref(data)))
+        if not data:  # an expert another expert-parallel rank computes (not materialised here)
+            return np.zeros((0, 0), dtype=np.float32)
         n = dims[0] * dims[1]
         return np.ctypeslib.as_array(data, shape=(n,)).reshape(dims[0], dims[1]).copy()
 
@@ -348,14 +357,42 @@ class Weights:
             self._h = None
 
 
+def moe_layers(cfg: PolicyConfig) -> int:
+    """MoE layers in engine order (encoder layers when they are MoE, then decoder layers)."""
+    return int(lib().orx_config_moe_layers(C.byref(cfg.to_c())))
+
+
+def _placement(cfg: PolicyConfig, owner) -> np.ndarray:
+    own = np.ascontiguousarray(np.asarray(owner, dtype=np.int32))
+    if own.shape != (moe_layers(cfg), cfg.n_experts):
+        raise ValueError(f"expert placement must be [moe_layers={moe_layers(cfg)}, n_experts={cfg.n_experts}]")
+    return own
+
+
+def ep_place(load, world: int, max_replicas: int):
+    """Load-balanced expert placement (csrc/ep_plan.hpp ep_place_balanced)
+    from per-layer expert loads [moe_layers, n_experts] (PolicyModel.expert_load):
+    returns (owner [moe_layers, n_experts] int32, predicted busiest/mean rank load per layer)."""
+    ld = np.ascontiguousarray(np.asarray(load, dtype=np.int64))
+    if ld.ndim != 2:
+        raise ValueError("load must be [moe_layers, n_experts]")
+    owner = np.empty(ld.shape, dtype=np.int32)
+    pred = np.empty(ld.shape[0], dtype=np.float64)
+    check(lib().orx_ep_place(ld.ctypes.data_as(C.POINTER(C.c_int64)), ld.shape[0], ld.shape[1], world, max_replicas,
+                             owner.ctypes.data_as(C.POINTER(C.c_int32)), pred.ctypes.data_as(C.POINTER(C.c_double))))
+    return owner, pred
+
+
 class PolicyModel:
     """Encoder + MoE decoder on one B200 (the engine owns device weights)."""
 
     def __init__(self, cfg: Optional[PolicyConfig] = None, *, weights: Optional[Weights] = None,
                  precision: str = "fp32", device: int = 0, max_users: int = 16, max_width: int = 128,
-                 ep: Optional[tuple] = None):
+                 ep: Optional[tuple] = None, ep_owner=None):
         """ep = (rank, world, unique_id bytes): expert-parallel engine holding
-        n_experts / world experts per MoE layer (see dist.ep_unique_id)."""
+        n_experts / world experts per MoE layer (see dist.ep_unique_id), or the
+        experts the placement ep_owner [moe_layers, n_experts] gives this rank
+        (rank, or -1 = replicated; the same table on every rank; see ep_place)."""
         if weights is None:
             if cfg is None:
                 raise ValueError("PolicyModel needs a config or weights")
@@ -372,8 +409,19 @@ class PolicyModel:
         else:
             rank, world, uid = ep
             buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
-            check(lib().orx_engine_create_ep(weights._h, device, PRECISION[precision], max_users, max_width, buf,
-                                             rank, world, C.byref(self._e)))
+            own = None if ep_owner is None else _placement(self.cfg, ep_owner)
+            check(lib().orx_engine_create_ep_placed(
+                weights._h, device, PRECISION[precision], max_users, max_width, buf, rank, world,
+                None if own is None else own.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(self._e)))
+
+    def expert_load(self, reset: bool = False) -> np.ndarray:
+        """Expert-parallel engines: rows routed to each expert of each MoE layer,
+        over every rank and call since creation / the last reset
+        [moe_layers, n_experts] (identical on every rank; zeros otherwise)."""
+        out = np.zeros((moe_layers(self.cfg), self.cfg.n_experts), dtype=np.int64)
+        if out.size:
+            check(lib().orx_engine_expert_load(self._e, out.ctypes.data_as(C.POINTER(C.c_int64)), int(reset)))
+        return out
 
     @staticmethod
     def load(path: str, **kw) -> "PolicyModel":

@@ -1,9 +1,11 @@
 """Worker for tests/test_ep_gpu.py (one process per GPU, launched by torchrun).
 
 Each rank owns its own users; an expert-parallel engine (n_experts / world
-experts per MoE layer, NCCL all-to-all dispatch/combine) must reproduce a
+experts per MoE layer, peer-memory dispatch / return) must reproduce a
 replica engine (all experts) bitwise: encoder output, teacher-forced logits
-and beams. Exits non-zero on any mismatch.
+and beams -- with contiguous expert blocks and with a load-balanced placement
+(replicated hot experts, permuted owners) made from the first engine's
+measured expert loads. Exits non-zero on any mismatch.
 """
 import os
 import sys
@@ -30,26 +32,45 @@ def main():
                                     moe_location="enc_and_dec")
         w = P.Weights.random(cfg)
         rep = P.PolicyModel(weights=w, precision=precision, device=local, max_users=users, max_width=width)
-        uid = ep_unique_id(device=torch.device("cuda", local))  # one id per communicator
-        w_ep = P.Weights.random_ep(cfg, rank, world)  # only this rank's experts materialised
-        ep = P.PolicyModel(weights=w_ep, precision=precision, device=local, max_users=users, max_width=width,
-                           ep=(rank, world, uid))
         # different users per rank (and a different ragged shape on odd ranks)
         lens = (20, 64, 300) if rank % 2 == 0 else (7, 31, 129)
         batch = P.SynthBatch(1, rank * users, users, *lens)
-        z_rep, z_ep = rep.encode_batch(batch), ep.encode_batch(batch)
         pres = [[], [5], [5, 77], [1000]]
         who = [0, 1, 2, 2]
+        z_rep = rep.encode_batch(batch)
         l_rep = rep.score_prefixes(batch, who, pres)
-        l_ep = ep.score_prefixes(batch, who, pres)
         c_rep, p_rep, _ = rep.beam_search_arrays(batch, width)
-        c_ep, p_ep, _ = ep.beam_search_arrays(batch, width)
-        checks = {"z": np.array_equal(z_rep, z_ep), "logits": np.array_equal(l_rep, l_ep),
-                  "beam codes": np.array_equal(c_rep, c_ep), "beam logp": np.array_equal(p_rep, p_ep)}
-        print(f"rank {rank} {precision}: " + ", ".join(f"{k} {'==' if v else '!='}" for k, v in checks.items()),
-              flush=True)
-        ok = ok and all(checks.values())
-        del ep, rep
+        # contiguous expert blocks, then a load-balanced placement from the first
+        # engine's measured loads (replicated hot experts, permuted owners)
+        owner = None
+        for placement in ("contiguous", "balanced"):
+            uid = ep_unique_id(device=torch.device("cuda", local))  # one id per communicator
+            w_ep = P.Weights.random_ep(cfg, rank, world, owner=owner)  # only the experts this rank computes
+            ep = P.PolicyModel(weights=w_ep, precision=precision, device=local, max_users=users, max_width=width,
+                               ep=(rank, world, uid), ep_owner=owner)
+            z_ep = ep.encode_batch(batch)
+            l_ep = ep.score_prefixes(batch, who, pres)
+            c_ep, p_ep, _ = ep.beam_search_arrays(batch, width)
+            checks = {"z": np.array_equal(z_rep, z_ep), "logits": np.array_equal(l_rep, l_ep),
+                      "beam codes": np.array_equal(c_rep, c_ep), "beam logp": np.array_equal(p_rep, p_ep)}
+            if placement == "contiguous":
+                load = ep.expert_load()
+                lt = torch.from_numpy(load).to(torch.device("cuda", local))
+                every = [torch.zeros_like(lt) for _ in range(world)]
+                dist.all_gather(every, lt)  # the loads come from all-gathered histograms: equal on every rank
+                checks["load"] = bool(load.sum() > 0 and all(torch.equal(t, lt) for t in every))
+                owner, pred = P.ep_place(load, world, 4)
+                # force at least one replicated expert per layer so the test covers that path
+                for li in range(owner.shape[0]):
+                    if (owner[li] < 0).sum() == 0:
+                        owner[li, int(np.argmax(load[li]))] = -1
+            else:
+                checks["replicated"] = bool((owner < 0).any())
+            print(f"rank {rank} {precision} {placement}: "
+                  + ", ".join(f"{k} {'==' if v else '!='}" for k, v in checks.items()), flush=True)
+            ok = ok and all(checks.values())
+            del ep
+        del rep
     flag = torch.tensor([1 if ok else 0], device=torch.device("cuda", local))
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     dist.destroy_process_group()

@@ -318,7 +318,7 @@ def main():
     ap.add_argument("--ep-replicas", type=int, default=None,
                     help="load-balanced expert placement: at most this many replicated experts per MoE layer, "
                          "from the expert loads of one calibration request on other users "
-                         "(default n_experts / N / 2; -1 = contiguous expert blocks, no calibration)")
+                         "(default n_experts / N; -1 = contiguous expert blocks, no calibration)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     lens = tuple(int(x) for x in args.lens.split(","))
@@ -354,7 +354,7 @@ def main():
                                  device=local, max_users=args.users, max_width=args.width, ep=(rank, world, uid),
                                  ep_owner=owner)
         model = ep_model(None)
-        reps = args.ep_replicas if args.ep_replicas is not None else pcfg.n_experts // world // 2
+        reps = args.ep_replicas if args.ep_replicas is not None else pcfg.n_experts // world
         if reps >= 0:
             # expert placement from one calibration request on OTHER users (the loads
             # are all-gathered, so every rank computes the same placement)

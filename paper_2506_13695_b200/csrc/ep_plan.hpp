@@ -87,9 +87,10 @@ struct EpPlacement {
 // Per layer, for r = 0 .. max_replicas: the r heaviest experts are replicated
 // (their load splits evenly over the ranks, as the token batches do) and the
 // rest are packed onto the ranks heaviest-first, each to the least-loaded rank
-// with a free slot (at most ceil((E - r) / W) owned experts per rank); the
-// first r whose heaviest rank is within `tolerance` of the mean wins, else the
-// best r. Deterministic: every rank computes the same placement from the same
+// with a free slot (at most ceil((E - r) / W) + 1 owned experts per rank),
+// then refined by moves / swaps that lower the busiest rank's load; the first
+// r whose busiest rank is within `tolerance` of the mean wins, else the best
+// r. Deterministic: every rank computes the same placement from the same
 // (all-gathered) loads.
 inline EpPlacement ep_place_balanced(const int64_t* load, int layers, int E, int W, int max_replicas,
                                      double tolerance = 1.05, std::vector<double>* predicted = nullptr) {
@@ -116,7 +117,7 @@ inline EpPlacement ep_place_balanced(const int64_t* load, int layers, int E, int
       double repl = 0;
       for (int i = 0; i < r; ++i) repl += static_cast<double>(l[order[i]]);
       for (int q = 0; q < W; ++q) rank_load[q] = repl / W;
-      const int cap = (E - r + W - 1) / W;
+      const int cap = (E - r + W - 1) / W + 1;
       for (int i = r; i < E; ++i) {
         int pick = -1;
         for (int q = 0; q < W; ++q)
@@ -124,6 +125,41 @@ inline EpPlacement ep_place_balanced(const int64_t* load, int layers, int E, int
         own[order[i]] = pick;
         rank_load[pick] += static_cast<double>(l[order[i]]);
         ++n_owned[pick];
+      }
+      // refinement: move one expert off the busiest rank, or swap it for a
+      // lighter one, whichever lowers the pair's maximum the most
+      for (int it = 0; it < 4 * E; ++it) {
+        const int b = static_cast<int>(std::max_element(rank_load.begin(), rank_load.end()) - rank_load.begin());
+        double best_max = rank_load[b];
+        int bx = -1, bq = -1, by = -1;
+        for (int x = 0; x < E; ++x) {
+          if (own[x] != b) continue;
+          const double lx = static_cast<double>(l[x]);
+          for (int q = 0; q < W; ++q) {
+            if (q == b) continue;
+            if (n_owned[q] < cap) {
+              const double m = std::max(rank_load[b] - lx, rank_load[q] + lx);
+              if (m < best_max - 1e-9) best_max = m, bx = x, bq = q, by = -1;
+            }
+            for (int y = 0; y < E; ++y) {
+              if (own[y] != q || l[y] >= l[x]) continue;
+              const double dl = lx - static_cast<double>(l[y]);
+              const double m = std::max(rank_load[b] - dl, rank_load[q] + dl);
+              if (m < best_max - 1e-9) best_max = m, bx = x, bq = q, by = y;
+            }
+          }
+        }
+        if (bx < 0) break;
+        const double lx = static_cast<double>(l[bx]), ly = by < 0 ? 0.0 : static_cast<double>(l[by]);
+        own[bx] = bq;
+        rank_load[b] -= lx - ly;
+        rank_load[bq] += lx - ly;
+        if (by >= 0) {
+          own[by] = b;
+        } else {
+          --n_owned[b];
+          ++n_owned[bq];
+        }
       }
       const double imb = mean > 0 ? *std::max_element(rank_load.begin(), rank_load.end()) / mean : 1.0;
       if (imb < best_imb - 1e-12) best_imb = imb, best = own;

@@ -277,10 +277,16 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
   int orr[8];  // output rows this lane stores: r = 4 * k + sub
 #pragma unroll
   for (int k = 0; k < 8; ++k) orr[k] = __shfl_sync(0xffffffffu, orow, 4 * k + sub);
-  unsigned long long pb[(MODE & EPI_PEER) ? 8 : 1];
+  // EPI_PEER stores 16 B per lane (4 lanes per row, rows 8k + lane / 4): half
+  // the store instructions of the 8-B layout, 64 B contiguous per row and chunk
+  unsigned long long pb[(MODE & EPI_PEER) ? 4 : 1];
+  int prow[(MODE & EPI_PEER) ? 4 : 1];
   if constexpr ((MODE & EPI_PEER) != 0) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) pb[k] = __shfl_sync(0xffffffffu, pbase, 4 * k + sub);
+    for (int k = 0; k < 4; ++k) {
+      pb[k] = __shfl_sync(0xffffffffu, pbase, 8 * k + (lane >> 2));
+      prow[k] = __shfl_sync(0xffffffffu, orow, 8 * k + (lane >> 2));
+    }
   }
   if (MODE & EPI_RESID) {
     if (orow >= 0)  // this row's residual segment into L2 while the MMAs run
@@ -355,6 +361,19 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
     for (int k = 0; k < 8; ++k)
       s4[lane * 8 + (k ^ (lane & 7))] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
     __syncwarp();
+    if constexpr ((MODE & EPI_PEER) != 0) {  // rows 8k + lane / 4, columns 8 (lane % 4) .. + 8
+      const int c8 = lane & 3, pc = col0 + e.col_off + 8 * c8;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = 8 * k + (lane >> 2);
+        const float4 a = s4[r * 8 + ((2 * c8) ^ (r & 7))], b = s4[r * 8 + ((2 * c8 + 1) ^ (r & 7))];
+        if (prow[k] >= 0)
+          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(pb[k]) + (size_t)prow[k] * e.ldo + pc) =
+              make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y), pack_bf16(b.z, b.w));
+      }
+      __syncwarp();
+      return;
+    }
     const int oc = col0 + e.col_off + 4 * q;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -365,10 +384,7 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
         const float4 y = cur[k];
         x.x += y.x, x.y += y.y, x.z += y.z, x.w += y.w;
       }
-      if constexpr ((MODE & EPI_PEER) != 0) {
-        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(pb[k]) + (size_t)orr[k] * e.ldo + oc) =
-            make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
-      } else if (MODE & EPI_BF16) {
+      if (MODE & EPI_BF16) {
         *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)orr[k] * e.ldo + oc) =
             make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
       } else {

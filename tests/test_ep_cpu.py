@@ -208,7 +208,7 @@ def test_ep_place_balances_and_replicates_hot_experts():
         assert ((own >= -1) & (own < world)).all()
         n_rep = int((own < 0).sum())
         assert n_rep <= 4
-        cap = (E24 - n_rep + world - 1) // world
+        cap = (E24 - n_rep + world - 1) // world + 1
         assert all((own == p).sum() <= cap for p in range(world))
         r = _rank_loads(load[li], own, world)
         assert abs(r.max() / r.mean() - pred[li]) < 1e-9

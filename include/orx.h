@@ -298,6 +298,14 @@ typedef struct orx_attn_args {
   int32_t kernel;
 } orx_attn_args;
 int orx_debug_attention(const orx_attn_args* args, void* stream);
+/* MoE gate routing through one router kernel, for the GPU tests (host
+ * buffers): x [rows * d] (the fp32 residual rows), gate [n_experts * d] (the
+ * pre-MoE RMSNorm gain folded in), bias [n_experts]; variant 0 = SIMT
+ * moe_route2, 1 = SIMT moe_route4 (swizzled gate), 2 = 3xTF32 tensor-pipe
+ * moe_route_tc. Outputs sel / wts [rows * k]: selected experts ascending and
+ * their softmax weights (moe_forward, nn.cpp:117-147). */
+int orx_debug_moe_route(int32_t rows, int32_t d, int32_t n_experts, int32_t k, const float* x, const float* gate,
+                        const float* bias, int32_t variant, int32_t* sel_out, float* wts_out);
 /* Rows of the beam-pruning fast path that took its exact radix-select
  * fallback since the last call (process-wide counter, reset on read). */
 int64_t orx_debug_topk_fallback_rows(void);

@@ -143,6 +143,8 @@ SIGNATURES = [
     ("orx_debug_gemm", C.c_int, [C.POINTER(orx_gemm_args), _P]),
     ("orx_debug_row_topk", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
     ("orx_debug_topk_fallback_rows", C.c_int64, []),
+    ("orx_debug_moe_route", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, _F32P, _F32P, _F32P, C.c_int32,
+                                      _I32P, _F32P]),
     ("orx_debug_attention", C.c_int, [C.POINTER(orx_attn_args), _P]),
     ("orx_debug_ep_plan", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _I32P, _I32P, C.c_int32, C.c_int32,
                                     C.c_int32, _I32P, _I32P, _I32P, _I32P, C.POINTER(C.c_int64)]),

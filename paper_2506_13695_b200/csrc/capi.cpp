@@ -12,6 +12,7 @@
 #include "ep_plan.hpp"
 #include "attention.cuh"
 #include "beam.cuh"
+#include "kernels.cuh"
 #include "compress.cuh"
 #include "gemm.cuh"
 #include "model.hpp"
@@ -540,6 +541,20 @@ int orx_debug_attention(const orx_attn_args* a, void* stream) {
     }
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) throw orx::RuntimeError(std::string("CUDA: ") + cudaGetErrorString(err));
+  });
+}
+
+int orx_debug_moe_route(int32_t rows, int32_t d, int32_t n_experts, int32_t k, const float* x, const float* gate,
+                        const float* bias, int32_t variant, int32_t* sel_out, float* wts_out) {
+  return guarded([&] {
+    need(x, "x");
+    need(gate, "gate");
+    need(bias, "bias");
+    need(sel_out, "sel_out");
+    need(wts_out, "wts_out");
+    if (rows < 0 || d <= 0 || n_experts < 1 || n_experts > 32 || k < 1 || k > n_experts || k > 8)
+      throw orx::InvalidArgument("debug_moe_route: bad shape");
+    orx::debug_moe_route(rows, d, n_experts, k, x, gate, bias, variant, sel_out, wts_out);
   });
 }
 

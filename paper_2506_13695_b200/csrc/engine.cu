@@ -460,25 +460,15 @@ class EngineT final : public Engine {
     for (int e = 0; e < E; ++e)
       for (int k = 0; k < d; ++k) gt[(size_t)e * d + k] *= gain.data[k];
     m.gate_gain = upload_f32(gt.data(), gt.size());
-    if (E <= 24 && d % 128 == 0) {  // moe_route4 layout: 4-column groups x 24 swizzled (4 experts x 1 column) units
-      std::vector<float> sw(static_cast<size_t>(d) * 24, 0.f);
-      for (int e = 0; e < E; ++e)
-        for (int c = 0; c < d; ++c) {
-          const int q = c >> 2, unit = ((c & 3) * 6 + (e >> 2)) ^ (q & 7);
-          sw[(size_t)q * 96 + unit * 4 + (e & 3)] = gt[(size_t)e * d + c];
-        }
+    if (E <= 24 && d % 128 == 0) {  // moe_route4's swizzled shared-memory layout
+      std::vector<float> sw(static_cast<size_t>(d) * 24);
+      gate_route4_layout(gt.data(), E, d, sw.data());
       m.gate_sw = upload_f32(sw.data(), sw.size());
     }
     if (kBf16 && moe_route_tc_supported(d, E, cfg_.experts_active, d) && !getenv("ORX_ROUTE_SIMT")) {
       // 3xTF32 gate for the tensor-pipe router: tf32-exact hi part and the fp32 residual, 32 expert rows
-      std::vector<float> hi(static_cast<size_t>(32) * d, 0.f), lo(static_cast<size_t>(32) * d, 0.f);
-      for (size_t i = 0; i < gt.size(); ++i) {
-        uint32_t b;
-        memcpy(&b, &gt[i], 4);
-        b &= 0xFFFFE000u;
-        memcpy(&hi[i], &b, 4);
-        lo[i] = gt[i] - hi[i];
-      }
+      std::vector<float> hi(static_cast<size_t>(32) * d), lo(static_cast<size_t>(32) * d);
+      gate_tf32_split(gt.data(), E, d, hi.data(), lo.data());
       m.gate_hi = upload_f32(hi.data(), hi.size());
       m.gate_lo = upload_f32(lo.data(), lo.size());
     }

@@ -98,6 +98,17 @@ void launch_fill_kv_pad(int n_pad, const int32_t* rows, const int32_t* row_user,
 // gate_hi / gate_lo [32][d] = the gain-folded gate split into tf32 hi and
 // residual lo (expert rows >= E zero). Same outputs as launch_moe_route.
 bool moe_route_tc_supported(int d, int E, int k, int ldx);
+// host-side gate layouts (pack_moe and orx_debug_moe_route): gate [E][d] ->
+// moe_route4's swizzled [d / 4][96] (E <= 24, d % 128 == 0), and the tf32
+// hi / residual lo split padded to 32 expert rows [32][d]
+void gate_route4_layout(const float* gate, int E, int d, float* sw);
+void gate_tf32_split(const float* gate, int E, int d, float* hi, float* lo);
+// Debug / test entry (orx_debug_moe_route): host x [rows][d], gate [E][d]
+// (gain folded), bias [E] -> host sel / wts [rows][k] through one router:
+// variant 0 = moe_route2 (SIMT), 1 = moe_route4 (SIMT, swizzled gate),
+// 2 = moe_route_tc (3xTF32 tensor pipe).
+void debug_moe_route(int rows, int d, int E, int k, const float* x, const float* gate, const float* bias,
+                     int variant, int32_t* sel, float* wts);
 void launch_moe_route_tc(int rows, int d, int E, int k, const float* x, int ldx, const float* gate_hi,
                          const float* gate_lo, const float* bias, int32_t* sel, float* wts, int32_t* counts,
                          cudaStream_t s);

@@ -5,9 +5,11 @@
 //   x.w ~= x_hi.w_hi + x_lo.w_hi + x_hi.w_lo     (dropped term ~2^-21 relative)
 // One CTA per SM walks 128-row tiles of h (fp32, the residual stream):
 //   warp 0    TMA: h tile (128 rows x 32 fp32, 128-byte swizzled rows) and the
-//             pre-split gate (32 expert rows x 32) per K block, 4-stage ring
+//             pre-split gate (32 expert rows x 32) per K block, 7-stage ring
+//             (the kernel is bound by HBM latency: 112 KB of h in flight per SM)
 //   warps 2-5 thread = row: split the staged fp32 row into tf32 hi (in place)
-//             and lo (second buffer), accumulate the row's sum of squares; at
+//             and lo (a 2-deep ring of its own, so a stage is 24 KB and the
+//             ring deep), accumulate the row's sum of squares; at
 //             the end of the tile read the row's 32 scores from TMEM, scale by
 //             rsqrt(mean(x^2) + eps), stable top-k by score + bias (ties ->
 //             lower id, nn.cpp:127-136), softmax over the selected raw scores
@@ -18,8 +20,10 @@
 // ~30 instructions per 32 columns, so the kernel runs at the HBM rate instead
 // of the shared-memory bound of a SIMT 24-expert dot product.
 #include <cfloat>
+#include <cstring>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -32,11 +36,12 @@ namespace {
 constexpr int kRtBM = 128;      // rows per tile
 constexpr int kRtBK = 32;       // fp32 columns per K block (128-byte rows)
 constexpr int kRtN = 32;        // expert slots (E <= 32)
-constexpr int kRtStages = 4;
+constexpr int kRtStages = 7;
+constexpr int kRtLo = 2;                      // lo ring depth
 constexpr uint32_t kRtA = kRtBM * kRtBK * 4;  // 16 KB
 constexpr uint32_t kRtB = kRtN * kRtBK * 4;   // 4 KB
-constexpr uint32_t kRtStage = 2 * kRtA + 2 * kRtB;  // A hi (in place) + A lo + B hi + B lo
-constexpr size_t kRtSmem = kRtStages * kRtStage + 1024 + 512;
+constexpr uint32_t kRtStage = kRtA + 2 * kRtB;  // A (hi in place) + B hi + B lo
+constexpr size_t kRtSmem = kRtStages * kRtStage + kRtLo * kRtA + 1024 + 512;
 
 // kind::tf32 instruction descriptor: fp32 accumulate, A/B tf32, both K-major
 constexpr uint32_t idesc_tf32(int m, int n) {
@@ -62,10 +67,12 @@ __global__ void __launch_bounds__(192, 1)
                         int32_t* __restrict__ counts) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRtStages * kRtStage);
+  uint8_t* lo_ring = smem + kRtStages * kRtStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(lo_ring + kRtLo * kRtA);
   uint64_t* conv = full + kRtStages;
   uint64_t* empty = conv + kRtStages;
-  uint64_t* acc_full = empty + kRtStages;   // [2]
+  uint64_t* lo_empty = empty + kRtStages;   // [kRtLo]
+  uint64_t* acc_full = lo_empty + kRtLo;    // [2]
   uint64_t* acc_empty = acc_full + 2;       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   int* hist = reinterpret_cast<int*>(tmem_slot + 4);  // [32]
@@ -80,6 +87,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 4);
     }
+    for (int a = 0; a < kRtLo; ++a) mbar_init(&lo_empty[a], 1);
     fence_mbar_init();
     tma_prefetch(&tmX);
     tma_prefetch(&tmBh);
@@ -106,8 +114,8 @@ __global__ void __launch_bounds__(192, 1)
           uint8_t* st = smem + stage * kRtStage;
           mbar_arrive_expect_tx(&full[stage], kRtA + 2 * kRtB);
           tma_load_2d(st, &tmX, &full[stage], kb * kRtBK, t * kRtBM, pol_x);
-          tma_load_2d(st + 2 * kRtA, &tmBh, &full[stage], kb * kRtBK, 0, pol_b);
-          tma_load_2d(st + 2 * kRtA + kRtB, &tmBl, &full[stage], kb * kRtBK, 0, pol_b);
+          tma_load_2d(st + kRtA, &tmBh, &full[stage], kb * kRtBK, 0, pol_b);
+          tma_load_2d(st + kRtA + kRtB, &tmBl, &full[stage], kb * kRtBK, 0, pol_b);
           if (++stage == kRtStages) stage = 0, phase ^= 1;
         }
       }
@@ -119,6 +127,7 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      int lslot = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -127,8 +136,8 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(&full[stage], phase);
           mbar_wait(&conv[stage], phase);
           tc_fence_after();
-          const uint32_t ah = smem_u32(smem + stage * kRtStage), al = ah + kRtA;
-          const uint32_t bh = ah + 2 * kRtA, bl = bh + kRtB;
+          const uint32_t ah = smem_u32(smem + stage * kRtStage), al = smem_u32(lo_ring + lslot * kRtA);
+          const uint32_t bh = ah + kRtA, bl = bh + kRtB;
 #pragma unroll
           for (int ks = 0; ks < kRtBK / 8; ++ks) {  // K = 8 tf32 = 32 bytes per step
             const uint32_t o = ks * 32;
@@ -138,7 +147,9 @@ __global__ void __launch_bounds__(192, 1)
             tc_mma_tf32(dt, umma_desc_sw128(ah + o), umma_desc_sw128(bl + o), idesc, 1);
           }
           tc_commit(&empty[stage]);
+          tc_commit(&lo_empty[lslot]);
           if (++stage == kRtStages) stage = 0, phase ^= 1;
+          if (++lslot == kRtLo) lslot = 0;
         }
         tc_commit(&acc_full[acc]);
         acc ^= 1;
@@ -153,13 +164,16 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int lslot = 0;
+    uint32_t lphase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       float ss = 0.f;
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait(&full[stage], phase);
+        mbar_wait(&lo_empty[lslot], lphase ^ 1);  // the MMAs of the lo buffer's previous use are done
         uint8_t* st = smem + stage * kRtStage;
         float4* hi = reinterpret_cast<float4*>(st + r * 128);
-        float4* lo = reinterpret_cast<float4*>(st + kRtA + r * 128);
+        float4* lo = reinterpret_cast<float4*>(lo_ring + lslot * kRtA + r * 128);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {  // the row's 8 16-byte units, elementwise: visit them XOR-rotated
           const int u = j ^ (r & 7);   // so the 8 lanes of a phase hit 8 different bank groups
@@ -178,6 +192,7 @@ __global__ void __launch_bounds__(192, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[stage]);
         if (++stage == kRtStages) stage = 0, phase ^= 1;
+        if (++lslot == kRtLo) lslot = 0, lphase ^= 1;
       }
       // epilogue: this row's expert scores
       mbar_wait(&acc_full[acc], acc_phase);
@@ -300,8 +315,76 @@ void launch_moe_route_tc(int rows, int d, int E, int k, const float* x, int ldx,
   const int tiles = (rows + kRtBM - 1) / kRtBM;
   const int grid = std::min(tiles, num_sms());
   ProfScope ps(PROF_MOE_ROUTE, s, 2.0 * 3 * rows * d * kRtN, double(rows) * (4.0 * d + 8.0 * k));
+  prof_note("moe_route_tc_kernel");
   launch_pdl(moe_route_tc_kernel, grid, 192, kRtSmem, s, mx, mh, ml, rows, d, E, k, bias, sel, wts, counts);
   ++launch_counter();
+}
+
+void gate_route4_layout(const float* gate, int E, int d, float* sw) {
+  for (size_t i = 0; i < static_cast<size_t>(d) * 24; ++i) sw[i] = 0.f;
+  for (int e = 0; e < E; ++e)
+    for (int c = 0; c < d; ++c) {  // 4-column groups x 24 swizzled (4 experts x 1 column) units
+      const int q = c >> 2, unit = ((c & 3) * 6 + (e >> 2)) ^ (q & 7);
+      sw[(size_t)q * 96 + unit * 4 + (e & 3)] = gate[(size_t)e * d + c];
+    }
+}
+
+void gate_tf32_split(const float* gate, int E, int d, float* hi, float* lo) {
+  for (size_t i = 0; i < static_cast<size_t>(kRtN) * d; ++i) hi[i] = lo[i] = 0.f;
+  for (size_t i = 0; i < static_cast<size_t>(E) * d; ++i) {
+    uint32_t b;
+    memcpy(&b, &gate[i], 4);
+    b &= 0xFFFFE000u;  // tf32-exact part
+    memcpy(&hi[i], &b, 4);
+    lo[i] = gate[i] - hi[i];
+  }
+}
+
+void debug_moe_route(int rows, int d, int E, int k, const float* x, const float* gate, const float* bias,
+                     int variant, int32_t* sel, float* wts) {
+  if (rows <= 0) return;
+  if (variant < 0 || variant > 2) throw std::invalid_argument("debug_moe_route: variant 0, 1 or 2");
+  if (variant == 1 && !(E <= 24 && d % 128 == 0)) throw std::invalid_argument("moe_route4 needs E <= 24, d % 128 == 0");
+  if (variant == 2 && !moe_route_tc_supported(d, E, k, d)) throw std::invalid_argument("moe_route_tc: unsupported shape");
+  std::vector<float> g2(static_cast<size_t>(kRtN) * d * 2);
+  const size_t nx = static_cast<size_t>(rows) * d, ng = static_cast<size_t>(E) * d;
+  float *dx, *dg, *dh, *dl, *dsw, *db, *dw;
+  int32_t *ds, *dc;
+  auto chk = [](cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("debug_moe_route: ") + cudaGetErrorString(e));
+  };
+  chk(cudaMalloc(&dx, nx * 4));
+  chk(cudaMalloc(&dg, ng * 4));
+  chk(cudaMalloc(&dh, g2.size() * 4));
+  dl = dh + static_cast<size_t>(kRtN) * d;
+  chk(cudaMalloc(&dsw, static_cast<size_t>(d) * 24 * 4));
+  chk(cudaMalloc(&db, E * 4));
+  chk(cudaMalloc(&ds, static_cast<size_t>(rows) * k * 4));
+  chk(cudaMalloc(&dw, static_cast<size_t>(rows) * k * 4));
+  chk(cudaMalloc(&dc, 32 * 4));
+  chk(cudaMemcpy(dx, x, nx * 4, cudaMemcpyHostToDevice));
+  chk(cudaMemcpy(dg, gate, ng * 4, cudaMemcpyHostToDevice));
+  chk(cudaMemcpy(db, bias, E * 4, cudaMemcpyHostToDevice));
+  chk(cudaMemset(dc, 0, 32 * 4));
+  if (variant == 1) {
+    std::vector<float> sw(static_cast<size_t>(d) * 24);
+    gate_route4_layout(gate, E, d, sw.data());
+    chk(cudaMemcpy(dsw, sw.data(), sw.size() * 4, cudaMemcpyHostToDevice));
+  }
+  if (variant == 2) {
+    gate_tf32_split(gate, E, d, g2.data(), g2.data() + static_cast<size_t>(kRtN) * d);
+    chk(cudaMemcpy(dh, g2.data(), g2.size() * 4, cudaMemcpyHostToDevice));
+    launch_moe_route_tc(rows, d, E, k, dx, d, dh, dl, db, ds, dw, dc, 0);
+  } else {
+    launch_moe_route(rows, d, E, k, dx, d, nullptr, dg, dg, db, ds, dw, dc, 0, variant == 1 ? dsw : nullptr);
+  }
+  chk(cudaGetLastError());
+  chk(cudaDeviceSynchronize());
+  chk(cudaMemcpy(sel, ds, static_cast<size_t>(rows) * k * 4, cudaMemcpyDeviceToHost));
+  chk(cudaMemcpy(wts, dw, static_cast<size_t>(rows) * k * 4, cudaMemcpyDeviceToHost));
+  for (void* p : {static_cast<void*>(dx), static_cast<void*>(dg), static_cast<void*>(dh), static_cast<void*>(dsw),
+                  static_cast<void*>(db), static_cast<void*>(ds), static_cast<void*>(dw), static_cast<void*>(dc)})
+    cudaFree(p);
 }
 
 }  // namespace orx

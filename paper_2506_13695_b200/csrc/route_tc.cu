@@ -15,7 +15,10 @@
 //             lower id, nn.cpp:127-136), softmax over the selected raw scores
 //             (nn.cpp:139-147), ids ascending
 //   warp 1    one thread issues tcgen05.mma kind::tf32 (M=128, N=32, K=8), three
-//             per K step, into one of two TMEM accumulators
+//             per K step, into six TMEM accumulators per tile (term x K-step
+//             parity: a chain of 384 dependent N=32 MMAs into one accumulator
+//             is latency-bound), double-buffered across tiles; the epilogue
+//             sums the six
 // The h tile is read once from HBM (4 d bytes per row); the per-row work is
 // ~30 instructions per 32 columns, so the kernel runs at the HBM rate instead
 // of the shared-memory bound of a SIMT 24-expert dot product.
@@ -36,8 +39,9 @@ namespace {
 constexpr int kRtBM = 128;      // rows per tile
 constexpr int kRtBK = 32;       // fp32 columns per K block (128-byte rows)
 constexpr int kRtN = 32;        // expert slots (E <= 32)
-constexpr int kRtStages = 7;
-constexpr int kRtLo = 2;                      // lo ring depth
+constexpr int kRtStages = 6;
+constexpr int kRtAcc = 6;                     // accumulators per tile (3 terms x 2 K-step parities)
+constexpr int kRtLo = 4;                      // lo ring depth
 constexpr uint32_t kRtA = kRtBM * kRtBK * 4;  // 16 KB
 constexpr uint32_t kRtB = kRtN * kRtBK * 4;   // 4 KB
 constexpr uint32_t kRtStage = kRtA + 2 * kRtB;  // A (hi in place) + B hi + B lo
@@ -94,7 +98,7 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&tmBl);
   }
   if (threadIdx.x < 32) hist[threadIdx.x] = 0;
-  if (warp == 1) tmem_alloc(tmem_slot, 64);
+  if (warp == 1) tmem_alloc(tmem_slot, 512);  // 2 tiles x 6 accumulators x 32 columns
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -113,9 +117,12 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * kRtStage;
           mbar_arrive_expect_tx(&full[stage], kRtA + 2 * kRtB);
-          tma_load_2d(st, &tmX, &full[stage], kb * kRtBK, t * kRtBM, pol_x);
-          tma_load_2d(st + kRtA, &tmBh, &full[stage], kb * kRtBK, 0, pol_b);
-          tma_load_2d(st + kRtA + kRtB, &tmBl, &full[stage], kb * kRtBK, 0, pol_b);
+          // K blocks in a per-CTA rotated order: in lockstep every CTA would read the
+          // same 8 KB of the gate at the same time (one L2 hot spot for 128 readers)
+          const int kr = (kb + blockIdx.x) % kblocks;
+          tma_load_2d(st, &tmX, &full[stage], kr * kRtBK, t * kRtBM, pol_x);
+          tma_load_2d(st + kRtA, &tmBh, &full[stage], kr * kRtBK, 0, pol_b);
+          tma_load_2d(st + kRtA + kRtB, &tmBl, &full[stage], kr * kRtBK, 0, pol_b);
           if (++stage == kRtStages) stage = 0, phase ^= 1;
         }
       }
@@ -131,7 +138,7 @@ __global__ void __launch_bounds__(192, 1)
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t dt = tmem + acc * kRtN;
+        const uint32_t dt = tmem + acc * kRtAcc * kRtN;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
           mbar_wait(&conv[stage], phase);
@@ -141,10 +148,11 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int ks = 0; ks < kRtBK / 8; ++ks) {  // K = 8 tf32 = 32 bytes per step
             const uint32_t o = ks * 32;
-            const uint32_t first = (kb | ks) != 0;
-            tc_mma_tf32(dt, umma_desc_sw128(ah + o), umma_desc_sw128(bh + o), idesc, first);
-            tc_mma_tf32(dt, umma_desc_sw128(al + o), umma_desc_sw128(bh + o), idesc, 1);
-            tc_mma_tf32(dt, umma_desc_sw128(ah + o), umma_desc_sw128(bl + o), idesc, 1);
+            const uint32_t accum = kb > 0 || ks >= 2;  // first use of each accumulator overwrites
+            const uint32_t da = dt + (ks & 1) * kRtN;
+            tc_mma_tf32(da, umma_desc_sw128(ah + o), umma_desc_sw128(bh + o), idesc, accum);
+            tc_mma_tf32(da + 2 * kRtN, umma_desc_sw128(al + o), umma_desc_sw128(bh + o), idesc, accum);
+            tc_mma_tf32(da + 4 * kRtN, umma_desc_sw128(ah + o), umma_desc_sw128(bl + o), idesc, accum);
           }
           tc_commit(&empty[stage]);
           tc_commit(&lo_empty[lslot]);
@@ -198,9 +206,15 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&acc_full[acc], acc_phase);
       __syncwarp();
       tc_fence_after();
-      uint32_t raw[32];
-      tmem_ld32_async(tmem + lane_off + acc * kRtN, raw);
-      tmem_wait_ld();
+      float sum[32];
+#pragma unroll 1
+      for (int a = 0; a < kRtAcc; ++a) {  // hi.hi (even, odd K steps), lo.hi, hi.lo
+        uint32_t raw[32];
+        tmem_ld32_async(tmem + lane_off + (acc * kRtAcc + a) * kRtN, raw);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) sum[e] = a == 0 ? __uint_as_float(raw[e]) : sum[e] + __uint_as_float(raw[e]);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
@@ -211,7 +225,7 @@ __global__ void __launch_bounds__(192, 1)
       const float inv = rsqrtf(ss / d + 1e-6f);
       float sc[32];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) sc[e] = __uint_as_float(raw[e]) * inv;
+      for (int e = 0; e < 32; ++e) sc[e] = sum[e] * inv;
       uint32_t taken = 0;
       int ids[8];
       float rw[8];
@@ -263,7 +277,7 @@ __global__ void __launch_bounds__(192, 1)
   if (threadIdx.x < E && hist[threadIdx.x]) atomicAdd(&counts[threadIdx.x], hist[threadIdx.x]);
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 64);
+    tmem_dealloc(tmem, 512);
   }
 }
 

@@ -610,6 +610,14 @@ class EngineT final : public Engine {
     f.pa = pa;
     f.pl = upload_f32(pl.data(), pl.size());
     f.u = upload_f32(uf.data(), uf.size());
+    // aid x label-combination rows pre-added (<= 64 MB): one L2 gather less per record
+    const size_t pal_rows = static_cast<size_t>(naid) << nf;
+    if (pal_rows * d * 4 <= (size_t(64) << 20) && !getenv("ORX_NO_FOLD_PAL")) {
+      float* pal = ar_.alloc<float>(pal_rows * d);
+      launch_fold_pal(naid, nf, d, pa, f.pl, pal, st_);
+      CUDA_CHECK(cudaGetLastError());
+      f.pal = pal;
+    }
     CUDA_CHECK(cudaStreamSynchronize(st_));
     return f;
   }

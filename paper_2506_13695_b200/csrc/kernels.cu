@@ -231,24 +231,27 @@ __global__ void __launch_bounds__(256, 4) features16_kernel(RecordsDev r, Featur
 // across the rows a warp visits, the Pv / Pa / Pl rows (L2-resident per
 // pathway) are gathered as float4. Replaces features16 + the fc1 GEMM
 // (n x 2.125d x d) per pathway.
-template <int G>
-__global__ void __launch_bounds__(256) fold_features_kernel(RecordsDev r, FoldTables f,
-                                                            __nv_bfloat16* __restrict__ out, int ldo) {
+constexpr int kFoldMaxD4 = 512;  // d <= 2048
+template <int G, bool PAL>
+__global__ void __launch_bounds__(256, 3) fold_features_kernel(RecordsDev r, FoldTables f,
+                                                               __nv_bfloat16* __restrict__ out, int ldo) {
+  // the 4 scalar-section vectors in shared memory, not registers: 3 blocks per
+  // SM instead of 2 (the kernel is bound by the latency of its gathers)
+  __shared__ float4 su[4][kFoldMaxD4];
   pdl_begin();
   constexpr int RPB = 8 / G;  // records in flight per block
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d4 = f.d / 4, cg = warp % G, rl = warp / G;
   const unsigned lmask = (1u << f.n_flags) - 1u;
+  for (int i = threadIdx.x; i < 4 * d4; i += blockDim.x)
+    su[i / d4][i % d4] = __ldg(reinterpret_cast<const float4*>(f.u) + i);
+  __syncthreads();
   int c4[2];
   bool ok[2];
-  float4 u[4][2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     c4[h] = cg * 64 + h * 32 + lane;
     ok[h] = c4[h] < d4;
-#pragma unroll
-    for (int s = 0; s < 4; ++s)
-      u[s][h] = ok[h] ? __ldg(reinterpret_cast<const float4*>(f.u) + s * d4 + c4[h]) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   // Software-pipelined over this warp's records: the record fields of row k+2
   // and the table rows of row k+1 are in flight while row k is finished (the
@@ -273,11 +276,18 @@ __global__ void __launch_bounds__(256) fold_features_kernel(RecordsDev r, FoldTa
   auto gather = [&](int row, const Rec& q, float4 (&a)[2], float4 (&b)[2], float4 (&l)[2]) {
     if (row >= r.n) return;
     const float4* pv = reinterpret_cast<const float4*>(f.pv) + (size_t)q.vid * d4;
-    const float4* pa = reinterpret_cast<const float4*>(f.pa) + (size_t)q.aid * d4;
-    const float4* pl = reinterpret_cast<const float4*>(f.pl) + (size_t)q.lab * d4;
+    if constexpr (PAL) {  // aid and label rows pre-added: two gathers per record
+      const float4* pb = reinterpret_cast<const float4*>(f.pal) + ((size_t)q.aid << f.n_flags | q.lab) * d4;
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
-      if (ok[h]) a[h] = __ldg(pv + c4[h]), b[h] = __ldg(pa + c4[h]), l[h] = __ldg(pl + c4[h]);
+      for (int h = 0; h < 2; ++h)
+        if (ok[h]) a[h] = __ldg(pv + c4[h]), b[h] = __ldg(pb + c4[h]);
+    } else {
+      const float4* pa = reinterpret_cast<const float4*>(f.pa) + (size_t)q.aid * d4;
+      const float4* pl = reinterpret_cast<const float4*>(f.pl) + (size_t)q.lab * d4;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (ok[h]) a[h] = __ldg(pv + c4[h]), b[h] = __ldg(pa + c4[h]), l[h] = __ldg(pl + c4[h]);
+    }
   };
   int row = blockIdx.x * RPB + rl;
   Rec q0{}, q1{}, q2{};
@@ -293,10 +303,12 @@ __global__ void __launch_bounds__(256) fold_features_kernel(RecordsDev r, FoldTa
     for (int h = 0; h < 2; ++h) {
       if (!ok[h]) continue;
       float v[4];
-      v[0] = a0[h].x + b0[h].x + l0[h].x + x0 * u[0][h].x + x1 * u[1][h].x + x2 * u[2][h].x + x3 * u[3][h].x;
-      v[1] = a0[h].y + b0[h].y + l0[h].y + x0 * u[0][h].y + x1 * u[1][h].y + x2 * u[2][h].y + x3 * u[3][h].y;
-      v[2] = a0[h].z + b0[h].z + l0[h].z + x0 * u[0][h].z + x1 * u[1][h].z + x2 * u[2][h].z + x3 * u[3][h].z;
-      v[3] = a0[h].w + b0[h].w + l0[h].w + x0 * u[0][h].w + x1 * u[1][h].w + x2 * u[2][h].w + x3 * u[3][h].w;
+      const float4 u0 = su[0][c4[h]], u1 = su[1][c4[h]], u2 = su[2][c4[h]], u3 = su[3][c4[h]];
+      if constexpr (PAL) l0[h] = make_float4(-0.f, -0.f, -0.f, -0.f);  // x + -0 == x: folds away
+      v[0] = a0[h].x + b0[h].x + l0[h].x + x0 * u0.x + x1 * u1.x + x2 * u2.x + x3 * u3.x;
+      v[1] = a0[h].y + b0[h].y + l0[h].y + x0 * u0.y + x1 * u1.y + x2 * u2.y + x3 * u3.y;
+      v[2] = a0[h].z + b0[h].z + l0[h].z + x0 * u0.z + x1 * u1.z + x2 * u2.z + x3 * u3.z;
+      v[3] = a0[h].w + b0[h].w + l0[h].w + x0 * u0.w + x1 * u1.w + x2 * u2.w + x3 * u3.w;
 #pragma unroll
       for (int j = 0; j < 4; ++j) v[j] = v[j] > 0.f ? v[j] : 0.01f * v[j];  // tape.hpp:88
       *reinterpret_cast<uint2*>(out + (size_t)row * ldo + c4[h] * 4) = make_uint2(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]));
@@ -305,6 +317,15 @@ __global__ void __launch_bounds__(256) fold_features_kernel(RecordsDev r, FoldTa
     q1 = q2;
 #pragma unroll
     for (int h = 0; h < 2; ++h) a0[h] = a1[h], b0[h] = b1[h], l0[h] = l1[h];
+  }
+}
+
+__global__ void fold_pal_kernel(int naid, int n_flags, int d, const float* __restrict__ pa,
+                                const float* __restrict__ pl, float* __restrict__ pal) {
+  const long long n = (long long)naid << n_flags;
+  for (long long i = blockIdx.x; i < n; i += gridDim.x) {
+    const long long a = i >> n_flags, m = i & ((1 << n_flags) - 1);
+    for (int j = threadIdx.x; j < d; j += blockDim.x) pal[i * d + j] = pa[a * d + j] + pl[m * d + j];
   }
 }
 
@@ -1390,14 +1411,25 @@ void launch_fold_features(const RecordsDev& r, const FoldTables& f, __nv_bfloat1
   if (!fold_features_supported(f.d, f.n_flags) || ldo % 4 != 0)
     throw std::invalid_argument("fold_features: unsupported shape");
   const int g = (f.d + 255) / 256, rpb = 8 / g;
-  const int grid = static_cast<int>(std::min<long long>((r.n + rpb - 1) / rpb, num_sms() * 2LL));  // 124 regs: 2 blocks per SM
+  const int grid = static_cast<int>(std::min<long long>((r.n + rpb - 1) / rpb, num_sms() * 3LL));  // 3 blocks per SM
   // records' scalar inputs in, bf16 hidden rows out (the table gathers are L2 hits)
   const double nb = double(r.n) * (2.0 * f.d + 28.0);
   auto go = [&](auto kern) { ORX_LAUNCH_CATB(PROF_FEAT, nb, launch_pdl(kern, grid, 256, 0, s, r, f, out, ldo)); };
-  if (g == 1) go(fold_features_kernel<1>);
-  else if (g == 2) go(fold_features_kernel<2>);
-  else if (g == 4) go(fold_features_kernel<4>);
-  else go(fold_features_kernel<8>);
+  if (f.pal) {
+    if (g == 1) go(fold_features_kernel<1, true>);
+    else if (g == 2) go(fold_features_kernel<2, true>);
+    else if (g == 4) go(fold_features_kernel<4, true>);
+    else go(fold_features_kernel<8, true>);
+  } else {
+    if (g == 1) go(fold_features_kernel<1, false>);
+    else if (g == 2) go(fold_features_kernel<2, false>);
+    else if (g == 4) go(fold_features_kernel<4, false>);
+    else go(fold_features_kernel<8, false>);
+  }
+}
+void launch_fold_pal(int naid, int n_flags, int d, const float* pa, const float* pl, float* pal, cudaStream_t s) {
+  const long long n = (long long)naid << n_flags;
+  fold_pal_kernel<<<static_cast<int>(std::min<long long>(n, 148LL * 16)), 256, 0, s>>>(naid, n_flags, d, pa, pl, pal);
 }
 template <class T>
 void launch_static_features(int U, const int32_t* uid, const int32_t* gender, const int32_t* age, const float* ue,

@@ -46,8 +46,13 @@ struct FoldTables {
   const float* pa = nullptr;  // [aid_vocab][d] = emb.aid . W1[d:d+ad]
   const float* pl = nullptr;  // [2^n_flags][d]: label multi-hot . W1[lab] + scalar-section b rows + fc1 bias
   const float* u = nullptr;   // [4][d]: tag / ts / playtime / duration w rows through W1
+  // optional [aid_vocab << n_flags][d] = pa[aid] + pl[labels]: one gather less per
+  // record (the kernel is bound by L2 reads of these rows)
+  const float* pal = nullptr;
   int d = 0, n_flags = 0;
 };
+// pal[(a << n_flags) | m][j] = pa[a][j] + pl[m][j]
+void launch_fold_pal(int naid, int n_flags, int d, const float* pa, const float* pl, float* pal, cudaStream_t s);
 bool fold_features_supported(int d, int n_flags);
 void launch_fold_features(const RecordsDev& r, const FoldTables& f, __nv_bfloat16* out, int ldo, cudaStream_t s);
 template <class T>

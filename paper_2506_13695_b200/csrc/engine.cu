@@ -1276,8 +1276,7 @@ class EngineT final : public Engine {
       gemm(xn_, d, q.fc1, U * Nq, e1);
       if (last) {
         Epi e2 = epi(z_, d, true);
-        e2.resid = z_;
-        e2.ld_resid = d;
+        pos_resid(e2);
         e2.row_map = dp<int32_t>(sg_.off_life_map);
         gemm(ffh_, c.ffn_hidden, q.fc2, U * Nq, e2);
       } else {
@@ -1324,11 +1323,19 @@ class EngineT final : public Engine {
     }
   }
 
+  // The pathway outputs land in z on top of the position embedding: the
+  // residual operand is the [Tn][d] position table, indexed by z row % Tn (it
+  // stays in L2), so z itself is initialised only at left-padding rows
+  // (launch_z_init) instead of being written once and read back.
+  void pos_resid(Epi& e) {
+    e.resid = pos_;
+    e.ld_resid = cfg_.d_model;
+    e.resid_mod = enc_seq_len(cfg_);
+  }
   void fc2_into_z(const Mlp& m, int rows, const int32_t* map) {
     const int d = cfg_.d_model;
     Epi e2 = epi(z_, d, true);
-    e2.resid = z_;
-    e2.ld_resid = d;
+    pos_resid(e2);
     e2.row_map = map;
     gemm(hid_, d, m.fc2, rows, e2);
   }
@@ -1338,8 +1345,7 @@ class EngineT final : public Engine {
     e1.act = ACT_LEAKY;
     gemm(x, ldx, m.fc1, rows, e1);
     Epi e2 = epi(z_, d, true);
-    e2.resid = z_;
-    e2.ld_resid = d;
+    pos_resid(e2);
     e2.row_map = map;
     gemm(hid_, d, m.fc2, rows, e2);
   }
@@ -1781,8 +1787,9 @@ class EngineT final : public Engine {
       gk.stride = Tn;
       gk.fixed_len = Tn;
       const int n_new = static_cast<int>(std::min<int64_t>(width, static_cast<int64_t>(n_live) * V));
-      // fused selection: unconstrained, and the head GEMM runs on the CTA-pair kernel (M > 128)
-      const bool fused = fused_select_ && !constrained && rows > 128;
+      // fused selection: unconstrained (the head GEMM then runs on the CTA-pair kernel, any M)
+      static const bool step0_topk = getenv("ORX_STEP0_TOPK") != nullptr;  // A/B: materialised path at M <= 128
+      const bool fused = fused_select_ && !constrained && (rows > 128 || !step0_topk);
       decode_step(step, rows, U, gq, gk, bs_[cur].codes, L, bs_[cur].anc, L, n_live, nullptr,
                   fused ? head_stats_ : nullptr);
       if (fused) {

@@ -40,8 +40,11 @@ constexpr int kBK = 64;  // 64 bf16 = 128 B = one swizzle row
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp 0 TMA, warp 1 MMA, 8 epilogue warps
 
+__device__ __forceinline__ int resid_row(const Epi& e, int orow) {
+  return e.resid_mod > 0 ? orow % e.resid_mod : orow;
+}
 __device__ __forceinline__ void epi_load_resid(const Epi& e, int orow, int col0, float (&r)[32]) {
-  const float* rp = e.resid + (size_t)orow * e.ld_resid + col0;
+  const float* rp = e.resid + (size_t)resid_row(e, orow) * e.ld_resid + col0;
   if (col0 + 32 <= e.n_out && ((reinterpret_cast<uintptr_t>(rp) & 15) == 0)) {
 #pragma unroll
     for (int j = 0; j < 32; j += 4) {
@@ -218,7 +221,7 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tb, int row
     if (hr) {
       // pull this thread's residual row segment (CH * 128 B) into L2 while the MMAs run;
       // the chunk loads below then hit L2 instead of waiting on HBM one chunk at a time
-      const float* rp = e.resid + (size_t)orow * e.ld_resid + nt * BN + half * CH * 32;
+      const float* rp = e.resid + (size_t)resid_row(e, orow) * e.ld_resid + nt * BN + half * CH * 32;
       if (nt * BN + (half + 1) * CH * 32 <= e.n_out && (reinterpret_cast<uintptr_t>(rp) & 15) == 0)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rp), "r"(CH * 128) : "memory");
       epi_load_resid(e, orow, nt * BN + half * CH * 32, rc);  // in flight while the MMAs finish
@@ -290,7 +293,7 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
   }
   if (MODE & EPI_RESID) {
     if (orow >= 0)  // this row's residual segment into L2 while the MMAs run
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(e.resid + (size_t)orow * e.ld_resid +
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(e.resid + (size_t)resid_row(e, orow) * e.ld_resid +
                                                                        nt * BN + half * CH * 32),
                    "r"(CH * 128)
                    : "memory");
@@ -303,7 +306,7 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
     const int col0 = nt * BN + (half * CH + i) * 32;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      dst[k] = orr[k] >= 0 ? __ldg(reinterpret_cast<const float4*>(e.resid + (size_t)orr[k] * e.ld_resid + col0) + q)
+      dst[k] = orr[k] >= 0 ? __ldg(reinterpret_cast<const float4*>(e.resid + (size_t)resid_row(e, orr[k]) * e.ld_resid + col0) + q)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
   };
   if (MODE & EPI_RESID) load_resid(0, rr[0]);
@@ -881,7 +884,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const float* __restrict_
         x = act_apply(x, epi.act);
         x *= rs;
       }
-      if (epi.resid) x += epi.resid[(size_t)orow * epi.ld_resid + oc];
+      if (epi.resid) x += epi.resid[(size_t)(epi.resid_mod > 0 ? orow % epi.resid_mod : orow) * epi.ld_resid + oc];
       oc += epi.col_off;
       if (epi.out_bf16)
         reinterpret_cast<__nv_bfloat16*>(epi.out)[(size_t)orow * epi.ldo + oc] = __float2bfloat16_rn(x);
@@ -1225,7 +1228,8 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
               " mode=" + std::to_string(ep.mode) + (grp && grp->tile_expert ? " grouped" : "") +
               (ep.swiglu ? " swiglu" : "") + (ep.vt ? " vt" : "") + (ep.row_map ? " row_map" : ""));
   const bool grouped = grp && grp->tile_expert;
-  const bool pair = grouped ? grp->tile_rows == 2 * kBM : (M > kBM && !force_single_cta());
+  // head statistics (EPI_STATS) come from the CTA-pair kernel's staged epilogue only: any M
+  const bool pair = grouped ? grp->tile_rows == 2 * kBM : ((M > kBM || epi.stats) && !force_single_cta());
   if (pair) {
     // BN=128 for small N, and where 256-wide tiles would leave a badly
     // filled last wave (e.g. M=16384, N=1024: 256 tiles on 74 pairs = 3.46

@@ -36,6 +36,7 @@ struct Epi {
   void* out = nullptr;               // [rows, ldo]
   const int* row_map = nullptr;      // output row = row_map[r] (< 0: dropped)
   int ld_resid = 0;
+  int resid_mod = 0;  // > 0: the residual row of output row r is r % resid_mod (a per-position table)
   int ldo = 0;
   int out_bf16 = 0;
   int act = 0;      // Act

@@ -357,6 +357,9 @@ __global__ void z_init_kernel(int U, int T, int d, const float* pos, const float
   } else if (t >= 1 + Ls && t < 1 + Ls + Lp) {
     if (t - 1 - Ls < Lp - n_p[u]) pad = pad_p;
   }
+  // every other row (static, records, QFormer queries) is written by a GEMM
+  // whose residual operand is the position table itself (engine pos_resid)
+  if (!pad) return;
   if (d % 4 == 0) {  // float4 path (the callers' buffers are 16-byte aligned)
     const float4* p4 = reinterpret_cast<const float4*>(pos + (size_t)t * d);
     const float4* q4 = reinterpret_cast<const float4*>(pad);

@@ -59,7 +59,8 @@ template <class T>
 void launch_static_features(int U, const int32_t* uid, const int32_t* gender, const int32_t* age,
                             const float* uid_emb, const float* gender_emb, const float* age_emb, int sdim,
                             int uid_vocab, int gender_vocab, int age_vocab, T* out, int ldo, cudaStream_t s);
-// z[u*T + t] = pos[t] (+ pad row where the pathway is left-padded).
+// z[u*T + t] = pos[t] + pad row at the left-padding rows of the short / positive
+// pathways only (every other row is a GEMM output over the position table).
 void launch_z_init(int U, int T, int d, const float* pos, const float* pad_short, const float* pad_pos,
                    const int32_t* n_short, const int32_t* n_pos, int Ls, int Lp, float* z, cudaStream_t s);
 template <class T>

@@ -802,9 +802,11 @@ class EngineT final : public Engine {
       CUDA_CHECK(cudaMemset(vt_x_, 0, static_cast<size_t>(Ld) * U * d * Tpad_ * sizeof(T)));
     }
     h_ = ar_.alloc<float>(static_cast<size_t>(Rd_) * d);
-    for (int p = 0; p < L; ++p) cache_.push_back(ar_.alloc<T>(static_cast<size_t>(Rd_) * Ld * 2 * d));
-    cache_ptrs_ = ar_.alloc<T*>(L);
-    CUDA_CHECK(cudaMemcpy(cache_ptrs_, cache_.data(), L * sizeof(T*), cudaMemcpyHostToDevice));
+    // self-attention K/V cache: each (position, layer) keeps its own QKV GEMM output
+    // [rows][3d]; later positions read the K|V columns of their ancestor rows there
+    for (int p = 0; p < L * Ld; ++p) kvpos_.push_back(ar_.alloc<T>(static_cast<size_t>(Rd_) * 3 * d));
+    kvpos_ptrs_ = ar_.alloc<T*>(static_cast<size_t>(L) * Ld);
+    CUDA_CHECK(cudaMemcpy(kvpos_ptrs_, kvpos_.data(), static_cast<size_t>(L) * Ld * sizeof(T*), cudaMemcpyHostToDevice));
     logits_ = ar_.alloc<float>(static_cast<size_t>(Rd_) * c.codebook_size);
     const int ksel = std::min(maxW_, c.codebook_size);
     cand_ = ar_.alloc<uint64_t>(static_cast<size_t>(Rd_) * ksel);
@@ -1650,8 +1652,9 @@ class EngineT final : public Engine {
       const DecL& w = dec_[l];
       if (!have_x) launch_rmsnorm<T>(rows, d, h_, d, w.n1, xn_, d, st_);
       have_x = false;
-      gemm(xn_, d, w.sqkv, rows, epi(qkv_, 3 * d, false));
-      launch_dec_self_attn<T>(rows, d, H, step, l, Ld, qkv_, cache_ptrs_, anc, anc_stride, att_, st_);
+      T* qkv_now = kvpos_[static_cast<size_t>(step) * Ld + l];  // this position's QKV = its K/V cache entry
+      gemm(xn_, d, w.sqkv, rows, epi(qkv_now, 3 * d, false));
+      launch_dec_self_attn<T>(rows, d, H, step, l, Ld, qkv_now, kvpos_ptrs_, anc, anc_stride, att_, st_);
       Epi e = epi(h_, d, true);
       e.resid = h_;
       e.ld_resid = d;
@@ -2210,8 +2213,8 @@ class EngineT final : public Engine {
   int max_tiles_ = 0;
   T *feat_, *hid_, *keys_, *kvl_, *xn_, *qkv_, *att_, *ffh_, *qproj_, *qcur_, *zt_, *xkv_;
   float *z_, *qo_, *h_, *logits_, *lse_;
-  std::vector<T*> cache_;
-  T** cache_ptrs_ = nullptr;
+  std::vector<T*> kvpos_;       // [position * dec_layers + layer] -> [Rd_][3d] QKV output (self-attention cache)
+  T** kvpos_ptrs_ = nullptr;
   uint64_t* cand_ = nullptr;
   int32_t* topk_fail_ = nullptr;
   BeamState bs_[2];

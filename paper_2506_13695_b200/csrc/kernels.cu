@@ -441,12 +441,19 @@ __global__ void dec_embed_kernel(int rows, int d, const float* table, const int3
   for (int c = threadIdx.x; c < d; c += blockDim.x) h[(size_t)r * d + c] = table[src + c];
 }
 
-// Warp per (row, head): keys are positions 0..step; position p < step comes
-// from the cache of that position at row anc[r][p], position `step` is the
-// row's own K/V (also appended to cache[step]).
+// K / V of position p < step for a row: the K|V columns of that position's
+// QKV GEMM output (kv[p * L + layer], [rows_p][3d]) at the ancestor row.
+template <class T>
+__device__ __forceinline__ const T* kv_at(T* const* kv, int p, int L, int layer, int row, int d) {
+  return kv[p * L + layer] + (size_t)row * 3 * d + d;
+}
+
+// Warp per (row, head): keys are positions 0..step; position p < step is read
+// from that position's QKV output at row anc[r][p], position `step` is the
+// row's own K/V (this step's QKV output stays in place as its cache entry).
 template <class T>
 __global__ void dec_self_attn_kernel(int rows, int d, int heads, int step, int layer, int L, const T* __restrict__ qkv,
-                                     T* const* __restrict__ cache, const int32_t* __restrict__ anc, int anc_stride,
+                                     T* const* __restrict__ kv, const int32_t* __restrict__ anc, int anc_stride,
                                      T* __restrict__ out) {
   pdl_begin();
   int gw = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -456,16 +463,11 @@ __global__ void dec_self_attn_kernel(int rows, int d, int heads, int step, int l
   const T* q = qkv + (size_t)r * 3 * d + h * dh;
   const T* kown = q + d;
   const T* vown = q + 2 * d;
-  T* cown = cache[step] + ((size_t)r * L + layer) * 2 * d;
-  for (int c = lane; c < dh; c += 32) {
-    cown[h * dh + c] = kown[c];
-    cown[d + h * dh + c] = vown[c];
-  }
   const float scale = rsqrtf(static_cast<float>(dh));
   float sc[8];
   float mx = -FLT_MAX;
   for (int p = 0; p <= step; ++p) {
-    const T* k = p == step ? kown : cache[p] + ((size_t)anc[(size_t)r * anc_stride + p] * L + layer) * 2 * d + h * dh;
+    const T* k = p == step ? kown : kv_at(kv, p, L, layer, anc[(size_t)r * anc_stride + p], d) + h * dh;
     float s = 0.f;
     for (int c = lane; c < dh; c += 32) s += to_f(q[c]) * to_f(k[c]);
     s = warp_sum(s) * scale;
@@ -480,7 +482,7 @@ __global__ void dec_self_attn_kernel(int rows, int d, int heads, int step, int l
   for (int c = lane; c < dh; c += 32) {
     float acc = 0.f;
     for (int p = 0; p <= step; ++p) {
-      const T* v = p == step ? vown : cache[p] + ((size_t)anc[(size_t)r * anc_stride + p] * L + layer) * 2 * d + d + h * dh;
+      const T* v = p == step ? vown : kv_at(kv, p, L, layer, anc[(size_t)r * anc_stride + p], d) + d + h * dh;
       acc += sc[p] * to_f(v[c]);
     }
     out[(size_t)r * d + h * dh + c] = from_f<T>(acc / den);
@@ -491,7 +493,7 @@ __global__ void dec_self_attn_kernel(int rows, int d, int heads, int step, int l
 // head dims; same math and order of operations as dec_self_attn_kernel.
 template <class T>
 __global__ void __launch_bounds__(256) dec_self_attn4_kernel(int rows, int d, int heads, int step, int layer, int L,
-                                                             const T* __restrict__ qkv, T* const* __restrict__ cache,
+                                                             const T* __restrict__ qkv, T* const* __restrict__ kv,
                                                              const int32_t* __restrict__ anc, int anc_stride,
                                                              T* __restrict__ out) {
   pdl_begin();
@@ -505,17 +507,12 @@ __global__ void __launch_bounds__(256) dec_self_attn4_kernel(int rows, int d, in
   const float4 q4 = ld4(q + c);
   const float4 k4 = ld4(q + d + c);
   const float4 v4 = ld4(q + 2 * d + c);
-  T* cown = cache[step] + ((size_t)r * L + layer) * 2 * d + h * dh;
-  if (on) {
-    st4(cown + c, k4);
-    st4(cown + d + c, v4);
-  }
   const float scale = rsqrtf(static_cast<float>(dh));
   float sc[8];
   float mx = -FLT_MAX;
   for (int p = 0; p <= step; ++p) {
     float4 kk = k4;
-    if (p < step) kk = ld4(cache[p] + ((size_t)anc[(size_t)r * anc_stride + p] * L + layer) * 2 * d + h * dh + c);
+    if (p < step) kk = ld4(kv_at(kv, p, L, layer, anc[(size_t)r * anc_stride + p], d) + h * dh + c);
     float s = on ? q4.x * kk.x + q4.y * kk.y + q4.z * kk.z + q4.w * kk.w : 0.f;
     s = warp_sum(s) * scale;
     sc[p] = s;
@@ -529,7 +526,7 @@ __global__ void __launch_bounds__(256) dec_self_attn4_kernel(int rows, int d, in
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int p = 0; p <= step; ++p) {
     float4 vv = v4;
-    if (p < step) vv = ld4(cache[p] + ((size_t)anc[(size_t)r * anc_stride + p] * L + layer) * 2 * d + d + h * dh + c);
+    if (p < step) vv = ld4(kv_at(kv, p, L, layer, anc[(size_t)r * anc_stride + p], d) + d + h * dh + c);
     acc.x += sc[p] * vv.x, acc.y += sc[p] * vv.y, acc.z += sc[p] * vv.z, acc.w += sc[p] * vv.w;
   }
   if (on) {
@@ -1531,7 +1528,7 @@ void launch_dec_embed(int rows, int d, const float* table, const int32_t* code, 
 template <int EPL>
 __global__ void __launch_bounds__(256) dec_self_attn_row_kernel(int rows, int d, int heads, int step, int layer, int L,
                                                                 const __nv_bfloat16* __restrict__ qkv,
-                                                                __nv_bfloat16* const* __restrict__ cache,
+                                                                __nv_bfloat16* const* __restrict__ kv,
                                                                 const int32_t* __restrict__ anc, int anc_stride,
                                                                 __nv_bfloat16* __restrict__ out) {
   pdl_begin();
@@ -1547,12 +1544,6 @@ __global__ void __launch_bounds__(256) dec_self_attn_row_kernel(int rows, int d,
     q[i] = __ldg(reinterpret_cast<const uint4*>(qr) + i);
     kv_own[0][i] = __ldg(reinterpret_cast<const uint4*>(qr + d) + i);
     kv_own[1][i] = __ldg(reinterpret_cast<const uint4*>(qr + 2 * d) + i);
-  }
-  __nv_bfloat16* cown = cache[step] + ((size_t)r * L + layer) * 2 * d + c0;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    reinterpret_cast<uint4*>(cown)[i] = kv_own[0][i];
-    reinterpret_cast<uint4*>(cown + d)[i] = kv_own[1][i];
   }
   const int a_l = lane < step ? anc[(size_t)r * anc_stride + lane] : 0;
   auto bf2 = [](uint32_t w) { return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w)); };
@@ -1578,7 +1569,7 @@ __global__ void __launch_bounds__(256) dec_self_attn_row_kernel(int rows, int d,
     float sp;
     if (p < step) {
       const int ar = __shfl_sync(0xffffffffu, a_l, p);
-      const uint4* kp = reinterpret_cast<const uint4*>(cache[p] + ((size_t)ar * L + layer) * 2 * d + c0);
+      const uint4* kp = reinterpret_cast<const uint4*>(kv_at(kv, p, L, layer, ar, d) + c0);
       uint4 kk[NV];
 #pragma unroll
       for (int i = 0; i < NV; ++i) kk[i] = kp[i];
@@ -1601,7 +1592,7 @@ __global__ void __launch_bounds__(256) dec_self_attn_row_kernel(int rows, int d,
     uint4 vv[NV];
     if (p < step) {
       const int ar = __shfl_sync(0xffffffffu, a_l, p);
-      const uint4* vp = reinterpret_cast<const uint4*>(cache[p] + ((size_t)ar * L + layer) * 2 * d + d + c0);
+      const uint4* vp = reinterpret_cast<const uint4*>(kv_at(kv, p, L, layer, ar, d) + d + c0);
 #pragma unroll
       for (int i = 0; i < NV; ++i) vv[i] = vp[i];
     } else {
@@ -1628,11 +1619,11 @@ __global__ void __launch_bounds__(256) dec_self_attn_row_kernel(int rows, int d,
 }
 
 template <class T>
-void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L, const T* qkv, T* const* cache,
+void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L, const T* qkv, T* const* kv,
                           const int32_t* anc, int anc_stride, T* out, cudaStream_t s) {
   if (rows <= 0) return;
-  // per row: q, k, v in; the ancestors' cached k, v; out row; this position's k, v into the cache
-  const double nb = double(rows) * d * sizeof(T) * (3.0 + 2.0 * step + 1.0 + 2.0);
+  // per row: q, k, v in; the ancestors' k, v; out row
+  const double nb = double(rows) * d * sizeof(T) * (3.0 + 2.0 * step + 1.0);
   long long warps = (long long)rows * heads;
   if constexpr (sizeof(T) == 2) {
     const int dh = d / heads, epl = d / 32, lph = epl > 0 ? dh / epl : 0;
@@ -1640,7 +1631,7 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L
       auto go = [&](auto kern) {
         ORX_LAUNCH_CATB(PROF_DEC_SELF, nb, launch_pdl(kern, (rows + 7) / 8, 256, 0, s, rows, d, heads, step, layer, L,
                                                  reinterpret_cast<const __nv_bfloat16*>(qkv),
-                                                 reinterpret_cast<__nv_bfloat16* const*>(cache), anc, anc_stride,
+                                                 reinterpret_cast<__nv_bfloat16* const*>(kv), anc, anc_stride,
                                                  reinterpret_cast<__nv_bfloat16*>(out)));
       };
       if (epl == 8) go(dec_self_attn_row_kernel<8>);
@@ -1652,11 +1643,11 @@ void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int L
   }
   if ((d / heads) % 4 == 0 && d / heads <= 128 && d % 4 == 0) {
     ORX_LAUNCH_CATB(PROF_DEC_SELF, nb, launch_pdl(dec_self_attn4_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, 
-        rows, d, heads, step, layer, L, qkv, cache, anc, anc_stride, out));
+        rows, d, heads, step, layer, L, qkv, kv, anc, anc_stride, out));
     return;
   }
   ORX_LAUNCH_CATB(PROF_DEC_SELF, nb, launch_pdl(dec_self_attn_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, 
-      rows, d, heads, step, layer, L, qkv, cache, anc, anc_stride, out));
+      rows, d, heads, step, layer, L, qkv, kv, anc, anc_stride, out));
 }
 void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, const float* gain, const float* gate_t,
                       const float* gate_gain, const float* bias, int32_t* sel, float* wts, int32_t* counts,

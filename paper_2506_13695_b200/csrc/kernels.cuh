@@ -76,10 +76,12 @@ void launch_fill_rows(int rows, int cols, const float* src_row, T* out, int ldo,
 void launch_dec_embed(int rows, int d, const float* table, const int32_t* code, int code_stride, float* h,
                       cudaStream_t s);
 // Decoder causal self-attention over cached positions (policy.cpp:282-283).
-// qkv: [rows][3d]; cache[p]: [rows_p][L][2][d]; anc: [rows][anc_stride] row index of position p < step.
+// qkv: [rows][3d] this position's QKV output; kv[p * n_layers + layer]: position p's
+// QKV output [rows_p][3d] (its K|V columns are the cache, nothing is copied);
+// anc: [rows][anc_stride] row index of position p < step.
 template <class T>
 void launch_dec_self_attn(int rows, int d, int heads, int step, int layer, int n_layers, const T* qkv,
-                          T* const* cache, const int32_t* anc, int anc_stride, T* out, cudaStream_t s);
+                          T* const* kv, const int32_t* anc, int anc_stride, T* out, cudaStream_t s);
 
 // MoE (nn.cpp:117-172)
 // Routing reads the fp32 residual x and the pre-MoE RMSNorm gain (norm recomputed in fp32).

@@ -849,7 +849,7 @@ class EngineT final : public Engine {
       sel_ = ar_.alloc<int32_t>(mrows * k);
       wts_ = ar_.alloc<float>(mrows * k);
       slot_ = ar_.alloc<int32_t>(mrows * k);
-      counts_ = ar_.alloc<int32_t>(E);
+      counts_ = ar_.alloc<int32_t>(2 * static_cast<size_t>(E));  // routing histogram | scatter fill counters
       cursor_ = ar_.alloc<int32_t>(E);
       tile_expert_ = ar_.alloc<int32_t>(max_tiles_);
       n_mtiles_ = ar_.alloc<int32_t>(1);
@@ -1184,9 +1184,16 @@ class EngineT final : public Engine {
   // ------------------------------------------------------------------------
   // encode (policy.cpp:254-265)
   // ------------------------------------------------------------------------
+  // MoE routing counters to zero at the start of a forward pass (each MoE
+  // combine re-zeroes them for the next layer; this also recovers from an
+  // interrupted pass)
+  void zero_moe_counters() {
+    if (counts_) CUDA_CHECK(cudaMemsetAsync(counts_, 0, 2 * cfg_.n_experts * sizeof(int32_t), st_));
+  }
   void run_encode() {
     require(staged_, "no user batch staged");
     const orx_config& c = cfg_;
+    if (enc_moe(c)) zero_moe_counters();
     const int d = c.d_model, U = sg_.U, Tn = enc_seq_len(c), Nq = c.n_queries, H = c.n_heads, dh = d / H;
     launch_z_init(U, Tn, d, pos_, pad_s_, pad_p_, dp<int32_t>(sg_.off_ns), dp<int32_t>(sg_.off_np), c.short_len,
                   c.positive_len, z_, st_);
@@ -1389,7 +1396,8 @@ class EngineT final : public Engine {
            const float* post_gain = nullptr) {
     const orx_config& c = cfg_;
     const int d = c.d_model, E = c.n_experts, k = c.experts_active;
-    CUDA_CHECK(cudaMemsetAsync(counts_, 0, E * sizeof(int32_t), st_));
+    // counts_ (histogram | scatter fill) is zero here: zeroed once per forward pass
+    // (zero_moe_counters) and by every MoE combine for the next layer
     // tensor-pipe router for large row counts (one 128-row tile per SM is latency-bound: the SIMT
     // router is faster below a few thousand rows)
     if (m.gate_hi && rows >= 4096)
@@ -1399,13 +1407,21 @@ class EngineT final : public Engine {
                        m.gate_sw);
     if (route_stats_) record_routing(rows);
     if (ep_world_ > 1) return moe_ep(m, x, rows, h, post, post_gain);
-    launch_moe_plan(E, counts_, cursor_, tile_expert_, max_tiles_, n_mtiles_, kMoeTile, st_);
-    launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, cursor_, slot_, xg_, row_scale_, st_);
+    MoePlan plan;
+    plan.counts = counts_;
+    plan.fill = counts_ + E;
+    plan.tile_expert = tile_expert_;
+    plan.n_mtiles = n_mtiles_;
+    plan.max_tiles = max_tiles_;
+    plan.tile_rows = kMoeTile;
+    plan.E = E;
+    launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, plan, slot_, xg_, row_scale_, st_);
     expert_ffn(m, static_cast<int>(S_), static_cast<long long>(rows) * k);
     if constexpr (kBf16) {
-      if (post && launch_moe_combine_norm(rows, k, d, yg_, slot_, h, d, post_gain, post, d, st_)) return true;
+      if (post && launch_moe_combine_norm(rows, k, d, yg_, slot_, h, d, post_gain, post, d, st_, counts_, 2 * E))
+        return true;
     }
-    launch_moe_combine(rows, k, d, yg_, slot_, h, d, st_);
+    launch_moe_combine(rows, k, d, yg_, slot_, h, d, st_, counts_, 2 * E);
     return false;
   }
 
@@ -1607,9 +1623,10 @@ class EngineT final : public Engine {
     launch_ep_wait(ep_, EP_RETURN, st_);
     const T* yr = static_cast<const T*>(ep_.yr[ep_rank_]);
     if constexpr (kBf16) {
-      if (post && launch_moe_combine_norm(rows, k, d, yr, slot_, h, d, post_gain, post, d, st_)) return true;
+      if (post && launch_moe_combine_norm(rows, k, d, yr, slot_, h, d, post_gain, post, d, st_, counts_, 2 * E))
+        return true;
     }
-    launch_moe_combine(rows, k, d, yr, slot_, h, d, st_);
+    launch_moe_combine(rows, k, d, yr, slot_, h, d, st_, counts_, 2 * E);
     return false;
   }
 
@@ -1645,6 +1662,7 @@ class EngineT final : public Engine {
                    float2* head_stats = nullptr) {
     const orx_config& c = cfg_;
     const int d = c.d_model, H = c.n_heads, dh = d / H, Ld = dec_layers(c), Tn = enc_seq_len(c);
+    if (c.moe_enabled) zero_moe_counters();
     launch_dec_embed(rows, d, step == 0 ? bos_ : tokens_[step - 1], step == 0 ? nullptr : codes + (step - 1),
                      code_stride, h_, st_);
     bool have_x = false;  // xn_ already holds the next op's input (fused into the MoE combine)

@@ -548,8 +548,9 @@ __device__ __forceinline__ float4 ldy4(const __nv_bfloat16* p) {
 template <class YT>
 __global__ void __launch_bounds__(256) moe_combine4_kernel(int rows, int k, int d, const YT* __restrict__ yg,
                                                            const int32_t* __restrict__ slot, float* __restrict__ h,
-                                                           int ldh) {
+                                                           int ldh, int32_t* __restrict__ zero, int nzero) {
   pdl_begin();
+  if (blockIdx.x == 0 && threadIdx.x < nzero) zero[threadIdx.x] = 0;  // routing counters, for the next MoE layer
   const int q = d / 4;
   const long long n = (long long)rows * q;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -965,52 +966,49 @@ __global__ void __launch_bounds__(256, 1) moe_route4_kernel(int rows, int d, int
 }
 
 // Segment offsets padded to the GEMM expert tile (128 rows, 256 for the CTA-pair kernel); tile -> expert table.
-__global__ void moe_plan_kernel(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
-                                int32_t* n_mtiles, int tile_rows) {
-  pdl_begin();
-  // lane e: tiles of expert e, exclusive prefix over experts (E <= 32), then
-  // every thread of the block fills the tile -> expert table
-  __shared__ int first[33];
-  const int lane = threadIdx.x & 31;
+// The grouped-GEMM plan inside the scatter (no separate launch): every CTA
+// derives the expert segments (padded to the tile) from the final routing
+// histogram, CTA 0 also writes the tile -> expert table; a pair's slot is its
+// expert's segment start + an atomic on the zeroed per-expert fill counter.
+__device__ __forceinline__ void moe_plan_block(const MoePlan& p, int* seg0) {
   if (threadIdx.x < 32) {
-    const int nt = lane < E ? (counts[lane] + tile_rows - 1) / tile_rows : 0;
+    const int lane = threadIdx.x;
+    const int nt = lane < p.E ? (p.counts[lane] + p.tile_rows - 1) / p.tile_rows : 0;
     int incl = nt;
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-    if (lane < E) {
-      first[lane] = incl - nt;
-      cursor[lane] = (incl - nt) * tile_rows;
-    }
-    if (lane == 31) {
-      first[E] = min(incl, max_tiles);
-      *n_mtiles = min(incl, max_tiles);
-    }
+    seg0[lane] = incl - nt;  // first tile of expert `lane`
+    if (lane == 31) seg0[32] = min(incl, p.max_tiles);
   }
   __syncthreads();
-  const int total = first[E];
-  for (int i = threadIdx.x; i < max_tiles; i += blockDim.x) {
-    int e = -1;
-    if (i < total)
-      for (int x = 0; x < E; ++x)
-        if (i >= first[x]) e = x;
-    tile_expert[i] = e;
+  if (blockIdx.x == 0) {
+    const int total = seg0[32];
+    if (threadIdx.x == 0) *p.n_mtiles = total;
+    for (int i = threadIdx.x; i < p.max_tiles; i += blockDim.x) {
+      int e = -1;
+      if (i < total)
+        for (int x = 0; x < p.E; ++x)
+          if (i >= seg0[x]) e = x;
+      p.tile_expert[i] = e;
+    }
   }
 }
 
 template <class T>
 __global__ void moe_scatter_kernel(int rows, int k, int d, const T* __restrict__ x, int ldx,
-                                   const int32_t* __restrict__ sel, const float* __restrict__ wts,
-                                   int32_t* __restrict__ cursor, int32_t* __restrict__ slot, T* __restrict__ xg,
-                                   float* __restrict__ row_scale) {
+                                   const int32_t* __restrict__ sel, const float* __restrict__ wts, MoePlan plan,
+                                   int32_t* __restrict__ slot, T* __restrict__ xg, float* __restrict__ row_scale) {
+  __shared__ int seg0[33];
   pdl_begin();
+  moe_plan_block(plan, seg0);
   int gw = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (gw >= rows * k) return;
   int r = gw / k;
   int e = sel[gw];
   int s = 0;
-  if (lane == 0) s = atomicAdd(&cursor[e], 1);
+  if (lane == 0) s = seg0[e] * plan.tile_rows + atomicAdd(&plan.fill[e], 1);
   s = __shfl_sync(0xffffffffu, s, 0);
   if (lane == 0) {
     slot[gw] = s;
@@ -1031,10 +1029,12 @@ __global__ void moe_scatter_kernel(int rows, int k, int d, const T* __restrict__
 // then the warp copies the 32 rows with 16-byte accesses (bf16, d % 8 == 0).
 __global__ void __launch_bounds__(256) moe_scatter32_kernel(int rows, int k, int d, const __nv_bfloat16* __restrict__ x,
                                                             int ldx, const int32_t* __restrict__ sel,
-                                                            const float* __restrict__ wts, int32_t* __restrict__ cursor,
+                                                            const float* __restrict__ wts, MoePlan plan,
                                                             int32_t* __restrict__ slot, __nv_bfloat16* __restrict__ xg,
                                                             float* __restrict__ row_scale) {
+  __shared__ int seg0[33];
   pdl_begin();
+  moe_plan_block(plan, seg0);
   const int lane = threadIdx.x & 31;
   const int base_pair = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
   const int n_pairs = rows * k;
@@ -1046,7 +1046,7 @@ __global__ void __launch_bounds__(256) moe_scatter32_kernel(int rows, int k, int
   const unsigned peers = __match_any_sync(0xffffffffu, e);
   const int leader = __ffs(peers) - 1;
   int base = 0;
-  if (on && lane == leader) base = atomicAdd(&cursor[e], __popc(peers));
+  if (on && lane == leader) base = seg0[e] * plan.tile_rows + atomicAdd(&plan.fill[e], __popc(peers));
   base = __shfl_sync(0xffffffffu, base, leader);
   const int my_slot = base + __popc(peers & ((1u << lane) - 1u));
   if (on) {
@@ -1066,8 +1066,10 @@ __global__ void __launch_bounds__(256) moe_scatter32_kernel(int rows, int k, int
 // h[r] += sum_j (ascending expert) y[slot[r][j]]; y already carries the gate weight.
 template <class YT>
 __global__ void moe_combine_kernel(int rows, int k, int d, const YT* __restrict__ yg,
-                                   const int32_t* __restrict__ slot, float* __restrict__ h, int ldh) {
+                                   const int32_t* __restrict__ slot, float* __restrict__ h, int ldh,
+                                   int32_t* __restrict__ zero, int nzero) {
   pdl_begin();
+  if (blockIdx.x == 0 && threadIdx.x < nzero) zero[threadIdx.x] = 0;
   int r = blockIdx.x;
   if (r >= rows) return;
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
@@ -1691,14 +1693,10 @@ void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, co
   ORX_LAUNCH_CAT(PROF_MOE_ROUTE, launch_pdl(moe_route_kernel, blocks, 256, smem, s, rows, d, E, k, x, ldx, gain, gate_t, bias,
                                                                             sel, wts, counts));
 }
-void launch_moe_plan(int E, const int32_t* counts, int32_t* cursor, int32_t* tile_expert, int max_tiles,
-                     int32_t* n_mtiles, int tile_rows, cudaStream_t s) {
-  ORX_LAUNCH_CAT(PROF_MOE_ROUTE,
-                 launch_pdl(moe_plan_kernel, 1, 256, 0, s, E, counts, cursor, tile_expert, max_tiles, n_mtiles, tile_rows));
-}
 template <class T>
 void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
-                        int32_t* cursor, int32_t* slot, T* xg, float* row_scale, cudaStream_t s) {
+                        const MoePlan& plan, int32_t* slot, T* xg, float* row_scale, cudaStream_t s) {
+  if (plan.E > 32) throw std::invalid_argument("moe_scatter: at most 32 experts");
   const double nb = double(rows) * d * sizeof(T) * (1.0 + k);  // token rows in, k expert-sorted copies out
   if (rows <= 0) return;
   long long warps = (long long)rows * k;
@@ -1706,13 +1704,13 @@ void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32
     if (d % 8 == 0 && ldx % 8 == 0 && warps >= 8192) {  // many pairs: aggregate the slot atomics per warp
       const long long w32 = (warps + 31) / 32;
       ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_scatter32_kernel, static_cast<int>((w32 + 7) / 8), 256, 0, s, 
-                                         rows, k, d, reinterpret_cast<const __nv_bfloat16*>(x), ldx, sel, wts, cursor,
+                                         rows, k, d, reinterpret_cast<const __nv_bfloat16*>(x), ldx, sel, wts, plan,
                                          slot, reinterpret_cast<__nv_bfloat16*>(xg), row_scale));
       return;
     }
   }
   ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_scatter_kernel<T>, static_cast<int>((warps + 7) / 8), 256, 0, s, rows, k, d, x, ldx, sel, wts,
-                                                                                      cursor, slot, xg, row_scale));
+                                                                                      plan, slot, xg, row_scale));
 }
 // h += sum_j yg[slot[r][j]] (as moe_combine4_kernel, same order), then the
 // NEXT op's input from the updated row while it is in registers: the next
@@ -1722,8 +1720,10 @@ template <int NC, class YT>
 __global__ void __launch_bounds__(256) moe_combine_norm_kernel(int rows, int k, int d, const YT* __restrict__ yg,
                                                                const int32_t* __restrict__ slot, float* __restrict__ h,
                                                                int ldh, const float* __restrict__ gain,
-                                                               __nv_bfloat16* __restrict__ out, int ldo) {
+                                                               __nv_bfloat16* __restrict__ out, int ldo,
+                                                               int32_t* __restrict__ zero, int nzero) {
   pdl_begin();
+  if (blockIdx.x == 0 && threadIdx.x < nzero) zero[threadIdx.x] = 0;
   const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (r >= rows) return;
   // every load of a pass is issued before its first use (the row's h segment and
@@ -1772,7 +1772,9 @@ __global__ void __launch_bounds__(256) moe_combine_norm_kernel(int rows, int k, 
 
 template <class YT>
 bool launch_moe_combine_norm(int rows, int k, int d, const YT* yg, const int32_t* slot, float* h, int ldh,
-                             const float* gain, __nv_bfloat16* out, int ldo, cudaStream_t s) {
+                             const float* gain, __nv_bfloat16* out, int ldo, cudaStream_t s, int32_t* zero,
+                             int nzero) {
+  if (nzero > 256) throw std::invalid_argument("moe_combine: at most 256 counters to zero");
   if ((d != 512 && d != 1024) || ldh % 4 || ldo % 4 || reinterpret_cast<uintptr_t>(h) % 16 ||
       reinterpret_cast<uintptr_t>(out) % 16 || (gain && reinterpret_cast<uintptr_t>(gain) % 16) ||
       getenv("ORX_NO_COMBINE_NORM"))
@@ -1781,23 +1783,24 @@ bool launch_moe_combine_norm(int rows, int k, int d, const YT* yg, const int32_t
   const double nb = double(rows) * d * (sizeof(YT) * k + 8.0 + 2.0);  // k expert outputs + residual in/out + bf16 row
   if (d == 1024)
     ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_norm_kernel<8, YT>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
-                                              slot, h, ldh, gain, out, ldo));
+                                              slot, h, ldh, gain, out, ldo, zero, nzero));
   else
     ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_norm_kernel<4, YT>, (rows + 7) / 8, 256, 0, s, rows, k, d, yg,
-                                              slot, h, ldh, gain, out, ldo));
+                                              slot, h, ldh, gain, out, ldo, zero, nzero));
   return true;
 }
 
 template <class YT>
 void launch_moe_combine(int rows, int k, int d, const YT* yg, const int32_t* slot, float* h, int ldh,
-                        cudaStream_t s) {
+                        cudaStream_t s, int32_t* zero, int nzero) {
+  if (nzero > 256) throw std::invalid_argument("moe_combine: at most 256 counters to zero");
   const double nb = double(rows) * d * (sizeof(YT) * k + 8.0);  // k expert outputs + residual in/out
   if (rows <= 0) return;
   if (d % 4 == 0 && ldh % 4 == 0) {
-    ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine4_kernel<YT>, grid_for((long long)rows * d / 4, 256, num_sms() * 8), 256, 0, s, rows, k, d, yg, slot, h, ldh));
+    ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine4_kernel<YT>, grid_for((long long)rows * d / 4, 256, num_sms() * 8), 256, 0, s, rows, k, d, yg, slot, h, ldh, zero, nzero));
     return;
   }
-  ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_kernel<YT>, rows, 256, 0, s, rows, k, d, yg, slot, h, ldh));
+  ORX_LAUNCH_CATB(PROF_MOE_ROUTE, nb, launch_pdl(moe_combine_kernel<YT>, rows, 256, 0, s, rows, k, d, yg, slot, h, ldh, zero, nzero));
 }
 void launch_swiglu_mul(long long n, const float* a, const float* b, float* out, cudaStream_t s) {
   if (n <= 0) return;
@@ -1865,14 +1868,15 @@ void launch_fill_kv_pad(int n_pad, const int32_t* rows, const int32_t* row_user,
                                       int, T*, int, long long, long long, int, cudaStream_t);                      \
   template void launch_dec_self_attn<T>(int, int, int, int, int, int, const T*, T* const*, const int32_t*, int,   \
                                         T*, cudaStream_t);                                                       \
-  template void launch_moe_scatter<T>(int, int, int, const T*, int, const int32_t*, const float*, int32_t*,       \
+  template void launch_moe_scatter<T>(int, int, int, const T*, int, const int32_t*, const float*, const MoePlan&, \
                                       int32_t*, T*, float*, cudaStream_t);                                        \
   template void launch_ep_dispatch<T>(int, int, int, const T*, int, const int32_t*, const float*, int32_t*,       \
                                       int32_t*, const int32_t*, const EpPeers&, cudaStream_t);                               \
   template void launch_ep_return<T>(int, int, const int32_t*, const T*, const EpPeers&, cudaStream_t);           \
-  template void launch_moe_combine<T>(int, int, int, const T*, const int32_t*, float*, int, cudaStream_t);         \
+  template void launch_moe_combine<T>(int, int, int, const T*, const int32_t*, float*, int, cudaStream_t, int32_t*, \
+                                      int);                                                                        \
   template bool launch_moe_combine_norm<T>(int, int, int, const T*, const int32_t*, float*, int, const float*,    \
-                                           __nv_bfloat16*, int, cudaStream_t);
+                                           __nv_bfloat16*, int, cudaStream_t, int32_t*, int);
 INST(float)
 INST(__nv_bfloat16)
 

@@ -94,8 +94,10 @@ void launch_moe_route(int rows, int d, int E, int k, const float* x, int ldx, co
 // `gain`, or a plain bf16 copy when gain is null); false if the shape is not
 // supported (then run launch_moe_combine + the norm / convert).
 template <class YT>
+// zero / nzero (<= 256): counters zeroed by the combine for the next MoE layer
 bool launch_moe_combine_norm(int rows, int k, int d, const YT* yg, const int32_t* slot, float* h, int ldh,
-                             const float* gain, __nv_bfloat16* out, int ldo, cudaStream_t s);
+                             const float* gain, __nv_bfloat16* out, int ldo, cudaStream_t s, int32_t* zero = nullptr,
+                             int nzero = 0);
 // K|V of the empty-history pad key rows when the lifelong fc2 is folded into the
 // QFormer K|V weights (engine build_kv_fold): kv = pad . Wkv [2 nkv] (K then V).
 template <class T>
@@ -120,15 +122,23 @@ void debug_moe_route(int rows, int d, int E, int k, const float* x, const float*
 void launch_moe_route_tc(int rows, int d, int E, int k, const float* x, int ldx, const float* gate_hi,
                          const float* gate_lo, const float* bias, int32_t* sel, float* wts, int32_t* counts,
                          cudaStream_t s);
-void launch_moe_plan(int E, const int32_t* counts, int32_t* seg_cursor, int32_t* tile_expert, int max_tiles,
-                     int32_t* n_mtiles, int tile_rows, cudaStream_t s);
+// The grouped-GEMM plan, computed by the scatter itself from the final routing
+// histogram: expert segments padded to tile_rows, tile_expert / n_mtiles for
+// the grouped GEMMs; fill [E] must be zero (it is zeroed with counts).
+struct MoePlan {
+  const int32_t* counts = nullptr;
+  int32_t* fill = nullptr;
+  int32_t* tile_expert = nullptr;
+  int32_t* n_mtiles = nullptr;
+  int max_tiles = 0, tile_rows = 0, E = 0;
+};
 template <class T>
 void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,
-                        int32_t* seg_cursor, int32_t* slot, T* xg, float* row_scale, cudaStream_t s);
+                        const MoePlan& plan, int32_t* slot, T* xg, float* row_scale, cudaStream_t s);
 // yg: fp32 (fp32 engine) or bf16 (bf16 engine) weighted expert outputs
 template <class YT>
 void launch_moe_combine(int rows, int k, int d, const YT* yg, const int32_t* slot, float* h, int ldh,
-                        cudaStream_t s);
+                        cudaStream_t s, int32_t* zero = nullptr, int nzero = 0);
 
 // ---- expert-parallel exchange over NVLink peer memory (graph-capturable) ----
 // Every rank maps every peer's symmetric exchange region (CUDA IPC); the

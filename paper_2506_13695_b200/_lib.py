@@ -168,7 +168,10 @@ def lib():
             raise ImportError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
                               "(there is no CPU fallback)")
         h = C.CDLL(LIB_PATH)
+        ab = "ORX_LIB_PATH" in os.environ  # A/B timing against an older build: skip entry points it lacks
         for name, res, args in SIGNATURES:
+            if ab and not hasattr(h, name):
+                continue
             f = getattr(h, name)
             f.restype = res
             f.argtypes = args

@@ -1663,9 +1663,12 @@ class EngineT final : public Engine {
     const orx_config& c = cfg_;
     const int d = c.d_model, H = c.n_heads, dh = d / H, Ld = dec_layers(c), Tn = enc_seq_len(c);
     if (c.moe_enabled) zero_moe_counters();
-    launch_dec_embed(rows, d, step == 0 ? bos_ : tokens_[step - 1], step == 0 ? nullptr : codes + (step - 1),
-                     code_stride, h_, st_);
-    bool have_x = false;  // xn_ already holds the next op's input (fused into the MoE combine)
+    const float* emb = step == 0 ? bos_ : tokens_[step - 1];
+    const int32_t* emb_code = step == 0 ? nullptr : codes + (step - 1);
+    bool have_x = false;  // xn_ already holds the next op's input (fused into the MoE combine / embedding)
+    if constexpr (kBf16)
+      have_x = launch_dec_embed_norm(rows, d, emb, emb_code, code_stride, h_, dec_[0].n1, xn_, st_);
+    if (!have_x) launch_dec_embed(rows, d, emb, emb_code, code_stride, h_, st_);
     for (int l = 0; l < Ld; ++l) {
       const DecL& w = dec_[l];
       if (!have_x) launch_rmsnorm<T>(rows, d, h_, d, w.n1, xn_, d, st_);

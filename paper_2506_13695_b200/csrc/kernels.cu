@@ -441,6 +441,38 @@ __global__ void dec_embed_kernel(int rows, int d, const float* table, const int3
   for (int c = threadIdx.x; c < d; c += blockDim.x) h[(size_t)r * d + c] = table[src + c];
 }
 
+// dec_embed + the first decoder layer's RMSNorm in one pass (bf16 engine,
+// d = 128 * NC): warp per row, the embedding row in registers.
+template <int NC>
+__global__ void __launch_bounds__(256) dec_embed_norm_kernel(int rows, int d, const float* __restrict__ table,
+                                                             const int32_t* __restrict__ code, int code_stride,
+                                                             float* __restrict__ h, const float* __restrict__ gain,
+                                                             __nv_bfloat16* __restrict__ out) {
+  pdl_begin();
+  const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  const float4* t4 = reinterpret_cast<const float4*>(table + (code ? (size_t)code[(size_t)r * code_stride] * d : 0));
+  float4 v[NC];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    v[i] = __ldg(t4 + lane + 32 * i);
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  }
+  float4* h4 = reinterpret_cast<float4*>(h + (size_t)r * d);
+#pragma unroll
+  for (int i = 0; i < NC; ++i) h4[lane + 32 * i] = v[i];
+  ss = warp_sum(ss);
+  const float rs = rsqrtf(ss / d + 1e-6f);
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int c = (lane + 32 * i) * 4;
+    const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
+    *reinterpret_cast<uint2*>(out + (size_t)r * d + c) =
+        make_uint2(pack_bf16(v[i].x * rs * g.x, v[i].y * rs * g.y), pack_bf16(v[i].z * rs * g.z, v[i].w * rs * g.w));
+  }
+}
+
 // K / V of position p < step for a row: the K|V columns of that position's
 // QKV GEMM output (kv[p * L + layer], [rows_p][3d]) at the ancestor row.
 template <class T>
@@ -1520,6 +1552,27 @@ void launch_dec_embed(int rows, int d, const float* table, const int32_t* code, 
     throw std::invalid_argument("dec_embed: buffers must be 16-byte aligned");
   ORX_LAUNCH(launch_pdl(dec_embed_kernel, rows, d % 4 == 0 ? std::min(256, d / 4) : 256, 0, s, rows, d, table, code,
                         code_stride, h));
+}
+bool launch_dec_embed_norm(int rows, int d, const float* table, const int32_t* code, int code_stride, float* h,
+                           const float* gain, __nv_bfloat16* out, cudaStream_t s) {
+  if (d % 128 != 0 || d > 1024 || reinterpret_cast<uintptr_t>(table) % 16 || reinterpret_cast<uintptr_t>(h) % 16 ||
+      reinterpret_cast<uintptr_t>(out) % 16 || reinterpret_cast<uintptr_t>(gain) % 16)
+    return false;
+  if (rows <= 0) return true;
+  const int nc = d / 128;
+  const double nb = double(rows) * d * (4.0 + 4.0 + 2.0);
+  auto go = [&](auto kern) {
+    ORX_LAUNCH_CATB(PROF_NORM, nb, launch_pdl(kern, (rows + 7) / 8, 256, 0, s, rows, d, table, code, code_stride, h,
+                                              gain, out));
+  };
+  switch (nc) {
+    case 1: go(dec_embed_norm_kernel<1>); break;
+    case 2: go(dec_embed_norm_kernel<2>); break;
+    case 4: go(dec_embed_norm_kernel<4>); break;
+    case 8: go(dec_embed_norm_kernel<8>); break;
+    default: return false;
+  }
+  return true;
 }
 // bf16 decoder self-attention, one warp per ROW (all heads): lane l owns
 // columns [l * EPL, (l + 1) * EPL) of q / k / v (16-byte loads), a head spans

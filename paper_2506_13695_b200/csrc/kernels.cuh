@@ -75,6 +75,10 @@ void launch_fill_rows(int rows, int cols, const float* src_row, T* out, int ldo,
 // Decoder: h[r] = step == 0 ? bos : tokens[code[r]]
 void launch_dec_embed(int rows, int d, const float* table, const int32_t* code, int code_stride, float* h,
                       cudaStream_t s);
+// bf16: dec_embed and the first decoder layer's RMSNorm (gain) into out in one
+// pass; false if the shape is unsupported (then launch_dec_embed + rmsnorm)
+bool launch_dec_embed_norm(int rows, int d, const float* table, const int32_t* code, int code_stride, float* h,
+                           const float* gain, __nv_bfloat16* out, cudaStream_t s);
 // Decoder causal self-attention over cached positions (policy.cpp:282-283).
 // qkv: [rows][3d] this position's QKV output; kv[p * n_layers + layer]: position p's
 // QKV output [rows_p][3d] (its K|V columns are the cache, nothing is copied);

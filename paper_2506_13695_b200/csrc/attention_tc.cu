@@ -260,6 +260,19 @@ __global__ void __launch_bounds__(192) fmha_tc_kernel(const __grid_constant__ CU
     Tile T;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       if (!tile_at(t, T)) continue;
+      if (T.q0 + q * 32 >= T.qlen) {
+        // no query row of this warp's quadrant is real (the 21-row tail tile of
+        // a 405-row encoder segment, decode step 0): its P rows only feed
+        // output rows that are never stored, so skip the softmax and only keep
+        // the block handshake: one p_full arrival per block, each only after the
+        // previous block's phase completed (an early arrival would count
+        // towards the current phase and release P . V before the real rows)
+        for (int j = 0; j < T.nb; ++j, ++g) {
+          if (g >= 1) mbar_wait(&p_full, (g - 1) & 1);
+          if (lane == 0) mbar_arrive(&p_full);
+        }
+        continue;
+      }
       float m = -FLT_MAX, l = 0.f;
       bool first = true;
       for (int j = 0; j < T.nb; ++j, ++g) {

@@ -700,7 +700,7 @@ class EngineT final : public Engine {
       if (!tc_attn_) q.wkv = pack(hw, {n + ".attn.wk.w", n + ".attn.wv.w"});
       q.wo = pack(hw, {n + ".attn.wo.w"});
       q.gain = up(hw, n + ".norm.gain");
-      q.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b");
+      q.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b", fold_norm_ ? n + ".norm.gain" : "");
       q.fc2 = pack(hw, {n + ".ffn.fc2.w"}, n + ".ffn.fc2.b");
       qblocks_.push_back(q);
     }
@@ -1278,10 +1278,15 @@ class EngineT final : public Engine {
         gemm(keys_, d, q.wkv, sg_.n_keys, epi(kvl_, 2 * d, false));
         launch_attention<T>(U, Nq, H, dh, qproj_, d, kvl_, 2 * d, kvl_ + d, 2 * d, att_, d, qs, ks, os, st_, aflops);
       }
-      gemm(att_, d, q.wo, U * Nq, epi(qo_, d, true));
-      launch_rmsnorm<T>(U * Nq, d, qo_, d, q.gain, xn_, d, st_);
+      // folded norm (fc1 carries the gain) when the GEMMs run on the CTA-pair kernel
+      const bool nfq = fold_norm_ && U * Nq > 128;
+      Epi eo = epi(qo_, d, true);
+      if (nfq) norm_out(eo);
+      gemm(att_, d, q.wo, U * Nq, eo);
+      if (!nfq) launch_rmsnorm<T>(U * Nq, d, qo_, d, fold_norm_ ? ones_ : q.gain, xn_, d, st_);
       Epi e1 = epi(ffh_, c.ffn_hidden, false);
       e1.act = ACT_SILU;
+      if (nfq) norm_in(e1);
       gemm(xn_, d, q.fc1, U * Nq, e1);
       if (last) {
         Epi e2 = epi(z_, d, true);

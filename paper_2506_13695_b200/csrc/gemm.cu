@@ -1009,6 +1009,12 @@ void launch_tc2_mode(int staged, const void* A, int lda, const void* B, int ldb,
         return;
       }
       break;
+    case EPI_XSSQ:
+      if constexpr (BN == 256) {
+        launch_tc2<BN, S, EPI_XSSQ>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+        return;
+      }
+      break;
     case EPI_BIAS | EPI_RESID | EPI_XSSQ:
       if constexpr (BN == 256) {
         launch_tc2<BN, S, EPI_BIAS | EPI_RESID | EPI_XSSQ>(A, lda, B, ldb, M, N, K, epi, grp, stream);
@@ -1105,7 +1111,7 @@ int epi_mode(const Epi& e) {
     case EPI_RS | EPI_BF16: case EPI_RS | EPI_BF16 | EPI_PEER:
     case 0: case EPI_RS: case EPI_RESID: case EPI_BIAS | EPI_RESID: case EPI_BF16: case EPI_BIAS | EPI_BF16:
     case EPI_BIAS | EPI_LEAKY | EPI_BF16: case EPI_BIAS | EPI_SILU | EPI_BF16:
-    case EPI_RESID | EPI_XSSQ: case EPI_BIAS | EPI_RESID | EPI_XSSQ: case EPI_BF16 | EPI_RSQ:
+    case EPI_XSSQ: case EPI_RESID | EPI_XSSQ: case EPI_BIAS | EPI_RESID | EPI_XSSQ: case EPI_BF16 | EPI_RSQ:
     case EPI_BIAS | EPI_SILU | EPI_BF16 | EPI_RSQ:
       return m;
     default:

@@ -499,6 +499,11 @@ class EngineT final : public Engine {
       return hw.get(n + ".expert" + std::to_string(glob[e]) + "." + w + ".w");
     };
     if (kBf16) {
+      // folded RMSNorm (fold_norm_): the pre-MoE norm's gain goes into W1|W3's input
+      // rows; the tokens arrive un-normalised (or gain-free normalised) and are scaled
+      // per row in the SwiGLU epilogue (Epi::row_rsq) or by an explicit ones-gain norm
+      std::vector<float> g(static_cast<size_t>(d), 1.f);
+      if (fold_norm_) g.assign(gain.data.begin(), gain.data.end());
       std::vector<T> w13(static_cast<size_t>(El) * 2 * h * dp, to_t<T>(0.f));
       for (int e = 0; e < El; ++e) {
         if (glob[e] < 0) continue;
@@ -509,8 +514,8 @@ class EngineT final : public Engine {
           size_t r1 = (size_t)e * 2 * h + (j / 128) * 256 + (j % 128);
           size_t r3 = r1 + 128;
           for (int k = 0; k < d; ++k) {
-            w13[r1 * dp + k] = to_t<T>(w1.data[(size_t)k * h + j]);
-            w13[r3 * dp + k] = to_t<T>(w3.data[(size_t)k * h + j]);
+            w13[r1 * dp + k] = to_t<T>(w1.data[(size_t)k * h + j] * g[k]);
+            w13[r3 * dp + k] = to_t<T>(w3.data[(size_t)k * h + j] * g[k]);
           }
         }
       }
@@ -743,7 +748,7 @@ class EngineT final : public Engine {
       xkv.push_back(n + ".cross.wv.w");
       if (c.moe_enabled) e.moe = pack_moe(hw, n + ".moe", n + ".n3.gain");
       else {
-        e.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b");
+        e.fc1 = pack(hw, {n + ".ffn.fc1.w"}, n + ".ffn.fc1.b", fold_norm_ ? n + ".n3.gain" : "");
         e.fc2 = pack(hw, {n + ".ffn.fc2.w"}, n + ".ffn.fc2.b");
       }
       dec_.push_back(e);
@@ -854,6 +859,7 @@ class EngineT final : public Engine {
       tile_expert_ = ar_.alloc<int32_t>(max_tiles_);
       n_mtiles_ = ar_.alloc<int32_t>(1);
       row_scale_ = ar_.alloc<float>(S_);
+      if (fold_norm_) row_rsq_ = ar_.alloc<float>(S_);
       xg_ = ar_.alloc<T>(static_cast<size_t>(S_) * d);
       hg_ = ar_.alloc<T>(static_cast<size_t>(S_) * rup(h, 8));
       yg_ = ar_.alloc<T>(static_cast<size_t>(S_) * d);
@@ -1328,7 +1334,7 @@ class EngineT final : public Engine {
       eo.ld_resid = d;
       if (nf) norm_out(eo);
       gemm(att_, d, l.wo, R, eo);
-      if (!nf) launch_rmsnorm<T>(R, d, z_, d, l.n2, xn_, d, st_);
+      if (!nf) launch_rmsnorm<T>(R, d, z_, d, enc_moe(c) && fold_norm_ ? ones_ : l.n2, xn_, d, st_);
       if (enc_moe(c)) {
         moe(l.moe, xn_, R, z_, l.n2);
       } else {
@@ -1398,7 +1404,7 @@ class EngineT final : public Engine {
   // updated h in the combine pass: RMSNorm(h) with gain `post_gain` into `post`,
   // or a plain bf16 copy when post_gain is null. Returns whether it did.
   bool moe(const MoeW& m, const T* x, int rows, float* h, const float* norm_gain, T* post = nullptr,
-           const float* post_gain = nullptr) {
+           const float* post_gain = nullptr, bool x_unnormed = false) {
     const orx_config& c = cfg_;
     const int d = c.d_model, E = c.n_experts, k = c.experts_active;
     // counts_ (histogram | scatter fill) is zero here: zeroed once per forward pass
@@ -1420,8 +1426,15 @@ class EngineT final : public Engine {
     plan.max_tiles = max_tiles_;
     plan.tile_rows = kMoeTile;
     plan.E = E;
+    if (x_unnormed) {  // x = bf16(h) with ssq_ partials (norm_out): per-grouped-row scales for W1|W3
+      plan.ssq = ssq_;
+      plan.ssq_ld = ssq_ld_;
+      plan.ssq_n = 2 * d / 256;
+      plan.inv_d = 1.f / d;
+      plan.row_rsq = row_rsq_;
+    }
     launch_moe_scatter<T>(rows, k, d, x, d, sel_, wts_, plan, slot_, xg_, row_scale_, st_);
-    expert_ffn(m, static_cast<int>(S_), static_cast<long long>(rows) * k);
+    expert_ffn(m, static_cast<int>(S_), static_cast<long long>(rows) * k, false, x_unnormed ? row_rsq_ : nullptr);
     if constexpr (kBf16) {
       if (post && launch_moe_combine_norm(rows, k, d, yg_, slot_, h, d, post_gain, post, d, st_, counts_, 2 * E))
         return true;
@@ -1471,7 +1484,7 @@ class EngineT final : public Engine {
   // yg_ = row_scale * W2(silu(W1 x) * W3 x)  (swiglu, nn.cpp:75-86; weight nn.cpp:167-168)
   // peer: expert-parallel (bf16) -- the W2 epilogue stores every output row
   // straight into its token rank's return buffer (ep_.src codes, ep_.yr views).
-  void expert_ffn(const MoeW& m, int M, long long algo_rows, bool peer = false) {
+  void expert_ffn(const MoeW& m, int M, long long algo_rows, bool peer = false, const float* row_rsq = nullptr) {
     const orx_config& c = cfg_;
     const int d = c.d_model, he = expert_hidden(c), hp = rup(he, 8);
     Grouped g;
@@ -1483,6 +1496,7 @@ class EngineT final : public Engine {
     if constexpr (kBf16) {
       Epi e1 = epi(hg_, hp, false);
       e1.swiglu = 1;
+      e1.row_rsq = row_rsq;
       e1.n_out = he;
       e1.m_valid = M;
       g.b_rows_per_expert = 2 * he;
@@ -1706,12 +1720,19 @@ class EngineT final : public Engine {
         launch_attention<T>(groups, max_group_rows, H, dh, qkv_, d, xkv_ + (size_t)l * 2 * d, ldkv,
                             xkv_ + (size_t)l * 2 * d + d, ldkv, att_, d, gq, gk, gq, st_, 4.0 * rows * Tn * d);
       }
-      gemm(att_, d, w.co, rows, e);
-      launch_rmsnorm<T>(rows, d, h_, d, w.n3, xn_, d, st_);
+      // folded n3 (FFN fc1 / MoE W1|W3 carry its gain): co writes bf16(h) and its sums of
+      // squares; fc1 scales rows, the MoE scatter hands each grouped row its scale to the
+      // SwiGLU epilogue (expert-parallel: an explicit gain-free norm before the dispatch)
+      static const bool no_n3 = getenv("ORX_NO_N3_FOLD") != nullptr;  // A/B
+      const bool nf3 = fold_norm_ && rows > 128 && (!c.moe_enabled || ep_world_ == 1) && !no_n3;
+      Epi e3 = e;
+      if (nf3) norm_out(e3);
+      gemm(att_, d, w.co, rows, e3);
+      if (!nf3) launch_rmsnorm<T>(rows, d, h_, d, fold_norm_ ? ones_ : w.n3, xn_, d, st_);
       if (c.moe_enabled)  // next layer's n1 norm (or the head's bf16 copy) fused into the combine
-        have_x = moe(w.moe, xn_, rows, h_, w.n3, xn_, l + 1 < Ld ? dec_[l + 1].n1 : nullptr);
+        have_x = moe(w.moe, xn_, rows, h_, w.n3, xn_, l + 1 < Ld ? dec_[l + 1].n1 : nullptr, nf3);
       else
-        ffn(w.fc1, w.fc2, xn_, rows, h_);
+        ffn(w.fc1, w.fc2, xn_, rows, h_, nf3);
     }
     (void)Tn;
     // position_logits: no final norm (policy.cpp:290-295)
@@ -2261,6 +2282,7 @@ class EngineT final : public Engine {
           *n_mtiles_ = nullptr;
   float *wts_ = nullptr, *row_scale_ = nullptr, *ga_ = nullptr, *gb_ = nullptr;
   T* yg_ = nullptr;  // weighted expert outputs (bf16 in the bf16 engine)
+  float* row_rsq_ = nullptr;  // folded pre-MoE RMSNorm: scale of every grouped row
   T *xg_ = nullptr, *hg_ = nullptr;
   // expert parallelism
   int ep_rank_ = 0, ep_world_ = 1, El_ = 0;  // El_: local expert slots per MoE layer

@@ -427,6 +427,7 @@ __device__ __forceinline__ void epilogue_tile_swiglu_staged(const Epi& e, float*
   constexpr int CP = BN / 64 / 2;  // 32-column output chunks per warp
   const int lane = threadIdx.x & 31, sub = lane >> 3, q = lane & 7;
   const int orow = row < e.m_valid ? (e.row_map ? e.row_map[row] : row) : -1;
+  const float rr = e.row_rsq && row < e.m_valid ? e.row_rsq[row] : 1.f;  // folded RMSNorm scale of this row
   int orr[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) orr[k] = __shfl_sync(0xffffffffu, orow, 4 * k + sub);
@@ -445,7 +446,8 @@ __device__ __forceinline__ void epilogue_tile_swiglu_staged(const Epi& e, float*
     for (int k = 0; k < 8; ++k) {
       float v[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = silu_fast(__uint_as_float(ra[4 * k + j])) * __uint_as_float(rb[4 * k + j]);
+      for (int j = 0; j < 4; ++j)
+        v[j] = silu_fast(__uint_as_float(ra[4 * k + j]) * rr) * (__uint_as_float(rb[4 * k + j]) * rr);
       s4[lane * 8 + (k ^ (lane & 7))] = make_float4(v[0], v[1], v[2], v[3]);
     }
     __syncwarp();
@@ -1260,6 +1262,8 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
       throw std::invalid_argument("gemm_bf16: head statistics need full, aligned 256-column tiles");
     if ((ep.out2 || ep.rsq) && (staged < 0 || small_n))
       throw std::invalid_argument("gemm_bf16: the folded RMSNorm needs the staged 256-wide epilogue");
+    if (ep.row_rsq && staged != (EPI_SWIGLU | EPI_BF16))
+      throw std::invalid_argument("gemm_bf16: per-row RMSNorm scales need the staged SwiGLU epilogue");
     if (ep.peer_code && staged < 0)
       throw std::invalid_argument("gemm_bf16: peer-scattered rows need the staged epilogue (full 128-column tiles)");
     if (small_n)
@@ -1270,6 +1274,7 @@ void gemm_bf16(const void* A, int lda, const void* B, int ldb, int M, int N, int
     if (ep.stats) throw std::invalid_argument("gemm_bf16: head statistics need the CTA-pair kernel (M > 128)");
     if (ep.out2 || ep.rsq) throw std::invalid_argument("gemm_bf16: the folded RMSNorm needs the CTA-pair kernel");
     if (ep.peer_code) throw std::invalid_argument("gemm_bf16: peer-scattered rows need the CTA-pair kernel");
+    if (ep.row_rsq) throw std::invalid_argument("gemm_bf16: per-row RMSNorm scales need the CTA-pair kernel");
     // M <= 128 (decoder step 0): the GEMM is a weight stream; 64-wide tiles put
     // 4x more SMs on it than 256-wide ones (N=1024: 16 CTAs instead of 4)
     const bool narrow = !epi.swiglu && !grouped && N >= 512 && M <= kBM && !getenv("ORX_GEMM_NO_NARROW");

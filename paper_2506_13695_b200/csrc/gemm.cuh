@@ -32,6 +32,9 @@ constexpr int kEpiMaxPeers = 8;
 struct Epi {
   const float* bias = nullptr;       // [N] (or [N/2] for swiglu: not used)
   const float* row_scale = nullptr;  // [M] per-row multiplier
+  // SwiGLU only (the grouped W1|W3 GEMM): per-row pre-scale of both halves,
+  // rsqrt(mean(x^2) + eps) of the un-normalised token row (folded pre-MoE RMSNorm)
+  const float* row_rsq = nullptr;
   const float* resid = nullptr;      // fp32 [rows, ld_resid], indexed by output row
   void* out = nullptr;               // [rows, ldo]
   const int* row_map = nullptr;      // output row = row_map[r] (< 0: dropped)

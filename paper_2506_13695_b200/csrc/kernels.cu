@@ -1045,6 +1045,11 @@ __global__ void moe_scatter_kernel(int rows, int k, int d, const T* __restrict__
   if (lane == 0) {
     slot[gw] = s;
     row_scale[s] = wts[gw];
+    if (plan.row_rsq) {
+      float ss = 0.f;
+      for (int i = 0; i < plan.ssq_n; ++i) ss += plan.ssq[(long long)i * plan.ssq_ld + r];
+      plan.row_rsq[s] = rsqrtf(ss * plan.inv_d + 1e-6f);
+    }
   }
   const T* src = x + (size_t)r * ldx;
   T* dst = xg + (size_t)s * d;
@@ -1084,6 +1089,12 @@ __global__ void __launch_bounds__(256) moe_scatter32_kernel(int rows, int k, int
   if (on) {
     slot[gw] = my_slot;
     row_scale[my_slot] = wts[gw];
+    if (plan.row_rsq) {
+      const int r = gw / k;
+      float ss = 0.f;
+      for (int i = 0; i < plan.ssq_n; ++i) ss += plan.ssq[(long long)i * plan.ssq_ld + r];
+      plan.row_rsq[my_slot] = rsqrtf(ss * plan.inv_d + 1e-6f);
+    }
   }
   for (int i = 0; i < 32; ++i) {
     if (!((act >> i) & 1u)) break;

@@ -135,6 +135,13 @@ struct MoePlan {
   int32_t* tile_expert = nullptr;
   int32_t* n_mtiles = nullptr;
   int max_tiles = 0, tile_rows = 0, E = 0;
+  // optional folded pre-MoE RMSNorm: the token rows are un-normalised; every
+  // grouped row gets rsqrt(sum_i ssq[i][token] / d + 1e-6) in row_rsq
+  const float* ssq = nullptr;
+  long long ssq_ld = 0;
+  int ssq_n = 0;
+  float inv_d = 0.f;
+  float* row_rsq = nullptr;
 };
 template <class T>
 void launch_moe_scatter(int rows, int k, int d, const T* x, int ldx, const int32_t* sel, const float* wts,

@@ -293,7 +293,7 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
   }
   if (MODE & EPI_RESID) {
     if (orow >= 0)  // this row's residual segment into L2 while the MMAs run
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(e.resid + (size_t)resid_row(e, orow) * e.ld_resid +
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(e.resid + (size_t)((MODE & EPI_RMOD) ? orow % e.resid_mod : orow) * e.ld_resid +
                                                                        nt * BN + half * CH * 32),
                    "r"(CH * 128)
                    : "memory");
@@ -306,7 +306,7 @@ __device__ __forceinline__ void epilogue_tile_staged(const Epi& e, float* stg, u
     const int col0 = nt * BN + (half * CH + i) * 32;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      dst[k] = orr[k] >= 0 ? __ldg(reinterpret_cast<const float4*>(e.resid + (size_t)resid_row(e, orr[k]) * e.ld_resid + col0) + q)
+      dst[k] = orr[k] >= 0 ? __ldg(reinterpret_cast<const float4*>(e.resid + (size_t)((MODE & EPI_RMOD) ? orr[k] % e.resid_mod : orr[k]) * e.ld_resid + col0) + q)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
   };
   if (MODE & EPI_RESID) load_resid(0, rr[0]);
@@ -997,6 +997,9 @@ void launch_tc2_mode(int staged, const void* A, int lda, const void* B, int ldb,
       return;
     case EPI_RESID: launch_tc2<BN, S, EPI_RESID>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
     case EPI_BIAS | EPI_RESID: launch_tc2<BN, S, EPI_BIAS | EPI_RESID>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
+    case EPI_BIAS | EPI_RESID | EPI_RMOD:
+      launch_tc2<BN, S, EPI_BIAS | EPI_RESID | EPI_RMOD>(A, lda, B, ldb, M, N, K, epi, grp, stream);
+      return;
     case EPI_BF16: launch_tc2<BN, S, EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
     case EPI_BIAS | EPI_BF16: launch_tc2<BN, S, EPI_BIAS | EPI_BF16>(A, lda, B, ldb, M, N, K, epi, grp, stream); return;
     case EPI_BIAS | EPI_LEAKY | EPI_BF16:
@@ -1109,8 +1112,9 @@ int epi_mode(const Epi& e) {
   }
   if (e.rsq) m |= EPI_RSQ;
   if (e.peer_code) m |= EPI_PEER;
+  if (e.resid && e.resid_mod > 0) m |= EPI_RMOD;
   switch (m) {
-    case EPI_RS | EPI_BF16: case EPI_RS | EPI_BF16 | EPI_PEER:
+    case EPI_RS | EPI_BF16: case EPI_RS | EPI_BF16 | EPI_PEER: case EPI_BIAS | EPI_RESID | EPI_RMOD:
     case 0: case EPI_RS: case EPI_RESID: case EPI_BIAS | EPI_RESID: case EPI_BF16: case EPI_BIAS | EPI_BF16:
     case EPI_BIAS | EPI_LEAKY | EPI_BF16: case EPI_BIAS | EPI_SILU | EPI_BF16:
     case EPI_XSSQ: case EPI_RESID | EPI_XSSQ: case EPI_BIAS | EPI_RESID | EPI_XSSQ: case EPI_BF16 | EPI_RSQ:

@@ -25,7 +25,8 @@ enum EpiMode {
   EPI_STATS = 256,    // fp32 out + per-(row, 32-column chunk) log-sum-exp statistics (the head GEMM)
   EPI_XSSQ = 512,     // residual producers: also a bf16 copy of the output and per-row sum-of-squares partials
   EPI_RSQ = 1024,     // consumers: accumulator pre-scaled by rsqrt(mean(x^2) + eps) from those partials
-  EPI_PEER = 2048     // rows scattered to peer memory: row r -> peer_out[code >> 24] + (code & 0xFFFFFF) * ldo
+  EPI_PEER = 2048,    // rows scattered to peer memory: row r -> peer_out[code >> 24] + (code & 0xFFFFFF) * ldo
+  EPI_RMOD = 4096     // residual row = output row % resid_mod (a per-position residual table)
 };
 constexpr int kEpiMaxPeers = 8;
 

@@ -319,6 +319,8 @@ def main():
                     help="load-balanced expert placement: at most this many replicated experts per MoE layer, "
                          "from the expert loads of one calibration request on other users "
                          "(default n_experts / N; -1 = contiguous expert blocks, no calibration)")
+    ap.add_argument("--ep-min-replicas", type=int, default=0,
+                    help="replicate at least this many of each MoE layer's hottest experts (less NVLink traffic)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     lens = tuple(int(x) for x in args.lens.split(","))
@@ -361,11 +363,12 @@ def main():
             cb, cn = _shard(rank, world, args.users)
             calib = P.SynthBatch(7, 1_000_000 + cb, cn, *lens)
             model.beam_search_arrays(calib, args.width)
-            owner, pred = P.ep_place(model.expert_load(), world, reps)
+            owner, pred = P.ep_place(model.expert_load(), world, reps, min(args.ep_min_replicas, reps))
             del model
             model = ep_model(owner)
             ep_info = {"placement": "load-balanced (calibration: 1 request, other users, seed 7)",
-                       "max_replicas": reps, "replicated_per_layer": float((owner < 0).sum(axis=1).mean()),
+                       "max_replicas": reps, "min_replicas": min(args.ep_min_replicas, reps),
+                       "replicated_per_layer": float((owner < 0).sum(axis=1).mean()),
                        "predicted_busiest_over_mean": [round(float(x), 3) for x in pred]}
         else:
             ep_info = {"placement": "contiguous expert blocks"}

@@ -172,13 +172,15 @@ int orx_weights_create_random_ep_placed(const orx_config* cfg, int32_t ep_rank, 
  * n_experts]; identical on every expert-parallel rank (zeros otherwise). */
 int orx_engine_expert_load(orx_engine* e, int64_t* load_out, int32_t reset);
 /* Load-balanced placement from such loads (csrc/ep_plan.hpp
- * ep_place_balanced): per layer the fewest heaviest experts (at most
- * max_replicas) are replicated such that the rest, packed heaviest-first onto
- * the least-loaded rank, leave the busiest rank within 5% of the mean (else
- * the best found). predicted_imbalance [moe_layers] (optional) = busiest /
- * mean rank load under that placement. Deterministic. */
-int orx_ep_place(const int64_t* load, int32_t layers, int32_t n_experts, int32_t world, int32_t max_replicas,
-                 int32_t* owner_out, double* predicted_imbalance);
+ * ep_place_balanced): per layer the fewest heaviest experts (between
+ * min_replicas and max_replicas) are replicated such that the rest, packed
+ * heaviest-first onto the least-loaded rank and refined by moves / swaps, leave
+ * the busiest rank within 5% of the mean (else the best found); replicated
+ * experts' rows stay on their token's rank, so min_replicas > 0 trades expert
+ * memory for NVLink traffic. predicted_imbalance [moe_layers] (optional) =
+ * busiest / mean rank load under that placement. Deterministic. */
+int orx_ep_place(const int64_t* load, int32_t layers, int32_t n_experts, int32_t world, int32_t min_replicas,
+                 int32_t max_replicas, int32_t* owner_out, double* predicted_imbalance);
 
 /* z_out (host, optional): [n_users * enc_seq_len * d_model] fp32. */
 int orx_encode(orx_engine* e, const orx_user_batch* batch, float* z_out);

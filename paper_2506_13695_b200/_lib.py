@@ -119,7 +119,7 @@ SIGNATURES = [
     ("orx_engine_create_ep_placed", C.c_int, [_P, C.c_int, C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_uint8),
                                               C.c_int32, C.c_int32, _I32P, C.POINTER(_P)]),
     ("orx_engine_expert_load", C.c_int, [_P, C.POINTER(C.c_int64), C.c_int32]),
-    ("orx_ep_place", C.c_int, [C.POINTER(C.c_int64), C.c_int32, C.c_int32, C.c_int32, C.c_int32, _I32P,
+    ("orx_ep_place", C.c_int, [C.POINTER(C.c_int64), C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _I32P,
                                C.POINTER(C.c_double)]),
     ("orx_encode", C.c_int, [_P, C.POINTER(orx_user_batch), _F32P]),
     ("orx_next_logits", C.c_int, [_P, _F32P, C.c_int32, C.c_int32, _I32P, _I32P, _I32P, _F32P]),

@@ -144,13 +144,14 @@ int orx_weights_create_random_ep_placed(const orx_config* cfg, int32_t ep_rank, 
 
 int32_t orx_config_moe_layers(const orx_config* cfg) { return cfg ? orx::moe_layers(*cfg) : 0; }
 
-int orx_ep_place(const int64_t* load, int32_t layers, int32_t n_experts, int32_t world, int32_t max_replicas,
-                 int32_t* owner_out, double* predicted_imbalance) {
+int orx_ep_place(const int64_t* load, int32_t layers, int32_t n_experts, int32_t world, int32_t min_replicas,
+                 int32_t max_replicas, int32_t* owner_out, double* predicted_imbalance) {
   return guarded([&] {
     need(load, "load");
     need(owner_out, "owner_out");
     std::vector<double> pred;
-    const orx::EpPlacement p = orx::ep_place_balanced(load, layers, n_experts, world, max_replicas, 1.05, &pred);
+    const orx::EpPlacement p =
+        orx::ep_place_balanced(load, layers, n_experts, world, max_replicas, 1.05, &pred, min_replicas);
     p.validate();
     std::copy(p.owner.begin(), p.owner.end(), owner_out);
     if (predicted_imbalance) std::copy(pred.begin(), pred.end(), predicted_imbalance);

@@ -84,17 +84,19 @@ struct EpPlacement {
 
 // Load-balanced placement from per-layer expert loads (rows routed to each
 // expert, summed over every rank and some calls; EngineT accumulates them).
-// Per layer, for r = 0 .. max_replicas: the r heaviest experts are replicated
+// Per layer, for r = min_replicas .. max_replicas: the r heaviest experts are replicated
 // (their load splits evenly over the ranks, as the token batches do) and the
 // rest are packed onto the ranks heaviest-first, each to the least-loaded rank
 // with a free slot (at most ceil((E - r) / W) + 1 owned experts per rank),
 // then refined by moves / swaps that lower the busiest rank's load; the first
 // r whose busiest rank is within `tolerance` of the mean wins, else the best
-// r. Deterministic: every rank computes the same placement from the same
-// (all-gathered) loads.
+// r. A replicated expert's rows never cross NVLink, so min_replicas > 0
+// trades expert memory for exchange traffic. Deterministic: every rank
+// computes the same placement from the same (all-gathered) loads.
 inline EpPlacement ep_place_balanced(const int64_t* load, int layers, int E, int W, int max_replicas,
-                                     double tolerance = 1.05, std::vector<double>* predicted = nullptr) {
-  if (W < 1 || E < 1 || E > 32 || layers < 0 || max_replicas < 0)
+                                     double tolerance = 1.05, std::vector<double>* predicted = nullptr,
+                                     int min_replicas = 0) {
+  if (W < 1 || E < 1 || E > 32 || layers < 0 || max_replicas < 0 || min_replicas < 0 || min_replicas > max_replicas)
     throw std::invalid_argument("ep_place: bad layers / experts / world / replicas");
   EpPlacement p;
   p.layers = layers, p.E = E, p.W = W;
@@ -110,7 +112,7 @@ inline EpPlacement ep_place_balanced(const int64_t* load, int layers, int E, int
     const double mean = total / W;
     std::vector<int32_t> best;
     double best_imb = 1e300;
-    for (int r = 0; r <= std::min(max_replicas, E); ++r) {
+    for (int r = std::min(min_replicas, E); r <= std::min(max_replicas, E); ++r) {
       std::vector<int32_t> own(E, -1);
       std::vector<double> rank_load(W, 0.0);
       std::vector<int> n_owned(W, 0);

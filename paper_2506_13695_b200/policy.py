@@ -369,7 +369,7 @@ def _placement(cfg: PolicyConfig, owner) -> np.ndarray:
     return own
 
 
-def ep_place(load, world: int, max_replicas: int):
+def ep_place(load, world: int, max_replicas: int, min_replicas: int = 0):
     """Load-balanced expert placement (csrc/ep_plan.hpp ep_place_balanced)
     from per-layer expert loads [moe_layers, n_experts] (PolicyModel.expert_load):
     returns (owner [moe_layers, n_experts] int32, predicted busiest/mean rank load per layer)."""
@@ -378,7 +378,8 @@ def ep_place(load, world: int, max_replicas: int):
         raise ValueError("load must be [moe_layers, n_experts]")
     owner = np.empty(ld.shape, dtype=np.int32)
     pred = np.empty(ld.shape[0], dtype=np.float64)
-    check(lib().orx_ep_place(ld.ctypes.data_as(C.POINTER(C.c_int64)), ld.shape[0], ld.shape[1], world, max_replicas,
+    check(lib().orx_ep_place(ld.ctypes.data_as(C.POINTER(C.c_int64)), ld.shape[0], ld.shape[1], world, min_replicas,
+                             max_replicas,
                              owner.ctypes.data_as(C.POINTER(C.c_int32)), pred.ctypes.data_as(C.POINTER(C.c_double))))
     return owner, pred
 

@@ -218,6 +218,15 @@ def test_ep_place_balances_and_replicates_hot_experts():
     # no replicas allowed: plain packing, still no worse than contiguous blocks
     owner0, _ = P.ep_place(load, world, 0)
     assert (owner0 >= 0).all()
+    # at least 3 replicated (the hottest) per layer: fewer rows cross NVLink
+    owner3, pred3 = P.ep_place(load, world, 6, min_replicas=3)
+    for li in range(layers):
+        rep = np.flatnonzero(owner3[li] < 0)
+        assert len(rep) >= 3
+        hottest = np.argsort(-load[li], kind="stable")[:len(rep)]
+        assert set(rep) == set(hottest.tolist())
+    with pytest.raises(Exception):
+        P.ep_place(load, world, 2, min_replicas=3)
 
 
 def test_placed_weights_materialise_the_computed_experts():

@@ -319,8 +319,9 @@ def main():
                     help="load-balanced expert placement: at most this many replicated experts per MoE layer, "
                          "from the expert loads of one calibration request on other users "
                          "(default n_experts / N; -1 = contiguous expert blocks, no calibration)")
-    ap.add_argument("--ep-min-replicas", type=int, default=0,
-                    help="replicate at least this many of each MoE layer's hottest experts (less NVLink traffic)")
+    ap.add_argument("--ep-min-replicas", type=int, default=2,
+                    help="replicate at least this many of each MoE layer's hottest experts (less NVLink traffic, "
+                         "more expert memory per GPU; the line reports expert_slots_per_gpu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     lens = tuple(int(x) for x in args.lens.split(","))
@@ -369,6 +370,9 @@ def main():
             ep_info = {"placement": "load-balanced (calibration: 1 request, other users, seed 7)",
                        "max_replicas": reps, "min_replicas": min(args.ep_min_replicas, reps),
                        "replicated_per_layer": float((owner < 0).sum(axis=1).mean()),
+                       "expert_slots_per_gpu": int(max(((owner == q) | (owner < 0)).sum(axis=1).max()
+                                                       for q in range(world))),
+                       "experts_per_layer": int(pcfg.n_experts),
                        "predicted_busiest_over_mean": [round(float(x), 3) for x in pred]}
         else:
             ep_info = {"placement": "contiguous expert blocks"}

@@ -855,6 +855,12 @@ class EngineT final : public Engine {
       wts_ = ar_.alloc<float>(mrows * k);
       slot_ = ar_.alloc<int32_t>(mrows * k);
       counts_ = ar_.alloc<int32_t>(2 * static_cast<size_t>(E));  // routing histogram | scatter fill counters
+      if constexpr (kBf16) {  // split-K tensor-pipe router: per-(tile, K half) partials and tile tickets
+        route_part_ = ar_.alloc<float>(moe_route_tc_scratch_floats(static_cast<int>(mrows)));
+        const size_t nt = static_cast<size_t>((mrows + 127) / 128);
+        route_ticket_ = ar_.alloc<int32_t>(nt);
+        CUDA_CHECK(cudaMemset(route_ticket_, 0, nt * 4));
+      }
       cursor_ = ar_.alloc<int32_t>(E);
       tile_expert_ = ar_.alloc<int32_t>(max_tiles_);
       n_mtiles_ = ar_.alloc<int32_t>(1);
@@ -1412,7 +1418,8 @@ class EngineT final : public Engine {
     // tensor-pipe router for large row counts (one 128-row tile per SM is latency-bound: the SIMT
     // router is faster below a few thousand rows)
     if (m.gate_hi && rows >= 4096)
-      launch_moe_route_tc(rows, d, E, k, h, d, m.gate_hi, m.gate_lo, m.bias, sel_, wts_, counts_, st_);
+      launch_moe_route_tc(rows, d, E, k, h, d, m.gate_hi, m.gate_lo, m.bias, sel_, wts_, counts_, route_part_,
+                          route_ticket_, st_);
     else
       launch_moe_route(rows, d, E, k, h, d, norm_gain, m.gate_t, m.gate_gain, m.bias, sel_, wts_, counts_, st_,
                        m.gate_sw);
@@ -2283,6 +2290,8 @@ class EngineT final : public Engine {
   float *wts_ = nullptr, *row_scale_ = nullptr, *ga_ = nullptr, *gb_ = nullptr;
   T* yg_ = nullptr;  // weighted expert outputs (bf16 in the bf16 engine)
   float* row_rsq_ = nullptr;  // folded pre-MoE RMSNorm: scale of every grouped row
+  float* route_part_ = nullptr;      // tensor-pipe router: K-half partial scores
+  int32_t* route_ticket_ = nullptr;  // tensor-pipe router: per-tile arrival tickets
   T *xg_ = nullptr, *hg_ = nullptr;
   // expert parallelism
   int ep_rank_ = 0, ep_world_ = 1, El_ = 0;  // El_: local expert slots per MoE layer

@@ -123,9 +123,12 @@ void gate_tf32_split(const float* gate, int E, int d, float* hi, float* lo);
 // 2 = moe_route_tc (3xTF32 tensor pipe).
 void debug_moe_route(int rows, int d, int E, int k, const float* x, const float* gate, const float* bias,
                      int variant, int32_t* sel, float* wts);
+// part: moe_route_tc_scratch_floats(max rows) floats; ticket: one int per 128-row
+// tile, zero before the first call (the kernel leaves it zero)
+size_t moe_route_tc_scratch_floats(int max_rows);
 void launch_moe_route_tc(int rows, int d, int E, int k, const float* x, int ldx, const float* gate_hi,
                          const float* gate_lo, const float* bias, int32_t* sel, float* wts, int32_t* counts,
-                         cudaStream_t s);
+                         float* part, int32_t* ticket, cudaStream_t s);
 // The grouped-GEMM plan, computed by the scatter itself from the final routing
 // histogram: expert segments padded to tile_rows, tile_expert / n_mtiles for
 // the grouped GEMMs; fill [E] must be zero (it is zeroed with counts).

@@ -3,25 +3,27 @@
 // keeps fp32-grade scores (moe_forward, nn.cpp:117-147):
 //   x = x_hi + x_lo, w = w_hi + w_lo (x_hi, w_hi tf32-exact, x_lo = x - x_hi)
 //   x.w ~= x_hi.w_hi + x_lo.w_hi + x_hi.w_lo     (dropped term ~2^-21 relative)
-// One CTA per SM walks 128-row tiles of h (fp32, the residual stream):
+// Split-K over two CTAs per 128-row tile (work item = tile x K half), two
+// CTAs per SM: a single CTA walking all 32 K blocks of its tile was bound by
+// the serial latency of its stage ring (23 us for the TMA / barrier skeleton
+// alone at 16384 rows), so each half runs its 16 K blocks concurrently.
 //   warp 0    TMA: h tile (128 rows x 32 fp32, 128-byte swizzled rows) and the
-//             pre-split gate (32 expert rows x 32) per K block, 7-stage ring
-//             (the kernel is bound by HBM latency: 112 KB of h in flight per SM)
+//             pre-split gate (32 expert rows x 32) per K block, 3-stage ring
 //   warps 2-5 thread = row: split the staged fp32 row into tf32 hi (in place)
-//             and lo (a 2-deep ring of its own, so a stage is 24 KB and the
-//             ring deep), accumulate the row's sum of squares; at
-//             the end of the tile read the row's 32 scores from TMEM, scale by
-//             rsqrt(mean(x^2) + eps), stable top-k by score + bias (ties ->
-//             lower id, nn.cpp:127-136), softmax over the selected raw scores
+//             and lo (a 2-deep ring of its own), accumulate the row's partial
+//             sum of squares; at the end of the half read the row's 32 partial
+//             scores from TMEM and store them (with the partial sum) to a
+//             scratch slot; the second CTA of the tile to finish (atomic
+//             ticket) adds the other half's partials in a fixed order
+//             (half 0 + half 1), scales by rsqrt(mean(x^2) + eps), and does
+//             the stable top-k by score + bias (ties -> lower id,
+//             nn.cpp:127-136), softmax over the selected raw scores
 //             (nn.cpp:139-147), ids ascending
 //   warp 1    one thread issues tcgen05.mma kind::tf32 (M=128, N=32, K=8), three
-//             per K step, into six TMEM accumulators per tile (term x K-step
-//             parity: a chain of 384 dependent N=32 MMAs into one accumulator
-//             is latency-bound), double-buffered across tiles; the epilogue
-//             sums the six
+//             per K step (one TMEM accumulator per term), double-buffered
+//             across work items
 // The h tile is read once from HBM (4 d bytes per row); the per-row work is
-// ~30 instructions per 32 columns, so the kernel runs at the HBM rate instead
-// of the shared-memory bound of a SIMT 24-expert dot product.
+// ~30 instructions per 32 columns.
 #include <cfloat>
 #include <cstring>
 #include <stdexcept>
@@ -39,9 +41,10 @@ namespace {
 constexpr int kRtBM = 128;      // rows per tile
 constexpr int kRtBK = 32;       // fp32 columns per K block (128-byte rows)
 constexpr int kRtN = 32;        // expert slots (E <= 32)
-constexpr int kRtStages = 6;
-constexpr int kRtAcc = 6;                     // accumulators per tile (3 terms x 2 K-step parities)
-constexpr int kRtLo = 4;                      // lo ring depth
+constexpr int kRtStages = 3;
+constexpr int kRtAcc = 3;                     // accumulators per work item (3 terms)
+constexpr int kRtLo = 2;                      // lo ring depth
+constexpr int kRtPart = 33;                   // partial scores (32) + partial sum of squares per row
 constexpr uint32_t kRtA = kRtBM * kRtBK * 4;  // 16 KB
 constexpr uint32_t kRtB = kRtN * kRtBK * 4;   // 4 KB
 constexpr uint32_t kRtStage = kRtA + 2 * kRtB;  // A (hi in place) + B hi + B lo
@@ -64,11 +67,11 @@ ORX_DEV void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint
 }
 ORX_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, 2)
     moe_route_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmBh,
                         const __grid_constant__ CUtensorMap tmBl, int rows, int d, int E, int k,
                         const float* __restrict__ bias, int32_t* __restrict__ sel, float* __restrict__ wts,
-                        int32_t* __restrict__ counts) {
+                        int32_t* __restrict__ counts, float* __restrict__ part, int32_t* __restrict__ ticket) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* lo_ring = smem + kRtStages * kRtStage;
@@ -80,6 +83,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* acc_empty = acc_full + 2;       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   int* hist = reinterpret_cast<int*>(tmem_slot + 4);  // [32]
+  int* last_flag = hist + 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRtStages; ++s) {
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&tmBl);
   }
   if (threadIdx.x < 32) hist[threadIdx.x] = 0;
-  if (warp == 1) tmem_alloc(tmem_slot, 512);  // 2 tiles x 6 accumulators x 32 columns
+  if (warp == 1) tmem_alloc(tmem_slot, 256);  // 2 work items x 3 accumulators x 32 columns
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -106,20 +110,24 @@ __global__ void __launch_bounds__(192, 1)
   pdl_begin();
   const int tiles = (rows + kRtBM - 1) / kRtBM;
   const int kblocks = d / kRtBK;
+  const int items = 2 * tiles;  // (tile, K half)
+  auto kb_begin = [&](int half) { return half ? kblocks / 2 : 0; };
+  auto kb_end = [&](int half) { return half ? kblocks : kblocks / 2; };
 
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_x = l2_policy_evict_first(), pol_b = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        for (int kb = 0; kb < kblocks; ++kb) {
+      for (int w = blockIdx.x; w < items; w += gridDim.x) {
+        const int t = w >> 1, k0 = kb_begin(w & 1), nk = kb_end(w & 1) - k0;
+        for (int i = 0; i < nk; ++i) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * kRtStage;
           mbar_arrive_expect_tx(&full[stage], kRtA + 2 * kRtB);
           // K blocks in a per-CTA rotated order: in lockstep every CTA would read the
-          // same 8 KB of the gate at the same time (one L2 hot spot for 128 readers)
-          const int kr = (kb + blockIdx.x) % kblocks;
+          // same 8 KB of the gate at the same time (one L2 hot spot for all readers)
+          const int kr = k0 + (i + blockIdx.x) % nk;
           tma_load_2d(st, &tmX, &full[stage], kr * kRtBK, t * kRtBM, pol_x);
           tma_load_2d(st + kRtA, &tmBh, &full[stage], kr * kRtBK, 0, pol_b);
           tma_load_2d(st + kRtA + kRtB, &tmBl, &full[stage], kr * kRtBK, 0, pol_b);
@@ -135,11 +143,12 @@ __global__ void __launch_bounds__(192, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       int lslot = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int w = blockIdx.x; w < items; w += gridDim.x) {
+        const int nk = kb_end(w & 1) - kb_begin(w & 1);
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t dt = tmem + acc * kRtAcc * kRtN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
           mbar_wait(&conv[stage], phase);
           tc_fence_after();
@@ -148,11 +157,10 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int ks = 0; ks < kRtBK / 8; ++ks) {  // K = 8 tf32 = 32 bytes per step
             const uint32_t o = ks * 32;
-            const uint32_t accum = kb > 0 || ks >= 2;  // first use of each accumulator overwrites
-            const uint32_t da = dt + (ks & 1) * kRtN;
-            tc_mma_tf32(da, umma_desc_sw128(ah + o), umma_desc_sw128(bh + o), idesc, accum);
-            tc_mma_tf32(da + 2 * kRtN, umma_desc_sw128(al + o), umma_desc_sw128(bh + o), idesc, accum);
-            tc_mma_tf32(da + 4 * kRtN, umma_desc_sw128(ah + o), umma_desc_sw128(bl + o), idesc, accum);
+            const uint32_t accum = kb > 0 || ks > 0;  // first use of each accumulator overwrites
+            tc_mma_tf32(dt, umma_desc_sw128(ah + o), umma_desc_sw128(bh + o), idesc, accum);
+            tc_mma_tf32(dt + kRtN, umma_desc_sw128(al + o), umma_desc_sw128(bh + o), idesc, accum);
+            tc_mma_tf32(dt + 2 * kRtN, umma_desc_sw128(ah + o), umma_desc_sw128(bl + o), idesc, accum);
           }
           tc_commit(&empty[stage]);
           tc_commit(&lo_empty[lslot]);
@@ -174,9 +182,10 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t acc_phase = 0;
     int lslot = 0;
     uint32_t lphase = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int w = blockIdx.x; w < items; w += gridDim.x) {
+      const int t = w >> 1, half = w & 1, nk = kb_end(half) - kb_begin(half);
       float ss = 0.f;
-      for (int kb = 0; kb < kblocks; ++kb) {
+      for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&full[stage], phase);
         mbar_wait(&lo_empty[lslot], lphase ^ 1);  // the MMAs of the lo buffer's previous use are done
         uint8_t* st = smem + stage * kRtStage;
@@ -208,7 +217,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       float sum[32];
 #pragma unroll 1
-      for (int a = 0; a < kRtAcc; ++a) {  // hi.hi (even, odd K steps), lo.hi, hi.lo
+      for (int a = 0; a < kRtAcc; ++a) {  // hi.hi, lo.hi, hi.lo
         uint32_t raw[32];
         tmem_ld32_async(tmem + lane_off + (acc * kRtAcc + a) * kRtN, raw);
         tmem_wait_ld();
@@ -220,12 +229,36 @@ __global__ void __launch_bounds__(192, 1)
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      // this half's partials into its scratch slot [item][33][128] (coalesced over rows)
+      float* mine = part + (size_t)w * kRtPart * kRtBM + r;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) mine[e * kRtBM] = sum[e];
+      mine[32 * kRtBM] = ss;
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
+      if (threadIdx.x == 64) {
+        const int old = atomicAdd(&ticket[t], 1);
+        __threadfence();
+        *last_flag = old;
+        if (old == 1) ticket[t] = 0;  // both halves are in: reset for the next call
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (*last_flag == 0) continue;  // the other half finishes the tile
+      const float* other = part + (size_t)(w ^ 1) * kRtPart * kRtBM + r;
+      float tot[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {  // fixed order: K half 0 + K half 1
+        const float o = __ldcg(other + e * kRtBM);
+        tot[e] = half == 0 ? sum[e] + o : o + sum[e];
+      }
+      const float os = __ldcg(other + 32 * kRtBM);
+      ss = half == 0 ? ss + os : os + ss;
       const int row = t * kRtBM + r;
       if (row >= rows) continue;
       const float inv = rsqrtf(ss / d + 1e-6f);
       float sc[32];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) sc[e] = sum[e] * inv;
+      for (int e = 0; e < 32; ++e) sc[e] = tot[e] * inv;
       uint32_t taken = 0;
       int ids[8];
       float rw[8];
@@ -277,7 +310,7 @@ __global__ void __launch_bounds__(192, 1)
   if (threadIdx.x < E && hist[threadIdx.x]) atomicAdd(&counts[threadIdx.x], hist[threadIdx.x]);
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, 256);
   }
 }
 
@@ -313,9 +346,12 @@ bool moe_route_tc_supported(int d, int E, int k, int ldx) {
   return E <= kRtN && k >= 1 && k <= 8 && d % kRtBK == 0 && ldx % 4 == 0;
 }
 
+size_t moe_route_tc_scratch_floats(int max_rows) {
+  return static_cast<size_t>(2) * ((max_rows + kRtBM - 1) / kRtBM) * kRtPart * kRtBM;
+}
 void launch_moe_route_tc(int rows, int d, int E, int k, const float* x, int ldx, const float* gate_hi,
                          const float* gate_lo, const float* bias, int32_t* sel, float* wts, int32_t* counts,
-                         cudaStream_t s) {
+                         float* part, int32_t* ticket, cudaStream_t s) {
   if (rows <= 0) return;
   if (!moe_route_tc_supported(d, E, k, ldx)) throw std::invalid_argument("moe_route_tc: unsupported shape");
   static bool attr = false;
@@ -327,10 +363,11 @@ void launch_moe_route_tc(int rows, int d, int E, int k, const float* x, int ldx,
   const CUtensorMap mh = map_f32(gate_hi, kRtN, d, d, kRtN);
   const CUtensorMap ml = map_f32(gate_lo, kRtN, d, d, kRtN);
   const int tiles = (rows + kRtBM - 1) / kRtBM;
-  const int grid = std::min(tiles, num_sms());
+  const int grid = std::min(2 * tiles, 2 * num_sms());
   ProfScope ps(PROF_MOE_ROUTE, s, 2.0 * 3 * rows * d * kRtN, double(rows) * (4.0 * d + 8.0 * k));
   prof_note("moe_route_tc_kernel");
-  launch_pdl(moe_route_tc_kernel, grid, 192, kRtSmem, s, mx, mh, ml, rows, d, E, k, bias, sel, wts, counts);
+  launch_pdl(moe_route_tc_kernel, grid, 192, kRtSmem, s, mx, mh, ml, rows, d, E, k, bias, sel, wts, counts, part,
+             ticket);
   ++launch_counter();
 }
 
@@ -388,7 +425,19 @@ void debug_moe_route(int rows, int d, int E, int k, const float* x, const float*
   if (variant == 2) {
     gate_tf32_split(gate, E, d, g2.data(), g2.data() + static_cast<size_t>(kRtN) * d);
     chk(cudaMemcpy(dh, g2.data(), g2.size() * 4, cudaMemcpyHostToDevice));
-    launch_moe_route_tc(rows, d, E, k, dx, d, dh, dl, db, ds, dw, dc, 0);
+    float* part = nullptr;
+    int32_t* ticket = nullptr;
+    chk(cudaMalloc(&part, moe_route_tc_scratch_floats(rows) * 4));
+    chk(cudaMalloc(&ticket, ((rows + kRtBM - 1) / kRtBM) * 4));
+    chk(cudaMemset(ticket, 0, ((rows + kRtBM - 1) / kRtBM) * 4));
+    launch_moe_route_tc(rows, d, E, k, dx, d, dh, dl, db, ds, dw, dc, part, ticket, 0);
+    chk(cudaDeviceSynchronize());
+    std::vector<int32_t> tk((rows + kRtBM - 1) / kRtBM);
+    chk(cudaMemcpy(tk.data(), ticket, tk.size() * 4, cudaMemcpyDeviceToHost));
+    for (int32_t v : tk)
+      if (v != 0) throw std::runtime_error("moe_route_tc: tile tickets not reset");
+    cudaFree(part);
+    cudaFree(ticket);
   } else {
     launch_moe_route(rows, d, E, k, dx, d, nullptr, dg, dg, db, ds, dw, dc, 0, variant == 1 ? dsw : nullptr);
   }

@@ -854,12 +854,14 @@ class EngineT final : public Engine {
       sel_ = ar_.alloc<int32_t>(mrows * k);
       wts_ = ar_.alloc<float>(mrows * k);
       slot_ = ar_.alloc<int32_t>(mrows * k);
-      counts_ = ar_.alloc<int32_t>(2 * static_cast<size_t>(E));  // routing histogram | scatter fill counters
-      if constexpr (kBf16) {  // split-K tensor-pipe router: per-(tile, K half) partials and tile tickets
+      // routing histogram | scatter fill counters | the split-K router's per-tile tickets,
+      // zeroed together once per forward pass (zero_moe_counters)
+      n_route_tickets_ = kBf16 ? static_cast<int>((mrows + 127) / 128) : 0;
+      counts_ = ar_.alloc<int32_t>(2 * static_cast<size_t>(E) + n_route_tickets_);
+      CUDA_CHECK(cudaMemset(counts_, 0, (2 * static_cast<size_t>(E) + n_route_tickets_) * 4));
+      if constexpr (kBf16) {  // split-K tensor-pipe router: per-(tile, K half) partials
         route_part_ = ar_.alloc<float>(moe_route_tc_scratch_floats(static_cast<int>(mrows)));
-        const size_t nt = static_cast<size_t>((mrows + 127) / 128);
-        route_ticket_ = ar_.alloc<int32_t>(nt);
-        CUDA_CHECK(cudaMemset(route_ticket_, 0, nt * 4));
+        route_ticket_ = counts_ + 2 * E;
       }
       cursor_ = ar_.alloc<int32_t>(E);
       tile_expert_ = ar_.alloc<int32_t>(max_tiles_);
@@ -1200,7 +1202,8 @@ class EngineT final : public Engine {
   // combine re-zeroes them for the next layer; this also recovers from an
   // interrupted pass)
   void zero_moe_counters() {
-    if (counts_) CUDA_CHECK(cudaMemsetAsync(counts_, 0, 2 * cfg_.n_experts * sizeof(int32_t), st_));
+    if (counts_)
+      CUDA_CHECK(cudaMemsetAsync(counts_, 0, (2 * static_cast<size_t>(cfg_.n_experts) + n_route_tickets_) * 4, st_));
   }
   void run_encode() {
     require(staged_, "no user batch staged");
@@ -2291,7 +2294,8 @@ class EngineT final : public Engine {
   T* yg_ = nullptr;  // weighted expert outputs (bf16 in the bf16 engine)
   float* row_rsq_ = nullptr;  // folded pre-MoE RMSNorm: scale of every grouped row
   float* route_part_ = nullptr;      // tensor-pipe router: K-half partial scores
-  int32_t* route_ticket_ = nullptr;  // tensor-pipe router: per-tile arrival tickets
+  int32_t* route_ticket_ = nullptr;  // tensor-pipe router: per-tile arrival tickets (after counts_)
+  int n_route_tickets_ = 0;
   T *xg_ = nullptr, *hg_ = nullptr;
   // expert parallelism
   int ep_rank_ = 0, ep_world_ = 1, El_ = 0;  // El_: local expert slots per MoE layer

@@ -1345,9 +1345,15 @@ class EngineT final : public Engine {
       gemm(att_, d, l.wo, R, eo);
       if (!nf) launch_rmsnorm<T>(R, d, z_, d, enc_moe(c) && fold_norm_ ? ones_ : l.n2, xn_, d, st_);
       if (enc_moe(c)) {
-        moe(l.moe, xn_, R, z_, l.n2);
+        // the last layer's combine also writes bf16(z): the decoder's cross K|V GEMM operand
+        if (kBf16 && li + 1 == enc_.size()) zt_fresh_ = moe(l.moe, xn_, R, z_, l.n2, zt_, nullptr);
+        else moe(l.moe, xn_, R, z_, l.n2);
       } else {
-        ffn(l.fc1, l.fc2, xn_, R, z_, nf, nf && li + 1 < enc_.size());
+        const bool last = li + 1 == enc_.size();
+        // the last fc2 also writes bf16(z) for the decoder's cross K|V GEMM (XSSQ epilogue,
+        // sums of squares unused) instead of a separate conversion pass
+        ffn(l.fc1, l.fc2, xn_, R, z_, nf, nf && !last, nf && last ? zt_ : nullptr);
+        zt_fresh_ = nf && last;
       }
     }
   }
@@ -1383,7 +1389,7 @@ class EngineT final : public Engine {
   // scales from ssq_); fold_out: fc2 also writes bf16(h) to xn_ and its sums
   // of squares to ssq_ for the next folded RMSNorm.
   void ffn(const Lin<T>& fc1, const Lin<T>& fc2, const T* x, int rows, float* h, bool fold_in = false,
-           bool fold_out = false) {
+           bool fold_out = false, T* copy_out = nullptr) {
     const int d = cfg_.d_model;
     Epi e1 = epi(ffh_, cfg_.ffn_hidden, false);
     e1.act = ACT_SILU;
@@ -1393,6 +1399,10 @@ class EngineT final : public Engine {
     e2.resid = h;
     e2.ld_resid = d;
     if (fold_out) norm_out(e2);
+    if (copy_out) {  // bf16 copy of the updated rows (the folded-norm epilogue; its sums of squares unused)
+      norm_out(e2);
+      e2.out2 = copy_out;
+    }
     gemm(ffh_, cfg_.ffn_hidden, fc2, rows, e2);
   }
   // RMSNorm folded into the GEMMs around it (Epi::out2 / ssq / rsq, fold_norm_)
@@ -1671,7 +1681,8 @@ class EngineT final : public Engine {
 
   void prepare_decoder(int U) {
     const int d = cfg_.d_model, Tn = enc_seq_len(cfg_);
-    if constexpr (kBf16) launch_convert<T>(U * Tn, d, z_, d, zt_, d, st_);
+    if constexpr (kBf16)
+      if (!zt_fresh_) launch_convert<T>(U * Tn, d, z_, d, zt_, d, st_);  // else the encoder's last GEMM wrote it
     if (tc_attn_) {  // cross K of every decoder layer [rows][Ld*d]; cross V transposed per layer
       const int kn = xkv_w_.N / 2;  // K of all layers | V of all layers
       gemm(zt_, d, xkv_w_, U * Tn,
@@ -2229,6 +2240,7 @@ class EngineT final : public Engine {
     const size_t nz = static_cast<size_t>(n_z) * enc_seq_len(cfg_) * cfg_.d_model;
     require_finite(z, nz);
     CUDA_CHECK(cudaMemcpyAsync(z_, z, nz * 4, cudaMemcpyHostToDevice, st_));
+    zt_fresh_ = false;  // caller-supplied encodings: convert
     prepare_decoder(n_z);
     teacher_forced(n_z, n, z_index, prefixes, prefix_len, logits);
   }
@@ -2270,6 +2282,7 @@ class EngineT final : public Engine {
   int max_tiles_ = 0;
   T *feat_, *hid_, *keys_, *kvl_, *xn_, *qkv_, *att_, *ffh_, *qproj_, *qcur_, *zt_, *xkv_;
   float *z_, *qo_, *h_, *logits_, *lse_;
+  bool zt_fresh_ = false;  // zt_ = bf16(z_) was written by the encoder's last GEMM / combine
   std::vector<T*> kvpos_;       // [position * dec_layers + layer] -> [Rd_][3d] QKV output (self-attention cache)
   T** kvpos_ptrs_ = nullptr;
   uint64_t* cand_ = nullptr;

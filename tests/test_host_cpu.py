@@ -40,6 +40,10 @@ def test_presets_and_expert_hidden():
     assert c.expert_hidden() == 2816  # test_moe.cpp:261-265
     assert c.enc_seq_len() == 405
     assert P.PolicyConfig.preset("2.633B").moe_location == "enc_and_dec"
+    # MoE layers in engine order (the expert-placement table's rows)
+    assert P.moe_layers(c) == 4  # decoder-only MoE: 4 decoder layers
+    assert P.moe_layers(P.PolicyConfig.preset("2.633B")) == 24  # 12 encoder + 12 decoder
+    assert P.moe_layers(P.PolicyConfig.preset("0.121B")) == 0
     with pytest.raises(ValueError):
         P.PolicyConfig.preset("nope")
 
